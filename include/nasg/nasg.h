@@ -1,0 +1,181 @@
+/* nasg.h — C ABI of the B200-native NASG path-guiding hot path.
+ *
+ * Drop-in for the reference's guiding API (/root/reference/proj/include/nasg),
+ * batched and stream-ordered.  Every entry point cites the reference
+ * interface it replaces.  Plain C types only: device buffers are passed as
+ * raw pointers (cudaMalloc'd, 16-byte aligned), streams as `void *`
+ * (a cudaStream_t, NULL = the context's stream).  No function throws; all
+ * return an `int` nasg_status.  Host arrays are row-major, little-endian.
+ *
+ * Data layouts (device or host, per argument):
+ *   query SoA    x, wo, nrm : n x float4 (xyz + ignored w)  — position,
+ *                omega_o and shading normal of encode_inputs (encoding.hpp:26)
+ *   xi           n x float4 = (xi_select, xi0, xi1, xi2) of mixture_sample
+ *                (sphdist.hpp:97-98)
+ *   dir_pdf      n x float4 = (direction xyz, mixture pdf)  — DirectionSample
+ *                (sphdist.hpp:93-96)
+ *   raw          n x (8N+1) float, reference raw-output order (guiding.hpp:25-30)
+ *   train sample n x nasg_train_sample (64 B)  — TrainingSample (guiding.hpp:54-63)
+ *   weights      W1(64x128) W2(128x128) W3(128x128) W4(128x(8N+1)) row-major,
+ *                concatenated — NetworkParameters<float> (net.hpp:22-40)
+ *
+ * Threading (guiding.hpp:139-141): one context per GPU; the
+ * training calls and nasg_publish are single-writer; query calls read the
+ * published snapshot and may run concurrently on other streams.
+ */
+#ifndef NASG_H
+#define NASG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    NASG_OK = 0,
+    NASG_ERR_INVALID = 1,     /* bad argument / shape */
+    NASG_ERR_CUDA = 2,        /* CUDA runtime error (or no sm_100a device) */
+    NASG_ERR_NCCL = 3,        /* NCCL unavailable / failed */
+    NASG_ERR_IO = 4,          /* checkpoint I/O (net.cpp:34-79 exceptions) */
+    NASG_ERR_OOM = 5,
+    NASG_ERR_UNSUPPORTED = 6  /* configuration not compiled in */
+} nasg_status;
+
+/* MLP arithmetic of the query path. */
+typedef enum {
+    NASG_MLP_FP32 = 0, /* fp32 FFMA, bit-for-tolerance with the fp32 reference */
+    NASG_MLP_BF16 = 1  /* bf16 operands, fp32 accumulate, tcgen05/TMEM tensor cores */
+} nasg_precision;
+
+/* TrainerConfig (guiding.hpp:122-130); defaults via nasg_config_default. */
+typedef struct {
+    int n_components;     /* N = 8 */
+    int sample_capacity;  /* S = 2^16 */
+    int batch_size;       /* t = 2^12 */
+    int step_factor;      /* nu = 1 */
+    float learning_rate;  /* 0.002 */
+    double loss_blend;    /* e = 0.2 */
+    uint64_t seed;        /* 0 */
+} nasg_config;
+
+/* TrainStats (guiding.hpp:132-137). */
+typedef struct {
+    int steps;
+    double mean_loss;
+    uint64_t dropped_samples;
+    uint64_t skipped_updates;
+} nasg_train_stats;
+
+/* TrainingSample (guiding.hpp:54-63) packed to 64 bytes. bsdf_is_delta
+ * samples are never recorded (SPEC.md guider design decisions). */
+typedef struct {
+    float position[3];
+    float p_value;        /* luminance target p */
+    float omega_o[3];
+    float q_sampling;     /* pdf the sample obeyed (> 0) */
+    float normal[3];
+    float bsdf_pdf_at_wi;
+    float omega_i[3];
+    float pad;
+} nasg_train_sample;
+
+typedef struct nasg_ctx nasg_ctx;
+
+/* ---- lifetime (Trainer::Trainer guiding.cpp:184-190) ------------------- */
+void nasg_config_default(nasg_config *cfg);
+/* Initialises the live weights with init_network<float>(64, 8N+1, seed)
+ * (net.hpp:43-57, bit-exact), zero Adam state, and publishes them. */
+int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const float bmax[3],
+                nasg_ctx **out);
+int nasg_destroy(nasg_ctx *ctx);
+const char *nasg_status_string(int status);
+const char *nasg_last_error(void);  /* thread-local detail of the last failure */
+int nasg_n_weights(int n_components); /* 64*128 + 2*128*128 + 128*(8N+1) */
+
+/* ---- parameters / snapshots (Trainer::parameters/mutable_parameters/publish/
+ * snapshot guiding.hpp:151-157; NetworkSnapshot net.hpp:161) -------------- */
+int nasg_set_weights(nasg_ctx *ctx, const float *host_w, size_t n_floats); /* live, then publish */
+int nasg_get_weights(nasg_ctx *ctx, float *host_w, size_t n_floats, int published);
+int nasg_publish(nasg_ctx *ctx);  /* snapshot live -> published (stream-ordered) */
+int nasg_set_precision(nasg_ctx *ctx, int precision); /* nasg_precision for queries */
+int nasg_get_precision(nasg_ctx *ctx);
+/* save_checkpoint / load_checkpoint (net.hpp:163-167, net.cpp:31-82): NASGNET1. */
+int nasg_save_checkpoint(nasg_ctx *ctx, const char *path);
+int nasg_load_checkpoint(nasg_ctx *ctx, const char *path);
+
+/* ---- queries (device buffers; read the published snapshot) -------------- */
+/* infer_guide (guiding.hpp:169) + mixture_sample (sphdist.hpp:97): per query
+ * encode -> MLP -> decode -> inverse-CDF lobe pick -> NASG sample -> mixture
+ * pdf at the sample.  c (nullable) receives the clamped selection prob. */
+int nasg_query_sample(nasg_ctx *ctx, int64_t n, const float *x, const float *wo,
+                      const float *nrm, const float *xi, float *dir_pdf, float *c,
+                      void *stream);
+/* mixture_pdf (sphdist.hpp:84) and guided_pdf (guiding.hpp:51) at given
+ * directions dir (n x float4).  Either output may be NULL. */
+int nasg_query_pdf(nasg_ctx *ctx, int64_t n, const float *x, const float *wo, const float *nrm,
+                   const float *dir, float b, const float *bsdf_pdf, float *mix_pdf,
+                   float *guided_pdf, void *stream);
+/* encode_inputs + forward (infer_guide without decode): raw outputs in the
+ * reference order, n x (8N+1).  Parity entry for the MLP. */
+int nasg_query_raw(nasg_ctx *ctx, int64_t n, const float *x, const float *wo, const float *nrm,
+                   float *raw, void *stream);
+/* decode (guiding.hpp:47) + mixture_sample on given raw outputs — the
+ * NASG epilogue alone (parity entry). */
+int nasg_decode_sample_raw(nasg_ctx *ctx, int64_t n, const float *raw, const float *xi,
+                           float *dir_pdf, float *c, void *stream);
+int nasg_decode_pdf_raw(nasg_ctx *ctx, int64_t n, const float *raw, const float *dir, float b,
+                        const float *bsdf_pdf, float *mix_pdf, float *guided_pdf, void *stream);
+/* Host-buffer form of nasg_query_sample for callers without device memory:
+ * pipelines H2D / kernel / D2H over chunks on the context's streams and
+ * returns when dir_pdf (and c) are written.  Inputs are 4 floats/query. */
+int nasg_query_sample_host(nasg_ctx *ctx, int64_t n, const float *x, const float *wo,
+                           const float *nrm, const float *xi, float *dir_pdf, float *c);
+
+/* ---- training (Trainer::train_iteration guiding.hpp:149, guiding.cpp:196-282)
+ * Runs T = nu*ceil(S/t) minibatch steps over the n samples (epochs reshuffled
+ * with the reference's PCG32 Fisher-Yates), then publishes.  n == 0 is a
+ * no-op + publish.  samples is a device array.  Blocks until stats are ready
+ * when stats != NULL. */
+int nasg_train_iteration(nasg_ctx *ctx, int64_t n, const nasg_train_sample *samples,
+                         double blend_b, nasg_train_stats *stats, void *stream);
+/* One data-parallel minibatch step on rows samples[order[0..count)] with the
+ * 1/global_count scaling of guiding.cpp:262 (global_count = rows over all
+ * ranks).  Accumulates loss/drop statistics into the context; gradient
+ * exchange happens inside when a communicator is attached. */
+int nasg_train_step(nasg_ctx *ctx, const nasg_train_sample *samples, const uint32_t *order,
+                    int64_t count, int64_t global_count, double blend_b, void *stream);
+/* Reads (and resets) the statistics accumulated by nasg_train_step. */
+int nasg_train_stats_take(nasg_ctx *ctx, nasg_train_stats *stats);
+/* Gradient of the last step (canonical weight layout, host copy). */
+int nasg_get_last_grad(nasg_ctx *ctx, float *host_g, size_t n_floats);
+int64_t nasg_adam_t(nasg_ctx *ctx);
+
+/* ---- multi-GPU (NCCL over NVLink; one rank per GPU) --------------------- */
+int nasg_comm_unique_id(void *out_128_bytes);
+int nasg_comm_init(nasg_ctx *ctx, const void *unique_id_128_bytes, int rank, int nranks);
+
+/* ---- counters (encode_clamp_count encoding.hpp:31-32) ------------------- */
+uint64_t nasg_encode_clamp_count(nasg_ctx *ctx);
+void nasg_reset_encode_clamp_count(nasg_ctx *ctx);
+/* Number of device kernel launches issued by this context since creation. */
+uint64_t nasg_kernel_launches(nasg_ctx *ctx);
+
+/* ---- host-side schedule helpers (guiding.hpp:77-120, guiding.cpp:178-182) */
+double nasg_blend_coefficient(int64_t iteration, int m, int b_steps);
+double nasg_stride_update(double l, uint64_t collected, uint64_t capacity);
+
+/* ---- synthetic workloads (bench / tests) ----------------- */
+/* Query i: Pcg32(hash_combine(seed, i), 0x51) -> x ~ U(bounds), omega_o and
+ * normal ~ U(S^2), xi ~ U[0,1) as (u32 >> 8) * 2^-24.  Host arrays. */
+void nasg_synth_queries(uint64_t seed, int64_t first, int64_t n, const float bmin[3],
+                        const float bmax[3], float *x, float *wo, float *nrm, float *xi);
+/* Sample i with the fixed analytic target of SURVEY §8d. */
+void nasg_synth_samples(uint64_t seed, int64_t first, int64_t n, const float bmin[3],
+                        const float bmax[3], nasg_train_sample *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NASG_H */

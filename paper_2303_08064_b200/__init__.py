@@ -1,0 +1,349 @@
+"""B200-native NASG online path-guiding hot path (arXiv 2303.08064).
+
+Thin ctypes binding of the C ABI in ``include/nasg/nasg.h`` (implemented in
+``csrc/`` and built to ``lib/libnasg_b200.so`` for sm_100a).  It mirrors the
+reference's C++ guiding API nouns (guiding.hpp): ``TrainerConfig``,
+``TrainStats``, ``Trainer.train_iteration``, ``publish``/``snapshot``,
+``infer_guide`` + ``mixture_sample`` (batched as ``query_sample``),
+``guided_pdf`` (``query_pdf``), ``decode`` (``decode_sample_raw``).
+
+Device buffers are passed as torch CUDA tensors (PyTorch is used only for
+device memory and streams); host buffers as numpy arrays.  There is no CPU
+fallback: every call runs the CUDA library or raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libnasg_b200.so")
+
+NASG_MLP_FP32 = 0
+NASG_MLP_BF16 = 1
+
+
+class NasgError(RuntimeError):
+    pass
+
+
+class _Config(C.Structure):
+    _fields_ = [("n_components", C.c_int), ("sample_capacity", C.c_int), ("batch_size", C.c_int),
+                ("step_factor", C.c_int), ("learning_rate", C.c_float), ("loss_blend", C.c_double),
+                ("seed", C.c_uint64)]
+
+
+class _Stats(C.Structure):
+    _fields_ = [("steps", C.c_int), ("mean_loss", C.c_double), ("dropped_samples", C.c_uint64),
+                ("skipped_updates", C.c_uint64)]
+
+
+@dataclass
+class TrainerConfig:
+    """TrainerConfig (guiding.hpp:122-130)."""
+    n_components: int = 8
+    sample_capacity: int = 1 << 16
+    batch_size: int = 1 << 12
+    step_factor: int = 1
+    learning_rate: float = 0.002
+    loss_blend: float = 0.2
+    seed: int = 0
+
+
+@dataclass
+class TrainStats:
+    """TrainStats (guiding.hpp:132-137)."""
+    steps: int
+    mean_loss: float
+    dropped_samples: int
+    skipped_updates: int
+
+
+_lib = None
+
+
+def lib():
+    """Load libnasg_b200.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NasgError(f"CUDA library missing: {LIB_PATH} (run `python -c 'import __graft_entry__ as g; g.build()'`)")
+    L = C.CDLL(LIB_PATH)
+    vp, i64, u64, i32, f32, f64, sz = C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_float, C.c_double, C.c_size_t
+    sigs = {
+        "nasg_config_default": (None, [vp]),
+        "nasg_create": (i32, [vp, i32, vp, vp, C.POINTER(vp)]),
+        "nasg_destroy": (i32, [vp]),
+        "nasg_status_string": (C.c_char_p, [i32]),
+        "nasg_last_error": (C.c_char_p, []),
+        "nasg_n_weights": (i32, [i32]),
+        "nasg_set_weights": (i32, [vp, vp, sz]),
+        "nasg_get_weights": (i32, [vp, vp, sz, i32]),
+        "nasg_publish": (i32, [vp]),
+        "nasg_set_precision": (i32, [vp, i32]),
+        "nasg_get_precision": (i32, [vp]),
+        "nasg_save_checkpoint": (i32, [vp, C.c_char_p]),
+        "nasg_load_checkpoint": (i32, [vp, C.c_char_p]),
+        "nasg_query_sample": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp]),
+        "nasg_query_pdf": (i32, [vp, i64, vp, vp, vp, vp, f32, vp, vp, vp, vp]),
+        "nasg_query_raw": (i32, [vp, i64, vp, vp, vp, vp, vp]),
+        "nasg_decode_sample_raw": (i32, [vp, i64, vp, vp, vp, vp, vp]),
+        "nasg_decode_pdf_raw": (i32, [vp, i64, vp, vp, f32, vp, vp, vp, vp]),
+        "nasg_query_sample_host": (i32, [vp, i64, vp, vp, vp, vp, vp, vp]),
+        "nasg_train_iteration": (i32, [vp, i64, vp, f64, vp, vp]),
+        "nasg_train_step": (i32, [vp, vp, vp, i64, i64, f64, vp]),
+        "nasg_train_stats_take": (i32, [vp, vp]),
+        "nasg_get_last_grad": (i32, [vp, vp, sz]),
+        "nasg_adam_t": (i64, [vp]),
+        "nasg_comm_unique_id": (i32, [vp]),
+        "nasg_comm_init": (i32, [vp, vp, i32, i32]),
+        "nasg_encode_clamp_count": (u64, [vp]),
+        "nasg_reset_encode_clamp_count": (None, [vp]),
+        "nasg_kernel_launches": (u64, [vp]),
+        "nasg_blend_coefficient": (f64, [i64, i32, i32]),
+        "nasg_stride_update": (f64, [f64, u64, u64]),
+        "nasg_synth_queries": (None, [u64, i64, i64, vp, vp, vp, vp, vp, vp]),
+        "nasg_synth_samples": (None, [u64, i64, i64, vp, vp, vp]),
+    }
+    for name, (res, args) in sigs.items():
+        fn = getattr(L, name)
+        fn.restype, fn.argtypes = res, args
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names of every function declared in include/nasg/nasg.h."""
+    import re
+    hdr = os.path.join(os.path.dirname(_HERE), "include", "nasg", "nasg.h")
+    txt = re.sub(r"/\*.*?\*/", "", open(hdr).read(), flags=re.S)
+    return sorted(set(re.findall(r"\b(nasg_[a-z0-9_]+)\s*\(", txt)))
+
+
+def _check(rc):
+    if rc != 0:
+        L = lib()
+        raise NasgError(f"{L.nasg_status_string(rc).decode()}: {L.nasg_last_error().decode()}")
+
+
+def _f3(v):
+    return np.ascontiguousarray(np.asarray(v, np.float32).reshape(3))
+
+
+def _ptr(t):
+    """Device pointer of a torch tensor (or None), host pointer of a numpy array."""
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    if hasattr(t, "data_ptr"):
+        if not t.is_contiguous():
+            raise NasgError("tensor must be contiguous")
+        return t.data_ptr()
+    return int(t)
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def n_weights(n_components: int = 8) -> int:
+    return lib().nasg_n_weights(n_components)
+
+
+def blend_coefficient(iteration: int, m: int = 4, b_steps: int = 64) -> float:
+    """BlendSchedule::coefficient (guiding.hpp:83-86)."""
+    return lib().nasg_blend_coefficient(iteration, m, b_steps)
+
+
+def stride_update(l: float, collected: int, capacity: int) -> float:
+    """stride_update (guiding.cpp:178-182)."""
+    return lib().nasg_stride_update(l, collected, capacity)
+
+
+def synth_queries(seed: int, n: int, first: int = 0, bmin=(-1, -1, -1), bmax=(1, 1, 1), pinned: bool = False):
+    """Synthetic queries of SURVEY.md §8d as host float32 arrays (n,4) x 4: x, wo, nrm, xi."""
+    arrs = []
+    for _ in range(4):
+        if pinned:
+            import torch
+            arrs.append(torch.empty((n, 4), dtype=torch.float32).pin_memory().numpy())
+        else:
+            arrs.append(np.empty((n, 4), np.float32))
+    lib().nasg_synth_queries(seed, first, n, _f3(bmin).ctypes.data, _f3(bmax).ctypes.data,
+                             *[a.ctypes.data for a in arrs])
+    return tuple(arrs)
+
+
+def synth_samples(seed: int, n: int, first: int = 0, bmin=(-1, -1, -1), bmax=(1, 1, 1)):
+    """Synthetic training samples (n,16) float32 (nasg_train_sample layout)."""
+    out = np.empty((n, 16), np.float32)
+    lib().nasg_synth_samples(seed, first, n, _f3(bmin).ctypes.data, _f3(bmax).ctypes.data, out.ctypes.data)
+    return out
+
+
+class Guide:
+    """One GPU's guiding context: live Trainer state + published snapshot.
+
+    Mirrors ``nasg::Trainer`` (guiding.hpp:142-166) and the per-point query
+    functions, batched over device tensors.
+    """
+
+    def __init__(self, config: TrainerConfig | None = None, device: int = 0, bmin=(-1, -1, -1), bmax=(1, 1, 1)):
+        self.config = config or TrainerConfig()
+        cfg = _Config(self.config.n_components, self.config.sample_capacity, self.config.batch_size,
+                      self.config.step_factor, self.config.learning_rate, self.config.loss_blend, self.config.seed)
+        h = C.c_void_p()
+        _check(lib().nasg_create(C.byref(cfg), device, _f3(bmin).ctypes.data, _f3(bmax).ctypes.data, C.byref(h)))
+        self._h = h
+        self.device = device
+        self.n_components = self.config.n_components
+        self.out_dim = 8 * self.n_components + 1
+        self.nw = n_weights(self.n_components)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nasg_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- parameters ------------------------------------------------------------
+    def set_weights(self, w):
+        w = np.ascontiguousarray(w, np.float32)
+        _check(lib().nasg_set_weights(self._h, w.ctypes.data, w.size))
+
+    def get_weights(self, published: bool = False):
+        w = np.empty(self.nw, np.float32)
+        _check(lib().nasg_get_weights(self._h, w.ctypes.data, w.size, int(published)))
+        return w
+
+    def publish(self):
+        _check(lib().nasg_publish(self._h))
+
+    @property
+    def precision(self) -> int:
+        return lib().nasg_get_precision(self._h)
+
+    @precision.setter
+    def precision(self, p: int):
+        _check(lib().nasg_set_precision(self._h, int(p)))
+
+    def save_checkpoint(self, path: str):
+        _check(lib().nasg_save_checkpoint(self._h, path.encode()))
+
+    def load_checkpoint(self, path: str):
+        _check(lib().nasg_load_checkpoint(self._h, path.encode()))
+
+    @property
+    def kernel_launches(self) -> int:
+        return lib().nasg_kernel_launches(self._h)
+
+    @property
+    def encode_clamp_count(self) -> int:
+        return lib().nasg_encode_clamp_count(self._h)
+
+    def reset_encode_clamp_count(self):
+        lib().nasg_reset_encode_clamp_count(self._h)
+
+    # ---- queries (torch CUDA tensors, (n,4) float32) --------------------------------
+    def query_sample(self, x, wo, nrm, xi, dir_pdf=None, c=None, stream=None):
+        import torch
+        n = x.shape[0]
+        if dir_pdf is None:
+            dir_pdf = torch.empty((n, 4), dtype=torch.float32, device=x.device)
+        _check(lib().nasg_query_sample(self._h, n, _ptr(x), _ptr(wo), _ptr(nrm), _ptr(xi), _ptr(dir_pdf), _ptr(c),
+                                       _stream(stream)))
+        return dir_pdf, c
+
+    def query_pdf(self, x, wo, nrm, dirs, b, bsdf_pdf=None, stream=None):
+        import torch
+        n = x.shape[0]
+        mix = torch.empty(n, dtype=torch.float32, device=x.device)
+        guided = torch.empty(n, dtype=torch.float32, device=x.device)
+        _check(lib().nasg_query_pdf(self._h, n, _ptr(x), _ptr(wo), _ptr(nrm), _ptr(dirs), float(b), _ptr(bsdf_pdf),
+                                    _ptr(mix), _ptr(guided), _stream(stream)))
+        return mix, guided
+
+    def query_raw(self, x, wo, nrm, stream=None):
+        import torch
+        n = x.shape[0]
+        raw = torch.empty((n, self.out_dim), dtype=torch.float32, device=x.device)
+        _check(lib().nasg_query_raw(self._h, n, _ptr(x), _ptr(wo), _ptr(nrm), _ptr(raw), _stream(stream)))
+        return raw
+
+    def decode_sample_raw(self, raw, xi, stream=None):
+        import torch
+        n = raw.shape[0]
+        out = torch.empty((n, 4), dtype=torch.float32, device=raw.device)
+        c = torch.empty(n, dtype=torch.float32, device=raw.device)
+        _check(lib().nasg_decode_sample_raw(self._h, n, _ptr(raw), _ptr(xi), _ptr(out), _ptr(c), _stream(stream)))
+        return out, c
+
+    def decode_pdf_raw(self, raw, dirs, b, bsdf_pdf=None, stream=None):
+        import torch
+        n = raw.shape[0]
+        mix = torch.empty(n, dtype=torch.float32, device=raw.device)
+        guided = torch.empty(n, dtype=torch.float32, device=raw.device)
+        _check(lib().nasg_decode_pdf_raw(self._h, n, _ptr(raw), _ptr(dirs), float(b), _ptr(bsdf_pdf), _ptr(mix),
+                                         _ptr(guided), _stream(stream)))
+        return mix, guided
+
+    def query_sample_host(self, x, wo, nrm, xi, dir_pdf=None, c=None):
+        """Host numpy in/out; H2D, kernel and D2H are pipelined inside the library."""
+        n = x.shape[0]
+        if dir_pdf is None:
+            dir_pdf = np.empty((n, 4), np.float32)
+        _check(lib().nasg_query_sample_host(self._h, n, _ptr(x), _ptr(wo), _ptr(nrm), _ptr(xi), _ptr(dir_pdf),
+                                            _ptr(c)))
+        return dir_pdf, c
+
+    # ---- training ----------------------------------------------------------------------
+    def train_iteration(self, samples, blend_b: float, stream=None, stats: bool = True) -> TrainStats | None:
+        """Trainer::train_iteration (guiding.cpp:196-282) on a device (n,16) float32 tensor."""
+        n = 0 if samples is None else samples.shape[0]
+        st = _Stats()
+        _check(lib().nasg_train_iteration(self._h, n, _ptr(samples) if n else None, float(blend_b),
+                                          C.byref(st) if stats else None, _stream(stream)))
+        if not stats:
+            return None
+        return TrainStats(st.steps, st.mean_loss, st.dropped_samples, st.skipped_updates)
+
+    def train_step(self, samples, order, count: int, global_count: int, blend_b: float, stream=None):
+        _check(lib().nasg_train_step(self._h, _ptr(samples), _ptr(order), count, global_count, float(blend_b),
+                                     _stream(stream)))
+
+    def train_stats_take(self) -> TrainStats:
+        st = _Stats()
+        _check(lib().nasg_train_stats_take(self._h, C.byref(st)))
+        return TrainStats(st.steps, st.mean_loss, st.dropped_samples, st.skipped_updates)
+
+    def last_grad(self):
+        g = np.empty(self.nw, np.float32)
+        _check(lib().nasg_get_last_grad(self._h, g.ctypes.data, g.size))
+        return g
+
+    @property
+    def adam_t(self) -> int:
+        return lib().nasg_adam_t(self._h)
+
+    # ---- multi-GPU ------------------------------------------------------------------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        buf = (C.c_char * 128)()
+        _check(lib().nasg_comm_unique_id(buf))
+        return bytes(buf)
+
+    def comm_init(self, unique_id: bytes, rank: int, nranks: int):
+        buf = (C.c_char * 128).from_buffer_copy(unique_id)
+        _check(lib().nasg_comm_init(self._h, buf, rank, nranks))

@@ -1,0 +1,223 @@
+// fp32 query path: fused encode -> 4-layer MLP (FFMA) -> NASG epilogue,
+// plus the weight-packing kernel and the raw-output parity kernels.
+//
+// One persistent CTA (256 threads) per SM walks 128-query tiles.  Per tile:
+//   K1 encode     encode_inputs (encoding.cpp:21-46) into smem, feature-major
+//   K2 MLP        forward<float> (net.hpp:69-76), 4 x tile_layer
+//   K3 epilogue   decode + mixture_sample + mixture_pdf, or mixture/guided
+//                 pdf at a given direction, one thread per query
+// Only the 64 B/query of inputs and 16-20 B/query of outputs touch HBM.
+#include <cstdio>
+
+#include "nasg_internal.h"
+#include "nasg_math.cuh"
+#include "simt_gemm.cuh"
+
+namespace nasg {
+
+// ---------------------------------------------------------------- packing --
+// wp : W1[64][128] W2[128][128] W3[128][128] W4p[128][128] (packed cols)
+// wtp: W2^T[128][128] W3^T[128][128] W4p^T[128][128] (rows = packed col)
+__global__ void pack_fp32_kernel(const float *__restrict__ w, int n_comp, float *__restrict__ wp,
+                                 float *__restrict__ wtp) {
+    const int D = 8 * n_comp + 1;
+    const int NP = packed_width(n_comp);
+    const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kPackedF32; e += gridDim.x * blockDim.x) {
+        float v;
+        if (e < o3) {
+            v = w[e];
+        } else {
+            const int k = (e - o3) / kHidden, col = (e - o3) % kHidden;
+            int j = -1;  // reference raw index of packed column col
+            if (col < NP) {
+                const int H = packed_header(n_comp);
+                if (col < n_comp) j = 7 * n_comp + col;
+                else if (col == n_comp) j = 8 * n_comp;
+                else if (col >= H) {
+                    const int i = (col - H) / 8, kk = (col - H) % 8;
+                    j = kk < 5 ? 5 * i + kk : (kk == 5 ? 5 * n_comp + 2 * i : (kk == 6 ? 5 * n_comp + 2 * i + 1 : -1));
+                }
+            }
+            v = j >= 0 ? w[o3 + k * D + j] : 0.f;
+        }
+        wp[e] = v;
+        if (wtp && e >= o1) {  // transposed W2, W3, W4p
+            const int l = e < o2 ? 0 : (e < o3 ? 1 : 2);
+            const int base = l == 0 ? o1 : (l == 1 ? o2 : o3);
+            const int k = (e - base) / kHidden, col = (e - base) % kHidden;
+            wtp[l * kHidden * kHidden + col * kHidden + k] = v;
+        }
+    }
+}
+
+void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStream_t s) {
+    pack_fp32_kernel<<<148, 256, 0, s>>>(w, n_comp, wp, wtp);
+}
+
+// ------------------------------------------------------------- encoding --
+// One-blob encoding of one query into column r of the feature-major tile.
+// t = (p - min) / ext in double as in encoding.cpp:30; bins in fp32.
+__device__ __forceinline__ int encode_row(const float4 x, const float4 wo, const float4 nrm,
+                                          const Bounds &bd, float *act, int r) {
+    int clamped = 0;
+    const float xs[3] = {x.x, x.y, x.z};
+#pragma unroll
+    for (int axis = 0; axis < 3; ++axis) {
+        double t = bd.ext[axis] > 0.0 ? ((double)xs[axis] - (double)bd.bmin[axis]) / bd.ext[axis] : 0.5;
+        if (t < 0.0 || t > 1.0) {
+            ++clamped;
+            t = fmin(fmax(t, 0.0), 1.0);
+        }
+#pragma unroll
+        for (int i = 0; i < kBins; ++i) {
+            float d = (float)(t - (i + 0.5) / kBins);
+            act[(axis * kBins + i) * kLda + r] = expf(-d * d * 180.5f);
+        }
+    }
+    act[57 * kLda + r] = wo.x; act[58 * kLda + r] = wo.y; act[59 * kLda + r] = wo.z;
+    act[60 * kLda + r] = nrm.x; act[61 * kLda + r] = nrm.y; act[62 * kLda + r] = nrm.z;
+    act[63 * kLda + r] = 1.f;
+    return clamped;
+}
+
+// ---------------------------------------------------------- fused kernel --
+template <int N, int MODE>
+__global__ void __launch_bounds__(256, 1)
+query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
+    extern __shared__ __align__(16) float smem[];
+    float *actA = smem;                      // [128][kLda]
+    float *actB = actA + kHidden * kLda;     // [128][kLda]
+    float *wbuf = actB + kHidden * kLda;     // [2][16][128]
+    __shared__ int s_clamped;
+    const int tid = threadIdx.x;
+    const int64_t ntiles = (a.n + kTileRows - 1) / kTileRows;
+    const float *W1 = wp, *W2 = W1 + kIn * kHidden, *W3 = W2 + kHidden * kHidden,
+                *W4 = W3 + kHidden * kHidden;
+    if (tid == 0) s_clamped = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row0 = tile * kTileRows;
+        if (tid < kTileRows) {
+            const int64_t q = row0 + tid;
+            if (q < a.n) {
+                int cl = encode_row(a.x[q], a.wo[q], a.nrm[q], a.bounds, actA, tid);
+                if (cl) atomicAdd(&s_clamped, cl);
+            } else {
+                for (int k = 0; k < kIn; ++k) actA[k * kLda + tid] = 0.f;
+            }
+        }
+        __syncthreads();
+        tile_layer<128, kIn, kEpiRelu>(actA, actB, W1, wbuf, nullptr, tid);
+        tile_layer<128, kHidden, kEpiRelu>(actB, actA, W2, wbuf, nullptr, tid);
+        tile_layer<128, kHidden, kEpiRelu>(actA, actB, W3, wbuf, nullptr, tid);
+        tile_layer<128, kHidden, kEpiNone>(actB, actA, W4, wbuf, nullptr, tid);
+        if (tid < kTileRows) {
+            const int64_t q = row0 + tid;
+            if (q < a.n) {
+                const float *col = actA + tid;
+                auto raw = [&](int j) { return col[j * kLda]; };
+                if (MODE == kModeSample) {
+                    float c;
+                    a.dir_pdf[q] = guide_sample<N, true>(raw, a.xi[q], c);
+                    if (a.c) a.c[q] = c;
+                } else if (MODE == kModePdf) {
+                    float4 d = a.dir[q];
+                    float2 p = guide_pdf<N, true>(raw, make_float3(d.x, d.y, d.z), a.b,
+                                                  a.bsdf_pdf ? a.bsdf_pdf[q] : 0.f);
+                    if (a.mix_pdf) a.mix_pdf[q] = p.x;
+                    if (a.guided_pdf) a.guided_pdf[q] = p.y;
+                } else {
+                    constexpr int D = 8 * N + 1;
+                    for (int j = 0; j < D; ++j) a.raw[q * D + j] = raw(packed_col(j, N));
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (tid == 0 && s_clamped && a.clamp_count) atomicAdd(a.clamp_count, (unsigned long long)s_clamped);
+}
+
+constexpr size_t kQuerySmem = (2 * kHidden * kLda + 2 * kChunk * 128) * sizeof(float);
+
+template <int N>
+static int query_fp32_n(QueryMode mode, const float *wp, const QueryArgs &a, int num_sms, cudaStream_t s) {
+    const int64_t ntiles = (a.n + kTileRows - 1) / kTileRows;
+    const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+    if (grid == 0) return 0;
+    switch (mode) {
+#define NASG_LAUNCH(M)                                                                             \
+    case M: {                                                                                      \
+        auto k = query_fp32_kernel<N, M>;                                                          \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuerySmem);     \
+        k<<<grid, 256, kQuerySmem, s>>>(wp, a);                                                    \
+        break;                                                                                     \
+    }
+        NASG_LAUNCH(kModeSample)
+        NASG_LAUNCH(kModePdf)
+        NASG_LAUNCH(kModeRaw)
+#undef NASG_LAUNCH
+    }
+    return 1;
+}
+
+int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, int num_sms, cudaStream_t s) {
+    switch (n_comp) {  // packed W4 must fit 128 columns: H + 8N <= 128
+        case 4: return query_fp32_n<4>(mode, wp, a, num_sms, s);
+        case 8: return query_fp32_n<8>(mode, wp, a, num_sms, s);
+        default: return -1;
+    }
+}
+
+// ------------------------------------------------------ raw-output parity --
+template <int N, bool SAMPLE>
+__global__ void decode_raw_kernel(int64_t n, const float *__restrict__ raw, const float4 *xi,
+                                  const float4 *dir, float b, const float *bsdf_pdf, float4 *dir_pdf,
+                                  float *c, float *mix_pdf, float *guided_pdf) {
+    constexpr int D = 8 * N + 1, H = packed_header(N);
+    const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= n) return;
+    const float *row = raw + q * D;
+    auto rawf = [&](int j) -> float {  // packed column -> reference raw index
+        if (j < N) return row[7 * N + j];
+        if (j == N) return row[8 * N];
+        if (j < H) return 0.f;
+        const int i = (j - H) >> 3, k = (j - H) & 7;
+        return k < 5 ? row[5 * i + k] : (k == 5 ? row[5 * N + 2 * i] : (k == 6 ? row[5 * N + 2 * i + 1] : 0.f));
+    };
+    if (SAMPLE) {
+        float cc;
+        dir_pdf[q] = guide_sample<N, true>(rawf, xi[q], cc);
+        if (c) c[q] = cc;
+    } else {
+        float4 d = dir[q];
+        float2 p = guide_pdf<N, true>(rawf, make_float3(d.x, d.y, d.z), b, bsdf_pdf ? bsdf_pdf[q] : 0.f);
+        if (mix_pdf) mix_pdf[q] = p.x;
+        if (guided_pdf) guided_pdf[q] = p.y;
+    }
+}
+
+template <int N>
+static int decode_raw_n(bool sample, int64_t n, const float *raw, const float4 *xi, const float4 *dir,
+                        float b, const float *bsdf_pdf, float4 *dir_pdf, float *c, float *mix_pdf,
+                        float *guided_pdf, cudaStream_t s) {
+    const int blocks = (int)((n + 127) / 128);
+    if (blocks == 0) return 0;
+    if (sample)
+        decode_raw_kernel<N, true><<<blocks, 128, 0, s>>>(n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf);
+    else
+        decode_raw_kernel<N, false><<<blocks, 128, 0, s>>>(n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf);
+    return 1;
+}
+
+int decode_raw(int n_comp, bool sample, int64_t n, const float *raw, const float4 *xi, const float4 *dir,
+               float b, const float *bsdf_pdf, float4 *dir_pdf, float *c, float *mix_pdf, float *guided_pdf,
+               cudaStream_t s) {
+    switch (n_comp) {
+        case 4: return decode_raw_n<4>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s);
+        case 8: return decode_raw_n<8>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s);
+        case 16: return decode_raw_n<16>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s);
+        default: return -1;
+    }
+}
+
+}  // namespace nasg

@@ -1,0 +1,405 @@
+// fp32 training step (Trainer::train_iteration inner loop, guiding.cpp:236-276):
+//
+//   K_fb   per 64-row tile, on-chip: encode -> forward (h1..h3, raw) ->
+//          KL gradient epilogue (delta4, loss, drops) -> delta3, delta2,
+//          delta1 through W^T with the ReLU gates (backward net.hpp:95-110).
+//          Activations and deltas are written row-major for K_dw.
+//   K_dw   dW_l = h_l^T delta_{l+1}, split over rows into per-CTA partials
+//          (fixed split boundaries -> deterministic).
+//   K_red  grad = sum of partials in split order; non-finite flag.
+//          [multi-GPU: ncclAllReduce of grad + step stats happens here]
+//   K_fin  one thread: skip decision (net.hpp:140-144), t, bias corrections,
+//          loss/drop accumulation in tile order.
+//   K_adam adam_step<float> (net.hpp:146-156) with the reference's float
+//          operation order (no FMA contraction), and re-packing of the
+//          updated weights for the next step's K_fb.
+#include <cstdio>
+
+#include "nasg_internal.h"
+#include "nasg_math.cuh"
+#include "simt_gemm.cuh"
+
+namespace nasg {
+
+constexpr int kTrainRows = 64;
+constexpr int kTLda = kTrainRows + 4;  // 68
+
+// smem carve-up of K_fb (floats)
+constexpr int kOffH0 = 0;
+constexpr int kOffH1 = kOffH0 + kIn * kTLda;
+constexpr int kOffH2 = kOffH1 + kHidden * kTLda;
+constexpr int kOffH3 = kOffH2 + kHidden * kTLda;
+constexpr int kOffDA = kOffH3 + kHidden * kTLda;
+constexpr int kOffDB = kOffDA + kHidden * kTLda;
+constexpr int kOffW = kOffDB + kHidden * kTLda;
+constexpr int kOffRow = kOffW + 2 * kChunk * 128;          // 64 x 8 per-row sample data
+constexpr int kOffLoss = kOffRow + kTrainRows * 8;          // 64 losses
+constexpr int kFbFloats = kOffLoss + kTrainRows * 2;
+constexpr size_t kFbSmem = kFbFloats * sizeof(float);
+
+// feature-major smem [F][kTLda] -> row-major global [rows][F], rows < valid
+template <int F>
+__device__ __forceinline__ void store_rows(const float *sm, float *g, int64_t row0, int valid, int tid) {
+    for (int idx = tid; idx < kTrainRows * (F / 4); idx += 256) {
+        const int r = idx / (F / 4), f4 = (idx % (F / 4)) * 4;
+        float4 v;
+        if (r < valid) {
+            v = make_float4(sm[f4 * kTLda + r], sm[(f4 + 1) * kTLda + r], sm[(f4 + 2) * kTLda + r],
+                            sm[(f4 + 3) * kTLda + r]);
+        } else {
+            v = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        *reinterpret_cast<float4 *>(g + (row0 + r) * F + f4) = v;
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(256, 1)
+train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
+                const nasg_train_sample *__restrict__ samples, const uint32_t *__restrict__ order,
+                int64_t count, float gscale, float b, float e, Bounds bd, TrainScratch sc,
+                unsigned long long *clamp_count) {
+    constexpr int H = packed_header(N), NP = packed_width(N), D = 8 * N + 1;
+    extern __shared__ __align__(16) float sm[];
+    float *h0 = sm + kOffH0, *h1 = sm + kOffH1, *h2 = sm + kOffH2, *h3 = sm + kOffH3;
+    float *da = sm + kOffDA, *db = sm + kOffDB, *wbuf = sm + kOffW;
+    float *rowd = sm + kOffRow, *rloss = sm + kOffLoss;
+    __shared__ int s_clamped;
+    const int tid = threadIdx.x;
+    const float *W1 = wp, *W2 = W1 + kIn * kHidden, *W3 = W2 + kHidden * kHidden, *W4 = W3 + kHidden * kHidden;
+    const float *T2 = wtp, *T3 = T2 + kHidden * kHidden, *T4 = T3 + kHidden * kHidden;
+    const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
+    if (tid == 0) s_clamped = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row0 = (int64_t)tile * kTrainRows;
+        const int valid = (int)min((int64_t)kTrainRows, count - row0);
+        // ---- K1: gather + encode (guiding.cpp:209-214, 242-244)
+        if (tid < kTrainRows) {
+            float *rd = rowd + tid * 8;
+            if (tid < valid) {
+                const int64_t src = order ? (int64_t)order[row0 + tid] : row0 + tid;
+                const float4 *s4 = reinterpret_cast<const float4 *>(samples + src);
+                float4 a = s4[0], o = s4[1], n = s4[2], w = s4[3];
+                int cl = 0;
+                const float xs[3] = {a.x, a.y, a.z};
+#pragma unroll
+                for (int axis = 0; axis < 3; ++axis) {
+                    double t = bd.ext[axis] > 0.0 ? ((double)xs[axis] - (double)bd.bmin[axis]) / bd.ext[axis] : 0.5;
+                    if (t < 0.0 || t > 1.0) { ++cl; t = fmin(fmax(t, 0.0), 1.0); }
+#pragma unroll
+                    for (int i = 0; i < kBins; ++i) {
+                        float d = (float)(t - (i + 0.5) / kBins);
+                        h0[(axis * kBins + i) * kTLda + tid] = expf(-d * d * 180.5f);
+                    }
+                }
+                h0[57 * kTLda + tid] = o.x; h0[58 * kTLda + tid] = o.y; h0[59 * kTLda + tid] = o.z;
+                h0[60 * kTLda + tid] = n.x; h0[61 * kTLda + tid] = n.y; h0[62 * kTLda + tid] = n.z;
+                h0[63 * kTLda + tid] = 1.f;
+                if (cl) atomicAdd(&s_clamped, cl);
+                rd[0] = w.x; rd[1] = w.y; rd[2] = w.z;   // omega_i
+                rd[3] = a.w; rd[4] = o.w; rd[5] = n.w;   // p, q_sampling, bsdf_pdf
+            } else {
+                for (int k = 0; k < kIn; ++k) h0[k * kTLda + tid] = 0.f;
+            }
+        }
+        __syncthreads();
+        // ---- K2: forward (net.hpp:69-76)
+        tile_layer<kTrainRows, kIn, kEpiRelu, kTLda>(h0, h1, W1, wbuf, nullptr, tid);
+        tile_layer<kTrainRows, kHidden, kEpiRelu, kTLda>(h1, h2, W2, wbuf, nullptr, tid);
+        tile_layer<kTrainRows, kHidden, kEpiRelu, kTLda>(h2, h3, W3, wbuf, nullptr, tid);
+        tile_layer<kTrainRows, kHidden, kEpiNone, kTLda>(h3, da, W4, wbuf, nullptr, tid);
+        store_rows<kIn>(h0, sc.h0, row0, valid, tid);
+        store_rows<kHidden>(h1, sc.h1, row0, valid, tid);
+        store_rows<kHidden>(h2, sc.h2, row0, valid, tid);
+        store_rows<kHidden>(h3, sc.h3, row0, valid, tid);
+        // ---- K5: KL gradient epilogue, one thread per row (guiding.cpp:250-270)
+        if (tid < kTrainRows) {
+            float *col = da + tid;
+            float loss = 0.f;
+            int state = 0;  // 0 invalid row, 1 ok, 2 dropped
+            if (tid < valid) {
+                bool finite = true;
+                for (int j = 0; j < NP; ++j) finite &= isfinite(col[j * kTLda]);
+                if (!finite) {  // non-finite network output row -> dropped (:251-254)
+                    for (int j = 0; j < kHidden; ++j) col[j * kTLda] = 0.f;
+                    state = 2;
+                } else {
+                    const float *rd = rowd + tid * 8;
+                    TrainRow s;
+                    s.wi = make_float3(rd[0], rd[1], rd[2]);
+                    s.p = rd[3]; s.q_s = rd[4]; s.pbsdf = rd[5];
+                    auto raw = [&](int j) { return col[j * kTLda]; };
+                    auto put = [&](int j, float g) { col[j * kTLda] = g; };
+                    bool ok = kl_grad_row<N, true>(raw, s, b, e, gscale, put, loss);
+                    state = ok ? 1 : 2;
+                    for (int j = NP; j < kHidden; ++j) col[j * kTLda] = 0.f;
+                }
+            } else {
+                for (int j = 0; j < kHidden; ++j) col[j * kTLda] = 0.f;
+            }
+            rloss[tid] = (state == 1 && isfinite(loss)) ? loss : 0.f;
+            rloss[kTrainRows + tid] = __int_as_float(state == 1 && isfinite(loss) ? 1 : (state == 2 ? 2 : 0));
+            // delta4 in reference raw order, padded to 80 floats per row
+            float *g4 = sc.d4 + (row0 + tid) * 80;
+            if (tid < valid) {
+                for (int j = 0; j < D; ++j) g4[j] = col[packed_col(j, N) * kTLda];
+                for (int j = D; j < 80; ++j) g4[j] = 0.f;
+            } else {
+                for (int j = 0; j < 80; ++j) g4[j] = 0.f;
+            }
+        }
+        __syncthreads();
+        if (tid == 0) {  // tile statistics in row order (deterministic)
+            float ls = 0.f;
+            int lc = 0, dr = 0;
+            for (int r = 0; r < kTrainRows; ++r) {
+                int st = __float_as_int(rloss[kTrainRows + r]);
+                ls += rloss[r];
+                lc += st == 1;
+                dr += st == 2;
+            }
+            sc.tile_loss[tile] = ls;
+            sc.tile_loss_count[tile] = lc;
+            sc.tile_dropped[tile] = dr;
+        }
+        // ---- K6: delta propagation with ReLU gates (net.hpp:101-107)
+        tile_layer<kTrainRows, kHidden, kEpiMask, kTLda>(da, db, T4, wbuf, h3, tid);
+        store_rows<kHidden>(db, sc.d3, row0, valid, tid);
+        tile_layer<kTrainRows, kHidden, kEpiMask, kTLda>(db, da, T3, wbuf, h2, tid);
+        store_rows<kHidden>(da, sc.d2, row0, valid, tid);
+        tile_layer<kTrainRows, kHidden, kEpiMask, kTLda>(da, db, T2, wbuf, h1, tid);
+        store_rows<kHidden>(db, sc.d1, row0, valid, tid);
+        __syncthreads();
+    }
+    if (tid == 0 && s_clamped && clamp_count) atomicAdd(clamp_count, (unsigned long long)s_clamped);
+}
+
+int train_forward_backward(int n_comp, const float *wp, const float *wtp, const nasg_train_sample *samples,
+                           const uint32_t *order, int64_t count, int64_t global_count, float b, float loss_blend,
+                           const Bounds &bounds, TrainScratch &sc, int num_sms, unsigned long long *clamp_count,
+                           cudaStream_t s) {
+    const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
+    if (ntiles == 0) return 0;
+    const int grid = ntiles < num_sms ? ntiles : num_sms;
+    const float gscale = (float)(1.0 / (double)global_count);
+    if (n_comp != 8 && n_comp != 4) return -1;
+    auto k = n_comp == 8 ? train_fb_kernel<8> : train_fb_kernel<4>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
+    k<<<grid, 256, kFbSmem, s>>>(wp, wtp, samples, order, count, gscale, b, loss_blend, bounds, sc, clamp_count);
+    return 1;
+}
+
+// ------------------------------------------------------------------ K_dw --
+// partial[split][layer block] = sum over this split's rows of H^T Delta.
+template <int M>
+__global__ void __launch_bounds__(256)
+dw_kernel(const float *__restrict__ Hm, const float *__restrict__ Dm, int ldd, int n_out,
+          int64_t rows, int rows_per_split, float *__restrict__ partial, size_t partial_stride) {
+    __shared__ __align__(16) float As[2][kChunk][M];
+    __shared__ __align__(16) float Bs[2][kChunk][128];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    const int split = blockIdx.x;
+    const int64_t r0 = (int64_t)split * rows_per_split;
+    const int64_t r1 = min(rows, r0 + rows_per_split);
+    constexpr int RM = M / 16;
+    float acc[RM][8];
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+    const int nchunks = r1 > r0 ? (int)((r1 - r0 + kChunk - 1) / kChunk) : 0;
+    auto load = [&](int c, int buf) {
+        const int64_t rb = r0 + (int64_t)c * kChunk;
+        for (int e = tid; e < kChunk * M / 4; e += 256) {  // H rows (contiguous)
+            const int rr = e / (M / 4), f4 = (e % (M / 4)) * 4;
+            cp_async16(&As[buf][rr][f4], Hm + (rb + rr) * M + f4);
+        }
+        for (int e = tid; e < kChunk * 32; e += 256) {  // Delta rows, 128 cols (reads past ldd are discarded)
+            const int rr = e / 32, f4 = (e % 32) * 4;
+            cp_async16(&Bs[buf][rr][f4], Dm + (rb + rr) * ldd + f4);
+        }
+    };
+    if (nchunks > 0) {
+        load(0, 0);
+        cp_async_commit();
+    }
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) {
+            load(c + 1, (c + 1) & 1);
+            cp_async_commit();
+            cp_async_wait<1>();
+        } else {
+            cp_async_wait<0>();
+        }
+        __syncthreads();
+        const int buf = c & 1;
+#pragma unroll
+        for (int kk = 0; kk < kChunk; ++kk) {
+            float a[RM];
+#pragma unroll
+            for (int h = 0; h < RM / 4; ++h) {
+                float4 t = *reinterpret_cast<const float4 *>(&As[buf][kk][ty * 4 + 64 * h]);
+                a[4 * h] = t.x; a[4 * h + 1] = t.y; a[4 * h + 2] = t.z; a[4 * h + 3] = t.w;
+            }
+            float4 b0 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][tx * 4]);
+            float4 b1 = *reinterpret_cast<const float4 *>(&Bs[buf][kk][64 + tx * 4]);
+            float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+            for (int i = 0; i < RM; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], bb[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+    float *out = partial + (size_t)split * partial_stride;
+#pragma unroll
+    for (int i = 0; i < RM; ++i) {
+        const int m = ty * 4 + 64 * (i / 4) + (i % 4);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int n = (j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+            if (n < n_out) out[(size_t)m * n_out + n] = acc[i][j];
+        }
+    }
+}
+
+__global__ void dw_reduce_kernel(const float *__restrict__ partial, int splits, size_t stride, int nw,
+                                 float *__restrict__ grad, int *nonfinite) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nw) return;
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += partial[(size_t)k * stride + e];
+    grad[e] = s;
+    if (!isfinite(s)) atomicOr(nonfinite, 1);
+}
+
+int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStream_t s) {
+    const int D = 8 * n_comp + 1;
+    const int nw = n_weights(n_comp);
+    const int64_t rows = ((count + kTrainRows - 1) / kTrainRows) * kTrainRows;  // zero-padded tail
+    int splits = (int)((rows + 63) / 64);
+    if (splits > sc.splits) splits = sc.splits;
+    int rps = (int)((rows + splits - 1) / splits);
+    rps = ((rps + kChunk - 1) / kChunk) * kChunk;
+    splits = (int)((rows + rps - 1) / rps);
+    const size_t stride = (size_t)nw;
+    float *p = sc.dw_partial;
+    const size_t o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
+    dw_kernel<64><<<splits, 256, 0, s>>>(sc.h0, sc.d1, 128, 128, rows, rps, p, stride);
+    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h1, sc.d2, 128, 128, rows, rps, p + o1, stride);
+    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h2, sc.d3, 128, 128, rows, rps, p + o2, stride);
+    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h3, sc.d4, 80, D, rows, rps, p + o3, stride);
+    sc.last_splits = splits;
+    return 1;
+}
+
+int train_reduce(int n_comp, const TrainScratch &sc, float *grad, int *nonfinite, cudaStream_t s) {
+    const int nw = n_weights(n_comp);
+    dw_reduce_kernel<<<(nw + 255) / 256, 256, 0, s>>>(sc.dw_partial, sc.last_splits, (size_t)nw, nw, grad, nonfinite);
+    return 1;
+}
+
+// step_stats[0..2] = loss_sum, loss_count, dropped of this step (tile order)
+__global__ void step_stats_kernel(const float *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
+                                  double *step_stats) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double ls = 0.0, lc = 0.0, dr = 0.0;
+    for (int t = 0; t < ntiles; ++t) {
+        ls += (double)tile_loss[t];
+        lc += tile_lc[t];
+        dr += tile_dr[t];
+    }
+    step_stats[0] = ls;
+    step_stats[1] = lc;
+    step_stats[2] = dr;
+}
+
+int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s) {
+    const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
+    step_stats_kernel<<<1, 32, 0, s>>>(sc.tile_loss, sc.tile_loss_count, sc.tile_dropped, ntiles, step_stats);
+    return 1;
+}
+
+// acc[0..4] = loss_sum, loss_count, dropped, skipped, steps (context accumulators)
+__global__ void finalize_kernel(int *nonfinite, int64_t *adam_t, float *corr, int *skip, const double *step_stats,
+                                double *acc) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    const int sk = *nonfinite != 0;
+    *nonfinite = 0;
+    *skip = sk;
+    if (!sk) {
+        const int64_t t = *adam_t + 1;
+        *adam_t = t;
+        // corr = 1 - beta^t computed as powf would (float result), net.hpp:146-147
+        corr[0] = 1.0f - (float)pow((double)0.9f, (double)(float)t);
+        corr[1] = 1.0f - (float)pow((double)0.999f, (double)(float)t);
+    }
+    acc[0] += step_stats[0];
+    acc[1] += step_stats[1];
+    acc[2] += step_stats[2];
+    acc[3] += sk;
+    acc[4] += 1.0;
+}
+
+int train_finalize_step(int *nonfinite, int64_t *adam_t, float *corr, int *skip, const double *step_stats,
+                        double *acc, cudaStream_t s) {
+    finalize_kernel<<<1, 32, 0, s>>>(nonfinite, adam_t, corr, skip, step_stats, acc);
+    return 1;
+}
+
+// ---------------------------------------------------------------- K_adam --
+// adam_step<float> net.hpp:146-156 with the reference's operation order and
+// IEEE rounding of every float op (no FMA contraction), then re-pack.
+__global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict__ m, float *__restrict__ v,
+                            const float *__restrict__ g, const float *corr, const int *skip, float lr,
+                            float *__restrict__ wp, float *__restrict__ wtp) {
+    const int nw = n_weights(n_comp);
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nw || *skip) return;
+    const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+    const float c1 = corr[0], c2 = corr[1];
+    const float gi = g[e];
+    const float mi = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(__fsub_rn(1.f, b1), gi));
+    const float vi = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(__fsub_rn(1.f, b2), __fmul_rn(gi, gi)));
+    const float mh = __fdiv_rn(mi, c1), vh = __fdiv_rn(vi, c2);
+    const float wi = __fsub_rn(w[e], __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps)));
+    m[e] = mi;
+    v[e] = vi;
+    w[e] = wi;
+    // re-pack (same mapping as pack_fp32_kernel)
+    const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
+    if (e < o3) {
+        wp[e] = wi;
+        if (e >= o1) {
+            const int l = e < o2 ? 0 : 1, base = l == 0 ? o1 : o2;
+            const int k = (e - base) / kHidden, col = (e - base) % kHidden;
+            wtp[l * kHidden * kHidden + col * kHidden + k] = wi;
+        }
+    } else {
+        const int D = 8 * n_comp + 1;
+        const int k = (e - o3) / D, j = (e - o3) % D;
+        const int pc = packed_col(j, n_comp);
+        wp[o3 + k * kHidden + pc] = wi;
+        wtp[2 * kHidden * kHidden + pc * kHidden + k] = wi;
+    }
+}
+
+int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, const float *corr, const int *skip,
+               float lr, float *wp, float *wtp, cudaStream_t s) {
+    const int nw = n_weights(n_comp);
+    adam_kernel<<<(nw + 255) / 256, 256, 0, s>>>(n_comp, w, m, v, grad, corr, skip, lr, wp, wtp);
+    return 1;
+}
+
+}  // namespace nasg
+
+namespace nasg {
+__global__ void check_finite_kernel(const float *x, int n, int *nonfinite) {
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n && !isfinite(x[e])) atomicOr(nonfinite, 1);
+}
+int check_finite(const float *x, int n, int *nonfinite, cudaStream_t s) {
+    check_finite_kernel<<<(n + 255) / 256, 256, 0, s>>>(x, n, nonfinite);
+    return 1;
+}
+}  // namespace nasg

@@ -1,0 +1,811 @@
+// Host side of the B200-native NASG guiding path: context, snapshots,
+// training loop, checkpoint I/O, NCCL, synthetic workloads — all behind the
+// C ABI in include/nasg/nasg.h.  Mirrors the reference's C++ guiding API
+// (guiding.hpp, net.hpp, sphdist.hpp) with batched, stream-ordered calls.
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include "nasg/nasg.h"
+#include "nasg_internal.h"
+
+using namespace nasg;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define CUDA_TRY(x)                                                                        \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) return fail(NASG_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+#define CHECK_LAUNCH()                                                                     \
+    do {                                                                                   \
+        cudaError_t e_ = cudaGetLastError();                                               \
+        if (e_ != cudaSuccess) return fail(NASG_ERR_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+// splitmix64 / hash_combine / PCG32 (math.hpp:74-121) — the specified RNG of
+// the reference's weight init, epoch shuffle and our synthetic inputs.
+uint64_t hash_mix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+uint64_t hash_combine(uint64_t a, uint64_t b) { return hash_mix(a ^ (b + 0x9e3779b97f4a7c15ull + (a << 6) + (a >> 2))); }
+
+struct Pcg32 {
+    uint64_t state = 0, inc = 0;
+    Pcg32(uint64_t initstate, uint64_t initseq) {
+        inc = (initseq << 1u) | 1u;
+        next();
+        state += initstate;
+        next();
+    }
+    uint32_t next() {
+        uint64_t old = state;
+        state = old * 6364136223846793005ull + inc;
+        uint32_t xs = (uint32_t)(((old >> 18u) ^ old) >> 27u);
+        uint32_t rot = (uint32_t)(old >> 59u);
+        return (xs >> rot) | (xs << ((~rot + 1u) & 31));
+    }
+    double next_double() { return next() * 0x1p-32; }
+    uint32_t next_below(uint32_t n) { return (uint32_t)(((uint64_t)next() * n) >> 32); }
+    float next_f24() { return (float)(next() >> 8) * 0x1p-24f; }
+};
+
+// init_network<float> (net.hpp:43-57), bit-exact.
+void init_network(uint64_t seed, int n_comp, float *w) {
+    const int dims[5] = {kIn, kHidden, kHidden, kHidden, 8 * n_comp + 1};
+    Pcg32 rng(hash_mix(seed), 0xda3e39cb94b95bdbull);
+    for (int l = 0; l < 4; ++l) {
+        const double limit = std::sqrt(6.0 / dims[l]);
+        for (int r = 0; r < dims[l]; ++r)
+            for (int c = 0; c < dims[l + 1]; ++c) *w++ = (float)((rng.next_double() * 2.0 - 1.0) * limit);
+    }
+}
+
+// ---- NCCL, loaded lazily (the query path never needs it) ----------------------
+struct Nccl {
+    void *h = nullptr;
+    ncclResult_t (*getUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    const char *(*errStr)(ncclResult_t) = nullptr;
+    bool load() {
+        if (h) return true;
+        h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) return false;
+        getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+        commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+        allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+        commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+        errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
+        return getUniqueId && commInitRank && allReduce && commDestroy;
+    }
+};
+Nccl g_nccl;
+std::mutex g_nccl_mu;
+
+}  // namespace
+
+struct nasg_ctx {
+    nasg_config cfg{};
+    int device = 0, N = 8, D = 65, nw = 0, num_sms = 148;
+    Bounds bounds{};
+    float bmax[3]{};
+    cudaStream_t stream = nullptr;
+    cudaStream_t lanes[3] = {nullptr, nullptr, nullptr};
+    // live parameters + Adam (Trainer::params_, adam_ guiding.hpp:162-163)
+    float *w = nullptr, *m = nullptr, *v = nullptr, *grad = nullptr;
+    float *wp = nullptr, *wtp = nullptr;  // packed live (training forward/backward)
+    // published snapshot (NetworkSnapshot net.hpp:161)
+    float *w_pub = nullptr, *wp_pub = nullptr;
+    void *tc_pub = nullptr;
+    int precision = NASG_MLP_FP32;
+    unsigned long long *d_clamp = nullptr;
+    // Adam / step state on device
+    int64_t *d_adam_t = nullptr;
+    float *d_corr = nullptr;
+    int *d_skip = nullptr, *d_nonfinite = nullptr;
+    double *d_step_stats = nullptr, *d_acc = nullptr;
+    TrainScratch sc{};
+    uint32_t *d_order = nullptr, *h_order = nullptr;
+    size_t order_cap = 0;
+    int64_t iterations = 0;
+    // host pipeline buffers (nasg_query_sample_host)
+    float *lane_in[3] = {nullptr, nullptr, nullptr}, *lane_out[3] = {nullptr, nullptr, nullptr};
+    int64_t lane_cap = 0;
+    // NCCL
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    uint64_t launches = 0;
+};
+
+namespace {
+
+int ensure_scratch(nasg_ctx *c, int64_t count) {
+    const int64_t rows = ((count + 63) / 64) * 64;
+    if (rows <= c->sc.max_rows) return NASG_OK;
+    TrainScratch &s = c->sc;
+    float **bufs[8] = {&s.h0, &s.h1, &s.h2, &s.h3, &s.d1, &s.d2, &s.d3, &s.d4};
+    const int widths[8] = {64, 128, 128, 128, 128, 128, 128, 80};
+    for (int i = 0; i < 8; ++i) {
+        if (*bufs[i]) cudaFree(*bufs[i]);
+        *bufs[i] = nullptr;
+        CUDA_TRY(cudaMalloc(bufs[i], (size_t)(rows * widths[i] + 128) * sizeof(float)));
+    }
+    const int tiles = (int)(rows / 64);
+    if (s.tile_loss) cudaFree(s.tile_loss);
+    if (s.tile_loss_count) cudaFree(s.tile_loss_count);
+    if (s.tile_dropped) cudaFree(s.tile_dropped);
+    CUDA_TRY(cudaMalloc(&s.tile_loss, tiles * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&s.tile_loss_count, tiles * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&s.tile_dropped, tiles * sizeof(int)));
+    if (!s.dw_partial) {
+        s.splits = 128;
+        CUDA_TRY(cudaMalloc(&s.dw_partial, (size_t)s.splits * c->nw * sizeof(float)));
+    }
+    s.max_rows = rows;
+    s.max_tiles = tiles;
+    return NASG_OK;
+}
+
+int ensure_order(nasg_ctx *c, size_t n) {
+    if (n <= c->order_cap) return NASG_OK;
+    if (c->d_order) cudaFree(c->d_order);
+    if (c->h_order) cudaFreeHost(c->h_order);
+    CUDA_TRY(cudaMalloc(&c->d_order, n * sizeof(uint32_t)));
+    CUDA_TRY(cudaMallocHost(&c->h_order, n * sizeof(uint32_t)));
+    c->order_cap = n;
+    return NASG_OK;
+}
+
+int do_publish(nasg_ctx *c) {
+    CUDA_TRY(cudaMemcpyAsync(c->w_pub, c->w, c->nw * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    launch_pack_fp32(c->w_pub, c->N, c->wp_pub, nullptr, c->stream);
+    c->launches++;
+    if (c->tc_pub) {
+        launch_pack_tc(c->w_pub, c->N, c->tc_pub, c->stream);
+        c->launches++;
+    }
+    CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+int repack_live(nasg_ctx *c) {
+    launch_pack_fp32(c->w, c->N, c->wp, c->wtp, c->stream);
+    c->launches++;
+    CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+cudaStream_t pick(nasg_ctx *c, void *s) { return s ? (cudaStream_t)s : c->stream; }
+
+QueryArgs base_args(nasg_ctx *c, int64_t n) {
+    QueryArgs a{};
+    a.n = n;
+    a.bounds = c->bounds;
+    a.clamp_count = c->d_clamp;
+    return a;
+}
+
+int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
+    if (a.n == 0) return NASG_OK;
+    int r;
+    if (c->precision == NASG_MLP_BF16) {
+        if (!c->tc_pub) return fail(NASG_ERR_UNSUPPORTED, "bf16 tensor-core path not available for this N");
+        r = query_tc(c->N, mode, c->tc_pub, a, c->num_sms, s);
+    } else {
+        r = query_fp32(c->N, mode, c->wp_pub, a, c->num_sms, s);
+    }
+    if (r < 0) return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for this path");
+    c->launches += r;
+    CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+// One minibatch step (guiding.cpp:236-276) on rows samples[order[0..count)].
+int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
+                    int64_t global_count, double b, cudaStream_t s) {
+    if (count <= 0 && c->nranks == 1) return NASG_OK;
+    int r = ensure_scratch(c, std::max<int64_t>(count, 1));
+    if (r) return r;
+    if (count > 0) {
+        if (train_forward_backward(c->N, c->wp, c->wtp, samples, order, count, global_count, (float)b,
+                                   (float)c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, c->d_clamp, s) < 0)
+            return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for training");
+        train_dw(c->N, count, c->sc, c->grad, s);
+        train_reduce(c->N, c->sc, c->grad, c->d_nonfinite, s);
+        train_step_stats(c->sc, count, c->d_step_stats, s);
+        c->launches += 8;
+    } else {
+        CUDA_TRY(cudaMemsetAsync(c->grad, 0, c->nw * sizeof(float), s));
+        CUDA_TRY(cudaMemsetAsync(c->d_step_stats, 0, 3 * sizeof(double), s));
+    }
+    CHECK_LAUNCH();
+    if (c->nranks > 1) {  // data-parallel exchange: sum of unnormalised-by-rank grads
+        ncclResult_t e1 = g_nccl.allReduce(c->grad, c->grad, c->nw, ncclFloat32, ncclSum, c->comm, s);
+        ncclResult_t e2 = g_nccl.allReduce(c->d_step_stats, c->d_step_stats, 3, ncclFloat64, ncclSum, c->comm, s);
+        if (e1 != ncclSuccess || e2 != ncclSuccess) return fail(NASG_ERR_NCCL, "ncclAllReduce failed");
+        CUDA_TRY(cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int), s));
+        check_finite(c->grad, c->nw, c->d_nonfinite, s);
+        c->launches++;
+    }
+    train_finalize_step(c->d_nonfinite, c->d_adam_t, c->d_corr, c->d_skip, c->d_step_stats, c->d_acc, s);
+    train_adam(c->N, c->w, c->m, c->v, c->grad, c->d_corr, c->d_skip, c->cfg.learning_rate, c->wp, c->wtp, s);
+    c->launches += 2;
+    CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+bool is_pinned(const void *p) {
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *nasg_status_string(int s) {
+    switch (s) {
+        case NASG_OK: return "ok";
+        case NASG_ERR_INVALID: return "invalid argument";
+        case NASG_ERR_CUDA: return "cuda error";
+        case NASG_ERR_NCCL: return "nccl error";
+        case NASG_ERR_IO: return "i/o error";
+        case NASG_ERR_OOM: return "out of memory";
+        case NASG_ERR_UNSUPPORTED: return "unsupported";
+        default: return "unknown";
+    }
+}
+
+const char *nasg_last_error(void) { return g_err.c_str(); }
+
+int nasg_n_weights(int n_components) { return n_weights(n_components); }
+
+void nasg_config_default(nasg_config *c) {
+    c->n_components = 8;
+    c->sample_capacity = 1 << 16;
+    c->batch_size = 1 << 12;
+    c->step_factor = 1;
+    c->learning_rate = 0.002f;
+    c->loss_blend = 0.2;
+    c->seed = 0;
+}
+
+int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const float bmax[3], nasg_ctx **out) {
+    if (!cfg || !out || !bmin || !bmax) return fail(NASG_ERR_INVALID, "null argument");
+    if (cfg->n_components != 4 && cfg->n_components != 8)
+        return fail(NASG_ERR_UNSUPPORTED, "n_components must be 4 or 8 in this build");
+    if (cfg->batch_size <= 0 || cfg->sample_capacity <= 0 || cfg->step_factor <= 0)
+        return fail(NASG_ERR_INVALID, "batch_size, sample_capacity, step_factor must be > 0");
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(NASG_ERR_INVALID, "bad device ordinal");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(NASG_ERR_CUDA, "this build targets sm_100a (B200); device is sm_" +
+                                       std::to_string(prop.major * 10 + prop.minor));
+    nasg_ctx *c = new nasg_ctx();
+    c->cfg = *cfg;
+    c->device = device;
+    c->N = cfg->n_components;
+    c->D = 8 * c->N + 1;
+    c->nw = n_weights(c->N);
+    c->num_sms = prop.multiProcessorCount;
+    for (int k = 0; k < 3; ++k) {
+        c->bounds.bmin[k] = bmin[k];
+        c->bmax[k] = bmax[k];
+        c->bounds.ext[k] = (double)bmax[k] - (double)bmin[k];
+    }
+    auto cleanup_fail = [&](int code) {
+        nasg_destroy(c);
+        return code;
+    };
+#define ALLOC(p, bytes)                                                             \
+    do {                                                                            \
+        if (cudaMalloc(&(p), (bytes)) != cudaSuccess) {                            \
+            cudaGetLastError();                                                     \
+            fail(NASG_ERR_OOM, "cudaMalloc failed");                                \
+            return cleanup_fail(NASG_ERR_OOM);                                      \
+        }                                                                           \
+    } while (0)
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return cleanup_fail(fail(NASG_ERR_CUDA, "stream create failed"));
+    for (auto &l : c->lanes)
+        if (cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking) != cudaSuccess)
+            return cleanup_fail(fail(NASG_ERR_CUDA, "stream create failed"));
+    const size_t wb = c->nw * sizeof(float);
+    ALLOC(c->w, wb); ALLOC(c->m, wb); ALLOC(c->v, wb); ALLOC(c->grad, wb); ALLOC(c->w_pub, wb);
+    ALLOC(c->wp, kPackedF32 * sizeof(float));
+    ALLOC(c->wtp, kPackedT32 * sizeof(float));
+    ALLOC(c->wp_pub, kPackedF32 * sizeof(float));
+    if (tc_supported(c->N)) ALLOC(c->tc_pub, tc_image_bytes(c->N));
+    ALLOC(c->d_clamp, sizeof(unsigned long long));
+    ALLOC(c->d_adam_t, sizeof(int64_t));
+    ALLOC(c->d_corr, 2 * sizeof(float));
+    ALLOC(c->d_skip, sizeof(int));
+    ALLOC(c->d_nonfinite, sizeof(int));
+    ALLOC(c->d_step_stats, 3 * sizeof(double));
+    ALLOC(c->d_acc, 5 * sizeof(double));
+#undef ALLOC
+    cudaMemsetAsync(c->m, 0, wb, c->stream);
+    cudaMemsetAsync(c->v, 0, wb, c->stream);
+    cudaMemsetAsync(c->d_clamp, 0, sizeof(unsigned long long), c->stream);
+    cudaMemsetAsync(c->d_adam_t, 0, sizeof(int64_t), c->stream);
+    cudaMemsetAsync(c->d_skip, 0, sizeof(int), c->stream);
+    cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int), c->stream);
+    cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream);
+    std::vector<float> w(c->nw);
+    init_network(cfg->seed, c->N, w.data());
+    if (cudaMemcpy(c->w, w.data(), wb, cudaMemcpyHostToDevice) != cudaSuccess)
+        return cleanup_fail(fail(NASG_ERR_CUDA, "weight upload failed"));
+    int r = repack_live(c);
+    if (!r) r = do_publish(c);
+    if (!r && cudaStreamSynchronize(c->stream) != cudaSuccess) r = fail(NASG_ERR_CUDA, "init sync failed");
+    if (r) return cleanup_fail(r);
+    *out = c;
+    return NASG_OK;
+}
+
+int nasg_destroy(nasg_ctx *c) {
+    if (!c) return NASG_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+    void *bufs[] = {c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->w_pub, c->wp_pub, c->tc_pub, c->d_clamp,
+                    c->d_adam_t, c->d_corr, c->d_skip, c->d_nonfinite, c->d_step_stats, c->d_acc, c->d_order,
+                    c->sc.h0, c->sc.h1, c->sc.h2, c->sc.h3, c->sc.d1, c->sc.d2, c->sc.d3, c->sc.d4,
+                    c->sc.dw_partial, c->sc.tile_loss, c->sc.tile_loss_count, c->sc.tile_dropped,
+                    c->lane_in[0], c->lane_in[1], c->lane_in[2], c->lane_out[0], c->lane_out[1], c->lane_out[2]};
+    for (void *p : bufs)
+        if (p) cudaFree(p);
+    if (c->h_order) cudaFreeHost(c->h_order);
+    for (auto l : c->lanes)
+        if (l) cudaStreamDestroy(l);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return NASG_OK;
+}
+
+int nasg_set_weights(nasg_ctx *c, const float *host_w, size_t n) {
+    if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
+    if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
+    CUDA_TRY(cudaMemcpyAsync(c->w, host_w, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
+    int r = repack_live(c);
+    if (!r) r = do_publish(c);
+    if (!r) CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return r;
+}
+
+int nasg_get_weights(nasg_ctx *c, float *host_w, size_t n, int published) {
+    if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
+    if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
+    CUDA_TRY(cudaMemcpyAsync(host_w, published ? c->w_pub : c->w, n * sizeof(float), cudaMemcpyDeviceToHost,
+                             c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return NASG_OK;
+}
+
+int nasg_publish(nasg_ctx *c) {
+    if (!c) return fail(NASG_ERR_INVALID, "null context");
+    return do_publish(c);
+}
+
+int nasg_set_precision(nasg_ctx *c, int p) {
+    if (!c) return fail(NASG_ERR_INVALID, "null context");
+    if (p != NASG_MLP_FP32 && p != NASG_MLP_BF16) return fail(NASG_ERR_INVALID, "bad precision");
+    if (p == NASG_MLP_BF16 && !c->tc_pub) return fail(NASG_ERR_UNSUPPORTED, "bf16 path unavailable");
+    c->precision = p;
+    return NASG_OK;
+}
+
+int nasg_get_precision(nasg_ctx *c) { return c ? c->precision : -1; }
+
+// NASGNET1 (net.cpp:31-82): magic, u32 N, u32 5, u32 dims[5], row-major f32 W1..W4.
+int nasg_save_checkpoint(nasg_ctx *c, const char *path) {
+    if (!c || !path) return fail(NASG_ERR_INVALID, "null argument");
+    std::vector<float> w(c->nw);
+    int r = nasg_get_weights(c, w.data(), w.size(), 0);
+    if (r) return r;
+    FILE *f = std::fopen(path, "wb");
+    if (!f) return fail(NASG_ERR_IO, std::string("cannot open checkpoint for writing: ") + path);
+    auto u32 = [&](uint32_t v) {
+        unsigned char b[4] = {(unsigned char)v, (unsigned char)(v >> 8), (unsigned char)(v >> 16), (unsigned char)(v >> 24)};
+        std::fwrite(b, 1, 4, f);
+    };
+    std::fwrite("NASGNET1", 1, 8, f);
+    u32((uint32_t)c->N);
+    u32(5);
+    const uint32_t dims[5] = {(uint32_t)kIn, (uint32_t)kHidden, (uint32_t)kHidden, (uint32_t)kHidden, (uint32_t)c->D};
+    for (uint32_t d : dims) u32(d);
+    bool ok = std::fwrite(w.data(), sizeof(float), w.size(), f) == w.size();
+    ok &= std::fclose(f) == 0;
+    return ok ? NASG_OK : fail(NASG_ERR_IO, std::string("short write on checkpoint: ") + path);
+}
+
+int nasg_load_checkpoint(nasg_ctx *c, const char *path) {
+    if (!c || !path) return fail(NASG_ERR_INVALID, "null argument");
+    FILE *f = std::fopen(path, "rb");
+    if (!f) return fail(NASG_ERR_IO, std::string("cannot open checkpoint: ") + path);
+    char magic[8];
+    bool ok = std::fread(magic, 1, 8, f) == 8 && std::memcmp(magic, "NASGNET1", 8) == 0;
+    auto u32 = [&]() -> uint32_t {
+        unsigned char b[4] = {0, 0, 0, 0};
+        if (std::fread(b, 1, 4, f) != 4) ok = false;
+        return (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+    };
+    if (!ok) {
+        std::fclose(f);
+        return fail(NASG_ERR_IO, std::string("not a network checkpoint: ") + path);
+    }
+    const uint32_t n = u32(), nd = u32();
+    if (!ok || nd != 5) {
+        std::fclose(f);
+        return fail(NASG_ERR_IO, std::string("unexpected layer count in checkpoint: ") + path);
+    }
+    uint32_t dims[5];
+    for (auto &d : dims) d = u32();
+    if ((int)n != c->N || dims[0] != (uint32_t)kIn || dims[1] != (uint32_t)kHidden || dims[2] != (uint32_t)kHidden ||
+        dims[3] != (uint32_t)kHidden || dims[4] != (uint32_t)c->D) {
+        std::fclose(f);
+        return fail(NASG_ERR_INVALID, "checkpoint shape does not match this context");
+    }
+    std::vector<float> w(c->nw);
+    ok &= std::fread(w.data(), sizeof(float), w.size(), f) == w.size();
+    std::fclose(f);
+    if (!ok) return fail(NASG_ERR_IO, std::string("truncated checkpoint: ") + path);
+    return nasg_set_weights(c, w.data(), w.size());
+}
+
+// ---- queries --------------------------------------------------------------------
+int nasg_query_sample(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, const float *xi,
+                      float *dir_pdf, float *cc, void *stream) {
+    if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
+    QueryArgs a = base_args(c, n);
+    a.x = (const float4 *)x; a.wo = (const float4 *)wo; a.nrm = (const float4 *)nrm; a.xi = (const float4 *)xi;
+    a.dir_pdf = (float4 *)dir_pdf; a.c = cc;
+    return run_query(c, kModeSample, a, pick(c, stream));
+}
+
+int nasg_query_pdf(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, const float *dir,
+                   float b, const float *bsdf_pdf, float *mix_pdf, float *guided_pdf, void *stream) {
+    if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !dir))) return fail(NASG_ERR_INVALID, "bad argument");
+    QueryArgs a = base_args(c, n);
+    a.x = (const float4 *)x; a.wo = (const float4 *)wo; a.nrm = (const float4 *)nrm; a.dir = (const float4 *)dir;
+    a.b = b; a.bsdf_pdf = bsdf_pdf; a.mix_pdf = mix_pdf; a.guided_pdf = guided_pdf;
+    return run_query(c, kModePdf, a, pick(c, stream));
+}
+
+int nasg_query_raw(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, float *raw,
+                   void *stream) {
+    if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !raw))) return fail(NASG_ERR_INVALID, "bad argument");
+    QueryArgs a = base_args(c, n);
+    a.x = (const float4 *)x; a.wo = (const float4 *)wo; a.nrm = (const float4 *)nrm; a.raw = raw;
+    return run_query(c, kModeRaw, a, pick(c, stream));
+}
+
+int nasg_decode_sample_raw(nasg_ctx *c, int64_t n, const float *raw, const float *xi, float *dir_pdf, float *cc,
+                           void *stream) {
+    if (!c || n < 0 || (n > 0 && (!raw || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
+    if (n == 0) return NASG_OK;
+    if (decode_raw(c->N, true, n, raw, (const float4 *)xi, nullptr, 0.f, nullptr, (float4 *)dir_pdf, cc, nullptr,
+                   nullptr, pick(c, stream)) < 0)
+        return fail(NASG_ERR_UNSUPPORTED, "n_components");
+    c->launches++;
+    CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+int nasg_decode_pdf_raw(nasg_ctx *c, int64_t n, const float *raw, const float *dir, float b, const float *bsdf_pdf,
+                        float *mix_pdf, float *guided_pdf, void *stream) {
+    if (!c || n < 0 || (n > 0 && (!raw || !dir))) return fail(NASG_ERR_INVALID, "bad argument");
+    if (n == 0) return NASG_OK;
+    if (decode_raw(c->N, false, n, raw, nullptr, (const float4 *)dir, b, bsdf_pdf, nullptr, nullptr, mix_pdf,
+                   guided_pdf, pick(c, stream)) < 0)
+        return fail(NASG_ERR_UNSUPPORTED, "n_components");
+    c->launches++;
+    CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+// Host-buffer query: 3 lanes (streams) x chunk; lane k: H2D(i) -> kernel(i) ->
+// D2H(i), so copies in both directions overlap the kernels of other chunks.
+int nasg_query_sample_host(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm,
+                           const float *xi, float *dir_pdf, float *cc) {
+    if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
+    if (n == 0) return NASG_OK;
+    const int64_t chunk = std::min<int64_t>(n, 1 << 20);
+    if (chunk > c->lane_cap) {
+        for (int k = 0; k < 3; ++k) {
+            if (c->lane_in[k]) cudaFree(c->lane_in[k]);
+            if (c->lane_out[k]) cudaFree(c->lane_out[k]);
+            c->lane_in[k] = c->lane_out[k] = nullptr;
+            CUDA_TRY(cudaMalloc(&c->lane_in[k], chunk * 16 * sizeof(float)));
+            CUDA_TRY(cudaMalloc(&c->lane_out[k], chunk * 5 * sizeof(float)));
+        }
+        c->lane_cap = chunk;
+    }
+    // the snapshot must be complete before any lane reads it
+    cudaEvent_t ready;
+    CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ready, c->stream));
+    for (auto l : c->lanes) CUDA_TRY(cudaStreamWaitEvent(l, ready, 0));
+    cudaEventDestroy(ready);
+    int64_t i = 0;
+    for (int64_t off = 0; off < n; off += chunk, ++i) {
+        const int64_t m = std::min(chunk, n - off);
+        const int k = (int)(i % 3);
+        cudaStream_t s = c->lanes[k];
+        float *in = c->lane_in[k], *out = c->lane_out[k];
+        const size_t vb = (size_t)m * 4 * sizeof(float);
+        CUDA_TRY(cudaMemcpyAsync(in, x + off * 4, vb, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(in + chunk * 4, wo + off * 4, vb, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(in + chunk * 8, nrm + off * 4, vb, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(in + chunk * 12, xi + off * 4, vb, cudaMemcpyHostToDevice, s));
+        int r = nasg_query_sample(c, m, in, in + chunk * 4, in + chunk * 8, in + chunk * 12, out,
+                                  cc ? out + chunk * 4 : nullptr, s);
+        if (r) return r;
+        CUDA_TRY(cudaMemcpyAsync(dir_pdf + off * 4, out, vb, cudaMemcpyDeviceToHost, s));
+        if (cc) CUDA_TRY(cudaMemcpyAsync(cc + off, out + chunk * 4, m * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    for (auto l : c->lanes) CUDA_TRY(cudaStreamSynchronize(l));
+    return NASG_OK;
+}
+
+// ---- training -----------------------------------------------------------------------
+int nasg_train_step(nasg_ctx *c, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
+                    int64_t global_count, double b, void *stream) {
+    if (!c || count < 0 || global_count <= 0 || (count > 0 && !samples)) return fail(NASG_ERR_INVALID, "bad argument");
+    return train_step_impl(c, samples, order, count, global_count, b, pick(c, stream));
+}
+
+int nasg_train_stats_take(nasg_ctx *c, nasg_train_stats *st) {
+    if (!c || !st) return fail(NASG_ERR_INVALID, "null argument");
+    double acc[5];
+    CUDA_TRY(cudaMemcpyAsync(acc, c->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, sizeof(acc), c->stream));
+    st->steps = (int)acc[4];
+    st->mean_loss = acc[1] > 0 ? acc[0] / acc[1] : 0.0;
+    st->dropped_samples = (uint64_t)acc[2];
+    st->skipped_updates = (uint64_t)acc[3];
+    return NASG_OK;
+}
+
+// Trainer::train_iteration (guiding.cpp:196-282).
+int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *samples, double b,
+                         nasg_train_stats *stats, void *stream) {
+    if (!c || n < 0 || (n > 0 && !samples)) return fail(NASG_ERR_INVALID, "bad argument");
+    cudaStream_t s = pick(c, stream);
+    if (s != c->stream) {  // the context's own stream carries publish; order it after s
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ev, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    if (n == 0) {  // empty buffer: no-op + publish (:198-202)
+        ++c->iterations;
+        int r = do_publish(c);
+        if (stats) *stats = nasg_train_stats{0, 0.0, 0, 0};
+        return r;
+    }
+    if (n > 0xffffffffll) return fail(NASG_ERR_INVALID, "buffer too large");
+    const int t = c->cfg.batch_size;
+    const int steps = c->cfg.step_factor * ((c->cfg.sample_capacity + t - 1) / t);  // config S (:204-206)
+    int r = ensure_order(c, (size_t)n);
+    if (r) return r;
+    Pcg32 rng(hash_combine(c->cfg.seed, 0x7261696e) + (uint64_t)c->iterations, 5);  // :216
+    uint32_t *ord = c->h_order;
+    for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
+    auto reshuffle = [&]() {  // Fisher-Yates :219-224
+        for (int64_t i = n; i > 1; --i) {
+            uint32_t j = rng.next_below((uint32_t)i);
+            std::swap(ord[i - 1], ord[j]);
+        }
+    };
+    reshuffle();
+    CUDA_TRY(cudaMemcpyAsync(c->d_order, ord, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    if (stats) CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), s));
+    int64_t cursor = 0;
+    for (int step = 0; step < steps; ++step) {
+        if (cursor >= n) {
+            CUDA_TRY(cudaStreamSynchronize(s));  // h_order is still the source of the last upload
+            reshuffle();
+            CUDA_TRY(cudaMemcpyAsync(c->d_order, ord, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            cursor = 0;
+        }
+        const int64_t count = std::min<int64_t>(t, n - cursor);
+        r = train_step_impl(c, samples, c->d_order + cursor, count, count, b, s);
+        if (r) return r;
+        cursor += count;
+    }
+    ++c->iterations;
+    if (s != c->stream) {
+        cudaEvent_t ev;
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventRecord(ev, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, ev, 0));
+        cudaEventDestroy(ev);
+    }
+    r = do_publish(c);
+    if (r) return r;
+    if (stats) return nasg_train_stats_take(c, stats);
+    return NASG_OK;
+}
+
+int nasg_get_last_grad(nasg_ctx *c, float *host_g, size_t n) {
+    if (!c || !host_g || n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "bad argument");
+    CUDA_TRY(cudaMemcpyAsync(host_g, c->grad, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return NASG_OK;
+}
+
+int64_t nasg_adam_t(nasg_ctx *c) {
+    if (!c) return -1;
+    int64_t t = 0;
+    if (cudaMemcpy(&t, c->d_adam_t, sizeof(t), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+    return t;
+}
+
+// ---- multi-GPU ------------------------------------------------------------------------
+int nasg_comm_unique_id(void *out) {
+    if (!out) return fail(NASG_ERR_INVALID, "null argument");
+    std::lock_guard<std::mutex> lk(g_nccl_mu);
+    if (!g_nccl.load()) return fail(NASG_ERR_NCCL, "libnccl.so.2 not loadable");
+    ncclUniqueId id;
+    if (g_nccl.getUniqueId(&id) != ncclSuccess) return fail(NASG_ERR_NCCL, "ncclGetUniqueId failed");
+    std::memcpy(out, &id, sizeof(id));
+    return NASG_OK;
+}
+
+int nasg_comm_init(nasg_ctx *c, const void *uid, int rank, int nranks) {
+    if (!c || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(NASG_ERR_INVALID, "bad argument");
+    if (nranks == 1) return NASG_OK;
+    {
+        std::lock_guard<std::mutex> lk(g_nccl_mu);
+        if (!g_nccl.load()) return fail(NASG_ERR_NCCL, "libnccl.so.2 not loadable");
+    }
+    ncclUniqueId id;
+    std::memcpy(&id, uid, sizeof(id));
+    CUDA_TRY(cudaSetDevice(c->device));
+    ncclResult_t e = g_nccl.commInitRank(&c->comm, nranks, id, rank);
+    if (e != ncclSuccess) return fail(NASG_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(e) : ""));
+    c->rank = rank;
+    c->nranks = nranks;
+    return NASG_OK;
+}
+
+// ---- counters / schedules ------------------------------------------------------------
+uint64_t nasg_encode_clamp_count(nasg_ctx *c) {
+    if (!c) return 0;
+    unsigned long long v = 0;
+    cudaStreamSynchronize(c->stream);
+    cudaDeviceSynchronize();
+    cudaMemcpy(&v, c->d_clamp, sizeof(v), cudaMemcpyDeviceToHost);
+    return v;
+}
+
+void nasg_reset_encode_clamp_count(nasg_ctx *c) {
+    if (c) cudaMemset(c->d_clamp, 0, sizeof(unsigned long long));
+}
+
+uint64_t nasg_kernel_launches(nasg_ctx *c) { return c ? c->launches : 0; }
+
+double nasg_blend_coefficient(int64_t i, int m, int b_steps) {  // BlendSchedule guiding.hpp:78-88
+    double b = (double)(i / m) / b_steps;
+    return b < 1.0 ? b : 1.0;
+}
+
+double nasg_stride_update(double l, uint64_t s, uint64_t cap) {  // guiding.cpp:178-182
+    double next = l * std::sqrt((double)s / (double)cap);
+    return std::max(1.0, next);
+}
+
+}  // extern "C"
+
+// ---- synthetic workloads ---------------------------------------------------------------
+static void sphere(Pcg32 &r, float *out) {
+    const double z = 1.0 - 2.0 * r.next_f24();
+    const double phi = 2.0 * 3.14159265358979323846 * r.next_f24();
+    const double rr = std::sqrt(std::max(0.0, 1.0 - z * z));
+    out[0] = (float)(rr * std::cos(phi));
+    out[1] = (float)(rr * std::sin(phi));
+    out[2] = (float)z;
+    out[3] = 0.f;
+}
+
+template <class F>
+static void parallel_for(int64_t n, F f) {
+    const int64_t per = 1 << 16;
+    int nt = (int)std::min<int64_t>((n + per - 1) / per, std::max(1u, std::thread::hardware_concurrency()));
+    if (nt <= 1) {
+        f(0, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    const int64_t step = (n + nt - 1) / nt;
+    for (int k = 0; k < nt; ++k) {
+        const int64_t a = k * step, b = std::min(n, a + step);
+        if (a < b) th.emplace_back(f, a, b);
+    }
+    for (auto &t : th) t.join();
+}
+
+extern "C" {
+
+void nasg_synth_queries(uint64_t seed, int64_t first, int64_t n, const float bmin[3], const float bmax[3], float *x,
+                        float *wo, float *nrm, float *xi) {
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) {
+            Pcg32 r(hash_combine(seed, (uint64_t)(first + i)), 0x51);
+            for (int k = 0; k < 3; ++k) x[4 * i + k] = bmin[k] + (bmax[k] - bmin[k]) * r.next_f24();
+            x[4 * i + 3] = 0.f;
+            sphere(r, wo + 4 * i);
+            sphere(r, nrm + 4 * i);
+            for (int k = 0; k < 4; ++k) xi[4 * i + k] = r.next_f24();
+        }
+    });
+}
+
+void nasg_synth_samples(uint64_t seed, int64_t first, int64_t n, const float bmin[3], const float bmax[3],
+                        nasg_train_sample *out) {
+    parallel_for(n, [&](int64_t a, int64_t b) {
+        for (int64_t i = a; i < b; ++i) {
+            Pcg32 r(hash_combine(seed, (uint64_t)(first + i)), 0x53);
+            nasg_train_sample &s = out[i];
+            float wo[4], nn[4], wi[4];
+            for (int k = 0; k < 3; ++k) s.position[k] = bmin[k] + (bmax[k] - bmin[k]) * r.next_f24();
+            sphere(r, wo);
+            sphere(r, nn);
+            sphere(r, wi);
+            for (int k = 0; k < 3; ++k) {
+                s.omega_o[k] = wo[k];
+                s.normal[k] = nn[k];
+                s.omega_i[k] = wi[k];
+            }
+            const double cosn = std::max(0.0, (double)wi[0] * nn[0] + (double)wi[1] * nn[1] + (double)wi[2] * nn[2]);
+            // fixed analytic target field mu(x)
+            double mu[3] = {std::sin(2.0 * s.position[0]) + 0.5, std::cos(3.0 * s.position[1]),
+                            1.0 + 0.5 * std::sin((double)s.position[2])};
+            const double inv = 1.0 / std::sqrt(mu[0] * mu[0] + mu[1] * mu[1] + mu[2] * mu[2]);
+            const double d = (wi[0] * mu[0] + wi[1] * mu[1] + wi[2] * mu[2]) * inv;
+            s.p_value = (float)(std::exp(20.0 * (d - 1.0)) * cosn);
+            s.q_sampling = (float)(1.0 / (4.0 * 3.14159265358979323846));
+            s.bsdf_pdf_at_wi = (float)(cosn / 3.14159265358979323846);
+            s.pad = 0.f;
+        }
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,95 @@
+// Internal declarations shared by the host API (nasg_api.cpp) and the
+// kernel translation units.  Not part of the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "nasg/nasg.h"
+
+namespace nasg {
+
+constexpr int kIn = 64;        // encoding.hpp:12
+constexpr int kHidden = 128;   // net.hpp:14
+constexpr int kBins = 19;      // encoding.hpp:11
+constexpr int kTileRows = 128; // query tile (one TMEM lane / thread per row)
+
+// fp32 packed weight image used by the SIMT kernels: W1[64][128], W2, W3,
+// W4[128][128] (columns in the packed raw order, zero-padded to 128).
+constexpr int kPackedF32 = kIn * kHidden + 3 * kHidden * kHidden;  // 57344 floats
+// transposed copies for the backward delta GEMMs: W2^T, W3^T [128][128] and
+// W4^T [128 packed cols][128] (rows >= NP are zero).
+constexpr int kPackedT32 = 3 * kHidden * kHidden;
+
+__host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHidden * kHidden + kHidden * (8 * n + 1); }
+
+struct Bounds {
+    float bmin[3];
+    double ext[3];  // bmax - bmin in double (Aabb::extent, math.hpp:70)
+};
+
+// ---- kernels: packing -------------------------------------------------------
+void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStream_t s);
+// bf16 weight image for the tcgen05 kernel (smem image, UMMA core-matrix layout)
+size_t tc_image_bytes(int n_comp);
+void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s);
+
+// ---- kernels: queries -------------------------------------------------------
+enum QueryMode { kModeSample = 0, kModePdf = 1, kModeRaw = 2 };
+
+struct QueryArgs {
+    int64_t n;
+    const float4 *x, *wo, *nrm;
+    const float4 *xi;   // sample mode
+    const float4 *dir;  // pdf mode
+    const float *bsdf_pdf;
+    float b;
+    float4 *dir_pdf;
+    float *c;
+    float *mix_pdf, *guided_pdf;
+    float *raw;  // raw mode (reference order)
+    unsigned long long *clamp_count;
+    Bounds bounds;
+};
+
+int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, int num_sms,
+               cudaStream_t s);
+int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, int num_sms,
+             cudaStream_t s);
+bool tc_supported(int n_comp);
+
+int decode_raw(int n_comp, bool sample, int64_t n, const float *raw, const float4 *xi,
+               const float4 *dir, float b, const float *bsdf_pdf, float4 *dir_pdf, float *c,
+               float *mix_pdf, float *guided_pdf, cudaStream_t s);
+
+// ---- kernels: training ------------------------------------------------------
+struct TrainScratch {
+    // per-row activations (row-major [rows][features]) for the dW GEMMs
+    float *h0, *h1, *h2, *h3;   // 64, 128, 128, 128 wide
+    float *d1, *d2, *d3, *d4;   // 128, 128, 128, 80 (canonical raw order, padded)
+    float *dw_partial;          // [splits][n_weights]
+    float *tile_loss;           // per tile loss sum (float)
+    int *tile_loss_count, *tile_dropped;
+    int64_t max_rows;
+    int max_tiles;
+    int splits;       // capacity of dw_partial
+    int last_splits;  // splits used by the last train_dw
+};
+
+int train_forward_backward(int n_comp, const float *wp, const float *wtp,
+                           const nasg_train_sample *samples, const uint32_t *order,
+                           int64_t count, int64_t global_count, float b, float loss_blend,
+                           const Bounds &bounds, TrainScratch &sc, int num_sms,
+                           unsigned long long *clamp_count, cudaStream_t s);
+int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStream_t s);
+int train_reduce(int n_comp, const TrainScratch &sc, float *grad, int *nonfinite, cudaStream_t s);
+int check_finite(const float *x, int n, int *nonfinite, cudaStream_t s);
+int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s);
+// skip decision, Adam t / bias corrections, accumulation of step stats into
+// acc[0..4] = loss_sum, loss_count, dropped, skipped, steps
+int train_finalize_step(int *nonfinite, int64_t *adam_t, float *corr, int *skip,
+                        const double *step_stats, double *acc, cudaStream_t s);
+int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, const float *corr,
+               const int *skip, float lr, float *wp, float *wtp, cudaStream_t s);
+
+}  // namespace nasg
