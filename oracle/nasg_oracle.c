@@ -156,7 +156,7 @@ static void gemm_f(const float *x, const float *w, int64_t n, int K, int N, floa
             for (int j = 0; j < N; ++j) yr[j] += a * wr[j];
         }
         if (relu)
-            for (int j = 0; j < N; ++j) yr[j] = yr[j] > 0.0f ? yr[j] : 0.0f; /* cwiseMax net.hpp:74 */
+            for (int j = 0; j < N; ++j) yr[j] = yr[j] < 0.0f ? 0.0f : yr[j]; /* cwiseMax net.hpp:74: std::max, NaN propagates */
     }
 }
 
@@ -194,6 +194,13 @@ void orc_forward(const float *w, int out_dim, int64_t n, const float *in64, floa
     fcache_free(&c);
 }
 
+/* Test knob: sum the dW reduction over batch rows in reverse order.  This is
+ * "the reference under another valid summation order" and measures how far
+ * the training trajectory moves from fp32 reassociation alone — the yardstick
+ * for the GPU's tracking tolerance (tests/test_gpu_train.py). */
+static int g_reverse_sum = 0;
+void orc_set_reverse_sum(int on) { g_reverse_sum = on; }
+
 /* backward net.hpp:95-110: dW_l = h_l^T delta; delta <- (delta W_l^T) .* [h_l > 0] */
 static void backward_cached(const float *w, int out_dim, const fcache_t *c, const float *og,
                             float *dw) {
@@ -209,7 +216,8 @@ static void backward_cached(const float *w, int out_dim, const fcache_t *c, cons
         for (int i = 0; i < K; ++i) {
             float *gr = g + (size_t)i * N;
             for (int j = 0; j < N; ++j) gr[j] = 0.0f;
-            for (int64_t b = 0; b < n; ++b) {
+            for (int64_t bb = 0; bb < n; ++bb) {
+                const int64_t b = g_reverse_sum ? n - 1 - bb : bb;
                 float a = h[b * K + i];
                 const float *dr = delta + b * N;
                 for (int j = 0; j < N; ++j) gr[j] += a * dr[j];

@@ -65,6 +65,7 @@ void orc_trainer_train(void *t, int64_t n, const float *samples, double b, doubl
 void orc_trainer_get_weights(void *t, float *w);
 void orc_trainer_set_weights(void *t, const float *w);
 
+void orc_set_reverse_sum(int on);
 int orc_save_checkpoint(const char *path, const float *w, int out_dim, int n_comp);
 int orc_load_checkpoint(const char *path, float *w, int max_floats, int *n_comp);
 

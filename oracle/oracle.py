@@ -218,6 +218,12 @@ class Oracle:
         return w[:total].copy(), n.value
 
     # ---- trainer --------------------------------------------------------------
+    def set_reverse_sum(self, on: bool):
+        """Restatement only: sum dW over batch rows in reverse (reassociation yardstick)."""
+        fn = self.lib.orc_set_reverse_sum
+        fn.argtypes, fn.restype = [C.c_int], None
+        fn(int(on))
+
     def trainer(self, **kw):
         return _Trainer(self, **kw)
 

@@ -147,10 +147,18 @@ def _ptr(t):
     return int(t)
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: torch's default stream has handle 0
+
+
 def _stream(stream):
+    """Stream handle for the C ABI; defaults to torch's current stream so that
+    results are ordered with the caller's torch work (NULL would mean the
+    context's private stream)."""
     if stream is None:
-        return None
-    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        import torch
+        stream = torch.cuda.current_stream()
+    h = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+    return h if h else _CUDA_STREAM_LEGACY
 
 
 def n_weights(n_components: int = 8) -> int:
@@ -176,7 +184,8 @@ def synth_queries(seed: int, n: int, first: int = 0, bmin=(-1, -1, -1), bmax=(1,
             arrs.append(torch.empty((n, 4), dtype=torch.float32).pin_memory().numpy())
         else:
             arrs.append(np.empty((n, 4), np.float32))
-    lib().nasg_synth_queries(seed, first, n, _f3(bmin).ctypes.data, _f3(bmax).ctypes.data,
+    lo, hi = _f3(bmin), _f3(bmax)  # keep alive across the call
+    lib().nasg_synth_queries(seed, first, n, lo.ctypes.data, hi.ctypes.data,
                              *[a.ctypes.data for a in arrs])
     return tuple(arrs)
 
@@ -184,7 +193,8 @@ def synth_queries(seed: int, n: int, first: int = 0, bmin=(-1, -1, -1), bmax=(1,
 def synth_samples(seed: int, n: int, first: int = 0, bmin=(-1, -1, -1), bmax=(1, 1, 1)):
     """Synthetic training samples (n,16) float32 (nasg_train_sample layout)."""
     out = np.empty((n, 16), np.float32)
-    lib().nasg_synth_samples(seed, first, n, _f3(bmin).ctypes.data, _f3(bmax).ctypes.data, out.ctypes.data)
+    lo, hi = _f3(bmin), _f3(bmax)
+    lib().nasg_synth_samples(seed, first, n, lo.ctypes.data, hi.ctypes.data, out.ctypes.data)
     return out
 
 
@@ -200,7 +210,8 @@ class Guide:
         cfg = _Config(self.config.n_components, self.config.sample_capacity, self.config.batch_size,
                       self.config.step_factor, self.config.learning_rate, self.config.loss_blend, self.config.seed)
         h = C.c_void_p()
-        _check(lib().nasg_create(C.byref(cfg), device, _f3(bmin).ctypes.data, _f3(bmax).ctypes.data, C.byref(h)))
+        lo, hi = _f3(bmin), _f3(bmax)
+        _check(lib().nasg_create(C.byref(cfg), device, lo.ctypes.data, hi.ctypes.data, C.byref(h)))
         self._h = h
         self.device = device
         self.n_components = self.config.n_components

@@ -11,6 +11,7 @@
 
 #include "nasg_internal.h"
 #include "nasg_math.cuh"
+#include "nasg_refmath.cuh"
 #include "simt_gemm.cuh"
 
 namespace nasg {
@@ -71,8 +72,7 @@ __device__ __forceinline__ int encode_row(const float4 x, const float4 wo, const
         }
 #pragma unroll
         for (int i = 0; i < kBins; ++i) {
-            float d = (float)(t - (i + 0.5) / kBins);
-            act[(axis * kBins + i) * kLda + r] = expf(-d * d * 180.5f);
+            act[(axis * kBins + i) * kLda + r] = ref::one_blob_bin(t, i);
         }
     }
     act[57 * kLda + r] = wo.x; act[58 * kLda + r] = wo.y; act[59 * kLda + r] = wo.z;
@@ -95,6 +95,7 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
     const float *W1 = wp, *W2 = W1 + kIn * kHidden, *W3 = W2 + kHidden * kHidden,
                 *W4 = W3 + kHidden * kHidden;
     if (tid == 0) s_clamped = 0;
+    __syncthreads();
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t row0 = tile * kTileRows;
         if (tid < kTileRows) {
@@ -118,11 +119,11 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
                 auto raw = [&](int j) { return col[j * kLda]; };
                 if (MODE == kModeSample) {
                     float c;
-                    a.dir_pdf[q] = guide_sample<N, true>(raw, a.xi[q], c);
+                    a.dir_pdf[q] = ref::guide_sample<N>(raw, a.xi[q], c);
                     if (a.c) a.c[q] = c;
                 } else if (MODE == kModePdf) {
                     float4 d = a.dir[q];
-                    float2 p = guide_pdf<N, true>(raw, make_float3(d.x, d.y, d.z), a.b,
+                    float2 p = ref::guide_pdf<N>(raw, make_float3(d.x, d.y, d.z), a.b,
                                                   a.bsdf_pdf ? a.bsdf_pdf[q] : 0.f);
                     if (a.mix_pdf) a.mix_pdf[q] = p.x;
                     if (a.guided_pdf) a.guided_pdf[q] = p.y;
@@ -186,11 +187,11 @@ __global__ void decode_raw_kernel(int64_t n, const float *__restrict__ raw, cons
     };
     if (SAMPLE) {
         float cc;
-        dir_pdf[q] = guide_sample<N, true>(rawf, xi[q], cc);
+        dir_pdf[q] = ref::guide_sample<N>(rawf, xi[q], cc);
         if (c) c[q] = cc;
     } else {
         float4 d = dir[q];
-        float2 p = guide_pdf<N, true>(rawf, make_float3(d.x, d.y, d.z), b, bsdf_pdf ? bsdf_pdf[q] : 0.f);
+        float2 p = ref::guide_pdf<N>(rawf, make_float3(d.x, d.y, d.z), b, bsdf_pdf ? bsdf_pdf[q] : 0.f);
         if (mix_pdf) mix_pdf[q] = p.x;
         if (guided_pdf) guided_pdf[q] = p.y;
     }

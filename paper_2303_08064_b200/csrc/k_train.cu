@@ -17,6 +17,7 @@
 
 #include "nasg_internal.h"
 #include "nasg_math.cuh"
+#include "nasg_refmath.cuh"
 #include "simt_gemm.cuh"
 
 namespace nasg {
@@ -33,8 +34,8 @@ constexpr int kOffDA = kOffH3 + kHidden * kTLda;
 constexpr int kOffDB = kOffDA + kHidden * kTLda;
 constexpr int kOffW = kOffDB + kHidden * kTLda;
 constexpr int kOffRow = kOffW + 2 * kChunk * 128;          // 64 x 8 per-row sample data
-constexpr int kOffLoss = kOffRow + kTrainRows * 8;          // 64 losses
-constexpr int kFbFloats = kOffLoss + kTrainRows * 2;
+constexpr int kOffLoss = kOffRow + kTrainRows * 8;          // 64 double losses + 64 int states
+constexpr int kFbFloats = kOffLoss + kTrainRows * 3;
 constexpr size_t kFbSmem = kFbFloats * sizeof(float);
 
 // feature-major smem [F][kTLda] -> row-major global [rows][F], rows < valid
@@ -57,19 +58,22 @@ template <int N>
 __global__ void __launch_bounds__(256, 1)
 train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
                 const nasg_train_sample *__restrict__ samples, const uint32_t *__restrict__ order,
-                int64_t count, float gscale, float b, float e, Bounds bd, TrainScratch sc,
+                int64_t count, double gscale, double b, double e, Bounds bd, TrainScratch sc,
                 unsigned long long *clamp_count) {
     constexpr int H = packed_header(N), NP = packed_width(N), D = 8 * N + 1;
     extern __shared__ __align__(16) float sm[];
     float *h0 = sm + kOffH0, *h1 = sm + kOffH1, *h2 = sm + kOffH2, *h3 = sm + kOffH3;
     float *da = sm + kOffDA, *db = sm + kOffDB, *wbuf = sm + kOffW;
-    float *rowd = sm + kOffRow, *rloss = sm + kOffLoss;
+    float *rowd = sm + kOffRow;
+    double *rloss = reinterpret_cast<double *>(sm + kOffLoss);
+    int *rstate = reinterpret_cast<int *>(sm + kOffLoss + 2 * kTrainRows);
     __shared__ int s_clamped;
     const int tid = threadIdx.x;
     const float *W1 = wp, *W2 = W1 + kIn * kHidden, *W3 = W2 + kHidden * kHidden, *W4 = W3 + kHidden * kHidden;
     const float *T2 = wtp, *T3 = T2 + kHidden * kHidden, *T4 = T3 + kHidden * kHidden;
     const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
     if (tid == 0) s_clamped = 0;
+    __syncthreads();
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t row0 = (int64_t)tile * kTrainRows;
         const int valid = (int)min((int64_t)kTrainRows, count - row0);
@@ -88,8 +92,7 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
                     if (t < 0.0 || t > 1.0) { ++cl; t = fmin(fmax(t, 0.0), 1.0); }
 #pragma unroll
                     for (int i = 0; i < kBins; ++i) {
-                        float d = (float)(t - (i + 0.5) / kBins);
-                        h0[(axis * kBins + i) * kTLda + tid] = expf(-d * d * 180.5f);
+                        h0[(axis * kBins + i) * kTLda + tid] = ref::one_blob_bin(t, i);
                     }
                 }
                 h0[57 * kTLda + tid] = o.x; h0[58 * kTLda + tid] = o.y; h0[59 * kTLda + tid] = o.z;
@@ -115,7 +118,7 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
         // ---- K5: KL gradient epilogue, one thread per row (guiding.cpp:250-270)
         if (tid < kTrainRows) {
             float *col = da + tid;
-            float loss = 0.f;
+            double loss = 0.0;
             int state = 0;  // 0 invalid row, 1 ok, 2 dropped
             if (tid < valid) {
                 bool finite = true;
@@ -130,15 +133,15 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
                     s.p = rd[3]; s.q_s = rd[4]; s.pbsdf = rd[5];
                     auto raw = [&](int j) { return col[j * kTLda]; };
                     auto put = [&](int j, float g) { col[j * kTLda] = g; };
-                    bool ok = kl_grad_row<N, true>(raw, s, b, e, gscale, put, loss);
+                    bool ok = ref::kl_grad_row<N>(raw, s, b, e, gscale, put, loss);
                     state = ok ? 1 : 2;
                     for (int j = NP; j < kHidden; ++j) col[j * kTLda] = 0.f;
                 }
             } else {
                 for (int j = 0; j < kHidden; ++j) col[j * kTLda] = 0.f;
             }
-            rloss[tid] = (state == 1 && isfinite(loss)) ? loss : 0.f;
-            rloss[kTrainRows + tid] = __int_as_float(state == 1 && isfinite(loss) ? 1 : (state == 2 ? 2 : 0));
+            rloss[tid] = (state == 1 && isfinite(loss)) ? loss : 0.0;
+            rstate[tid] = state == 1 && isfinite(loss) ? 1 : (state == 2 ? 2 : 0);
             // delta4 in reference raw order, padded to 80 floats per row
             float *g4 = sc.d4 + (row0 + tid) * 80;
             if (tid < valid) {
@@ -150,10 +153,10 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
         }
         __syncthreads();
         if (tid == 0) {  // tile statistics in row order (deterministic)
-            float ls = 0.f;
+            double ls = 0.0;
             int lc = 0, dr = 0;
             for (int r = 0; r < kTrainRows; ++r) {
-                int st = __float_as_int(rloss[kTrainRows + r]);
+                int st = rstate[r];
                 ls += rloss[r];
                 lc += st == 1;
                 dr += st == 2;
@@ -175,13 +178,13 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
 }
 
 int train_forward_backward(int n_comp, const float *wp, const float *wtp, const nasg_train_sample *samples,
-                           const uint32_t *order, int64_t count, int64_t global_count, float b, float loss_blend,
+                           const uint32_t *order, int64_t count, int64_t global_count, double b, double loss_blend,
                            const Bounds &bounds, TrainScratch &sc, int num_sms, unsigned long long *clamp_count,
                            cudaStream_t s) {
     const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
     if (ntiles == 0) return 0;
     const int grid = ntiles < num_sms ? ntiles : num_sms;
-    const float gscale = (float)(1.0 / (double)global_count);
+    const double gscale = 1.0 / (double)global_count;  // guiding.cpp:262
     if (n_comp != 8 && n_comp != 4) return -1;
     auto k = n_comp == 8 ? train_fb_kernel<8> : train_fb_kernel<4>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
@@ -300,12 +303,12 @@ int train_reduce(int n_comp, const TrainScratch &sc, float *grad, int *nonfinite
 }
 
 // step_stats[0..2] = loss_sum, loss_count, dropped of this step (tile order)
-__global__ void step_stats_kernel(const float *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
+__global__ void step_stats_kernel(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
                                   double *step_stats) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     double ls = 0.0, lc = 0.0, dr = 0.0;
     for (int t = 0; t < ntiles; ++t) {
-        ls += (double)tile_loss[t];
+        ls += tile_loss[t];
         lc += tile_lc[t];
         dr += tile_dr[t];
     }

@@ -141,6 +141,7 @@ struct nasg_ctx {
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
     uint64_t launches = 0;
+    cudaEvent_t pub_ev = nullptr;  // recorded on `stream` after every publish
 };
 
 namespace {
@@ -160,7 +161,7 @@ int ensure_scratch(nasg_ctx *c, int64_t count) {
     if (s.tile_loss) cudaFree(s.tile_loss);
     if (s.tile_loss_count) cudaFree(s.tile_loss_count);
     if (s.tile_dropped) cudaFree(s.tile_dropped);
-    CUDA_TRY(cudaMalloc(&s.tile_loss, tiles * sizeof(float)));
+    CUDA_TRY(cudaMalloc(&s.tile_loss, tiles * sizeof(double)));
     CUDA_TRY(cudaMalloc(&s.tile_loss_count, tiles * sizeof(int)));
     CUDA_TRY(cudaMalloc(&s.tile_dropped, tiles * sizeof(int)));
     if (!s.dw_partial) {
@@ -191,6 +192,7 @@ int do_publish(nasg_ctx *c) {
         c->launches++;
     }
     CHECK_LAUNCH();
+    CUDA_TRY(cudaEventRecord(c->pub_ev, c->stream));
     return NASG_OK;
 }
 
@@ -213,6 +215,7 @@ QueryArgs base_args(nasg_ctx *c, int64_t n) {
 
 int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
     if (a.n == 0) return NASG_OK;
+    if (s != c->stream) CUDA_TRY(cudaStreamWaitEvent(s, c->pub_ev, 0));  // read a complete snapshot
     int r;
     if (c->precision == NASG_MLP_BF16) {
         if (!c->tc_pub) return fail(NASG_ERR_UNSUPPORTED, "bf16 tensor-core path not available for this N");
@@ -233,8 +236,8 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
     int r = ensure_scratch(c, std::max<int64_t>(count, 1));
     if (r) return r;
     if (count > 0) {
-        if (train_forward_backward(c->N, c->wp, c->wtp, samples, order, count, global_count, (float)b,
-                                   (float)c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, c->d_clamp, s) < 0)
+        if (train_forward_backward(c->N, c->wp, c->wtp, samples, order, count, global_count, b,
+                                   c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, c->d_clamp, s) < 0)
             return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for training");
         train_dw(c->N, count, c->sc, c->grad, s);
         train_reduce(c->N, c->sc, c->grad, c->d_nonfinite, s);
@@ -367,7 +370,9 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream);
     std::vector<float> w(c->nw);
     init_network(cfg->seed, c->N, w.data());
-    if (cudaMemcpy(c->w, w.data(), wb, cudaMemcpyHostToDevice) != cudaSuccess)
+    if (cudaEventCreateWithFlags(&c->pub_ev, cudaEventDisableTiming) != cudaSuccess)
+        return cleanup_fail(fail(NASG_ERR_CUDA, "event create failed"));
+    if (cudaMemcpyAsync(c->w, w.data(), wb, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
         return cleanup_fail(fail(NASG_ERR_CUDA, "weight upload failed"));
     int r = repack_live(c);
     if (!r) r = do_publish(c);
@@ -393,6 +398,7 @@ int nasg_destroy(nasg_ctx *c) {
     for (auto l : c->lanes)
         if (l) cudaStreamDestroy(l);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->pub_ev) cudaEventDestroy(c->pub_ev);
     delete c;
     return NASG_OK;
 }
@@ -400,6 +406,7 @@ int nasg_destroy(nasg_ctx *c) {
 int nasg_set_weights(nasg_ctx *c, const float *host_w, size_t n) {
     if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
     if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
+    CUDA_TRY(cudaDeviceSynchronize());  // training may be in flight on a caller stream
     CUDA_TRY(cudaMemcpyAsync(c->w, host_w, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
     int r = repack_live(c);
     if (!r) r = do_publish(c);
@@ -410,6 +417,7 @@ int nasg_set_weights(nasg_ctx *c, const float *host_w, size_t n) {
 int nasg_get_weights(nasg_ctx *c, float *host_w, size_t n, int published) {
     if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
     if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
+    CUDA_TRY(cudaDeviceSynchronize());  // host-synchronous getter: order after all caller streams
     CUDA_TRY(cudaMemcpyAsync(host_w, published ? c->w_pub : c->w, n * sizeof(float), cudaMemcpyDeviceToHost,
                              c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
@@ -592,6 +600,7 @@ int nasg_train_step(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
 int nasg_train_stats_take(nasg_ctx *c, nasg_train_stats *st) {
     if (!c || !st) return fail(NASG_ERR_INVALID, "null argument");
     double acc[5];
+    CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemcpyAsync(acc, c->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, sizeof(acc), c->stream));
@@ -666,6 +675,7 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
 
 int nasg_get_last_grad(nasg_ctx *c, float *host_g, size_t n) {
     if (!c || !host_g || n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "bad argument");
+    CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemcpyAsync(host_g, c->grad, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     return NASG_OK;
@@ -674,6 +684,7 @@ int nasg_get_last_grad(nasg_ctx *c, float *host_g, size_t n) {
 int64_t nasg_adam_t(nasg_ctx *c) {
     if (!c) return -1;
     int64_t t = 0;
+    if (cudaDeviceSynchronize() != cudaSuccess) return -1;
     if (cudaMemcpy(&t, c->d_adam_t, sizeof(t), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
     return t;
 }

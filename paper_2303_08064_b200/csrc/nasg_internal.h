@@ -68,7 +68,7 @@ struct TrainScratch {
     float *h0, *h1, *h2, *h3;   // 64, 128, 128, 128 wide
     float *d1, *d2, *d3, *d4;   // 128, 128, 128, 80 (canonical raw order, padded)
     float *dw_partial;          // [splits][n_weights]
-    float *tile_loss;           // per tile loss sum (float)
+    double *tile_loss;          // per tile loss sum
     int *tile_loss_count, *tile_dropped;
     int64_t max_rows;
     int max_tiles;
@@ -78,7 +78,7 @@ struct TrainScratch {
 
 int train_forward_backward(int n_comp, const float *wp, const float *wtp,
                            const nasg_train_sample *samples, const uint32_t *order,
-                           int64_t count, int64_t global_count, float b, float loss_blend,
+                           int64_t count, int64_t global_count, double b, double loss_blend,
                            const Bounds &bounds, TrainScratch &sc, int num_sms,
                            unsigned long long *clamp_count, cudaStream_t s);
 int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStream_t s);

@@ -91,8 +91,56 @@ __device__ __forceinline__ void sigmoid_pair(float r, float &s, float &sm) {
 
 // Decode one lobe from its seven packed logits: orientation (5), lambda, a.
 // guiding.cpp:26-60 + sphdist.cpp:87-101 + sphdist.cpp:142-146.
+// Precise variant: the decode itself in double, as the reference does
+// (guiding.cpp:26-60 computes sigmoid, trig, frame, lambda and a in double
+// from the float raw outputs), so the lobe frame agrees with the oracle to
+// ~1e-16 and only the per-direction evaluation runs in fp32.
+__device__ __forceinline__ void decode_lobe_double(const float r[7], Lobe &L) {
+    double trig[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        const double s = 1.0 / (1.0 + exp(-(double)r[k]));  // sigmoid guiding.cpp:9
+        L.sig[k] = (float)s;
+        L.sigm[k] = (float)(1.0 - s);
+        trig[k] = s * 2.0 - 1.0;
+    }
+    double n1 = sqrt(trig[1] * trig[1] + trig[2] * trig[2]);
+    if (n1 < 1e-6) { trig[1] = 0.0; trig[2] = 1.0; L.pn_phi = 0.f; }
+    else { trig[1] /= n1; trig[2] /= n1; L.pn_phi = (float)n1; }
+    double n2 = sqrt(trig[3] * trig[3] + trig[4] * trig[4]);
+    if (n2 < 1e-6) { trig[3] = 0.0; trig[4] = 1.0; L.pn_tau = 0.f; }
+    else { trig[3] /= n2; trig[4] /= n2; L.pn_tau = (float)n2; }
+    const double ct = fmin(fmax(trig[0], -1.0), 1.0);
+    const double st = sqrt(fmax(0.0, 1.0 - ct * ct));
+    const double sp = trig[1], cp = trig[2], stau = trig[3], ctau = trig[4];
+    L.zd0 = cp * st; L.zd1 = sp * st; L.zd2 = ct;
+    L.xd0 = ct * cp * ctau - sp * stau;
+    L.xd1 = ct * sp * ctau + cp * stau;
+    L.xd2 = -st * ctau;
+    const double yd0 = L.zd1 * L.xd2 - L.zd2 * L.xd1, yd1 = L.zd2 * L.xd0 - L.zd0 * L.xd2,
+                 yd2 = L.zd0 * L.xd1 - L.zd1 * L.xd0;
+    L.z = make_float3((float)L.zd0, (float)L.zd1, (float)L.zd2);
+    L.x = make_float3((float)L.xd0, (float)L.xd1, (float)L.xd2);
+    L.y = make_float3((float)yd0, (float)yd1, (float)yd2);
+    L.ct = (float)ct; L.st = (float)st; L.sp = (float)sp; L.cp = (float)cp;
+    L.stau = (float)stau; L.ctau = (float)ctau;
+    const double lam = exp((double)r[5]), a = exp((double)r[6]);
+    const double lc = fmin(fmax(lam, 1e-3), 3e3), ac = fmin(a, 3e3);
+    L.lam_clamped = lc != lam;
+    L.a_clamped = ac != a;
+    L.lambda = (float)lc;
+    L.a = (float)ac;
+    const double ome = -expm1(-2.0 * lc);
+    L.one_m_emin = (float)ome;
+    L.log_k = (float)(1.8378770664093453 + log(ome) - log(lc) - 0.5 * log1p(ac));
+}
+
 template <bool Precise>
 __device__ __forceinline__ void decode_lobe(const float r[7], Lobe &L) {
+    if (Precise) {
+        decode_lobe_double(r, L);
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 5; ++k) sigmoid_pair(r[k], L.sig[k], L.sigm[k]);
     // trig = 2 sigmoid - 1 = s - (1 - s)
@@ -112,17 +160,6 @@ __device__ __forceinline__ void decode_lobe(const float r[7], Lobe &L) {
     L.z = make_float3(cp * sth, sp * sth, ct);
     L.x = make_float3(ct * cp * ctau - sp * st_, ct * sp * ctau + cp * st_, -sth * ctau);
     L.y = cross3(L.z, L.x);
-    if (Precise) {
-        // exactly unit-norm axes in double from the same (fp32) trig values
-        double cd = ct, spd = sp, cpd = cp, std_ = st_, ctd = ctau;
-        double i1 = rsqrt(spd * spd + cpd * cpd), i2 = rsqrt(std_ * std_ + ctd * ctd);
-        spd *= i1; cpd *= i1; std_ *= i2; ctd *= i2;
-        double sd = sqrt(fmax(0.0, 1.0 - cd * cd));
-        L.zd0 = cpd * sd; L.zd1 = spd * sd; L.zd2 = cd;
-        L.xd0 = cd * cpd * ctd - spd * std_;
-        L.xd1 = cd * spd * ctd + cpd * std_;
-        L.xd2 = -sd * ctd;
-    }
     // lambda = clamp(e^r, 1e-3, 3e3), a = min(e^r, 3e3)  guiding.cpp:53-59
     float lam = expf(r[5]), a = expf(r[6]);
     L.lambda = fminf(fmaxf(lam, kLambdaMinF), kLambdaMaxF);

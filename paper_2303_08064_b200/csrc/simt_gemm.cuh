@@ -89,12 +89,13 @@ __device__ __forceinline__ void tile_layer(const float *in, float *out,
 #pragma unroll
         for (int h = 0; h < RM / 4; ++h) {
             float4 v = make_float4(acc[4 * h][j], acc[4 * h + 1][j], acc[4 * h + 2][j], acc[4 * h + 3][j]);
-            if (EPI == kEpiRelu) {
-                v.x = fmaxf(v.x, 0.f); v.y = fmaxf(v.y, 0.f); v.z = fmaxf(v.z, 0.f); v.w = fmaxf(v.w, 0.f);
-            } else if (EPI == kEpiMask) {
+            if (EPI == kEpiRelu) {  // std::max(x, 0) as Eigen's cwiseMax: NaN propagates
+                v.x = v.x < 0.f ? 0.f : v.x; v.y = v.y < 0.f ? 0.f : v.y;
+                v.z = v.z < 0.f ? 0.f : v.z; v.w = v.w < 0.f ? 0.f : v.w;
+            } else if (EPI == kEpiMask) {  // delta *= [h > 0] as a product (inf*0 = NaN, net.hpp:106)
                 float4 m = *reinterpret_cast<const float4 *>(mask + n * LDA + ty * 4 + 64 * h);
-                v.x = m.x > 0.f ? v.x : 0.f; v.y = m.y > 0.f ? v.y : 0.f;
-                v.z = m.z > 0.f ? v.z : 0.f; v.w = m.w > 0.f ? v.w : 0.f;
+                v.x *= m.x > 0.f ? 1.f : 0.f; v.y *= m.y > 0.f ? 1.f : 0.f;
+                v.z *= m.z > 0.f ? 1.f : 0.f; v.w *= m.w > 0.f ? 1.f : 0.f;
             }
             *reinterpret_cast<float4 *>(out + n * LDA + ty * 4 + 64 * h) = v;
         }
