@@ -1,0 +1,292 @@
+#!/usr/bin/env python
+"""Benchmark of the NASG guided-query hot path (BASELINE.json metric).
+
+One step = one guided query pass (encode -> MLP -> NASG decode -> lobe select
+-> sample -> mixture pdf) over one batch of Q synthetic queries (config 2 of
+BASELINE.json at its largest size, Q = 2^24 per GPU), inputs resident in HBM.
+Queries shard by pixel tile / query range across GPUs with no collective
+(weak scaling); value = all ranks' queries / max-over-ranks time.
+
+Also reported (same JSON line):
+  e2e          the same metric through the host-buffer API nasg_query_sample_host
+               (pinned H2D of the inputs + D2H of the results inside the timed region)
+  roofline     the fused query kernel vs the measured bf16 tensor peak
+  cpu_baseline the reference (oracle/_ref, all host cores) on a bounded sample
+  train        config 3: fused fwd+KL+bwd+Adam at 2^18 samples per step
+
+`--impl reference` times the reference's own CPU implementation (oracle/_ref:
+the unmodified reference TUs + Eigen-API shim, OpenMP over queries) instead.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "NASG guided queries/sec (fwd+sample+pdf) & train samples/sec, 1–8 B200"
+FLOP_PER_QUERY = 2 * (64 * 128 + 128 * 128 + 128 * 128 + 128 * 65)  # 98,560
+BYTES_PER_QUERY = 68  # 36 B x/wo/n + 16 B xi in + 16 B dir+pdf out (algorithmic)
+FLOP_PER_SAMPLE = 279_296  # fwd 98,560 + dW 98,560 + delta 82,176
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[2:]) if v.lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        import torch
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return ws, rank, local
+
+
+def max_over_ranks(x, ws):
+    if ws == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def cpu_reference_rate(n_total, seconds, threads=None):
+    """The reference's own query path (infer_guide + mixture_sample), OpenMP over queries."""
+    from oracle.oracle import Oracle, available
+    import paper_2303_08064_b200 as nasg
+    kind = "reference" if available("ref") else "port"
+    o = Oracle("ref" if kind == "reference" else "orc")
+    threads = threads or os.cpu_count()
+    w = o.init_network(0)
+    chunk = 1 << 14
+    x, wo, nrm, xi = nasg.synth_queries(12345, chunk)
+    q9 = np.ascontiguousarray(np.concatenate([x[:, :3], wo[:, :3], nrm[:, :3]], 1))
+    o.query_sample(w, q9[:256], xi[:256], threads=threads)  # warm-up (thread pool)
+    done, t0 = 0, time.perf_counter()
+    while done < n_total and time.perf_counter() - t0 < seconds:
+        o.query_sample(w, q9, xi, threads=threads)
+        done += chunk
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "queries/s", "cores": threads, "kind": kind,
+            "sample": f"{done} synthetic queries (infer_guide+mixture_sample per query, N=8, "
+                      f"{threads} OpenMP threads, {dt:.1f} s)"}
+
+
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return
+    cb = cpu_reference_rate(args.queries * args.steps, args.cpu_seconds)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "queries/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "config 2: guided query fwd+sample+pdf, N=8, host CPU reference",
+                       "queries_per_step": args.queries},
+            "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "queries/s",
+                                        "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def time_events(fn, k, stream):
+    import torch
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
+    ev[0].record(stream)
+    for i in range(k):
+        fn()
+        ev[i + 1].record(stream)
+    ev[-1].synchronize()
+    return [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(k)]
+
+
+def bench_train(g_cls, nasg, args, ws, rank):
+    """Config 3: S = t = 2^18 samples per Adam step (one step per train_iteration)."""
+    import torch
+    n = args.train_samples
+    g = g_cls(nasg.TrainerConfig(seed=3, sample_capacity=n, batch_size=n))
+    s = torch.from_numpy(nasg.synth_samples(11 + rank, n, first=rank * n)).cuda()
+    stream = torch.cuda.current_stream()
+    for i in range(2):
+        g.train_iteration(s, 1.0, stats=False)
+    torch.cuda.synchronize()
+    barrier(ws)
+    times = time_events(lambda: g.train_iteration(s, 1.0, stats=False), args.train_steps, stream)
+    t = max_over_ranks(sum(times), ws)
+    st = g.train_iteration(s, 1.0)
+    g.close()
+    rate = n * ws * args.train_steps / t
+    return {"metric": "train samples/s (config 3: 2^18 samples/step, fused fwd+KL+bwd+Adam, fp32)",
+            "value": rate, "unit": "samples/s", "ms_per_step": 1e3 * t / args.train_steps,
+            "achieved_tflops": rate / ws * FLOP_PER_SAMPLE / 1e12, "dtype": "fp32",
+            "last_mean_loss": st.mean_loss}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--queries", type=int, default=1 << 24)
+    ap.add_argument("--train-samples", type=int, default=1 << 18)
+    ap.add_argument("--train-steps", type=int, default=5)
+    ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    ws, rank, local = dist_init()
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+        return
+
+    import torch
+    import paper_2303_08064_b200 as nasg
+    torch.cuda.set_device(local)
+    n = args.queries
+    g = nasg.Guide(nasg.TrainerConfig(seed=0), device=local)
+    prec = nasg.NASG_MLP_BF16 if args.precision == "bf16" else nasg.NASG_MLP_FP32
+    try:
+        g.precision = prec
+    except nasg.NasgError:
+        prec = nasg.NASG_MLP_FP32
+        g.precision = prec
+    dtype = "bf16" if prec == nasg.NASG_MLP_BF16 else "fp32"
+    # this rank's pixel-tile shard of the synthetic queries (weak scaling)
+    host = nasg.synth_queries(2024, n, first=rank * n, pinned=True)
+    dev = [torch.from_numpy(a).cuda() for a in host]
+    out = torch.empty((n, 4), dtype=torch.float32, device="cuda")
+    cbuf = torch.empty(n, dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        g.query_sample(*dev, dir_pdf=out, c=cbuf)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier(ws)
+    l0 = g.kernel_launches
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        times = time_events(step, args.steps, stream)
+        torch.cuda.synchronize()
+    launches = g.kernel_launches - l0
+    barrier(ws)
+    t_local = sum(times)
+    t = max_over_ranks(t_local, ws)
+    value = n * ws * args.steps / t
+    per_launch = t_local / args.steps  # one fused kernel per step
+    pk, pk_kind = peaks()
+    achieved = n * FLOP_PER_QUERY / per_launch / 1e12
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get(dtype)
+    roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
+            "frac": achieved / pk["bf16_tflops"], "traffic": traffic,
+            "peak_kind": f"{pk_kind} bf16 burst", "frac_sustained": achieved / pk.get("bf16_tflops_sustained", 1400.0),
+            "hbm_frac": n * BYTES_PER_QUERY / per_launch / 1e9 / pk["hbm_gbs"],
+            "kernel": f"query_{'tc' if dtype == 'bf16' else 'fp32'}_kernel<8,sample>"}
+
+    # ---- e2e through the host-buffer public API (pinned in, pinned out) ----
+    hout = torch.empty((n, 4), dtype=torch.float32).pin_memory().numpy()
+    hc = torch.empty(n, dtype=torch.float32).pin_memory().numpy()
+    for _ in range(2):
+        g.query_sample_host(*host, dir_pdf=hout, c=hc)
+    barrier(ws)
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        g.query_sample_host(*host, dir_pdf=hout, c=hc)
+    te = max_over_ranks(time.perf_counter() - t0, ws)
+    e2e = {"value": n * ws * e2e_steps / te, "unit": "queries/s", "h2d_bytes_per_step": n * 64 * ws,
+           "d2h_bytes_per_step": n * 20 * ws, "api": "nasg_query_sample_host (pinned host buffers)"}
+    g.close()
+    del dev, out, cbuf
+    torch.cuda.empty_cache()
+
+    train = None if args.no_train else bench_train(nasg.Guide, nasg, args, ws, rank)
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        cpu = cpu_reference_rate(1 << 30, args.cpu_seconds)
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+                "config": {"workload": f"config 2: {n} guided queries/step/GPU (fwd+sample+pdf), N=8 lobes, "
+                                       f"64-128-128-128-65 MLP", "queries_per_step_per_gpu": n,
+                           "l2": "inputs (1 GiB/GPU) exceed the 126 MB L2", "parallelism": f"query shards x{ws}"},
+                "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
+                "clocks": clk.summary(), "train": train}
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

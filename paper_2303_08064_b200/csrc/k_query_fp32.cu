@@ -170,7 +170,7 @@ int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, 
 }
 
 // ------------------------------------------------------ raw-output parity --
-template <int N, bool SAMPLE>
+template <int N, bool SAMPLE, bool FAST>
 __global__ void decode_raw_kernel(int64_t n, const float *__restrict__ raw, const float4 *xi,
                                   const float4 *dir, float b, const float *bsdf_pdf, float4 *dir_pdf,
                                   float *c, float *mix_pdf, float *guided_pdf) {
@@ -187,38 +187,48 @@ __global__ void decode_raw_kernel(int64_t n, const float *__restrict__ raw, cons
     };
     if (SAMPLE) {
         float cc;
-        dir_pdf[q] = ref::guide_sample<N>(rawf, xi[q], cc);
+        dir_pdf[q] = FAST ? guide_sample<N>(rawf, xi[q], cc) : ref::guide_sample<N>(rawf, xi[q], cc);
         if (c) c[q] = cc;
     } else {
-        float4 d = dir[q];
-        float2 p = ref::guide_pdf<N>(rawf, make_float3(d.x, d.y, d.z), b, bsdf_pdf ? bsdf_pdf[q] : 0.f);
+        const float4 d = dir[q];
+        const float3 v = make_float3(d.x, d.y, d.z);
+        const float bp = bsdf_pdf ? bsdf_pdf[q] : 0.f;
+        const float2 p = FAST ? guide_pdf<N>(rawf, v, b, bp) : ref::guide_pdf<N>(rawf, v, b, bp);
         if (mix_pdf) mix_pdf[q] = p.x;
         if (guided_pdf) guided_pdf[q] = p.y;
     }
 }
 
-template <int N>
-static int decode_raw_n(bool sample, int64_t n, const float *raw, const float4 *xi, const float4 *dir,
-                        float b, const float *bsdf_pdf, float4 *dir_pdf, float *c, float *mix_pdf,
-                        float *guided_pdf, cudaStream_t s) {
+template <int N, bool FAST>
+static int decode_raw_n(bool sample, int64_t n, const float *raw, const float4 *xi, const float4 *dir, float b,
+                        const float *bsdf_pdf, float4 *dir_pdf, float *c, float *mix_pdf, float *guided_pdf,
+                        cudaStream_t s) {
     const int blocks = (int)((n + 127) / 128);
     if (blocks == 0) return 0;
     if (sample)
-        decode_raw_kernel<N, true><<<blocks, 128, 0, s>>>(n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf);
+        decode_raw_kernel<N, true, FAST><<<blocks, 128, 0, s>>>(n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf,
+                                                                guided_pdf);
     else
-        decode_raw_kernel<N, false><<<blocks, 128, 0, s>>>(n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf);
+        decode_raw_kernel<N, false, FAST><<<blocks, 128, 0, s>>>(n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf,
+                                                                 guided_pdf);
     return 1;
 }
 
-int decode_raw(int n_comp, bool sample, int64_t n, const float *raw, const float4 *xi, const float4 *dir,
+// fast = true: the fp32 epilogue of the bf16 tensor-core path (nasg_math.cuh);
+// false: the double restatement used by the fp32 path (nasg_refmath.cuh).
+int decode_raw(int n_comp, bool sample, bool fast, int64_t n, const float *raw, const float4 *xi, const float4 *dir,
                float b, const float *bsdf_pdf, float4 *dir_pdf, float *c, float *mix_pdf, float *guided_pdf,
                cudaStream_t s) {
+#define NASG_DR(NN)                                                                                         \
+    return fast ? decode_raw_n<NN, true>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s) \
+                : decode_raw_n<NN, false>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s)
     switch (n_comp) {
-        case 4: return decode_raw_n<4>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s);
-        case 8: return decode_raw_n<8>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s);
-        case 16: return decode_raw_n<16>(sample, n, raw, xi, dir, b, bsdf_pdf, dir_pdf, c, mix_pdf, guided_pdf, s);
+        case 4: NASG_DR(4);
+        case 8: NASG_DR(8);
+        case 16: NASG_DR(16);
         default: return -1;
     }
+#undef NASG_DR
 }
 
 }  // namespace nasg

@@ -526,7 +526,7 @@ int nasg_decode_sample_raw(nasg_ctx *c, int64_t n, const float *raw, const float
                            void *stream) {
     if (!c || n < 0 || (n > 0 && (!raw || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
     if (n == 0) return NASG_OK;
-    if (decode_raw(c->N, true, n, raw, (const float4 *)xi, nullptr, 0.f, nullptr, (float4 *)dir_pdf, cc, nullptr,
+    if (decode_raw(c->N, true, c->precision == NASG_MLP_BF16, n, raw, (const float4 *)xi, nullptr, 0.f, nullptr, (float4 *)dir_pdf, cc, nullptr,
                    nullptr, pick(c, stream)) < 0)
         return fail(NASG_ERR_UNSUPPORTED, "n_components");
     c->launches++;
@@ -538,7 +538,7 @@ int nasg_decode_pdf_raw(nasg_ctx *c, int64_t n, const float *raw, const float *d
                         float *mix_pdf, float *guided_pdf, void *stream) {
     if (!c || n < 0 || (n > 0 && (!raw || !dir))) return fail(NASG_ERR_INVALID, "bad argument");
     if (n == 0) return NASG_OK;
-    if (decode_raw(c->N, false, n, raw, nullptr, (const float4 *)dir, b, bsdf_pdf, nullptr, nullptr, mix_pdf,
+    if (decode_raw(c->N, false, c->precision == NASG_MLP_BF16, n, raw, nullptr, (const float4 *)dir, b, bsdf_pdf, nullptr, nullptr, mix_pdf,
                    guided_pdf, pick(c, stream)) < 0)
         return fail(NASG_ERR_UNSUPPORTED, "n_components");
     c->launches++;

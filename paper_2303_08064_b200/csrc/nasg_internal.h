@@ -58,7 +58,7 @@ int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, in
              cudaStream_t s);
 bool tc_supported(int n_comp);
 
-int decode_raw(int n_comp, bool sample, int64_t n, const float *raw, const float4 *xi,
+int decode_raw(int n_comp, bool sample, bool fast, int64_t n, const float *raw, const float4 *xi,
                const float4 *dir, float b, const float *bsdf_pdf, float4 *dir_pdf, float *c,
                float *mix_pdf, float *guided_pdf, cudaStream_t s);
 

@@ -24,14 +24,6 @@ namespace ref {
 constexpr double kPi = 3.14159265358979323846;
 constexpr double kTwoPi = 2.0 * kPi;
 
-template <int I, int N, class F>
-__device__ __forceinline__ void static_for(F &&f) {
-    if constexpr (I < N) {
-        f(std::integral_constant<int, I>{});
-        static_for<I + 1, N>(f);
-    }
-}
-
 // one_blob bin i of a normalised coordinate t (encoding.cpp:11-19): the
 // Gaussian bump in double, rounded to float — identical to the reference's
 // encoding up to CUDA-vs-glibc exp ulps.
