@@ -247,8 +247,9 @@ def main():
     achieved = n * FLOP_PER_QUERY / per_launch / 1e12
     traffic = None
     tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tp):
-        traffic = json.load(open(tp)).get(dtype)
+    if os.path.exists(tp):  # dram read+write of the same kernel from the committed ncu --set full capture
+        tr = json.load(open(tp)).get(dtype)
+        traffic = tr["bytes_per_query"] * n if tr else None
     roof = {"bound": "tensor", "achieved": achieved, "peak": pk["bf16_tflops"], "unit": "TFLOP/s",
             "frac": achieved / pk["bf16_tflops"], "traffic": traffic,
             "peak_kind": f"{pk_kind} bf16 burst", "frac_sustained": achieved / pk.get("bf16_tflops_sustained", 1400.0),

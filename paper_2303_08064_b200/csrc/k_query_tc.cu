@@ -9,15 +9,15 @@
 //               layers 1-3: TMEM -> regs -> ReLU -> bf16 -> A tile (next
 //               layer's operand); layer 4: TMEM -> 80 raw outputs in
 //               registers -> decode / sample / pdf (nasg_math.cuh).
-//   warp 12     TMEM allocator + a single elected thread that TMA-bulk-copies
-//               the 100 KB bf16 weight image into smem once and issues every
-//               tcgen05.mma, round-robin over the three warpgroups, so the
-//               tensor core runs one group's layer while the others run their
-//               epilogues.
-// Handshakes are mbarriers: a_full[g] (4 warp arrivals: A operand written and
-// fenced to the async proxy) and acc_full[g] (tcgen05.commit: accumulator
-// ready).  Only the 64 B/query of inputs and 16-20 B/query of outputs touch
-// HBM; weights are read from HBM/L2 once per CTA.
+//               After writing an A tile the group syncs on its named barrier
+//               and its thread 0 issues that layer's tcgen05.mma chain
+//               (K/16 UMMAs) and tcgen05.commit -> acc_full[g].  The groups
+//               run independently, drift out of phase, and the tensor core
+//               interleaves one group's layers with the others' epilogues;
+//               a tile's NASG epilogue overlaps the next tile's layer 1.
+//   warp 12     TMEM allocator (512 columns) + one thread that TMA-bulk-copies
+//               the 100 KB bf16 weight image into smem once per CTA.
+// Only the 64 B/query of inputs and 16-20 B/query of outputs touch HBM.
 #include <cuda_bf16.h>
 
 #include "nasg_internal.h"
@@ -29,7 +29,7 @@ namespace nasg {
 namespace {
 
 constexpr int kWG = 3;                          // epilogue warpgroups
-constexpr int kMmaWarp = kWG * 4;               // warp index of the MMA / TMEM warp
+constexpr int kAuxWarp = kWG * 4;               // TMEM allocation + weight TMA warp
 constexpr int kThreads = kWG * 128 + 32;        // 416
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one bf16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;
@@ -44,7 +44,7 @@ __host__ __device__ constexpr uint32_t img_bytes(int n) { return 81920u + (uint3
 __host__ __device__ constexpr uint32_t align1k(uint32_t x) { return (x + 1023u) & ~1023u; }
 template <int N>
 constexpr size_t smem_bytes() {
-    return align1k(img_bytes(N)) + kWG * kABytes + (2 * kWG + 2) * sizeof(uint64_t);
+    return align1k(img_bytes(N)) + kWG * kABytes + (kWG + 2) * sizeof(uint64_t);
 }
 
 }  // namespace
@@ -129,12 +129,8 @@ __device__ __forceinline__ int encode_tile_row(const QueryArgs &a, int64_t q, co
     return clamped;
 }
 
-// A operand written by this warp -> visible to the tensor core; then arrive.
-__device__ __forceinline__ void publish_a(uint64_t *bar, int lane) {
-    tc::fence_proxy_async_smem();
-    __syncwarp();
-    if (lane == 0) tc::mbar_arrive(bar);
-}
+// named barrier over the 128 threads of epilogue warpgroup g (id 0 is __syncthreads)
+__device__ __forceinline__ void wg_sync(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
 
 // ------------------------------------------------------------------ kernel --
 template <int N, int MODE>
@@ -144,61 +140,31 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     constexpr uint32_t IMG = img_bytes(N);
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t *a_full = reinterpret_cast<uint64_t *>(smem + A_OFF + kWG * kABytes);
-    uint64_t *acc_full = a_full + kWG;
+    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + A_OFF + kWG * kABytes);
     uint64_t *w_bar = acc_full + kWG;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     __shared__ int s_clamped;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
     const int64_t ntiles = (a.n + 127) / 128;
 
     if (threadIdx.x == 0) {
-        for (int g = 0; g < kWG; ++g) {
-            tc::mbar_init(&a_full[g], 4);
-            tc::mbar_init(&acc_full[g], 1);
-        }
+        for (int g = 0; g < kWG; ++g) tc::mbar_init(&acc_full[g], 1);
         tc::mbar_init(w_bar, 1);
         s_clamped = 0;
         tc::fence_mbar_init();
     }
-    if (warp == kMmaWarp) tc::tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == kAuxWarp) tc::tmem_alloc(tmem_slot, kTmemCols);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == kMmaWarp) {
-        if (lane == 0) {
-            // weights: TMA bulk copies global -> smem, once per CTA
+    if (warp == kAuxWarp) {
+        if ((threadIdx.x & 31) == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
             tc::mbar_arrive_expect_tx(w_bar, IMG);
             for (uint32_t off = 0; off < IMG; off += 16384)
                 tc::bulk_g2s(smem + off, img + off, (IMG - off) < 16384u ? (IMG - off) : 16384u, w_bar);
-            tc::mbar_wait(w_bar, 0);
-            const uint32_t sW = tc::smem_u32(smem), sA = tc::smem_u32(smem + A_OFF);
-            uint32_t aph[kWG];
-#pragma unroll
-            for (int g = 0; g < kWG; ++g) aph[g] = 0;
-            for (int64_t st = blockIdx.x; st * kWG < ntiles; st += gridDim.x) {
-#pragma unroll 1
-                for (int l = 0; l < 4; ++l) {
-                    const int K = l == 0 ? kIn : kHidden;
-                    const uint32_t sbo = (uint32_t)K * 16u;
-                    const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
-#pragma unroll
-                    for (int g = 0; g < kWG; ++g) {
-                        if (st * kWG + g >= ntiles) continue;
-                        tc::mbar_wait(&a_full[g], aph[g]);
-                        aph[g] ^= 1u;
-                        tc::tc_fence_after();
-                        const uint32_t a0 = sA + g * kABytes, b0 = sW + w_off(l), d = tmem + g * 128;
-                        for (int k = 0; k < K / 16; ++k)
-                            tc::mma_bf16(d, tc::smem_desc(a0 + k * 256, 128, sbo), tc::smem_desc(b0 + k * 256, 128, sbo),
-                                         idesc, k > 0 ? 1u : 0u);
-                        tc::mma_commit(&acc_full[g]);
-                    }
-                }
-            }
         }
         __syncwarp();
     } else {
@@ -207,6 +173,29 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + g * kABytes);
         const uint32_t a_row64 = a_base + (t >> 3) * 1024 + (t & 7) * 16;   // K = 64 layout
         const uint32_t a_row128 = a_base + (t >> 3) * 2048 + (t & 7) * 16;  // K = 128 layout
+        const uint32_t sW = tc::smem_u32(smem);
+        // The group's A tile is complete in smem (and its TMEM reads are done):
+        // make it visible to the tensor core, then thread 0 of the group issues
+        // the layer's UMMAs and commits them to acc_full[g].  Each group drives
+        // its own chain, so the three groups drift out of phase and the
+        // tensor core interleaves their layers with the others' epilogues.
+        auto issue = [&](int l) {
+            tc::fence_proxy_async_smem();
+            tc::tc_fence_before();
+            wg_sync(g);
+            if (t == 0) {
+                tc::mbar_wait(w_bar, 0);
+                tc::tc_fence_after();
+                const int K = l == 0 ? kIn : kHidden;
+                const uint32_t sbo = (uint32_t)K * 16u;
+                const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
+                const uint32_t b0 = sW + w_off(l), d = tmem + g * 128;
+                for (int k = 0; k < K / 16; ++k)
+                    tc::mma_bf16(d, tc::smem_desc(a_base + k * 256, 128, sbo), tc::smem_desc(b0 + k * 256, 128, sbo),
+                                 idesc, k > 0 ? 1u : 0u);
+                tc::mma_commit(&acc_full[g]);
+            }
+        };
         float inv_ext[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) inv_ext[k] = a.bounds.ext[k] > 0.0 ? (float)(1.0 / a.bounds.ext[k]) : 0.f;
@@ -216,11 +205,11 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         const int64_t stride = (int64_t)gridDim.x * kWG;
         if (tile < ntiles) {
             clamped += encode_tile_row(a, tile * 128 + t, inv_ext, a_row64);
-            publish_a(&a_full[g], lane);
+            issue(0);
         }
         while (tile < ntiles) {
 #pragma unroll 1
-            for (int l = 0; l < 3; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
+            for (int l = 1; l < 4; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
                 tc::mbar_wait(&acc_full[g], acc_ph);
                 acc_ph ^= 1u;
                 tc::tc_fence_after();
@@ -233,18 +222,15 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     for (int c = 0; c < 4; ++c) {
                         uint32_t p[4];
 #pragma unroll
-                        for (int h = 0; h < 4; ++h) {
-                            const float lo = v[8 * c + 2 * h], hi = v[8 * c + 2 * h + 1];
-                            p[h] = tc::pack_bf16x2(lo < 0.f ? 0.f : lo, hi < 0.f ? 0.f : hi);
-                        }
+                        for (int h = 0; h < 4; ++h) p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
                         tc::st_shared_v4(a_row128 + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
                     }
                 }
-                tc::tc_fence_before();
-                publish_a(&a_full[g], lane);
+                issue(l);
             }
             // output layer ready: encode the next tile into the (now free) A tile,
-            // then drain the raw outputs and hand the group back to the MMA warp
+            // drain the raw outputs, start the next tile, then run the NASG
+            // epilogue of this tile while the tensor core works on the next
             tc::mbar_wait(&acc_full[g], acc_ph);
             acc_ph ^= 1u;
             tc::tc_fence_after();
@@ -268,8 +254,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     for (int i = 0; i < 16; ++i) raw[(NP / 32) * 32 + i] = u[i];
                 }
             }
-            tc::tc_fence_before();
-            if (next < ntiles) publish_a(&a_full[g], lane);
+            if (next < ntiles) issue(0);
             const int64_t q = tile * 128 + t;
             if (q < a.n) {
                 auto rawf = [&](int j) { return raw[j]; };
@@ -294,7 +279,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == kMmaWarp) {
+    if (warp == kAuxWarp) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem, kTmemCols);
     }

@@ -80,10 +80,42 @@ struct Lobe {
 
 __device__ __forceinline__ float dot3(float3 a, float3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
 
+// ---- fast primitives (MUFU + short polynomials), accurate where the NASG
+// formulas need relative accuracy ------------------------------------------------
+__device__ __forceinline__ float rcp_fast(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float sqrt_fast(float x) {
+    float r;
+    asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+// log1p(x), x > -1: 2 atanh(x / (2 + x)) series for |x| < 1/4 (relative error
+// < 1e-7), log(1 + x) from MUFU.LG2 otherwise (|log| > 0.22 there).
+__device__ __forceinline__ float log1p_fast(float x) {
+    const float sx = x * rcp_fast(2.f + x), s2 = sx * sx;
+    const float ser = 2.f * sx * fmaf(s2, fmaf(s2, fmaf(s2, fmaf(s2, 1.f / 9.f, 1.f / 7.f), 1.f / 5.f), 1.f / 3.f), 1.f);
+    return fabsf(x) < 0.25f ? ser : __logf(1.f + x);
+}
+// expm1(y): degree-8 Taylor polynomial for |y| < 1/2 (relative error < 1e-8),
+// exp(y) - 1 from MUFU.EX2 otherwise (|result| > 0.39 there).
+__device__ __forceinline__ float expm1_fast(float y) {
+    float p = fmaf(y, 1.f / 40320.f, 1.f / 5040.f);
+    p = fmaf(p, y, 1.f / 720.f);
+    p = fmaf(p, y, 1.f / 120.f);
+    p = fmaf(p, y, 1.f / 24.f);
+    p = fmaf(p, y, 1.f / 6.f);
+    p = fmaf(p, y, 0.5f);
+    p = fmaf(p, y, 1.f);
+    return fabsf(y) < 0.5f ? p * y : __expf(y) - 1.f;
+}
+
 // s = 1/(1+e^-r) and 1 - s, both without cancellation.
 __device__ __forceinline__ void sigmoid_pair(float r, float &s, float &sm) {
     const float e = __expf(-fabsf(r));
-    const float big = __frcp_rn(1.f + e), small = e * big;
+    const float big = rcp_fast(1.f + e), small = e * big;
     s = r >= 0.f ? big : small;
     sm = r >= 0.f ? small : big;
 }
@@ -96,27 +128,30 @@ __device__ __forceinline__ void decode_lobe(const float r[7], Lobe &L) {
     const float ct = s[0] - sm[0];  // 2 sigmoid - 1
     float sp = s[1] - sm[1], cp = s[2] - sm[2], st = s[3] - sm[3], ctau = s[4] - sm[4];
     const float n1 = sp * sp + cp * cp, n2 = st * st + ctau * ctau;
-    if (n1 < 1e-12f) { sp = 0.f; cp = 1.f; }  // degenerate pair -> (0, 1)
-    else { const float i = rsqrtf(n1); sp *= i; cp *= i; }
-    if (n2 < 1e-12f) { st = 0.f; ctau = 1.f; }
-    else { const float i = rsqrtf(n2); st *= i; ctau *= i; }
-    const float sth = 2.f * sqrtf(s[0] * sm[0]);  // sqrt(1 - ct^2)
+    const bool d1 = n1 < 1e-12f, d2 = n2 < 1e-12f;  // degenerate pair -> (0, 1)
+    const float i1 = rsqrtf(d1 ? 1.f : n1), i2 = rsqrtf(d2 ? 1.f : n2);
+    sp = d1 ? 0.f : sp * i1;
+    cp = d1 ? 1.f : cp * i1;
+    st = d2 ? 0.f : st * i2;
+    ctau = d2 ? 1.f : ctau * i2;
+    const float sth = 2.f * sqrt_fast(s[0] * sm[0]);  // sqrt(1 - ct^2)
     L.z = make_float3(cp * sth, sp * sth, ct);
     L.x = make_float3(ct * cp * ctau - sp * st, ct * sp * ctau + cp * st, -sth * ctau);
     L.y = make_float3(L.z.y * L.x.z - L.z.z * L.x.y, L.z.z * L.x.x - L.z.x * L.x.z, L.z.x * L.x.y - L.z.y * L.x.x);
     L.lambda = fminf(fmaxf(__expf(r[5]), kLambdaMinF), kLambdaMaxF);
     L.a = fminf(__expf(r[6]), kEccMaxF);
-    L.one_m_emin = -expm1f(-2.f * L.lambda);
-    L.log_k = kLog2Pi + __logf(L.one_m_emin / L.lambda) - 0.5f * log1pf(L.a);
+    L.one_m_emin = -expm1_fast(-2.f * L.lambda);
+    // log K = log 2pi + log((1 - e^{-2l}) / l) - log(1 + a) / 2  (absolute error ~1e-7)
+    L.log_k = kLog2Pi + __logf(L.one_m_emin * rcp_fast(L.lambda)) - 0.5f * __logf(1.f + L.a);
 }
 
 // log G at v (sphdist.cpp:133-140), from local w = 1 - dz, q = 1 + dz, t2.
 __device__ __forceinline__ float lobe_log_g(const Lobe &L, float w, float q, float t2) {
-    if (q <= 1e-12f) return -INFINITY;  // v = -z sentinel
-    float log_u = w < 1.f ? log1pf(-0.5f * w) : __logf(0.5f * q);
+    float log_u = w < 1.f ? log1p_fast(-0.5f * w) : __logf(0.5f * q);
     log_u = fmaxf(log_u, -27.631021f);  // u >= 1e-12
     const float beta = L.a * t2;
-    return 2.f * L.lambda * expm1f((1.f + beta) * log_u) + beta * log_u;
+    const float lg = 2.f * L.lambda * expm1_fast((1.f + beta) * log_u) + beta * log_u;
+    return q <= 1e-12f ? -INFINITY : lg;  // v = -z sentinel
 }
 
 __device__ __forceinline__ float lobe_log_g_at(const Lobe &L, float3 v) {
@@ -126,27 +161,27 @@ __device__ __forceinline__ float lobe_log_g_at(const Lobe &L, float3 v) {
     const float h = 0.5f * dot3(e, e);
     const float w = dz >= 0.f ? h : 2.f - h, q = dz >= 0.f ? 2.f - h : h;
     const float dx = dot3(e, L.x);
-    const float t2 = fminf(fmaxf(dx * dx / fmaxf(w * q, 1e-12f), 0.f), 1.f);
+    const float t2 = fminf(fmaxf(dx * dx * rcp_fast(fmaxf(w * q, 1e-12f)), 0.f), 1.f);
     return lobe_log_g(L, w, q, t2);
 }
 
 // nasg_sample (sphdist.cpp:159-181); also returns the lobe-local w, q, t2.
 __device__ __forceinline__ float3 sample_lobe(const Lobe &L, float xi0, float xi1, float xi2, float &w_out,
                                               float &q_out, float &t2_out) {
-    const float ln_s = log1pf(-(1.f - xi0) * L.one_m_emin);  // s = 1 - (1-xi0)(1-e^-2l)
-    const float ratio = ln_s / (2.f * L.lambda);               // in [-1, 0]
+    const float ln_s = log1p_fast(-(1.f - xi0) * L.one_m_emin);  // s = 1 - (1-xi0)(1-e^-2l)
+    const float ratio = fmaxf(ln_s * rcp_fast(2.f * L.lambda), -1.f);  // in [-1, 0]
     float srho, crho;
-    sincospif(xi1 - 0.5f, &srho, &crho);  // rho = (xi1 - 1/2) pi
-    const float expo = (1.f + L.a * srho * srho) / (1.f + L.a);
+    __sincosf((xi1 - 0.5f) * 3.14159265358979f, &srho, &crho);  // rho = (xi1 - 1/2) pi
+    const float expo = (1.f + L.a * srho * srho) * rcp_fast(1.f + L.a);
     float one_m_c = 2.f, one_p_c = 0.f;  // base clamped to 0 -> theta = pi
     if (ratio > -1.f) {
-        const float el = expo * log1pf(ratio);
-        one_m_c = fminf(fmaxf(-2.f * expm1f(el), 0.f), 2.f);
+        const float el = expo * log1p_fast(ratio);
+        one_m_c = fminf(fmaxf(-2.f * expm1_fast(el), 0.f), 2.f);
         one_p_c = 2.f * __expf(el);
     }
     const float cth = 1.f - one_m_c;
-    const float sth = sqrtf(fmaxf(one_m_c * one_p_c, 0.f));
-    const float st = sqrtf(1.f + L.a) * srho;  // phi = atan2(sqrt(1+a) sin rho, cos rho)
+    const float sth = sqrt_fast(fmaxf(one_m_c * one_p_c, 0.f));
+    const float st = sqrt_fast(1.f + L.a) * srho;  // phi = atan2(sqrt(1+a) sin rho, cos rho)
     const float inv = rsqrtf(crho * crho + st * st);
     float cph = crho * inv, sph = st * inv;
     if (xi2 <= 0.5f) { cph = -cph; sph = -sph; }  // western chart: phi + pi
