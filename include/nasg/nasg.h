@@ -152,7 +152,17 @@ int nasg_train_stats_take(nasg_ctx *ctx, nasg_train_stats *stats);
 int nasg_get_last_grad(nasg_ctx *ctx, float *host_g, size_t n_floats);
 int64_t nasg_adam_t(nasg_ctx *ctx);
 
-/* ---- multi-GPU (NCCL over NVLink; one rank per GPU) --------------------- */
+/* ---- multi-GPU (NCCL over NVLink; one rank per GPU) ---------------------
+ * Data-parallel train_iteration: rank r holds n_per_rank[r] samples.  The
+ * global minibatch t is split over ranks in proportion to their buffers;
+ * each rank walks its own PCG32-shuffled buffer with the reference's
+ * cursor / epoch rule (guiding.cpp:236-243) for T = nu*ceil(S/t) steps.
+ * Fills, per step, this rank's row count, the global row count (the 1/count
+ * of guiding.cpp:262) and whether this rank reshuffles before the step.
+ * With nranks == 1 the plan is exactly the reference's.  Host-only; returns
+ * the number of steps, or -1 on bad arguments. */
+int nasg_dp_plan(const nasg_config *cfg, const int64_t *n_per_rank, int nranks, int rank, int max_steps,
+                 int64_t *local_count, int64_t *global_count, int32_t *reshuffle_before);
 int nasg_comm_unique_id(void *out_128_bytes);
 int nasg_comm_init(nasg_ctx *ctx, const void *unique_id_128_bytes, int rank, int nranks);
 

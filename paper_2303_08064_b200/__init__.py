@@ -108,6 +108,7 @@ def lib():
         "nasg_stride_update": (f64, [f64, u64, u64]),
         "nasg_synth_queries": (None, [u64, i64, i64, vp, vp, vp, vp, vp, vp]),
         "nasg_synth_samples": (None, [u64, i64, i64, vp, vp, vp]),
+        "nasg_dp_plan": (i32, [vp, vp, i32, i32, i32, vp, vp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -196,6 +197,23 @@ def synth_samples(seed: int, n: int, first: int = 0, bmin=(-1, -1, -1), bmax=(1,
     lo, hi = _f3(bmin), _f3(bmax)
     lib().nasg_synth_samples(seed, first, n, lo.ctypes.data, hi.ctypes.data, out.ctypes.data)
     return out
+
+
+def dp_plan(config: TrainerConfig, n_per_rank, rank: int):
+    """Data-parallel minibatch plan of one train_iteration (host-only, see nasg.h):
+    returns (local_count, global_count, reshuffle_before) arrays, one entry per step."""
+    cfg = _Config(config.n_components, config.sample_capacity, config.batch_size, config.step_factor,
+                  config.learning_rate, config.loss_blend, config.seed)
+    n_all = np.ascontiguousarray(n_per_rank, np.int64)
+    max_steps = config.step_factor * -(-config.sample_capacity // config.batch_size)
+    loc = np.zeros(max_steps, np.int64)
+    glo = np.zeros(max_steps, np.int64)
+    res = np.zeros(max_steps, np.int32)
+    steps = lib().nasg_dp_plan(C.byref(cfg), n_all.ctypes.data, len(n_all), rank, max_steps, loc.ctypes.data,
+                               glo.ctypes.data, res.ctypes.data)
+    if steps < 0:
+        raise NasgError("bad data-parallel plan arguments")
+    return loc[:steps], glo[:steps], res[:steps].astype(bool)
 
 
 class Guide:

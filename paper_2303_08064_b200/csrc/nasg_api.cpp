@@ -90,6 +90,7 @@ struct Nccl {
     ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                               cudaStream_t) = nullptr;
+    ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
     const char *(*errStr)(ncclResult_t) = nullptr;
     bool load() {
@@ -101,8 +102,9 @@ struct Nccl {
         commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
         allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
         commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+        allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
         errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-        return getUniqueId && commInitRank && allReduce && commDestroy;
+        return getUniqueId && commInitRank && allReduce && allGather && commDestroy;
     }
 };
 Nccl g_nccl;
@@ -611,6 +613,60 @@ int nasg_train_stats_take(nasg_ctx *c, nasg_train_stats *st) {
     return NASG_OK;
 }
 
+// Data-parallel minibatch plan (see nasg.h).  Global batch t is split over the
+// ranks in proportion to their buffer sizes; each rank walks its own shuffled
+// buffer with the reference's cursor/epoch rule (guiding.cpp:236-243).
+int nasg_dp_plan(const nasg_config *cfg, const int64_t *n_per_rank, int nranks, int rank, int max_steps,
+                 int64_t *local_count, int64_t *global_count, int32_t *reshuffle_before) {
+    if (!cfg || !n_per_rank || nranks < 1 || rank < 0 || rank >= nranks || cfg->batch_size <= 0 ||
+        cfg->sample_capacity <= 0 || cfg->step_factor <= 0)
+        return -1;
+    const int64_t t = cfg->batch_size;
+    const int steps = cfg->step_factor * (int)((cfg->sample_capacity + t - 1) / t);  // guiding.cpp:204-206
+    if (steps > max_steps) return -1;
+    int64_t total = 0;
+    for (int k = 0; k < nranks; ++k) {
+        if (n_per_rank[k] < 0) return -1;
+        total += n_per_rank[k];
+    }
+    if (total == 0) return 0;  // empty global buffer: no-op (guiding.cpp:198-202)
+    std::vector<int64_t> tr(nranks), cur(nranks, 0);
+    int64_t assigned = 0;
+    for (int k = 0; k < nranks; ++k) {
+        tr[k] = (int64_t)(((unsigned __int128)t * (uint64_t)n_per_rank[k]) / (uint64_t)total);
+        assigned += tr[k];
+    }
+    for (int k = 0; assigned < t && k < nranks; ++k)  // remainder to the first non-empty ranks
+        if (n_per_rank[k] > 0) {
+            ++tr[k];
+            ++assigned;
+        }
+    for (int k = 0; k < nranks; ++k)
+        if (n_per_rank[k] > 0 && tr[k] == 0) tr[k] = 1;
+    for (int step = 0; step < steps; ++step) {
+        int64_t g = 0;
+        for (int k = 0; k < nranks; ++k) {
+            int64_t cnt = 0;
+            bool resh = step == 0;
+            if (n_per_rank[k] > 0) {
+                if (cur[k] >= n_per_rank[k]) {
+                    cur[k] = 0;
+                    resh = true;
+                }
+                cnt = std::min(tr[k], n_per_rank[k] - cur[k]);
+                cur[k] += cnt;
+            }
+            g += cnt;
+            if (k == rank) {
+                local_count[step] = cnt;
+                if (reshuffle_before) reshuffle_before[step] = (resh && n_per_rank[k] > 0) ? 1 : 0;
+            }
+        }
+        global_count[step] = g;
+    }
+    return steps;
+}
+
 // Trainer::train_iteration (guiding.cpp:196-282).
 int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *samples, double b,
                          nasg_train_stats *stats, void *stream) {
@@ -623,18 +679,37 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
         CUDA_TRY(cudaStreamWaitEvent(c->stream, ev, 0));
         cudaEventDestroy(ev);
     }
-    if (n == 0) {  // empty buffer: no-op + publish (:198-202)
+    if (n == 0 && c->nranks == 1) {  // empty buffer: no-op + publish (:198-202)
         ++c->iterations;
         int r = do_publish(c);
         if (stats) *stats = nasg_train_stats{0, 0.0, 0, 0};
         return r;
     }
     if (n > 0xffffffffll) return fail(NASG_ERR_INVALID, "buffer too large");
-    const int t = c->cfg.batch_size;
-    const int steps = c->cfg.step_factor * ((c->cfg.sample_capacity + t - 1) / t);  // config S (:204-206)
-    int r = ensure_order(c, (size_t)n);
+    // Data-parallel plan: every rank learns every rank's buffer size, then walks
+    // the same deterministic schedule (single rank: exactly guiding.cpp:204-276).
+    std::vector<int64_t> n_all((size_t)c->nranks, 0);
+    n_all[(size_t)c->rank] = n;
+    if (c->nranks > 1) {
+        int64_t *d_n = nullptr;
+        CUDA_TRY(cudaMalloc(&d_n, sizeof(int64_t) * c->nranks));
+        CUDA_TRY(cudaMemcpyAsync(d_n + c->rank, &n, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        if (g_nccl.allGather(d_n + c->rank, d_n, 1, ncclInt64, c->comm, s) != ncclSuccess)
+            return fail(NASG_ERR_NCCL, "ncclAllGather of buffer sizes failed");
+        CUDA_TRY(cudaMemcpyAsync(n_all.data(), d_n, sizeof(int64_t) * c->nranks, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        cudaFree(d_n);
+    }
+    const int max_steps = c->cfg.step_factor * ((c->cfg.sample_capacity + c->cfg.batch_size - 1) / c->cfg.batch_size);
+    std::vector<int64_t> local(max_steps), global(max_steps);
+    std::vector<int32_t> resh(max_steps);
+    const int steps = nasg_dp_plan(&c->cfg, n_all.data(), c->nranks, c->rank, max_steps, local.data(),
+                                   global.data(), resh.data());
+    if (steps < 0) return fail(NASG_ERR_INVALID, "bad data-parallel plan");
+    int r = ensure_order(c, (size_t)std::max<int64_t>(n, 1));
     if (r) return r;
-    Pcg32 rng(hash_combine(c->cfg.seed, 0x7261696e) + (uint64_t)c->iterations, 5);  // :216
+    // epoch shuffle (guiding.cpp:216-225); rank 0 uses the reference's stream 5
+    Pcg32 rng(hash_combine(c->cfg.seed, 0x7261696e) + (uint64_t)c->iterations, 5 + 2 * (uint64_t)c->rank);
     uint32_t *ord = c->h_order;
     for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
     auto reshuffle = [&]() {  // Fisher-Yates :219-224
@@ -643,21 +718,18 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
             std::swap(ord[i - 1], ord[j]);
         }
     };
-    reshuffle();
-    CUDA_TRY(cudaMemcpyAsync(c->d_order, ord, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
     if (stats) CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), s));
     int64_t cursor = 0;
     for (int step = 0; step < steps; ++step) {
-        if (cursor >= n) {
-            CUDA_TRY(cudaStreamSynchronize(s));  // h_order is still the source of the last upload
+        if (resh[step]) {
+            CUDA_TRY(cudaStreamSynchronize(s));  // h_order may still be the source of the last upload
             reshuffle();
             CUDA_TRY(cudaMemcpyAsync(c->d_order, ord, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
             cursor = 0;
         }
-        const int64_t count = std::min<int64_t>(t, n - cursor);
-        r = train_step_impl(c, samples, c->d_order + cursor, count, count, b, s);
+        r = train_step_impl(c, samples, c->d_order + cursor, local[step], global[step], b, s);
         if (r) return r;
-        cursor += count;
+        cursor += local[step];
     }
     ++c->iterations;
     if (s != c->stream) {
