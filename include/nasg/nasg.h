@@ -101,6 +101,12 @@ int nasg_get_weights(nasg_ctx *ctx, float *host_w, size_t n_floats, int publishe
 int nasg_publish(nasg_ctx *ctx);  /* snapshot live -> published (stream-ordered) */
 int nasg_set_precision(nasg_ctx *ctx, int precision); /* nasg_precision for queries */
 int nasg_get_precision(nasg_ctx *ctx);
+/* MLP arithmetic of training: NASG_MLP_FP32 (FFMA forward/backward, the
+ * reference's float MLP; default) or NASG_MLP_BF16 (tcgen05 forward, backward
+ * and dW GEMMs with bf16 operands, fp32 accumulation, fp32 master weights and
+ * Adam).  The KL gradient is computed in double on both paths. */
+int nasg_set_train_precision(nasg_ctx *ctx, int precision);
+int nasg_get_train_precision(nasg_ctx *ctx);
 /* save_checkpoint / load_checkpoint (net.hpp:163-167, net.cpp:31-82): NASGNET1. */
 int nasg_save_checkpoint(nasg_ctx *ctx, const char *path);
 int nasg_load_checkpoint(nasg_ctx *ctx, const char *path);

@@ -86,6 +86,8 @@ def lib():
         "nasg_publish": (i32, [vp]),
         "nasg_set_precision": (i32, [vp, i32]),
         "nasg_get_precision": (i32, [vp]),
+        "nasg_set_train_precision": (i32, [vp, i32]),
+        "nasg_get_train_precision": (i32, [vp]),
         "nasg_save_checkpoint": (i32, [vp, C.c_char_p]),
         "nasg_load_checkpoint": (i32, [vp, C.c_char_p]),
         "nasg_query_sample": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp]),
@@ -267,6 +269,15 @@ class Guide:
     @precision.setter
     def precision(self, p: int):
         _check(lib().nasg_set_precision(self._h, int(p)))
+
+    @property
+    def train_precision(self) -> int:
+        """MLP arithmetic of training (NASG_MLP_FP32 default, NASG_MLP_BF16 tensor cores)."""
+        return lib().nasg_get_train_precision(self._h)
+
+    @train_precision.setter
+    def train_precision(self, p: int):
+        _check(lib().nasg_set_train_precision(self._h, int(p)))
 
     def save_checkpoint(self, path: str):
         _check(lib().nasg_save_checkpoint(self._h, path.encode()))

@@ -23,25 +23,18 @@
 #include "nasg_internal.h"
 #include "nasg_math.cuh"
 #include "tc_ptx.cuh"
+#include "tc_common.cuh"
 
 namespace nasg {
 
 namespace {
 
 constexpr int kWG = 3;                          // epilogue warpgroups
-constexpr int kAuxWarp = kWG * 4;               // TMEM allocation + weight TMA warp
-constexpr int kThreads = kWG * 128 + 32;        // 416
+               // TMEM allocation + weight TMA warp
+constexpr int kThreads = kWG * 128;  // 12 warps: 3 per SMSP -> up to 168 registers        // 416
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one bf16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;
 
-// bf16 weight image: per layer the UMMA B operand W_l^T as [N_out][K_in],
-// K-major, no swizzle: 8-row x 16-byte core matrices, LBO = 128 B between the
-// two K chunks of a K=16 slab, SBO = K_in * 16 B between 8-row groups.
-__host__ __device__ constexpr uint32_t w_off(int l) {
-    return l == 0 ? 0u : (l == 1 ? 16384u : (l == 2 ? 49152u : 81920u));
-}
-__host__ __device__ constexpr uint32_t img_bytes(int n) { return 81920u + (uint32_t)packed_width(n) * 256u; }
-__host__ __device__ constexpr uint32_t align1k(uint32_t x) { return (x + 1023u) & ~1023u; }
 template <int N>
 constexpr size_t smem_bytes() {
     return align1k(img_bytes(N)) + kWG * kABytes + (kWG + 2) * sizeof(uint64_t);
@@ -91,47 +84,6 @@ void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s) {
     pack_tc_kernel<<<148, 256, 0, s>>>(w, n_comp, static_cast<__nv_bfloat16 *>(img));
 }
 
-// --------------------------------------------------------------- encoding --
-// encode_inputs (encoding.cpp:21-46) in fp32, written as bf16 into row t of
-// the K=64 A tile (core-matrix layout).  Returns clamped coordinates.
-__device__ __forceinline__ int encode_tile_row(const QueryArgs &a, int64_t q, const float (&inv_ext)[3],
-                                               uint32_t a_row) {
-    float e[64];
-    int clamped = 0;
-    if (q < a.n) {
-        const float4 x = a.x[q], wo = a.wo[q], nrm = a.nrm[q];
-        const float xs[3] = {x.x, x.y, x.z};
-#pragma unroll
-        for (int axis = 0; axis < 3; ++axis) {
-            float t = inv_ext[axis] > 0.f ? (xs[axis] - a.bounds.bmin[axis]) * inv_ext[axis] : 0.5f;
-            if (t < 0.f || t > 1.f) {
-                ++clamped;
-                t = fminf(fmaxf(t, 0.f), 1.f);
-            }
-#pragma unroll
-            for (int i = 0; i < kBins; ++i) {
-                const float d = t - (i + 0.5f) * (1.f / kBins);
-                e[axis * kBins + i] = __expf(-d * d * 180.5f);
-            }
-        }
-        e[57] = wo.x; e[58] = wo.y; e[59] = wo.z;
-        e[60] = nrm.x; e[61] = nrm.y; e[62] = nrm.z;
-        e[63] = 1.f;
-    } else {
-#pragma unroll
-        for (int k = 0; k < 64; ++k) e[k] = 0.f;
-    }
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-        tc::st_shared_v4(a_row + c * 128, tc::pack_bf16x2(e[8 * c], e[8 * c + 1]),
-                         tc::pack_bf16x2(e[8 * c + 2], e[8 * c + 3]), tc::pack_bf16x2(e[8 * c + 4], e[8 * c + 5]),
-                         tc::pack_bf16x2(e[8 * c + 6], e[8 * c + 7]));
-    return clamped;
-}
-
-// named barrier over the 128 threads of epilogue warpgroup g (id 0 is __syncthreads)
-__device__ __forceinline__ void wg_sync(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
-
 // ------------------------------------------------------------------ kernel --
 template <int N, int MODE>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -154,20 +106,18 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         s_clamped = 0;
         tc::fence_mbar_init();
     }
-    if (warp == kAuxWarp) tc::tmem_alloc(tmem_slot, kTmemCols);
+    if (warp == 0) tc::tmem_alloc(tmem_slot, kTmemCols);
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == kAuxWarp) {
-        if ((threadIdx.x & 31) == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
-            tc::mbar_arrive_expect_tx(w_bar, IMG);
-            for (uint32_t off = 0; off < IMG; off += 16384)
-                tc::bulk_g2s(smem + off, img + off, (IMG - off) < 16384u ? (IMG - off) : 16384u, w_bar);
-        }
-        __syncwarp();
-    } else {
+    if (threadIdx.x == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
+        tc::mbar_arrive_expect_tx(w_bar, IMG);
+        for (uint32_t off = 0; off < IMG; off += 16384)
+            tc::bulk_g2s(smem + off, img + off, (IMG - off) < 16384u ? (IMG - off) : 16384u, w_bar);
+    }
+    {
         const int g = warp >> 2, t = threadIdx.x & 127;
         const uint32_t my_tmem = tmem + g * 128 + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + g * kABytes);
@@ -279,7 +229,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (warp == kAuxWarp) {
+    if (warp == 0) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem, kTmemCols);
     }

@@ -303,24 +303,44 @@ int train_reduce(int n_comp, const TrainScratch &sc, float *grad, int *nonfinite
 }
 
 // step_stats[0..2] = loss_sum, loss_count, dropped of this step (tile order)
+// One block: strided per-thread partial sums, then a fixed-shape tree
+// (deterministic for a given tile count).
 __global__ void step_stats_kernel(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
                                   double *step_stats) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    __shared__ double sl[256], sc[256], sd[256];
+    const int t = threadIdx.x;
     double ls = 0.0, lc = 0.0, dr = 0.0;
-    for (int t = 0; t < ntiles; ++t) {
-        ls += tile_loss[t];
-        lc += tile_lc[t];
-        dr += tile_dr[t];
+    for (int i = t; i < ntiles; i += 256) {
+        ls += tile_loss[i];
+        lc += tile_lc[i];
+        dr += tile_dr[i];
     }
-    step_stats[0] = ls;
-    step_stats[1] = lc;
-    step_stats[2] = dr;
+    sl[t] = ls; sc[t] = lc; sd[t] = dr;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (t < s) {
+            sl[t] += sl[t + s];
+            sc[t] += sc[t + s];
+            sd[t] += sd[t + s];
+        }
+        __syncthreads();
+    }
+    if (t == 0) {
+        step_stats[0] = sl[0];
+        step_stats[1] = sc[0];
+        step_stats[2] = sd[0];
+    }
+}
+
+int train_step_stats_n(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
+                       double *step_stats, cudaStream_t s) {
+    step_stats_kernel<<<1, 256, 0, s>>>(tile_loss, tile_lc, tile_dr, ntiles, step_stats);
+    return 1;
 }
 
 int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s) {
     const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
-    step_stats_kernel<<<1, 32, 0, s>>>(sc.tile_loss, sc.tile_loss_count, sc.tile_dropped, ntiles, step_stats);
-    return 1;
+    return train_step_stats_n(sc.tile_loss, sc.tile_loss_count, sc.tile_dropped, ntiles, step_stats, s);
 }
 
 // acc[0..4] = loss_sum, loss_count, dropped, skipped, steps (context accumulators)

@@ -1,0 +1,439 @@
+// bf16 tensor-core training step (Trainer::train_iteration inner loop,
+// guiding.cpp:236-276) — the fast training path; fp32 master weights + Adam.
+//
+//   K_fb (train_tc_fb_kernel)  persistent, 3 epilogue warpgroups x 128-row tiles,
+//        like the query kernel: gather + encode -> 4 forward UMMA layers (TMEM
+//        accumulators, ReLU fused into the bf16 conversion, ReLU gate bits kept
+//        in registers) -> KL gradient of every row in fp32 (kl_grad_row_fast,
+//        nasg_math.cuh; guiding.cpp:108-165) -> delta4 -> 3 backward UMMA
+//        layers delta_l = (delta_{l+1} W_l^T) .* [h_l > 0] (net.hpp:101-107)
+//        that read the SAME smem weight images as the forward, as MN-major B
+//        operands.  Every h_l / delta_l tile is written once to HBM as bf16 in
+//        the tensor-core's core-matrix layout.
+//   K_dw (train_tc_dw_kernel)  dW_l = h_l^T delta_{l+1} (net.hpp:102) as a
+//        split-K UMMA GEMM over 128-row blocks: both operands MN-major, TMA
+//        bulk copies into a 2-stage smem ring, fp32 accumulation in TMEM,
+//        per-split partials reduced in fixed order (deterministic).
+//   then the fp32 tail shared with the fp32 path: step stats, skip decision,
+//   Adam (k_train.cu), and a re-pack of the live bf16 image.
+#include <cuda_bf16.h>
+
+#include "nasg_internal.h"
+#include "nasg_math.cuh"
+#include "nasg_refmath.cuh"
+#include "tc_common.cuh"
+#include "tc_ptx.cuh"
+
+namespace nasg {
+
+namespace {
+
+constexpr int kWGt = 3;
+
+constexpr int kThreadsT = kWGt * 128;  // 12 warps: 3 per SMSP -> up to 168 registers
+constexpr uint32_t kATile = 128 * 128 * 2;
+constexpr uint32_t kTmemColsT = 512;
+
+template <int N>
+constexpr size_t fb_smem() {
+    return align1k(img_bytes(N)) + kWGt * kATile + 64 + kWGt * 4 * 3 * sizeof(double);
+}
+
+// byte offset of row t's 16-byte chunk c inside a 128-row block / A tile with F features
+__device__ __forceinline__ uint32_t blk_off(int t, int F) { return (uint32_t)((t >> 3) * (F * 16) + (t & 7) * 16); }
+
+__device__ __forceinline__ void st_g16(uint8_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    *reinterpret_cast<uint4 *>(p) = make_uint4(a, b, c, d);
+}
+
+__device__ __forceinline__ uint32_t nz_bits(uint32_t p) {  // (lo != 0) | (hi != 0) << 1 of a bf16 pair
+    return ((p & 0xFFFFu) ? 1u : 0u) | ((p >> 16) ? 2u : 0u);
+}
+
+}  // namespace
+
+size_t tc_train_block_bytes(int n_comp) {  // bf16 bytes per 128-row block over all 8 arrays
+    return (size_t)(64 + 3 * 128 + 3 * 128 + packed_width(n_comp)) * 256;
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreadsT, 1)
+train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__restrict__ samples,
+                   const uint32_t *__restrict__ order, int64_t count, double gscale, double b, double e, Bounds bd,
+                   TcTrainBufs tb, unsigned long long *clamp_count) {
+    constexpr int NP = packed_width(N);
+    constexpr uint32_t IMG = img_bytes(N);
+    constexpr uint32_t A_OFF = align1k(IMG);
+    extern __shared__ __align__(1024) uint8_t smem[];
+    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + A_OFF + kWGt * kATile);
+    uint64_t *w_bar = acc_full + kWGt;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
+    double *red = reinterpret_cast<double *>(smem + A_OFF + kWGt * kATile + 64);
+    __shared__ int s_clamped;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t ntiles = (count + 127) / 128;
+    if (threadIdx.x == 0) {
+        for (int g = 0; g < kWGt; ++g) tc::mbar_init(&acc_full[g], 1);
+        tc::mbar_init(w_bar, 1);
+        s_clamped = 0;
+        tc::fence_mbar_init();
+    }
+    if (warp == 0) tc::tmem_alloc(tmem_slot, kTmemColsT);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (threadIdx.x == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
+        tc::mbar_arrive_expect_tx(w_bar, IMG);
+        for (uint32_t off = 0; off < IMG; off += 16384)
+            tc::bulk_g2s(smem + off, img + off, (IMG - off) < 16384u ? (IMG - off) : 16384u, w_bar);
+    }
+    {
+        const int g = warp >> 2, t = threadIdx.x & 127;
+        const uint32_t my_tmem = tmem + g * 128 + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint32_t a_base = tc::smem_u32(smem + A_OFF + g * kATile);
+        const uint32_t sW = tc::smem_u32(smem);
+        // forward layer l (0..3): A = activations (K = 64 | 128), B = W_l^T image (K-major)
+        // backward through W_l (l = 3, 2, 1): A = delta (K = NP | 128), B = the same image read MN-major
+        auto issue = [&](int l, bool bwd) {
+            tc::fence_proxy_async_smem();
+            tc::tc_fence_before();
+            wg_sync(g);
+            if (t == 0) {
+                tc::mbar_wait(w_bar, 0);
+                tc::tc_fence_after();
+                const uint32_t d = tmem + g * 128, b0 = sW + w_off(l);
+                if (!bwd) {
+                    const int K = l == 0 ? kIn : kHidden;
+                    const uint32_t sbo = (uint32_t)K * 16u;
+                    const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
+                    for (int k = 0; k < K / 16; ++k)
+                        tc::mma_bf16(d, tc::smem_desc(a_base + k * 256, 128, sbo), tc::smem_desc(b0 + k * 256, 128, sbo),
+                                     idesc, k > 0 ? 1u : 0u);
+                } else {
+                    const int K = l == 3 ? NP : kHidden;              // contraction over W_l's output index
+                    const uint32_t sbo_a = (uint32_t)K * 16u;          // delta tile, K-major
+                    const uint32_t lbo_b = (uint32_t)kHidden * 16u;    // image rows (out index) in 8-groups
+                    const uint32_t idesc = tc::idesc_bf16(128, kHidden, false, true);
+                    for (int k = 0; k < K / 16; ++k)
+                        tc::mma_bf16(d, tc::smem_desc(a_base + k * 256, 128, sbo_a),
+                                     tc::smem_desc(b0 + k * 2 * lbo_b, lbo_b, 128), idesc, k > 0 ? 1u : 0u);
+                }
+                tc::mma_commit(&acc_full[g]);
+            }
+        };
+        uint32_t acc_ph = 0;
+        auto wait_acc = [&]() {
+            tc::mbar_wait(&acc_full[g], acc_ph);
+            acc_ph ^= 1u;
+            tc::tc_fence_after();
+        };
+        float inv_ext[3];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) inv_ext[k] = bd.ext[k] > 0.0 ? (float)(1.0 / bd.ext[k]) : 0.f;
+        int clamped = 0;
+        uint8_t *H[3] = {tb.h1, tb.h2, tb.h3};
+        uint8_t *DL[3] = {tb.d1, tb.d2, tb.d3};
+        for (int64_t tile = (int64_t)blockIdx.x * kWGt + g; tile < ntiles; tile += (int64_t)gridDim.x * kWGt) {
+            const int64_t row = tile * 128 + t;
+            const bool valid = row < count;
+            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
+            if (valid) {  // gather through the epoch permutation (guiding.cpp:242-244)
+                const int64_t src = order ? (int64_t)order[row] : row;
+                const float4 *sp = reinterpret_cast<const float4 *>(samples + src);
+                s0 = sp[0]; s1 = sp[1]; s2 = sp[2]; s3 = sp[3];
+            }
+            clamped += encode_row_bf16(valid, s0, s1, s2, bd, inv_ext, a_base + blk_off(t, 64),
+                                       tb.h0 + tile * (64 * 256) + blk_off(t, 64));
+            issue(0, false);
+            uint32_t mask[3][4];
+#pragma unroll 1
+            for (int l = 1; l < 4; ++l) {  // hidden layers: ReLU, bf16, gate bits, next A, h_l block
+                wait_acc();
+                uint8_t *gh = H[l - 1] + tile * (128 * 256) + blk_off(t, 128);
+                uint32_t mk[4];
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    float v[32];
+                    tc::tmem_ld32(my_tmem + q4 * 32, v);
+                    tc::tmem_ld_wait();
+                    uint32_t bits = 0;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t p[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                            bits |= nz_bits(p[h]) << (8 * c + 2 * h);
+                        }
+                        tc::st_shared_v4(a_base + blk_off(t, 128) + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                        st_g16(gh + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                    }
+                    mk[q4] = bits;
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) mask[l - 1][q] = mk[q];
+                issue(l, false);
+            }
+            wait_acc();
+            float raw[NP];
+            {
+                float v[32];
+#pragma unroll
+                for (int q = 0; q < NP / 32; ++q) {
+                    tc::tmem_ld32(my_tmem + q * 32, v);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) raw[q * 32 + i] = v[i];
+                }
+                if constexpr (NP % 32 != 0) {
+                    float u[16];
+                    tc::tmem_ld16(my_tmem + (NP / 32) * 32, u);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) raw[(NP / 32) * 32 + i] = u[i];
+                }
+            }
+            // ---- KL gradient (fp32 stable forms), in place: raw -> delta4 (packed order)
+            double loss = 0.0;
+            int state = 0;  // 0 invalid row, 1 ok (loss counted), 2 dropped, 3 ok (loss not finite)
+            if (valid) {
+                bool finite = true;
+#pragma unroll
+                for (int j = 0; j < NP; ++j) finite &= isfinite(raw[j]);
+                if (!finite) {
+                    state = 2;  // non-finite network output row (guiding.cpp:251-254)
+                } else {
+                    TrainRow srow;
+                    srow.wi = make_float3(s3.x, s3.y, s3.z);
+                    srow.p = s0.w;
+                    srow.q_s = s1.w;
+                    srow.pbsdf = s2.w;
+                    auto rawf = [&](int j) { return raw[j]; };
+                    auto put = [&](int j, float v) { raw[j] = v; };
+                    float lossf = 0.f;
+                    const bool ok = kl_grad_row_fast<N>(rawf, srow, (float)b, (float)e, (float)gscale, put, lossf);
+                    loss = lossf;
+                    state = ok ? (isfinite(lossf) ? 1 : 3) : 2;
+                }
+            }
+            if (state != 1 && state != 3) {
+#pragma unroll
+                for (int j = 0; j < NP; ++j) raw[j] = 0.f;
+            }
+            {  // delta4 -> A tile (K = NP) and the d4 block
+                uint8_t *gd = tb.d4 + tile * (NP * 256) + blk_off(t, NP);
+#pragma unroll
+                for (int c = 0; c < NP / 8; ++c) {
+                    const uint32_t p0 = tc::pack_bf16x2(raw[8 * c], raw[8 * c + 1]),
+                                   p1 = tc::pack_bf16x2(raw[8 * c + 2], raw[8 * c + 3]),
+                                   p2 = tc::pack_bf16x2(raw[8 * c + 4], raw[8 * c + 5]),
+                                   p3 = tc::pack_bf16x2(raw[8 * c + 6], raw[8 * c + 7]);
+                    tc::st_shared_v4(a_base + blk_off(t, NP) + c * 128, p0, p1, p2, p3);
+                    st_g16(gd + c * 128, p0, p1, p2, p3);
+                }
+            }
+            issue(3, true);
+            {  // tile statistics, deterministic order (warp tree, then warps 0..3)
+                double ls = state == 1 ? loss : 0.0, lc = state == 1 ? 1.0 : 0.0, dr = state == 2 ? 1.0 : 0.0;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    ls += __shfl_xor_sync(0xffffffffu, ls, o);
+                    lc += __shfl_xor_sync(0xffffffffu, lc, o);
+                    dr += __shfl_xor_sync(0xffffffffu, dr, o);
+                }
+                double *rg = red + g * 12;
+                if (lane == 0) {
+                    rg[(warp & 3) * 3] = ls;
+                    rg[(warp & 3) * 3 + 1] = lc;
+                    rg[(warp & 3) * 3 + 2] = dr;
+                }
+                wg_sync(g);
+                if (t == 0) {
+                    tb.tile_loss[tile] = ((rg[0] + rg[3]) + rg[6]) + rg[9];
+                    tb.tile_lc[tile] = (int)(rg[1] + rg[4] + rg[7] + rg[10]);
+                    tb.tile_dr[tile] = (int)(rg[2] + rg[5] + rg[8] + rg[11]);
+                }
+            }
+            // ---- backward: delta_l = (delta_{l+1} W_l^T) .* [h_l > 0]
+#pragma unroll 1
+            for (int l = 3; l >= 1; --l) {
+                wait_acc();
+                uint8_t *gd = DL[l - 1] + tile * (128 * 256) + blk_off(t, 128);
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    float v[32];
+                    tc::tmem_ld32(my_tmem + q4 * 32, v);
+                    tc::tmem_ld_wait();
+                    const uint32_t bits = mask[l - 1][q4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t p[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h) {
+                            const int i0 = 8 * c + 2 * h;
+                            const float lo = (bits >> i0) & 1u ? v[i0] : 0.f;
+                            const float hi = (bits >> (i0 + 1)) & 1u ? v[i0 + 1] : 0.f;
+                            p[h] = tc::pack_bf16x2(lo, hi);
+                        }
+                        if (l > 1) tc::st_shared_v4(a_base + blk_off(t, 128) + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                        st_g16(gd + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                    }
+                }
+                if (l > 1) issue(l - 1, true);
+            }
+            tc::tc_fence_before();
+        }
+        if (clamped) atomicAdd(&s_clamped, clamped);
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem, kTmemColsT);
+    }
+    if (threadIdx.x == 0 && s_clamped && clamp_count) atomicAdd(clamp_count, (unsigned long long)s_clamped);
+}
+
+// ------------------------------------------------------------------- K_dw --
+// grid (splits, 4 layers).  Layer L computes D[128][FB] = A^T-contraction over
+// rows of A block [rows][128] and B block [rows][FB], both MN-major:
+//   L0: A = delta1, B = h0 -> dW1^T   L1: A = h1, B = delta2 -> dW2
+//   L2: A = h2, B = delta3 -> dW3     L3: A = h3, B = delta4 -> dW4 (packed cols)
+__global__ void __launch_bounds__(128, 1)
+train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
+    extern __shared__ __align__(1024) uint8_t smem[];
+    const int L = blockIdx.y;
+    const uint8_t *A = L == 0 ? tb.d1 : (L == 1 ? tb.h1 : (L == 2 ? tb.h2 : tb.h3));
+    const uint8_t *B = L == 0 ? tb.h0 : (L == 1 ? tb.d2 : (L == 2 ? tb.d3 : tb.d4));
+    const int FB = L == 0 ? 64 : (L == 3 ? np : 128);
+    const uint32_t abytes = 128u * 256u, bbytes = (uint32_t)FB * 256u;
+    constexpr uint32_t kStage = 65536;
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + 2 * kStage);
+    uint64_t *empty = full + 2;
+    uint64_t *done = full + 4;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + 5);
+    const int warp = threadIdx.x >> 5;
+    const int64_t b0 = (int64_t)blockIdx.x * bps, b1 = min(nblocks, b0 + bps);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < 2; ++s) {
+            tc::mbar_init(&full[s], 1);
+            tc::mbar_init(&empty[s], 1);
+        }
+        tc::mbar_init(done, 1);
+        tc::fence_mbar_init();
+    }
+    if (warp == 0) tc::tmem_alloc(tmem_slot, 128);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (threadIdx.x == 0 && b1 > b0) {
+        const uint32_t idesc = tc::idesc_bf16(128, FB, true, true);
+        auto load = [&](int64_t blk, int s) {
+            tc::mbar_arrive_expect_tx(&full[s], abytes + bbytes);
+            for (uint32_t off = 0; off < abytes; off += 16384)
+                tc::bulk_g2s(smem + s * kStage + off, A + blk * abytes + off, 16384, &full[s]);
+            for (uint32_t off = 0; off < bbytes; off += 16384)
+                tc::bulk_g2s(smem + s * kStage + abytes + off, B + blk * bbytes + off,
+                             (bbytes - off) < 16384u ? (bbytes - off) : 16384u, &full[s]);
+        };
+        uint32_t fph[2] = {0, 0}, eph[2] = {0, 0};
+        load(b0, 0);
+        if (b0 + 1 < b1) load(b0 + 1, 1);
+        for (int64_t i = b0; i < b1; ++i) {
+            const int s = (int)((i - b0) & 1);
+            tc::mbar_wait(&full[s], fph[s]);
+            fph[s] ^= 1u;
+            tc::tc_fence_after();
+            const uint32_t sa = tc::smem_u32(smem + s * kStage), sb = sa + abytes;
+            for (int k = 0; k < 8; ++k)  // 128 rows = 8 x K16
+                tc::mma_bf16(tmem, tc::smem_desc(sa + k * 2 * 2048, 2048, 128),
+                             tc::smem_desc(sb + k * 2 * (FB * 16), FB * 16, 128), idesc, (i > b0 || k > 0) ? 1u : 0u);
+            tc::mma_commit(&empty[s]);
+            if (i + 2 < b1) {
+                tc::mbar_wait(&empty[s], eph[s]);
+                eph[s] ^= 1u;
+                load(i + 2, s);
+            }
+        }
+        tc::mma_commit(done);
+    }
+    __syncthreads();
+    if (b1 > b0) {
+        tc::mbar_wait(done, 0);
+        tc::tc_fence_after();
+        float *out = tb.partial + ((size_t)L * tb.splits + blockIdx.x) * (128 * 128) + threadIdx.x * 128;
+        const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
+        for (int q = 0; q < FB / 16; ++q) {
+            float v[16];
+            tc::tmem_ld16(ta + q * 16, v);
+            tc::tmem_ld_wait();
+#pragma unroll
+            for (int i = 0; i < 16; i += 4)
+                *reinterpret_cast<float4 *>(out + q * 16 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem, 128);
+    }
+}
+
+// canonical grad[e] = sum over splits (fixed order) of the layer partials
+__global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, float *grad, int *nonfinite) {
+    const int nw = n_weights(n_comp), D = 8 * n_comp + 1;
+    const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
+    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nw) return;
+    int L, m, n;
+    if (e < o1) { L = 0; m = e % kHidden; n = e / kHidden; }           // dW1^T[n_out][k_in]
+    else if (e < o2) { L = 1; m = (e - o1) / kHidden; n = (e - o1) % kHidden; }
+    else if (e < o3) { L = 2; m = (e - o2) / kHidden; n = (e - o2) % kHidden; }
+    else { L = 3; m = (e - o3) / D; n = packed_col((e - o3) % D, n_comp); }
+    const float *p = tb.partial + (size_t)L * tb.splits * (128 * 128) + m * 128 + n;  // layer stride = capacity
+    float s = 0.f;
+    for (int k = 0; k < splits; ++k) s += p[(size_t)k * (128 * 128)];
+    grad[e] = s;
+    if (!isfinite(s)) atomicOr(nonfinite, 1);
+}
+
+int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
+                  int64_t global_count, double b, double loss_blend, const Bounds &bounds, TcTrainBufs &tb,
+                  int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s) {
+    if (n_comp != 8 && n_comp != 4) return -1;
+    const int64_t ntiles = (count + 127) / 128;
+    const double gscale = 1.0 / (double)global_count;
+    if (ntiles > 0) {
+        const int64_t supers = (ntiles + kWGt - 1) / kWGt;
+        const int grid = (int)(supers < num_sms ? supers : num_sms);
+        const uint8_t *im = static_cast<const uint8_t *>(img);
+        if (n_comp == 8) {
+            constexpr size_t sm = fb_smem<8>();
+            cudaFuncSetAttribute(train_tc_fb_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            train_tc_fb_kernel<8><<<grid, kThreadsT, sm, s>>>(im, samples, order, count, gscale, b, loss_blend, bounds,
+                                                             tb, clamp_count);
+        } else {
+            constexpr size_t sm = fb_smem<4>();
+            cudaFuncSetAttribute(train_tc_fb_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            train_tc_fb_kernel<4><<<grid, kThreadsT, sm, s>>>(im, samples, order, count, gscale, b, loss_blend, bounds,
+                                                             tb, clamp_count);
+        }
+        int splits = (int)(ntiles < tb.splits ? ntiles : tb.splits);
+        const int bps = (int)((ntiles + splits - 1) / splits);
+        splits = (int)((ntiles + bps - 1) / bps);
+        const size_t sm = 2 * 65536 + 64;
+        cudaFuncSetAttribute(train_tc_dw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        train_tc_dw_kernel<<<dim3(splits, 4), 128, sm, s>>>(tb, ntiles, bps, packed_width(n_comp));
+        const int nw = n_weights(n_comp);
+        train_tc_reduce_kernel<<<(nw + 255) / 256, 256, 0, s>>>(tb, splits, n_comp, grad, nonfinite);
+        train_step_stats_n(tb.tile_loss, tb.tile_lc, tb.tile_dr, (int)ntiles, tb.step_stats, s);
+    }
+    return 4;
+}
+
+}  // namespace nasg

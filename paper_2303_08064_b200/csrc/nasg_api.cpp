@@ -125,7 +125,10 @@ struct nasg_ctx {
     // published snapshot (NetworkSnapshot net.hpp:161)
     float *w_pub = nullptr, *wp_pub = nullptr;
     void *tc_pub = nullptr;
-    int precision = NASG_MLP_FP32;
+    int precision = NASG_MLP_FP32;        // query path MLP arithmetic
+    int train_precision = NASG_MLP_FP32;  // training path MLP arithmetic
+    void *tc_live = nullptr;              // bf16 image of the live weights (bf16 training)
+    TcTrainBufs tcb{};
     unsigned long long *d_clamp = nullptr;
     // Adam / step state on device
     int64_t *d_adam_t = nullptr;
@@ -201,7 +204,37 @@ int do_publish(nasg_ctx *c) {
 int repack_live(nasg_ctx *c) {
     launch_pack_fp32(c->w, c->N, c->wp, c->wtp, c->stream);
     c->launches++;
+    if (c->tc_live) {
+        launch_pack_tc(c->w, c->N, c->tc_live, c->stream);
+        c->launches++;
+    }
     CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+int ensure_tc_scratch(nasg_ctx *c, int64_t count) {
+    const int64_t blocks = (count + 127) / 128;
+    TcTrainBufs &t = c->tcb;
+    if (blocks <= t.max_blocks) return NASG_OK;
+    uint8_t **bufs[8] = {&t.h0, &t.h1, &t.h2, &t.h3, &t.d1, &t.d2, &t.d3, &t.d4};
+    const int feats[8] = {64, 128, 128, 128, 128, 128, 128, packed_width(c->N)};
+    for (int i = 0; i < 8; ++i) {
+        if (*bufs[i]) cudaFree(*bufs[i]);
+        *bufs[i] = nullptr;
+        CUDA_TRY(cudaMalloc(bufs[i], (size_t)blocks * feats[i] * 256));
+    }
+    if (t.tile_loss) cudaFree(t.tile_loss);
+    if (t.tile_lc) cudaFree(t.tile_lc);
+    if (t.tile_dr) cudaFree(t.tile_dr);
+    CUDA_TRY(cudaMalloc(&t.tile_loss, blocks * sizeof(double)));
+    CUDA_TRY(cudaMalloc(&t.tile_lc, blocks * sizeof(int)));
+    CUDA_TRY(cudaMalloc(&t.tile_dr, blocks * sizeof(int)));
+    if (!t.partial) {
+        t.splits = 2 * 37;  // 4 layers x 74 splits ~ 2 waves over 148 SMs
+        CUDA_TRY(cudaMalloc(&t.partial, (size_t)4 * t.splits * 128 * 128 * sizeof(float)));
+    }
+    t.step_stats = c->d_step_stats;
+    t.max_blocks = blocks;
     return NASG_OK;
 }
 
@@ -235,9 +268,15 @@ int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
 int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
                     int64_t global_count, double b, cudaStream_t s) {
     if (count <= 0 && c->nranks == 1) return NASG_OK;
-    int r = ensure_scratch(c, std::max<int64_t>(count, 1));
+    const bool tc = c->train_precision == NASG_MLP_BF16;
+    int r = tc ? ensure_tc_scratch(c, std::max<int64_t>(count, 1)) : ensure_scratch(c, std::max<int64_t>(count, 1));
     if (r) return r;
-    if (count > 0) {
+    if (count > 0 && tc) {
+        const int k = train_tc_step(c->N, c->tc_live, samples, order, count, global_count, b, c->cfg.loss_blend,
+                                    c->bounds, c->tcb, c->num_sms, c->d_clamp, c->grad, c->d_nonfinite, s);
+        if (k < 0) return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for bf16 training");
+        c->launches += k;
+    } else if (count > 0) {
         if (train_forward_backward(c->N, c->wp, c->wtp, samples, order, count, global_count, b,
                                    c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, c->d_clamp, s) < 0)
             return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for training");
@@ -261,6 +300,10 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
     train_finalize_step(c->d_nonfinite, c->d_adam_t, c->d_corr, c->d_skip, c->d_step_stats, c->d_acc, s);
     train_adam(c->N, c->w, c->m, c->v, c->grad, c->d_corr, c->d_skip, c->cfg.learning_rate, c->wp, c->wtp, s);
     c->launches += 2;
+    if (tc) {  // bf16 operands of the next step from the fp32 master weights
+        launch_pack_tc(c->w, c->N, c->tc_live, s);
+        c->launches++;
+    }
     CHECK_LAUNCH();
     return NASG_OK;
 }
@@ -354,7 +397,10 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     ALLOC(c->wp, kPackedF32 * sizeof(float));
     ALLOC(c->wtp, kPackedT32 * sizeof(float));
     ALLOC(c->wp_pub, kPackedF32 * sizeof(float));
-    if (tc_supported(c->N)) ALLOC(c->tc_pub, tc_image_bytes(c->N));
+    if (tc_supported(c->N)) {
+        ALLOC(c->tc_pub, tc_image_bytes(c->N));
+        ALLOC(c->tc_live, tc_image_bytes(c->N));
+    }
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));
     ALLOC(c->d_corr, 2 * sizeof(float));
@@ -389,7 +435,9 @@ int nasg_destroy(nasg_ctx *c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
-    void *bufs[] = {c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->w_pub, c->wp_pub, c->tc_pub, c->d_clamp,
+    void *bufs[] = {c->tc_live, c->tcb.h0, c->tcb.h1, c->tcb.h2, c->tcb.h3, c->tcb.d1, c->tcb.d2, c->tcb.d3,
+                    c->tcb.d4, c->tcb.tile_loss, c->tcb.tile_lc, c->tcb.tile_dr, c->tcb.partial,
+                    c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->w_pub, c->wp_pub, c->tc_pub, c->d_clamp,
                     c->d_adam_t, c->d_corr, c->d_skip, c->d_nonfinite, c->d_step_stats, c->d_acc, c->d_order,
                     c->sc.h0, c->sc.h1, c->sc.h2, c->sc.h3, c->sc.d1, c->sc.d2, c->sc.d3, c->sc.d4,
                     c->sc.dw_partial, c->sc.tile_loss, c->sc.tile_loss_count, c->sc.tile_dropped,
@@ -440,6 +488,16 @@ int nasg_set_precision(nasg_ctx *c, int p) {
 }
 
 int nasg_get_precision(nasg_ctx *c) { return c ? c->precision : -1; }
+
+int nasg_set_train_precision(nasg_ctx *c, int p) {
+    if (!c) return fail(NASG_ERR_INVALID, "null context");
+    if (p != NASG_MLP_FP32 && p != NASG_MLP_BF16) return fail(NASG_ERR_INVALID, "bad precision");
+    if (p == NASG_MLP_BF16 && !c->tc_live) return fail(NASG_ERR_UNSUPPORTED, "bf16 training unavailable");
+    c->train_precision = p;
+    return NASG_OK;
+}
+
+int nasg_get_train_precision(nasg_ctx *c) { return c ? c->train_precision : -1; }
 
 // NASGNET1 (net.cpp:31-82): magic, u32 N, u32 5, u32 dims[5], row-major f32 W1..W4.
 int nasg_save_checkpoint(nasg_ctx *c, const char *path) {

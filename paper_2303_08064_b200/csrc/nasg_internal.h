@@ -21,6 +21,11 @@ constexpr int kPackedF32 = kIn * kHidden + 3 * kHidden * kHidden;  // 57344 floa
 // W4^T [128 packed cols][128] (rows >= NP are zero).
 constexpr int kPackedT32 = 3 * kHidden * kHidden;
 
+// Packed raw-output layout of the last layer (see nasg_math.cuh): header of
+// round_up(N + 1, 16) columns (weight logits, selection logit), then 8 columns per lobe.
+__host__ __device__ constexpr int packed_header(int n) { return ((n + 1 + 15) / 16) * 16; }
+__host__ __device__ constexpr int packed_width(int n) { return packed_header(n) + 8 * n; }
+
 __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHidden * kHidden + kHidden * (8 * n + 1); }
 
 struct Bounds {
@@ -75,6 +80,24 @@ struct TrainScratch {
     int splits;       // capacity of dw_partial
     int last_splits;  // splits used by the last train_dw
 };
+
+// bf16 tensor-core training scratch: per-128-row blocks of bf16 activations /
+// deltas in the UMMA core-matrix layout, per-tile stats, dW partials.
+struct TcTrainBufs {
+    uint8_t *h0, *h1, *h2, *h3, *d1, *d2, *d3, *d4;
+    double *tile_loss;
+    int *tile_lc, *tile_dr;
+    double *step_stats;
+    float *partial;  // [4 layers][splits][128][128]
+    int splits;
+    int64_t max_blocks;
+};
+size_t tc_train_block_bytes(int n_comp);
+int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
+                  int64_t global_count, double b, double loss_blend, const Bounds &bounds, TcTrainBufs &tb,
+                  int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s);
+int train_step_stats_n(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
+                       double *step_stats, cudaStream_t s);
 
 int train_forward_backward(int n_comp, const float *wp, const float *wtp,
                            const nasg_train_sample *samples, const uint32_t *order,

@@ -36,6 +36,8 @@
 #include <type_traits>
 #include <cuda_runtime.h>
 
+#include "nasg_internal.h"  // packed_header / packed_width
+
 namespace nasg {
 
 constexpr float kLog2Pi = 1.8378770664093453f;  // log(2*pi)
@@ -44,8 +46,6 @@ constexpr float kLambdaMaxF = 3e3f;             // sphdist.hpp:14
 constexpr float kEccMaxF = 3e3f;                // sphdist.hpp:15
 constexpr float kSelMin = 0.01f, kSelMax = 0.99f;  // guiding.hpp:22-23
 
-__host__ __device__ constexpr int packed_header(int n) { return ((n + 1 + 15) / 16) * 16; }
-__host__ __device__ constexpr int packed_width(int n) { return packed_header(n) + 8 * n; }
 
 // Packed column of reference raw index j (guiding.hpp:25-30 layout).
 __host__ __device__ constexpr int packed_col(int j, int n) {
@@ -277,6 +277,194 @@ __device__ __forceinline__ float2 guide_pdf(RawFn raw, float3 v, float b, float 
     });
     const float ce = b * c;
     return make_float2(pdf, ce <= 0.f ? bsdf_pdf : ce * pdf + (1.f - ce) * bsdf_pdf);
+}
+
+// ---- KL gradient in fp32 (bf16 training path) --------------------------------
+// Decode intermediates the chain rule needs (DecodedGuide guiding.hpp:34-42).
+struct LobeG {
+    Lobe L;
+    float sig[5], sigm[5];      // sigmoid(raw) and 1 - sigmoid(raw)
+    float ct, st, sp, cp, stau, ctau;
+    float pn1, pn2;             // pre-normalisation pair norms (0 => degenerate)
+    bool lam_cl, a_cl;
+};
+
+__device__ __forceinline__ void decode_lobe_g(const float r[7], LobeG &G) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) sigmoid_pair(r[k], G.sig[k], G.sigm[k]);
+    const float ct = G.sig[0] - G.sigm[0];
+    float sp = G.sig[1] - G.sigm[1], cp = G.sig[2] - G.sigm[2], st = G.sig[3] - G.sigm[3], ctau = G.sig[4] - G.sigm[4];
+    const float n1 = sqrt_fast(sp * sp + cp * cp), n2 = sqrt_fast(st * st + ctau * ctau);
+    const bool d1 = n1 < 1e-6f, d2 = n2 < 1e-6f;
+    const float i1 = rcp_fast(d1 ? 1.f : n1), i2 = rcp_fast(d2 ? 1.f : n2);
+    sp = d1 ? 0.f : sp * i1;
+    cp = d1 ? 1.f : cp * i1;
+    st = d2 ? 0.f : st * i2;
+    ctau = d2 ? 1.f : ctau * i2;
+    G.pn1 = d1 ? 0.f : n1;
+    G.pn2 = d2 ? 0.f : n2;
+    const float sth = 2.f * sqrt_fast(G.sig[0] * G.sigm[0]);
+    G.ct = ct; G.st = sth; G.sp = sp; G.cp = cp; G.stau = st; G.ctau = ctau;
+    Lobe &L = G.L;
+    L.z = make_float3(cp * sth, sp * sth, ct);
+    L.x = make_float3(ct * cp * ctau - sp * st, ct * sp * ctau + cp * st, -sth * ctau);
+    L.y = make_float3(0.f, 0.f, 0.f);  // unused by the gradient
+    const float lam = __expf(r[5]), a = __expf(r[6]);
+    L.lambda = fminf(fmaxf(lam, kLambdaMinF), kLambdaMaxF);
+    L.a = fminf(a, kEccMaxF);
+    G.lam_cl = L.lambda != lam;
+    G.a_cl = L.a != a;
+    L.one_m_emin = -expm1_fast(-2.f * L.lambda);
+    L.log_k = kLog2Pi + __logf(L.one_m_emin * rcp_fast(L.lambda)) - 0.5f * __logf(1.f + L.a);
+}
+
+// d log K / d lambda = coth(l) - 1 - 1/l, with a series below l = 0.05 (sphdist.cpp:217)
+__device__ __forceinline__ float dlogk_dlambda(float l, float one_m_emin) {
+    const float l2 = l * l;
+    const float ser = -1.f + l * (1.f / 3.f - l2 * (1.f / 45.f - l2 * (2.f / 945.f)));
+    return l < 0.05f ? ser : 2.f * (1.f - one_m_emin) * rcp_fast(one_m_emin) - rcp_fast(l);
+}
+
+// One-sample KL gradient w.r.t. the packed raw outputs, fp32 restatement of
+// kl_loss_gradient (guiding.cpp:108-165) + nasg_grad_logpdf (sphdist.cpp:200-274)
+// in one O(N) pass; put(col, g) receives g * gscale for every packed column.
+// Returns false when the sample is dropped; loss = loss_surrogate (:167-176).
+template <int N, class RawFn, class PutFn>
+__device__ __forceinline__ bool kl_grad_row_fast(RawFn raw, const TrainRow &s, float b, float e, float gscale,
+                                                 PutFn put, float &loss) {
+    constexpr int H = packed_header(N), NP = H + 8 * N;
+    loss = 0.f;
+    if (s.p == 0.f) {  // valid cheap path (guiding.cpp:112)
+        static_for<0, NP>([&](auto jc) { put(decltype(jc)::value, 0.f); });
+        return true;
+    }
+    float w[N], c, c_sig;
+    {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < N; ++i) mx = fmaxf(mx, raw(i));
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            w[i] = __expf(raw(i) - mx);
+            sum += w[i];
+        }
+        const float inv = rcp_fast(sum);
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[i] *= inv;
+        float sm;
+        sigmoid_pair(raw(N), c_sig, sm);
+        c = fminf(fmaxf(c_sig, kSelMin), kSelMax);
+    }
+    float pdf[N];
+    float q_mix = 0.f;
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        float r[7];
+        lobe_logits<N>(raw, i, r);
+        Lobe L;
+        decode_lobe(r, L);
+        pdf[i] = __expf(lobe_log_g_at(L, s.wi) - L.log_k);
+        q_mix += w[i] * pdf[i];
+    });
+    const float c_eff = b * c;
+    const float q_hat = c_eff * q_mix + (1.f - c_eff) * s.pbsdf;
+    if (!(isfinite(q_mix) && q_mix > 0.f && isfinite(q_hat) && q_hat > 0.f) || !(s.q_s > 0.f)) {
+        static_for<0, NP>([&](auto jc) { put(decltype(jc)::value, 0.f); });
+        loss = __int_as_float(0x7fc00000);
+        return false;
+    }
+    const float ws = s.p / s.q_s;
+    const float mix_scale = e * (c_eff * q_mix / q_hat) + (1.f - e);
+    const float scale = -ws * mix_scale * gscale;
+    const float inv_q = rcp_fast(q_mix);
+    bool finite = true;
+    {
+        const float dsig = (c != c_sig) ? 0.f : c_sig * (1.f - c_sig);
+        const float gc = -ws * e * b * (q_mix - s.pbsdf) / q_hat * dsig * gscale;
+        finite &= isfinite(gc);
+        put(N, gc);
+        static_for<N + 1, H>([&](auto jc) { put(decltype(jc)::value, 0.f); });
+    }
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        float r[7];
+        lobe_logits<N>(raw, i, r);
+        LobeG G;
+        decode_lobe_g(r, G);
+        const Lobe &L = G.L;
+        const float ri = w[i] * pdf[i] * inv_q;  // posterior responsibility
+        const float gl = scale * (ri - w[i]);
+        finite &= isfinite(gl);
+        put(i, gl);
+        // local frame of omega_i (stable fp32 forms, nasg_math.cuh header)
+        const float3 v = s.wi;
+        const float dz = dot3(v, L.z);
+        const float sg = dz >= 0.f ? 1.f : -1.f;
+        const float3 ev = make_float3(v.x - sg * L.z.x, v.y - sg * L.z.y, v.z - sg * L.z.z);
+        const float hh = 0.5f * dot3(ev, ev);
+        const float wl = dz >= 0.f ? hh : 2.f - hh, ql = dz >= 0.f ? 2.f - hh : hh;
+        const float dx = dot3(ev, L.x);
+        const float denom = fmaxf(wl * ql, 1e-12f);
+        const float t2 = fminf(fmaxf(dx * dx * rcp_fast(denom), 0.f), 1.f);
+        float g7[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d log q / d (ct, sp, cp, st, ctau, lambda, a)
+        if (fminf(wl, ql) >= 1e-6f && pdf[i] > 0.f) {      // pole guard sphdist.cpp:205
+            const float lam = L.lambda, a = L.a;
+            float log_u = wl < 1.f ? log1p_fast(-0.5f * wl) : __logf(0.5f * ql);
+            log_u = fmaxf(log_u, -27.631021f);
+            const float u = fmaxf(0.5f * ql, 1e-12f);
+            const float beta = a * t2, m = 1.f + beta;
+            const float um1 = expm1_fast(m * log_u), um = um1 + 1.f;
+            const float inv_u = rcp_fast(u), inv_den = rcp_fast(denom);
+            const float dG_dbeta = (2.f * lam * um + 1.f) * log_u;
+            const float dG_du = 2.f * lam * m * (um * inv_u) + beta * inv_u;
+            const float dt2_ddz = 2.f * dz * t2 * inv_den;
+            const float dG_ddz = 0.5f * dG_du + dG_dbeta * a * dt2_ddz;
+            const float dG_ddx = dG_dbeta * a * 2.f * dx * inv_den;
+            g7[5] = ri * (2.f * um1 - dlogk_dlambda(lam, L.one_m_emin));
+            g7[6] = ri * (t2 * dG_dbeta + 0.5f * rcp_fast(1.f + a));
+            const float ct = G.ct, st = fmaxf(G.st, 1e-9f), dst = -ct * rcp_fast(st);
+            const float cs = G.cp * v.x + G.sp * v.y;
+            float g_ct = dG_ddz * (dst * cs + v.z) + dG_ddx * (G.ctau * cs - dst * G.ctau * v.z);
+            float g_sp = dG_ddz * (st * v.y) + dG_ddx * (-G.stau * v.x + ct * G.ctau * v.y);
+            float g_cp = dG_ddz * (st * v.x) + dG_ddx * (ct * G.ctau * v.x + G.stau * v.y);
+            float g_st = dG_ddx * (-G.sp * v.x + G.cp * v.y);
+            float g_ctau = dG_ddx * (ct * G.cp * v.x + ct * G.sp * v.y - st * v.z);
+            float ps = G.cp * (G.cp * g_sp - G.sp * g_cp), pc = G.sp * (G.sp * g_cp - G.cp * g_sp);
+            g_sp = ps; g_cp = pc;
+            ps = G.ctau * (G.ctau * g_st - G.stau * g_ctau);
+            pc = G.stau * (G.stau * g_ctau - G.ctau * g_st);
+            g_st = ps; g_ctau = pc;
+            g7[0] = ri * g_ct; g7[1] = ri * g_sp; g7[2] = ri * g_cp; g7[3] = ri * g_st; g7[4] = ri * g_ctau;
+            bool ok = true;
+#pragma unroll
+            for (int k = 0; k < 7; ++k) ok &= isfinite(g7[k]);
+            if (!ok) {
+#pragma unroll
+                for (int k = 0; k < 7; ++k) g7[k] = 0.f;
+            }
+        }
+        const float inv1 = G.pn1 > 0.f ? rcp_fast(G.pn1) : 0.f, inv2 = G.pn2 > 0.f ? rcp_fast(G.pn2) : 0.f;
+        const float scl[5] = {1.f, inv1, inv1, inv2, inv2};
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const float go = scale * g7[k] * scl[k] * 2.f * G.sig[k] * G.sigm[k];
+            finite &= isfinite(go);
+            put(H + 8 * i + k, go);
+        }
+        const float gl5 = G.lam_cl ? 0.f : scale * g7[5] * L.lambda;
+        const float gl6 = G.a_cl ? 0.f : scale * g7[6] * L.a;
+        finite &= isfinite(gl5) && isfinite(gl6);
+        put(H + 8 * i + 5, gl5);
+        put(H + 8 * i + 6, gl6);
+        put(H + 8 * i + 7, 0.f);
+    });
+    if (!finite) {
+        static_for<0, NP>([&](auto jc) { put(decltype(jc)::value, 0.f); });
+        return false;
+    }
+    loss = -ws * (e * __logf(q_hat) + (1.f - e) * __logf(q_mix));
+    return true;
 }
 
 }  // namespace nasg

@@ -330,7 +330,7 @@ __device__ __forceinline__ bool kl_grad_row(RawFn raw, const TrainRow &s, double
     constexpr int H = packed_header(N);
     loss = 0.0;
     if (s.p == 0.f) {
-        for (int j = 0; j < H + 8 * N; ++j) put(j, 0.f);
+        static_for<0, H + 8 * N>([&](auto jc) { put(decltype(jc)::value, 0.f); });
         return true;
     }
     double w[N], c, c_sig;
@@ -341,7 +341,7 @@ __device__ __forceinline__ bool kl_grad_row(RawFn raw, const TrainRow &s, double
     const double q_hat = c_eff * q_mix + (1.0 - c_eff) * (double)s.pbsdf;
     const bool usable = isfinite(q_mix) && q_mix > 1e-300 && isfinite(q_hat) && q_hat > 1e-300;
     if (!usable || !(s.q_s > 0.f)) {
-        for (int j = 0; j < H + 8 * N; ++j) put(j, 0.f);
+        static_for<0, H + 8 * N>([&](auto jc) { put(decltype(jc)::value, 0.f); });
         loss = NAN;
         return false;
     }
@@ -354,7 +354,7 @@ __device__ __forceinline__ bool kl_grad_row(RawFn raw, const TrainRow &s, double
     const double gc = -ws * e * b * (q_mix - (double)s.pbsdf) / q_hat * dsig_c;
     finite &= isfinite(gc);
     put(N, (float)(gc * gscale));
-    for (int j = N + 1; j < H; ++j) put(j, 0.f);
+    static_for<N + 1, H>([&](auto jc) { put(decltype(jc)::value, 0.f); });
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         float r[7];
@@ -387,7 +387,7 @@ __device__ __forceinline__ bool kl_grad_row(RawFn raw, const TrainRow &s, double
         }
     });
     if (!finite) {
-        for (int j = 0; j < H + 8 * N; ++j) put(j, 0.f);
+        static_for<0, H + 8 * N>([&](auto jc) { put(decltype(jc)::value, 0.f); });
         return false;
     }
     loss = -ws * (e * log(q_hat) + (1.0 - e) * log(q_mix));

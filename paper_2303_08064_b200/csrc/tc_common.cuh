@@ -1,0 +1,74 @@
+// Shared pieces of the tcgen05 kernels (query and training): the bf16 weight
+// image layout, the one-blob encoder writing a bf16 A tile, and the
+// warpgroup barrier.
+#pragma once
+
+#include <cuda_bf16.h>
+
+#include "nasg_internal.h"
+#include "nasg_math.cuh"
+#include "tc_ptx.cuh"
+
+namespace nasg {
+
+// bf16 weight image: per layer the UMMA B operand W_l^T as [N_out][K_in],
+// K-major, no swizzle: 8-row x 16-byte core matrices, LBO = 128 B between the
+// two K chunks of a K=16 slab, SBO = K_in * 16 B between 8-row groups.
+__host__ __device__ constexpr uint32_t w_off(int l) {
+    return l == 0 ? 0u : (l == 1 ? 16384u : (l == 2 ? 49152u : 81920u));
+}
+__host__ __device__ constexpr uint32_t img_bytes(int n) { return 81920u + (uint32_t)packed_width(n) * 256u; }
+__host__ __device__ constexpr uint32_t align1k(uint32_t x) { return (x + 1023u) & ~1023u; }
+
+// --------------------------------------------------------------- encoding --
+// encode_inputs (encoding.cpp:21-46) in fp32, written as bf16 into row t of
+// the K=64 A tile (core-matrix layout); optionally also to `gdst` (a global
+// row block with the same byte layout).  Returns clamped coordinates.
+__device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
+                                               const float (&inv_ext)[3], uint32_t a_row, uint8_t *gdst = nullptr) {
+    float e[64];
+    int clamped = 0;
+    if (valid) {
+        const float xs[3] = {x.x, x.y, x.z};
+#pragma unroll
+        for (int axis = 0; axis < 3; ++axis) {
+            float t = inv_ext[axis] > 0.f ? (xs[axis] - bd.bmin[axis]) * inv_ext[axis] : 0.5f;
+            if (t < 0.f || t > 1.f) {
+                ++clamped;
+                t = fminf(fmaxf(t, 0.f), 1.f);
+            }
+#pragma unroll
+            for (int i = 0; i < kBins; ++i) {
+                const float d = t - (i + 0.5f) * (1.f / kBins);
+                e[axis * kBins + i] = __expf(-d * d * 180.5f);
+            }
+        }
+        e[57] = wo.x; e[58] = wo.y; e[59] = wo.z;
+        e[60] = nrm.x; e[61] = nrm.y; e[62] = nrm.z;
+        e[63] = 1.f;
+    } else {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) e[k] = 0.f;
+    }
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        const uint32_t p0 = tc::pack_bf16x2(e[8 * c], e[8 * c + 1]), p1 = tc::pack_bf16x2(e[8 * c + 2], e[8 * c + 3]),
+                       p2 = tc::pack_bf16x2(e[8 * c + 4], e[8 * c + 5]), p3 = tc::pack_bf16x2(e[8 * c + 6], e[8 * c + 7]);
+        tc::st_shared_v4(a_row + c * 128, p0, p1, p2, p3);
+        if (gdst) *reinterpret_cast<uint4 *>(gdst + c * 128) = make_uint4(p0, p1, p2, p3);
+    }
+    return clamped;
+}
+
+__device__ __forceinline__ int encode_tile_row(const QueryArgs &a, int64_t q, const float (&inv_ext)[3],
+                                               uint32_t a_row) {
+    const bool valid = q < a.n;
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    return encode_row_bf16(valid, valid ? a.x[q] : z, valid ? a.wo[q] : z, valid ? a.nrm[q] : z, a.bounds, inv_ext,
+                           a_row);
+}
+
+// named barrier over the 128 threads of epilogue warpgroup g (id 0 is __syncthreads)
+__device__ __forceinline__ void wg_sync(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
+
+}  // namespace nasg

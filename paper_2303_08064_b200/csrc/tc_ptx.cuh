@@ -127,11 +127,14 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr, uint32_t lbo, uint
     return d;
 }
 
-// Instruction descriptor for kind::f16: A = B = bf16 (K-major), D = f32.
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+// Instruction descriptor for kind::f16: A = B = bf16, D = f32.  a_mn / b_mn
+// select MN-major operands (bits 15 / 16); default K-major.
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn = false, bool b_mn = false) {
     return (1u << 4)                      // D format f32
            | (1u << 7)                    // A format bf16
            | (1u << 10)                   // B format bf16
+           | ((a_mn ? 1u : 0u) << 15)     // A major
+           | ((b_mn ? 1u : 0u) << 16)     // B major
            | ((uint32_t)(N >> 3) << 17)   // N / 8
            | ((uint32_t)(M >> 4) << 24);  // M / 16
 }
