@@ -164,26 +164,37 @@ def time_events(fn, k, stream):
     return [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(k)]
 
 
-def bench_train(g_cls, nasg, args, ws, rank):
-    """Config 3: S = t = 2^18 samples per Adam step (one step per train_iteration)."""
+def bench_train(g_cls, nasg, args, ws, rank, precision):
+    """Config 3: S = t = 2^18 samples per Adam step (one step per train_iteration),
+    data-parallel over ranks (each rank trains on its own 2^18 samples; with
+    N > 1 the dW allreduce runs inside every step)."""
     import torch
     n = args.train_samples
-    g = g_cls(nasg.TrainerConfig(seed=3, sample_capacity=n, batch_size=n))
+    # global S = t = ws * 2^18: the data-parallel plan gives every rank its own 2^18 rows per step
+    g = g_cls(nasg.TrainerConfig(seed=3, sample_capacity=n * ws, batch_size=n * ws))
+    g.train_precision = nasg.NASG_MLP_BF16 if precision == "bf16" else nasg.NASG_MLP_FP32
+    if ws > 1:
+        import torch.distributed as dist
+        uid = [g.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        g.comm_init(uid[0], rank, ws)
     s = torch.from_numpy(nasg.synth_samples(11 + rank, n, first=rank * n)).cuda()
     stream = torch.cuda.current_stream()
-    for i in range(2):
+    for i in range(3):
         g.train_iteration(s, 1.0, stats=False)
     torch.cuda.synchronize()
     barrier(ws)
+    l0 = g.kernel_launches
     times = time_events(lambda: g.train_iteration(s, 1.0, stats=False), args.train_steps, stream)
+    launches = g.kernel_launches - l0
     t = max_over_ranks(sum(times), ws)
     st = g.train_iteration(s, 1.0)
     g.close()
     rate = n * ws * args.train_steps / t
-    return {"metric": "train samples/s (config 3: 2^18 samples/step, fused fwd+KL+bwd+Adam, fp32)",
+    return {"metric": f"train samples/s (config 3: 2^18 samples/step/GPU, fused fwd+KL+bwd+dW+Adam, {precision})",
             "value": rate, "unit": "samples/s", "ms_per_step": 1e3 * t / args.train_steps,
-            "achieved_tflops": rate / ws * FLOP_PER_SAMPLE / 1e12, "dtype": "fp32",
-            "last_mean_loss": st.mean_loss}
+            "achieved_tflops": rate / ws * FLOP_PER_SAMPLE / 1e12, "dtype": precision,
+            "gpu_launches": launches, "last_mean_loss": st.mean_loss}
 
 
 def main():
@@ -273,7 +284,7 @@ def main():
     del dev, out, cbuf
     torch.cuda.empty_cache()
 
-    train = None if args.no_train else bench_train(nasg.Guide, nasg, args, ws, rank)
+    train = None if args.no_train else {p: bench_train(nasg.Guide, nasg, args, ws, rank, p) for p in ("bf16", "fp32")}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_reference_rate(1 << 30, args.cpu_seconds)
