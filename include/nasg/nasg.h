@@ -118,6 +118,10 @@ int nasg_load_checkpoint(nasg_ctx *ctx, const char *path);
 int nasg_query_sample(nasg_ctx *ctx, int64_t n, const float *x, const float *wo,
                       const float *nrm, const float *xi, float *dir_pdf, float *c,
                       void *stream);
+/* Same as nasg_query_sample with the packed row format: 13 floats per query
+ * (position xyz, omega_o xyz, normal xyz, xi_select, xi0, xi1, xi2). */
+int nasg_query_sample_packed(nasg_ctx *ctx, int64_t n, const float *q13, float *dir_pdf, float *c,
+                             void *stream);
 /* mixture_pdf (sphdist.hpp:84) and guided_pdf (guiding.hpp:51) at given
  * directions dir (n x float4).  Either output may be NULL. */
 int nasg_query_pdf(nasg_ctx *ctx, int64_t n, const float *x, const float *wo, const float *nrm,
@@ -138,6 +142,9 @@ int nasg_decode_pdf_raw(nasg_ctx *ctx, int64_t n, const float *raw, const float 
  * returns when dir_pdf (and c) are written.  Inputs are 4 floats/query. */
 int nasg_query_sample_host(nasg_ctx *ctx, int64_t n, const float *x, const float *wo,
                            const float *nrm, const float *xi, float *dir_pdf, float *c);
+/* Host-buffer form over packed 13-float rows: 52 B/query host->device instead
+ * of 64 B, for PCIe-bound callers. */
+int nasg_query_sample_host_packed(nasg_ctx *ctx, int64_t n, const float *q13, float *dir_pdf, float *c);
 
 /* ---- training (Trainer::train_iteration guiding.hpp:149, guiding.cpp:196-282)
  * Runs T = nu*ceil(S/t) minibatch steps over the n samples (epochs reshuffled

@@ -96,6 +96,8 @@ def lib():
         "nasg_decode_sample_raw": (i32, [vp, i64, vp, vp, vp, vp, vp]),
         "nasg_decode_pdf_raw": (i32, [vp, i64, vp, vp, f32, vp, vp, vp, vp]),
         "nasg_query_sample_host": (i32, [vp, i64, vp, vp, vp, vp, vp, vp]),
+        "nasg_query_sample_packed": (i32, [vp, i64, vp, vp, vp, vp]),
+        "nasg_query_sample_host_packed": (i32, [vp, i64, vp, vp, vp]),
         "nasg_train_iteration": (i32, [vp, i64, vp, f64, vp, vp]),
         "nasg_train_step": (i32, [vp, vp, vp, i64, i64, f64, vp]),
         "nasg_train_stats_take": (i32, [vp, vp]),
@@ -346,6 +348,23 @@ class Guide:
             dir_pdf = np.empty((n, 4), np.float32)
         _check(lib().nasg_query_sample_host(self._h, n, _ptr(x), _ptr(wo), _ptr(nrm), _ptr(xi), _ptr(dir_pdf),
                                             _ptr(c)))
+        return dir_pdf, c
+
+    def query_sample_packed(self, q13, dir_pdf=None, c=None, stream=None):
+        """Device (n,13) float32 rows: position, omega_o, normal, xi."""
+        import torch
+        n = q13.shape[0]
+        if dir_pdf is None:
+            dir_pdf = torch.empty((n, 4), dtype=torch.float32, device=q13.device)
+        _check(lib().nasg_query_sample_packed(self._h, n, _ptr(q13), _ptr(dir_pdf), _ptr(c), _stream(stream)))
+        return dir_pdf, c
+
+    def query_sample_host_packed(self, q13, dir_pdf=None, c=None):
+        """Host (n,13) float32 rows; 52 B/query over PCIe."""
+        n = q13.shape[0]
+        if dir_pdf is None:
+            dir_pdf = np.empty((n, 4), np.float32)
+        _check(lib().nasg_query_sample_host_packed(self._h, n, _ptr(q13), _ptr(dir_pdf), _ptr(c)))
         return dir_pdf, c
 
     # ---- training ----------------------------------------------------------------------

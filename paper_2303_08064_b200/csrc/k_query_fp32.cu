@@ -101,7 +101,9 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
         if (tid < kTileRows) {
             const int64_t q = row0 + tid;
             if (q < a.n) {
-                int cl = encode_row(a.x[q], a.wo[q], a.nrm[q], a.bounds, actA, tid);
+                float4 qx, qwo, qn;
+                load_query(a, q, qx, qwo, qn);
+                int cl = encode_row(qx, qwo, qn, a.bounds, actA, tid);
                 if (cl) atomicAdd(&s_clamped, cl);
             } else {
                 for (int k = 0; k < kIn; ++k) actA[k * kLda + tid] = 0.f;
@@ -119,7 +121,7 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
                 auto raw = [&](int j) { return col[j * kLda]; };
                 if (MODE == kModeSample) {
                     float c;
-                    a.dir_pdf[q] = ref::guide_sample<N>(raw, a.xi[q], c);
+                    a.dir_pdf[q] = ref::guide_sample<N>(raw, load_xi(a, q), c);
                     if (a.c) a.c[q] = c;
                 } else if (MODE == kModePdf) {
                     float4 d = a.dir[q];

@@ -210,7 +210,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 auto rawf = [&](int j) { return raw[j]; };
                 if constexpr (MODE == kModeSample) {
                     float c;
-                    a.dir_pdf[q] = guide_sample<N>(rawf, a.xi[q], c);
+                    a.dir_pdf[q] = guide_sample<N>(rawf, load_xi(a, q), c);
                     if (a.c) a.c[q] = c;
                 } else if constexpr (MODE == kModePdf) {
                     const float4 d = a.dir[q];

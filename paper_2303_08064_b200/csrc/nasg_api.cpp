@@ -565,6 +565,52 @@ int nasg_query_sample(nasg_ctx *c, int64_t n, const float *x, const float *wo, c
     return run_query(c, kModeSample, a, pick(c, stream));
 }
 
+int nasg_query_sample_packed(nasg_ctx *c, int64_t n, const float *q13, float *dir_pdf, float *cc, void *stream) {
+    if (!c || n < 0 || (n > 0 && (!q13 || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
+    QueryArgs a = base_args(c, n);
+    a.packed = q13;
+    a.dir_pdf = (float4 *)dir_pdf;
+    a.c = cc;
+    return run_query(c, kModeSample, a, pick(c, stream));
+}
+
+// Packed host rows (52 B/query in, 16 + 4 B out): the PCIe-lean form of
+// nasg_query_sample_host, same 3-lane H2D / kernel / D2H pipeline.
+int nasg_query_sample_host_packed(nasg_ctx *c, int64_t n, const float *q13, float *dir_pdf, float *cc) {
+    if (!c || n < 0 || (n > 0 && (!q13 || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
+    if (n == 0) return NASG_OK;
+    const int64_t chunk = std::min<int64_t>(n, 1 << 20);
+    if (chunk > c->lane_cap) {
+        for (int k = 0; k < 3; ++k) {
+            if (c->lane_in[k]) cudaFree(c->lane_in[k]);
+            if (c->lane_out[k]) cudaFree(c->lane_out[k]);
+            c->lane_in[k] = c->lane_out[k] = nullptr;
+            CUDA_TRY(cudaMalloc(&c->lane_in[k], chunk * 16 * sizeof(float)));
+            CUDA_TRY(cudaMalloc(&c->lane_out[k], chunk * 5 * sizeof(float)));
+        }
+        c->lane_cap = chunk;
+    }
+    cudaEvent_t ready;
+    CUDA_TRY(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ready, c->stream));
+    for (auto l : c->lanes) CUDA_TRY(cudaStreamWaitEvent(l, ready, 0));
+    cudaEventDestroy(ready);
+    int64_t i = 0;
+    for (int64_t off = 0; off < n; off += chunk, ++i) {
+        const int64_t m = std::min(chunk, n - off);
+        const int k = (int)(i % 3);
+        cudaStream_t s = c->lanes[k];
+        float *in = c->lane_in[k], *out = c->lane_out[k];
+        CUDA_TRY(cudaMemcpyAsync(in, q13 + off * 13, (size_t)m * 13 * sizeof(float), cudaMemcpyHostToDevice, s));
+        int r = nasg_query_sample_packed(c, m, in, out, cc ? out + chunk * 4 : nullptr, s);
+        if (r) return r;
+        CUDA_TRY(cudaMemcpyAsync(dir_pdf + off * 4, out, (size_t)m * 4 * sizeof(float), cudaMemcpyDeviceToHost, s));
+        if (cc) CUDA_TRY(cudaMemcpyAsync(cc + off, out + chunk * 4, m * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    for (auto l : c->lanes) CUDA_TRY(cudaStreamSynchronize(l));
+    return NASG_OK;
+}
+
 int nasg_query_pdf(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, const float *dir,
                    float b, const float *bsdf_pdf, float *mix_pdf, float *guided_pdf, void *stream) {
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !dir))) return fail(NASG_ERR_INVALID, "bad argument");

@@ -55,7 +55,32 @@ struct QueryArgs {
     float *raw;  // raw mode (reference order)
     unsigned long long *clamp_count;
     Bounds bounds;
+    // optional packed host format: 13 floats per query = position, omega_o,
+    // normal (3 each) and xi (4); replaces x / wo / nrm / xi when non-null
+    const float *packed;
 };
+
+#ifdef __CUDACC__
+__device__ __forceinline__ void load_query(const QueryArgs &a, int64_t q, float4 &x, float4 &wo, float4 &nrm) {
+    if (a.packed) {
+        const float *p = a.packed + q * 13;
+        x = make_float4(p[0], p[1], p[2], 0.f);
+        wo = make_float4(p[3], p[4], p[5], 0.f);
+        nrm = make_float4(p[6], p[7], p[8], 0.f);
+    } else {
+        x = a.x[q];
+        wo = a.wo[q];
+        nrm = a.nrm[q];
+    }
+}
+__device__ __forceinline__ float4 load_xi(const QueryArgs &a, int64_t q) {
+    if (a.packed) {
+        const float *p = a.packed + q * 13 + 9;
+        return make_float4(p[0], p[1], p[2], p[3]);
+    }
+    return a.xi[q];
+}
+#endif
 
 int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, int num_sms,
                cudaStream_t s);

@@ -63,9 +63,9 @@ __device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, 
 __device__ __forceinline__ int encode_tile_row(const QueryArgs &a, int64_t q, const float (&inv_ext)[3],
                                                uint32_t a_row) {
     const bool valid = q < a.n;
-    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-    return encode_row_bf16(valid, valid ? a.x[q] : z, valid ? a.wo[q] : z, valid ? a.nrm[q] : z, a.bounds, inv_ext,
-                           a_row);
+    float4 x = make_float4(0.f, 0.f, 0.f, 0.f), wo = x, nrm = x;
+    if (valid) load_query(a, q, x, wo, nrm);
+    return encode_row_bf16(valid, x, wo, nrm, a.bounds, inv_ext, a_row);
 }
 
 // named barrier over the 128 threads of epilogue warpgroup g (id 0 is __syncthreads)

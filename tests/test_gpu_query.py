@@ -187,3 +187,24 @@ def test_snapshot_isolation(orc):
     assert np.allclose(after, orc.forward(w, enc), rtol=1e-4, atol=2e-5)
     assert not np.allclose(before, after)
     g.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_packed_rows_match_soa(guide, prec):
+    """nasg_query_sample_packed / _host_packed (13-float rows) == the SoA entry points."""
+    guide.precision = nasg.NASG_MLP_BF16 if prec == "bf16" else nasg.NASG_MLP_FP32
+    try:
+        n = 300_001
+        x, wo, nrm, xi = nasg.synth_queries(11, n)
+        q13 = np.ascontiguousarray(np.concatenate([x[:, :3], wo[:, :3], nrm[:, :3], xi], 1))
+        dev = [torch.from_numpy(a).cuda() for a in (x, wo, nrm, xi)]
+        c1 = torch.empty(n, dtype=torch.float32, device="cuda")
+        ref, _ = guide.query_sample(*dev, c=c1)
+        c2 = torch.empty(n, dtype=torch.float32, device="cuda")
+        out, _ = guide.query_sample_packed(torch.from_numpy(q13).cuda(), c=c2)
+        assert torch.equal(out, ref) and torch.equal(c1, c2)
+        hc = np.empty(n, np.float32)
+        hout, _ = guide.query_sample_host_packed(q13, c=hc)
+        assert np.array_equal(hout, ref.cpu().numpy()) and np.array_equal(hc, c1.cpu().numpy())
+    finally:
+        guide.precision = nasg.NASG_MLP_FP32
