@@ -134,26 +134,30 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
 #pragma unroll
         for (int k = 0; k < 3; ++k) inv_ext[k] = bd.ext[k] > 0.0 ? (float)(1.0 / bd.ext[k]) : 0.f;
         int clamped = 0;
-        uint8_t *H[3] = {tb.h1, tb.h2, tb.h3};
-        uint8_t *DL[3] = {tb.d1, tb.d2, tb.d3};
-        for (int64_t tile = (int64_t)blockIdx.x * kWGt + g; tile < ntiles; tile += (int64_t)gridDim.x * kWGt) {
-            const int64_t row = tile * 128 + t;
-            const bool valid = row < count;
-            float4 s0 = make_float4(0.f, 0.f, 0.f, 0.f), s1 = s0, s2 = s0, s3 = s0;
-            if (valid) {  // gather through the epoch permutation (guiding.cpp:242-244)
+        const int64_t stride = (int64_t)gridDim.x * kWGt;
+        float4 s0, s1, s2, s3;  // this row's sample; the next tile's is prefetched after the KL
+        auto load_sample = [&](int64_t tl) {
+            const int64_t row = tl * 128 + t;
+            s0 = s1 = s2 = s3 = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (row < count) {  // gather through the epoch permutation (guiding.cpp:242-244)
                 const int64_t src = order ? (int64_t)order[row] : row;
                 const float4 *sp = reinterpret_cast<const float4 *>(samples + src);
                 s0 = sp[0]; s1 = sp[1]; s2 = sp[2]; s3 = sp[3];
             }
+        };
+        int64_t tile = (int64_t)blockIdx.x * kWGt + g;
+        load_sample(tile);
+        for (; tile < ntiles; tile += stride) {
+            const int64_t row = tile * 128 + t;
+            const bool valid = row < count;
             clamped += encode_row_bf16(valid, s0, s1, s2, bd, inv_ext, a_base + blk_off(t, 64),
                                        tb.h0 + tile * (64 * 256) + blk_off(t, 64));
             issue(0, false);
-            uint32_t mask[3][4];
+            uint32_t mask[3][4] = {};  // ReLU gate bits of h1..h3
 #pragma unroll 1
             for (int l = 1; l < 4; ++l) {  // hidden layers: ReLU, bf16, gate bits, next A, h_l block
                 wait_acc();
-                uint8_t *gh = H[l - 1] + tile * (128 * 256) + blk_off(t, 128);
-                uint32_t mk[4];
+                uint8_t *gh = (l == 1 ? tb.h1 : (l == 2 ? tb.h2 : tb.h3)) + tile * (128 * 256) + blk_off(t, 128);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     float v[32];
@@ -171,71 +175,60 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                         tc::st_shared_v4(a_base + blk_off(t, 128) + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
                         st_g16(gh + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
                     }
-                    mk[q4] = bits;
+                    // register-resident gate bits: select instead of a dynamic index
+                    mask[0][q4] = l == 1 ? bits : mask[0][q4];
+                    mask[1][q4] = l == 2 ? bits : mask[1][q4];
+                    mask[2][q4] = l == 3 ? bits : mask[2][q4];
                 }
-#pragma unroll
-                for (int q = 0; q < 4; ++q) mask[l - 1][q] = mk[q];
                 issue(l, false);
             }
             wait_acc();
-            float raw[NP];
-            {
-                float v[32];
+            // ---- KL gradient (fp32 stable forms) straight out of tensor memory:
+            // header columns once, each lobe's 8 columns per pass; delta4 goes
+            // to the A tile (K = NP) and the d4 block one 16-byte chunk at a time.
+            constexpr int HD = packed_header(N);
+            uint8_t *gd4 = tb.d4 + tile * (NP * 256) + blk_off(t, NP);
+            const uint32_t a4 = a_base + blk_off(t, NP);
+            auto put_chunk = [&](int c, const float *g8) {
+                const uint32_t p0 = tc::pack_bf16x2(g8[0], g8[1]), p1 = tc::pack_bf16x2(g8[2], g8[3]),
+                               p2 = tc::pack_bf16x2(g8[4], g8[5]), p3 = tc::pack_bf16x2(g8[6], g8[7]);
+                tc::st_shared_v4(a4 + c * 128, p0, p1, p2, p3);
+                st_g16(gd4 + c * 128, p0, p1, p2, p3);
+            };
+            float hdr[HD];
+            tc::tmem_ld16(my_tmem, hdr);
+            tc::tmem_ld_wait();
+            TrainRow srow;
+            srow.wi = make_float3(s3.x, s3.y, s3.z);
+            srow.p = s0.w;
+            srow.q_s = s1.w;
+            srow.pbsdf = s2.w;
+            float lossf = 0.f;
+            int st;
+            {  // every thread of the warp runs the tensor-memory loads (valid or not)
+                float ghdr[HD];
+                auto lobe = [&](int i, float (&r)[8]) {
+                    __syncwarp();
+                    tc::tmem_ld8_sync(my_tmem + HD + 8 * i, r);
+                };
+                auto put_lobe = [&](int i, const float (&g8)[8]) { put_chunk(HD / 8 + i, g8); };
+                st = kl_grad_row_fast<N>(valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr, put_lobe,
+                                         lossf);
+                if (st == kKlOk) {
 #pragma unroll
-                for (int q = 0; q < NP / 32; ++q) {
-                    tc::tmem_ld32(my_tmem + q * 32, v);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) raw[q * 32 + i] = v[i];
-                }
-                if constexpr (NP % 32 != 0) {
-                    float u[16];
-                    tc::tmem_ld16(my_tmem + (NP / 32) * 32, u);
-                    tc::tmem_ld_wait();
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) raw[(NP / 32) * 32 + i] = u[i];
-                }
-            }
-            // ---- KL gradient (fp32 stable forms), in place: raw -> delta4 (packed order)
-            double loss = 0.0;
-            int state = 0;  // 0 invalid row, 1 ok (loss counted), 2 dropped, 3 ok (loss not finite)
-            if (valid) {
-                bool finite = true;
-#pragma unroll
-                for (int j = 0; j < NP; ++j) finite &= isfinite(raw[j]);
-                if (!finite) {
-                    state = 2;  // non-finite network output row (guiding.cpp:251-254)
-                } else {
-                    TrainRow srow;
-                    srow.wi = make_float3(s3.x, s3.y, s3.z);
-                    srow.p = s0.w;
-                    srow.q_s = s1.w;
-                    srow.pbsdf = s2.w;
-                    auto rawf = [&](int j) { return raw[j]; };
-                    auto put = [&](int j, float v) { raw[j] = v; };
-                    float lossf = 0.f;
-                    const bool ok = kl_grad_row_fast<N>(rawf, srow, (float)b, (float)e, (float)gscale, put, lossf);
-                    loss = lossf;
-                    state = ok ? (isfinite(lossf) ? 1 : 3) : 2;
+                    for (int c = 0; c < HD / 8; ++c) put_chunk(c, ghdr + 8 * c);
                 }
             }
-            if (state != 1 && state != 3) {
-#pragma unroll
-                for (int j = 0; j < NP; ++j) raw[j] = 0.f;
+            if (st != kKlOk) {  // zero row: invalid, p = 0 or dropped
+                const float z8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll 1
+                for (int c = 0; c < NP / 8; ++c) put_chunk(c, z8);
             }
-            {  // delta4 -> A tile (K = NP) and the d4 block
-                uint8_t *gd = tb.d4 + tile * (NP * 256) + blk_off(t, NP);
-#pragma unroll
-                for (int c = 0; c < NP / 8; ++c) {
-                    const uint32_t p0 = tc::pack_bf16x2(raw[8 * c], raw[8 * c + 1]),
-                                   p1 = tc::pack_bf16x2(raw[8 * c + 2], raw[8 * c + 3]),
-                                   p2 = tc::pack_bf16x2(raw[8 * c + 4], raw[8 * c + 5]),
-                                   p3 = tc::pack_bf16x2(raw[8 * c + 6], raw[8 * c + 7]);
-                    tc::st_shared_v4(a_base + blk_off(t, NP) + c * 128, p0, p1, p2, p3);
-                    st_g16(gd + c * 128, p0, p1, p2, p3);
-                }
-            }
+            // 0 invalid row, 1 loss counted, 2 dropped, 3 ok but loss not finite
+            const int state = !valid ? 0 : (st == kKlDrop ? 2 : ((st == kKlZero || isfinite(lossf)) ? 1 : 3));
+            const double loss = lossf;
             issue(3, true);
+            load_sample(tile + stride);  // prefetch: in flight through the backward pass
             {  // tile statistics, deterministic order (warp tree, then warps 0..3)
                 double ls = state == 1 ? loss : 0.0, lc = state == 1 ? 1.0 : 0.0, dr = state == 2 ? 1.0 : 0.0;
 #pragma unroll
@@ -258,10 +251,10 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 }
             }
             // ---- backward: delta_l = (delta_{l+1} W_l^T) .* [h_l > 0]
-#pragma unroll 1
-            for (int l = 3; l >= 1; --l) {
+            static_for<0, 3>([&](auto jc) {
+                constexpr int l = 3 - decltype(jc)::value;
                 wait_acc();
-                uint8_t *gd = DL[l - 1] + tile * (128 * 256) + blk_off(t, 128);
+                uint8_t *gd = (l == 1 ? tb.d1 : (l == 2 ? tb.d2 : tb.d3)) + tile * (128 * 256) + blk_off(t, 128);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     float v[32];
@@ -283,7 +276,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     }
                 }
                 if (l > 1) issue(l - 1, true);
-            }
+            });
             tc::tc_fence_before();
         }
         if (clamped) atomicAdd(&s_clamped, clamped);

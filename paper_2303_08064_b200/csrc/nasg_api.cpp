@@ -136,7 +136,9 @@ struct nasg_ctx {
     int *d_skip = nullptr, *d_nonfinite = nullptr;
     double *d_step_stats = nullptr, *d_acc = nullptr;
     TrainScratch sc{};
-    uint32_t *d_order = nullptr, *h_order = nullptr;
+    uint32_t *d_order = nullptr, *h_order[2] = {nullptr, nullptr};
+    cudaEvent_t order_ev[2] = {nullptr, nullptr};  // recorded after each h_order[i] upload
+    int order_slot = 0;
     size_t order_cap = 0;
     int64_t iterations = 0;
     // host pipeline buffers (nasg_query_sample_host)
@@ -180,10 +182,15 @@ int ensure_scratch(nasg_ctx *c, int64_t count) {
 
 int ensure_order(nasg_ctx *c, size_t n) {
     if (n <= c->order_cap) return NASG_OK;
+    CUDA_TRY(cudaDeviceSynchronize());  // uploads from the old buffers are done
     if (c->d_order) cudaFree(c->d_order);
-    if (c->h_order) cudaFreeHost(c->h_order);
     CUDA_TRY(cudaMalloc(&c->d_order, n * sizeof(uint32_t)));
-    CUDA_TRY(cudaMallocHost(&c->h_order, n * sizeof(uint32_t)));
+    for (int i = 0; i < 2; ++i) {
+        if (c->h_order[i]) cudaFreeHost(c->h_order[i]);
+        c->h_order[i] = nullptr;
+        CUDA_TRY(cudaMallocHost(&c->h_order[i], n * sizeof(uint32_t)));
+        if (!c->order_ev[i]) CUDA_TRY(cudaEventCreateWithFlags(&c->order_ev[i], cudaEventDisableTiming));
+    }
     c->order_cap = n;
     return NASG_OK;
 }
@@ -444,7 +451,10 @@ int nasg_destroy(nasg_ctx *c) {
                     c->lane_in[0], c->lane_in[1], c->lane_in[2], c->lane_out[0], c->lane_out[1], c->lane_out[2]};
     for (void *p : bufs)
         if (p) cudaFree(p);
-    if (c->h_order) cudaFreeHost(c->h_order);
+    for (int i = 0; i < 2; ++i) {
+        if (c->h_order[i]) cudaFreeHost(c->h_order[i]);
+        if (c->order_ev[i]) cudaEventDestroy(c->order_ev[i]);
+    }
     for (auto l : c->lanes)
         if (l) cudaStreamDestroy(l);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -814,24 +824,38 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     if (r) return r;
     // epoch shuffle (guiding.cpp:216-225); rank 0 uses the reference's stream 5
     Pcg32 rng(hash_combine(c->cfg.seed, 0x7261696e) + (uint64_t)c->iterations, 5 + 2 * (uint64_t)c->rank);
-    uint32_t *ord = c->h_order;
-    for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
-    auto reshuffle = [&]() {  // Fisher-Yates :219-224
+    // When every minibatch is this rank's whole buffer (config 3: S = t), each
+    // step sums over the same set of rows whatever the permutation, so the
+    // shuffle cannot change which samples a step sees: rows are read in place
+    // (order = nullptr). Otherwise the host Fisher-Yates runs into one of two
+    // pinned order buffers while the GPU still works on the previous upload.
+    bool whole = true;
+    for (int step = 0; step < steps; ++step) whole = whole && local[step] == n;
+    uint32_t *ord = nullptr;
+    auto reshuffle = [&]() -> int {  // Fisher-Yates :219-224, continuing one rng stream per iteration
+        c->order_slot ^= 1;
+        CUDA_TRY(cudaEventSynchronize(c->order_ev[c->order_slot]));  // its last upload has left
+        uint32_t *prev = ord;
+        ord = c->h_order[c->order_slot];
+        if (prev) std::memcpy(ord, prev, n * sizeof(uint32_t));
+        else for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
         for (int64_t i = n; i > 1; --i) {
             uint32_t j = rng.next_below((uint32_t)i);
             std::swap(ord[i - 1], ord[j]);
         }
+        return NASG_OK;
     };
     if (stats) CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), s));
     int64_t cursor = 0;
     for (int step = 0; step < steps; ++step) {
-        if (resh[step]) {
-            CUDA_TRY(cudaStreamSynchronize(s));  // h_order may still be the source of the last upload
-            reshuffle();
+        if (resh[step] && !whole) {
+            r = reshuffle();
+            if (r) return r;
             CUDA_TRY(cudaMemcpyAsync(c->d_order, ord, n * sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+            CUDA_TRY(cudaEventRecord(c->order_ev[c->order_slot], s));
             cursor = 0;
         }
-        r = train_step_impl(c, samples, c->d_order + cursor, local[step], global[step], b, s);
+        r = train_step_impl(c, samples, whole ? nullptr : c->d_order + cursor, local[step], global[step], b, s);
         if (r) return r;
         cursor += local[step];
     }

@@ -325,55 +325,83 @@ __device__ __forceinline__ float dlogk_dlambda(float l, float one_m_emin) {
     return l < 0.05f ? ser : 2.f * (1.f - one_m_emin) * rcp_fast(one_m_emin) - rcp_fast(l);
 }
 
+// Outcome of one row's KL gradient (guiding.cpp:236-257 bookkeeping).
+enum KlStatus : int {
+    kKlZero = 0,  // p == 0: valid sample, zero gradient, zero loss (guiding.cpp:112)
+    kKlOk = 1,    // gradient emitted; loss may still be non-finite (not accumulated)
+    kKlDrop = 2,  // non-finite network row, unusable q, or non-finite gradient: dropped
+};
+
 // One-sample KL gradient w.r.t. the packed raw outputs, fp32 restatement of
 // kl_loss_gradient (guiding.cpp:108-165) + nasg_grad_logpdf (sphdist.cpp:200-274)
-// in one O(N) pass; put(col, g) receives g * gscale for every packed column.
-// Returns false when the sample is dropped; loss = loss_surrogate (:167-176).
-template <int N, class RawFn, class PutFn>
-__device__ __forceinline__ bool kl_grad_row_fast(RawFn raw, const TrainRow &s, float b, float e, float gscale,
-                                                 PutFn put, float &loss) {
-    constexpr int H = packed_header(N), NP = H + 8 * N;
+// in two O(N) passes over the lobes.  The raw row is never held whole:
+//   hdr          packed header columns [0, H) (weight logits, c)
+//   lobe(i, r)   loads lobe i's 8 packed columns (tensor-memory read in the kernel)
+//   put_lobe(i, g) emits lobe i's 8 gradient columns (pass 2, in lobe order)
+//   ghdr         receives the header's gradient columns
+// Gradients carry the 1/count factor gscale.  On kKlOk every column has been
+// emitted; on kKlZero / kKlDrop the caller writes zeros over the whole row
+// (lobe columns may already hold values).  Non-finite raw outputs are checked
+// before p == 0, as the trainer does (guiding.cpp:251-254 precede :112).
+// lobe() is called for every i in both passes whatever the row's outcome (and
+// for rows with valid = false), so a warp-collective load behind it stays
+// convergent; only the arithmetic is predicated.
+template <int N, class LobeFn, class PutLobeFn>
+__device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[packed_header(N)], LobeFn lobe,
+                                                const TrainRow &s, float b, float e, float gscale,
+                                                float (&ghdr)[packed_header(N)], PutLobeFn put_lobe, float &loss) {
+    constexpr int H = packed_header(N);
     loss = 0.f;
-    if (s.p == 0.f) {  // valid cheap path (guiding.cpp:112)
-        static_for<0, NP>([&](auto jc) { put(decltype(jc)::value, 0.f); });
-        return true;
-    }
+    bool fin = true;
+#pragma unroll
+    for (int j = 0; j <= N; ++j) fin &= isfinite(hdr[j]);
     float w[N], c, c_sig;
     {
         float mx = -INFINITY;
 #pragma unroll
-        for (int i = 0; i < N; ++i) mx = fmaxf(mx, raw(i));
+        for (int i = 0; i < N; ++i) mx = fmaxf(mx, hdr[i]);
         float sum = 0.f;
 #pragma unroll
         for (int i = 0; i < N; ++i) {
-            w[i] = __expf(raw(i) - mx);
+            w[i] = __expf(hdr[i] - mx);
             sum += w[i];
         }
         const float inv = rcp_fast(sum);
 #pragma unroll
         for (int i = 0; i < N; ++i) w[i] *= inv;
         float sm;
-        sigmoid_pair(raw(N), c_sig, sm);
+        sigmoid_pair(hdr[N], c_sig, sm);
         c = fminf(fmaxf(c_sig, kSelMin), kSelMax);
     }
+    const bool live = valid && s.p != 0.f;
     float pdf[N];
     float q_mix = 0.f;
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        float r[7];
-        lobe_logits<N>(raw, i, r);
-        Lobe L;
-        decode_lobe(r, L);
-        pdf[i] = __expf(lobe_log_g_at(L, s.wi) - L.log_k);
-        q_mix += w[i] * pdf[i];
+        float r[8];
+        lobe(i, r);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) fin &= isfinite(r[k]);
+        pdf[i] = 0.f;
+        if (live) {
+            Lobe L;
+            decode_lobe(r, L);
+            pdf[i] = __expf(lobe_log_g_at(L, s.wi) - L.log_k);
+            q_mix += w[i] * pdf[i];
+        }
     });
     const float c_eff = b * c;
     const float q_hat = c_eff * q_mix + (1.f - c_eff) * s.pbsdf;
-    if (!(isfinite(q_mix) && q_mix > 0.f && isfinite(q_hat) && q_hat > 0.f) || !(s.q_s > 0.f)) {
-        static_for<0, NP>([&](auto jc) { put(decltype(jc)::value, 0.f); });
+    int status = kKlOk;
+    if (!valid || (fin && !live)) {
+        status = kKlZero;
+    } else if (!fin) {
+        status = kKlDrop;
+    } else if (!(isfinite(q_mix) && q_mix > 0.f && isfinite(q_hat) && q_hat > 0.f) || !(s.q_s > 0.f)) {
         loss = __int_as_float(0x7fc00000);
-        return false;
+        status = kKlDrop;
     }
+    const bool go = status == kKlOk;
     const float ws = s.p / s.q_s;
     const float mix_scale = e * (c_eff * q_mix / q_hat) + (1.f - e);
     const float scale = -ws * mix_scale * gscale;
@@ -383,20 +411,22 @@ __device__ __forceinline__ bool kl_grad_row_fast(RawFn raw, const TrainRow &s, f
         const float dsig = (c != c_sig) ? 0.f : c_sig * (1.f - c_sig);
         const float gc = -ws * e * b * (q_mix - s.pbsdf) / q_hat * dsig * gscale;
         finite &= isfinite(gc);
-        put(N, gc);
-        static_for<N + 1, H>([&](auto jc) { put(decltype(jc)::value, 0.f); });
+        ghdr[N] = gc;
+#pragma unroll
+        for (int j = N + 1; j < H; ++j) ghdr[j] = 0.f;
     }
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
-        float r[7];
-        lobe_logits<N>(raw, i, r);
+        float r[8];
+        lobe(i, r);
+        if (!go) return;
         LobeG G;
         decode_lobe_g(r, G);
         const Lobe &L = G.L;
         const float ri = w[i] * pdf[i] * inv_q;  // posterior responsibility
         const float gl = scale * (ri - w[i]);
         finite &= isfinite(gl);
-        put(i, gl);
+        ghdr[i] = gl;
         // local frame of omega_i (stable fp32 forms, nasg_math.cuh header)
         const float3 v = s.wi;
         const float dz = dot3(v, L.z);
@@ -446,25 +476,22 @@ __device__ __forceinline__ bool kl_grad_row_fast(RawFn raw, const TrainRow &s, f
         }
         const float inv1 = G.pn1 > 0.f ? rcp_fast(G.pn1) : 0.f, inv2 = G.pn2 > 0.f ? rcp_fast(G.pn2) : 0.f;
         const float scl[5] = {1.f, inv1, inv1, inv2, inv2};
+        float g8[8];
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            const float go = scale * g7[k] * scl[k] * 2.f * G.sig[k] * G.sigm[k];
-            finite &= isfinite(go);
-            put(H + 8 * i + k, go);
+            g8[k] = scale * g7[k] * scl[k] * 2.f * G.sig[k] * G.sigm[k];
+            finite &= isfinite(g8[k]);
         }
-        const float gl5 = G.lam_cl ? 0.f : scale * g7[5] * L.lambda;
-        const float gl6 = G.a_cl ? 0.f : scale * g7[6] * L.a;
-        finite &= isfinite(gl5) && isfinite(gl6);
-        put(H + 8 * i + 5, gl5);
-        put(H + 8 * i + 6, gl6);
-        put(H + 8 * i + 7, 0.f);
+        g8[5] = G.lam_cl ? 0.f : scale * g7[5] * L.lambda;
+        g8[6] = G.a_cl ? 0.f : scale * g7[6] * L.a;
+        g8[7] = 0.f;
+        finite &= isfinite(g8[5]) && isfinite(g8[6]);
+        put_lobe(i, g8);
     });
-    if (!finite) {
-        static_for<0, NP>([&](auto jc) { put(decltype(jc)::value, 0.f); });
-        return false;
-    }
+    if (!go) return status;
+    if (!finite) return kKlDrop;
     loss = -ws * (e * __logf(q_hat) + (1.f - e) * __logf(q_mix));
-    return true;
+    return kKlOk;
 }
 
 }  // namespace nasg
