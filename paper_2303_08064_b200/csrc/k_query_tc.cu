@@ -160,9 +160,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         while (tile < ntiles) {
 #pragma unroll 1
             for (int l = 1; l < 4; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
-                tc::mbar_wait(&acc_full[g], acc_ph);
-                acc_ph ^= 1u;
-                tc::tc_fence_after();
+                wg_wait_acc(&acc_full[g], acc_ph, g, warp & 3);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     float v[32];
@@ -181,9 +179,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             // output layer ready: encode the next tile into the (now free) A tile,
             // drain the raw outputs, start the next tile, then run the NASG
             // epilogue of this tile while the tensor core works on the next
-            tc::mbar_wait(&acc_full[g], acc_ph);
-            acc_ph ^= 1u;
-            tc::tc_fence_after();
+            wg_wait_acc(&acc_full[g], acc_ph, g, warp & 3);
             const int64_t next = tile + stride;
             if (next < ntiles) clamped += encode_tile_row(a, next * 128 + t, inv_ext, a_row64);
             float raw[NP];

@@ -37,10 +37,13 @@ __device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, 
                 ++clamped;
                 t = fminf(fmaxf(t, 0.f), 1.f);
             }
+            // exp(-180.5 d^2) = 2^-(u^2), u = (t - c_i) sqrt(180.5 log2 e): FFMA, FMUL, MUFU.EX2
+            constexpr float kS = 16.13711420547236f;
+            const float ts = t * kS;
 #pragma unroll
             for (int i = 0; i < kBins; ++i) {
-                const float d = t - (i + 0.5f) * (1.f / kBins);
-                e[axis * kBins + i] = __expf(-d * d * 180.5f);
+                const float u = ts - (i + 0.5f) * (kS / kBins);
+                e[axis * kBins + i] = tc::ex2_approx(-u * u);
             }
         }
         e[57] = wo.x; e[58] = wo.y; e[59] = wo.z;
@@ -70,5 +73,15 @@ __device__ __forceinline__ int encode_tile_row(const QueryArgs &a, int64_t q, co
 
 // named barrier over the 128 threads of epilogue warpgroup g (id 0 is __syncthreads)
 __device__ __forceinline__ void wg_sync(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
+
+// Wait until warpgroup g's accumulator is complete (its tcgen05.commit arrived):
+// one warp of the group polls the mbarrier, the other three sleep on the group's
+// named barrier instead of spending issue slots on try_wait.
+__device__ __forceinline__ void wg_wait_acc(uint64_t *bar, uint32_t &phase, int g, int warp_in_group) {
+    if (warp_in_group == 0) tc::mbar_wait(bar, phase);
+    wg_sync(g);
+    phase ^= 1u;
+    tc::tc_fence_after();
+}
 
 }  // namespace nasg

@@ -160,6 +160,13 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return r;
 }
 
+// 2^x on the MUFU (flush-to-zero: no denormal range fix-up around it)
+__device__ __forceinline__ float ex2_approx(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // max(x, 0) of both values fused into the bf16 conversion (one F2FP.RELU).
 __device__ __forceinline__ uint32_t pack_bf16x2_relu(float lo, float hi) {
     uint32_t r;
