@@ -92,12 +92,22 @@ __device__ __forceinline__ float sqrt_fast(float x) {
     asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// Branch-free select: both inputs are computed, so a lane-divergent choice
+// between two short formulas does not split the warp into two passes.
+__device__ __forceinline__ float sel(bool c, float a, float b) {
+    float r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %3, 0;\n\tselp.f32 %0, %1, %2, p;\n\t}"
+        : "=f"(r)
+        : "f"(a), "f"(b), "r"((int)c));
+    return r;
+}
+
 // log1p(x), x > -1: 2 atanh(x / (2 + x)) series for |x| < 1/4 (relative error
 // < 1e-7), log(1 + x) from MUFU.LG2 otherwise (|log| > 0.22 there).
 __device__ __forceinline__ float log1p_fast(float x) {
     const float sx = x * rcp_fast(2.f + x), s2 = sx * sx;
     const float ser = 2.f * sx * fmaf(s2, fmaf(s2, fmaf(s2, fmaf(s2, 1.f / 9.f, 1.f / 7.f), 1.f / 5.f), 1.f / 3.f), 1.f);
-    return fabsf(x) < 0.25f ? ser : __logf(1.f + x);
+    return sel(fabsf(x) < 0.25f, ser, __logf(1.f + x));
 }
 // expm1(y): degree-8 Taylor polynomial for |y| < 1/2 (relative error < 1e-8),
 // exp(y) - 1 from MUFU.EX2 otherwise (|result| > 0.39 there).
@@ -109,7 +119,7 @@ __device__ __forceinline__ float expm1_fast(float y) {
     p = fmaf(p, y, 1.f / 6.f);
     p = fmaf(p, y, 0.5f);
     p = fmaf(p, y, 1.f);
-    return fabsf(y) < 0.5f ? p * y : __expf(y) - 1.f;
+    return sel(fabsf(y) < 0.5f, p * y, __expf(y) - 1.f);
 }
 
 // s = 1/(1+e^-r) and 1 - s, both without cancellation.
@@ -147,21 +157,28 @@ __device__ __forceinline__ void decode_lobe(const float r[7], Lobe &L) {
 
 // log G at v (sphdist.cpp:133-140), from local w = 1 - dz, q = 1 + dz, t2.
 __device__ __forceinline__ float lobe_log_g(const Lobe &L, float w, float q, float t2) {
-    float log_u = w < 1.f ? log1p_fast(-0.5f * w) : __logf(0.5f * q);
+    float log_u = sel(w < 1.f, log1p_fast(-0.5f * fminf(w, 1.f)), __logf(0.5f * q));
     log_u = fmaxf(log_u, -27.631021f);  // u >= 1e-12
     const float beta = L.a * t2;
     const float lg = 2.f * L.lambda * expm1_fast((1.f + beta) * log_u) + beta * log_u;
     return q <= 1e-12f ? -INFINITY : lg;  // v = -z sentinel
 }
 
-__device__ __forceinline__ float lobe_log_g_at(const Lobe &L, float3 v) {
+// lobe-local coordinates of v: w = 1 - dz, q = 1 + dz (cancellation-free) and t2
+__device__ __forceinline__ void lobe_local(const Lobe &L, float3 v, float &w, float &q, float &t2) {
     const float dz = dot3(v, L.z);
     const float sg = dz >= 0.f ? 1.f : -1.f;
     const float3 e = make_float3(v.x - sg * L.z.x, v.y - sg * L.z.y, v.z - sg * L.z.z);
     const float h = 0.5f * dot3(e, e);
-    const float w = dz >= 0.f ? h : 2.f - h, q = dz >= 0.f ? 2.f - h : h;
+    w = dz >= 0.f ? h : 2.f - h;
+    q = dz >= 0.f ? 2.f - h : h;
     const float dx = dot3(e, L.x);
-    const float t2 = fminf(fmaxf(dx * dx * rcp_fast(fmaxf(w * q, 1e-12f)), 0.f), 1.f);
+    t2 = fminf(fmaxf(dx * dx * rcp_fast(fmaxf(w * q, 1e-12f)), 0.f), 1.f);
+}
+
+__device__ __forceinline__ float lobe_log_g_at(const Lobe &L, float3 v) {
+    float w, q, t2;
+    lobe_local(L, v, w, q, t2);
     return lobe_log_g(L, w, q, t2);
 }
 
@@ -255,7 +272,12 @@ __device__ __forceinline__ float4 guide_sample(RawFn raw, float4 xi, float &c_ou
         lobe_logits<N>(raw, i, r);
         Lobe L;
         decode_lobe(r, L);
-        const float lg = (i == pick) ? lobe_log_g(L, ws, qs, t2s) : lobe_log_g_at(L, v);
+        // the picked lobe uses the sampler's exact local coordinates; selecting
+        // the inputs (not the evaluation) keeps one log G per lobe per lane
+        float wl, ql, t2l;
+        lobe_local(L, v, wl, ql, t2l);
+        const bool me = i == pick;
+        const float lg = lobe_log_g(L, sel(me, ws, wl), sel(me, qs, ql), sel(me, t2s, t2l));
         pdf += w[i] * __expf(lg - L.log_k);
     });
     return make_float4(v.x, v.y, v.z, pdf);
@@ -440,7 +462,7 @@ __device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[p
         float g7[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d log q / d (ct, sp, cp, st, ctau, lambda, a)
         if (fminf(wl, ql) >= 1e-6f && pdf[i] > 0.f) {      // pole guard sphdist.cpp:205
             const float lam = L.lambda, a = L.a;
-            float log_u = wl < 1.f ? log1p_fast(-0.5f * wl) : __logf(0.5f * ql);
+            float log_u = sel(wl < 1.f, log1p_fast(-0.5f * fminf(wl, 1.f)), __logf(0.5f * ql));
             log_u = fmaxf(log_u, -27.631021f);
             const float u = fmaxf(0.5f * ql, 1e-12f);
             const float beta = a * t2, m = 1.f + beta;
