@@ -1,23 +1,24 @@
 // bf16 tensor-core query path: fused encode -> 64-128-128-128-NP MLP on
 // tcgen05 (UMMA M=128, accumulators in TMEM) -> fp32 NASG epilogue.
 //
-// Persistent CTA per SM, warp-specialised:
-//   warps 0-11  three epilogue warpgroups; warpgroup g owns TMEM columns
-//               [128g, 128g+128) and one 128-row activation tile in smem.
-//               Thread t of the group owns query row t = TMEM lane t.
-//               Per tile: encode (encoding.cpp:21-46) -> bf16 A tile; then for
-//               layers 1-3: TMEM -> regs -> ReLU -> bf16 -> A tile (next
-//               layer's operand); layer 4: TMEM -> 80 raw outputs in
-//               registers -> decode / sample / pdf (nasg_math.cuh).
-//               After writing an A tile the group syncs on its named barrier
-//               and its thread 0 issues that layer's tcgen05.mma chain
-//               (K/16 UMMAs) and tcgen05.commit -> acc_full[g].  The groups
-//               run independently, drift out of phase, and the tensor core
-//               interleaves one group's layers with the others' epilogues;
-//               a tile's NASG epilogue overlaps the next tile's layer 1.
-//   warp 12     TMEM allocator (512 columns) + one thread that TMA-bulk-copies
-//               the 100 KB bf16 weight image into smem once per CTA.
-// Only the 64 B/query of inputs and 16-20 B/query of outputs touch HBM.
+// Persistent CTA per SM (16 warps), warp-specialised into two pipelines
+// ("pairs").  Pair m = one MLP warpgroup + one NASG warpgroup:
+//   MLP warpgroup m (warps 4m..4m+3, 112 registers): per 128-row tile, thread t
+//     owns row t = TMEM lane t.  Load + one-blob encode (encoding.cpp:21-46) ->
+//     bf16 A tile in smem; layers 1-3: thread 0 issues the layer's UMMAs
+//     (K/16 x M128) into the group's TMEM accumulator [128m, 128m+128),
+//     commit -> acc_full[m]; the group drains TMEM -> ReLU -> bf16 -> A tile.
+//     The output layer goes to the pair's raw buffer (TMEM columns
+//     [256+128m, 256+128m+NP)) once the NASG group has emptied it; its commit
+//     arrives on raw_full[m].
+//   NASG warpgroup m (warps 8+4m..11+4m, 144 registers): waits raw_full[m],
+//     copies its rows' NP raw outputs TMEM -> registers, releases the buffer
+//     (raw_empty[m]) and runs decode / sample / pdf (nasg_math.cuh) while the
+//     MLP group already computes the next tile.
+// The MLP side is bound by tensor-core latency, the NASG side by instruction
+// issue; decoupling them lets the two overlap instead of taking turns inside
+// one warpgroup.  setmaxnreg moves registers from the MLP to the NASG groups.
+// Only the 52 B/query of inputs and 16-20 B/query of outputs touch HBM.
 #include <cuda_bf16.h>
 
 #include "nasg_internal.h"
@@ -29,15 +30,15 @@ namespace nasg {
 
 namespace {
 
-constexpr int kWG = 3;                          // epilogue warpgroups
-               // TMEM allocation + weight TMA warp
-constexpr int kThreads = kWG * 128;  // 12 warps: 3 per SMSP -> up to 168 registers        // 416
+constexpr int kPairs = 2;                       // MLP + NASG warpgroup pairs
+constexpr int kThreads = 2 * kPairs * 128;      // 16 warps
+constexpr int kRegsMlp = 112, kRegsNasg = 144;  // 2 x 128 x (112 + 144) = 64K registers
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one bf16 activation tile, K = 128
-constexpr uint32_t kTmemCols = 512;
+constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
 template <int N>
 constexpr size_t smem_bytes() {
-    return align1k(img_bytes(N)) + kWG * kABytes + (kWG + 2) * sizeof(uint64_t);
+    return align1k(img_bytes(N)) + kPairs * kABytes + (3 * kPairs + 2) * sizeof(uint64_t);
 }
 
 }  // namespace
@@ -92,16 +93,27 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     constexpr uint32_t IMG = img_bytes(N);
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + A_OFF + kWG * kABytes);
-    uint64_t *w_bar = acc_full + kWG;
+    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + A_OFF + kPairs * kABytes);
+    uint64_t *raw_full = acc_full + kPairs;
+    uint64_t *raw_empty = raw_full + kPairs;
+    uint64_t *w_bar = raw_empty + kPairs;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     __shared__ int s_clamped;
 
-    const int warp = threadIdx.x >> 5;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = warp >> 2;        // warpgroup 0..3: named barrier g + 1
+    const int m = g & 1;            // pair
+    const int wq = warp & 3;        // TMEM lane quarter of this warp
+    const int t = threadIdx.x & 127;
     const int64_t ntiles = (a.n + 127) / 128;
+    const int64_t stride = (int64_t)gridDim.x * kPairs;
 
     if (threadIdx.x == 0) {
-        for (int g = 0; g < kWG; ++g) tc::mbar_init(&acc_full[g], 1);
+        for (int i = 0; i < kPairs; ++i) {
+            tc::mbar_init(&acc_full[i], 1);
+            tc::mbar_init(&raw_full[i], 1);
+            tc::mbar_init(&raw_empty[i], 4);  // one arrival per NASG warp
+        }
         tc::mbar_init(w_bar, 1);
         s_clamped = 0;
         tc::fence_mbar_init();
@@ -111,60 +123,72 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-
     if (threadIdx.x == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
         tc::mbar_arrive_expect_tx(w_bar, IMG);
         for (uint32_t off = 0; off < IMG; off += 16384)
             tc::bulk_g2s(smem + off, img + off, (IMG - off) < 16384u ? (IMG - off) : 16384u, w_bar);
     }
-    {
-        const int g = warp >> 2, t = threadIdx.x & 127;
-        const uint32_t my_tmem = tmem + g * 128 + ((uint32_t)((warp & 3) * 32) << 16);
-        const uint32_t a_base = tc::smem_u32(smem + A_OFF + g * kABytes);
+
+    if (g < kPairs) {
+        // ============================ MLP warpgroup ============================
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsMlp));
+        const uint32_t my_acc = tmem + m * 128 + ((uint32_t)(wq * 32) << 16);
+        const uint32_t a_base = tc::smem_u32(smem + A_OFF + m * kABytes);
         const uint32_t a_row64 = a_base + (t >> 3) * 1024 + (t & 7) * 16;   // K = 64 layout
         const uint32_t a_row128 = a_base + (t >> 3) * 2048 + (t & 7) * 16;  // K = 128 layout
         const uint32_t sW = tc::smem_u32(smem);
-        // The group's A tile is complete in smem (and its TMEM reads are done):
-        // make it visible to the tensor core, then thread 0 of the group issues
-        // the layer's UMMAs and commits them to acc_full[g].  Each group drives
-        // its own chain, so the three groups drift out of phase and the
-        // tensor core interleaves their layers with the others' epilogues.
-        auto issue = [&](int l) {
-            tc::fence_proxy_async_smem();
-            tc::tc_fence_before();
-            wg_sync(g);
-            if (t == 0) {
-                tc::mbar_wait(w_bar, 0);
-                tc::tc_fence_after();
-                const int K = l == 0 ? kIn : kHidden;
-                const uint32_t sbo = (uint32_t)K * 16u;
-                const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
-                const uint32_t b0 = sW + w_off(l), d = tmem + g * 128;
-                for (int k = 0; k < K / 16; ++k)
-                    tc::mma_bf16(d, tc::smem_desc(a_base + k * 256, 128, sbo), tc::smem_desc(b0 + k * 256, 128, sbo),
-                                 idesc, k > 0 ? 1u : 0u);
-                tc::mma_commit(&acc_full[g]);
-            }
-        };
         float inv_ext[3];
 #pragma unroll
         for (int k = 0; k < 3; ++k) inv_ext[k] = a.bounds.ext[k] > 0.0 ? (float)(1.0 / a.bounds.ext[k]) : 0.f;
         uint32_t acc_ph = 0;
         int clamped = 0;
-        int64_t tile = (int64_t)blockIdx.x * kWG + g;
-        const int64_t stride = (int64_t)gridDim.x * kWG;
-        if (tile < ntiles) {
-            clamped += encode_tile_row(a, tile * 128 + t, inv_ext, a_row64);
-            issue(0);
-        }
-        while (tile < ntiles) {
+        // A tile complete (and our TMEM reads done): thread 0 issues layer l.
+        // Layers 0-2 accumulate into the group's TMEM columns; the output layer
+        // goes to the pair's raw buffer once the NASG group has emptied it.
+        auto issue = [&](int l, int64_t k) {
+            tc::fence_proxy_async_smem();
+            tc::tc_fence_before();
+            wg_sync(g);
+            if (t == 0) {
+                tc::mbar_wait(w_bar, 0);
+                if (l == 3 && k > 0) tc::mbar_wait(&raw_empty[m], (uint32_t)((k - 1) & 1));
+                tc::tc_fence_after();
+                const int K = l == 0 ? kIn : kHidden;
+                const uint32_t sbo = (uint32_t)K * 16u;
+                const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
+                const uint32_t b0 = sW + w_off(l), d = tmem + (l == 3 ? 256 : 0) + m * 128;
+                for (int kk = 0; kk < K / 16; ++kk)
+                    tc::mma_bf16(d, tc::smem_desc(a_base + kk * 256, 128, sbo), tc::smem_desc(b0 + kk * 256, 128, sbo),
+                                 idesc, kk > 0 ? 1u : 0u);
+                tc::mma_commit(l == 3 ? &raw_full[m] : &acc_full[m]);
+            }
+        };
+        // Software pipeline over this group's tiles: the next tile's inputs are
+        // loaded one tile ahead, and its encoding is computed into registers
+        // while the output-layer MMA of the current tile is still reading the
+        // A tile; it is stored once that MMA has completed.
+        float4 nx, nwo, nnrm;  // prefetched inputs of the next tile
+        auto prefetch = [&](int64_t tl) {
+            nx = nwo = nnrm = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int64_t q = tl * 128 + t;
+            if (tl < ntiles && q < a.n) load_query(a, q, nx, nwo, nnrm);
+        };
+        int64_t tile = (int64_t)blockIdx.x * kPairs + m;
+        uint32_t pk[32];
+        prefetch(tile);
+        clamped += encode_row_pack(tile * 128 + t < a.n, nx, nwo, nnrm, a.bounds, inv_ext, pk);
+        prefetch(tile + stride);
+        store_row_pack(pk, a_row64);
+        uint32_t raw_ph = 0;
+        for (int64_t k = 0; tile < ntiles; tile += stride, ++k) {
+            issue(0, k);
 #pragma unroll 1
             for (int l = 1; l < 4; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
-                wg_wait_acc(&acc_full[g], acc_ph, g, warp & 3);
+                wg_wait_acc(&acc_full[m], acc_ph, g, wq);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     float v[32];
-                    tc::tmem_ld32(my_tmem + q4 * 32, v);
+                    tc::tmem_ld32(my_acc + q4 * 32, v);
                     tc::tmem_ld_wait();
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
@@ -174,43 +198,65 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                         tc::st_shared_v4(a_row128 + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
                     }
                 }
-                issue(l);
+                issue(l, k);
             }
-            // output layer ready: encode the next tile into the (now free) A tile,
-            // drain the raw outputs, start the next tile, then run the NASG
-            // epilogue of this tile while the tensor core works on the next
-            wg_wait_acc(&acc_full[g], acc_ph, g, warp & 3);
             const int64_t next = tile + stride;
-            if (next < ntiles) clamped += encode_tile_row(a, next * 128 + t, inv_ext, a_row64);
+            if (next < ntiles) {
+                clamped += encode_row_pack(next * 128 + t < a.n, nx, nwo, nnrm, a.bounds, inv_ext, pk);
+                prefetch(next + stride);
+            }
+            wg_wait_acc(&raw_full[m], raw_ph, g, wq);  // output layer done: the A tile is free
+            if (next < ntiles) store_row_pack(pk, a_row64);
+        }
+        if (clamped) atomicAdd(&s_clamped, clamped);
+    } else {
+        // ============================ NASG warpgroup ===========================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsNasg));
+        const uint32_t my_raw = tmem + 256 + m * 128 + ((uint32_t)(wq * 32) << 16);
+        int64_t k = 0;
+        for (int64_t tile = (int64_t)blockIdx.x * kPairs + m; tile < ntiles; tile += stride, ++k) {
+            const int64_t q = tile * 128 + t;
+            const bool valid = q < a.n;
+            float4 xi = make_float4(0.f, 0.f, 0.f, 0.f), dir = xi;
+            float bsdf = 0.f;
+            if (valid) {  // issued before the wait: the loads land while the MLP finishes
+                if constexpr (MODE == kModeSample) xi = load_xi(a, q);
+                if constexpr (MODE == kModePdf) {
+                    dir = a.dir[q];
+                    bsdf = a.bsdf_pdf ? a.bsdf_pdf[q] : 0.f;
+                }
+            }
+            uint32_t ph = (uint32_t)(k & 1);
+            wg_wait_acc(&raw_full[m], ph, g, wq);
             float raw[NP];
             {
                 float v[32];
 #pragma unroll
-                for (int q = 0; q < NP / 32; ++q) {
-                    tc::tmem_ld32(my_tmem + q * 32, v);
+                for (int i = 0; i < NP / 32; ++i) {
+                    tc::tmem_ld32(my_raw + i * 32, v);
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 32; ++i) raw[q * 32 + i] = v[i];
+                    for (int j = 0; j < 32; ++j) raw[i * 32 + j] = v[j];
                 }
                 if constexpr (NP % 32 != 0) {
                     float u[16];
-                    tc::tmem_ld16(my_tmem + (NP / 32) * 32, u);
+                    tc::tmem_ld16(my_raw + (NP / 32) * 32, u);
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (int i = 0; i < 16; ++i) raw[(NP / 32) * 32 + i] = u[i];
+                    for (int j = 0; j < 16; ++j) raw[(NP / 32) * 32 + j] = u[j];
                 }
             }
-            if (next < ntiles) issue(0);
-            const int64_t q = tile * 128 + t;
-            if (q < a.n) {
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&raw_empty[m]);  // buffer free for the next output layer
+            if (valid) {
                 auto rawf = [&](int j) { return raw[j]; };
                 if constexpr (MODE == kModeSample) {
                     float c;
-                    a.dir_pdf[q] = guide_sample<N>(rawf, load_xi(a, q), c);
+                    a.dir_pdf[q] = guide_sample<N>(rawf, xi, c);
                     if (a.c) a.c[q] = c;
                 } else if constexpr (MODE == kModePdf) {
-                    const float4 d = a.dir[q];
-                    const float2 p = guide_pdf<N>(rawf, make_float3(d.x, d.y, d.z), a.b, a.bsdf_pdf ? a.bsdf_pdf[q] : 0.f);
+                    const float2 p = guide_pdf<N>(rawf, make_float3(dir.x, dir.y, dir.z), a.b, bsdf);
                     if (a.mix_pdf) a.mix_pdf[q] = p.x;
                     if (a.guided_pdf) a.guided_pdf[q] = p.y;
                 } else {
@@ -219,9 +265,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     for (int j = 0; j < D; ++j) a.raw[q * D + j] = raw[packed_col(j, N)];
                 }
             }
-            tile = next;
         }
-        if (clamped) atomicAdd(&s_clamped, clamped);
     }
     tc::tc_fence_before();
     __syncthreads();
@@ -235,7 +279,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 template <int N>
 static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int num_sms, cudaStream_t s) {
     const int64_t ntiles = (a.n + 127) / 128;
-    const int64_t supers = (ntiles + kWG - 1) / kWG;
+    const int64_t supers = (ntiles + kPairs - 1) / kPairs;
     const int grid = (int)(supers < num_sms ? supers : num_sms);
     if (grid == 0) return 0;
     constexpr size_t sm = smem_bytes<N>();

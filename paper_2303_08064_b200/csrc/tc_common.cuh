@@ -21,11 +21,10 @@ __host__ __device__ constexpr uint32_t img_bytes(int n) { return 81920u + (uint3
 __host__ __device__ constexpr uint32_t align1k(uint32_t x) { return (x + 1023u) & ~1023u; }
 
 // --------------------------------------------------------------- encoding --
-// encode_inputs (encoding.cpp:21-46) in fp32, written as bf16 into row t of
-// the K=64 A tile (core-matrix layout); optionally also to `gdst` (a global
-// row block with the same byte layout).  Returns clamped coordinates.
-__device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
-                                               const float (&inv_ext)[3], uint32_t a_row, uint8_t *gdst = nullptr) {
+// encode_inputs (encoding.cpp:21-46) in fp32 -> 64 bf16 features packed in 32
+// registers (pairs in K order).  Returns the number of clamped coordinates.
+__device__ __forceinline__ int encode_row_pack(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
+                                               const float (&inv_ext)[3], uint32_t (&pk)[32]) {
     float e[64];
     int clamped = 0;
     if (valid) {
@@ -54,12 +53,25 @@ __device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, 
         for (int k = 0; k < 64; ++k) e[k] = 0.f;
     }
 #pragma unroll
+    for (int j = 0; j < 32; ++j) pk[j] = tc::pack_bf16x2(e[2 * j], e[2 * j + 1]);
+    return clamped;
+}
+
+// row t's 8 16-byte chunks of the K=64 A tile (core-matrix layout); optionally
+// also to `gdst` (a global row block with the same byte layout)
+__device__ __forceinline__ void store_row_pack(const uint32_t (&pk)[32], uint32_t a_row, uint8_t *gdst = nullptr) {
+#pragma unroll
     for (int c = 0; c < 8; ++c) {
-        const uint32_t p0 = tc::pack_bf16x2(e[8 * c], e[8 * c + 1]), p1 = tc::pack_bf16x2(e[8 * c + 2], e[8 * c + 3]),
-                       p2 = tc::pack_bf16x2(e[8 * c + 4], e[8 * c + 5]), p3 = tc::pack_bf16x2(e[8 * c + 6], e[8 * c + 7]);
-        tc::st_shared_v4(a_row + c * 128, p0, p1, p2, p3);
-        if (gdst) *reinterpret_cast<uint4 *>(gdst + c * 128) = make_uint4(p0, p1, p2, p3);
+        tc::st_shared_v4(a_row + c * 128, pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        if (gdst) *reinterpret_cast<uint4 *>(gdst + c * 128) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
     }
+}
+
+__device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
+                                               const float (&inv_ext)[3], uint32_t a_row, uint8_t *gdst = nullptr) {
+    uint32_t pk[32];
+    const int clamped = encode_row_pack(valid, x, wo, nrm, bd, inv_ext, pk);
+    store_row_pack(pk, a_row, gdst);
     return clamped;
 }
 
