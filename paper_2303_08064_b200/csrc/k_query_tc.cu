@@ -26,6 +26,7 @@
 #include "tc_ptx.cuh"
 #include "tc_common.cuh"
 
+
 namespace nasg {
 
 namespace {
@@ -36,9 +37,11 @@ constexpr int kRegsMlp = 112, kRegsNasg = 144;  // 2 x 128 x (112 + 144) = 64K r
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one bf16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
+constexpr uint32_t kInBytes = 128 * 52;         // one tile of inputs: 13-float rows or 3 x 2 KB SoA
+
 template <int N>
 constexpr size_t smem_bytes() {
-    return align1k(img_bytes(N)) + kPairs * kABytes + (3 * kPairs + 2) * sizeof(uint64_t);
+    return align1k(img_bytes(N)) + kPairs * kABytes + 2 * kPairs * kInBytes + (5 * kPairs + 2) * sizeof(uint64_t);
 }
 
 }  // namespace
@@ -93,10 +96,12 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     constexpr uint32_t IMG = img_bytes(N);
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + A_OFF + kPairs * kABytes);
+    constexpr uint32_t IN_OFF = A_OFF + kPairs * kABytes;  // input staging: [pair][2 buffers]
+    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + IN_OFF + 2 * kPairs * kInBytes);
     uint64_t *raw_full = acc_full + kPairs;
     uint64_t *raw_empty = raw_full + kPairs;
-    uint64_t *w_bar = raw_empty + kPairs;
+    uint64_t *in_full = raw_empty + kPairs;  // [pair][buffer]
+    uint64_t *w_bar = in_full + 2 * kPairs;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     __shared__ int s_clamped;
 
@@ -113,6 +118,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             tc::mbar_init(&acc_full[i], 1);
             tc::mbar_init(&raw_full[i], 1);
             tc::mbar_init(&raw_empty[i], 4);  // one arrival per NASG warp
+            tc::mbar_init(&in_full[2 * i], 1);
+            tc::mbar_init(&in_full[2 * i + 1], 1);
         }
         tc::mbar_init(w_bar, 1);
         s_clamped = 0;
@@ -142,48 +149,100 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         for (int k = 0; k < 3; ++k) inv_ext[k] = a.bounds.ext[k] > 0.0 ? (float)(1.0 / a.bounds.ext[k]) : 0.f;
         uint32_t acc_ph = 0;
         int clamped = 0;
-        // A tile complete (and our TMEM reads done): thread 0 issues layer l.
-        // Layers 0-2 accumulate into the group's TMEM columns; the output layer
-        // goes to the pair's raw buffer once the NASG group has emptied it.
-        auto issue = [&](int l, int64_t k) {
+        // A tile complete (and our TMEM reads done): warp 0 of the group issues
+        // layer L (compile-time) with one elected lane.  Layers 0-2 accumulate
+        // into the group's TMEM columns; the output layer goes to the pair's raw
+        // buffer once the NASG group has emptied it.
+        auto issue = [&](auto lc, int64_t k) {
+            constexpr int L = decltype(lc)::value;
             tc::fence_proxy_async_smem();
             tc::tc_fence_before();
             wg_sync(g);
-            if (t == 0) {
-                tc::mbar_wait(w_bar, 0);
-                if (l == 3 && k > 0) tc::mbar_wait(&raw_empty[m], (uint32_t)((k - 1) & 1));
+            if (wq == 0) {
+                __syncwarp();
+                if (L == 3 && k > 0) tc::mbar_wait(&raw_empty[m], (uint32_t)((k - 1) & 1));
                 tc::tc_fence_after();
-                const int K = l == 0 ? kIn : kHidden;
-                const uint32_t sbo = (uint32_t)K * 16u;
-                const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
-                const uint32_t b0 = sW + w_off(l), d = tmem + (l == 3 ? 256 : 0) + m * 128;
-                for (int kk = 0; kk < K / 16; ++kk)
-                    tc::mma_bf16(d, tc::smem_desc(a_base + kk * 256, 128, sbo), tc::smem_desc(b0 + kk * 256, 128, sbo),
-                                 idesc, kk > 0 ? 1u : 0u);
-                tc::mma_commit(l == 3 ? &raw_full[m] : &acc_full[m]);
+                constexpr int K = L == 0 ? kIn : kHidden;
+                constexpr uint32_t idesc = tc::idesc_bf16(128, L == 3 ? NP : kHidden);
+                const uint64_t ad = tc::smem_desc(a_base, 128, K * 16), bd = tc::smem_desc(sW + w_off(L), 128, K * 16);
+                const uint32_t d = tmem + (L == 3 ? 256 : 0) + m * 128;
+#pragma unroll
+                for (int kk = 0; kk < K / 16; ++kk)  // +256 B per K=16 slab = +16 in the address field
+                    tc::mma_bf16_elect(d, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc, kk > 0 ? 1u : 0u);
+                tc::mma_commit_elect(L == 3 ? &raw_full[m] : &acc_full[m]);
             }
         };
-        // Software pipeline over this group's tiles: the next tile's inputs are
-        // loaded one tile ahead, and its encoding is computed into registers
-        // while the output-layer MMA of the current tile is still reading the
-        // A tile; it is stored once that MMA has completed.
-        float4 nx, nwo, nnrm;  // prefetched inputs of the next tile
-        auto prefetch = [&](int64_t tl) {
-            nx = nwo = nnrm = make_float4(0.f, 0.f, 0.f, 0.f);
+        // Software pipeline over this group's tiles.  Inputs arrive two tiles
+        // ahead by TMA bulk copies into a double-buffered smem stage (an
+        // async-proxy load is not held up by the fence before each MMA issue,
+        // unlike a register prefetch); the next tile's encoding is computed into
+        // registers while the output-layer MMA of the current tile still reads
+        // the A tile, and stored once that MMA has completed.
+        const bool tma_in = a.packed ? ((reinterpret_cast<uintptr_t>(a.packed) & 15) == 0) : true;
+        auto load_tile = [&](int64_t tl, int buf) {  // thread 0 only
+            if (tl >= ntiles) return;
+            const int64_t q0 = tl * 128, rows = min((int64_t)128, a.n - q0);
+            uint64_t *bar = &in_full[2 * m + buf];
+            uint8_t *dst = smem + IN_OFF + (2 * m + buf) * kInBytes;
+            if (!tma_in) {
+                tc::mbar_arrive_expect_tx(bar, 0);
+            } else if (a.packed) {
+                const uint32_t bytes = (uint32_t)(rows * 52) & ~15u;
+                tc::mbar_arrive_expect_tx(bar, bytes);
+                if (bytes) tc::bulk_g2s(dst, a.packed + q0 * 13, bytes, bar);
+            } else {
+                const uint32_t bytes = (uint32_t)rows * 16u;
+                tc::mbar_arrive_expect_tx(bar, 3 * bytes);
+                tc::bulk_g2s(dst, a.x + q0, bytes, bar);
+                tc::bulk_g2s(dst + 2048, a.wo + q0, bytes, bar);
+                tc::bulk_g2s(dst + 4096, a.nrm + q0, bytes, bar);
+            }
+        };
+        auto encode = [&](int64_t tl, int64_t kt, uint32_t (&pk)[32]) {  // tile tl = this group's kt-th
+            const int buf = (int)(kt & 1);
+            tc::mbar_wait(&in_full[2 * m + buf], (uint32_t)((kt >> 1) & 1));
             const int64_t q = tl * 128 + t;
-            if (tl < ntiles && q < a.n) load_query(a, q, nx, nwo, nnrm);
+            const bool valid = q < a.n;
+            float4 x = make_float4(0.f, 0.f, 0.f, 0.f), wo = x, nrm = x;
+            const uint8_t *src = smem + IN_OFF + (2 * m + buf) * kInBytes;
+            if (valid) {
+                if (!tma_in) {
+                    load_query(a, q, x, wo, nrm);
+                } else if (a.packed) {
+                    const int64_t rows = min((int64_t)128, a.n - tl * 128);
+                    if ((uint32_t)(t * 52 + 52) <= ((uint32_t)(rows * 52) & ~15u)) {
+                        const float *p = reinterpret_cast<const float *>(src + t * 52);
+                        x = make_float4(p[0], p[1], p[2], 0.f);
+                        wo = make_float4(p[3], p[4], p[5], 0.f);
+                        nrm = make_float4(p[6], p[7], p[8], 0.f);
+                    } else {
+                        load_query(a, q, x, wo, nrm);  // tail rows past the 16-byte-rounded copy
+                    }
+                } else {
+                    x = *reinterpret_cast<const float4 *>(src + t * 16);
+                    wo = *reinterpret_cast<const float4 *>(src + 2048 + t * 16);
+                    nrm = *reinterpret_cast<const float4 *>(src + 4096 + t * 16);
+                }
+            }
+            return encode_row_pack(valid, x, wo, nrm, a.bounds, inv_ext, pk);
         };
         int64_t tile = (int64_t)blockIdx.x * kPairs + m;
         uint32_t pk[32];
-        prefetch(tile);
-        clamped += encode_row_pack(tile * 128 + t < a.n, nx, nwo, nnrm, a.bounds, inv_ext, pk);
-        prefetch(tile + stride);
-        store_row_pack(pk, a_row64);
+        if (wq == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
+        if (t == 0) {
+            load_tile(tile, 0);
+            load_tile(tile + stride, 1);
+        }
+        if (tile < ntiles) {
+            clamped += encode(tile, 0, pk);
+            store_row_pack(pk, a_row64);
+        }
         uint32_t raw_ph = 0;
         for (int64_t k = 0; tile < ntiles; tile += stride, ++k) {
-            issue(0, k);
-#pragma unroll 1
-            for (int l = 1; l < 4; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
+            issue(std::integral_constant<int, 0>{}, k);
+            if (t == 0) load_tile(tile + 2 * stride, (int)(k & 1));  // its buffer was read by encode(k)
+            static_for<1, 4>([&](auto lc) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
+                constexpr int l = decltype(lc)::value;
                 wg_wait_acc(&acc_full[m], acc_ph, g, wq);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
@@ -198,13 +257,10 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                         tc::st_shared_v4(a_row128 + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
                     }
                 }
-                issue(l, k);
-            }
+                issue(lc, k);
+            });
             const int64_t next = tile + stride;
-            if (next < ntiles) {
-                clamped += encode_row_pack(next * 128 + t < a.n, nx, nwo, nnrm, a.bounds, inv_ext, pk);
-                prefetch(next + stride);
-            }
+            if (next < ntiles) clamped += encode(next, k + 1, pk);
             wg_wait_acc(&raw_full[m], raw_ph, g, wq);  // output layer done: the A tile is free
             if (next < ntiles) store_row_pack(pk, a_row64);
         }
