@@ -144,17 +144,14 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         const uint32_t a_row64 = a_base + (t >> 3) * 1024 + (t & 7) * 16;   // K = 64 layout
         const uint32_t a_row128 = a_base + (t >> 3) * 2048 + (t & 7) * 16;  // K = 128 layout
         const uint32_t sW = tc::smem_u32(smem);
-        float inv_ext[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) inv_ext[k] = a.bounds.ext[k] > 0.0 ? (float)(1.0 / a.bounds.ext[k]) : 0.f;
+        const float(&inv_ext)[3] = a.bounds.inv_ext;
         uint32_t acc_ph = 0;
         int clamped = 0;
         // A tile complete (and our TMEM reads done): warp 0 of the group issues
         // layer L (compile-time) with one elected lane.  Layers 0-2 accumulate
         // into the group's TMEM columns; the output layer goes to the pair's raw
         // buffer once the NASG group has emptied it.
-        auto issue = [&](auto lc, int64_t k) {
-            constexpr int L = decltype(lc)::value;
+        auto issue = [&](int L, int64_t k) {
             tc::fence_proxy_async_smem();
             tc::tc_fence_before();
             wg_sync(g);
@@ -162,14 +159,25 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 __syncwarp();
                 if (L == 3 && k > 0) tc::mbar_wait(&raw_empty[m], (uint32_t)((k - 1) & 1));
                 tc::tc_fence_after();
-                constexpr int K = L == 0 ? kIn : kHidden;
-                constexpr uint32_t idesc = tc::idesc_bf16(128, L == 3 ? NP : kHidden);
-                const uint64_t ad = tc::smem_desc(a_base, 128, K * 16), bd = tc::smem_desc(sW + w_off(L), 128, K * 16);
-                const uint32_t d = tmem + (L == 3 ? 256 : 0) + m * 128;
+                auto chain = [&](auto lc) {
+                    constexpr int LL = decltype(lc)::value;
+                    constexpr int K = LL == 0 ? kIn : kHidden;
+                    constexpr uint32_t idesc = tc::idesc_bf16(128, LL == 3 ? NP : kHidden);
+                    const uint64_t ad = tc::smem_desc(a_base, 128, K * 16);
+                    const uint64_t bd = tc::smem_desc(sW + w_off(LL), 128, K * 16);
+                    const uint32_t d = tmem + (LL == 3 ? 256 : 0) + m * 128;
 #pragma unroll
-                for (int kk = 0; kk < K / 16; ++kk)  // +256 B per K=16 slab = +16 in the address field
-                    tc::mma_bf16_elect(d, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc, kk > 0 ? 1u : 0u);
-                tc::mma_commit_elect(L == 3 ? &raw_full[m] : &acc_full[m]);
+                    for (int kk = 0; kk < K / 16; ++kk)  // +256 B per K=16 slab = +16 in the address field
+                        tc::mma_bf16_elect(d, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc,
+                                           kk > 0 ? 1u : 0u);
+                    tc::mma_commit_elect(LL == 3 ? &raw_full[m] : &acc_full[m]);
+                };
+                switch (L) {
+                    case 0: chain(std::integral_constant<int, 0>{}); break;
+                    case 1: chain(std::integral_constant<int, 1>{}); break;
+                    case 2: chain(std::integral_constant<int, 2>{}); break;
+                    default: chain(std::integral_constant<int, 3>{}); break;
+                }
             }
         };
         // Software pipeline over this group's tiles.  Inputs arrive two tiles
@@ -226,43 +234,46 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             }
             return encode_row_pack(valid, x, wo, nrm, a.bounds, inv_ext, pk);
         };
-        int64_t tile = (int64_t)blockIdx.x * kPairs + m;
+        // One loop with a single encode site (k = -1 only encodes the first
+        // tile): the kernel's two roles run concurrently, so code size matters
+        // for the instruction cache.
         uint32_t pk[32];
         if (wq == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
+        int64_t tile = (int64_t)blockIdx.x * kPairs + m - stride;
         if (t == 0) {
-            load_tile(tile, 0);
-            load_tile(tile + stride, 1);
-        }
-        if (tile < ntiles) {
-            clamped += encode(tile, 0, pk);
-            store_row_pack(pk, a_row64);
+            load_tile(tile + stride, 0);
+            load_tile(tile + 2 * stride, 1);
         }
         uint32_t raw_ph = 0;
-        for (int64_t k = 0; tile < ntiles; tile += stride, ++k) {
-            issue(std::integral_constant<int, 0>{}, k);
-            if (t == 0) load_tile(tile + 2 * stride, (int)(k & 1));  // its buffer was read by encode(k)
-            static_for<1, 4>([&](auto lc) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
-                constexpr int l = decltype(lc)::value;
-                wg_wait_acc(&acc_full[m], acc_ph, g, wq);
+        for (int64_t k = -1;; tile += stride, ++k) {
+            if (k >= 0) {
+                issue(0, k);
+                if (t == 0) load_tile(tile + 2 * stride, (int)(k & 1));  // its buffer was read by encode(k)
+#pragma unroll 1
+                for (int l = 1; l < 4; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
+                    wg_wait_acc(&acc_full[m], acc_ph, g, wq);
 #pragma unroll
-                for (int q4 = 0; q4 < 4; ++q4) {
-                    float v[32];
-                    tc::tmem_ld32(my_acc + q4 * 32, v);
-                    tc::tmem_ld_wait();
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        float v[32];
+                        tc::tmem_ld32(my_acc + q4 * 32, v);
+                        tc::tmem_ld_wait();
 #pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        uint32_t p[4];
+                        for (int c = 0; c < 4; ++c) {
+                            uint32_t p[4];
 #pragma unroll
-                        for (int h = 0; h < 4; ++h) p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
-                        tc::st_shared_v4(a_row128 + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                            for (int h = 0; h < 4; ++h)
+                                p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                            tc::st_shared_v4(a_row128 + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                        }
                     }
+                    issue(l, k);
                 }
-                issue(lc, k);
-            });
+            }
             const int64_t next = tile + stride;
             if (next < ntiles) clamped += encode(next, k + 1, pk);
-            wg_wait_acc(&raw_full[m], raw_ph, g, wq);  // output layer done: the A tile is free
-            if (next < ntiles) store_row_pack(pk, a_row64);
+            if (k >= 0) wg_wait_acc(&raw_full[m], raw_ph, g, wq);  // output layer done: the A tile is free
+            if (next >= ntiles) break;
+            store_row_pack(pk, a_row64);
         }
         if (clamped) atomicAdd(&s_clamped, clamped);
     } else {

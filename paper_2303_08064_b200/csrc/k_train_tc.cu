@@ -126,9 +126,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         };
         uint32_t acc_ph = 0;
         auto wait_acc = [&]() { wg_wait_acc(&acc_full[g], acc_ph, g, warp & 3); };
-        float inv_ext[3];
-#pragma unroll
-        for (int k = 0; k < 3; ++k) inv_ext[k] = bd.ext[k] > 0.0 ? (float)(1.0 / bd.ext[k]) : 0.f;
+        const float(&inv_ext)[3] = bd.inv_ext;
         int clamped = 0;
         const int64_t stride = (int64_t)gridDim.x * kWGt;
         float4 s0, s1, s2, s3;  // this row's sample; the next tile's is prefetched after the KL

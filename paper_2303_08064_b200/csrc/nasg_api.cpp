@@ -381,6 +381,7 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
         c->bounds.bmin[k] = bmin[k];
         c->bmax[k] = bmax[k];
         c->bounds.ext[k] = (double)bmax[k] - (double)bmin[k];
+        c->bounds.inv_ext[k] = c->bounds.ext[k] > 0.0 ? (float)(1.0 / c->bounds.ext[k]) : 0.f;
     }
     auto cleanup_fail = [&](int code) {
         nasg_destroy(c);

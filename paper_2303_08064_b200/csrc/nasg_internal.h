@@ -30,7 +30,8 @@ __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHi
 
 struct Bounds {
     float bmin[3];
-    double ext[3];  // bmax - bmin in double (Aabb::extent, math.hpp:70)
+    double ext[3];      // bmax - bmin in double (Aabb::extent, math.hpp:70)
+    float inv_ext[3];   // (float)(1 / ext), 0 for a degenerate axis (fp32 encoders)
 };
 
 // ---- kernels: packing -------------------------------------------------------
