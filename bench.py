@@ -289,6 +289,23 @@ def main():
         g.query_sample_host(*host, dir_pdf=hout, c=hc)
     te = max_over_ranks(time.perf_counter() - t0, ws)
     e2e["soa_float4_api"] = {"value": n * ws * e2e_steps / te, "h2d_bytes_per_step": n * 64 * ws}
+    # the e2e path's own roofline: pinned host -> device copy bandwidth of this box
+    # (same byte count as one step's H2D, CUDA events, best of 3)
+    hbuf = torch.from_numpy(q13.reshape(-1).view(np.uint8))
+    dbuf = torch.empty(hbuf.numel(), dtype=torch.uint8, device="cuda")
+    best = float("inf")
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        dbuf.copy_(hbuf, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    h2d_gbs = hbuf.numel() / best / 1e9
+    e2e["pcie_h2d_gbs_measured"] = h2d_gbs
+    e2e["h2d_roofline_queries_per_s"] = h2d_gbs * 1e9 / 52 * ws
+    e2e["frac_of_h2d_roofline"] = e2e["value"] / e2e["h2d_roofline_queries_per_s"]
+    del dbuf, hbuf
     g.close()
     del dev, out, cbuf
     torch.cuda.empty_cache()
