@@ -127,6 +127,23 @@ int nasg_query_sample_packed(nasg_ctx *ctx, int64_t n, const float *q13, float *
 int nasg_query_pdf(nasg_ctx *ctx, int64_t n, const float *x, const float *wo, const float *nrm,
                    const float *dir, float b, const float *bsdf_pdf, float *mix_pdf,
                    float *guided_pdf, void *stream);
+/* Guided scattering for a wavefront path tracer (SPEC.md tracer trace_path:
+ * "scattering direction drawn from q-hat (mixture sample with probability c',
+ * BSDF otherwise; pdf always the full blend)", guided_pdf guiding.cpp:81-85,
+ * mixture_sample sphdist.cpp:183-198).  One network evaluation per vertex:
+ *   in   x, wo, nrm, xi (n x float4 each, as nasg_query_sample)
+ *        d_bsdf  n x float4: the caller's BSDF-sampled direction xyz, w = xi_t
+ *        d_nee   n x float4: the NEE direction xyz, w > 0 when present
+ *   out  out     2n x float4: [2i]   = (chosen direction xyz, q_mix there)
+ *                             [2i+1] = (q_mix(d_nee) or 0, c' = b c,
+ *                                       1 if the mixture was sampled else 0, c)
+ * The blend pdf the renderer needs is c' q_mix + (1 - c') p_bsdf at each
+ * direction (p_bsdf from its own material).  n_dev (nullable): a device int
+ * read by the kernel as the row count (min with n), so a queue filled on the
+ * device needs no host round trip; n is then the capacity. */
+int nasg_query_shade(nasg_ctx *ctx, int64_t n, const int *n_dev, const float *x, const float *wo,
+                     const float *nrm, const float *xi, const float *d_bsdf, const float *d_nee, float b,
+                     float *out, void *stream);
 /* encode_inputs + forward (infer_guide without decode): raw outputs in the
  * reference order, n x (8N+1).  Parity entry for the MLP. */
 int nasg_query_raw(nasg_ctx *ctx, int64_t n, const float *x, const float *wo, const float *nrm,

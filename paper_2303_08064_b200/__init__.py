@@ -93,6 +93,7 @@ def lib():
         "nasg_query_sample": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp]),
         "nasg_query_pdf": (i32, [vp, i64, vp, vp, vp, vp, f32, vp, vp, vp, vp]),
         "nasg_query_raw": (i32, [vp, i64, vp, vp, vp, vp, vp]),
+        "nasg_query_shade": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp, f32, vp, vp]),
         "nasg_decode_sample_raw": (i32, [vp, i64, vp, vp, vp, vp, vp]),
         "nasg_decode_pdf_raw": (i32, [vp, i64, vp, vp, f32, vp, vp, vp, vp]),
         "nasg_query_sample_host": (i32, [vp, i64, vp, vp, vp, vp, vp, vp]),
@@ -316,6 +317,16 @@ class Guide:
         _check(lib().nasg_query_pdf(self._h, n, _ptr(x), _ptr(wo), _ptr(nrm), _ptr(dirs), float(b), _ptr(bsdf_pdf),
                                     _ptr(mix), _ptr(guided), _stream(stream)))
         return mix, guided
+
+    def query_shade(self, x, wo, nrm, xi, d_bsdf, d_nee, b, n_dev=None, stream=None):
+        """Guided scattering at path vertices (nasg_query_shade): returns (n, 2, 4)
+        [(dir xyz, q_mix(dir)), (q_mix(nee), c', guided, c)]."""
+        import torch
+        n = x.shape[0]
+        out = torch.empty((n, 2, 4), dtype=torch.float32, device=x.device)
+        _check(lib().nasg_query_shade(self._h, n, _ptr(n_dev), _ptr(x), _ptr(wo), _ptr(nrm), _ptr(xi), _ptr(d_bsdf),
+                                      _ptr(d_nee), float(b), _ptr(out), _stream(stream)))
+        return out
 
     def query_raw(self, x, wo, nrm, stream=None):
         import torch

@@ -91,7 +91,8 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
     float *wbuf = actB + kHidden * kLda;     // [2][16][128]
     __shared__ int s_clamped;
     const int tid = threadIdx.x;
-    const int64_t ntiles = (a.n + kTileRows - 1) / kTileRows;
+    const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
+    const int64_t ntiles = (nrows + kTileRows - 1) / kTileRows;
     const float *W1 = wp, *W2 = W1 + kIn * kHidden, *W3 = W2 + kHidden * kHidden,
                 *W4 = W3 + kHidden * kHidden;
     if (tid == 0) s_clamped = 0;
@@ -100,7 +101,7 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
         const int64_t row0 = tile * kTileRows;
         if (tid < kTileRows) {
             const int64_t q = row0 + tid;
-            if (q < a.n) {
+            if (q < nrows) {
                 float4 qx, qwo, qn;
                 load_query(a, q, qx, qwo, qn);
                 int cl = encode_row(qx, qwo, qn, a.bounds, actA, tid);
@@ -116,7 +117,7 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
         tile_layer<128, kHidden, kEpiNone>(actB, actA, W4, wbuf, nullptr, tid);
         if (tid < kTileRows) {
             const int64_t q = row0 + tid;
-            if (q < a.n) {
+            if (q < nrows) {
                 const float *col = actA + tid;
                 auto raw = [&](int j) { return col[j * kLda]; };
                 if (MODE == kModeSample) {
@@ -129,6 +130,11 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
                                                   a.bsdf_pdf ? a.bsdf_pdf[q] : 0.f);
                     if (a.mix_pdf) a.mix_pdf[q] = p.x;
                     if (a.guided_pdf) a.guided_pdf[q] = p.y;
+                } else if (MODE == kModeShade) {
+                    float4 o0, o1;
+                    ref::guide_shade<N>(raw, load_xi(a, q), a.b, a.sh_bsdf[q], a.sh_nee[q], o0, o1);
+                    a.sh_out[2 * q] = o0;
+                    a.sh_out[2 * q + 1] = o1;
                 } else {
                     constexpr int D = 8 * N + 1;
                     for (int j = 0; j < D; ++j) a.raw[q * D + j] = raw(packed_col(j, N));
@@ -158,6 +164,7 @@ static int query_fp32_n(QueryMode mode, const float *wp, const QueryArgs &a, int
         NASG_LAUNCH(kModeSample)
         NASG_LAUNCH(kModePdf)
         NASG_LAUNCH(kModeRaw)
+        NASG_LAUNCH(kModeShade)
 #undef NASG_LAUNCH
     }
     return 1;

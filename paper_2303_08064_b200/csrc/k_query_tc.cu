@@ -110,7 +110,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     const int m = g & 1;            // pair
     const int wq = warp & 3;        // TMEM lane quarter of this warp
     const int t = threadIdx.x & 127;
-    const int64_t ntiles = (a.n + 127) / 128;
+    const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
+    const int64_t ntiles = (nrows + 127) / 128;
     const int64_t stride = (int64_t)gridDim.x * kPairs;
 
     if (threadIdx.x == 0) {
@@ -189,7 +190,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         const bool tma_in = a.packed ? ((reinterpret_cast<uintptr_t>(a.packed) & 15) == 0) : true;
         auto load_tile = [&](int64_t tl, int buf) {  // thread 0 only
             if (tl >= ntiles) return;
-            const int64_t q0 = tl * 128, rows = min((int64_t)128, a.n - q0);
+            const int64_t q0 = tl * 128, rows = min((int64_t)128, nrows - q0);
             uint64_t *bar = &in_full[2 * m + buf];
             uint8_t *dst = smem + IN_OFF + (2 * m + buf) * kInBytes;
             if (!tma_in) {
@@ -210,14 +211,14 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             const int buf = (int)(kt & 1);
             tc::mbar_wait(&in_full[2 * m + buf], (uint32_t)((kt >> 1) & 1));
             const int64_t q = tl * 128 + t;
-            const bool valid = q < a.n;
+            const bool valid = q < nrows;
             float4 x = make_float4(0.f, 0.f, 0.f, 0.f), wo = x, nrm = x;
             const uint8_t *src = smem + IN_OFF + (2 * m + buf) * kInBytes;
             if (valid) {
                 if (!tma_in) {
                     load_query(a, q, x, wo, nrm);
                 } else if (a.packed) {
-                    const int64_t rows = min((int64_t)128, a.n - tl * 128);
+                    const int64_t rows = min((int64_t)128, nrows - tl * 128);
                     if ((uint32_t)(t * 52 + 52) <= ((uint32_t)(rows * 52) & ~15u)) {
                         const float *p = reinterpret_cast<const float *>(src + t * 52);
                         x = make_float4(p[0], p[1], p[2], 0.f);
@@ -283,11 +284,15 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         int64_t k = 0;
         for (int64_t tile = (int64_t)blockIdx.x * kPairs + m; tile < ntiles; tile += stride, ++k) {
             const int64_t q = tile * 128 + t;
-            const bool valid = q < a.n;
-            float4 xi = make_float4(0.f, 0.f, 0.f, 0.f), dir = xi;
+            const bool valid = q < nrows;
+            float4 xi = make_float4(0.f, 0.f, 0.f, 0.f), dir = xi, dnee = xi;
             float bsdf = 0.f;
             if (valid) {  // issued before the wait: the loads land while the MLP finishes
-                if constexpr (MODE == kModeSample) xi = load_xi(a, q);
+                if constexpr (MODE == kModeSample || MODE == kModeShade) xi = load_xi(a, q);
+                if constexpr (MODE == kModeShade) {
+                    dir = a.sh_bsdf[q];
+                    dnee = a.sh_nee[q];
+                }
                 if constexpr (MODE == kModePdf) {
                     dir = a.dir[q];
                     bsdf = a.bsdf_pdf ? a.bsdf_pdf[q] : 0.f;
@@ -326,6 +331,11 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     const float2 p = guide_pdf<N>(rawf, make_float3(dir.x, dir.y, dir.z), a.b, bsdf);
                     if (a.mix_pdf) a.mix_pdf[q] = p.x;
                     if (a.guided_pdf) a.guided_pdf[q] = p.y;
+                } else if constexpr (MODE == kModeShade) {
+                    float4 o0, o1;
+                    guide_shade<N>(rawf, xi, a.b, dir, dnee, o0, o1);
+                    a.sh_out[2 * q] = o0;
+                    a.sh_out[2 * q + 1] = o1;
                 } else {
                     constexpr int D = 8 * N + 1;
 #pragma unroll
@@ -362,6 +372,7 @@ static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int n
         NASG_LAUNCH_TC(kModeSample)
         NASG_LAUNCH_TC(kModePdf)
         NASG_LAUNCH_TC(kModeRaw)
+        NASG_LAUNCH_TC(kModeShade)
 #undef NASG_LAUNCH_TC
     }
     return 1;

@@ -631,6 +631,17 @@ int nasg_query_pdf(nasg_ctx *c, int64_t n, const float *x, const float *wo, cons
     return run_query(c, kModePdf, a, pick(c, stream));
 }
 
+int nasg_query_shade(nasg_ctx *c, int64_t n, const int *n_dev, const float *x, const float *wo, const float *nrm,
+                     const float *xi, const float *d_bsdf, const float *d_nee, float b, float *out, void *stream) {
+    if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !xi || !d_bsdf || !d_nee || !out)))
+        return fail(NASG_ERR_INVALID, "bad argument");
+    QueryArgs a = base_args(c, n);
+    a.x = (const float4 *)x; a.wo = (const float4 *)wo; a.nrm = (const float4 *)nrm; a.xi = (const float4 *)xi;
+    a.n_dev = n_dev; a.b = b;
+    a.sh_bsdf = (const float4 *)d_bsdf; a.sh_nee = (const float4 *)d_nee; a.sh_out = (float4 *)out;
+    return run_query(c, kModeShade, a, pick(c, stream));
+}
+
 int nasg_query_raw(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, float *raw,
                    void *stream) {
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !raw))) return fail(NASG_ERR_INVALID, "bad argument");

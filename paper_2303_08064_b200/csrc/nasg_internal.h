@@ -41,7 +41,7 @@ size_t tc_image_bytes(int n_comp);
 void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s);
 
 // ---- kernels: queries -------------------------------------------------------
-enum QueryMode { kModeSample = 0, kModePdf = 1, kModeRaw = 2 };
+enum QueryMode { kModeSample = 0, kModePdf = 1, kModeRaw = 2, kModeShade = 3 };
 
 struct QueryArgs {
     int64_t n;
@@ -59,6 +59,12 @@ struct QueryArgs {
     // optional packed host format: 13 floats per query = position, omega_o,
     // normal (3 each) and xi (4); replaces x / wo / nrm / xi when non-null
     const float *packed;
+    // optional device-side row count (a wavefront queue): rows = min(*n_dev, n)
+    const int *n_dev;
+    // shade mode (guided scattering at path vertices): BSDF sample + xi_t, NEE
+    // direction + flag in; two float4 per row out (see guide_shade)
+    const float4 *sh_bsdf, *sh_nee;
+    float4 *sh_out;
 };
 
 #ifdef __CUDACC__

@@ -301,6 +301,62 @@ __device__ __forceinline__ float2 guide_pdf(RawFn raw, float3 v, float b, float 
     return make_float2(pdf, ce <= 0.f ? bsdf_pdf : ce * pdf + (1.f - ce) * bsdf_pdf);
 }
 
+// Guided scattering at one path vertex (SPEC tracer trace_path; guided_pdf
+// guiding.cpp:81-85): c' = b c; with probability c' (xi_t = dbsdf.w < c') the
+// direction is the mixture sample (mixture_sample sphdist.cpp:183-198), else the
+// caller's BSDF sample dbsdf.xyz.  One pass over the lobes evaluates the
+// mixture pdf at the chosen direction and at the NEE direction dnee.xyz (the
+// NEE pdf comes from the same network evaluation).
+//   o0 = (dir, q_mix(dir)),  o1 = (q_mix(nee) or 0 if dnee.w <= 0, c', guided ? 1 : 0, c)
+template <int N, class RawFn>
+__device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float4 dbsdf, float4 dnee, float4 &o0,
+                                            float4 &o1) {
+    float w[N], c;
+    decode_header<N>(raw, w, c);
+    const float ce = b * c;
+    const bool tech = dbsdf.w < ce;
+    int pick = N - 1;
+    bool found = false;
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        acc += w[i];
+        const bool hit = !found && xi.x < acc;
+        pick = hit ? i : pick;
+        found |= hit;
+    }
+    float rs[7];
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        float r[7];
+        lobe_logits<N>(raw, i, r);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) rs[k] = (i == 0 || i == pick) ? r[k] : rs[k];
+    });
+    Lobe Ls;
+    decode_lobe(rs, Ls);
+    float ws, qs, t2s;
+    const float3 vm = sample_lobe(Ls, xi.y, xi.z, xi.w, ws, qs, t2s);
+    const float3 v = make_float3(sel(tech, vm.x, dbsdf.x), sel(tech, vm.y, dbsdf.y), sel(tech, vm.z, dbsdf.z));
+    const float3 vn = make_float3(dnee.x, dnee.y, dnee.z);
+    float pv = 0.f, pn = 0.f;
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        float r[7];
+        lobe_logits<N>(raw, i, r);
+        Lobe L;
+        decode_lobe(r, L);
+        float wl, ql, t2l;
+        lobe_local(L, v, wl, ql, t2l);
+        const bool me = tech && i == pick;
+        pv += w[i] * __expf(lobe_log_g(L, sel(me, ws, wl), sel(me, qs, ql), sel(me, t2s, t2l)) - L.log_k);
+        lobe_local(L, vn, wl, ql, t2l);
+        pn += w[i] * __expf(lobe_log_g(L, wl, ql, t2l) - L.log_k);
+    });
+    o0 = make_float4(v.x, v.y, v.z, pv);
+    o1 = make_float4(dnee.w > 0.f ? pn : 0.f, ce, tech ? 1.f : 0.f, c);
+}
+
 // ---- KL gradient in fp32 (bf16 training path) --------------------------------
 // Decode intermediates the chain rule needs (DecodedGuide guiding.hpp:34-42).
 struct LobeG {

@@ -234,6 +234,30 @@ __device__ __forceinline__ float2 guide_pdf(RawFn raw, float3 dir, float b, floa
     return make_float2((float)pdf, (float)guided);
 }
 
+// guided scattering at a path vertex in double (same contract as nasg::guide_shade)
+template <int N, class RawFn>
+__device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float4 dbsdf, float4 dnee, float4 &o0,
+                                            float4 &o1) {
+    double w[N], c, c_sig;
+    ref::decode_header<N>(raw, w, c, c_sig);
+    const double ce = (double)b * c;
+    const bool tech = (double)dbsdf.w < ce;
+    V3 v = {(double)dbsdf.x, (double)dbsdf.y, (double)dbsdf.z};
+    double pv;
+    if (tech) {
+        float cc;
+        const float4 s = ref::guide_sample<N>(raw, xi, cc);
+        v = {(double)s.x, (double)s.y, (double)s.z};
+        pv = (double)s.w;
+    } else {
+        pv = ref::mixture_pdf<N>(raw, w, v);
+    }
+    const V3 vn = {(double)dnee.x, (double)dnee.y, (double)dnee.z};
+    const double pn = dnee.w > 0.f ? ref::mixture_pdf<N>(raw, w, vn) : 0.0;
+    o0 = make_float4((float)v.x, (float)v.y, (float)v.z, (float)pv);
+    o1 = make_float4((float)pn, (float)ce, tech ? 1.f : 0.f, (float)c);
+}
+
 // ---- KL gradient (guiding.cpp:96-176, sphdist.cpp:200-274) -----------------------
 struct Euler {
     double ct, sp, cp, st, ctau;
