@@ -206,6 +206,56 @@ uint64_t nasg_kernel_launches(nasg_ctx *ctx);
 double nasg_blend_coefficient(int64_t iteration, int m, int b_steps);
 double nasg_stride_update(double l, uint64_t collected, uint64_t capacity);
 
+/* ---- guided progressive render loop (SPEC.md tracer module :378-478; the
+ * reference specifies it but ships no code) ---
+ * A wavefront path tracer on the GPU: NEE + balance-heuristic MIS at every
+ * non-delta vertex, scattering from the blend q-hat through nasg_query_shade,
+ * Russian roulette from depth 5 (cap 0.95), max depth 16, per-vertex radiance
+ * back-propagation into TrainingSamples for one pixel per l x l tile, then
+ * train_iteration, stride_update and the progressive w_i ramp (SPEC accumulate).
+ * Multi-GPU: each rank renders the pixel rows [row_begin, row_end) and trains
+ * data-parallel through the context's NCCL communicator (nasg_comm_init). */
+typedef struct nasg_render nasg_render;
+enum { NASG_SCENE_FURNACE = 0, NASG_SCENE_BOX = 1, NASG_SCENE_CRACK = 2, NASG_SCENE_DARK = 3 };
+typedef struct {
+    int scene;             /* NASG_SCENE_* */
+    int width, height;     /* full image */
+    int row_begin, row_end;/* this rank's rows; row_end <= 0 means height */
+    uint64_t seed;
+    int max_depth;         /* 16 */
+    int rr_depth;          /* 5 */
+    int guiding;           /* 1: blend schedule b = min(1, floor(i/M)/B); 0: b = 0 always */
+    int collect;           /* 1: collect samples and train after every iteration */
+    int ramp;              /* 1: accumulate with w_i = min(i+1, M B)/(M B); 0: plain mean */
+    int schedule_m;        /* M = 4 */
+    int schedule_b;        /* B = 64 */
+} nasg_render_config;
+typedef struct {
+    int64_t iteration;     /* the iteration just rendered */
+    double b;              /* blend coefficient used */
+    double stride;         /* l used for collection (next one after stride_update) */
+    int64_t paths, vertices, guided_vertices;
+    int64_t collected;     /* samples produced by the selected pixels */
+    int64_t kept;          /* min(collected, this rank's capacity) */
+    int64_t nonfinite_paths;
+    nasg_train_stats train;
+} nasg_render_stats;
+void nasg_render_config_default(nasg_render_config *cfg);
+/* scene bounds for nasg_create (encoding's Aabb) */
+int nasg_render_scene_bounds(int scene, float bmin[3], float bmax[3]);
+int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render **out);
+int nasg_render_destroy(nasg_render *r);
+/* Render one sample per pixel, collect + train (cfg.collect), accumulate. */
+int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats);
+/* Host copy of this rank's rows, (row_end-row_begin) x width x 3 floats:
+ * which = 0 the accumulated image, 1 the last frame. */
+int nasg_render_image(nasg_render *r, float *rgb, int which);
+/* Device kernel launches issued by the render loop's own kernels. */
+uint64_t nasg_render_kernel_launches(nasg_render *r);
+/* MAPE (SPEC.md tracer mape, PAPER §7): per-pixel mean over channels of
+ * |img - ref| / (ref + 0.01), the worst floor(0.1% of pixels) dropped. */
+double nasg_mape(const float *img, const float *ref, int64_t npix);
+
 /* ---- synthetic workloads (bench / tests) ----------------- */
 /* Query i: Pcg32(hash_combine(seed, i), 0x51) -> x ~ U(bounds), omega_o and
  * normal ~ U(S^2), xi ~ U[0,1) as (u32 >> 8) * 2^-24.  Host arrays. */

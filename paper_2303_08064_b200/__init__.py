@@ -41,6 +41,22 @@ class _Stats(C.Structure):
                 ("skipped_updates", C.c_uint64)]
 
 
+class _RenderConfig(C.Structure):
+    _fields_ = [("scene", C.c_int), ("width", C.c_int), ("height", C.c_int), ("row_begin", C.c_int),
+                ("row_end", C.c_int), ("seed", C.c_uint64), ("max_depth", C.c_int), ("rr_depth", C.c_int),
+                ("guiding", C.c_int), ("collect", C.c_int), ("ramp", C.c_int), ("schedule_m", C.c_int),
+                ("schedule_b", C.c_int)]
+
+
+class _RenderStats(C.Structure):
+    _fields_ = [("iteration", C.c_int64), ("b", C.c_double), ("stride", C.c_double), ("paths", C.c_int64),
+                ("vertices", C.c_int64), ("guided_vertices", C.c_int64), ("collected", C.c_int64),
+                ("kept", C.c_int64), ("nonfinite_paths", C.c_int64), ("train", _Stats)]
+
+
+SCENE_FURNACE, SCENE_BOX, SCENE_CRACK, SCENE_DARK = 0, 1, 2, 3
+
+
 @dataclass
 class TrainerConfig:
     """TrainerConfig (guiding.hpp:122-130)."""
@@ -114,6 +130,14 @@ def lib():
         "nasg_synth_queries": (None, [u64, i64, i64, vp, vp, vp, vp, vp, vp]),
         "nasg_synth_samples": (None, [u64, i64, i64, vp, vp, vp]),
         "nasg_dp_plan": (i32, [vp, vp, i32, i32, i32, vp, vp, vp]),
+        "nasg_render_config_default": (None, [vp]),
+        "nasg_render_scene_bounds": (i32, [i32, vp, vp]),
+        "nasg_render_create": (i32, [vp, vp, C.POINTER(vp)]),
+        "nasg_render_destroy": (i32, [vp]),
+        "nasg_render_iteration": (i32, [vp, vp]),
+        "nasg_render_image": (i32, [vp, vp, i32]),
+        "nasg_render_kernel_launches": (u64, [vp]),
+        "nasg_mape": (f64, [vp, vp, i64]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -417,3 +441,68 @@ class Guide:
     def comm_init(self, unique_id: bytes, rank: int, nranks: int):
         buf = (C.c_char * 128).from_buffer_copy(unique_id)
         _check(lib().nasg_comm_init(self._h, buf, rank, nranks))
+
+
+# ---- guided progressive render loop (SPEC.md tracer module; nasg_render_*) -----------
+def scene_bounds(scene: int):
+    lo, hi = np.zeros(3, np.float32), np.zeros(3, np.float32)
+    _check(lib().nasg_render_scene_bounds(scene, lo.ctypes.data, hi.ctypes.data))
+    return lo, hi
+
+
+def mape(img, ref) -> float:
+    """SPEC.md tracer mape (PAPER §7): relative error with eps 0.01, worst 0.1 % dropped."""
+    a = np.ascontiguousarray(img, np.float32).reshape(-1, 3)
+    b = np.ascontiguousarray(ref, np.float32).reshape(-1, 3)
+    if a.shape != b.shape:
+        raise NasgError("mape: dimension mismatch")
+    return lib().nasg_mape(a.ctypes.data, b.ctypes.data, a.shape[0])
+
+
+class Render:
+    """nasg_render: wavefront guided path tracer + online training on one GPU's pixel rows."""
+
+    def __init__(self, guide: Guide, scene: int = SCENE_BOX, width: int = 256, height: int = 256,
+                 row_begin: int = 0, row_end: int = 0, seed: int = 1, guiding: bool = True,
+                 collect: bool = True, ramp: bool = True, max_depth: int = 16, rr_depth: int = 5,
+                 schedule_m: int = 4, schedule_b: int = 64):
+        cfg = _RenderConfig()
+        lib().nasg_render_config_default(C.byref(cfg))
+        cfg.scene, cfg.width, cfg.height = scene, width, height
+        cfg.row_begin, cfg.row_end, cfg.seed = row_begin, row_end, seed
+        cfg.max_depth, cfg.rr_depth = max_depth, rr_depth
+        cfg.guiding, cfg.collect, cfg.ramp = int(guiding), int(collect), int(ramp)
+        cfg.schedule_m, cfg.schedule_b = schedule_m, schedule_b
+        h = C.c_void_p()
+        _check(lib().nasg_render_create(guide._h, C.byref(cfg), C.byref(h)))
+        self._h, self.guide = h, guide
+        self.width = width
+        self.rows = (row_end if row_end > 0 else height) - row_begin
+
+    def iteration(self) -> dict:
+        st = _RenderStats()
+        _check(lib().nasg_render_iteration(self._h, C.byref(st)))
+        out = {k: getattr(st, k) for k, _ in _RenderStats._fields_ if k != "train"}
+        out["train"] = TrainStats(st.train.steps, st.train.mean_loss, st.train.dropped_samples,
+                                  st.train.skipped_updates)
+        return out
+
+    def image(self, which: int = 0) -> np.ndarray:
+        img = np.empty((self.rows, self.width, 3), np.float32)
+        _check(lib().nasg_render_image(self._h, img.ctypes.data, which))
+        return img
+
+    @property
+    def kernel_launches(self) -> int:
+        return lib().nasg_render_kernel_launches(self._h)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().nasg_render_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

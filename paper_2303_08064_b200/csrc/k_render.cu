@@ -1,0 +1,703 @@
+// Guided progressive render loop (SPEC.md tracer module, :378-478; PAPER §6):
+// a wavefront path tracer whose scattering at every non-delta vertex goes
+// through the fused network query (nasg_query_shade), and whose selected
+// pixels feed the online trainer (nasg_train_iteration) after every frame.
+//
+// One iteration (= 1 sample per pixel of this rank's rows):
+//   K_begin     camera rays, path state, which pixel of each l x l tile collects
+//   per bounce  K_isect  nearest hit; environment / emitter hits with the MIS
+//                        weight of the previous scatter; mirror bounces; at
+//                        non-delta vertices NEE (light sample + shadow ray), a
+//                        BSDF pre-sample, and a slot in the guide queue
+//               guide    nasg_query_shade over the queue (device row count):
+//                        technique, direction, q_mix at it and at the NEE dir
+//               K_update blend pdf, MIS-weighted NEE, throughput, training
+//                        record of collected paths, Russian roulette
+//   K_scan + K_records  per-vertex incident radiance by back-propagation
+//                        (L_i = (L_end - L_before) / beta), TrainingSamples in
+//                        deterministic tile order, first S kept
+//   K_accumulate film += w_i L (non-finite paths discarded and counted)
+//   train_iteration + publish, stride_update (host)
+// Path state is SoA in HBM (float4 per quantity); the guide queue is compacted
+// with one atomic per guided vertex, so the query kernel runs over exactly the
+// live vertices without a host round trip.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "nasg/nasg.h"
+#include "nasg_internal.h"
+#include "render_scene.cuh"
+
+namespace nasg {
+namespace rt {
+
+__constant__ Scene c_scene;
+
+constexpr int kMaxDepthCap = 16;
+constexpr int kBlock = 256;
+
+struct Paths {
+    int64_t n;  // paths = pixels of this rank
+    float4 *o, *d, *beta, *L;
+    float *prev_pdf;        // q-hat of the last scatter; < 0: camera ray or delta bounce
+    int *alive, *pending;   // pending: a non-delta vertex waiting for K_update
+    float4 *vx, *vn, *vwo, *vdb, *vdn, *vnee;
+    int *slot, *rank, *bsdf_ok;
+    // guide queue
+    float4 *qx, *qwo, *qn, *qxi, *qdb, *qdn, *qout;
+    int *qcount;
+    // training records [depth][ncap]
+    int64_t ncap;
+    float4 *rx, *rwo, *rn, *rwi, *rfc, *rbeta, *rlb;
+    int *rcnt, *rpix, *roff;
+    unsigned long long *ctr;  // 0 vertices, 1 guided, 2 nonfinite, 3 collected
+    float4 *film, *frame;
+    nasg_train_sample *samples;
+    int64_t cap_samples;
+};
+
+struct Frame {
+    uint64_t seed, iter;
+    int width, height, row0;
+    float l;          // collection stride
+    int tile_row0;    // floor(row0 / l)
+    int ntx;          // tiles per row
+    int collect, max_depth, rr_depth;
+};
+
+__device__ inline float4 f4(float3 v, float w) { return make_float4(v.x, v.y, v.z, w); }
+__device__ inline float3 xyz(float4 v) { return make_float3(v.x, v.y, v.z); }
+
+__global__ void k_begin(Paths P, Frame F) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    const Scene &S = c_scene;
+    const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
+    const uint64_t pix = (uint64_t)py * F.width + px;
+    const float jx = rnd(F.seed, pix, F.iter, 0, 0), jy = rnd(F.seed, pix, F.iter, 0, 1);
+    const float sx = 2.f * (px + jx) / F.width - 1.f, sy = 1.f - 2.f * (py + jy) / F.height;
+    const float3 d = normalize(S.cam.fwd + S.cam.right * sx + S.cam.up * sy);
+    P.o[i] = f4(S.cam.pos, 0.f);
+    P.d[i] = f4(d, 0.f);
+    P.beta[i] = make_float4(1.f, 1.f, 1.f, 0.f);
+    P.L[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+    P.prev_pdf[i] = -1.f;
+    P.alive[i] = 1;
+    P.pending[i] = 0;
+    int rank = -1;
+    if (F.collect) {  // one pixel per l x l tile (PAPER §6), uniformly at random per tile and iteration
+        const int tx = (int)floorf(px / F.l), ty = (int)floorf(py / F.l);
+        const uint64_t tile = ((uint64_t)ty << 32) | (uint32_t)tx;
+        const int cx = (int)floorf((tx + rnd(F.seed ^ 0x636f6c6cull, tile, F.iter, 0, 0)) * F.l);
+        const int cy = (int)floorf((ty + rnd(F.seed ^ 0x636f6c6cull, tile, F.iter, 0, 1)) * F.l);
+        if (cx == px && cy == py) {
+            const int64_t r = (int64_t)(ty - F.tile_row0) * F.ntx + tx;
+            if (r >= 0 && r < P.ncap) {
+                rank = (int)r;
+                P.rpix[r] = (int)i;
+            }
+        }
+    }
+    P.rank[i] = rank;
+    if (rank >= 0) P.rcnt[rank] = 0;
+}
+
+// per-bounce queue reset; the previous bounce's queue length feeds the counter
+__global__ void k_queue_reset(Paths P) {
+    P.ctr[1] += (unsigned long long)*P.qcount;
+    *P.qcount = 0;
+}
+
+__global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n || !P.alive[i]) return;
+    const Scene &S = c_scene;
+    const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
+    const uint64_t pix = (uint64_t)py * F.width + px;
+    auto R = [&](uint32_t dim) { return rnd(F.seed, pix, F.iter, (uint32_t)bounce + 1, dim); };
+    const float3 o = xyz(P.o[i]), d = xyz(P.d[i]);
+    float4 beta = P.beta[i], L = P.L[i];
+    Hit h;
+    if (!intersect(S, o, d, 1e30f, h)) {  // environment (not light-sampled: weight 1)
+        L.x += beta.x * S.env.x;
+        L.y += beta.y * S.env.y;
+        L.z += beta.z * S.env.z;
+        P.L[i] = L;
+        P.alive[i] = 0;
+        return;
+    }
+    const Prim &prim = S.prims[h.prim];
+    const Mat &m = S.mats[prim.mat];
+    if (m.type == kEmitter) {  // emitters absorb; MIS against NEE for scattered rays
+        const float cl = -dot(h.n, d);
+        if (cl > 0.f) {
+            const float pp = P.prev_pdf[i];
+            float w = 1.f;
+            if (pp >= 0.f) {
+                const float pl = light_pdf_at(S, o, h, d);
+                w = pp / (pp + pl);
+            }
+            L.x += beta.x * m.emission.x * w;
+            L.y += beta.y * m.emission.y * w;
+            L.z += beta.z * m.emission.z * w;
+            P.L[i] = L;
+        }
+        P.alive[i] = 0;
+        return;
+    }
+    atomicAdd(&P.ctr[0], 1ull);
+    const float3 wo = d * -1.f;
+    const float3 n = dot(h.n, wo) < 0.f ? h.n * -1.f : h.n;  // two-sided surfaces
+    if (m.type == kMirror) {  // delta vertex: no guiding, no NEE, no training record
+        const float3 r = reflect(wo, n);
+        beta.x *= m.albedo.x;
+        beta.y *= m.albedo.y;
+        beta.z *= m.albedo.z;
+        P.beta[i] = beta;
+        P.o[i] = f4(h.x + n * kEps, 0.f);
+        P.d[i] = f4(r, 0.f);
+        P.prev_pdf[i] = -1.f;
+        return;
+    }
+    // next-event estimation (SPEC nee_sample): one emitter by area, shadow ray
+    const LightSample ls = sample_light(S, h.x, R(0), R(1), R(2));
+    float3 nee = f3(0.f, 0.f, 0.f);
+    float pl = 0.f;
+    if (ls.pdf > 0.f && dot(n, ls.dir) > 0.f && !occluded(S, h.x + n * kEps, ls.dir, ls.dist)) {
+        const float3 f = bsdf_eval(m, n, wo, ls.dir);
+        nee = mul(ls.Le, f) * (dot(n, ls.dir) / ls.pdf);
+        pl = ls.pdf;
+    }
+    float3 db;
+    const bool ok = bsdf_sample(m, n, wo, [&](int k) { return R(8 + k); }, db);
+    if (!ok) db = n;
+    P.vx[i] = f4(h.x, (float)prim.mat);
+    P.vn[i] = f4(n, 0.f);
+    P.vwo[i] = f4(wo, 0.f);
+    P.vdb[i] = f4(db, R(3));                 // xi_t: technique selection
+    P.vdn[i] = f4(ls.dir, pl > 0.f ? 1.f : 0.f);
+    P.vnee[i] = f4(nee, pl);
+    P.bsdf_ok[i] = ok ? 1 : 0;
+    P.pending[i] = 1;
+    int slot = -1;
+    if (guided) {
+        slot = atomicAdd(P.qcount, 1);
+        P.qx[slot] = f4(h.x, 0.f);
+        P.qwo[slot] = f4(wo, 0.f);
+        P.qn[slot] = f4(n, 0.f);
+        P.qxi[slot] = make_float4(R(4), R(5), R(6), R(7));
+        P.qdb[slot] = P.vdb[i];
+        P.qdn[slot] = P.vdn[i];
+    }
+    P.slot[i] = slot;
+}
+
+__global__ void k_update(Paths P, Frame F, int bounce) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n || !P.pending[i]) return;
+    P.pending[i] = 0;
+    const Scene &S = c_scene;
+    const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
+    const uint64_t pix = (uint64_t)py * F.width + px;
+    const float4 vx = P.vx[i];
+    const Mat &m = S.mats[(int)vx.w];
+    const float3 x = xyz(vx), n = xyz(P.vn[i]), wo = xyz(P.vwo[i]);
+    const float4 vdb = P.vdb[i], vdn = P.vdn[i], vnee = P.vnee[i];
+    float3 v = xyz(vdb);
+    float qv = 0.f, qn = 0.f, ce = 0.f;
+    bool tech = false;
+    const int slot = P.slot[i];
+    if (slot >= 0) {
+        const float4 o0 = P.qout[2 * slot], o1 = P.qout[2 * slot + 1];
+        v = xyz(o0);
+        qv = o0.w;
+        qn = o1.x;
+        ce = o1.y;
+        tech = o1.z > 0.5f;
+    }
+    float4 beta = P.beta[i], L = P.L[i];
+    // NEE with the balance heuristic against the full blend q-hat at its direction
+    if (vdn.w > 0.f) {
+        const float qhn = ce * qn + (1.f - ce) * bsdf_pdf(m, n, wo, xyz(vdn));
+        const float w = vnee.w / (vnee.w + qhn);
+        L.x += beta.x * vnee.x * w;
+        L.y += beta.y * vnee.y * w;
+        L.z += beta.z * vnee.z * w;
+    }
+    const float pb = bsdf_pdf(m, n, wo, v);
+    const float qh = ce * qv + (1.f - ce) * pb;  // guided_pdf (guiding.cpp:81-85)
+    const float cs = dot(n, v);
+    const bool usable = (tech || P.bsdf_ok[i]) && qh > 0.f && isfinite(qh);
+    const float3 fc = usable && cs > 0.f ? bsdf_eval(m, n, wo, v) * cs : f3(0.f, 0.f, 0.f);
+    float4 nb = make_float4(beta.x * fc.x / qh, beta.y * fc.y / qh, beta.z * fc.z / qh, 0.f);
+    bool live = usable && (nb.x > 0.f || nb.y > 0.f || nb.z > 0.f);
+    if (live && bounce + 1 >= F.rr_depth) {  // Russian roulette from depth 5, capped at 0.95
+        const float q = fminf(0.95f, lum(f3(nb.x, nb.y, nb.z)));
+        if (rnd(F.seed, pix, F.iter, (uint32_t)bounce + 1, 31) >= q) {
+            live = false;
+        } else {
+            nb.x /= q;
+            nb.y /= q;
+            nb.z /= q;
+        }
+    }
+    const int r = P.rank[i];
+    if (r >= 0 && usable && bounce < kMaxDepthCap) {  // training record (SPEC PathVertexRecord)
+        const int k = P.rcnt[r]++;
+        const size_t at = (size_t)k * P.ncap + r;
+        P.rx[at] = f4(x, 0.f);
+        P.rwo[at] = f4(wo, qh);
+        P.rn[at] = f4(n, pb);
+        P.rwi[at] = f4(v, 0.f);
+        P.rfc[at] = f4(fc, 0.f);
+        P.rbeta[at] = live ? nb : make_float4(0.f, 0.f, 0.f, 0.f);
+        P.rlb[at] = L;
+    }
+    P.L[i] = L;
+    if (!live) {
+        P.alive[i] = 0;
+        return;
+    }
+    P.beta[i] = nb;
+    P.o[i] = f4(x + n * kEps, 0.f);
+    P.d[i] = f4(v, 0.f);
+    P.prev_pdf[i] = qh;
+}
+
+// exclusive prefix sum of rcnt over ranks (one block; ncap <= 4 S)
+__global__ void k_scan(Paths P) {
+    __shared__ long long part[1024];
+    const int64_t n = P.ncap;
+    const int64_t per = (n + blockDim.x - 1) / blockDim.x;
+    const int64_t b = threadIdx.x * per, e = min(n, b + per);
+    long long s = 0;
+    for (int64_t k = b; k < e; ++k) s += P.rpix[k] >= 0 ? P.rcnt[k] : 0;
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        long long acc = 0;
+        for (int k = 0; k < (int)blockDim.x; ++k) {
+            const long long v = part[k];
+            part[k] = acc;
+            acc += v;
+        }
+        P.ctr[3] += (unsigned long long)acc;
+        P.ctr[4] = (unsigned long long)acc;
+    }
+    __syncthreads();
+    long long acc = part[threadIdx.x];
+    for (int64_t k = b; k < e; ++k) {
+        P.roff[k] = (int)acc;
+        acc += P.rpix[k] >= 0 ? P.rcnt[k] : 0;
+    }
+}
+
+// per-vertex incident radiance by back-propagation -> TrainingSamples
+__global__ void k_records(Paths P) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= P.ncap) return;
+    const int pi = P.rpix[r];
+    if (pi < 0) return;
+    const int cnt = P.rcnt[r];
+    const float4 Le = P.L[pi];
+    for (int k = 0; k < cnt; ++k) {
+        const int64_t o = (int64_t)P.roff[r] + k;
+        if (o >= P.cap_samples) break;
+        const size_t at = (size_t)k * P.ncap + r;
+        const float4 b = P.rbeta[at], lb = P.rlb[at], fc = P.rfc[at];
+        // incident radiance along omega_i: everything gathered after this vertex
+        const float3 li = f3(b.x > 0.f ? (Le.x - lb.x) / b.x : 0.f, b.y > 0.f ? (Le.y - lb.y) / b.y : 0.f,
+                             b.z > 0.f ? (Le.z - lb.z) / b.z : 0.f);
+        float p = lum(mul(xyz(fc), li));  // luminance of f_s L_i |cos| (SPEC guider)
+        if (!(p > 0.f) || !isfinite(p)) p = 0.f;
+        const float4 x = P.rx[at], wo = P.rwo[at], n = P.rn[at], wi = P.rwi[at];
+        nasg_train_sample s;
+        s.position[0] = x.x; s.position[1] = x.y; s.position[2] = x.z;
+        s.p_value = p;
+        s.omega_o[0] = wo.x; s.omega_o[1] = wo.y; s.omega_o[2] = wo.z;
+        s.q_sampling = wo.w;
+        s.normal[0] = n.x; s.normal[1] = n.y; s.normal[2] = n.z;
+        s.bsdf_pdf_at_wi = n.w;
+        s.omega_i[0] = wi.x; s.omega_i[1] = wi.y; s.omega_i[2] = wi.z;
+        s.pad = 0.f;
+        P.samples[o] = s;
+    }
+}
+
+__global__ void k_accumulate(Paths P, float w, int first) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= P.n) return;
+    float4 L = P.L[i];
+    if (!(isfinite(L.x) && isfinite(L.y) && isfinite(L.z))) {  // discarded, counted, never on film
+        atomicAdd(&P.ctr[2], 1ull);
+        L = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    L.w = 1.f;
+    P.frame[i] = L;
+    float4 f = first ? make_float4(0.f, 0.f, 0.f, 0.f) : P.film[i];
+    f.x += w * L.x;
+    f.y += w * L.y;
+    f.z += w * L.z;
+    f.w += w;
+    P.film[i] = f;
+}
+
+// ------------------------------------------------------------------ scenes --
+static Prim quad(float3 p, float3 u, float3 v, int mat) {
+    Prim q{};
+    q.type = kQuad;
+    q.mat = mat;
+    q.p = p;
+    q.u = u;
+    q.v = v;
+    return q;
+}
+static Prim sphere(float3 c, float r, int mat) {
+    Prim s{};
+    s.type = kSphere;
+    s.mat = mat;
+    s.p = c;
+    s.r = r;
+    return s;
+}
+static Mat mat(int type, float3 albedo, float e = 0.f, float3 em = f3(0.f, 0.f, 0.f)) {
+    Mat m{};
+    m.type = type;
+    m.albedo = albedo;
+    m.exponent = e;
+    m.emission = em;
+    return m;
+}
+
+static void look_at(Camera &c, float3 pos, float3 at, float3 up, float vfov_deg, int w, int h) {
+    c.pos = pos;
+    c.fwd = normalize(at - pos);
+    const float3 r = normalize(cross(c.fwd, up));
+    const float3 u = cross(r, c.fwd);
+    const float th = tanf(vfov_deg * 0.5f * kPiF / 180.f);
+    c.right = r * (th * (float)w / (float)h);
+    c.up = u * th;
+    c.width = w;
+    c.height = h;
+}
+
+// Cornell-style box [0,1]^3 open at z = 0 (SPEC Scene: spheres, axis-aligned quads,
+// lambertian / phong / mirror, area emitters); CRACK hides the light above a
+// partition so the room is lit through a narrow slit (anisotropic indirect light,
+// the case PAPER §7 targets).
+static bool build_scene(int kind, int w, int h, Scene &s) {
+    std::memset(&s, 0, sizeof(s));
+    const float3 white = f3(0.73f, 0.73f, 0.73f), red = f3(0.65f, 0.05f, 0.05f), green = f3(0.12f, 0.45f, 0.15f);
+    int np = 0, nm = 0;
+    auto addm = [&](Mat m) { s.mats[nm] = m; return nm++; };
+    auto addp = [&](Prim p) { s.prims[np++] = p; };
+    if (kind == NASG_SCENE_FURNACE || kind == NASG_SCENE_DARK) {
+        // SPEC trace_path examples: constant environment 1 over a lambertian plane
+        // of albedo 0.5 (pixel expectation 0.5); DARK: no emitters, zero environment
+        const int m0 = addm(mat(kLambert, f3(0.5f, 0.5f, 0.5f)));
+        addp(quad(f3(-50.f, -50.f, 0.f), f3(100.f, 0.f, 0.f), f3(0.f, 100.f, 0.f), m0));
+        s.env = kind == NASG_SCENE_FURNACE ? f3(1.f, 1.f, 1.f) : f3(0.f, 0.f, 0.f);
+        look_at(s.cam, f3(0.f, -1.2f, 1.6f), f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), 40.f, w, h);
+        const float lo[3] = {-1.5f, -1.5f, -0.5f}, hi[3] = {1.5f, 1.5f, 2.5f};
+        std::memcpy(s.bmin, lo, sizeof(lo));
+        std::memcpy(s.bmax, hi, sizeof(hi));
+    } else if (kind == NASG_SCENE_BOX || kind == NASG_SCENE_CRACK) {
+        const int mw = addm(mat(kLambert, white)), mr = addm(mat(kLambert, red)), mg = addm(mat(kLambert, green));
+        const int mgl = addm(mat(kPhong, f3(0.8f, 0.8f, 0.8f), 60.f));
+        const int mmi = addm(mat(kMirror, f3(0.95f, 0.95f, 0.95f)));
+        const int mle = addm(mat(kEmitter, f3(0.f, 0.f, 0.f), 0.f, kind == NASG_SCENE_BOX ? f3(17.f, 12.f, 4.f)
+                                                                                         : f3(60.f, 48.f, 30.f)));
+        addp(quad(f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), f3(1.f, 0.f, 0.f), kind == NASG_SCENE_CRACK ? mgl : mw));
+        addp(quad(f3(0.f, 1.f, 0.f), f3(1.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), mw));  // ceiling
+        addp(quad(f3(0.f, 0.f, 1.f), f3(0.f, 1.f, 0.f), f3(1.f, 0.f, 0.f), mw));  // back
+        addp(quad(f3(0.f, 0.f, 0.f), f3(0.f, 1.f, 0.f), f3(0.f, 0.f, 1.f), mr));  // left
+        addp(quad(f3(1.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), f3(0.f, 1.f, 0.f), mg));  // right
+        if (kind == NASG_SCENE_BOX) {
+            addp(quad(f3(0.4f, 0.999f, 0.4f), f3(0.2f, 0.f, 0.f), f3(0.f, 0.f, 0.2f), mle));
+            addp(sphere(f3(0.3f, 0.2f, 0.62f), 0.2f, mgl));
+            addp(sphere(f3(0.72f, 0.18f, 0.35f), 0.18f, mmi));
+        } else {
+            // partition at y = 0.85 with a slit 0.47 < x < 0.53; the light lies above it
+            addp(quad(f3(0.f, 0.85f, 0.f), f3(0.47f, 0.f, 0.f), f3(0.f, 0.f, 1.f), mw));
+            addp(quad(f3(0.53f, 0.85f, 0.f), f3(0.47f, 0.f, 0.f), f3(0.f, 0.f, 1.f), mw));
+            addp(quad(f3(0.2f, 0.999f, 0.3f), f3(0.6f, 0.f, 0.f), f3(0.f, 0.f, 0.4f), mle));
+            addp(sphere(f3(0.3f, 0.2f, 0.6f), 0.2f, mw));
+            addp(sphere(f3(0.72f, 0.18f, 0.35f), 0.18f, mmi));
+        }
+        s.env = f3(0.f, 0.f, 0.f);
+        look_at(s.cam, f3(0.5f, 0.5f, -1.25f), f3(0.5f, 0.45f, 0.5f), f3(0.f, 1.f, 0.f), 40.f, w, h);
+        const float lo[3] = {-0.05f, -0.05f, -0.05f}, hi[3] = {1.05f, 1.05f, 1.05f};
+        std::memcpy(s.bmin, lo, sizeof(lo));
+        std::memcpy(s.bmax, hi, sizeof(hi));
+    } else {
+        return false;
+    }
+    s.nprims = np;
+    float area = 0.f;
+    for (int i = 0; i < np; ++i) {
+        const Prim &p = s.prims[i];
+        if (s.mats[p.mat].type != kEmitter) continue;
+        if (p.type != kQuad || s.nlights == kMaxLights) return false;
+        const float3 c = cross(p.u, p.v);
+        area += sqrtf(dot(c, c));
+        s.light_prim[s.nlights] = i;
+        s.light_cdf[s.nlights++] = area;
+    }
+    for (int k = 0; k < s.nlights; ++k) s.light_cdf[k] /= area;
+    s.light_area_total = area;
+    return true;
+}
+
+}  // namespace rt
+}  // namespace nasg
+
+using namespace nasg;
+using namespace nasg::rt;
+
+struct nasg_render {
+    nasg_ctx *ctx = nullptr;
+    nasg_render_config cfg{};
+    Scene scene{};
+    Paths P{};
+    cudaStream_t stream = nullptr;
+    int rows = 0;
+    int64_t iter = 0;
+    double l = 1.0, l_min = 1.0;
+    double wsum = 0.0;
+    uint64_t launches = 0;
+    std::vector<void *> bufs;
+    int nranks = 1;
+};
+
+namespace {
+
+thread_local char g_rerr[256];
+
+int rfail(int code, const char *msg) {
+    std::snprintf(g_rerr, sizeof(g_rerr), "%s", msg);
+    return code;
+}
+
+#define RCUDA(x)                                                        \
+    do {                                                                \
+        cudaError_t e_ = (x);                                           \
+        if (e_ != cudaSuccess) return rfail(NASG_ERR_CUDA, cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+int alloc(nasg_render *r, T **p, size_t count) {
+    void *q = nullptr;
+    RCUDA(cudaMalloc(&q, std::max<size_t>(count, 1) * sizeof(T)));
+    r->bufs.push_back(q);
+    *p = static_cast<T *>(q);
+    return NASG_OK;
+}
+
+unsigned grid_of(int64_t n) { return (unsigned)((n + kBlock - 1) / kBlock); }
+
+}  // namespace
+
+extern "C" {
+
+void nasg_render_config_default(nasg_render_config *c) {
+    if (!c) return;
+    std::memset(c, 0, sizeof(*c));
+    c->scene = NASG_SCENE_BOX;
+    c->width = 256;
+    c->height = 256;
+    c->row_begin = 0;
+    c->row_end = 0;
+    c->seed = 1;
+    c->max_depth = 16;
+    c->rr_depth = 5;
+    c->guiding = 1;
+    c->collect = 1;
+    c->ramp = 1;
+    c->schedule_m = 4;
+    c->schedule_b = 64;
+}
+
+int nasg_render_scene_bounds(int scene, float bmin[3], float bmax[3]) {
+    Scene s;
+    if (!bmin || !bmax || !build_scene(scene, 16, 16, s)) return NASG_ERR_INVALID;
+    for (int k = 0; k < 3; ++k) {
+        bmin[k] = s.bmin[k];
+        bmax[k] = s.bmax[k];
+    }
+    return NASG_OK;
+}
+
+int nasg_render_destroy(nasg_render *r) {
+    if (!r) return NASG_OK;
+    if (r->stream) cudaStreamSynchronize(r->stream);
+    for (void *p : r->bufs) cudaFree(p);
+    if (r->stream) cudaStreamDestroy(r->stream);
+    delete r;
+    return NASG_OK;
+}
+
+int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render **out) {
+    if (!ctx || !cfg || !out) return NASG_ERR_INVALID;
+    *out = nullptr;
+    nasg_render_config c = *cfg;
+    if (c.row_end <= 0) c.row_end = c.height;
+    if (c.width <= 0 || c.height <= 0 || c.row_begin < 0 || c.row_end > c.height || c.row_begin >= c.row_end ||
+        c.max_depth < 1 || c.max_depth > kMaxDepthCap || c.schedule_m < 1 || c.schedule_b < 1)
+        return NASG_ERR_INVALID;
+    auto *r = new nasg_render();
+    r->ctx = ctx;
+    r->cfg = c;
+    if (!build_scene(c.scene, c.width, c.height, r->scene)) {
+        delete r;
+        return NASG_ERR_INVALID;
+    }
+    r->nranks = std::max(1, ctx_nranks(ctx));
+    int rc = NASG_OK;
+    auto fail_out = [&](int code) {
+        nasg_render_destroy(r);
+        return code;
+    };
+    if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
+    r->rows = c.row_end - c.row_begin;
+    Paths &P = r->P;
+    P.n = (int64_t)r->rows * c.width;
+    // this rank's share of the capacity S; record storage bounded to 4 S paths
+    P.cap_samples = std::max<int64_t>(1, (ctx_sample_capacity(ctx) + r->nranks - 1) / r->nranks);
+    r->l_min = std::max(1.0, std::sqrt((double)P.n / (4.0 * (double)P.cap_samples)));
+    r->l = r->l_min;
+    const int ntx_max = (int)std::ceil(c.width / r->l_min) + 1;
+    const int nty_max = (int)std::ceil(r->rows / r->l_min) + 2;
+    P.ncap = (int64_t)ntx_max * nty_max;
+#define A(ptr, count) \
+    if ((rc = alloc(r, &(ptr), (size_t)(count))) != NASG_OK) return fail_out(rc);
+    A(P.o, P.n) A(P.d, P.n) A(P.beta, P.n) A(P.L, P.n) A(P.prev_pdf, P.n) A(P.alive, P.n) A(P.pending, P.n)
+    A(P.vx, P.n) A(P.vn, P.n) A(P.vwo, P.n) A(P.vdb, P.n) A(P.vdn, P.n) A(P.vnee, P.n)
+    A(P.slot, P.n) A(P.rank, P.n) A(P.bsdf_ok, P.n)
+    A(P.qx, P.n) A(P.qwo, P.n) A(P.qn, P.n) A(P.qxi, P.n) A(P.qdb, P.n) A(P.qdn, P.n) A(P.qout, 2 * P.n)
+    A(P.qcount, 1)
+    const size_t nrec = (size_t)P.ncap * kMaxDepthCap;
+    A(P.rx, nrec) A(P.rwo, nrec) A(P.rn, nrec) A(P.rwi, nrec) A(P.rfc, nrec) A(P.rbeta, nrec) A(P.rlb, nrec)
+    A(P.rcnt, P.ncap) A(P.rpix, P.ncap) A(P.roff, P.ncap)
+    A(P.ctr, 8) A(P.film, P.n) A(P.frame, P.n) A(P.samples, P.cap_samples)
+#undef A
+    if (cudaMemsetAsync(P.film, 0, P.n * sizeof(float4), r->stream) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
+    *out = r;
+    return NASG_OK;
+}
+
+uint64_t nasg_render_kernel_launches(nasg_render *r) { return r ? r->launches : 0; }
+
+int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
+    if (!r) return NASG_ERR_INVALID;
+    const nasg_render_config &c = r->cfg;
+    Paths &P = r->P;
+    cudaStream_t s = r->stream;
+    RCUDA(cudaMemcpyToSymbolAsync(c_scene, &r->scene, sizeof(Scene), 0, cudaMemcpyHostToDevice, s));
+    const double b = c.guiding ? nasg_blend_coefficient(r->iter, c.schedule_m, c.schedule_b) : 0.0;
+    Frame F{};
+    F.seed = c.seed;
+    F.iter = (uint64_t)r->iter;
+    F.width = c.width;
+    F.height = c.height;
+    F.row0 = c.row_begin;
+    F.l = (float)r->l;
+    F.tile_row0 = (int)std::floor(c.row_begin / r->l);
+    F.ntx = (int)std::ceil(c.width / r->l) + 1;
+    F.collect = c.collect;
+    F.max_depth = c.max_depth;
+    F.rr_depth = c.rr_depth;
+    RCUDA(cudaMemsetAsync(P.ctr, 0, 8 * sizeof(unsigned long long), s));
+    RCUDA(cudaMemsetAsync(P.qcount, 0, sizeof(int), s));
+    if (c.collect) RCUDA(cudaMemsetAsync(P.rpix, 0xff, P.ncap * sizeof(int), s));
+    const unsigned g = grid_of(P.n);
+    k_begin<<<g, kBlock, 0, s>>>(P, F);
+    r->launches++;
+    const bool guided = b > 0.0;
+    for (int bounce = 0; bounce < c.max_depth; ++bounce) {
+        k_queue_reset<<<1, 1, 0, s>>>(P);
+        k_isect<<<g, kBlock, 0, s>>>(P, F, bounce, guided ? 1 : 0);
+        r->launches += 2;
+        if (guided) {
+            const int rc = nasg_query_shade(r->ctx, P.n, P.qcount, (const float *)P.qx, (const float *)P.qwo,
+                                            (const float *)P.qn, (const float *)P.qxi, (const float *)P.qdb,
+                                            (const float *)P.qdn, (float)b, (float *)P.qout, s);
+            if (rc != NASG_OK) return rc;
+        }
+        k_update<<<g, kBlock, 0, s>>>(P, F, bounce);
+        r->launches++;
+    }
+    k_queue_reset<<<1, 1, 0, s>>>(P);
+    r->launches++;
+    if (c.collect) {
+        k_scan<<<1, 1024, 0, s>>>(P);
+        k_records<<<grid_of(P.ncap), kBlock, 0, s>>>(P);
+        r->launches += 2;
+    }
+    const int64_t mb = (int64_t)c.schedule_m * c.schedule_b;
+    const double w = c.ramp ? (double)std::min<int64_t>(r->iter + 1, mb) / (double)mb : 1.0;
+    k_accumulate<<<g, kBlock, 0, s>>>(P, (float)w, r->iter == 0 ? 1 : 0);
+    r->launches++;
+    RCUDA(cudaGetLastError());
+    unsigned long long ctr[8];
+    RCUDA(cudaMemcpyAsync(ctr, P.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaStreamSynchronize(s));
+    r->wsum += w;
+    nasg_render_stats st{};
+    st.iteration = r->iter;
+    st.b = b;
+    st.stride = r->l;
+    st.paths = P.n;
+    st.vertices = (int64_t)ctr[0];
+    st.guided_vertices = (int64_t)ctr[1];
+    st.nonfinite_paths = (int64_t)ctr[2];
+    st.collected = (int64_t)ctr[4];
+    st.kept = std::min<int64_t>(st.collected, P.cap_samples);
+    if (c.collect) {
+        // Trainer::train_iteration on this rank's buffer (data-parallel across ranks)
+        const int rc = nasg_train_iteration(r->ctx, st.kept, P.samples, b, &st.train, s);
+        if (rc != NASG_OK) return rc;
+        // l = max(1, l sqrt(s / S)) (guiding.cpp:178-182) with the record-storage floor
+        r->l = std::max(r->l_min, nasg_stride_update(r->l, (uint64_t)st.collected, (uint64_t)P.cap_samples));
+    }
+    ++r->iter;
+    if (stats) *stats = st;
+    return NASG_OK;
+}
+
+int nasg_render_image(nasg_render *r, float *rgb, int which) {
+    if (!r || !rgb) return NASG_ERR_INVALID;
+    const Paths &P = r->P;
+    std::vector<float4> h((size_t)P.n);
+    RCUDA(cudaMemcpyAsync(h.data(), which ? P.frame : P.film, P.n * sizeof(float4), cudaMemcpyDeviceToHost,
+                          r->stream));
+    RCUDA(cudaStreamSynchronize(r->stream));
+    for (int64_t i = 0; i < P.n; ++i) {
+        const float inv = which ? 1.f : (h[i].w > 0.f ? 1.f / h[i].w : 0.f);
+        rgb[3 * i] = h[i].x * inv;
+        rgb[3 * i + 1] = h[i].y * inv;
+        rgb[3 * i + 2] = h[i].z * inv;
+    }
+    return NASG_OK;
+}
+
+double nasg_mape(const float *img, const float *ref, int64_t npix) {
+    if (!img || !ref || npix <= 0) return -1.0;
+    std::vector<double> e((size_t)npix);
+    for (int64_t i = 0; i < npix; ++i) {
+        double s = 0.0;
+        for (int k = 0; k < 3; ++k) s += std::fabs((double)img[3 * i + k] - ref[3 * i + k]) / (ref[3 * i + k] + 0.01);
+        e[i] = s / 3.0;
+    }
+    std::sort(e.begin(), e.end());
+    const int64_t keep = npix - (int64_t)std::floor(npix * 0.001);
+    double acc = 0.0;
+    for (int64_t i = 0; i < keep; ++i) acc += e[i];
+    return acc / (double)keep;
+}
+
+}  // extern "C"

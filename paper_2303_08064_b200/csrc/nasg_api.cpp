@@ -151,6 +151,11 @@ struct nasg_ctx {
     cudaEvent_t pub_ev = nullptr;  // recorded on `stream` after every publish
 };
 
+namespace nasg {
+int64_t ctx_sample_capacity(const nasg_ctx *c) { return c ? (int64_t)c->cfg.sample_capacity : 0; }
+int ctx_nranks(const nasg_ctx *c) { return c ? c->nranks : 1; }
+}  // namespace nasg
+
 namespace {
 
 int ensure_scratch(nasg_ctx *c, int64_t count) {

@@ -28,6 +28,10 @@ __host__ __device__ constexpr int packed_width(int n) { return packed_header(n) 
 
 __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHidden * kHidden + kHidden * (8 * n + 1); }
 
+// context accessors for the render loop (k_render.cu; nasg_ctx is opaque there)
+int64_t ctx_sample_capacity(const nasg_ctx *c);  // TrainerConfig::sample_capacity S
+int ctx_nranks(const nasg_ctx *c);               // data-parallel ranks (1 without NCCL)
+
 struct Bounds {
     float bmin[3];
     double ext[3];      // bmax - bmin in double (Aabb::extent, math.hpp:70)

@@ -1,0 +1,138 @@
+"""Guided progressive render loop (nasg_render_*), checked against the SPEC.md
+tracer module's examples and invariants (:378-478).  The reference specifies
+the tracer but ships no code for it, so its oracle here is analytic:
+  * white furnace: constant environment 1 over a lambertian plane of albedo
+    0.5 -> every pixel's expectation is 0.5, with guiding on and any network
+    state (SPEC trace_path example; the estimator must stay unbiased);
+  * no emitters and zero environment -> exactly 0;
+  * determinism: identical seed -> bitwise-identical film, guiding and online
+    training included;
+  * unbiasedness: guided and unguided renders of the box scene agree within
+    3 combined standard errors; the ramp-free accumulation is the plain mean;
+  * training records: collected samples are finite with q > 0, at most S kept.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2303_08064_b200 as nasg  # noqa: E402
+
+
+def make(scene, prec="bf16", seed=5, **kw):
+    lo, hi = nasg.scene_bounds(scene)
+    g = nasg.Guide(nasg.TrainerConfig(seed=seed), bmin=lo, bmax=hi)
+    p = nasg.NASG_MLP_BF16 if prec == "bf16" else nasg.NASG_MLP_FP32
+    g.precision = p
+    g.train_precision = p
+    return g, nasg.Render(g, scene=scene, **kw)
+
+
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_white_furnace_guided_is_unbiased(prec):
+    # b = 1 from the second iteration (M = B = 1): guided scattering with whatever the
+    # network has learnt so far; every frame must still average 0.5
+    g, r = make(nasg.SCENE_FURNACE, prec, width=96, height=96, seed=11, schedule_m=1, schedule_b=1)
+    try:
+        vals = []
+        for it in range(8):
+            st = r.iteration()
+            fr = r.image(1)[..., 0].ravel().astype(np.float64)
+            if it >= 1:
+                assert st["b"] == 1.0 and st["guided_vertices"] == st["vertices"] > 0
+                vals.append(fr)
+            assert st["nonfinite_paths"] == 0
+        v = np.concatenate(vals)  # independent pixel estimates pooled over the guided frames
+        se = v.std() / np.sqrt(v.size)
+        assert se > 0  # guided frames do have variance (mixture sampling is live)
+        assert abs(v.mean() - 0.5) <= 4 * se, (v.mean(), se)
+    finally:
+        r.close()
+        g.close()
+
+
+def test_dark_scene_is_black():
+    g, r = make(nasg.SCENE_DARK, width=64, height=64, schedule_m=1, schedule_b=1)
+    try:
+        for _ in range(3):
+            r.iteration()
+        assert np.all(r.image() == 0.0)
+    finally:
+        r.close()
+        g.close()
+
+
+def test_render_is_deterministic():
+    imgs = []
+    for _ in range(2):
+        g, r = make(nasg.SCENE_BOX, width=80, height=64, seed=7, schedule_m=1, schedule_b=4)
+        try:
+            for _ in range(6):
+                r.iteration()
+            imgs.append((r.image(), g.get_weights()))
+        finally:
+            r.close()
+            g.close()
+    assert np.array_equal(imgs[0][0], imgs[1][0])
+    assert np.array_equal(imgs[0][1], imgs[1][1])
+
+
+def test_guided_matches_unguided_mean():
+    """Guiding changes variance, never the mean (SPEC tracer invariants)."""
+    res = {}
+    for guiding in (False, True):
+        g, r = make(nasg.SCENE_BOX, width=64, height=64, seed=3 + guiding, guiding=guiding,
+                    ramp=False, schedule_m=1, schedule_b=2)
+        try:
+            fm = []
+            for _ in range(40):
+                r.iteration()
+                fm.append(np.asarray(r.image(1)).mean(axis=(0, 1)) @ np.array([0.2126, 0.7152, 0.0722]))
+            res[guiding] = np.array(fm[2:])  # guided frames from b = 1 on
+        finally:
+            r.close()
+            g.close()
+    a, b = res[False], res[True]
+    se = np.sqrt(a.var(ddof=1) / a.size + b.var(ddof=1) / b.size)
+    assert abs(a.mean() - b.mean()) <= 3 * se, (a.mean(), b.mean(), se)
+
+
+def test_plain_mean_without_ramp_and_records():
+    g, r = make(nasg.SCENE_CRACK, width=64, height=48, seed=9, ramp=False)
+    try:
+        frames = []
+        for _ in range(4):
+            st = r.iteration()
+            frames.append(r.image(1))
+            assert 0 < st["kept"] <= g.config.sample_capacity
+            assert st["kept"] == min(st["collected"], g.config.sample_capacity)
+            assert st["train"].steps > 0 and np.isfinite(st["train"].mean_loss)
+            assert st["train"].dropped_samples == 0
+        assert np.allclose(r.image(), np.mean(frames, axis=0), rtol=1e-5, atol=1e-6)
+    finally:
+        r.close()
+        g.close()
+
+
+def test_row_shards_tile_the_image():
+    """Config 5's sharding: rows [0, h/2) and [h/2, h) rendered separately equal the full image."""
+    full_g, full = make(nasg.SCENE_BOX, width=64, height=64, seed=13, collect=False, guiding=False)
+    parts = []
+    try:
+        full.iteration()
+        ref = full.image()
+        for rb, re in ((0, 32), (32, 64)):
+            g, r = make(nasg.SCENE_BOX, width=64, height=64, seed=13, collect=False, guiding=False,
+                        row_begin=rb, row_end=re)
+            r.iteration()
+            parts.append(r.image())
+            r.close()
+            g.close()
+    finally:
+        full.close()
+        full_g.close()
+    assert np.array_equal(np.concatenate(parts, axis=0), ref)

@@ -3,6 +3,8 @@ against the library exactly as a renderer would link it."""
 import os
 import subprocess
 
+import numpy as np
+
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -37,3 +39,32 @@ def test_cpp_example_runs_on_gpu(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "train: 16 steps" in r.stdout
+
+
+def test_mape_spec_examples():
+    """SPEC.md tracer mape examples (PAPER §7 metric)."""
+    import paper_2303_08064_b200 as nasg
+    img = np.ones((2, 3), np.float32)
+    assert nasg.mape(img, img) == 0.0
+    render = np.array([[1, 1, 1], [2, 2, 2]], np.float32)
+    ref = np.ones((2, 3), np.float32)
+    assert abs(nasg.mape(render, ref) - 0.5 * (1 / 1.01)) < 1e-12
+    rng = np.random.default_rng(0)
+    a, b = rng.random((5000, 3)).astype(np.float32), rng.random((5000, 3)).astype(np.float32)
+    perm = rng.permutation(5000)
+    assert abs(nasg.mape(a, b) - nasg.mape(a[perm], b[perm])) < 1e-12
+    # the worst floor(0.1 %) of pixels are dropped
+    a2 = a.copy()
+    a2[:5] = 1e6
+    a64, b64 = a2.astype(np.float64), b.astype(np.float64)
+    expect = np.sort((np.abs(a64 - b64) / (b64 + 0.01)).mean(1))[:-5].mean()
+    assert abs(nasg.mape(a2, b) - expect) < 1e-9
+
+
+def test_render_scene_bounds():
+    import paper_2303_08064_b200 as nasg
+    for s in (nasg.SCENE_FURNACE, nasg.SCENE_BOX, nasg.SCENE_CRACK, nasg.SCENE_DARK):
+        lo, hi = nasg.scene_bounds(s)
+        assert np.all(hi > lo)
+    with pytest.raises(nasg.NasgError):
+        nasg.scene_bounds(99)
