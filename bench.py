@@ -13,6 +13,8 @@ Also reported (same JSON line):
   roofline     the fused query kernel vs the measured bf16 tensor peak
   cpu_baseline the reference (oracle/_ref, all host cores) on a bounded sample
   train        config 3: fused fwd+KL+bwd+Adam at 2^18 samples per step
+  render       configs 4-5: the guided progressive render loop (1024^2 x 512 spp;
+               4K sharded by pixel rows over the ranks)
 
 `--impl reference` times the reference's own CPU implementation (oracle/_ref:
 the unmodified reference TUs + Eigen-API shim, OpenMP over queries) instead.
@@ -197,6 +199,50 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
             "gpu_launches": launches, "last_mean_loss": st.mean_loss}
 
 
+def bench_render(nasg, args, ws, rank, width, height, iters, label):
+    """Configs 4-5: the guided progressive render loop (nasg_render_*): per iteration one
+    path per pixel of this rank's rows (wavefront tracer, NEE+MIS, guided scattering
+    through the fused network query), sample collection, one train_iteration (S = 2^16,
+    t = 2^12: 16 Adam steps, data-parallel over ranks through NCCL) and accumulation.
+    Rows are split evenly over ranks (strong scaling of the fixed image)."""
+    import torch
+    scene = nasg.SCENE_CRACK
+    lo, hi = nasg.scene_bounds(scene)
+    g = nasg.Guide(nasg.TrainerConfig(seed=5), bmin=lo, bmax=hi)
+    g.precision = nasg.NASG_MLP_BF16
+    g.train_precision = nasg.NASG_MLP_BF16
+    if ws > 1:
+        import torch.distributed as dist
+        uid = [g.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        g.comm_init(uid[0], rank, ws)
+    rb, re = rank * height // ws, (rank + 1) * height // ws
+    r = nasg.Render(g, scene=scene, width=width, height=height, row_begin=rb, row_end=re, seed=3)
+    torch.cuda.synchronize()
+    barrier(ws)
+    l0 = g.kernel_launches + r.kernel_launches
+    t0 = time.perf_counter()
+    verts = guided = kept = 0
+    for _ in range(iters):
+        st = r.iteration()
+        verts += st["vertices"]
+        guided += st["guided_vertices"]
+        kept += st["kept"]
+    torch.cuda.synchronize()
+    dt = max_over_ranks(time.perf_counter() - t0, ws)
+    launches = g.kernel_launches + r.kernel_launches - l0
+    img = r.image()
+    finite = bool(np.isfinite(img).all())
+    r.close()
+    g.close()
+    return {"workload": label, "scene": "crack (box lit through a slit: anisotropic indirect light)",
+            "iterations": iters, "seconds": dt, "ms_per_iteration": 1e3 * dt / iters,
+            "paths_per_s": width * height * iters / dt, "vertices_per_s_rank0": verts / dt,
+            "guided_queries_per_s_rank0": guided / dt, "train_samples_per_iteration_rank0": kept / iters,
+            "gpu_launches_rank0": launches, "final_b": st["b"], "image_finite": finite, "scaling": "strong",
+            "cpu_baseline": None, "note": "the reference specifies this tracer (SPEC.md:378-478) but ships no code"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -208,6 +254,8 @@ def main():
     ap.add_argument("--train-samples", type=int, default=1 << 18)
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--no-train", action="store_true")
+    ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--render-4k-iters", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
@@ -311,6 +359,13 @@ def main():
     torch.cuda.empty_cache()
 
     train = None if args.no_train else {p: bench_train(nasg.Guide, nasg, args, ws, rank, p) for p in ("bf16", "fp32")}
+    render = None
+    if not args.no_render:
+        render = {"config4": bench_render(nasg, args, ws, rank, 1024, 1024, 512,
+                                          "config 4: 1024x1024, 512 spp, interleaved train/render"),
+                  "config5": bench_render(nasg, args, ws, rank, 3840, 2160, args.render_4k_iters,
+                                          f"config 5: 3840x2160 sharded by pixel rows over {ws} GPU(s), "
+                                          f"{args.render_4k_iters} spp")}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_reference_rate(1 << 30, args.cpu_seconds)
@@ -322,7 +377,7 @@ def main():
                                        f"64-128-128-128-65 MLP", "queries_per_step_per_gpu": n,
                            "l2": "inputs (1 GiB/GPU) exceed the 126 MB L2", "parallelism": f"query shards x{ws}"},
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
-                "clocks": clk.summary(), "train": train}
+                "clocks": clk.summary(), "train": train, "render": render}
         print(json.dumps(line), flush=True)
 
 
