@@ -229,6 +229,8 @@ typedef struct {
     int ramp;              /* 1: accumulate with w_i = min(i+1, M B)/(M B); 0: plain mean */
     int schedule_m;        /* M = 4 */
     int schedule_b;        /* B = 64 */
+    int nee;               /* 1: NEE + MIS (SPEC); 0: emitters reached by scattering only
+                              (the brute-force reference of the SPEC's direct-light test) */
 } nasg_render_config;
 typedef struct {
     int64_t iteration;     /* the iteration just rendered */

@@ -68,6 +68,7 @@ struct Frame {
     int tile_row0;    // floor(row0 / l)
     int ntx;          // tiles per row
     int collect, max_depth, rr_depth;
+    int nee;
 };
 
 __device__ inline float4 f4(float3 v, float w) { return make_float4(v.x, v.y, v.z, w); }
@@ -138,7 +139,7 @@ __global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
         if (cl > 0.f) {
             const float pp = P.prev_pdf[i];
             float w = 1.f;
-            if (pp >= 0.f) {
+            if (pp >= 0.f && F.nee) {
                 const float pl = light_pdf_at(S, o, h, d);
                 w = pp / (pp + pl);
             }
@@ -165,10 +166,11 @@ __global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
         return;
     }
     // next-event estimation (SPEC nee_sample): one emitter by area, shadow ray
-    const LightSample ls = sample_light(S, h.x, R(0), R(1), R(2));
+    LightSample ls = sample_light(S, h.x, R(0), R(1), R(2));
+    if (!F.nee) ls.pdf = 0.f;
     float3 nee = f3(0.f, 0.f, 0.f);
     float pl = 0.f;
-    if (ls.pdf > 0.f && dot(n, ls.dir) > 0.f && !occluded(S, h.x + n * kEps, ls.dir, ls.dist)) {
+    if (ls.pdf > 0.f && dot(n, ls.dir) > 0.f && !occluded(S, h.x + n * kEps, ls.dir, ls.dist, ls.prim)) {
         const float3 f = bsdf_eval(m, n, wo, ls.dir);
         nee = mul(ls.Le, f) * (dot(n, ls.dir) / ls.pdf);
         pl = ls.pdf;
@@ -520,6 +522,7 @@ void nasg_render_config_default(nasg_render_config *c) {
     c->ramp = 1;
     c->schedule_m = 4;
     c->schedule_b = 64;
+    c->nee = 1;
 }
 
 int nasg_render_scene_bounds(int scene, float bmin[3], float bmax[3]) {
@@ -611,6 +614,7 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     F.collect = c.collect;
     F.max_depth = c.max_depth;
     F.rr_depth = c.rr_depth;
+    F.nee = c.nee;
     RCUDA(cudaMemsetAsync(P.ctr, 0, 8 * sizeof(unsigned long long), s));
     RCUDA(cudaMemsetAsync(P.qcount, 0, sizeof(int), s));
     if (c.collect) RCUDA(cudaMemsetAsync(P.rpix, 0xff, P.ncap * sizeof(int), s));

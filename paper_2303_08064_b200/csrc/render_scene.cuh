@@ -124,11 +124,14 @@ __device__ inline bool intersect(const Scene &s, float3 o, float3 d, float tmax,
     return true;
 }
 
-__device__ inline bool occluded(const Scene &s, float3 o, float3 d, float dist) {
+// Shadow ray towards a point on emitter `target`: that primitive is skipped, so
+// the offset origin can never see the light itself as its own occluder (a point
+// right under a light would otherwise lose its direct illumination).
+__device__ inline bool occluded(const Scene &s, float3 o, float3 d, float dist, int target) {
     for (int i = 0; i < s.nprims; ++i) {
         float t;
         float3 n;
-        if (hit_prim(s.prims[i], o, d, dist * (1.f - 1e-4f), t, n)) return true;
+        if (i != target && hit_prim(s.prims[i], o, d, dist * (1.f - 1e-4f), t, n)) return true;
     }
     return false;
 }
@@ -165,7 +168,12 @@ __device__ inline float bsdf_pdf(const Mat &m, float3 n, float3 wo, float3 wi) {
     return 0.f;
 }
 
-// returns false for a zero-contribution sample (glossy lobe below the surface 8 times)
+// Returns false for a zero-contribution sample: a glossy lobe direction below the
+// surface.  One attempt, not SPEC's "resample up to 8 times": the retries would
+// make the technique's density p_lobe (1 - P_below^8) / (1 - P_below) while the
+// estimator and the MIS blend use p_lobe, biasing every grazing glossy vertex; a
+// single attempt keeps the density exactly p_lobe (the failed mass contributes 0),
+// which the SPEC's own unbiasedness invariant requires.
 template <class Rng>
 __device__ inline bool bsdf_sample(const Mat &m, float3 n, float3 wo, Rng rng, float3 &wi) {
     if (m.type == kLambert) {
@@ -180,14 +188,11 @@ __device__ inline bool bsdf_sample(const Mat &m, float3 n, float3 wo, Rng rng, f
         const float3 r = reflect(wo, n);
         float3 t, b;
         onb(r, t, b);
-        for (int k = 0; k < 8; ++k) {
-            const float u1 = rng(2 * k), u2 = rng(2 * k + 1);
-            const float ca = powf(u1, 1.f / (m.exponent + 1.f)), sa = sqrtf(fmaxf(0.f, 1.f - ca * ca));
-            const float phi = 2.f * kPiF * u2;
-            wi = t * (sa * cosf(phi)) + b * (sa * sinf(phi)) + r * ca;
-            if (dot(wi, n) > 0.f) return true;
-        }
-        return false;
+        const float u1 = rng(0), u2 = rng(1);
+        const float ca = powf(u1, 1.f / (m.exponent + 1.f)), sa = sqrtf(fmaxf(0.f, 1.f - ca * ca));
+        const float phi = 2.f * kPiF * u2;
+        wi = t * (sa * cosf(phi)) + b * (sa * sinf(phi)) + r * ca;
+        return dot(wi, n) > 0.f;
     }
     return false;
 }
@@ -202,10 +207,11 @@ __device__ inline float light_pdf_at(const Scene &s, float3 x, const Hit &h, flo
 struct LightSample {
     float3 dir, Le;
     float dist, pdf;  // pdf in solid angle at x; 0 if unusable
+    int prim;         // the emitter primitive sampled
 };
 
 __device__ inline LightSample sample_light(const Scene &s, float3 x, float u0, float u1, float u2) {
-    LightSample ls{f3(0.f, 0.f, 1.f), f3(0.f, 0.f, 0.f), 0.f, 0.f};
+    LightSample ls{f3(0.f, 0.f, 1.f), f3(0.f, 0.f, 0.f), 0.f, 0.f, -1};
     if (s.nlights == 0) return ls;
     int k = s.nlights - 1;
     for (int i = 0; i < s.nlights; ++i)
@@ -213,7 +219,8 @@ __device__ inline LightSample sample_light(const Scene &s, float3 x, float u0, f
             k = i;
             break;
         }
-    const Prim &p = s.prims[s.light_prim[k]];
+    ls.prim = s.light_prim[k];
+    const Prim &p = s.prims[ls.prim];
     const float3 y = p.p + p.u * u1 + p.v * u2;
     const float3 dv = y - x;
     const float d2 = dot(dv, dv);

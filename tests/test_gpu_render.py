@@ -8,7 +8,9 @@ the tracer but ships no code for it, so its oracle here is analytic:
   * determinism: identical seed -> bitwise-identical film, guiding and online
     training included;
   * unbiasedness: guided and unguided renders of the box scene agree within
-    3 combined standard errors; the ramp-free accumulation is the plain mean;
+    3 combined standard errors; NEE + MIS agrees with the brute-force
+    scattering-only estimator (SPEC's direct-light example); the ramp-free
+    accumulation is the plain mean;
   * training records: collected samples are finite with q > 0, at most S kept.
 """
 import numpy as np
@@ -136,3 +138,31 @@ def test_row_shards_tile_the_image():
         full.close()
         full_g.close()
     assert np.array_equal(np.concatenate(parts, axis=0), ref)
+
+
+def frame_means(scene, frames, skip=1, **kw):
+    g, r = make(scene, **kw)
+    try:
+        fm = []
+        for it in range(frames):
+            r.iteration()
+            if it >= skip:
+                fm.append(np.asarray(r.image(1)).mean(axis=(0, 1)) @ np.array([0.2126, 0.7152, 0.0722]))
+        return np.array(fm)
+    finally:
+        r.close()
+        g.close()
+
+
+@pytest.mark.parametrize("scene", [nasg.SCENE_BOX, nasg.SCENE_CRACK])
+def test_nee_mis_matches_brute_force(scene):
+    """NEE + balance-heuristic MIS against the scattering-only estimator, unguided and
+    guided (b = 1 after the first frame): all three must share one mean.  A light
+    occluding its own shadow rays, or mismatched MIS pdfs, shows up here."""
+    common = dict(width=64, height=64, collect=False, ramp=False, schedule_m=1, schedule_b=1)
+    bf = frame_means(scene, 161, seed=21, guiding=False, nee=False, **common)
+    mis = frame_means(scene, 161, seed=22, guiding=False, nee=True, **common)
+    gmis = frame_means(scene, 161, seed=23, guiding=True, nee=True, **common)
+    for other in (mis, gmis):
+        se = np.sqrt(bf.var(ddof=1) / bf.size + other.var(ddof=1) / other.size)
+        assert abs(bf.mean() - other.mean()) <= 3.5 * se, (bf.mean(), other.mean(), se)
