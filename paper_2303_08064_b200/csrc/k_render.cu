@@ -15,7 +15,7 @@
 //                        record of collected paths, Russian roulette
 //   K_scan + K_records  per-vertex incident radiance by back-propagation
 //                        (L_i = (L_end - L_before) / beta), TrainingSamples in
-//                        deterministic tile order, first S kept
+//                        deterministic tile order, an evenly spread S kept
 //   K_accumulate film += w_i L (non-finite paths discarded and counted)
 //   train_iteration + publish, stride_update (host)
 // Path state is SoA in HBM (float4 per quantity); the guide queue is compacted
@@ -307,9 +307,16 @@ __global__ void k_records(Paths P) {
     if (pi < 0) return;
     const int cnt = P.rcnt[r];
     const float4 Le = P.L[pi];
+    // more samples than the capacity S: keep an evenly spread S of them (sample o
+    // goes to slot floor(o S / T) when that slot changes), not the first S rows
+    const int64_t T = (int64_t)P.ctr[4], Sc = P.cap_samples;
     for (int k = 0; k < cnt; ++k) {
-        const int64_t o = (int64_t)P.roff[r] + k;
-        if (o >= P.cap_samples) break;
+        int64_t o = (int64_t)P.roff[r] + k;
+        if (T > Sc) {
+            const int64_t a = o * Sc / T, b = (o + 1) * Sc / T;
+            if (b == a) continue;
+            o = a;
+        }
         const size_t at = (size_t)k * P.ncap + r;
         const float4 b = P.rbeta[at], lb = P.rlb[at], fc = P.rfc[at];
         // incident radiance along omega_i: everything gathered after this vertex
