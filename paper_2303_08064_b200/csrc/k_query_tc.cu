@@ -2,22 +2,24 @@
 // tcgen05 (UMMA M=128, accumulators in TMEM) -> fp32 NASG epilogue.
 //
 // Persistent CTA per SM (16 warps), warp-specialised into two pipelines
-// ("pairs").  Pair m = one MLP warpgroup + one NASG warpgroup:
-//   MLP warpgroup m (warps 4m..4m+3, 112 registers): per 128-row tile, thread t
-//     owns row t = TMEM lane t.  Load + one-blob encode (encoding.cpp:21-46) ->
-//     bf16 A tile in smem; layers 1-3: thread 0 issues the layer's UMMAs
-//     (K/16 x M128) into the group's TMEM accumulator [128m, 128m+128),
-//     commit -> acc_full[m]; the group drains TMEM -> ReLU -> bf16 -> A tile.
-//     The output layer goes to the pair's raw buffer (TMEM columns
-//     [256+128m, 256+128m+NP)) once the NASG group has emptied it; its commit
-//     arrives on raw_full[m].
-//   NASG warpgroup m (warps 8+4m..11+4m, 144 registers): waits raw_full[m],
-//     copies its rows' NP raw outputs TMEM -> registers, releases the buffer
-//     (raw_empty[m]) and runs decode / sample / pdf (nasg_math.cuh) while the
-//     MLP group already computes the next tile.
-// The MLP side is bound by tensor-core latency, the NASG side by instruction
-// issue; decoupling them lets the two overlap instead of taking turns inside
-// one warpgroup.  setmaxnreg moves registers from the MLP to the NASG groups.
+// ("pairs").  Pair m = one MLP warpgroup + one NASG warpgroup; thread t of a
+// group owns row t of the pair's current 128-row tile (= TMEM lane t).
+//   MLP warpgroup m (warps 4m..4m+3, 104 registers): only the latency-critical
+//     chain.  Layer 0 reads the encoded tile E_m straight from smem; for
+//     layers 1-3 the group drains its TMEM accumulator [128m, 128m+128) ->
+//     ReLU -> bf16 -> A tile; warp 0 issues each layer's UMMAs with one
+//     elected lane and commits them to acc_full[m].  The output layer writes
+//     the pair's raw buffer (TMEM [256+128m, 256+128m+NP)) once the NASG group
+//     has emptied it and commits to raw_full[m].
+//   NASG warpgroup m (warps 8+4m..11+4m, 152 registers): everything with
+//     slack.  It stages tile inputs by TMA bulk copies two tiles ahead, encodes
+//     the NEXT tile (one-blob, encoding.cpp:21-46) into E_m as soon as the
+//     MLP's layer 0 has consumed it (e_empty[m]), then waits raw_full[m],
+//     copies its rows' raw outputs to registers, releases the buffer and runs
+//     decode / sample / pdf (nasg_math.cuh) while the MLP computes the next tile.
+// The MLP chain (4 MMA round trips) is bound by latency, the NASG side by
+// instruction issue; this split keeps the chain free of every instruction
+// that can run elsewhere.  setmaxnreg moves registers from MLP to NASG groups.
 // Only the 52 B/query of inputs and 16-20 B/query of outputs touch HBM.
 #include <cuda_bf16.h>
 
@@ -27,21 +29,36 @@
 #include "tc_common.cuh"
 
 
+// Development-only phase timestamps (build with EXTRA=-DNASG_TRACE into a
+// scratch directory; the shipped library compiles them out): clock64() of
+// thread 0 of pair 0 in CTA 0 at fixed points of the first 32 tiles.
+#ifdef NASG_TRACE
+__device__ unsigned long long g_trace[2 * 32 * 16];
+extern "C" int nasg_trace_read(void *host) { return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)); }
+#define NASG_TRACE_AT(role, k, slot)                                                   \
+    if (blockIdx.x == 0 && t == 0 && m == 0 && (k) < 32)                               \
+        g_trace[((role) * 32 + (k)) * 16 + (slot)] = clock64();
+#else
+#define NASG_TRACE_AT(role, k, slot)
+#endif
+
 namespace nasg {
 
 namespace {
 
 constexpr int kPairs = 2;                       // MLP + NASG warpgroup pairs
 constexpr int kThreads = 2 * kPairs * 128;      // 16 warps
-constexpr int kRegsMlp = 112, kRegsNasg = 144;  // 2 x 128 x (112 + 144) = 64K registers
+constexpr int kRegsMlp = 104, kRegsNasg = 152;  // 2 x 128 x (104 + 152) = 64K registers
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one bf16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
+constexpr uint32_t kEBytes = 128 * 64 * 2;      // one encoded tile (layer 0's A operand, K = 64)
 constexpr uint32_t kInBytes = 128 * 52;         // one tile of inputs: 13-float rows or 3 x 2 KB SoA
 
 template <int N>
 constexpr size_t smem_bytes() {
-    return align1k(img_bytes(N)) + kPairs * kABytes + 2 * kPairs * kInBytes + (5 * kPairs + 2) * sizeof(uint64_t);
+    return align1k(img_bytes(N)) + kPairs * (kABytes + kEBytes) + 2 * kPairs * kInBytes +
+           (7 * kPairs + 2) * sizeof(uint64_t);
 }
 
 }  // namespace
@@ -96,12 +113,15 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     constexpr uint32_t IMG = img_bytes(N);
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
-    constexpr uint32_t IN_OFF = A_OFF + kPairs * kABytes;  // input staging: [pair][2 buffers]
+    constexpr uint32_t E_OFF = A_OFF + kPairs * kABytes;    // encoded tiles E_m
+    constexpr uint32_t IN_OFF = E_OFF + kPairs * kEBytes;   // input staging: [pair][2 buffers]
     uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + IN_OFF + 2 * kPairs * kInBytes);
     uint64_t *raw_full = acc_full + kPairs;
     uint64_t *raw_empty = raw_full + kPairs;
     uint64_t *in_full = raw_empty + kPairs;  // [pair][buffer]
-    uint64_t *w_bar = in_full + 2 * kPairs;
+    uint64_t *e_full = in_full + 2 * kPairs;
+    uint64_t *e_empty = e_full + kPairs;
+    uint64_t *w_bar = e_empty + kPairs;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     __shared__ int s_clamped;
 
@@ -121,6 +141,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             tc::mbar_init(&raw_empty[i], 4);  // one arrival per NASG warp
             tc::mbar_init(&in_full[2 * i], 1);
             tc::mbar_init(&in_full[2 * i + 1], 1);
+            tc::mbar_init(&e_full[i], 1);
+            tc::mbar_init(&e_empty[i], 1);
         }
         tc::mbar_init(w_bar, 1);
         s_clamped = 0;
@@ -142,30 +164,36 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsMlp));
         const uint32_t my_acc = tmem + m * 128 + ((uint32_t)(wq * 32) << 16);
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + m * kABytes);
-        const uint32_t a_row64 = a_base + (t >> 3) * 1024 + (t & 7) * 16;   // K = 64 layout
+        const uint32_t e_base = tc::smem_u32(smem + E_OFF + m * kEBytes);
         const uint32_t a_row128 = a_base + (t >> 3) * 2048 + (t & 7) * 16;  // K = 128 layout
         const uint32_t sW = tc::smem_u32(smem);
-        const float(&inv_ext)[3] = a.bounds.inv_ext;
         uint32_t acc_ph = 0;
-        int clamped = 0;
-        // A tile complete (and our TMEM reads done): warp 0 of the group issues
-        // layer L (compile-time) with one elected lane.  Layers 0-2 accumulate
-        // into the group's TMEM columns; the output layer goes to the pair's raw
-        // buffer once the NASG group has emptied it.
+        // The A operand is complete in smem (and our TMEM reads are done): warp 0
+        // issues layer L with one elected lane.  Layer 0 reads E_m (once the NASG
+        // group has filled it), layers 1-2 accumulate into the group's TMEM
+        // columns, the output layer into the pair's raw buffer once it is empty.
         auto issue = [&](int L, int64_t k) {
-            tc::fence_proxy_async_smem();
-            tc::tc_fence_before();
-            wg_sync(g);
+            if (L > 0) {
+                tc::fence_proxy_async_smem();
+                tc::tc_fence_before();
+                wg_sync(g);
+            }
             if (wq == 0) {
                 __syncwarp();
+                if (L == 0) tc::mbar_wait(&e_full[m], (uint32_t)(k & 1));
                 if (L == 3 && k > 0) tc::mbar_wait(&raw_empty[m], (uint32_t)((k - 1) & 1));
                 tc::tc_fence_after();
                 auto chain = [&](auto lc) {
                     constexpr int LL = decltype(lc)::value;
                     constexpr int K = LL == 0 ? kIn : kHidden;
                     constexpr uint32_t idesc = tc::idesc_bf16(128, LL == 3 ? NP : kHidden);
-                    const uint64_t ad = tc::smem_desc(a_base, 128, K * 16);
-                    const uint64_t bd = tc::smem_desc(sW + w_off(LL), 128, K * 16);
+                    // descriptors rebuilt at issue time from opaque copies of the base
+                    // addresses: hoisted out of the tile loop they would occupy ~60
+                    // registers and spill
+                    const uint32_t abase = tc::opaque(LL == 0 ? e_base : a_base);
+                    const uint32_t bbase = tc::opaque(sW) + w_off(LL);
+                    const uint64_t ad = tc::smem_desc(abase, 128, K * 16);
+                    const uint64_t bd = tc::smem_desc(bbase, 128, K * 16);
                     const uint32_t d = tmem + (LL == 3 ? 256 : 0) + m * 128;
 #pragma unroll
                     for (int kk = 0; kk < K / 16; ++kk)  // +256 B per K=16 slab = +16 in the address field
@@ -181,12 +209,46 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 }
             }
         };
-        // Software pipeline over this group's tiles.  Inputs arrive two tiles
-        // ahead by TMA bulk copies into a double-buffered smem stage (an
-        // async-proxy load is not held up by the fence before each MMA issue,
-        // unlike a register prefetch); the next tile's encoding is computed into
-        // registers while the output-layer MMA of the current tile still reads
-        // the A tile, and stored once that MMA has completed.
+        if (wq == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
+        int64_t k = 0;
+        for (int64_t tile = (int64_t)blockIdx.x * kPairs + m; tile < ntiles; tile += stride, ++k) {
+            NASG_TRACE_AT(0, k, 0)
+            issue(0, k);
+            NASG_TRACE_AT(0, k, 1)
+#pragma unroll 1
+            for (int l = 1; l < 4; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
+                // (layer 1's wait also covers the previous tile's output layer,
+                //  which still read the A tile: commits track all earlier MMAs)
+                wg_wait_acc(&acc_full[m], acc_ph, g, wq);
+                NASG_TRACE_AT(0, k, 2 * l)
+                if (l == 1 && t == 0) tc::mbar_arrive(&e_empty[m]);  // layer 0 has consumed E_m
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                    float v[32];
+                    tc::tmem_ld32(my_acc + q4 * 32, v);
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        uint32_t p[4];
+#pragma unroll
+                        for (int h = 0; h < 4; ++h)
+                            p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                        tc::st_shared_v4(a_row128 + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                    }
+                }
+                issue(l, k);
+                NASG_TRACE_AT(0, k, 2 * l + 1)
+            }
+        }
+    } else {
+        // ============================ NASG warpgroup ===========================
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsNasg));
+        const uint32_t my_raw = tmem + 256 + m * 128 + ((uint32_t)(wq * 32) << 16);
+        const uint32_t e_row64 = tc::smem_u32(smem + E_OFF + m * kEBytes) + (t >> 3) * 1024 + (t & 7) * 16;
+        const float(&inv_ext)[3] = a.bounds.inv_ext;
+        int clamped = 0;
+        // Inputs arrive two tiles ahead by TMA bulk copies into a double-buffered
+        // smem stage; kt = index of the tile within this pair's sequence.
         const bool tma_in = a.packed ? ((reinterpret_cast<uintptr_t>(a.packed) & 15) == 0) : true;
         auto load_tile = [&](int64_t tl, int buf) {  // thread 0 only
             if (tl >= ntiles) return;
@@ -207,7 +269,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 tc::bulk_g2s(dst + 4096, a.nrm + q0, bytes, bar);
             }
         };
-        auto encode = [&](int64_t tl, int64_t kt, uint32_t (&pk)[32]) {  // tile tl = this group's kt-th
+        // encode tile tl (the pair's kt-th) into E_m and hand it to the MLP group
+        auto encode = [&](int64_t tl, int64_t kt) {
             const int buf = (int)(kt & 1);
             tc::mbar_wait(&in_full[2 * m + buf], (uint32_t)((kt >> 1) & 1));
             const int64_t q = tl * 128 + t;
@@ -233,56 +296,33 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     nrm = *reinterpret_cast<const float4 *>(src + 4096 + t * 16);
                 }
             }
-            return encode_row_pack(valid, x, wo, nrm, a.bounds, inv_ext, pk);
-        };
-        // One loop with a single encode site (k = -1 only encodes the first
-        // tile): the kernel's two roles run concurrently, so code size matters
-        // for the instruction cache.
-        uint32_t pk[32];
-        if (wq == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
-        int64_t tile = (int64_t)blockIdx.x * kPairs + m - stride;
-        if (t == 0) {
-            load_tile(tile + stride, 0);
-            load_tile(tile + 2 * stride, 1);
-        }
-        uint32_t raw_ph = 0;
-        for (int64_t k = -1;; tile += stride, ++k) {
-            if (k >= 0) {
-                issue(0, k);
-                if (t == 0) load_tile(tile + 2 * stride, (int)(k & 1));  // its buffer was read by encode(k)
-#pragma unroll 1
-                for (int l = 1; l < 4; ++l) {  // hidden layers: TMEM -> ReLU -> bf16 -> next A operand
-                    wg_wait_acc(&acc_full[m], acc_ph, g, wq);
-#pragma unroll
-                    for (int q4 = 0; q4 < 4; ++q4) {
-                        float v[32];
-                        tc::tmem_ld32(my_acc + q4 * 32, v);
-                        tc::tmem_ld_wait();
-#pragma unroll
-                        for (int c = 0; c < 4; ++c) {
-                            uint32_t p[4];
-#pragma unroll
-                            for (int h = 0; h < 4; ++h)
-                                p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
-                            tc::st_shared_v4(a_row128 + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
-                        }
-                    }
-                    issue(l, k);
-                }
+            uint32_t pk[32];
+            clamped += encode_row_pack(valid, x, wo, nrm, a.bounds, inv_ext, pk);
+            store_row_pack(pk, e_row64);
+            tc::fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
+            wg_sync(g);
+            if (t == 0) {
+                tc::mbar_arrive(&e_full[m]);
+                load_tile(tl + 2 * stride, buf);  // every row of this buffer has been read
             }
-            const int64_t next = tile + stride;
-            if (next < ntiles) clamped += encode(next, k + 1, pk);
-            if (k >= 0) wg_wait_acc(&raw_full[m], raw_ph, g, wq);  // output layer done: the A tile is free
-            if (next >= ntiles) break;
-            store_row_pack(pk, a_row64);
+        };
+        int64_t tile = (int64_t)blockIdx.x * kPairs + m;
+        if (t == 0) {
+            load_tile(tile, 0);
+            load_tile(tile + stride, 1);
         }
-        if (clamped) atomicAdd(&s_clamped, clamped);
-    } else {
-        // ============================ NASG warpgroup ===========================
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsNasg));
-        const uint32_t my_raw = tmem + 256 + m * 128 + ((uint32_t)(wq * 32) << 16);
-        int64_t k = 0;
-        for (int64_t tile = (int64_t)blockIdx.x * kPairs + m; tile < ntiles; tile += stride, ++k) {
+        if (tile < ntiles) encode(tile, 0);
+        uint32_t e_ph = 0;
+        for (int64_t k = 0; tile < ntiles; tile += stride, ++k) {
+            // the next tile's encoding first: the MLP needs it right after this
+            // tile's output layer, the raw outputs arrive only then
+            NASG_TRACE_AT(1, k, 0)
+            if (tile + stride < ntiles) {
+                wg_wait_acc(&e_empty[m], e_ph, g, wq);
+                NASG_TRACE_AT(1, k, 1)
+                encode(tile + stride, k + 1);
+            }
+            NASG_TRACE_AT(1, k, 2)
             const int64_t q = tile * 128 + t;
             const bool valid = q < nrows;
             float4 xi = make_float4(0.f, 0.f, 0.f, 0.f), dir = xi, dnee = xi;
@@ -300,6 +340,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             }
             uint32_t ph = (uint32_t)(k & 1);
             wg_wait_acc(&raw_full[m], ph, g, wq);
+            NASG_TRACE_AT(1, k, 3)
             float raw[NP];
             {
                 float v[32];
@@ -342,7 +383,9 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     for (int j = 0; j < D; ++j) a.raw[q * D + j] = raw[packed_col(j, N)];
                 }
             }
+            NASG_TRACE_AT(1, k, 4)
         }
+        if (clamped) atomicAdd(&s_clamped, clamped);
     }
     tc::tc_fence_before();
     __syncthreads();

@@ -9,6 +9,12 @@
 namespace nasg {
 namespace tc {
 
+// a value the compiler cannot see through (keeps derived values from being hoisted)
+__device__ __forceinline__ uint32_t opaque(uint32_t x) {
+    asm volatile("mov.b32 %0, %0;" : "+r"(x));
+    return x;
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
