@@ -1,7 +1,7 @@
 // fp32 query path: fused encode -> 4-layer MLP (FFMA) -> NASG epilogue,
 // plus the weight-packing kernel and the raw-output parity kernels.
 //
-// One persistent CTA (256 threads) per SM walks 128-query tiles.  Per tile:
+// Two persistent CTAs (256 threads) per SM walk 128-query tiles.  Per tile:
 //   K1 encode     encode_inputs (encoding.cpp:21-46) into smem, feature-major
 //   K2 MLP        forward<float> (net.hpp:69-76), 4 x tile_layer
 //   K3 epilogue   decode + mixture_sample + mixture_pdf, or mixture/guided
@@ -83,12 +83,15 @@ __device__ __forceinline__ int encode_row(const float4 x, const float4 wo, const
 
 // ---------------------------------------------------------- fused kernel --
 template <int N, int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(256, 2)
 query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
     extern __shared__ __align__(16) float smem[];
+    // one activation tile, updated in place: each layer keeps its outputs in
+    // registers until every thread has read its last input chunk (tile_layer's
+    // chunk barrier), so ~84 KB of smem -> two CTAs per SM, and one CTA's
+    // half-occupied NASG epilogue overlaps the other's FFMA GEMMs
     float *actA = smem;                      // [128][kLda]
-    float *actB = actA + kHidden * kLda;     // [128][kLda]
-    float *wbuf = actB + kHidden * kLda;     // [2][16][128]
+    float *wbuf = actA + kHidden * kLda;     // [2][16][128]
     __shared__ int s_clamped;
     const int tid = threadIdx.x;
     const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
@@ -111,10 +114,10 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
             }
         }
         __syncthreads();
-        tile_layer<128, kIn, kEpiRelu>(actA, actB, W1, wbuf, nullptr, tid);
-        tile_layer<128, kHidden, kEpiRelu>(actB, actA, W2, wbuf, nullptr, tid);
-        tile_layer<128, kHidden, kEpiRelu>(actA, actB, W3, wbuf, nullptr, tid);
-        tile_layer<128, kHidden, kEpiNone>(actB, actA, W4, wbuf, nullptr, tid);
+        tile_layer<128, kIn, kEpiRelu>(actA, actA, W1, wbuf, nullptr, tid);
+        tile_layer<128, kHidden, kEpiRelu>(actA, actA, W2, wbuf, nullptr, tid);
+        tile_layer<128, kHidden, kEpiRelu>(actA, actA, W3, wbuf, nullptr, tid);
+        tile_layer<128, kHidden, kEpiNone>(actA, actA, W4, wbuf, nullptr, tid);
         if (tid < kTileRows) {
             const int64_t q = row0 + tid;
             if (q < nrows) {
@@ -146,12 +149,12 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
     if (tid == 0 && s_clamped && a.clamp_count) atomicAdd(a.clamp_count, (unsigned long long)s_clamped);
 }
 
-constexpr size_t kQuerySmem = (2 * kHidden * kLda + 2 * kChunk * 128) * sizeof(float);
+constexpr size_t kQuerySmem = (kHidden * kLda + 2 * kChunk * 128) * sizeof(float);
 
 template <int N>
 static int query_fp32_n(QueryMode mode, const float *wp, const QueryArgs &a, int num_sms, cudaStream_t s) {
     const int64_t ntiles = (a.n + kTileRows - 1) / kTileRows;
-    const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
+    const int grid = (int)(ntiles < 2 * num_sms ? ntiles : 2 * num_sms);  // two CTAs per SM
     if (grid == 0) return 0;
     switch (mode) {
 #define NASG_LAUNCH(M)                                                                             \
