@@ -97,31 +97,36 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         const uint32_t sW = tc::smem_u32(smem);
         // forward layer l (0..3): A = activations (K = 64 | 128), B = W_l^T image (K-major)
         // backward through W_l (l = 3, 2, 1): A = delta (K = NP | 128), B = the same image read MN-major
+        // warp 0 of the group issues with one elected lane; descriptors are rebuilt
+        // from opaque base addresses (hoisted they would pin ~60 registers)
         auto issue = [&](int l, bool bwd) {
             tc::fence_proxy_async_smem();
             tc::tc_fence_before();
             wg_sync(g);
-            if (t == 0) {
-                tc::mbar_wait(w_bar, 0);
+            if ((warp & 3) == 0) {
+                __syncwarp();
                 tc::tc_fence_after();
-                const uint32_t d = tmem + g * 128, b0 = sW + w_off(l);
+                const uint32_t d = tmem + g * 128;
+                const uint32_t abase = tc::opaque(a_base), b0 = tc::opaque(sW) + w_off(l);
                 if (!bwd) {
                     const int K = l == 0 ? kIn : kHidden;
                     const uint32_t sbo = (uint32_t)K * 16u;
                     const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
-                    for (int k = 0; k < K / 16; ++k)
-                        tc::mma_bf16(d, tc::smem_desc(a_base + k * 256, 128, sbo), tc::smem_desc(b0 + k * 256, 128, sbo),
-                                     idesc, k > 0 ? 1u : 0u);
+                    const uint64_t ad = tc::smem_desc(abase, 128, sbo), bdsc = tc::smem_desc(b0, 128, sbo);
+                    for (int k = 0; k < K / 16; ++k)  // +256 B per K=16 slab = +16 in the address field
+                        tc::mma_bf16_elect(d, ad + (uint64_t)(k * 16), bdsc + (uint64_t)(k * 16), idesc,
+                                           k > 0 ? 1u : 0u);
                 } else {
                     const int K = l == 3 ? NP : kHidden;              // contraction over W_l's output index
                     const uint32_t sbo_a = (uint32_t)K * 16u;          // delta tile, K-major
                     const uint32_t lbo_b = (uint32_t)kHidden * 16u;    // image rows (out index) in 8-groups
                     const uint32_t idesc = tc::idesc_bf16(128, kHidden, false, true);
-                    for (int k = 0; k < K / 16; ++k)
-                        tc::mma_bf16(d, tc::smem_desc(a_base + k * 256, 128, sbo_a),
-                                     tc::smem_desc(b0 + k * 2 * lbo_b, lbo_b, 128), idesc, k > 0 ? 1u : 0u);
+                    const uint64_t ad = tc::smem_desc(abase, 128, sbo_a), bdsc = tc::smem_desc(b0, lbo_b, 128);
+                    for (int k = 0; k < K / 16; ++k)  // B advances 2 x 8 image rows per K=16 slab
+                        tc::mma_bf16_elect(d, ad + (uint64_t)(k * 16), bdsc + (uint64_t)(k * 2 * lbo_b / 16), idesc,
+                                           k > 0 ? 1u : 0u);
                 }
-                tc::mma_commit(&acc_full[g]);
+                tc::mma_commit_elect(&acc_full[g]);
             }
         };
         uint32_t acc_ph = 0;
@@ -141,6 +146,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         };
         int64_t tile = (int64_t)blockIdx.x * kWGt + g;
         load_sample(tile);
+        if ((warp & 3) == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
         for (; tile < ntiles; tile += stride) {
             const int64_t row = tile * 128 + t;
             const bool valid = row < count;
