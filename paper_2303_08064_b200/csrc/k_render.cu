@@ -13,7 +13,7 @@
 //                        technique, direction, q_mix at it and at the NEE dir
 //               K_update blend pdf, MIS-weighted NEE, throughput, training
 //                        record of collected paths, Russian roulette
-//   K_scan + K_records  per-vertex incident radiance by back-propagation
+//   K_scan_* + K_records  per-vertex incident radiance by back-propagation
 //                        (L_i = (L_end - L_before) / beta), TrainingSamples in
 //                        deterministic tile order, an evenly spread S kept
 //   K_accumulate film += w_i L (non-finite paths discarded and counted)
@@ -54,7 +54,7 @@ struct Paths {
     // training records [depth][ncap]
     int64_t ncap;
     float4 *rx, *rwo, *rn, *rwi, *rfc, *rbeta, *rlb;
-    int *rcnt, *rpix, *roff;
+    int *rcnt, *rpix, *roff, *bsum, *boff;  // record counts, owning path, offsets (block-local + block)
     unsigned long long *ctr;  // 0 vertices, 1 guided, 2 nonfinite, 3 collected
     float4 *film, *frame;
     nasg_train_sample *samples;
@@ -271,31 +271,55 @@ __global__ void k_update(Paths P, Frame F, int bounce) {
     P.prev_pdf[i] = qh;
 }
 
-// exclusive prefix sum of rcnt over ranks (one block; ncap <= 4 S)
-__global__ void k_scan(Paths P) {
-    __shared__ long long part[1024];
-    const int64_t n = P.ncap;
-    const int64_t per = (n + blockDim.x - 1) / blockDim.x;
-    const int64_t b = threadIdx.x * per, e = min(n, b + per);
-    long long s = 0;
-    for (int64_t k = b; k < e; ++k) s += P.rpix[k] >= 0 ? P.rcnt[k] : 0;
-    part[threadIdx.x] = s;
+// Exclusive prefix sum of the collected paths' record counts, in two passes:
+// k_scan_local scans 1024-rank blocks (warp shuffles) and writes block totals,
+// k_scan_blocks scans the block totals (ncap <= 1024^2); k_records adds both.
+__device__ inline int warp_incl_scan(int v) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if ((threadIdx.x & 31) >= o) v += u;
+    }
+    return v;
+}
+
+__global__ void k_scan_local(Paths P) {
+    __shared__ int wsum[32];
+    const int64_t k = (int64_t)blockIdx.x * 1024 + threadIdx.x;
+    const int c = (k < P.ncap && P.rpix[k] >= 0) ? P.rcnt[k] : 0;
+    const int incl = warp_incl_scan(c);
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 31) wsum[w] = incl;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        long long acc = 0;
-        for (int k = 0; k < (int)blockDim.x; ++k) {
-            const long long v = part[k];
-            part[k] = acc;
-            acc += v;
-        }
-        P.ctr[3] += (unsigned long long)acc;
-        P.ctr[4] = (unsigned long long)acc;
+    if (w == 0) {
+        const int t = warp_incl_scan(wsum[lane]);
+        wsum[lane] = t;
     }
     __syncthreads();
-    long long acc = part[threadIdx.x];
-    for (int64_t k = b; k < e; ++k) {
-        P.roff[k] = (int)acc;
-        acc += P.rpix[k] >= 0 ? P.rcnt[k] : 0;
+    const int excl = incl - c + (w > 0 ? wsum[w - 1] : 0);
+    if (k < P.ncap) P.roff[k] = excl;
+    if (threadIdx.x == 1023) P.bsum[blockIdx.x] = excl + c;
+}
+
+__global__ void k_scan_blocks(Paths P, int nblocks) {
+    __shared__ int wsum[32];
+    const int i = threadIdx.x;
+    const int c = i < nblocks ? P.bsum[i] : 0;
+    const int incl = warp_incl_scan(c);
+    const int w = i >> 5, lane = i & 31;
+    if (lane == 31) wsum[w] = incl;
+    __syncthreads();
+    if (w == 0) {
+        const int t = warp_incl_scan(wsum[lane]);
+        wsum[lane] = t;
+    }
+    __syncthreads();
+    const int excl = incl - c + (w > 0 ? wsum[w - 1] : 0);
+    if (i < nblocks) P.boff[i] = excl;
+    if (i == 1023) {
+        const unsigned long long total = (unsigned long long)(excl + c);
+        P.ctr[3] += total;
+        P.ctr[4] = total;
     }
 }
 
@@ -311,7 +335,7 @@ __global__ void k_records(Paths P) {
     // goes to slot floor(o S / T) when that slot changes), not the first S rows
     const int64_t T = (int64_t)P.ctr[4], Sc = P.cap_samples;
     for (int k = 0; k < cnt; ++k) {
-        int64_t o = (int64_t)P.roff[r] + k;
+        int64_t o = (int64_t)P.roff[r] + P.boff[r >> 10] + k;
         if (T > Sc) {
             const int64_t a = o * Sc / T, b = (o + 1) * Sc / T;
             if (b == a) continue;
@@ -578,11 +602,16 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     P.n = (int64_t)r->rows * c.width;
     // this rank's share of the capacity S; record storage bounded to 4 S paths
     P.cap_samples = std::max<int64_t>(1, (ctx_sample_capacity(ctx) + r->nranks - 1) / r->nranks);
+    // (and to the 1024 x 1024 ranks the two-pass scan covers)
     r->l_min = std::max(1.0, std::sqrt((double)P.n / (4.0 * (double)P.cap_samples)));
+    for (;;) {
+        const int64_t ntx_max = (int64_t)std::ceil(c.width / r->l_min) + 1;
+        const int64_t nty_max = (int64_t)std::ceil(r->rows / r->l_min) + 2;
+        P.ncap = ntx_max * nty_max;
+        if (P.ncap <= 1024 * 1024) break;
+        r->l_min *= 1.05;
+    }
     r->l = r->l_min;
-    const int ntx_max = (int)std::ceil(c.width / r->l_min) + 1;
-    const int nty_max = (int)std::ceil(r->rows / r->l_min) + 2;
-    P.ncap = (int64_t)ntx_max * nty_max;
 #define A(ptr, count) \
     if ((rc = alloc(r, &(ptr), (size_t)(count))) != NASG_OK) return fail_out(rc);
     A(P.o, P.n) A(P.d, P.n) A(P.beta, P.n) A(P.L, P.n) A(P.prev_pdf, P.n) A(P.alive, P.n) A(P.pending, P.n)
@@ -592,7 +621,7 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     A(P.qcount, 1)
     const size_t nrec = (size_t)P.ncap * kMaxDepthCap;
     A(P.rx, nrec) A(P.rwo, nrec) A(P.rn, nrec) A(P.rwi, nrec) A(P.rfc, nrec) A(P.rbeta, nrec) A(P.rlb, nrec)
-    A(P.rcnt, P.ncap) A(P.rpix, P.ncap) A(P.roff, P.ncap)
+    A(P.rcnt, P.ncap) A(P.rpix, P.ncap) A(P.roff, P.ncap) A(P.bsum, 1024) A(P.boff, 1024)
     A(P.ctr, 8) A(P.film, P.n) A(P.frame, P.n) A(P.samples, P.cap_samples)
 #undef A
     if (cudaMemsetAsync(P.film, 0, P.n * sizeof(float4), r->stream) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
@@ -645,9 +674,11 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     k_queue_reset<<<1, 1, 0, s>>>(P);
     r->launches++;
     if (c.collect) {
-        k_scan<<<1, 1024, 0, s>>>(P);
+        const int nb = (int)((P.ncap + 1023) / 1024);
+        k_scan_local<<<nb, 1024, 0, s>>>(P);
+        k_scan_blocks<<<1, 1024, 0, s>>>(P, nb);
         k_records<<<grid_of(P.ncap), kBlock, 0, s>>>(P);
-        r->launches += 2;
+        r->launches += 3;
     }
     const int64_t mb = (int64_t)c.schedule_m * c.schedule_b;
     const double w = c.ramp ? (double)std::min<int64_t>(r->iter + 1, mb) / (double)mb : 1.0;
