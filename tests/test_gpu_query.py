@@ -208,3 +208,22 @@ def test_packed_rows_match_soa(guide, prec):
         assert np.array_equal(hout, ref.cpu().numpy()) and np.array_equal(hc, c1.cpu().numpy())
     finally:
         guide.precision = nasg.NASG_MLP_FP32
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_packed_rows_unaligned_pointer(guide, prec):
+    """A 13-float row array that is not 16-byte aligned (no TMA staging) gives the same results."""
+    guide.precision = nasg.NASG_MLP_BF16 if prec == "bf16" else nasg.NASG_MLP_FP32
+    try:
+        n = 5_003
+        x, wo, nrm, xi = nasg.synth_queries(12, n)
+        q13 = np.concatenate([x[:, :3], wo[:, :3], nrm[:, :3], xi], 1).astype(np.float32)
+        buf = torch.zeros(n * 13 + 1, dtype=torch.float32, device="cuda")
+        buf[1:] = torch.from_numpy(q13.ravel()).cuda()
+        un = buf[1:].view(n, 13)  # 4-byte offset from a 256-byte aligned allocation
+        assert un.data_ptr() % 16 == 4
+        out_u, _ = guide.query_sample_packed(un)
+        out_a, _ = guide.query_sample_packed(torch.from_numpy(q13).cuda())
+        assert torch.equal(out_u, out_a)
+    finally:
+        guide.precision = nasg.NASG_MLP_FP32
