@@ -75,14 +75,6 @@ __device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, 
     return clamped;
 }
 
-__device__ __forceinline__ int encode_tile_row(const QueryArgs &a, int64_t q, const float (&inv_ext)[3],
-                                               uint32_t a_row) {
-    const bool valid = q < a.n;
-    float4 x = make_float4(0.f, 0.f, 0.f, 0.f), wo = x, nrm = x;
-    if (valid) load_query(a, q, x, wo, nrm);
-    return encode_row_bf16(valid, x, wo, nrm, a.bounds, inv_ext, a_row);
-}
-
 // named barrier over the 128 threads of epilogue warpgroup g (id 0 is __syncthreads)
 __device__ __forceinline__ void wg_sync(int g) { asm volatile("bar.sync %0, 128;" ::"r"(g + 1) : "memory"); }
 
