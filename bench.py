@@ -12,6 +12,7 @@ Also reported (same JSON line):
                (pinned H2D of the inputs + D2H of the results inside the timed region)
   roofline     the fused query kernel vs the measured bf16 tensor peak
   cpu_baseline the reference (oracle/_ref, all host cores) on a bounded sample
+  sweep        config 2: 2^20 - 2^24 queries per batch, bf16 vs fp32 MLP
   train        config 3: fused fwd+KL+bwd+Adam at 2^18 samples per step
   render       configs 4-5: the guided progressive render loop (1024^2 x 512 spp;
                4K sharded by pixel rows over the ranks)
@@ -199,6 +200,36 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
             "gpu_launches": launches, "last_mean_loss": st.mean_loss}
 
 
+def bench_sweep(nasg, args, ws, rank):
+    """Config 2's sweep: 2^20 - 2^24 queries per batch, fp32 (FFMA) vs bf16 (tcgen05) MLP,
+    device-resident inputs, CUDA events on the launching stream, max over ranks."""
+    import torch
+    out = {}
+    nmax = 1 << 24
+    host = nasg.synth_queries(77, nmax, first=rank * nmax)
+    dev = [torch.from_numpy(a).cuda() for a in host]
+    res = torch.empty((nmax, 4), dtype=torch.float32, device="cuda")
+    g = nasg.Guide(nasg.TrainerConfig(seed=0))
+    stream = torch.cuda.current_stream()
+    for prec, name in ((nasg.NASG_MLP_BF16, "bf16"), (nasg.NASG_MLP_FP32, "fp32")):
+        g.precision = prec
+        for lg in (20, 22, 24):
+            n = 1 << lg
+            reps = max(2, (1 << 24) // n) if name == "bf16" else 2
+            d = [a[:n] for a in dev]
+            for _ in range(2):
+                g.query_sample(*d, dir_pdf=res[:n])
+            torch.cuda.synchronize()
+            barrier(ws)
+            t = max_over_ranks(sum(time_events(lambda: g.query_sample(*d, dir_pdf=res[:n]), reps, stream)), ws)
+            out[f"{name}_2^{lg}"] = n * ws * reps / t
+    g.close()
+    del dev, res
+    torch.cuda.empty_cache()
+    return {"unit": "queries/s", "note": "config 2 sweep; value = all ranks' queries / max-over-ranks time",
+            **out}
+
+
 def bench_render(nasg, args, ws, rank, width, height, iters, label):
     """Configs 4-5: the guided progressive render loop (nasg_render_*): per iteration one
     path per pixel of this rank's rows (wavefront tracer, NEE+MIS, guided scattering
@@ -255,6 +286,7 @@ def main():
     ap.add_argument("--train-steps", type=int, default=5)
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-render", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--render-4k-iters", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -358,6 +390,7 @@ def main():
     del dev, out, cbuf
     torch.cuda.empty_cache()
 
+    sweep = None if args.no_sweep else bench_sweep(nasg, args, ws, rank)
     train = None if args.no_train else {p: bench_train(nasg.Guide, nasg, args, ws, rank, p) for p in ("bf16", "fp32")}
     render = None
     if not args.no_render:
@@ -377,7 +410,7 @@ def main():
                                        f"64-128-128-128-65 MLP", "queries_per_step_per_gpu": n,
                            "l2": "inputs (1 GiB/GPU) exceed the 126 MB L2", "parallelism": f"query shards x{ws}"},
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
-                "clocks": clk.summary(), "train": train, "render": render}
+                "clocks": clk.summary(), "sweep": sweep, "train": train, "render": render}
         print(json.dumps(line), flush=True)
 
 
