@@ -249,7 +249,12 @@ __global__ void k_update(Paths P, Frame F, int bounce) {
         }
     }
     const int r = P.rank[i];
-    if (r >= 0 && usable && bounce < kMaxDepthCap) {  // training record (SPEC PathVertexRecord)
+    // training record (SPEC PathVertexRecord).  A direction whose radiance was never
+    // traced (the path ended by Russian roulette or at the depth limit) has an
+    // unknown, not a zero, target: such vertices are dropped; a zero f cos is a
+    // genuine p = 0 sample and is kept.
+    const bool zero_f = !(fc.x > 0.f || fc.y > 0.f || fc.z > 0.f);
+    if (r >= 0 && usable && (zero_f || (live && bounce + 1 < F.max_depth))) {
         const int k = P.rcnt[r]++;
         const size_t at = (size_t)k * P.ncap + r;
         P.rx[at] = f4(x, 0.f);
@@ -257,7 +262,7 @@ __global__ void k_update(Paths P, Frame F, int bounce) {
         P.rn[at] = f4(n, pb);
         P.rwi[at] = f4(v, 0.f);
         P.rfc[at] = f4(fc, 0.f);
-        P.rbeta[at] = live ? nb : make_float4(0.f, 0.f, 0.f, 0.f);
+        P.rbeta[at] = zero_f ? make_float4(0.f, 0.f, 0.f, 0.f) : nb;
         P.rlb[at] = L;
     }
     P.L[i] = L;
@@ -439,13 +444,15 @@ static bool build_scene(int kind, int w, int h, Scene &s) {
         const float lo[3] = {-1.5f, -1.5f, -0.5f}, hi[3] = {1.5f, 1.5f, 2.5f};
         std::memcpy(s.bmin, lo, sizeof(lo));
         std::memcpy(s.bmax, hi, sizeof(hi));
-    } else if (kind == NASG_SCENE_BOX || kind == NASG_SCENE_CRACK) {
+    } else if (kind == NASG_SCENE_BOX || kind == NASG_SCENE_CRACK || kind == NASG_SCENE_ATTIC) {
+        const bool crack = kind != NASG_SCENE_BOX;
         const int mw = addm(mat(kLambert, white)), mr = addm(mat(kLambert, red)), mg = addm(mat(kLambert, green));
         const int mgl = addm(mat(kPhong, f3(0.8f, 0.8f, 0.8f), 60.f));
         const int mmi = addm(mat(kMirror, f3(0.95f, 0.95f, 0.95f)));
-        const int mle = addm(mat(kEmitter, f3(0.f, 0.f, 0.f), 0.f, kind == NASG_SCENE_BOX ? f3(17.f, 12.f, 4.f)
-                                                                                         : f3(60.f, 48.f, 30.f)));
-        addp(quad(f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), f3(1.f, 0.f, 0.f), kind == NASG_SCENE_CRACK ? mgl : mw));
+        const float3 le = kind == NASG_SCENE_BOX ? f3(17.f, 12.f, 4.f)
+                          : (kind == NASG_SCENE_CRACK ? f3(60.f, 48.f, 30.f) : f3(400.f, 320.f, 200.f));
+        const int mle = addm(mat(kEmitter, f3(0.f, 0.f, 0.f), 0.f, le));
+        addp(quad(f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), f3(1.f, 0.f, 0.f), crack ? mgl : mw));
         addp(quad(f3(0.f, 1.f, 0.f), f3(1.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), mw));  // ceiling
         addp(quad(f3(0.f, 0.f, 1.f), f3(0.f, 1.f, 0.f), f3(1.f, 0.f, 0.f), mw));  // back
         addp(quad(f3(0.f, 0.f, 0.f), f3(0.f, 1.f, 0.f), f3(0.f, 0.f, 1.f), mr));  // left
@@ -458,7 +465,11 @@ static bool build_scene(int kind, int w, int h, Scene &s) {
             // partition at y = 0.85 with a slit 0.47 < x < 0.53; the light lies above it
             addp(quad(f3(0.f, 0.85f, 0.f), f3(0.47f, 0.f, 0.f), f3(0.f, 0.f, 1.f), mw));
             addp(quad(f3(0.53f, 0.85f, 0.f), f3(0.47f, 0.f, 0.f), f3(0.f, 0.f, 1.f), mw));
-            addp(quad(f3(0.2f, 0.999f, 0.3f), f3(0.6f, 0.f, 0.f), f3(0.f, 0.f, 0.4f), mle));
+            if (kind == NASG_SCENE_CRACK)  // light at the ceiling, partly visible through the slit
+                addp(quad(f3(0.2f, 0.999f, 0.3f), f3(0.6f, 0.f, 0.f), f3(0.f, 0.f, 0.4f), mle));
+            else  // ATTIC: light lying on the partition facing the ceiling; the room below
+                  // only sees light that bounced off the ceiling and came through the slit
+                addp(quad(f3(0.05f, 0.86f, 0.3f), f3(0.f, 0.f, 0.4f), f3(0.3f, 0.f, 0.f), mle));
             addp(sphere(f3(0.3f, 0.2f, 0.6f), 0.2f, mw));
             addp(sphere(f3(0.72f, 0.18f, 0.35f), 0.18f, mmi));
         }

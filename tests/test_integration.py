@@ -63,7 +63,7 @@ def test_mape_spec_examples():
 
 def test_render_scene_bounds():
     import paper_2303_08064_b200 as nasg
-    for s in (nasg.SCENE_FURNACE, nasg.SCENE_BOX, nasg.SCENE_CRACK, nasg.SCENE_DARK):
+    for s in (nasg.SCENE_FURNACE, nasg.SCENE_BOX, nasg.SCENE_CRACK, nasg.SCENE_DARK, nasg.SCENE_ATTIC):
         lo, hi = nasg.scene_bounds(s)
         assert np.all(hi > lo)
     with pytest.raises(nasg.NasgError):
