@@ -142,6 +142,26 @@ def cpu_reference_rate(n_total, seconds, threads=None):
                       f"{threads} OpenMP threads, {dt:.1f} s)"}
 
 
+def cpu_reference_train_rate(seconds=8.0):
+    """The reference's own Trainer::train_iteration (oracle/_ref, single-threaded by
+    design, guiding.cpp:196-282) on config-1 sized buffers (S = 2^14 samples, t = 2^12)."""
+    from oracle.oracle import Oracle, available
+    import paper_2303_08064_b200 as nasg
+    kind = "reference" if available("ref") else "port"
+    o = Oracle("ref" if kind == "reference" else "orc")
+    n = 1 << 14
+    tr = o.trainer(capacity=n, batch=1 << 12, seed=3)
+    s = nasg.synth_samples(11, n)
+    done, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < seconds:
+        tr.train(s, 1.0)
+        done += n
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": "samples/s", "cores": 1, "kind": kind,
+            "sample": f"{done} synthetic samples through train_iteration (S = t*4 = 16384, 4 Adam steps per call), "
+                      f"{dt:.1f} s, 1 thread"}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -402,6 +422,8 @@ def main():
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_reference_rate(1 << 30, args.cpu_seconds)
+        if train is not None:
+            train["cpu_baseline"] = cpu_reference_train_rate()
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
