@@ -144,7 +144,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 s0 = sp[0]; s1 = sp[1]; s2 = sp[2]; s3 = sp[3];
             }
         };
-        int64_t tile = (int64_t)blockIdx.x * kWGt + g;
+        // warpgroup-major tile order: a small batch (the render loop's t = 4096 is 32
+        // tiles) spreads one tile per SM instead of three per SM on a third of them
+        int64_t tile = (int64_t)g * gridDim.x + blockIdx.x;
         load_sample(tile);
         if ((warp & 3) == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
         for (; tile < ntiles; tile += stride) {
@@ -402,8 +404,7 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
     const int64_t ntiles = (count + 127) / 128;
     const double gscale = 1.0 / (double)global_count;
     if (ntiles > 0) {
-        const int64_t supers = (ntiles + kWGt - 1) / kWGt;
-        const int grid = (int)(supers < num_sms ? supers : num_sms);
+        const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
         const uint8_t *im = static_cast<const uint8_t *>(img);
         if (n_comp == 8) {
             constexpr size_t sm = fb_smem<8>();
