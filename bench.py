@@ -162,6 +162,13 @@ def cpu_reference_train_rate(seconds=8.0):
                       f"{dt:.1f} s, 1 thread"}
 
 
+def bench_config(n, ws):
+    """The workload both arms report (config 2 of BASELINE.json at its largest size)."""
+    return {"workload": f"config 2: {n} guided queries/step/GPU (fwd+sample+pdf), N=8 lobes, "
+                        f"64-128-128-128-65 MLP", "queries_per_step_per_gpu": n,
+            "l2": "inputs (1 GiB/GPU) exceed the 126 MB L2", "parallelism": f"query shards x{ws}"}
+
+
 def run_reference(args, ws, rank):
     if rank != 0:
         return
@@ -169,8 +176,7 @@ def run_reference(args, ws, rank):
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "queries/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": "config 2: guided query fwd+sample+pdf, N=8, host CPU reference",
-                       "queries_per_step": args.queries},
+            "config": bench_config(args.queries, ws),
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "queries/s",
                                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -428,9 +434,7 @@ def main():
         line = {"metric": METRIC, "value": value, "unit": "queries/s", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
-                "config": {"workload": f"config 2: {n} guided queries/step/GPU (fwd+sample+pdf), N=8 lobes, "
-                                       f"64-128-128-128-65 MLP", "queries_per_step_per_gpu": n,
-                           "l2": "inputs (1 GiB/GPU) exceed the 126 MB L2", "parallelism": f"query shards x{ws}"},
+                "config": bench_config(n, ws),
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
                 "clocks": clk.summary(), "sweep": sweep, "train": train, "render": render}
         print(json.dumps(line), flush=True)
