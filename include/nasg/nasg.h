@@ -258,6 +258,65 @@ uint64_t nasg_render_kernel_launches(nasg_render *r);
  * |img - ref| / (ref + 0.01), the worst floor(0.1% of pixels) dropped. */
 double nasg_mape(const float *img, const float *ref, int64_t npix);
 
+/* ---- explicit-parameter mixtures: NASG and the vMF / SG baseline ----------
+ * (sphdist.hpp:33-121).  Context-free, on the current CUDA
+ * device, stream-ordered, device buffers.  Computed in double from fp32
+ * records, as the reference computes in double.  Per query q, k components:
+ *   NASG record  3 x float4 = (x_axis xyz, lambda), (y_axis xyz, a),
+ *                (z_axis xyz, epsilon)    — NasgComponent sphdist.hpp:33-38
+ *   vMF record   1 x float4 = (mu xyz, lambda) — VmfComponent sphdist.hpp:49-52
+ *   comp         n x k records; weights n x k floats (sum to 1 per query)
+ *   dir, xi      n x float4 (xi = xi_select, xi0, xi1, xi2; vMF ignores xi2)
+ */
+enum { NASG_DIST_NASG = 0, NASG_DIST_VMF = 1 };
+/* mixture_pdf sphdist.hpp:84 / vmf_mixture_pdf :117 -> pdf (n floats) */
+int nasg_dist_mixture_pdf(int kind, int64_t n, int k, const float *comp, const float *weights,
+                          const float *dir, float *pdf, void *stream);
+/* mixture_sample :97-98 / vmf_mixture_sample :119-120 -> dir_pdf (n x float4) */
+int nasg_dist_mixture_sample(int kind, int64_t n, int k, const float *comp, const float *weights,
+                             const float *xi, float *dir_pdf, void *stream);
+/* nasg_grad_logpdf :68-71 (8 floats per component: d_cos_theta, d_sin_phi,
+ * d_cos_phi, d_sin_tau, d_cos_tau, d_lambda, d_a, 0) / vmf_grad_logpdf :121
+ * (4 floats: d_mu xyz, d_lambda) for every component of every query. */
+int nasg_dist_grad_logpdf(int kind, int64_t n, int k, const float *comp, const float *weights,
+                          const float *dir, float *grad, void *stream);
+
+/* ---- NASG vs vMF expressiveness fit (SPEC.md run_fit :500-508, PAPER Fig. 5)
+ * Fits n_fits independent position-free guide distributions (one CTA each)
+ * to an analytic target mixture with the guider's KL gradient on directions
+ * drawn from the target and the reference's Adam.  Model raw vectors:
+ *   NASG  8N+1 floats in the network's raw-output order (guiding.hpp:25-30),
+ *         decoded by decode_full (guiding.cpp:15-77); N in {1, 2, 4, 8}
+ *   vMF   5K floats: K unnormalised mean directions (xyz), K log-sharpness,
+ *         K weight logits; K <= 32
+ * Host buffers; blocks until done. */
+typedef struct {
+    int model;            /* NASG_DIST_NASG | NASG_DIST_VMF */
+    int n_components;     /* the paper's comparison: 8 NASG (64 scalars) vs 14 vMF (70) */
+    int batch;            /* target samples per Adam step */
+    int steps;            /* Adam steps */
+    int checkpoints;      /* raw snapshots, every steps/checkpoints steps (>= 1) */
+    float learning_rate;
+    uint64_t seed;
+} nasg_fit_config;
+int nasg_fit_raw_dim(int model, int n_components); /* -1 if unsupported */
+/* target_comp / target_w: one explicit mixture of target_kind (records as
+ * above, target_k <= 32).  raw_init (nullable): n_fits x raw_dim start
+ * vectors, else a seeded init.  raw_out: n_fits x checkpoints x raw_dim.
+ * kl_out (nullable): n_fits x checkpoints KL(target || model), integrated on
+ * an equal-area grid of quad_nz x 2 quad_nz cells. */
+int nasg_fit(const nasg_fit_config *cfg, int n_fits, int target_kind, int target_k,
+             const float *target_comp, const float *target_w, const float *raw_init,
+             float *raw_out, double *kl_out, int quad_nz);
+/* The fit's mean gradient over given samples (n x float4: direction xyz,
+ * target pdf p; q_sampling = p), raw_dim floats out — parity entry. */
+int nasg_fit_gradient(int model, int n_components, const float *raw, int64_t n,
+                      const float *samples, float *grad_out);
+/* KL(target || model) for n_models raw vectors on the quad_nz grid. */
+int nasg_fit_kl(int target_kind, int target_k, const float *target_comp, const float *target_w,
+                int model, int n_components, int n_models, const float *raws, int quad_nz,
+                double *kl_out);
+
 /* ---- synthetic workloads (bench / tests) ----------------- */
 /* Query i: Pcg32(hash_combine(seed, i), 0x51) -> x ~ U(bounds), omega_o and
  * normal ~ U(S^2), xi ~ U[0,1) as (u32 >> 8) * 2^-24.  Host arrays. */

@@ -718,6 +718,187 @@ void orc_kl_grad(int64_t n, int n_comp, const float *raw, const float *samples, 
     }
 }
 
+
+/* ---------------- explicit mixtures and the vMF / SG baseline ----------------
+ * sphdist.cpp:152-198 (NASG mixture pdf / sample), :200-274 (grad log pdf),
+ * :276-340 (vMF).  Records as nasg.h: NASG 12 floats (x_axis, lambda,
+ * y_axis, a, z_axis, epsilon), vMF 4 floats (mu, lambda); weights k floats. */
+static void nasg_records(int k, const float *comp, const float *w, decoded_t *d) {
+    d->n = k;
+    for (int i = 0; i < k; ++i) {
+        const float *r = comp + 12 * i;
+        lobe_t *l = &d->lobe[i];
+        for (int j = 0; j < 3; ++j) {
+            l->x[j] = r[j];
+            l->y[j] = r[4 + j];
+            l->z[j] = r[8 + j];
+        }
+        l->lambda = r[3]; l->a = r[7]; l->eps = r[11];
+        d->w[i] = w[i];
+    }
+}
+
+typedef struct { double mu[3], lambda; } vmf_t;
+
+static double vmf_log_eval(const vmf_t *c, const double *v) { return c->lambda * (dot3(c->mu, v) - 1.0); } /* :276-278 */
+static double vmf_norm_const(const vmf_t *c) { return K_TWO_PI * (-expm1(-2.0 * c->lambda)) / c->lambda; } /* :280-282 */
+static double vmf_pdf(const vmf_t *c, const double *v) { return exp(vmf_log_eval(c, v)) / vmf_norm_const(c); }
+static double vmf_mixture_pdf(int k, const vmf_t *c, const double *w, const double *v) { /* :288-293 */
+    double pdf = 0.0;
+    for (int i = 0; i < k; ++i) pdf += w[i] * vmf_pdf(&c[i], v);
+    return pdf;
+}
+static void normalize3(double *v) { /* math.hpp:43 */
+    double l = sqrt(dot3(v, v));
+    v[0] /= l; v[1] /= l; v[2] /= l;
+}
+static void cross3(const double *a, const double *b, double *o) {
+    o[0] = a[1] * b[2] - a[2] * b[1];
+    o[1] = a[2] * b[0] - a[0] * b[2];
+    o[2] = a[0] * b[1] - a[1] * b[0];
+}
+static void vmf_sample(const vmf_t *c, double xi0, double xi1, double *v) { /* :295-305 */
+    double cos_t = clampd(1.0 + log1p(-xi0 * (-expm1(-2.0 * c->lambda))) / c->lambda, -1.0, 1.0);
+    double sin_t = sqrt(1.0 - cos_t * cos_t);
+    double phi = K_TWO_PI * xi1;
+    double z[3] = {c->mu[0], c->mu[1], c->mu[2]}, x[3], y[3]; /* frame_around :103-110 */
+    normalize3(z);
+    double helper[3] = {1.0, 0.0, 0.0};
+    if (!(fabs(z[0]) < 0.9)) { helper[0] = 0.0; helper[1] = 1.0; }
+    cross3(helper, z, x);
+    normalize3(x);
+    cross3(z, x, y);
+    for (int j = 0; j < 3; ++j) v[j] = x[j] * (sin_t * cos(phi)) + y[j] * (sin_t * sin(phi)) + z[j] * cos_t;
+}
+static void vmf_grad(const vmf_t *c, double wi, const double *v, double q, double *g4) { /* :324-340 */
+    g4[0] = g4[1] = g4[2] = g4[3] = 0.0;
+    if (!(q > 0.0) || !isfinite(q)) return;
+    double r = wi * vmf_pdf(c, v) / q;
+    double expm2l = exp(-2.0 * c->lambda);
+    double dlogK = 2.0 * expm2l / (1.0 - expm2l) - 1.0 / c->lambda;
+    g4[3] = r * ((dot3(c->mu, v) - 1.0) - dlogK);
+    double gm[3] = {v[0] * c->lambda, v[1] * c->lambda, v[2] * c->lambda};
+    double p = dot3(gm, c->mu);
+    for (int j = 0; j < 3; ++j) g4[j] = (gm[j] - c->mu[j] * p) * r;
+}
+static void vmf_records(int k, const float *comp, const float *w, vmf_t *c, double *wd) {
+    for (int i = 0; i < k; ++i) {
+        for (int j = 0; j < 3; ++j) c[i].mu[j] = comp[4 * i + j];
+        c[i].lambda = comp[4 * i + 3];
+        wd[i] = w[i];
+    }
+}
+
+void orc_dist_pdf(int kind, int64_t n, int k, const float *comp, const float *w, const float *dir4, double *out) {
+    for (int64_t q = 0; q < n; ++q) {
+        double v[3] = {dir4[4 * q], dir4[4 * q + 1], dir4[4 * q + 2]};
+        if (kind == 0) {
+            decoded_t d;
+            nasg_records(k, comp + 12 * k * q, w + k * q, &d);
+            out[q] = mixture_pdf(&d, v);
+        } else {
+            vmf_t c[ORC_MAX_LOBES];
+            double wd[ORC_MAX_LOBES];
+            vmf_records(k, comp + 4 * k * q, w + k * q, c, wd);
+            out[q] = vmf_mixture_pdf(k, c, wd, v);
+        }
+    }
+}
+
+void orc_dist_sample(int kind, int64_t n, int k, const float *comp, const float *w, const float *xi4, double *out4) {
+    for (int64_t q = 0; q < n; ++q) {
+        const float *x = xi4 + 4 * q;
+        double v[3];
+        if (kind == 0) {
+            decoded_t d;
+            nasg_records(k, comp + 12 * k * q, w + k * q, &d);
+            out4[4 * q + 3] = mixture_sample(&d, x, v);
+        } else {
+            vmf_t c[ORC_MAX_LOBES];
+            double wd[ORC_MAX_LOBES];
+            vmf_records(k, comp + 4 * k * q, w + k * q, c, wd);
+            int pick = k - 1; /* vmf_mixture_sample :307-322 */
+            double acc = 0.0;
+            for (int i = 0; i < k; ++i) {
+                acc += wd[i];
+                if ((double)x[0] < acc) { pick = i; break; }
+            }
+            vmf_sample(&c[pick], x[1], x[2], v);
+            out4[4 * q + 3] = vmf_mixture_pdf(k, c, wd, v);
+        }
+        for (int j = 0; j < 3; ++j) out4[4 * q + j] = v[j];
+    }
+}
+
+void orc_dist_grad(int kind, int64_t n, int k, const float *comp, const float *w, const float *dir4, double *out) {
+    for (int64_t q = 0; q < n; ++q) {
+        double v[3] = {dir4[4 * q], dir4[4 * q + 1], dir4[4 * q + 2]};
+        if (kind == 0) {
+            decoded_t d;
+            nasg_records(k, comp + 12 * k * q, w + k * q, &d);
+            double qm = mixture_pdf(&d, v);
+            for (int i = 0; i < k; ++i) {
+                pgrad_t g = grad_logpdf(&d, i, v, qm);
+                double *o = out + 8 * (k * q + i);
+                o[0] = g.d_ct; o[1] = g.d_sp; o[2] = g.d_cp; o[3] = g.d_st; o[4] = g.d_ctau;
+                o[5] = g.d_lambda; o[6] = g.d_a; o[7] = 0.0;
+            }
+        } else {
+            vmf_t c[ORC_MAX_LOBES];
+            double wd[ORC_MAX_LOBES];
+            vmf_records(k, comp + 4 * k * q, w + k * q, c, wd);
+            double qm = vmf_mixture_pdf(k, c, wd, v);
+            for (int i = 0; i < k; ++i) vmf_grad(&c[i], wd[i], v, qm, out + 4 * (k * q + i));
+        }
+    }
+}
+
+/* The fit's vMF model (k_sphdist.cu header): raw = [k mean directions xyz,
+ * k log-sharpness, k weight logits]; per-sample gradient of -w log q_mix with
+ * w = p / q_s = 1 (samples drawn from the target, q_s = p), chained through
+ * vmf_grad_logpdf.  p == 0 -> zero gradient, ok; unusable or non-finite ->
+ * zero gradient, not ok (the kl_loss_gradient conventions, guiding.cpp:108-165). */
+void orc_vmf_fit_grad(int k, const float *raw, int64_t n, const float *samples4, double *grad_out, int *ok_out) {
+    vmf_t c[ORC_MAX_LOBES];
+    double wd[ORC_MAX_LOBES], nr[ORC_MAX_LOBES], mx = -INFINITY, sum = 0.0;
+    int clamped[ORC_MAX_LOBES];
+    for (int i = 0; i < k; ++i) {
+        double r[3] = {raw[3 * i], raw[3 * i + 1], raw[3 * i + 2]};
+        nr[i] = sqrt(dot3(r, r));
+        int deg = nr[i] < 1e-6;
+        for (int j = 0; j < 3; ++j) c[i].mu[j] = deg ? (j == 2 ? 1.0 : 0.0) : r[j] / nr[i];
+        if (deg) nr[i] = 0.0;
+        double lam = exp((double)raw[3 * k + i]);
+        c[i].lambda = clampd(lam, 1e-3, 3e3);
+        clamped[i] = c[i].lambda != lam;
+    }
+    for (int i = 0; i < k; ++i) mx = fmax(mx, (double)raw[4 * k + i]);
+    for (int i = 0; i < k; ++i) sum += (wd[i] = exp((double)raw[4 * k + i] - mx));
+    for (int i = 0; i < k; ++i) wd[i] /= sum;
+    const int D = 5 * k;
+    for (int64_t s = 0; s < n; ++s) {
+        double *g = grad_out + D * s;
+        memset(g, 0, D * sizeof(double));
+        ok_out[s] = 1;
+        const float *sm = samples4 + 4 * s;
+        if (sm[3] == 0.0f) continue;
+        double v[3] = {sm[0], sm[1], sm[2]};
+        double q = vmf_mixture_pdf(k, c, wd, v);
+        if (!(isfinite(q) && q > DENSITY_FLOOR)) { ok_out[s] = 0; continue; }
+        int fin = 1;
+        for (int i = 0; i < k; ++i) {
+            double g4[4];
+            vmf_grad(&c[i], wd[i], v, q, g4);
+            double inv = nr[i] > 0.0 ? 1.0 / nr[i] : 0.0;
+            for (int j = 0; j < 3; ++j) g[3 * i + j] = -g4[j] * inv;
+            g[3 * k + i] = clamped[i] ? 0.0 : -g4[3] * c[i].lambda;
+            g[4 * k + i] = -(wd[i] * vmf_pdf(&c[i], v) / q - wd[i]);
+        }
+        for (int j = 0; j < D; ++j) fin &= isfinite(g[j]) != 0;
+        if (!fin) { memset(g, 0, D * sizeof(double)); ok_out[s] = 0; }
+    }
+}
+
 /* ---------------- schedules (guiding.hpp:78-92, guiding.cpp:178-182) ---------------- */
 double orc_stride_update(double l, uint64_t s, uint64_t cap) {
     double next = l * sqrt((double)s / (double)cap);

@@ -54,6 +54,11 @@ void orc_query_sample(const float *w, int out_dim, int64_t nq, const float *q9,
 void orc_kl_grad(int64_t n, int n_comp, const float *raw, const float *samples, double b,
                  double loss_blend, double *grad_out, int *ok_out, double *loss_out);
 
+void orc_dist_pdf(int kind, int64_t n, int k, const float *comp, const float *w, const float *dir4, double *out);
+void orc_dist_sample(int kind, int64_t n, int k, const float *comp, const float *w, const float *xi4, double *out4);
+void orc_dist_grad(int kind, int64_t n, int k, const float *comp, const float *w, const float *dir4, double *out);
+void orc_vmf_fit_grad(int k, const float *raw, int64_t n, const float *samples4, double *grad_out, int *ok_out);
+
 double orc_stride_update(double l, uint64_t s, uint64_t cap);
 double orc_blend_coefficient(int64_t i, int m, int bsteps);
 

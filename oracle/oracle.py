@@ -49,6 +49,10 @@ _SIGS = {
     "decode_pdf": (None, [_i64, _int, _f32p, _f32p, _dbl, _vp, _vp, _vp]),
     "query_sample": (None, [_f32p, _int, _i64, _f32p, _f32p, _f32p, _f32p, _f32p, _vp, _int]),
     "kl_grad": (None, [_i64, _int, _f32p, _f32p, _dbl, _dbl, _f64p, _i32p, _f64p]),
+    "dist_pdf": (None, [_int, _i64, _int, _f32p, _f32p, _f32p, _f64p]),
+    "dist_sample": (None, [_int, _i64, _int, _f32p, _f32p, _f32p, _f64p]),
+    "dist_grad": (None, [_int, _i64, _int, _f32p, _f32p, _f32p, _f64p]),
+    "vmf_fit_grad": (None, [_int, _f32p, _i64, _f32p, _f64p, _i32p]),
     "stride_update": (_dbl, [_dbl, _u64, _u64]),
     "blend_coefficient": (_dbl, [_i64, _int, _int]),
     "trainer_create": (_vp, [_int, _int, _int, _int, _flt, _dbl, _u64, _f32p, _f32p]),
@@ -198,6 +202,44 @@ class Oracle:
         loss = np.empty(len(raw), np.float64)
         self._kl_grad(len(raw), n_comp, raw, s, b, loss_blend, g, ok, loss)
         return g, ok.astype(bool), loss
+
+    # ---- explicit mixtures (sphdist.hpp) and the fit's vMF model ------------------
+    # kind 0 = NASG (12-float records), 1 = vMF (4-float records); comp is
+    # (n, k, rec) float32, w (n, k), dirs / xi (n, 4)
+    def _dist_args(self, kind, comp, w, v4):
+        rec = 12 if kind == 0 else 4
+        w = np.ascontiguousarray(w, np.float32)
+        n, k = w.shape
+        comp = np.ascontiguousarray(comp, np.float32).reshape(n, k, rec)
+        v4 = np.ascontiguousarray(v4, np.float32).reshape(n, 4)
+        return n, k, comp, w, v4
+
+    def dist_pdf(self, kind, comp, w, dirs):
+        n, k, comp, w, d = self._dist_args(kind, comp, w, dirs)
+        out = np.empty(n, np.float64)
+        self._dist_pdf(kind, n, k, comp, w, d, out)
+        return out
+
+    def dist_sample(self, kind, comp, w, xi):
+        n, k, comp, w, x = self._dist_args(kind, comp, w, xi)
+        out = np.empty((n, 4), np.float64)
+        self._dist_sample(kind, n, k, comp, w, x, out)
+        return out
+
+    def dist_grad(self, kind, comp, w, dirs):
+        n, k, comp, w, d = self._dist_args(kind, comp, w, dirs)
+        out = np.empty((n, k, 8 if kind == 0 else 4), np.float64)
+        self._dist_grad(kind, n, k, comp, w, d, out)
+        return out
+
+    def vmf_fit_grad(self, raw, samples4):
+        raw = np.ascontiguousarray(raw, np.float32)
+        k = len(raw) // 5
+        s = np.ascontiguousarray(samples4, np.float32).reshape(-1, 4)
+        g = np.empty((len(s), 5 * k), np.float64)
+        ok = np.empty(len(s), np.int32)
+        self._vmf_fit_grad(k, raw, len(s), s, g, ok)
+        return g, ok.astype(bool)
 
     def stride_update(self, l, s, cap):
         return self._stride_update(l, s, cap)

@@ -17,7 +17,10 @@
 //            bsdf_pdf, omega_i xyz, pad
 //   lobe   : 13 doubles = z xyz, x xyz, y xyz, lambda, a, weight, log K
 
+#include <algorithm>
+#include <cmath>
 #include <cstdint>
+#include <limits>
 #include <cstring>
 #include <span>
 #include <vector>
@@ -275,6 +278,139 @@ void ref_kl_grad(int64_t n, int n_comp, const float *raw, const float *samples, 
         for (int k = 0; k < D; ++k) grad_out[i * D + k] = g[k];
         ok_out[i] = ok ? 1 : 0;
         loss_out[i] = loss_surrogate(s, d, b, loss_blend);
+    }
+}
+
+
+// ---- explicit mixtures and the vMF / SG baseline (sphdist.hpp:33-121) --------
+// Records as include/nasg/nasg.h: NASG 12 floats (x_axis, lambda, y_axis, a,
+// z_axis, epsilon), vMF 4 floats (mu, lambda); weights k floats per query.
+static NasgMixture nasg_mixture_of(int k, const float *comp, const float *w) {
+    NasgMixture m;
+    for (int i = 0; i < k; ++i) {
+        const float *r = comp + 12 * i;
+        NasgComponent c;
+        c.frame.x_axis = v3(r);
+        c.frame.y_axis = v3(r + 4);
+        c.frame.z_axis = v3(r + 8);
+        c.lambda = r[3];
+        c.a = r[7];
+        c.epsilon = r[11];
+        m.components.push_back(c);
+        m.weights.push_back(w[i]);
+    }
+    return m;
+}
+static VmfMixture vmf_mixture_of(int k, const float *comp, const float *w) {
+    VmfMixture m;
+    for (int i = 0; i < k; ++i) {
+        VmfComponent c;
+        c.mu = v3(comp + 4 * i);
+        c.lambda = comp[4 * i + 3];
+        m.components.push_back(c);
+        m.weights.push_back(w[i]);
+    }
+    return m;
+}
+
+void ref_dist_pdf(int kind, int64_t n, int k, const float *comp, const float *w, const float *dir4, double *out) {
+    for (int64_t q = 0; q < n; ++q) {
+        Vec3 v = v3(dir4 + 4 * q);
+        out[q] = kind == 0 ? mixture_pdf(nasg_mixture_of(k, comp + 12 * k * q, w + k * q), v)
+                           : vmf_mixture_pdf(vmf_mixture_of(k, comp + 4 * k * q, w + k * q), v);
+    }
+}
+
+void ref_dist_sample(int kind, int64_t n, int k, const float *comp, const float *w, const float *xi4, double *out4) {
+    for (int64_t q = 0; q < n; ++q) {
+        const float *x = xi4 + 4 * q;
+        DirectionSample s = kind == 0 ? mixture_sample(nasg_mixture_of(k, comp + 12 * k * q, w + k * q), x[0], x[1], x[2], x[3])
+                                      : vmf_mixture_sample(vmf_mixture_of(k, comp + 4 * k * q, w + k * q), x[0], x[1], x[2]);
+        out4[4 * q] = s.direction.x;
+        out4[4 * q + 1] = s.direction.y;
+        out4[4 * q + 2] = s.direction.z;
+        out4[4 * q + 3] = s.pdf;
+    }
+}
+
+void ref_dist_grad(int kind, int64_t n, int k, const float *comp, const float *w, const float *dir4, double *out) {
+    for (int64_t q = 0; q < n; ++q) {
+        Vec3 v = v3(dir4 + 4 * q);
+        if (kind == 0) {
+            NasgMixture m = nasg_mixture_of(k, comp + 12 * k * q, w + k * q);
+            for (int i = 0; i < k; ++i) {
+                ParamGradient g = nasg_grad_logpdf(m, i, v);
+                double *o = out + 8 * (k * q + i);
+                o[0] = g.d_cos_theta; o[1] = g.d_sin_phi; o[2] = g.d_cos_phi; o[3] = g.d_sin_tau;
+                o[4] = g.d_cos_tau; o[5] = g.d_lambda; o[6] = g.d_a; o[7] = 0.0;
+            }
+        } else {
+            VmfMixture m = vmf_mixture_of(k, comp + 4 * k * q, w + k * q);
+            for (int i = 0; i < k; ++i) {
+                VmfParamGradient g = vmf_grad_logpdf(m, i, v);
+                double *o = out + 4 * (k * q + i);
+                o[0] = g.d_mu.x; o[1] = g.d_mu.y; o[2] = g.d_mu.z; o[3] = g.d_lambda;
+            }
+        }
+    }
+}
+
+// The fit's vMF model (see nasg_oracle.c orc_vmf_fit_grad): the chain rule is
+// this harness's, every density / gradient value is the reference's.
+void ref_vmf_fit_grad(int k, const float *raw, int64_t n, const float *samples4, double *grad_out, int *ok_out) {
+    VmfMixture m;
+    std::vector<double> nr(k);
+    std::vector<int> clamped(k);
+    double mx = -std::numeric_limits<double>::infinity(), sum = 0.0;
+    for (int i = 0; i < k; ++i) {
+        Vec3 r{raw[3 * i], raw[3 * i + 1], raw[3 * i + 2]};
+        nr[i] = length(r);
+        VmfComponent c;
+        if (nr[i] < 1e-6) {
+            c.mu = Vec3{0.0, 0.0, 1.0};
+            nr[i] = 0.0;
+        } else {
+            c.mu = r / nr[i];
+        }
+        double lam = std::exp((double)raw[3 * k + i]);
+        c.lambda = std::clamp(lam, 1e-3, 3e3);
+        clamped[i] = c.lambda != lam;
+        m.components.push_back(c);
+    }
+    for (int i = 0; i < k; ++i) mx = std::max(mx, (double)raw[4 * k + i]);
+    for (int i = 0; i < k; ++i) {
+        m.weights.push_back(std::exp((double)raw[4 * k + i] - mx));
+        sum += m.weights.back();
+    }
+    for (double &x : m.weights) x /= sum;
+    const int D = 5 * k;
+    for (int64_t s = 0; s < n; ++s) {
+        double *g = grad_out + D * s;
+        std::fill(g, g + D, 0.0);
+        ok_out[s] = 1;
+        const float *sm = samples4 + 4 * s;
+        if (sm[3] == 0.0f) continue;
+        Vec3 v = v3(sm);
+        double q = vmf_mixture_pdf(m, v);
+        if (!(std::isfinite(q) && q > 1e-300)) {
+            ok_out[s] = 0;
+            continue;
+        }
+        bool fin = true;
+        for (int i = 0; i < k; ++i) {
+            VmfParamGradient pg = vmf_grad_logpdf(m, i, v);
+            double inv = nr[i] > 0.0 ? 1.0 / nr[i] : 0.0;
+            g[3 * i] = -pg.d_mu.x * inv;
+            g[3 * i + 1] = -pg.d_mu.y * inv;
+            g[3 * i + 2] = -pg.d_mu.z * inv;
+            g[3 * k + i] = clamped[i] ? 0.0 : -pg.d_lambda * m.components[i].lambda;
+            g[4 * k + i] = -(m.weights[i] * vmf_pdf(m.components[i], v) / q - m.weights[i]);
+        }
+        for (int j = 0; j < D; ++j) fin = fin && std::isfinite(g[j]);
+        if (!fin) {
+            std::fill(g, g + D, 0.0);
+            ok_out[s] = 0;
+        }
     }
 }
 

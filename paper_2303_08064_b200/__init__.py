@@ -138,6 +138,13 @@ def lib():
         "nasg_render_image": (i32, [vp, vp, i32]),
         "nasg_render_kernel_launches": (u64, [vp]),
         "nasg_mape": (f64, [vp, vp, i64]),
+        "nasg_dist_mixture_pdf": (i32, [i32, i64, i32, vp, vp, vp, vp, vp]),
+        "nasg_dist_mixture_sample": (i32, [i32, i64, i32, vp, vp, vp, vp, vp]),
+        "nasg_dist_grad_logpdf": (i32, [i32, i64, i32, vp, vp, vp, vp, vp]),
+        "nasg_fit_raw_dim": (i32, [i32, i32]),
+        "nasg_fit": (i32, [vp, i32, i32, i32, vp, vp, vp, vp, vp, i32]),
+        "nasg_fit_gradient": (i32, [i32, i32, vp, i64, vp, vp]),
+        "nasg_fit_kl": (i32, [i32, i32, vp, vp, i32, i32, i32, vp, i32, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(L, name)
@@ -507,3 +514,104 @@ class Render:
             self.close()
         except Exception:
             pass
+
+
+# ---- explicit-parameter mixtures: NASG and the vMF / SG baseline (sphdist.hpp) --
+DIST_NASG, DIST_VMF = 0, 1
+_REC = {DIST_NASG: 12, DIST_VMF: 4}
+
+
+def _dist(fn, kind, comp, weights, v4, out, stream):
+    n, k = weights.shape
+    if comp.numel() != n * k * _REC[kind] or v4.numel() != 4 * n:
+        raise NasgError("shape mismatch")
+    _check(fn(kind, n, k, _ptr(comp), _ptr(weights), _ptr(v4), _ptr(out), _stream(stream)))
+    return out
+
+
+def dist_mixture_pdf(kind, comp, weights, dirs, stream=None):
+    """mixture_pdf (sphdist.hpp:84) / vmf_mixture_pdf (:117) over per-query explicit
+    mixtures.  comp (n, k, 12|4) float32 records, weights (n, k), dirs (n, 4) CUDA tensors."""
+    import torch
+    out = torch.empty(weights.shape[0], dtype=torch.float32, device=weights.device)
+    return _dist(lib().nasg_dist_mixture_pdf, kind, comp, weights, dirs, out, stream)
+
+
+def dist_mixture_sample(kind, comp, weights, xi, stream=None):
+    """mixture_sample (sphdist.hpp:97-98) / vmf_mixture_sample (:119-120): (n, 4) dir + pdf."""
+    import torch
+    out = torch.empty((weights.shape[0], 4), dtype=torch.float32, device=weights.device)
+    return _dist(lib().nasg_dist_mixture_sample, kind, comp, weights, xi, out, stream)
+
+
+def dist_grad_logpdf(kind, comp, weights, dirs, stream=None):
+    """nasg_grad_logpdf (sphdist.hpp:68-71, 8 floats per component) /
+    vmf_grad_logpdf (:121, 4 floats) for every component: (n, k, 8|4)."""
+    import torch
+    n, k = weights.shape
+    out = torch.empty((n, k, 8 if kind == DIST_NASG else 4), dtype=torch.float32, device=weights.device)
+    return _dist(lib().nasg_dist_grad_logpdf, kind, comp, weights, dirs, out, stream)
+
+
+class _FitConfig(C.Structure):
+    _fields_ = [("model", C.c_int), ("n_components", C.c_int), ("batch", C.c_int), ("steps", C.c_int),
+                ("checkpoints", C.c_int), ("learning_rate", C.c_float), ("seed", C.c_uint64)]
+
+
+@dataclass
+class FitConfig:
+    """SPEC run_fit: fit one position-free guide distribution."""
+    model: int = DIST_NASG
+    n_components: int = 8
+    batch: int = 1024
+    steps: int = 1000
+    checkpoints: int = 10
+    learning_rate: float = 0.01
+    seed: int = 0
+
+
+def fit_raw_dim(model: int, n_components: int) -> int:
+    return lib().nasg_fit_raw_dim(model, n_components)
+
+
+def _host_f32(a):
+    return np.ascontiguousarray(np.asarray(a, np.float32))
+
+
+def fit(config: FitConfig, n_fits: int, target_kind: int, target_comp, target_w, raw_init=None, quad_nz: int = 256):
+    """Fits n_fits models (one CTA each) to the target mixture; returns
+    (raw snapshots (n_fits, checkpoints, D), KL(target || model) (n_fits, checkpoints))."""
+    D = fit_raw_dim(config.model, config.n_components)
+    if D < 0:
+        raise NasgError("unsupported fit model")
+    tw = _host_f32(target_w).reshape(-1)
+    tc = _host_f32(target_comp).reshape(len(tw), _REC[target_kind])
+    init = None if raw_init is None else _host_f32(raw_init).reshape(n_fits, D)
+    raw = np.empty((n_fits, config.checkpoints, D), np.float32)
+    kl = np.empty((n_fits, config.checkpoints), np.float64)
+    c = _FitConfig(config.model, config.n_components, config.batch, config.steps, config.checkpoints,
+                   config.learning_rate, config.seed)
+    _check(lib().nasg_fit(C.byref(c), n_fits, target_kind, len(tw), _ptr(tc), _ptr(tw), _ptr(init), _ptr(raw),
+                          _ptr(kl) if quad_nz > 0 else None, quad_nz))
+    return raw, kl
+
+
+def fit_gradient(model: int, n_components: int, raw, samples4):
+    """The fit's mean gradient over given (direction xyz, target pdf) rows."""
+    raw = _host_f32(raw).reshape(-1)
+    s = _host_f32(samples4).reshape(-1, 4)
+    g = np.empty(len(raw), np.float32)
+    _check(lib().nasg_fit_gradient(model, n_components, _ptr(raw), len(s), _ptr(s), _ptr(g)))
+    return g
+
+
+def fit_kl(target_kind: int, target_comp, target_w, model: int, n_components: int, raws, quad_nz: int = 256):
+    """KL(target || model) on the equal-area quad_nz x 2 quad_nz grid, per raw vector."""
+    D = fit_raw_dim(model, n_components)
+    raws = _host_f32(raws).reshape(-1, D)
+    tw = _host_f32(target_w).reshape(-1)
+    tc = _host_f32(target_comp).reshape(len(tw), _REC[target_kind])
+    kl = np.empty(len(raws), np.float64)
+    _check(lib().nasg_fit_kl(target_kind, len(tw), _ptr(tc), _ptr(tw), model, n_components, len(raws), _ptr(raws),
+                             quad_nz, _ptr(kl)))
+    return kl

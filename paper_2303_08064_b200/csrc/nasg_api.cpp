@@ -329,6 +329,88 @@ bool is_pinned(const void *p) {
     return at.type == cudaMemoryTypeHost;
 }
 
+
+// ---- explicit mixtures and the NASG-vs-vMF fit (k_sphdist.cu) ---------------
+int check_current_device() {
+    int dev = 0;
+    CUDA_TRY(cudaGetDevice(&dev));
+    cudaDeviceProp prop{};
+    CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(NASG_ERR_CUDA, "this build targets sm_100a (B200); device is sm_" +
+                                       std::to_string(prop.major * 10 + prop.minor));
+    return NASG_OK;
+}
+
+int dist_call(int op, int kind, int64_t n, int k, const float *comp, const float *w, const float *in, float *out,
+              void *stream) {
+    if (kind != NASG_DIST_NASG && kind != NASG_DIST_VMF) return fail(NASG_ERR_INVALID, "unknown distribution kind");
+    if (n < 0 || k <= 0) return fail(NASG_ERR_INVALID, "n must be >= 0 and k > 0");
+    if (n > 0 && (!comp || !w || !in || !out)) return fail(NASG_ERR_INVALID, "null buffer");
+    if (n == 0) return NASG_OK;
+    int r = check_current_device();
+    if (r) return r;
+    dist_launch(op, kind, n, k, comp, w, in, out, (cudaStream_t)stream);
+    CHECK_LAUNCH();
+    return NASG_OK;
+}
+
+// RAII device buffer for the blocking fit calls
+struct DevBuf {
+    void *p = nullptr;
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    int alloc(size_t bytes) {
+        if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(NASG_ERR_OOM, "cudaMalloc failed");
+        }
+        return NASG_OK;
+    }
+    template <class T>
+    T *as() const { return static_cast<T *>(p); }
+};
+
+int fit_check_model(int model, int k) {
+    if (model != NASG_DIST_NASG && model != NASG_DIST_VMF) return fail(NASG_ERR_INVALID, "unknown model kind");
+    if (model == NASG_DIST_NASG && k != 1 && k != 2 && k != 4 && k != 8)
+        return fail(NASG_ERR_UNSUPPORTED, "NASG fit: n_components must be 1, 2, 4 or 8");
+    if (model == NASG_DIST_VMF && (k < 1 || k > fit_max_components(NASG_DIST_VMF)))
+        return fail(NASG_ERR_UNSUPPORTED, "vMF fit: n_components must be in [1, 32]");
+    return NASG_OK;
+}
+
+int fit_upload_target(int tkind, int tk, const float *tcomp, const float *tw, DevBuf &dc, DevBuf &dw) {
+    if (tkind != NASG_DIST_NASG && tkind != NASG_DIST_VMF) return fail(NASG_ERR_INVALID, "unknown target kind");
+    if (tk < 1 || tk > fit_max_target_components()) return fail(NASG_ERR_INVALID, "target_k must be in [1, 32]");
+    if (!tcomp || !tw) return fail(NASG_ERR_INVALID, "null target");
+    const size_t cb = (size_t)tk * (tkind == NASG_DIST_NASG ? 12 : 4) * sizeof(float);
+    int r = dc.alloc(cb);
+    if (!r) r = dw.alloc(tk * sizeof(float));
+    if (r) return r;
+    CUDA_TRY(cudaMemcpy(dc.p, tcomp, cb, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(dw.p, tw, tk * sizeof(float), cudaMemcpyHostToDevice));
+    return NASG_OK;
+}
+
+// KL of n_models device raw vectors against the target grid p (device, nz x 2nz)
+int fit_kl_device(int model, int k, const float *d_raws, int n_models, int nz, const double *d_p, double *kl_out) {
+    const int blocks = 148;
+    DevBuf part;
+    int r = part.alloc((size_t)blocks * n_models * sizeof(double));
+    if (r) return r;
+    fit_kl(model, k, d_raws, n_models, nz, d_p, part.as<double>(), blocks, 0);
+    CHECK_LAUNCH();
+    std::vector<double> h((size_t)blocks * n_models);
+    CUDA_TRY(cudaMemcpy(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int m = 0; m < n_models; ++m) {
+        double s = 0.0;
+        for (int b = 0; b < blocks; ++b) s += h[(size_t)m * blocks + b];
+        kl_out[m] = s;
+    }
+    return NASG_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -1034,6 +1116,118 @@ void nasg_synth_samples(uint64_t seed, int64_t first, int64_t n, const float bmi
             s.pad = 0.f;
         }
     });
+}
+
+
+int nasg_dist_mixture_pdf(int kind, int64_t n, int k, const float *comp, const float *weights, const float *dir,
+                          float *pdf, void *stream) {
+    return dist_call(0, kind, n, k, comp, weights, dir, pdf, stream);
+}
+int nasg_dist_mixture_sample(int kind, int64_t n, int k, const float *comp, const float *weights, const float *xi,
+                             float *dir_pdf, void *stream) {
+    return dist_call(1, kind, n, k, comp, weights, xi, dir_pdf, stream);
+}
+int nasg_dist_grad_logpdf(int kind, int64_t n, int k, const float *comp, const float *weights, const float *dir,
+                          float *grad, void *stream) {
+    return dist_call(2, kind, n, k, comp, weights, dir, grad, stream);
+}
+
+int nasg_fit_raw_dim(int model, int k) {
+    if (model == NASG_DIST_NASG) return (k == 1 || k == 2 || k == 4 || k == 8) ? fit_raw_dim_host(model, k) : -1;
+    if (model == NASG_DIST_VMF) return (k >= 1 && k <= fit_max_components(model)) ? fit_raw_dim_host(model, k) : -1;
+    return -1;
+}
+
+int nasg_fit(const nasg_fit_config *cfg, int n_fits, int target_kind, int target_k, const float *target_comp,
+             const float *target_w, const float *raw_init, float *raw_out, double *kl_out, int quad_nz) {
+    if (!cfg || n_fits <= 0 || !raw_out) return fail(NASG_ERR_INVALID, "bad argument");
+    int r = fit_check_model(cfg->model, cfg->n_components);
+    if (r) return r;
+    if (cfg->batch <= 0 || cfg->steps <= 0 || cfg->checkpoints <= 0 || cfg->checkpoints > cfg->steps)
+        return fail(NASG_ERR_INVALID, "batch, steps > 0 and 1 <= checkpoints <= steps");
+    if (kl_out && quad_nz <= 0) return fail(NASG_ERR_INVALID, "quad_nz must be > 0");
+    if ((r = check_current_device())) return r;
+    DevBuf dc, dw, dinit, dout, dp;
+    if ((r = fit_upload_target(target_kind, target_k, target_comp, target_w, dc, dw))) return r;
+    const int D = fit_raw_dim_host(cfg->model, cfg->n_components);
+    const size_t outn = (size_t)n_fits * cfg->checkpoints * D;
+    if ((r = dout.alloc(outn * sizeof(float)))) return r;
+    if (raw_init) {
+        if ((r = dinit.alloc((size_t)n_fits * D * sizeof(float)))) return r;
+        CUDA_TRY(cudaMemcpy(dinit.p, raw_init, (size_t)n_fits * D * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    FitLaunch L{};
+    L.model = cfg->model;
+    L.k = cfg->n_components;
+    L.tkind = target_kind;
+    L.tk = target_k;
+    L.tcomp = dc.as<float>();
+    L.tw = dw.as<float>();
+    L.batch = cfg->batch;
+    L.steps = cfg->steps;
+    L.n_ckpt = cfg->checkpoints;
+    L.n_fits = n_fits;
+    L.lr = cfg->learning_rate;
+    L.seed = cfg->seed;
+    L.raw_init = raw_init ? dinit.as<float>() : nullptr;
+    L.raw_out = dout.as<float>();
+    if (fit_launch(L, 0) < 0) return fail(NASG_ERR_UNSUPPORTED, "fit configuration not compiled");
+    CHECK_LAUNCH();
+    CUDA_TRY(cudaMemcpy(raw_out, dout.p, outn * sizeof(float), cudaMemcpyDeviceToHost));
+    if (kl_out) {
+        const int64_t npt = (int64_t)quad_nz * 2 * quad_nz;
+        if ((r = dp.alloc(npt * sizeof(double)))) return r;
+        fit_target_grid(target_kind, target_k, dc.as<float>(), dw.as<float>(), quad_nz, dp.as<double>(), 0);
+        CHECK_LAUNCH();
+        if ((r = fit_kl_device(cfg->model, cfg->n_components, dout.as<float>(), n_fits * cfg->checkpoints, quad_nz,
+                               dp.as<double>(), kl_out)))
+            return r;
+    }
+    return NASG_OK;
+}
+
+int nasg_fit_gradient(int model, int k, const float *raw, int64_t n, const float *samples, float *grad_out) {
+    int r = fit_check_model(model, k);
+    if (r) return r;
+    if (!raw || !grad_out || n <= 0 || !samples || n > (1 << 24)) return fail(NASG_ERR_INVALID, "bad argument");
+    if ((r = check_current_device())) return r;
+    const int D = fit_raw_dim_host(model, k);
+    DevBuf draw, ds, dg;
+    if ((r = draw.alloc(D * sizeof(float))) || (r = ds.alloc((size_t)n * 4 * sizeof(float))) ||
+        (r = dg.alloc(D * sizeof(float))))
+        return r;
+    CUDA_TRY(cudaMemcpy(draw.p, raw, D * sizeof(float), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(ds.p, samples, (size_t)n * 4 * sizeof(float), cudaMemcpyHostToDevice));
+    FitLaunch L{};
+    L.model = model;
+    L.k = k;
+    L.batch = (int)n;
+    L.n_fits = 1;
+    L.raw_init = draw.as<float>();
+    L.samples = ds.as<float>();
+    L.grad_out = dg.as<float>();
+    if (fit_launch(L, 0) < 0) return fail(NASG_ERR_UNSUPPORTED, "fit configuration not compiled");
+    CHECK_LAUNCH();
+    CUDA_TRY(cudaMemcpy(grad_out, dg.p, D * sizeof(float), cudaMemcpyDeviceToHost));
+    return NASG_OK;
+}
+
+int nasg_fit_kl(int target_kind, int target_k, const float *target_comp, const float *target_w, int model, int k,
+                int n_models, const float *raws, int quad_nz, double *kl_out) {
+    int r = fit_check_model(model, k);
+    if (r) return r;
+    if (n_models <= 0 || !raws || !kl_out || quad_nz <= 0) return fail(NASG_ERR_INVALID, "bad argument");
+    if ((r = check_current_device())) return r;
+    DevBuf dc, dw, draws, dp;
+    if ((r = fit_upload_target(target_kind, target_k, target_comp, target_w, dc, dw))) return r;
+    const int D = fit_raw_dim_host(model, k);
+    if ((r = draws.alloc((size_t)n_models * D * sizeof(float)))) return r;
+    CUDA_TRY(cudaMemcpy(draws.p, raws, (size_t)n_models * D * sizeof(float), cudaMemcpyHostToDevice));
+    const int64_t npt = (int64_t)quad_nz * 2 * quad_nz;
+    if ((r = dp.alloc(npt * sizeof(double)))) return r;
+    fit_target_grid(target_kind, target_k, dc.as<float>(), dw.as<float>(), quad_nz, dp.as<double>(), 0);
+    CHECK_LAUNCH();
+    return fit_kl_device(model, k, draws.as<float>(), n_models, quad_nz, dp.as<double>(), kl_out);
 }
 
 }  // extern "C"

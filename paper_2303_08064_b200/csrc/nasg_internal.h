@@ -151,4 +151,27 @@ int train_finalize_step(int *nonfinite, int64_t *adam_t, float *corr, int *skip,
 int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, const float *corr,
                const int *skip, float lr, float *wp, float *wtp, cudaStream_t s);
 
+
+// ---- explicit mixtures and the fit (k_sphdist.cu) --------------------------
+// op 0 = pdf, 1 = sample, 2 = grad_logpdf
+int dist_launch(int op, int kind, int64_t n, int k, const float *comp, const float *w, const float *in, float *out,
+                cudaStream_t s);
+struct FitLaunch {
+    int model, k, tkind, tk;
+    const float *tcomp, *tw;  // device
+    int batch, steps, n_ckpt, n_fits;
+    float lr;
+    uint64_t seed;
+    const float *raw_init;    // device, nullable
+    const float *samples;     // device; non-null = gradient-only mode
+    float *raw_out, *grad_out;
+};
+int fit_launch(const FitLaunch &L, cudaStream_t s);
+int fit_max_components(int model);
+int fit_max_target_components();
+int fit_raw_dim_host(int model, int k);
+int fit_target_grid(int tkind, int tk, const float *tcomp, const float *tw, int nz, double *p, cudaStream_t s);
+int fit_kl(int model, int k, const float *raws, int n_models, int nz, const double *p, double *partial, int blocks,
+           cudaStream_t s);
+
 }  // namespace nasg

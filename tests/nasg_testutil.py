@@ -51,3 +51,41 @@ def samples(rng, n, zero_p_frac=0.1):
     p[rng.random(n) < zero_p_frac] = 0.0
     s[:, 3] = p
     return s
+
+
+def frames(rng, n):
+    """(n,3,3) random right-handed orthonormal frames (x, y, z rows)."""
+    z = dirs(rng, n).astype(np.float64)
+    h = dirs(rng, n).astype(np.float64)
+    x = np.cross(h, z)
+    x /= np.linalg.norm(x, axis=1, keepdims=True)
+    y = np.cross(z, x)
+    return np.stack([x, y, z], 1)
+
+
+def nasg_records(rng, n, k, stress=False, eps_frac=0.25):
+    """(n,k,12) float32 NASG records (x, lambda, y, a, z, eps) and (n,k) weights.
+    Benign: lambda log-uniform [1e-2, 1e2], a log-uniform [1e-2, 1e2];
+    stress: lambda to the 3e3 clamp, a in [0, 3e3]; eps > 0 on eps_frac of lobes."""
+    f = frames(rng, n * k).reshape(n, k, 3, 3)
+    hi = np.log(3e3) if stress else np.log(1e2)
+    lam = np.exp(rng.uniform(np.log(1e-2), hi, (n, k)))
+    a = np.exp(rng.uniform(np.log(1e-2), hi, (n, k)))
+    a[rng.random((n, k)) < 0.1] = 0.0
+    eps = np.where(rng.random((n, k)) < eps_frac, rng.uniform(0.0, 2.0, (n, k)), 0.0)
+    rec = np.zeros((n, k, 12), np.float64)
+    rec[..., 0:3], rec[..., 3] = f[:, :, 0], lam
+    rec[..., 4:7], rec[..., 7] = f[:, :, 1], a
+    rec[..., 8:11], rec[..., 11] = f[:, :, 2], eps
+    w = rng.dirichlet(np.ones(k), n)
+    return rec.astype(np.float32), w.astype(np.float32)
+
+
+def vmf_records(rng, n, k, stress=False):
+    """(n,k,4) float32 vMF records (mu, lambda) and (n,k) weights."""
+    hi = np.log(3e3) if stress else np.log(1e2)
+    rec = np.zeros((n, k, 4), np.float64)
+    rec[..., 0:3] = dirs(rng, n * k).reshape(n, k, 3)
+    rec[..., 3] = np.exp(rng.uniform(np.log(1e-2), hi, (n, k)))
+    w = rng.dirichlet(np.ones(k), n)
+    return rec.astype(np.float32), w.astype(np.float32)

@@ -1,0 +1,276 @@
+"""GPU parity of the explicit-mixture density layer, the vMF / SG baseline and
+the NASG-vs-vMF fit against the CPU oracle
+(oracle/nasg_oracle.c, pinned to the reference by tests/test_oracle_dist.py).
+
+The kernels compute in double from fp32 records, as the reference does, and
+round results to fp32, so the tolerances are fp32-output tolerances:
+  pdf                  |d| <= 1e-6 |ref| (+1e-30)
+  sampled direction    |d| <= 2e-6; pdf at it 1e-6 relative
+  grad log pdf         |d| <= 1e-5 |ref| + 1e-6 max|ref| of the query
+  fit gradient (mean over samples of fp32-rounded per-sample terms)
+                       |d| <= 1e-5 max|ref| + 1e-5 |ref|
+"""
+import math
+
+import numpy as np
+import pytest
+
+import nasg_testutil as H
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover - CPU container
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2303_08064_b200 as nasg  # noqa: E402
+
+
+def cu(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def four(a3):
+    a = np.zeros((len(a3), 4), np.float32)
+    a[:, :3] = a3[:, :3]
+    return a
+
+
+def records(kind, rng, n, k, stress=False):
+    return (H.nasg_records if kind == nasg.DIST_NASG else H.vmf_records)(rng, n, k, stress=stress)
+
+
+@pytest.mark.parametrize("kind", [nasg.DIST_NASG, nasg.DIST_VMF])
+@pytest.mark.parametrize("stress", [False, True])
+def test_dist_kernels_match_oracle(orc, kind, stress):
+    rng = np.random.default_rng(100 + kind + 2 * stress)
+    n, k = 4096, (8 if kind == nasg.DIST_NASG else 14)
+    comp, w = records(kind, rng, n, k, stress)
+    d = four(H.dirs(rng, n))
+    xi = H.xis(rng, n)
+    c, wt = cu(comp), cu(w)
+    pdf = nasg.dist_mixture_pdf(kind, c, wt, cu(d)).cpu().numpy()
+    ref = orc.dist_pdf(kind, comp, w, d)
+    assert np.all(np.abs(pdf - ref) <= 1e-6 * np.abs(ref) + 1e-30)
+    s = nasg.dist_mixture_sample(kind, c, wt, cu(xi)).cpu().numpy()
+    rs = orc.dist_sample(kind, comp, w, xi)
+    assert np.abs(s[:, :3] - rs[:, :3]).max() <= 2e-6
+    assert np.all(np.abs(s[:, 3] - rs[:, 3]) <= 1e-6 * np.abs(rs[:, 3]) + 1e-30)
+    g = nasg.dist_grad_logpdf(kind, c, wt, cu(d)).cpu().numpy()
+    rg = orc.dist_grad(kind, comp, w, d)
+    scale = np.abs(rg).reshape(n, -1).max(1)[:, None, None]
+    assert np.all(np.abs(g - rg) <= 1e-5 * np.abs(rg) + 1e-6 * scale + 1e-30)
+
+
+def test_dist_empty_and_bad_args():
+    c = torch.zeros((1, 1, 4), device="cuda")
+    w = torch.ones((0, 1), device="cuda")
+    out = nasg.dist_mixture_pdf(nasg.DIST_VMF, c[:0], w, torch.zeros((0, 4), device="cuda"))
+    assert out.numel() == 0
+    with pytest.raises(nasg.NasgError):
+        nasg.lib()  # loaded
+        nasg._check(nasg.lib().nasg_dist_mixture_pdf(7, 1, 1, c.data_ptr(), c.data_ptr(), c.data_ptr(),
+                                                     c.data_ptr(), None))
+
+
+def test_vmf_sample_at_xi0_zero_is_mu():
+    # SPEC.md:116
+    rng = np.random.default_rng(4)
+    comp, w = H.vmf_records(rng, 1024, 3)
+    xi = H.xis(rng, 1024)
+    xi[:, 1] = 0.0
+    # pick lobe 0 surely
+    w[:] = np.array([1.0, 0.0, 0.0], np.float32)
+    s = nasg.dist_mixture_sample(nasg.DIST_VMF, cu(comp), cu(w), cu(xi)).cpu().numpy()
+    mu = comp[:, 0, :3] / np.linalg.norm(comp[:, 0, :3], axis=1, keepdims=True)
+    assert np.abs(s[:, :3] - mu).max() <= 2e-6
+
+
+def test_sg_reduction_identity_gpu():
+    # a = 0, eps = 0 -> NASG density equals the vMF density
+    rng = np.random.default_rng(6)
+    n = 8192
+    f = H.frames(rng, n)
+    lam = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), n))
+    rec = np.zeros((n, 1, 12), np.float32)
+    rec[:, 0, 0:3], rec[:, 0, 3], rec[:, 0, 4:7], rec[:, 0, 8:11] = f[:, 0], lam, f[:, 1], f[:, 2]
+    vm = np.zeros((n, 1, 4), np.float32)
+    vm[:, 0, 0:3], vm[:, 0, 3] = f[:, 2], lam
+    d = cu(four(H.dirs(rng, n)))
+    w = cu(np.ones((n, 1), np.float32))
+    a = nasg.dist_mixture_pdf(nasg.DIST_NASG, cu(rec), w, d).cpu().numpy()
+    b = nasg.dist_mixture_pdf(nasg.DIST_VMF, cu(vm), w, d).cpu().numpy()
+    assert np.all(np.abs(a - b) <= 1e-6 * np.abs(b) + 1e-30)
+
+
+def _grid_bins(v, nz, nphi):
+    iz = np.clip(((v[:, 2] + 1.0) * 0.5 * nz).astype(np.int64), 0, nz - 1)
+    ph = np.mod(np.arctan2(v[:, 1], v[:, 0]), 2 * np.pi)
+    ip = np.clip((ph / (2 * np.pi) * nphi).astype(np.int64), 0, nphi - 1)
+    return iz * nphi + ip
+
+
+@pytest.mark.parametrize("kind", [nasg.DIST_NASG, nasg.DIST_VMF])
+def test_sampler_matches_pdf_chi_square(kind):
+    # sampled directions follow the pdf (equal-area 16 x 32 bins,
+    # bin masses by an 8 x 8 sub-grid midpoint rule of the GPU pdf)
+    from scipy import stats
+    rng = np.random.default_rng(9 + kind)
+    k = 4
+    comp, w = records(kind, rng, 1, k)
+    if kind == nasg.DIST_NASG:
+        comp[0, :, 3] = [2.0, 5.0, 1.0, 8.0]   # moderate lambda: bins resolve the lobes
+        comp[0, :, 7] = [0.0, 3.0, 10.0, 1.0]  # a
+        comp[0, :, 11] = [0.0, 0.5, 0.0, 1.0]  # eps
+    else:
+        comp[0, :, 3] = [2.0, 5.0, 1.0, 8.0]
+    n = 1 << 19
+    s = nasg.dist_mixture_sample(kind, cu(np.repeat(comp, n, 0)), cu(np.repeat(w, n, 0)),
+                                 cu(H.xis(rng, n))).cpu().numpy()
+    nz, nphi, sub = 16, 32, 8
+    counts = np.bincount(_grid_bins(s[:, :3].astype(np.float64), nz, nphi), minlength=nz * nphi)
+    fz, fp = nz * sub, nphi * sub
+    z = -1.0 + (np.arange(fz) + 0.5) * 2.0 / fz
+    ph = (np.arange(fp) + 0.5) * 2 * np.pi / fp
+    Z, P = np.meshgrid(z, ph, indexing="ij")
+    r = np.sqrt(1 - Z * Z)
+    d = np.stack([r * np.cos(P), r * np.sin(P), Z, 0 * Z], -1).reshape(-1, 4).astype(np.float32)
+    m = len(d)
+    pdf = nasg.dist_mixture_pdf(kind, cu(np.repeat(comp, m, 0)), cu(np.repeat(w, m, 0)), cu(d)).cpu().numpy()
+    mass = (pdf.astype(np.float64) * 4 * np.pi / m).reshape(nz, sub, nphi, sub).sum((1, 3)).reshape(-1)
+    assert mass.sum() == pytest.approx(1.0, abs=2e-3)
+    exp = mass / mass.sum() * n
+    keep = exp > 5
+    chi2 = ((counts[keep] - exp[keep]) ** 2 / exp[keep]).sum()
+    assert stats.chi2.sf(chi2, keep.sum() - 1) > 1e-3, chi2
+
+
+def _target_samples(rng, kind, comp, w, n):
+    s = nasg.dist_mixture_sample(kind, cu(np.repeat(comp[None], n, 0)), cu(np.repeat(w[None], n, 0)),
+                                 cu(H.xis(rng, n))).cpu().numpy()
+    return s
+
+
+def test_fit_gradient_nasg_matches_kl_loss_gradient(orc):
+    # the fit's NASG gradient = mean over samples of kl_loss_gradient at b = 0, e = 0
+    # (guiding.cpp:108-165) with q_sampling = p and p_bsdf = 1/(4 pi)
+    rng = np.random.default_rng(12)
+    tc, tw = H.vmf_records(rng, 1, 5)
+    for n_comp in (1, 8):
+        raw = H.raw_outputs(rng, 1, n_comp=n_comp)[0]
+        s4 = _target_samples(rng, nasg.DIST_VMF, tc[0], tw[0], 3000)
+        s4[::50, 3] = 0.0  # p == 0 rows: zero gradient
+        g = nasg.fit_gradient(nasg.DIST_NASG, n_comp, raw, s4)
+        rows = np.zeros((len(s4), 16), np.float32)
+        rows[:, 12:15] = s4[:, :3]
+        rows[:, 3] = s4[:, 3]
+        rows[:, 7] = s4[:, 3]
+        rows[:, 11] = np.float32(0.25 / np.pi)
+        rg, ok, _ = orc.kl_grad(np.repeat(raw[None], len(s4), 0), rows, b=0.0, loss_blend=0.0, n_comp=n_comp)
+        ref = rg.mean(0)
+        assert np.all(np.abs(g - ref) <= 1e-5 * np.abs(ref).max() + 1e-5 * np.abs(ref)), n_comp
+
+
+def test_fit_gradient_vmf_matches_oracle(orc):
+    rng = np.random.default_rng(13)
+    tc, tw = H.nasg_records(rng, 1, 3)
+    for k in (1, 14, 32):
+        raw = rng.normal(0.0, 1.0, 5 * k).astype(np.float32)
+        s4 = _target_samples(rng, nasg.DIST_NASG, tc[0], tw[0], 3000)
+        s4[::50, 3] = 0.0
+        g = nasg.fit_gradient(nasg.DIST_VMF, k, raw, s4)
+        rg, ok = orc.vmf_fit_grad(raw, s4)
+        ref = rg.mean(0)
+        assert np.all(np.abs(g - ref) <= 1e-5 * np.abs(ref).max() + 1e-5 * np.abs(ref)), k
+
+
+def _decode_records(orc, model, k, raw):
+    """explicit records + weights of a fit model's raw vector (CPU)"""
+    if model == nasg.DIST_NASG:
+        d = orc.decode(raw[None], n_comp=k)[0]
+        rec = np.zeros((k, 12))
+        for i in range(k):
+            p = d[13 * i: 13 * i + 13]
+            rec[i, 0:3], rec[i, 3], rec[i, 4:7], rec[i, 7], rec[i, 8:11] = p[3:6], p[9], p[6:9], p[10], p[0:3]
+        w = np.array([d[13 * i + 11] for i in range(k)])
+    else:
+        r = raw[: 3 * k].reshape(k, 3).astype(np.float64)
+        rec = np.zeros((k, 4))
+        rec[:, :3] = r / np.linalg.norm(r, axis=1, keepdims=True)
+        rec[:, 3] = np.clip(np.exp(raw[3 * k: 4 * k].astype(np.float64)), 1e-3, 3e3)
+        e = np.exp(raw[4 * k:].astype(np.float64) - raw[4 * k:].max())
+        w = e / e.sum()
+    return rec.astype(np.float32), w.astype(np.float32)
+
+
+@pytest.mark.parametrize("model,k", [(nasg.DIST_NASG, 8), (nasg.DIST_VMF, 14)])
+def test_fit_kl_matches_cpu_quadrature(orc, model, k):
+    rng = np.random.default_rng(21 + model)
+    tc, tw = H.nasg_records(rng, 1, 3)
+    tc[0, :, 3] = [3.0, 10.0, 1.0]
+    raws = rng.normal(0.0, 0.7, (3, nasg.fit_raw_dim(model, k))).astype(np.float32)
+    nz = 48
+    kl = nasg.fit_kl(nasg.DIST_NASG, tc[0], tw[0], model, k, raws, quad_nz=nz)
+    z = -1.0 + (np.arange(nz) + 0.5) * 2.0 / nz
+    ph = (np.arange(2 * nz) + 0.5) * np.pi / nz
+    Z, P = np.meshgrid(z, ph, indexing="ij")
+    r = np.sqrt(1 - Z * Z)
+    d = np.stack([r * np.cos(P), r * np.sin(P), Z, 0 * Z], -1).reshape(-1, 4)
+    m = len(d)
+    # the kernel evaluates at double grid directions; the oracle takes fp32 ones
+    p = orc.dist_pdf(0, np.repeat(tc, m, 0), np.repeat(tw, m, 0), d.astype(np.float32))
+    for j in range(len(raws)):
+        rec, w = _decode_records(orc, model, k, raws[j])
+        q = orc.dist_pdf(model, np.repeat(rec[None], m, 0), np.repeat(w[None], m, 0), d.astype(np.float32))
+        ref = np.sum(np.where(p > 0, p * np.log(p / np.maximum(q, 1e-300)), 0.0)) * 4 * np.pi / m
+        assert kl[j] == pytest.approx(ref, rel=2e-3, abs=1e-5)
+
+
+def _nasg_lobe(z, hint, lam, a):
+    z = np.asarray(z, np.float64) / np.linalg.norm(z)
+    x = np.cross(hint, z)
+    x /= np.linalg.norm(x)
+    y = np.cross(z, x)
+    return [*x, lam, *y, a, *z, 0.0]
+
+
+def test_fit_self_nasg_component():
+    # target = one NASG component, model N = 1 -> final KL < 1e-2
+    tc = np.array([_nasg_lobe((0.3, -0.5, 0.8), (1.0, 0.0, 0.0), 20.0, 8.0)], np.float32)
+    tw = np.ones(1, np.float32)
+    cfg = nasg.FitConfig(model=nasg.DIST_NASG, n_components=1, batch=1024, steps=1500, checkpoints=5,
+                         learning_rate=0.02, seed=3)
+    raw, kl = nasg.fit(cfg, 3, nasg.DIST_NASG, tc, tw, quad_nz=384)
+    assert np.all(np.isfinite(kl))
+    assert np.all(kl[:, -1] < 1e-2), kl
+    # an untrained model is far away (the fit did the work)
+    rng = np.random.default_rng(3)
+    kl0 = nasg.fit_kl(nasg.DIST_NASG, tc, tw, nasg.DIST_NASG, 1, H.raw_outputs(rng, 4, n_comp=1), quad_nz=384)
+    assert np.all(kl0 > 0.3), kl0
+
+
+def test_fit_is_deterministic():
+    tc = np.array([[0.0, 0.0, 1.0, 5.0]], np.float32)
+    tw = np.ones(1, np.float32)
+    cfg = nasg.FitConfig(model=nasg.DIST_VMF, n_components=3, batch=512, steps=50, checkpoints=2, seed=9)
+    a, ka = nasg.fit(cfg, 2, nasg.DIST_VMF, tc, tw, quad_nz=64)
+    b, kb = nasg.fit(cfg, 2, nasg.DIST_VMF, tc, tw, quad_nz=64)
+    assert np.array_equal(a, b) and np.array_equal(ka, kb)
+
+
+def test_expressiveness_nasg_vs_vmf():
+    # SPEC.md:507-508 / acceptance 6 (:547): on an anisotropic band target,
+    # 8-lobe NASG (64 scalars) reaches a lower KL than 14-lobe vMF (70 scalars)
+    # for every one of 5 seeds after identical Adam budgets; on an isotropic
+    # target the two are within 2x (or both negligible).
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location(
+        "fit_compare", os.path.join(os.path.dirname(os.path.dirname(__file__)), "examples", "fit_compare.py"))
+    fc = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(fc)
+    res = fc.run(seeds=5, steps=2000)
+    band_n, band_v = np.array(res["band"]["nasg8"]["kl_final"]), np.array(res["band"]["vmf14"]["kl_final"])
+    assert np.all(band_n < band_v), (band_n, band_v)
+    iso_n, iso_v = np.median(res["isotropic"]["nasg8"]["kl_final"]), np.median(res["isotropic"]["vmf14"]["kl_final"])
+    assert max(iso_n, iso_v) < 1e-3 or max(iso_n, iso_v) / min(iso_n, iso_v) <= 2.0, (iso_n, iso_v)
