@@ -274,7 +274,8 @@ def bench_render(nasg, args, ws, rank, width, height, iters, label):
         dist.broadcast_object_list(uid, src=0)
         g.comm_init(uid[0], rank, ws)
     rb, re = rank * height // ws, (rank + 1) * height // ws
-    r = nasg.Render(g, scene=scene, width=width, height=height, row_begin=rb, row_end=re, seed=3)
+    r = nasg.Render(g, scene=scene, width=width, height=height, row_begin=rb, row_end=re, seed=3,
+                    lazy_train_stats=True)
     torch.cuda.synchronize()
     barrier(ws)
     l0 = g.kernel_launches + r.kernel_launches

@@ -231,6 +231,9 @@ typedef struct {
     int schedule_b;        /* B = 64 */
     int nee;               /* 1: NEE + MIS (SPEC); 0: emitters reached by scattering only
                               (the brute-force reference of the SPEC's direct-light test) */
+    int lazy_train_stats;  /* 0: stats.train is this iteration's TrainStats (the call waits for
+                              training to finish); 1: stats.train is the previous iteration's
+                              (no wait: the next iteration's tracing is queued behind training) */
 } nasg_render_config;
 typedef struct {
     int64_t iteration;     /* the iteration just rendered */

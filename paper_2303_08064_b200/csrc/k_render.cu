@@ -516,6 +516,8 @@ struct nasg_render {
     uint64_t launches = 0;
     std::vector<void *> bufs;
     int nranks = 1;
+    double *h_acc = nullptr;   // pinned: the last iteration's training statistics (lazy_train_stats)
+    bool acc_pending = false;  // h_acc is being written by the stream
 };
 
 namespace {
@@ -581,6 +583,7 @@ int nasg_render_destroy(nasg_render *r) {
     if (!r) return NASG_OK;
     if (r->stream) cudaStreamSynchronize(r->stream);
     for (void *p : r->bufs) cudaFree(p);
+    if (r->h_acc) cudaFreeHost(r->h_acc);
     if (r->stream) cudaStreamDestroy(r->stream);
     delete r;
     return NASG_OK;
@@ -608,6 +611,7 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
         return code;
     };
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
+    if (cudaMallocHost(&r->h_acc, 5 * sizeof(double)) != cudaSuccess) return fail_out(NASG_ERR_OOM);
     r->rows = c.row_end - c.row_begin;
     Paths &P = r->P;
     P.n = (int64_t)r->rows * c.width;
@@ -665,6 +669,11 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     RCUDA(cudaMemsetAsync(P.ctr, 0, 8 * sizeof(unsigned long long), s));
     RCUDA(cudaMemsetAsync(P.qcount, 0, sizeof(int), s));
     if (c.collect) RCUDA(cudaMemsetAsync(P.rpix, 0xff, P.ncap * sizeof(int), s));
+    // the buffer is usually full (kept = S): shuffle it on a host thread while the GPU traces
+    if (c.collect) {
+        const int rc = ctx_prefetch_shuffle(r->ctx, P.cap_samples);
+        if (rc != NASG_OK) return rc;
+    }
     const unsigned g = grid_of(P.n);
     k_begin<<<g, kBlock, 0, s>>>(P, F);
     r->launches++;
@@ -710,10 +719,18 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     st.nonfinite_paths = (int64_t)ctr[2];
     st.collected = (int64_t)ctr[4];
     st.kept = std::min<int64_t>(st.collected, P.cap_samples);
+    if (c.lazy_train_stats && r->acc_pending) {  // the previous training finished before the sync above
+        ctx_stats_from_acc(r->h_acc, &st.train);
+        r->acc_pending = false;
+    }
     if (c.collect) {
         // Trainer::train_iteration on this rank's buffer (data-parallel across ranks)
-        const int rc = nasg_train_iteration(r->ctx, st.kept, P.samples, b, &st.train, s);
+        const int rc = nasg_train_iteration(r->ctx, st.kept, P.samples, b, c.lazy_train_stats ? nullptr : &st.train, s);
         if (rc != NASG_OK) return rc;
+        if (c.lazy_train_stats) {
+            RCUDA((cudaError_t)(ctx_train_stats_async(r->ctx, r->h_acc, s) == NASG_OK ? cudaSuccess : cudaErrorUnknown));
+            r->acc_pending = true;
+        }
         // l = max(1, l sqrt(s / S)) (guiding.cpp:178-182) with the record-storage floor
         r->l = std::max(r->l_min, nasg_stride_update(r->l, (uint64_t)st.collected, (uint64_t)P.cap_samples));
     }

@@ -19,6 +19,7 @@
 #include "nasg_math.cuh"
 #include "nasg_refmath.cuh"
 #include "simt_gemm.cuh"
+#include "tc_common.cuh"  // bf16 image layout (w_off) for the fused re-pack
 
 namespace nasg {
 
@@ -343,74 +344,92 @@ int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, 
     return train_step_stats_n(sc.tile_loss, sc.tile_loss_count, sc.tile_dropped, ntiles, step_stats, s);
 }
 
-// acc[0..4] = loss_sum, loss_count, dropped, skipped, steps (context accumulators)
-__global__ void finalize_kernel(int *nonfinite, int64_t *adam_t, float *corr, int *skip, const double *step_stats,
-                                double *acc) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    const int sk = *nonfinite != 0;
-    *nonfinite = 0;
-    *skip = sk;
-    if (!sk) {
-        const int64_t t = *adam_t + 1;
-        *adam_t = t;
-        // corr = 1 - beta^t computed as powf would (float result), net.hpp:146-147
-        corr[0] = 1.0f - (float)pow((double)0.9f, (double)(float)t);
-        corr[1] = 1.0f - (float)pow((double)0.999f, (double)(float)t);
-    }
-    acc[0] += step_stats[0];
-    acc[1] += step_stats[1];
-    acc[2] += step_stats[2];
-    acc[3] += sk;
-    acc[4] += 1.0;
-}
-
-int train_finalize_step(int *nonfinite, int64_t *adam_t, float *corr, int *skip, const double *step_stats,
-                        double *acc, cudaStream_t s) {
-    finalize_kernel<<<1, 32, 0, s>>>(nonfinite, adam_t, corr, skip, step_stats, acc);
-    return 1;
-}
 
 // ---------------------------------------------------------------- K_adam --
-// adam_step<float> net.hpp:146-156 with the reference's operation order and
-// IEEE rounding of every float op (no FMA contraction), then re-pack.
+// One launch per step for the whole optimizer tail: the step's skip decision
+// and bias corrections (adam_step<float> net.hpp:137-147: a non-finite
+// gradient skips the update and bumps `skipped`; t++; corr = 1 - beta^t as
+// powf), the update (:148-155) with the reference's operation order and IEEE
+// rounding of every float op (no FMA contraction), the re-pack of the fp32
+// images and, when tc_img != null, of the bf16 tensor-core image, and the
+// statistics accumulation.  Every block reads the step's flag and t before
+// signalling completion; the last block to finish (atomic ticket) advances t,
+// accumulates the step statistics and clears the flag for the next step.
 __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict__ m, float *__restrict__ v,
-                            const float *__restrict__ g, const float *corr, const int *skip, float lr,
-                            float *__restrict__ wp, float *__restrict__ wtp) {
+                            const float *__restrict__ g, float lr, float *__restrict__ wp, float *__restrict__ wtp,
+                            __nv_bfloat16 *__restrict__ tc_img, int *nonfinite, int64_t *adam_t,
+                            const double *step_stats, double *acc, unsigned int *ticket) {
+    __shared__ int s_skip;
+    __shared__ float s_c1, s_c2;
+    if (threadIdx.x == 0) {
+        s_skip = *nonfinite != 0;
+        const int64_t t = *adam_t + 1;
+        // corr = 1 - beta^t computed as powf would (float result), net.hpp:146-147
+        s_c1 = 1.0f - (float)pow((double)0.9f, (double)(float)t);
+        s_c2 = 1.0f - (float)pow((double)0.999f, (double)(float)t);
+    }
+    __syncthreads();
     const int nw = n_weights(n_comp);
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= nw || *skip) return;
-    const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
-    const float c1 = corr[0], c2 = corr[1];
-    const float gi = g[e];
-    const float mi = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(__fsub_rn(1.f, b1), gi));
-    const float vi = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(__fsub_rn(1.f, b2), __fmul_rn(gi, gi)));
-    const float mh = __fdiv_rn(mi, c1), vh = __fdiv_rn(vi, c2);
-    const float wi = __fsub_rn(w[e], __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps)));
-    m[e] = mi;
-    v[e] = vi;
-    w[e] = wi;
-    // re-pack (same mapping as pack_fp32_kernel)
-    const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
-    if (e < o3) {
-        wp[e] = wi;
-        if (e >= o1) {
-            const int l = e < o2 ? 0 : 1, base = l == 0 ? o1 : o2;
-            const int k = (e - base) / kHidden, col = (e - base) % kHidden;
-            wtp[l * kHidden * kHidden + col * kHidden + k] = wi;
+    if (e < nw && !s_skip) {
+        const float b1 = 0.9f, b2 = 0.999f, eps = 1e-8f;
+        const float c1 = s_c1, c2 = s_c2;
+        const float gi = g[e];
+        const float mi = __fadd_rn(__fmul_rn(b1, m[e]), __fmul_rn(__fsub_rn(1.f, b1), gi));
+        const float vi = __fadd_rn(__fmul_rn(b2, v[e]), __fmul_rn(__fsub_rn(1.f, b2), __fmul_rn(gi, gi)));
+        const float mh = __fdiv_rn(mi, c1), vh = __fdiv_rn(vi, c2);
+        const float wi = __fsub_rn(w[e], __fdiv_rn(__fmul_rn(lr, mh), __fadd_rn(__fsqrt_rn(vh), eps)));
+        m[e] = mi;
+        v[e] = vi;
+        w[e] = wi;
+        // re-pack (same mappings as pack_fp32_kernel and pack_tc_kernel)
+        const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
+        int l, n, k;  // layer, output column (packed for the last layer), input row
+        if (e < o3) {
+            wp[e] = wi;
+            l = e < o1 ? 0 : (e < o2 ? 1 : 2);
+            const int base = l == 0 ? 0 : (l == 1 ? o1 : o2);
+            k = (e - base) / kHidden;
+            n = (e - base) % kHidden;
+            if (l > 0) wtp[(l - 1) * kHidden * kHidden + n * kHidden + k] = wi;
+        } else {
+            const int D = 8 * n_comp + 1;
+            k = (e - o3) / D;
+            n = packed_col((e - o3) % D, n_comp);
+            l = 3;
+            wp[o3 + k * kHidden + n] = wi;
+            wtp[2 * kHidden * kHidden + n * kHidden + k] = wi;
         }
-    } else {
-        const int D = 8 * n_comp + 1;
-        const int k = (e - o3) / D, j = (e - o3) % D;
-        const int pc = packed_col(j, n_comp);
-        wp[o3 + k * kHidden + pc] = wi;
-        wtp[2 * kHidden * kHidden + pc * kHidden + k] = wi;
+        if (tc_img) {
+            const int K = l == 0 ? kIn : kHidden;
+            const uint32_t byte = w_off(l) + (n / 8) * (K * 16) + (k / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
+            tc_img[byte / 2] = __float2bfloat16_rn(wi);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ticket, 1u) == gridDim.x - 1) {  // last block: every block has read flag and t
+            const int sk = s_skip;
+            if (!sk) *adam_t = *adam_t + 1;
+            *nonfinite = 0;
+            acc[0] += step_stats[0];
+            acc[1] += step_stats[1];
+            acc[2] += step_stats[2];
+            acc[3] += sk;
+            acc[4] += 1.0;
+            *ticket = 0;
+        }
     }
 }
 
-int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, const float *corr, const int *skip,
-               float lr, float *wp, float *wtp, cudaStream_t s) {
+int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
+               void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
+               unsigned int *ticket, cudaStream_t s) {
     const int nw = n_weights(n_comp);
-    adam_kernel<<<(nw + 255) / 256, 256, 0, s>>>(n_comp, w, m, v, grad, corr, skip, lr, wp, wtp);
+    adam_kernel<<<(nw + 255) / 256, 256, 0, s>>>(n_comp, w, m, v, grad, lr, wp, wtp,
+                                                 static_cast<__nv_bfloat16 *>(tc_img), nonfinite, adam_t,
+                                                 step_stats, acc, ticket);
     return 1;
 }
 

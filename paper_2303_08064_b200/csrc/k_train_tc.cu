@@ -379,8 +379,37 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
     }
 }
 
-// canonical grad[e] = sum over splits (fixed order) of the layer partials
-__global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, float *grad, int *nonfinite) {
+// canonical grad[e] = sum over splits (fixed order) of the layer partials; the
+// grid's extra last block reduces the per-tile loss / count / drop statistics
+// of the step (same fixed order as step_stats_kernel), saving a launch.
+__global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, float *grad, int *nonfinite,
+                                       int ntiles) {
+    if (blockIdx.x == gridDim.x - 1) {
+        __shared__ double sl[256], sc[256], sd[256];
+        const int t = threadIdx.x;
+        double ls = 0.0, lc = 0.0, dr = 0.0;
+        for (int i = t; i < ntiles; i += 256) {
+            ls += tb.tile_loss[i];
+            lc += tb.tile_lc[i];
+            dr += tb.tile_dr[i];
+        }
+        sl[t] = ls; sc[t] = lc; sd[t] = dr;
+        __syncthreads();
+        for (int h = 128; h > 0; h >>= 1) {
+            if (t < h) {
+                sl[t] += sl[t + h];
+                sc[t] += sc[t + h];
+                sd[t] += sd[t + h];
+            }
+            __syncthreads();
+        }
+        if (t == 0) {
+            tb.step_stats[0] = sl[0];
+            tb.step_stats[1] = sc[0];
+            tb.step_stats[2] = sd[0];
+        }
+        return;
+    }
     const int nw = n_weights(n_comp), D = 8 * n_comp + 1;
     const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
     const int e = blockIdx.x * blockDim.x + threadIdx.x;
@@ -424,10 +453,9 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
         cudaFuncSetAttribute(train_tc_dw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         train_tc_dw_kernel<<<dim3(splits, 4), 128, sm, s>>>(tb, ntiles, bps, packed_width(n_comp));
         const int nw = n_weights(n_comp);
-        train_tc_reduce_kernel<<<(nw + 255) / 256, 256, 0, s>>>(tb, splits, n_comp, grad, nonfinite);
-        train_step_stats_n(tb.tile_loss, tb.tile_lc, tb.tile_dr, (int)ntiles, tb.step_stats, s);
+        train_tc_reduce_kernel<<<(nw + 255) / 256 + 1, 256, 0, s>>>(tb, splits, n_comp, grad, nonfinite, (int)ntiles);
     }
-    return 4;
+    return 3;
 }
 
 }  // namespace nasg

@@ -132,13 +132,22 @@ struct nasg_ctx {
     unsigned long long *d_clamp = nullptr;
     // Adam / step state on device
     int64_t *d_adam_t = nullptr;
-    float *d_corr = nullptr;
-    int *d_skip = nullptr, *d_nonfinite = nullptr;
+    int *d_nonfinite = nullptr;
+    unsigned int *d_ticket = nullptr;  // last-block ticket of the fused Adam kernel
     double *d_step_stats = nullptr, *d_acc = nullptr;
     TrainScratch sc{};
     uint32_t *d_order = nullptr, *h_order[2] = {nullptr, nullptr};
     cudaEvent_t order_ev[2] = {nullptr, nullptr};  // recorded after each h_order[i] upload
     int order_slot = 0;
+    // first-epoch shuffle computed ahead on a host thread (ctx_prefetch_shuffle)
+    struct Prefetch {
+        std::thread th;
+        bool active = false;
+        int64_t n = 0;
+        uint64_t iteration = 0;
+        int slot = 0;
+        uint64_t rng_state = 0, rng_inc = 0;  // the shuffle stream after the first epoch
+    } pf;
     size_t order_cap = 0;
     int64_t iterations = 0;
     // host pipeline buffers (nasg_query_sample_host)
@@ -185,8 +194,12 @@ int ensure_scratch(nasg_ctx *c, int64_t count) {
     return NASG_OK;
 }
 
+void join_prefetch(nasg_ctx *c);
+
 int ensure_order(nasg_ctx *c, size_t n) {
     if (n <= c->order_cap) return NASG_OK;
+    join_prefetch(c);  // a prefetch writes into the old buffers
+    c->pf.active = false;
     CUDA_TRY(cudaDeviceSynchronize());  // uploads from the old buffers are done
     if (c->d_order) cudaFree(c->d_order);
     CUDA_TRY(cudaMalloc(&c->d_order, n * sizeof(uint32_t)));
@@ -198,6 +211,25 @@ int ensure_order(nasg_ctx *c, size_t n) {
     }
     c->order_cap = n;
     return NASG_OK;
+}
+
+void join_prefetch(nasg_ctx *c) {
+    if (c->pf.th.joinable()) c->pf.th.join();
+}
+
+// The shuffle stream of train_iteration (guiding.cpp:216-225): rank r uses
+// stream 5 + 2r of Pcg32(hash_combine(seed, 0x7261696e) + iteration).
+Pcg32 shuffle_rng(const nasg_ctx *c, uint64_t iteration) {
+    return Pcg32(hash_combine(c->cfg.seed, 0x7261696e) + iteration, 5 + 2 * (uint64_t)c->rank);
+}
+
+// Fisher-Yates of the identity (the first epoch of an iteration, :219-225).
+void first_epoch_shuffle(uint32_t *ord, int64_t n, Pcg32 &rng) {
+    for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
+    for (int64_t i = n; i > 1; --i) {
+        uint32_t j = rng.next_below((uint32_t)i);
+        std::swap(ord[i - 1], ord[j]);
+    }
 }
 
 int do_publish(nasg_ctx *c) {
@@ -309,13 +341,11 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
         check_finite(c->grad, c->nw, c->d_nonfinite, s);
         c->launches++;
     }
-    train_finalize_step(c->d_nonfinite, c->d_adam_t, c->d_corr, c->d_skip, c->d_step_stats, c->d_acc, s);
-    train_adam(c->N, c->w, c->m, c->v, c->grad, c->d_corr, c->d_skip, c->cfg.learning_rate, c->wp, c->wtp, s);
-    c->launches += 2;
-    if (tc) {  // bf16 operands of the next step from the fp32 master weights
-        launch_pack_tc(c->w, c->N, c->tc_live, s);
-        c->launches++;
-    }
+    // skip decision, t, Adam, re-pack of every live image (the bf16 operands of
+    // the next step included) and the statistics, in one launch
+    train_adam(c->N, c->w, c->m, c->v, c->grad, c->cfg.learning_rate, c->wp, c->wtp, c->tc_live, c->d_nonfinite,
+               c->d_adam_t, c->d_step_stats, c->d_acc, c->d_ticket, s);
+    c->launches += 1;
     CHECK_LAUNCH();
     return NASG_OK;
 }
@@ -413,6 +443,46 @@ int fit_kl_device(int model, int k, const float *d_raws, int n_models, int nz, c
 }
 }  // namespace
 
+namespace nasg {
+// Starts the next train_iteration's first-epoch shuffle for a buffer of n rows
+// on a host thread (used by the render loop while the GPU traces); the
+// iteration consumes it when its buffer has exactly n rows and computes the
+// permutation itself otherwise.  Results are identical either way.
+int ctx_prefetch_shuffle(nasg_ctx *c, int64_t n) {
+    if (!c || n <= 1 || n > 0xffffffffll) return NASG_OK;
+    join_prefetch(c);
+    c->pf.active = false;
+    int r = ensure_order(c, (size_t)n);
+    if (r) return r;
+    c->pf.n = n;
+    c->pf.iteration = (uint64_t)c->iterations;
+    c->pf.slot = c->order_slot ^ 1;
+    c->pf.active = true;
+    c->pf.th = std::thread([c, n]() {
+        cudaSetDevice(c->device);
+        cudaEventSynchronize(c->order_ev[c->pf.slot]);  // the slot's last upload has left
+        Pcg32 rng = shuffle_rng(c, c->pf.iteration);
+        first_epoch_shuffle(c->h_order[c->pf.slot], n, rng);
+        c->pf.rng_state = rng.state;
+        c->pf.rng_inc = rng.inc;
+    });
+    return NASG_OK;
+}
+
+int ctx_train_stats_async(nasg_ctx *c, double *acc, cudaStream_t s) {
+    CUDA_TRY(cudaMemcpyAsync(acc, c->d_acc, 5 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), s));
+    return NASG_OK;
+}
+
+void ctx_stats_from_acc(const double *acc, nasg_train_stats *st) {  // TrainStats (guiding.cpp:278-281)
+    st->steps = (int)acc[4];
+    st->mean_loss = acc[1] > 0 ? acc[0] / acc[1] : 0.0;
+    st->dropped_samples = (uint64_t)acc[2];
+    st->skipped_updates = (uint64_t)acc[3];
+}
+}  // namespace nasg
+
 extern "C" {
 
 const char *nasg_status_string(int s) {
@@ -498,9 +568,8 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     }
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));
-    ALLOC(c->d_corr, 2 * sizeof(float));
-    ALLOC(c->d_skip, sizeof(int));
     ALLOC(c->d_nonfinite, sizeof(int));
+    ALLOC(c->d_ticket, sizeof(unsigned int));
     ALLOC(c->d_step_stats, 3 * sizeof(double));
     ALLOC(c->d_acc, 5 * sizeof(double));
 #undef ALLOC
@@ -508,8 +577,8 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     cudaMemsetAsync(c->v, 0, wb, c->stream);
     cudaMemsetAsync(c->d_clamp, 0, sizeof(unsigned long long), c->stream);
     cudaMemsetAsync(c->d_adam_t, 0, sizeof(int64_t), c->stream);
-    cudaMemsetAsync(c->d_skip, 0, sizeof(int), c->stream);
     cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int), c->stream);
+    cudaMemsetAsync(c->d_ticket, 0, sizeof(unsigned int), c->stream);
     cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream);
     std::vector<float> w(c->nw);
     init_network(cfg->seed, c->N, w.data());
@@ -527,13 +596,14 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
 
 int nasg_destroy(nasg_ctx *c) {
     if (!c) return NASG_OK;
+    join_prefetch(c);
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
     void *bufs[] = {c->tc_live, c->tcb.h0, c->tcb.h1, c->tcb.h2, c->tcb.h3, c->tcb.d1, c->tcb.d2, c->tcb.d3,
                     c->tcb.d4, c->tcb.tile_loss, c->tcb.tile_lc, c->tcb.tile_dr, c->tcb.partial,
                     c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->w_pub, c->wp_pub, c->tc_pub, c->d_clamp,
-                    c->d_adam_t, c->d_corr, c->d_skip, c->d_nonfinite, c->d_step_stats, c->d_acc, c->d_order,
+                    c->d_adam_t, c->d_ticket, c->d_nonfinite, c->d_step_stats, c->d_acc, c->d_order,
                     c->sc.h0, c->sc.h1, c->sc.h2, c->sc.h3, c->sc.d1, c->sc.d2, c->sc.d3, c->sc.d4,
                     c->sc.dw_partial, c->sc.tile_loss, c->sc.tile_loss_count, c->sc.tile_dropped,
                     c->lane_in[0], c->lane_in[1], c->lane_in[2], c->lane_out[0], c->lane_out[1], c->lane_out[2]};
@@ -819,10 +889,7 @@ int nasg_train_stats_take(nasg_ctx *c, nasg_train_stats *st) {
     CUDA_TRY(cudaMemcpyAsync(acc, c->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, sizeof(acc), c->stream));
-    st->steps = (int)acc[4];
-    st->mean_loss = acc[1] > 0 ? acc[0] / acc[1] : 0.0;
-    st->dropped_samples = (uint64_t)acc[2];
-    st->skipped_updates = (uint64_t)acc[3];
+    ctx_stats_from_acc(acc, st);
     return NASG_OK;
 }
 
@@ -922,7 +989,7 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     int r = ensure_order(c, (size_t)std::max<int64_t>(n, 1));
     if (r) return r;
     // epoch shuffle (guiding.cpp:216-225); rank 0 uses the reference's stream 5
-    Pcg32 rng(hash_combine(c->cfg.seed, 0x7261696e) + (uint64_t)c->iterations, 5 + 2 * (uint64_t)c->rank);
+    Pcg32 rng = shuffle_rng(c, (uint64_t)c->iterations);
     // When every minibatch is this rank's whole buffer (config 3: S = t), each
     // step sums over the same set of rows whatever the permutation, so the
     // shuffle cannot change which samples a step sees: rows are read in place
@@ -932,12 +999,26 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     for (int step = 0; step < steps; ++step) whole = whole && local[step] == n;
     uint32_t *ord = nullptr;
     auto reshuffle = [&]() -> int {  // Fisher-Yates :219-224, continuing one rng stream per iteration
+        uint32_t *prev = ord;
+        if (!prev && c->pf.active) {  // first epoch computed ahead by ctx_prefetch_shuffle
+            join_prefetch(c);
+            c->pf.active = false;
+            if (c->pf.n == n && c->pf.iteration == (uint64_t)c->iterations) {
+                c->order_slot = c->pf.slot;
+                ord = c->h_order[c->order_slot];
+                rng.state = c->pf.rng_state;
+                rng.inc = c->pf.rng_inc;
+                return NASG_OK;
+            }
+        }
         c->order_slot ^= 1;
         CUDA_TRY(cudaEventSynchronize(c->order_ev[c->order_slot]));  // its last upload has left
-        uint32_t *prev = ord;
         ord = c->h_order[c->order_slot];
-        if (prev) std::memcpy(ord, prev, n * sizeof(uint32_t));
-        else for (int64_t i = 0; i < n; ++i) ord[i] = (uint32_t)i;
+        if (!prev) {
+            first_epoch_shuffle(ord, n, rng);
+            return NASG_OK;
+        }
+        std::memcpy(ord, prev, n * sizeof(uint32_t));
         for (int64_t i = n; i > 1; --i) {
             uint32_t j = rng.next_below((uint32_t)i);
             std::swap(ord[i - 1], ord[j]);
@@ -957,6 +1038,10 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
         r = train_step_impl(c, samples, whole ? nullptr : c->d_order + cursor, local[step], global[step], b, s);
         if (r) return r;
         cursor += local[step];
+    }
+    if (c->pf.active) {  // prefetched for a different buffer size / unused (whole-buffer steps)
+        join_prefetch(c);
+        c->pf.active = false;
     }
     ++c->iterations;
     if (s != c->stream) {

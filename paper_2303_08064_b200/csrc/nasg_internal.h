@@ -30,7 +30,13 @@ __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHi
 
 // context accessors for the render loop (k_render.cu; nasg_ctx is opaque there)
 int64_t ctx_sample_capacity(const nasg_ctx *c);  // TrainerConfig::sample_capacity S
-int ctx_nranks(const nasg_ctx *c);               // data-parallel ranks (1 without NCCL)
+int ctx_nranks(const nasg_ctx *c);
+// start the next train_iteration's first-epoch shuffle for n rows on a host thread
+int ctx_prefetch_shuffle(nasg_ctx *c, int64_t n);
+// enqueue on s: copy the training statistics accumulators (5 doubles) to a
+// pinned host buffer and clear them; ctx_stats_from_acc converts after a sync
+int ctx_train_stats_async(nasg_ctx *c, double *pinned_acc5, cudaStream_t s);
+void ctx_stats_from_acc(const double *acc5, nasg_train_stats *st);               // data-parallel ranks (1 without NCCL)
 
 struct Bounds {
     float bmin[3];
@@ -146,10 +152,12 @@ int check_finite(const float *x, int n, int *nonfinite, cudaStream_t s);
 int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s);
 // skip decision, Adam t / bias corrections, accumulation of step stats into
 // acc[0..4] = loss_sum, loss_count, dropped, skipped, steps
-int train_finalize_step(int *nonfinite, int64_t *adam_t, float *corr, int *skip,
-                        const double *step_stats, double *acc, cudaStream_t s);
-int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, const float *corr,
-               const int *skip, float lr, float *wp, float *wtp, cudaStream_t s);
+// Fused optimizer tail of one step (skip decision, t, bias corrections,
+// adam_step, re-pack of the fp32 images and of the bf16 image when tc_img is
+// set, statistics into acc, flag reset); ticket: a zeroed device counter.
+int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
+               void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
+               unsigned int *ticket, cudaStream_t s);
 
 
 // ---- explicit mixtures and the fit (k_sphdist.cu) --------------------------

@@ -83,6 +83,25 @@ def test_render_is_deterministic():
     assert np.array_equal(imgs[0][1], imgs[1][1])
 
 
+def test_lazy_train_stats_only_shifts_the_report():
+    # lazy_train_stats = 1 queues the next iteration behind training instead of
+    # waiting for it: same film, same weights; stats.train arrives one call later
+    out = []
+    for lazy in (False, True):
+        g, r = make(nasg.SCENE_BOX, width=80, height=64, seed=7, schedule_m=1, schedule_b=4, lazy_train_stats=lazy)
+        try:
+            tr = [r.iteration()["train"] for _ in range(6)]
+            out.append((r.image(), g.get_weights(), tr))
+        finally:
+            r.close()
+            g.close()
+    (ia, wa, ta), (ib, wb, tb) = out
+    assert np.array_equal(ia, ib) and np.array_equal(wa, wb)
+    assert tb[0].steps == 0
+    assert [t.steps for t in tb[1:]] == [t.steps for t in ta[:-1]]
+    assert [t.mean_loss for t in tb[1:]] == [t.mean_loss for t in ta[:-1]]
+
+
 def test_guided_matches_unguided_mean():
     """Guiding changes variance, never the mean (SPEC tracer invariants)."""
     res = {}
