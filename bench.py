@@ -256,7 +256,7 @@ def bench_sweep(nasg, args, ws, rank):
             **out}
 
 
-def bench_render(nasg, args, ws, rank, width, height, iters, label):
+def bench_render(nasg, args, ws, rank, width, height, iters, label, pipelined=False):
     """Configs 4-5: the guided progressive render loop (nasg_render_*): per iteration one
     path per pixel of this rank's rows (wavefront tracer, NEE+MIS, guided scattering
     through the fused network query), sample collection, one train_iteration (S = 2^16,
@@ -275,7 +275,7 @@ def bench_render(nasg, args, ws, rank, width, height, iters, label):
         g.comm_init(uid[0], rank, ws)
     rb, re = rank * height // ws, (rank + 1) * height // ws
     r = nasg.Render(g, scene=scene, width=width, height=height, row_begin=rb, row_end=re, seed=3,
-                    lazy_train_stats=True)
+                    lazy_train_stats=True, pipelined=pipelined)
     torch.cuda.synchronize()
     barrier(ws)
     l0 = g.kernel_launches + r.kernel_launches
@@ -298,6 +298,8 @@ def bench_render(nasg, args, ws, rank, width, height, iters, label):
             "paths_per_s": width * height * iters / dt, "vertices_per_s_rank0": verts / dt,
             "guided_queries_per_s_rank0": guided / dt, "train_samples_per_iteration_rank0": kept / iters,
             "gpu_launches_rank0": launches, "final_b": st["b"], "image_finite": finite, "scaling": "strong",
+            "loop": ("pipelined: tracing of iteration i+1 overlaps training i on a second stream (snapshot one "
+                     "iteration staler)" if pipelined else "serial SPEC loop: trace i -> train i -> publish -> trace i+1"),
             "cpu_baseline": None, "note": "the reference specifies this tracer (SPEC.md:378-478) but ships no code"}
 
 
@@ -423,9 +425,15 @@ def main():
     if not args.no_render:
         render = {"config4": bench_render(nasg, args, ws, rank, 1024, 1024, 512,
                                           "config 4: 1024x1024, 512 spp, interleaved train/render"),
+                  "config4_pipelined": bench_render(nasg, args, ws, rank, 1024, 1024, 512,
+                                                    "config 4: 1024x1024, 512 spp, interleaved train/render",
+                                                    pipelined=True),
                   "config5": bench_render(nasg, args, ws, rank, 3840, 2160, args.render_4k_iters,
                                           f"config 5: 3840x2160 sharded by pixel rows over {ws} GPU(s), "
-                                          f"{args.render_4k_iters} spp")}
+                                          f"{args.render_4k_iters} spp"),
+                  "config5_pipelined": bench_render(nasg, args, ws, rank, 3840, 2160, args.render_4k_iters,
+                                                    f"config 5: 3840x2160 sharded by pixel rows over {ws} GPU(s), "
+                                                    f"{args.render_4k_iters} spp", pipelined=True)}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
         cpu = cpu_reference_rate(1 << 30, args.cpu_seconds)

@@ -234,6 +234,10 @@ typedef struct {
     int lazy_train_stats;  /* 0: stats.train is this iteration's TrainStats (the call waits for
                               training to finish); 1: stats.train is the previous iteration's
                               (no wait: the next iteration's tracing is queued behind training) */
+    int pipelined;         /* 0: the SPEC loop (iteration i traces with the snapshot training i-1
+                              published); 1: tracing of i+1 overlaps training i on a second stream,
+                              so iteration i traces with the snapshot of training i-2 (one
+                              iteration staler), and stats.train is training i-2's */
 } nasg_render_config;
 typedef struct {
     int64_t iteration;     /* the iteration just rendered */

@@ -45,7 +45,8 @@ class _RenderConfig(C.Structure):
     _fields_ = [("scene", C.c_int), ("width", C.c_int), ("height", C.c_int), ("row_begin", C.c_int),
                 ("row_end", C.c_int), ("seed", C.c_uint64), ("max_depth", C.c_int), ("rr_depth", C.c_int),
                 ("guiding", C.c_int), ("collect", C.c_int), ("ramp", C.c_int), ("schedule_m", C.c_int),
-                ("schedule_b", C.c_int), ("nee", C.c_int), ("lazy_train_stats", C.c_int)]
+                ("schedule_b", C.c_int), ("nee", C.c_int), ("lazy_train_stats", C.c_int),
+                ("pipelined", C.c_int)]
 
 
 class _RenderStats(C.Structure):
@@ -472,7 +473,8 @@ class Render:
     def __init__(self, guide: Guide, scene: int = SCENE_BOX, width: int = 256, height: int = 256,
                  row_begin: int = 0, row_end: int = 0, seed: int = 1, guiding: bool = True,
                  collect: bool = True, ramp: bool = True, max_depth: int = 16, rr_depth: int = 5,
-                 schedule_m: int = 4, schedule_b: int = 64, nee: bool = True, lazy_train_stats: bool = False):
+                 schedule_m: int = 4, schedule_b: int = 64, nee: bool = True, lazy_train_stats: bool = False,
+                 pipelined: bool = False):
         cfg = _RenderConfig()
         lib().nasg_render_config_default(C.byref(cfg))
         cfg.scene, cfg.width, cfg.height = scene, width, height
@@ -482,6 +484,7 @@ class Render:
         cfg.schedule_m, cfg.schedule_b = schedule_m, schedule_b
         cfg.nee = int(nee)
         cfg.lazy_train_stats = int(lazy_train_stats)
+        cfg.pipelined = int(pipelined)
         h = C.c_void_p()
         _check(lib().nasg_render_create(guide._h, C.byref(cfg), C.byref(h)))
         self._h, self.guide = h, guide

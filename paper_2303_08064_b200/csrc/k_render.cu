@@ -516,8 +516,13 @@ struct nasg_render {
     uint64_t launches = 0;
     std::vector<void *> bufs;
     int nranks = 1;
-    double *h_acc = nullptr;   // pinned: the last iteration's training statistics (lazy_train_stats)
-    bool acc_pending = false;  // h_acc is being written by the stream
+    double *h_acc = nullptr;   // pinned 2 x 5: training statistics (lazy_train_stats / pipelined)
+    bool acc_pending[2] = {false, false};
+    // pipelined: trace i+1 overlaps training i (its own stream); two sample buffers
+    nasg_train_sample *samples_buf[2] = {nullptr, nullptr};
+    cudaStream_t tstream = nullptr;
+    cudaEvent_t ev_train = nullptr, ev_acc[2] = {nullptr, nullptr};
+    bool inflight = false;     // trace of iteration `iter` already launched
 };
 
 namespace {
@@ -582,8 +587,12 @@ int nasg_render_scene_bounds(int scene, float bmin[3], float bmax[3]) {
 int nasg_render_destroy(nasg_render *r) {
     if (!r) return NASG_OK;
     if (r->stream) cudaStreamSynchronize(r->stream);
+    if (r->tstream) cudaStreamSynchronize(r->tstream);
     for (void *p : r->bufs) cudaFree(p);
     if (r->h_acc) cudaFreeHost(r->h_acc);
+    if (r->tstream) cudaStreamDestroy(r->tstream);
+    for (cudaEvent_t e : {r->ev_train, r->ev_acc[0], r->ev_acc[1]})
+        if (e) cudaEventDestroy(e);
     if (r->stream) cudaStreamDestroy(r->stream);
     delete r;
     return NASG_OK;
@@ -611,7 +620,14 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
         return code;
     };
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
-    if (cudaMallocHost(&r->h_acc, 5 * sizeof(double)) != cudaSuccess) return fail_out(NASG_ERR_OOM);
+    if (cudaMallocHost(&r->h_acc, 10 * sizeof(double)) != cudaSuccess) return fail_out(NASG_ERR_OOM);
+    if (c.pipelined) {
+        if (cudaStreamCreateWithFlags(&r->tstream, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r->ev_train, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r->ev_acc[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r->ev_acc[1], cudaEventDisableTiming) != cudaSuccess)
+            return fail_out(NASG_ERR_CUDA);
+    }
     r->rows = c.row_end - c.row_begin;
     Paths &P = r->P;
     P.n = (int64_t)r->rows * c.width;
@@ -637,7 +653,9 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     const size_t nrec = (size_t)P.ncap * kMaxDepthCap;
     A(P.rx, nrec) A(P.rwo, nrec) A(P.rn, nrec) A(P.rwi, nrec) A(P.rfc, nrec) A(P.rbeta, nrec) A(P.rlb, nrec)
     A(P.rcnt, P.ncap) A(P.rpix, P.ncap) A(P.roff, P.ncap) A(P.bsum, 1024) A(P.boff, 1024)
-    A(P.ctr, 8) A(P.film, P.n) A(P.frame, P.n) A(P.samples, P.cap_samples)
+    A(P.ctr, 8) A(P.film, P.n) A(P.frame, P.n) A(r->samples_buf[0], P.cap_samples)
+    if (c.pipelined) A(r->samples_buf[1], P.cap_samples)
+    P.samples = r->samples_buf[0];
 #undef A
     if (cudaMemsetAsync(P.film, 0, P.n * sizeof(float4), r->stream) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
     *out = r;
@@ -646,16 +664,21 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
 
 uint64_t nasg_render_kernel_launches(nasg_render *r) { return r ? r->launches : 0; }
 
-int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
-    if (!r) return NASG_ERR_INVALID;
+namespace {
+
+// One iteration's tracing + collection on the render stream (everything but
+// the accumulation): camera rays, up to max_depth bounces of intersection,
+// guided scattering through the fused network query and the update, then the
+// collected paths' training records into `samples`.
+int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samples) {
     const nasg_render_config &c = r->cfg;
     Paths &P = r->P;
     cudaStream_t s = r->stream;
+    P.samples = samples;
     RCUDA(cudaMemcpyToSymbolAsync(c_scene, &r->scene, sizeof(Scene), 0, cudaMemcpyHostToDevice, s));
-    const double b = c.guiding ? nasg_blend_coefficient(r->iter, c.schedule_m, c.schedule_b) : 0.0;
     Frame F{};
     F.seed = c.seed;
-    F.iter = (uint64_t)r->iter;
+    F.iter = (uint64_t)iter;
     F.width = c.width;
     F.height = c.height;
     F.row0 = c.row_begin;
@@ -694,23 +717,54 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     k_queue_reset<<<1, 1, 0, s>>>(P);
     r->launches++;
     if (c.collect) {
+        // pipelined: the training two iterations back read this sample buffer
+        if (r->ev_train) RCUDA(cudaStreamWaitEvent(s, r->ev_train, 0));
         const int nb = (int)((P.ncap + 1023) / 1024);
         k_scan_local<<<nb, 1024, 0, s>>>(P);
         k_scan_blocks<<<1, 1024, 0, s>>>(P, nb);
         k_records<<<grid_of(P.ncap), kBlock, 0, s>>>(P);
         r->launches += 3;
     }
-    const int64_t mb = (int64_t)c.schedule_m * c.schedule_b;
-    const double w = c.ramp ? (double)std::min<int64_t>(r->iter + 1, mb) / (double)mb : 1.0;
-    k_accumulate<<<g, kBlock, 0, s>>>(P, (float)w, r->iter == 0 ? 1 : 0);
-    r->launches++;
     RCUDA(cudaGetLastError());
+    return NASG_OK;
+}
+
+// SPEC accumulate: the progressive w_i ramp (or the plain mean)
+int launch_accumulate(nasg_render *r, int64_t iter) {
+    const nasg_render_config &c = r->cfg;
+    const int64_t mb = (int64_t)c.schedule_m * c.schedule_b;
+    const double w = c.ramp ? (double)std::min<int64_t>(iter + 1, mb) / (double)mb : 1.0;
+    k_accumulate<<<grid_of(r->P.n), kBlock, 0, r->stream>>>(r->P, (float)w, iter == 0 ? 1 : 0);
+    r->launches++;
+    r->wsum += w;
+    RCUDA(cudaGetLastError());
+    return NASG_OK;
+}
+
+double blend_of(const nasg_render *r, int64_t iter) {
+    return r->cfg.guiding ? nasg_blend_coefficient(iter, r->cfg.schedule_m, r->cfg.schedule_b) : 0.0;
+}
+
+}  // namespace
+
+int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
+    if (!r) return NASG_ERR_INVALID;
+    const nasg_render_config &c = r->cfg;
+    Paths &P = r->P;
+    cudaStream_t s = r->stream;
+    const int64_t i = r->iter;
+    const double b = blend_of(r, i);
+    int rc;
+    if (!c.pipelined || !r->inflight) {
+        if ((rc = launch_trace(r, i, b, r->samples_buf[c.pipelined ? (i & 1) : 0])) != NASG_OK) return rc;
+    }
+    if ((rc = launch_accumulate(r, i)) != NASG_OK) return rc;
     unsigned long long ctr[8];
     RCUDA(cudaMemcpyAsync(ctr, P.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s));
     RCUDA(cudaStreamSynchronize(s));
-    r->wsum += w;
+    r->inflight = false;
     nasg_render_stats st{};
-    st.iteration = r->iter;
+    st.iteration = i;
     st.b = b;
     st.stride = r->l;
     st.paths = P.n;
@@ -719,20 +773,45 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     st.nonfinite_paths = (int64_t)ctr[2];
     st.collected = (int64_t)ctr[4];
     st.kept = std::min<int64_t>(st.collected, P.cap_samples);
-    if (c.lazy_train_stats && r->acc_pending) {  // the previous training finished before the sync above
-        ctx_stats_from_acc(r->h_acc, &st.train);
-        r->acc_pending = false;
-    }
     if (c.collect) {
-        // Trainer::train_iteration on this rank's buffer (data-parallel across ranks)
-        const int rc = nasg_train_iteration(r->ctx, st.kept, P.samples, b, c.lazy_train_stats ? nullptr : &st.train, s);
-        if (rc != NASG_OK) return rc;
-        if (c.lazy_train_stats) {
-            RCUDA((cudaError_t)(ctx_train_stats_async(r->ctx, r->h_acc, s) == NASG_OK ? cudaSuccess : cudaErrorUnknown));
-            r->acc_pending = true;
-        }
         // l = max(1, l sqrt(s / S)) (guiding.cpp:178-182) with the record-storage floor
         r->l = std::max(r->l_min, nasg_stride_update(r->l, (uint64_t)st.collected, (uint64_t)P.cap_samples));
+    }
+    if (c.pipelined) {
+        // stats of the training two iterations back (finished: this iteration's
+        // queries waited on the snapshot it published, or on its event below)
+        const int slot = (int)(i & 1);
+        if (r->acc_pending[slot]) {
+            RCUDA(cudaEventSynchronize(r->ev_acc[slot]));
+            ctx_stats_from_acc(r->h_acc + 5 * slot, &st.train);
+            r->acc_pending[slot] = false;
+        }
+        // trace iteration i+1 now, against the snapshot of training i-1 ...
+        if ((rc = launch_trace(r, i + 1, blend_of(r, i + 1), r->samples_buf[(i + 1) & 1])) != NASG_OK) return rc;
+        r->inflight = true;
+        // ... while training i runs on its own stream and publishes for i+2
+        if (c.collect) {
+            rc = nasg_train_iteration(r->ctx, st.kept, r->samples_buf[i & 1], b, nullptr, r->tstream);
+            if (rc != NASG_OK) return rc;
+            if (ctx_train_stats_async(r->ctx, r->h_acc + 5 * slot, r->tstream) != NASG_OK) return NASG_ERR_CUDA;
+            RCUDA(cudaEventRecord(r->ev_acc[slot], r->tstream));
+            RCUDA(cudaEventRecord(r->ev_train, r->tstream));
+            r->acc_pending[slot] = true;
+        }
+    } else {
+        if (c.lazy_train_stats && r->acc_pending[0]) {  // the previous training finished before the sync above
+            ctx_stats_from_acc(r->h_acc, &st.train);
+            r->acc_pending[0] = false;
+        }
+        if (c.collect) {
+            // Trainer::train_iteration on this rank's buffer (data-parallel across ranks)
+            rc = nasg_train_iteration(r->ctx, st.kept, r->samples_buf[0], b, c.lazy_train_stats ? nullptr : &st.train, s);
+            if (rc != NASG_OK) return rc;
+            if (c.lazy_train_stats) {
+                if (ctx_train_stats_async(r->ctx, r->h_acc, s) != NASG_OK) return NASG_ERR_CUDA;
+                r->acc_pending[0] = true;
+            }
+        }
     }
     ++r->iter;
     if (stats) *stats = st;

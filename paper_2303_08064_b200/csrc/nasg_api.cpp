@@ -123,6 +123,16 @@ struct nasg_ctx {
     float *w = nullptr, *m = nullptr, *v = nullptr, *grad = nullptr;
     float *wp = nullptr, *wtp = nullptr;  // packed live (training forward/backward)
     // published snapshot (NetworkSnapshot net.hpp:161)
+    // two snapshot slots (shared_ptr<const> snapshots, net.hpp:161): a publish
+    // fills the slot no reader can still be using, then makes it current
+    struct PubSlot {
+        float *w = nullptr, *wp = nullptr;
+        void *tc = nullptr;
+        cudaEvent_t ev = nullptr;  // recorded on `stream` when the slot's snapshot is complete
+        std::vector<std::pair<cudaStream_t, cudaEvent_t>> readers;  // last query per foreign stream
+    } pub[2];
+    int cur = 0;
+    // the current slot's images (aliases of pub[cur])
     float *w_pub = nullptr, *wp_pub = nullptr;
     void *tc_pub = nullptr;
     int precision = NASG_MLP_FP32;        // query path MLP arithmetic
@@ -157,7 +167,7 @@ struct nasg_ctx {
     ncclComm_t comm = nullptr;
     int rank = 0, nranks = 1;
     uint64_t launches = 0;
-    cudaEvent_t pub_ev = nullptr;  // recorded on `stream` after every publish
+    cudaEvent_t pub_ev = nullptr;  // = pub[cur].ev
 };
 
 namespace nasg {
@@ -233,15 +243,39 @@ void first_epoch_shuffle(uint32_t *ord, int64_t n, Pcg32 &rng) {
 }
 
 int do_publish(nasg_ctx *c) {
-    CUDA_TRY(cudaMemcpyAsync(c->w_pub, c->w, c->nw * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
-    launch_pack_fp32(c->w_pub, c->N, c->wp_pub, nullptr, c->stream);
+    auto &P = c->pub[c->cur ^ 1];
+    // queries still reading that older snapshot on other streams finish first
+    for (auto &rd : P.readers) CUDA_TRY(cudaStreamWaitEvent(c->stream, rd.second, 0));
+    CUDA_TRY(cudaMemcpyAsync(P.w, c->w, c->nw * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+    launch_pack_fp32(P.w, c->N, P.wp, nullptr, c->stream);
     c->launches++;
-    if (c->tc_pub) {
-        launch_pack_tc(c->w_pub, c->N, c->tc_pub, c->stream);
+    if (P.tc) {
+        launch_pack_tc(P.w, c->N, P.tc, c->stream);
         c->launches++;
     }
     CHECK_LAUNCH();
-    CUDA_TRY(cudaEventRecord(c->pub_ev, c->stream));
+    CUDA_TRY(cudaEventRecord(P.ev, c->stream));
+    c->cur ^= 1;
+    c->w_pub = P.w;
+    c->wp_pub = P.wp;
+    c->tc_pub = P.tc;
+    c->pub_ev = P.ev;
+    return NASG_OK;
+}
+
+// A query on stream s read the current snapshot: remember it so the publish
+// that next overwrites this slot waits for it.
+int note_reader(nasg_ctx *c, cudaStream_t s) {
+    if (s == c->stream) return NASG_OK;  // stream order already covers it
+    auto &rd = c->pub[c->cur].readers;
+    cudaEvent_t ev = nullptr;
+    for (auto &x : rd)
+        if (x.first == s) ev = x.second;
+    if (!ev) {
+        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        rd.emplace_back(s, ev);
+    }
+    CUDA_TRY(cudaEventRecord(ev, s));
     return NASG_OK;
 }
 
@@ -305,7 +339,7 @@ int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
     if (r < 0) return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for this path");
     c->launches += r;
     CHECK_LAUNCH();
-    return NASG_OK;
+    return note_reader(c, s);
 }
 
 // One minibatch step (guiding.cpp:236-276) on rows samples[order[0..count)].
@@ -558,14 +592,17 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
         if (cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking) != cudaSuccess)
             return cleanup_fail(fail(NASG_ERR_CUDA, "stream create failed"));
     const size_t wb = c->nw * sizeof(float);
-    ALLOC(c->w, wb); ALLOC(c->m, wb); ALLOC(c->v, wb); ALLOC(c->grad, wb); ALLOC(c->w_pub, wb);
+    ALLOC(c->w, wb); ALLOC(c->m, wb); ALLOC(c->v, wb); ALLOC(c->grad, wb);
+    for (auto &P : c->pub) {
+        ALLOC(P.w, wb);
+        ALLOC(P.wp, kPackedF32 * sizeof(float));
+        if (tc_supported(c->N)) ALLOC(P.tc, tc_image_bytes(c->N));
+        if (cudaEventCreateWithFlags(&P.ev, cudaEventDisableTiming) != cudaSuccess)
+            return cleanup_fail(fail(NASG_ERR_CUDA, "event create failed"));
+    }
     ALLOC(c->wp, kPackedF32 * sizeof(float));
     ALLOC(c->wtp, kPackedT32 * sizeof(float));
-    ALLOC(c->wp_pub, kPackedF32 * sizeof(float));
-    if (tc_supported(c->N)) {
-        ALLOC(c->tc_pub, tc_image_bytes(c->N));
-        ALLOC(c->tc_live, tc_image_bytes(c->N));
-    }
+    if (tc_supported(c->N)) ALLOC(c->tc_live, tc_image_bytes(c->N));
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));
     ALLOC(c->d_nonfinite, sizeof(int));
@@ -582,8 +619,6 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream);
     std::vector<float> w(c->nw);
     init_network(cfg->seed, c->N, w.data());
-    if (cudaEventCreateWithFlags(&c->pub_ev, cudaEventDisableTiming) != cudaSuccess)
-        return cleanup_fail(fail(NASG_ERR_CUDA, "event create failed"));
     if (cudaMemcpyAsync(c->w, w.data(), wb, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
         return cleanup_fail(fail(NASG_ERR_CUDA, "weight upload failed"));
     int r = repack_live(c);
@@ -602,7 +637,8 @@ int nasg_destroy(nasg_ctx *c) {
     if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
     void *bufs[] = {c->tc_live, c->tcb.h0, c->tcb.h1, c->tcb.h2, c->tcb.h3, c->tcb.d1, c->tcb.d2, c->tcb.d3,
                     c->tcb.d4, c->tcb.tile_loss, c->tcb.tile_lc, c->tcb.tile_dr, c->tcb.partial,
-                    c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->w_pub, c->wp_pub, c->tc_pub, c->d_clamp,
+                    c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->pub[0].w, c->pub[0].wp, c->pub[0].tc,
+                    c->pub[1].w, c->pub[1].wp, c->pub[1].tc, c->d_clamp,
                     c->d_adam_t, c->d_ticket, c->d_nonfinite, c->d_step_stats, c->d_acc, c->d_order,
                     c->sc.h0, c->sc.h1, c->sc.h2, c->sc.h3, c->sc.d1, c->sc.d2, c->sc.d3, c->sc.d4,
                     c->sc.dw_partial, c->sc.tile_loss, c->sc.tile_loss_count, c->sc.tile_dropped,
@@ -616,7 +652,10 @@ int nasg_destroy(nasg_ctx *c) {
     for (auto l : c->lanes)
         if (l) cudaStreamDestroy(l);
     if (c->stream) cudaStreamDestroy(c->stream);
-    if (c->pub_ev) cudaEventDestroy(c->pub_ev);
+    for (auto &P : c->pub) {
+        if (P.ev) cudaEventDestroy(P.ev);
+        for (auto &rd : P.readers) cudaEventDestroy(rd.second);
+    }
     delete c;
     return NASG_OK;
 }

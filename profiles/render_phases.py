@@ -19,13 +19,13 @@ sys.path.insert(0, ROOT)
 import paper_2303_08064_b200 as nasg  # noqa: E402
 
 
-def loop(collect, iters, size, lazy=False):
+def loop(collect, iters, size, lazy=False, pipelined=False):
     lo, hi = nasg.scene_bounds(nasg.SCENE_CRACK)
     g = nasg.Guide(nasg.TrainerConfig(seed=5), bmin=lo, bmax=hi)
     g.precision = nasg.NASG_MLP_BF16
     g.train_precision = nasg.NASG_MLP_BF16
     r = nasg.Render(g, scene=nasg.SCENE_CRACK, width=size, height=size, seed=3, collect=collect,
-                    lazy_train_stats=lazy)
+                    lazy_train_stats=lazy, pipelined=pipelined)
     torch.cuda.synchronize()
     per = []
     t0 = time.perf_counter()
@@ -74,6 +74,7 @@ def main():
         print(json.dumps(loop(True, a.iters, a.size, lazy=True)))
         return
     res = {"full": loop(True, a.iters, a.size), "full_lazy_stats": loop(True, a.iters, a.size, lazy=True),
+           "full_pipelined": loop(True, a.iters, a.size, pipelined=True),
            "no_train": loop(False, a.iters, a.size), "train_alone": train_alone()}
     print(json.dumps(res, indent=1))
 

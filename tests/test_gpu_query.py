@@ -190,6 +190,33 @@ def test_snapshot_isolation(orc):
 
 
 @pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_publish_never_overwrites_a_snapshot_in_use(orc, prec):
+    """A reader holds its snapshot (shared_ptr<const> NetworkSnapshot, net.hpp:161,
+    guiding.hpp:139-141): a query queued on another stream behind a long kernel
+    reads the weights that were published when it was issued, even when two
+    publishes (the second one reusing its slot) are issued before it runs."""
+    g = nasg.Guide(nasg.TrainerConfig(seed=3))
+    g.precision = nasg.NASG_MLP_FP32 if prec == "fp32" else nasg.NASG_MLP_BF16
+    rng = np.random.default_rng(4)
+    q9 = H.queries(rng, 4096)
+    xq = _split_q(q9)
+    xi = dev4(H.xis(rng, 4096))
+    ref, _ = g.query_sample(*xq, xi)
+    ref = ref.cpu().numpy()
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        torch.cuda._sleep(200_000_000)  # ~0.1 s: the query below waits behind it
+        out, _ = g.query_sample(*xq, xi, stream=side)
+    g.set_weights(orc.init_network(8))   # publish into the other slot
+    g.set_weights(orc.init_network(9))   # reuses the slot the queued query reads: must wait for it
+    side.synchronize()
+    assert np.array_equal(out.cpu().numpy(), ref)
+    new, _ = g.query_sample(*xq, xi)
+    assert not np.allclose(new.cpu().numpy(), ref)
+    g.close()
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
 def test_packed_rows_match_soa(guide, prec):
     """nasg_query_sample_packed / _host_packed (13-float rows) == the SoA entry points."""
     guide.precision = nasg.NASG_MLP_BF16 if prec == "bf16" else nasg.NASG_MLP_FP32

@@ -102,6 +102,53 @@ def test_lazy_train_stats_only_shifts_the_report():
     assert [t.mean_loss for t in tb[1:]] == [t.mean_loss for t in ta[:-1]]
 
 
+@pytest.mark.parametrize("prec", ["bf16", "fp32"])
+def test_pipelined_loop_is_unbiased_and_deterministic(prec):
+    # pipelined = 1: tracing of i+1 overlaps training i (snapshot one iteration
+    # staler).  The estimator stays unbiased (furnace expectation 0.5 with b = 1
+    # and a network that changes under it), the run is bitwise deterministic, and
+    # stats.train reports training i-2.
+    runs = []
+    for _ in range(2):
+        g, r = make(nasg.SCENE_FURNACE, prec, width=96, height=96, seed=11, schedule_m=1, schedule_b=1,
+                    pipelined=True)
+        try:
+            vals, trains = [], []
+            for it in range(8):
+                st = r.iteration()
+                trains.append(st["train"].steps)
+                fr = r.image(1)[..., 0].ravel().astype(np.float64)
+                if it >= 1:
+                    assert st["b"] == 1.0 and st["guided_vertices"] == st["vertices"] > 0
+                    vals.append(fr)
+            v = np.concatenate(vals)
+            se = v.std() / np.sqrt(v.size)
+            assert abs(v.mean() - 0.5) <= 4 * se, (v.mean(), se)
+            assert trains[:2] == [0, 0] and all(t > 0 for t in trains[2:]), trains
+            runs.append((r.image(), g.get_weights()))
+        finally:
+            r.close()
+            g.close()
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+
+
+def test_pipelined_box_matches_serial_mean():
+    # the box scene's pipelined render agrees with the serial SPEC loop's (both unbiased)
+    means = []
+    for pipelined in (False, True):
+        g, r = make(nasg.SCENE_BOX, width=128, height=128, seed=5, schedule_m=1, schedule_b=4, pipelined=pipelined)
+        try:
+            for _ in range(48):
+                r.iteration()
+            img = r.image().astype(np.float64)
+            means.append((img.mean(), img.std() / np.sqrt(img.size)))
+        finally:
+            r.close()
+            g.close()
+    (ma, sa), (mb, sb) = means
+    assert abs(ma - mb) <= 4 * np.hypot(sa, sb) + 1e-3 * ma, means
+
+
 def test_guided_matches_unguided_mean():
     """Guiding changes variance, never the mean (SPEC tracer invariants)."""
     res = {}
