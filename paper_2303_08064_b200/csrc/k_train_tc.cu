@@ -412,10 +412,13 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
     }
     const int nw = n_weights(n_comp), D = 8 * n_comp + 1;
     const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
-    const int e = blockIdx.x * blockDim.x + threadIdx.x;
+    int e = blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= nw) return;
     int L, m, n;
-    if (e < o1) { L = 0; m = e % kHidden; n = e / kHidden; }           // dW1^T[n_out][k_in]
+    // dW1^T[n_out][k_in] partials: consecutive threads take consecutive k_in so
+    // the split loads coalesce; the canonical W1 index (k_in * 128 + n_out) is
+    // then a strided store, once per weight
+    if (e < o1) { L = 0; m = e / kIn; n = e % kIn; e = n * kHidden + m; }
     else if (e < o2) { L = 1; m = (e - o1) / kHidden; n = (e - o1) % kHidden; }
     else if (e < o3) { L = 2; m = (e - o2) / kHidden; n = (e - o2) % kHidden; }
     else { L = 3; m = (e - o3) / D; n = packed_col((e - o3) % D, n_comp); }
