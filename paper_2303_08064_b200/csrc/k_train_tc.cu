@@ -35,8 +35,9 @@ constexpr uint32_t kATile = 128 * 128 * 2;
 constexpr uint32_t kTmemColsT = 512;
 
 template <int N>
-constexpr size_t fb_smem() {
-    return align1k(img_bytes(N)) + kWGt * kATile + 64 + kWGt * 4 * 3 * sizeof(double);
+constexpr size_t fb_smem() {  // weight image, A tiles, barriers, tile-stat partials, KL scratch
+    return align1k(img_bytes(N)) + kWGt * kATile + 64 + kWGt * 4 * 3 * sizeof(double) +
+           (size_t)kWGt * 2 * N * kKlScStride * sizeof(float);
 }
 
 // byte offset of row t's 16-byte chunk c inside a 128-row block / A tile with F features
@@ -69,6 +70,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
     uint64_t *w_bar = acc_full + kWGt;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     double *red = reinterpret_cast<double *>(smem + A_OFF + kWGt * kATile + 64);
+    float *kl_scratch = reinterpret_cast<float *>(red + kWGt * 4 * 3);
     __shared__ int s_clamped;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -215,7 +217,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 };
                 auto put_lobe = [&](int i, const float (&g8)[8]) { put_chunk(HD / 8 + i, g8); };
                 st = kl_grad_row_fast<N>(valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr, put_lobe,
-                                         lossf);
+                                         lossf, kl_scratch + g * (2 * N * kKlScStride) + t);
                 if (st == kKlOk) {
 #pragma unroll
                     for (int c = 0; c < HD / 8; ++c) put_chunk(c, ghdr + 8 * c);

@@ -424,10 +424,18 @@ enum KlStatus : int {
 // lobe() is called for every i in both passes whatever the row's outcome (and
 // for rows with valid = false), so a warp-collective load behind it stays
 // convergent; only the arithmetic is predicated.
+constexpr int kKlScStride = 128;  // rows per tile: per-row scratch interleaved across threads
+
 template <int N, class LobeFn, class PutLobeFn>
 __device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[packed_header(N)], LobeFn lobe,
                                                 const TrainRow &s, float b, float e, float gscale,
-                                                float (&ghdr)[packed_header(N)], PutLobeFn put_lobe, float &loss) {
+                                                float (&ghdr)[packed_header(N)], PutLobeFn put_lobe, float &loss,
+                                                float *sc) {
+    // The lobe loops are runtime loops (one copy of each body: the unrolled
+    // 2 x N bodies overflowed the instruction cache); the per-lobe values that
+    // cross from pass 1 to pass 2 live in this row's shared-memory scratch
+    // sc[k * kKlScStride], k < 2N: [i] = w_i pdf_i (then the weight-logit
+    // gradient), [N + i] = w_i.
     constexpr int H = packed_header(N);
     loss = 0.f;
     bool fin = true;
@@ -446,28 +454,28 @@ __device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[p
         }
         const float inv = rcp_fast(sum);
 #pragma unroll
-        for (int i = 0; i < N; ++i) w[i] *= inv;
+        for (int i = 0; i < N; ++i) sc[(N + i) * kKlScStride] = w[i] * inv;
         float sm;
         sigmoid_pair(hdr[N], c_sig, sm);
         c = fminf(fmaxf(c_sig, kSelMin), kSelMax);
     }
     const bool live = valid && s.p != 0.f;
-    float pdf[N];
     float q_mix = 0.f;
-    static_for<0, N>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
         float r[8];
         lobe(i, r);
 #pragma unroll
         for (int k = 0; k < 7; ++k) fin &= isfinite(r[k]);
-        pdf[i] = 0.f;
+        float wp = 0.f;
         if (live) {
             Lobe L;
             decode_lobe(r, L);
-            pdf[i] = __expf(lobe_log_g_at(L, s.wi) - L.log_k);
-            q_mix += w[i] * pdf[i];
+            wp = sc[(N + i) * kKlScStride] * __expf(lobe_log_g_at(L, s.wi) - L.log_k);
+            q_mix += wp;
         }
-    });
+        sc[i * kKlScStride] = wp;
+    }
     const float c_eff = b * c;
     const float q_hat = c_eff * q_mix + (1.f - c_eff) * s.pbsdf;
     int status = kKlOk;
@@ -493,18 +501,19 @@ __device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[p
 #pragma unroll
         for (int j = N + 1; j < H; ++j) ghdr[j] = 0.f;
     }
-    static_for<0, N>([&](auto ic) {
-        constexpr int i = decltype(ic)::value;
+#pragma unroll 1
+    for (int i = 0; i < N; ++i) {
         float r[8];
         lobe(i, r);
-        if (!go) return;
+        if (!go) continue;
         LobeG G;
         decode_lobe_g(r, G);
         const Lobe &L = G.L;
-        const float ri = w[i] * pdf[i] * inv_q;  // posterior responsibility
-        const float gl = scale * (ri - w[i]);
+        const float wpi = sc[i * kKlScStride], wi = sc[(N + i) * kKlScStride];
+        const float ri = wpi * inv_q;  // posterior responsibility
+        const float gl = scale * (ri - wi);
         finite &= isfinite(gl);
-        ghdr[i] = gl;
+        sc[i * kKlScStride] = gl;
         // local frame of omega_i (stable fp32 forms, nasg_math.cuh header)
         const float3 v = s.wi;
         const float dz = dot3(v, L.z);
@@ -516,7 +525,7 @@ __device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[p
         const float denom = fmaxf(wl * ql, 1e-12f);
         const float t2 = fminf(fmaxf(dx * dx * rcp_fast(denom), 0.f), 1.f);
         float g7[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d log q / d (ct, sp, cp, st, ctau, lambda, a)
-        if (fminf(wl, ql) >= 1e-6f && pdf[i] > 0.f) {      // pole guard sphdist.cpp:205
+        if (fminf(wl, ql) >= 1e-6f && wpi > 0.f) {         // pole guard sphdist.cpp:205
             const float lam = L.lambda, a = L.a;
             float log_u = sel(wl < 1.f, log1p_fast(-0.5f * fminf(wl, 1.f)), __logf(0.5f * ql));
             log_u = fmaxf(log_u, -27.631021f);
@@ -565,8 +574,10 @@ __device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[p
         g8[7] = 0.f;
         finite &= isfinite(g8[5]) && isfinite(g8[6]);
         put_lobe(i, g8);
-    });
+    }
     if (!go) return status;
+#pragma unroll
+    for (int i = 0; i < N; ++i) ghdr[i] = sc[i * kKlScStride];
     if (!finite) return kKlDrop;
     loss = -ws * (e * __logf(q_hat) + (1.f - e) * __logf(q_mix));
     return kKlOk;
