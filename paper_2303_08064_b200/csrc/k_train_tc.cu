@@ -47,8 +47,21 @@ __device__ __forceinline__ void st_g16(uint8_t *p, uint32_t a, uint32_t b, uint3
     *reinterpret_cast<uint4 *>(p) = make_uint4(a, b, c, d);
 }
 
-__device__ __forceinline__ uint32_t nz_bits(uint32_t p) {  // (lo != 0) | (hi != 0) << 1 of a bf16 pair
-    return ((p & 0xFFFFu) ? 1u : 0u) | ((p >> 16) ? 2u : 0u);
+// ReLU gate flags of the 16 packed bf16 pairs (32 columns) of a drain chunk in
+// one register: pair j's halves set bits 15 - j and 31 - j.  After the ReLU
+// conversion every half is a non-negative bf16 <= 0x7FC0, so adding 0x7FFF to
+// it sets its top bit exactly when it is non-zero, without a carry into the
+// other half (3 instructions per pair: add, shift, and-or).
+__device__ __forceinline__ uint32_t gate_flags(uint32_t acc, uint32_t p, int j) {
+    const uint32_t q = p + 0x7FFF7FFFu;
+    return acc | ((q >> j) & (0x80008000u >> j));
+}
+// 0xFFFF / 0x0000 per half of pair j from the chunk's flags: prmt replicates
+// the sign bit of byte 1 (bit 15) over the low half and of byte 3 over the high
+__device__ __forceinline__ uint32_t gate_mask(uint32_t flags, int j) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(r) : "r"(flags << j));
+    return r;
 }
 
 }  // namespace
@@ -174,7 +187,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
                             p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
-                            bits |= nz_bits(p[h]) << (8 * c + 2 * h);
+                            bits = gate_flags(bits, p[h], 4 * c + h);
                         }
                         tc::st_shared_v4(a_base + blk_off(t, 128) + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
                         st_g16(gh + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
@@ -271,9 +284,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
                             const int i0 = 8 * c + 2 * h;
-                            const float lo = (bits >> i0) & 1u ? v[i0] : 0.f;
-                            const float hi = (bits >> (i0 + 1)) & 1u ? v[i0 + 1] : 0.f;
-                            p[h] = tc::pack_bf16x2(lo, hi);
+                            p[h] = tc::pack_bf16x2(v[i0], v[i0 + 1]) & gate_mask(bits, 4 * c + h);
                         }
                         if (l > 1) tc::st_shared_v4(a_base + blk_off(t, 128) + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
                         st_g16(gd + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
