@@ -130,21 +130,33 @@ __device__ __forceinline__ void sigmoid_pair(float r, float &s, float &sm) {
     sm = r >= 0.f ? small : big;
 }
 
+// 2 sigmoid(r) - 1 = tanh(r/2) = sign(r) (1 - e) / (1 + e) with e = exp(-|r|).
+// A renormalised (sin, cos) pair only needs its direction, so both entries are
+// scaled by (1 + e_a)(1 + e_b) and no reciprocal is taken; the degenerate-pair
+// test (norm < 1e-6, sphdist.cpp:15-25) is applied to the unscaled norm.
+__device__ __forceinline__ void tanh_half_pair(float ra, float rb, float &a, float &b, float &scale2) {
+    const float ea = __expf(-fabsf(ra)), eb = __expf(-fabsf(rb));
+    const float pa = 1.f + ea, pb = 1.f + eb;
+    a = copysignf((1.f - ea) * pb, ra);
+    b = copysignf((1.f - eb) * pa, rb);
+    scale2 = (pa * pb) * (pa * pb);
+}
+
 // decode_full for one lobe (guiding.cpp:26-60) + frame_from_euler.
 __device__ __forceinline__ void decode_lobe(const float r[7], Lobe &L) {
-    float s[5], sm[5];
-#pragma unroll
-    for (int k = 0; k < 5; ++k) sigmoid_pair(r[k], s[k], sm[k]);
-    const float ct = s[0] - sm[0];  // 2 sigmoid - 1
-    float sp = s[1] - sm[1], cp = s[2] - sm[2], st = s[3] - sm[3], ctau = s[4] - sm[4];
+    const float e0 = __expf(-fabsf(r[0])), i0 = rcp_fast(1.f + e0);
+    const float ct = copysignf((1.f - e0) * i0, r[0]);  // 2 sigmoid - 1
+    const float sth = 2.f * sqrt_fast(e0) * i0;          // sqrt(1 - ct^2) = 2 sqrt(s (1 - s))
+    float sp, cp, st, ctau, k1, k2;
+    tanh_half_pair(r[1], r[2], sp, cp, k1);
+    tanh_half_pair(r[3], r[4], st, ctau, k2);
     const float n1 = sp * sp + cp * cp, n2 = st * st + ctau * ctau;
-    const bool d1 = n1 < 1e-12f, d2 = n2 < 1e-12f;  // degenerate pair -> (0, 1)
+    const bool d1 = n1 < 1e-12f * k1, d2 = n2 < 1e-12f * k2;  // degenerate pair -> (0, 1)
     const float i1 = rsqrtf(d1 ? 1.f : n1), i2 = rsqrtf(d2 ? 1.f : n2);
     sp = d1 ? 0.f : sp * i1;
     cp = d1 ? 1.f : cp * i1;
     st = d2 ? 0.f : st * i2;
     ctau = d2 ? 1.f : ctau * i2;
-    const float sth = 2.f * sqrt_fast(s[0] * sm[0]);  // sqrt(1 - ct^2)
     L.z = make_float3(cp * sth, sp * sth, ct);
     L.x = make_float3(ct * cp * ctau - sp * st, ct * sp * ctau + cp * st, -sth * ctau);
     L.y = make_float3(L.z.y * L.x.z - L.z.z * L.x.y, L.z.z * L.x.x - L.z.x * L.x.z, L.z.x * L.x.y - L.z.y * L.x.x);
