@@ -77,6 +77,22 @@ def run(seeds=5, steps=2000, batch=1024, lr=0.02, checkpoints=10, quad_nz=512):
     return out
 
 
+def sweep(seeds=3, steps=2000, batch=1024, lr=0.02, quad_nz=512):
+    """Lobe-count sweep (PAPER Table 4's N axis, position-free): NASG N in
+    {2, 4, 8, 16} and vMF with the same number of scalars (8N / 5 lobes)."""
+    out = {}
+    for tname, (tk, tc, tw) in targets().items():
+        row = {}
+        for n in (2, 4, 8, 16):
+            for model, k in ((nasg.DIST_NASG, n), (nasg.DIST_VMF, max(1, round(8 * n / 5)))):
+                cfg = nasg.FitConfig(model=model, n_components=k, batch=batch, steps=steps, checkpoints=1,
+                                     learning_rate=lr, seed=23)
+                _, kl = nasg.fit(cfg, seeds, tk, tc, tw, quad_nz=quad_nz)
+                row[f"{'nasg' if model == nasg.DIST_NASG else 'vmf'}{k}"] = float(np.median(kl[:, -1]))
+        out[tname] = row
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--seeds", type=int, default=5)
@@ -84,7 +100,15 @@ def main():
     ap.add_argument("--batch", type=int, default=1024)
     ap.add_argument("--lr", type=float, default=0.02)
     ap.add_argument("--json", default=None)
+    ap.add_argument("--sweep", action="store_true", help="lobe-count sweep instead of the 8-vs-14 comparison")
     a = ap.parse_args()
+    if a.sweep:
+        res = sweep(min(a.seeds, 3), a.steps, a.batch, a.lr)
+        for t, row in res.items():
+            print(f"{t:10s} " + "  ".join(f"{m}={v:.4f}" for m, v in row.items()))
+        if a.json:
+            json.dump(res, open(a.json, "w"), indent=1)
+        return
     res = run(a.seeds, a.steps, a.batch, a.lr)
     for t, row in res.items():
         for m, r in row.items():

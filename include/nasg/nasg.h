@@ -293,7 +293,7 @@ int nasg_dist_grad_logpdf(int kind, int64_t n, int k, const float *comp, const f
  * to an analytic target mixture with the guider's KL gradient on directions
  * drawn from the target and the reference's Adam.  Model raw vectors:
  *   NASG  8N+1 floats in the network's raw-output order (guiding.hpp:25-30),
- *         decoded by decode_full (guiding.cpp:15-77); N in {1, 2, 4, 8}
+ *         decoded by decode_full (guiding.cpp:15-77); N in {1, 2, 4, 8, 16}
  *   vMF   5K floats: K unnormalised mean directions (xyz), K log-sharpness,
  *         K weight logits; K <= 32
  * Host buffers; blocks until done. */

@@ -319,7 +319,8 @@ __global__ void __launch_bounds__(128) dist_grad_kernel(int64_t n, int k, const 
 // ---- fit -----------------------------------------------------------------------
 constexpr int kMaxTargetK = 32;
 constexpr int kMaxVmfK = 32;
-constexpr int kMaxRaw = 5 * kMaxVmfK;  // >= packed_width(8) = 80 and 5K for vMF
+constexpr int kMaxRaw = 5 * kMaxVmfK;  // >= packed_width(16) = 160 and 5K for vMF
+static_assert(kMaxRaw >= packed_width(16), "fit scratch too small for N = 16");
 
 struct FitShared {
     float raw[kMaxRaw];       // model parameters (NASG: packed layout; vMF: raw layout)
@@ -715,7 +716,7 @@ int dist_launch(int op, int kind, int64_t n, int k, const float *comp, const flo
     return 1;
 }
 
-int fit_max_components(int model) { return model == NASG_DIST_NASG ? 8 : dist::kMaxVmfK; }
+int fit_max_components(int model) { return model == NASG_DIST_NASG ? 16 : dist::kMaxVmfK; }
 int fit_max_target_components() { return dist::kMaxTargetK; }
 int fit_raw_dim_host(int model, int k) { return dist::fit_raw_dim(model, k); }
 
@@ -756,6 +757,7 @@ int fit_launch(const FitLaunch &L, cudaStream_t s) {
         case 2: return fit_launch_n<2>(L, s);
         case 4: return fit_launch_n<4>(L, s);
         case 8: return fit_launch_n<8>(L, s);
+        case 16: return fit_launch_n<16>(L, s);
         default: return -1;
     }
 }

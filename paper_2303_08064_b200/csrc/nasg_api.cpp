@@ -438,8 +438,8 @@ struct DevBuf {
 
 int fit_check_model(int model, int k) {
     if (model != NASG_DIST_NASG && model != NASG_DIST_VMF) return fail(NASG_ERR_INVALID, "unknown model kind");
-    if (model == NASG_DIST_NASG && k != 1 && k != 2 && k != 4 && k != 8)
-        return fail(NASG_ERR_UNSUPPORTED, "NASG fit: n_components must be 1, 2, 4 or 8");
+    if (model == NASG_DIST_NASG && k != 1 && k != 2 && k != 4 && k != 8 && k != 16)
+        return fail(NASG_ERR_UNSUPPORTED, "NASG fit: n_components must be 1, 2, 4, 8 or 16");
     if (model == NASG_DIST_VMF && (k < 1 || k > fit_max_components(NASG_DIST_VMF)))
         return fail(NASG_ERR_UNSUPPORTED, "vMF fit: n_components must be in [1, 32]");
     return NASG_OK;
@@ -1257,7 +1257,8 @@ int nasg_dist_grad_logpdf(int kind, int64_t n, int k, const float *comp, const f
 }
 
 int nasg_fit_raw_dim(int model, int k) {
-    if (model == NASG_DIST_NASG) return (k == 1 || k == 2 || k == 4 || k == 8) ? fit_raw_dim_host(model, k) : -1;
+    if (model == NASG_DIST_NASG)
+        return (k == 1 || k == 2 || k == 4 || k == 8 || k == 16) ? fit_raw_dim_host(model, k) : -1;
     if (model == NASG_DIST_VMF) return (k >= 1 && k <= fit_max_components(model)) ? fit_raw_dim_host(model, k) : -1;
     return -1;
 }
