@@ -133,6 +133,9 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
     const int64_t ntiles = (nrows + 127) / 128;
     const int64_t stride = (int64_t)gridDim.x * kPairs;
+    // a short device-sized queue (n_dev, the render loop's late bounces) leaves most
+    // CTAs without a tile: they leave before allocating TMEM and loading weights
+    if ((int64_t)blockIdx.x * kPairs >= ntiles) return;
 
     if (threadIdx.x == 0) {
         for (int i = 0; i < kPairs; ++i) {

@@ -46,6 +46,8 @@ struct Paths {
     float4 *o, *d, *beta, *L;
     float *prev_pdf;        // q-hat of the last scatter; < 0: camera ray or delta bounce
     int *alive, *pending;   // pending: a non-delta vertex waiting for K_update
+    int *act[2];            // compacted lists of the paths alive at the start of a bounce (by parity)
+    int *nact;              // their lengths [2]
     float4 *vx, *vn, *vwo, *vdb, *vdn, *vnee;
     int *slot, *rank, *bsdf_ok;
     // guide queue
@@ -90,6 +92,8 @@ __global__ void k_begin(Paths P, Frame F) {
     P.prev_pdf[i] = -1.f;
     P.alive[i] = 1;
     P.pending[i] = 0;
+    P.act[0][i] = (int)i;
+    if (i == 0) P.nact[0] = (int)P.n;
     int rank = -1;
     if (F.collect) {  // one pixel per l x l tile (PAPER §6), uniformly at random per tile and iteration
         const int tx = (int)floorf(px / F.l), ty = (int)floorf(py / F.l);
@@ -108,15 +112,16 @@ __global__ void k_begin(Paths P, Frame F) {
     if (rank >= 0) P.rcnt[rank] = 0;
 }
 
-// per-bounce queue reset; the previous bounce's queue length feeds the counter
-__global__ void k_queue_reset(Paths P) {
+// per-bounce queue reset; the previous bounce's queue length feeds the counter;
+// the list the coming bounce's survivors are appended to starts empty
+__global__ void k_queue_reset(Paths P, int next) {
     P.ctr[1] += (unsigned long long)*P.qcount;
     *P.qcount = 0;
+    P.nact[next] = 0;
 }
 
-__global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.n || !P.alive[i]) return;
+__device__ __forceinline__ void isect_path(Paths &P, const Frame &F, int bounce, int guided, int64_t i) {
+    if (!P.alive[i]) return;
     const Scene &S = c_scene;
     const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
     const uint64_t pix = (uint64_t)py * F.width + px;
@@ -199,9 +204,8 @@ __global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
     P.slot[i] = slot;
 }
 
-__global__ void k_update(Paths P, Frame F, int bounce) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= P.n || !P.pending[i]) return;
+__device__ __forceinline__ void update_path(Paths &P, const Frame &F, int bounce, int64_t i) {
+    if (!P.pending[i]) return;
     P.pending[i] = 0;
     const Scene &S = c_scene;
     const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
@@ -274,6 +278,41 @@ __global__ void k_update(Paths P, Frame F, int bounce) {
     P.o[i] = f4(x + n * kEps, 0.f);
     P.d[i] = f4(v, 0.f);
     P.prev_pdf[i] = qh;
+}
+
+// The bounce kernels walk the compacted list of paths alive at the bounce's
+// start (warp-uniform strides, so whole warps vote together); late bounces,
+// where Russian roulette has ended most paths, touch only the survivors.
+__global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
+    const int *list = P.act[bounce & 1];
+    const int cnt = P.nact[bounce & 1];
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); w < cnt;
+         w += (int64_t)gridDim.x * blockDim.x)
+        if (w + lane < cnt) isect_path(P, F, bounce, guided, list[w + lane]);
+}
+
+// update, then append the paths still alive to the next bounce's list
+// (one warp-aggregated atomic per warp; the list order never changes a path's
+// arithmetic, so the film stays bitwise deterministic)
+__global__ void k_update(Paths P, Frame F, int bounce) {
+    const int *list = P.act[bounce & 1];
+    int *next = P.act[(bounce + 1) & 1];
+    int *ncount = &P.nact[(bounce + 1) & 1];
+    const int cnt = P.nact[bounce & 1];
+    const int lane = threadIdx.x & 31;
+    for (int64_t w = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); w < cnt;
+         w += (int64_t)gridDim.x * blockDim.x) {
+        const bool valid = w + lane < cnt;
+        const int i = valid ? list[w + lane] : 0;
+        if (valid) update_path(P, F, bounce, i);
+        const bool keep = valid && P.alive[i] != 0;
+        const unsigned bal = __ballot_sync(0xffffffffu, keep);
+        int base = 0;
+        if (lane == 0 && bal) base = atomicAdd(ncount, __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (keep) next[base + __popc(bal & ((1u << lane) - 1u))] = i;
+    }
 }
 
 // Exclusive prefix sum of the collected paths' record counts, in two passes:
@@ -516,6 +555,7 @@ struct nasg_render {
     uint64_t launches = 0;
     std::vector<void *> bufs;
     int nranks = 1;
+    int nsm = 148;
     double *h_acc = nullptr;   // pinned 2 x 5: training statistics (lazy_train_stats / pipelined)
     bool acc_pending[2] = {false, false};
     // pipelined: trace i+1 overlaps training i (its own stream); two sample buffers
@@ -614,6 +654,11 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
         return NASG_ERR_INVALID;
     }
     r->nranks = std::max(1, ctx_nranks(ctx));
+    {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&r->nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
     int rc = NASG_OK;
     auto fail_out = [&](int code) {
         nasg_render_destroy(r);
@@ -647,7 +692,7 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     if ((rc = alloc(r, &(ptr), (size_t)(count))) != NASG_OK) return fail_out(rc);
     A(P.o, P.n) A(P.d, P.n) A(P.beta, P.n) A(P.L, P.n) A(P.prev_pdf, P.n) A(P.alive, P.n) A(P.pending, P.n)
     A(P.vx, P.n) A(P.vn, P.n) A(P.vwo, P.n) A(P.vdb, P.n) A(P.vdn, P.n) A(P.vnee, P.n)
-    A(P.slot, P.n) A(P.rank, P.n) A(P.bsdf_ok, P.n)
+    A(P.slot, P.n) A(P.rank, P.n) A(P.bsdf_ok, P.n) A(P.act[0], P.n) A(P.act[1], P.n) A(P.nact, 2)
     A(P.qx, P.n) A(P.qwo, P.n) A(P.qn, P.n) A(P.qxi, P.n) A(P.qdb, P.n) A(P.qdn, P.n) A(P.qout, 2 * P.n)
     A(P.qcount, 1)
     const size_t nrec = (size_t)P.ncap * kMaxDepthCap;
@@ -701,9 +746,10 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
     k_begin<<<g, kBlock, 0, s>>>(P, F);
     r->launches++;
     const bool guided = b > 0.0;
+    const unsigned gb = std::min<unsigned>(g, (unsigned)r->nsm * 8u);  // list-walking bounce kernels
     for (int bounce = 0; bounce < c.max_depth; ++bounce) {
-        k_queue_reset<<<1, 1, 0, s>>>(P);
-        k_isect<<<g, kBlock, 0, s>>>(P, F, bounce, guided ? 1 : 0);
+        k_queue_reset<<<1, 1, 0, s>>>(P, (bounce + 1) & 1);
+        k_isect<<<gb, kBlock, 0, s>>>(P, F, bounce, guided ? 1 : 0);
         r->launches += 2;
         if (guided) {
             const int rc = nasg_query_shade(r->ctx, P.n, P.qcount, (const float *)P.qx, (const float *)P.qwo,
@@ -711,10 +757,10 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
                                             (const float *)P.qdn, (float)b, (float *)P.qout, s);
             if (rc != NASG_OK) return rc;
         }
-        k_update<<<g, kBlock, 0, s>>>(P, F, bounce);
+        k_update<<<gb, kBlock, 0, s>>>(P, F, bounce);
         r->launches++;
     }
-    k_queue_reset<<<1, 1, 0, s>>>(P);
+    k_queue_reset<<<1, 1, 0, s>>>(P, c.max_depth & 1);
     r->launches++;
     if (c.collect) {
         // pipelined: the training two iterations back read this sample buffer
