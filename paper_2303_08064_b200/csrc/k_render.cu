@@ -26,6 +26,25 @@
 #include <cstdio>
 #include <cstring>
 #include <vector>
+#ifdef NASG_RENDER_PROF  // development-only phase timing (scratch builds), compiled out of the library
+#include <chrono>
+namespace {
+struct RProf {
+    cudaEvent_t a = nullptr, b = nullptr, c = nullptr, pc = nullptr;  // trace start, trace end, train end
+    double host[4] = {0, 0, 0, 0}, gpu[3] = {0, 0, 0};
+    int n = 0, ng = 0;
+    std::chrono::steady_clock::time_point t0;
+    ~RProf() {
+        if (n) fprintf(stderr, "[rprof] %d it: host enqueue-trace %.3f ms, wait-sync %.3f ms, train-call %.3f ms, rest %.3f ms | gpu trace %.3f, sync->train-end %.3f, idle-before-trace %.3f ms (%d)\n",
+                       n, host[0] / n, host[1] / n, host[2] / n, host[3] / n, gpu[0] / ng, gpu[1] / ng, gpu[2] / ng, ng);
+    }
+};
+RProf g_rprof;
+double ms_since(std::chrono::steady_clock::time_point t) {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count();
+}
+}  // namespace
+#endif
 
 #include <cuda_runtime.h>
 
@@ -801,13 +820,41 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     const int64_t i = r->iter;
     const double b = blend_of(r, i);
     int rc;
+#ifdef NASG_RENDER_PROF
+    RProf &pf = g_rprof;
+    if (!pf.a) {
+        cudaEventCreate(&pf.a); cudaEventCreate(&pf.b); cudaEventCreate(&pf.c); cudaEventCreate(&pf.pc);
+    }
+    auto T0 = std::chrono::steady_clock::now();
+    const bool have_prev = pf.n > 0;
+    cudaEventRecord(pf.a, s);
+#endif
     if (!c.pipelined || !r->inflight) {
         if ((rc = launch_trace(r, i, b, r->samples_buf[c.pipelined ? (i & 1) : 0])) != NASG_OK) return rc;
     }
     if ((rc = launch_accumulate(r, i)) != NASG_OK) return rc;
     unsigned long long ctr[8];
+#ifdef NASG_RENDER_PROF
+    cudaEventRecord(pf.b, s);
+    pf.host[0] += ms_since(T0);
+    auto T1 = std::chrono::steady_clock::now();
+#endif
     RCUDA(cudaMemcpyAsync(ctr, P.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s));
     RCUDA(cudaStreamSynchronize(s));
+#ifdef NASG_RENDER_PROF
+    pf.host[1] += ms_since(T1);
+    {
+        float x = 0.f;
+        cudaEventElapsedTime(&x, pf.a, pf.b);
+        pf.gpu[0] += x;
+        if (have_prev) {
+            cudaEventElapsedTime(&x, pf.pc, pf.a);  // previous train end -> this trace start
+            pf.gpu[2] += x;
+            ++pf.ng;
+        }
+    }
+    auto T2 = std::chrono::steady_clock::now();
+#endif
     r->inflight = false;
     nasg_render_stats st{};
     st.iteration = i;
@@ -859,6 +906,11 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
             }
         }
     }
+#ifdef NASG_RENDER_PROF
+    pf.host[2] += ms_since(T2);
+    cudaEventRecord(pf.pc, s);
+    ++pf.n;
+#endif
     ++r->iter;
     if (stats) *stats = st;
     return NASG_OK;
