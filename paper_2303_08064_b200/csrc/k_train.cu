@@ -116,43 +116,40 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
         store_rows<kHidden>(h1, sc.h1, row0, valid, tid);
         store_rows<kHidden>(h2, sc.h2, row0, valid, tid);
         store_rows<kHidden>(h3, sc.h3, row0, valid, tid);
-        // ---- K5: KL gradient epilogue, one thread per row (guiding.cpp:250-270)
-        if (tid < kTrainRows) {
-            float *col = da + tid;
+        // ---- K5: KL gradient epilogue (guiding.cpp:250-270), 4 lanes per row: all
+        // 8 warps run the double-precision math (kl_grad_row_par, 2 lobes per lane)
+        {
+            const int row = tid >> 2, part = tid & 3;
+            float *col = da + row;
+            bool rfin = true;  // non-finite network output row -> dropped (:251-254)
+            for (int j = part; j < NP; j += 4) rfin &= isfinite(col[j * kTLda]);
+#pragma unroll
+            for (int o = 1; o < 4; o <<= 1) rfin &= __shfl_xor_sync(0xffffffffu, (int)rfin, o) != 0;
+            const bool vrow = row < valid;
+            const float *rd = rowd + row * 8;
+            TrainRow s;
+            s.wi = make_float3(rd[0], rd[1], rd[2]);
+            s.p = (vrow && rfin) ? rd[3] : 0.f;  // p = 0: zero gradient (invalid and dropped rows too)
+            s.q_s = rd[4];
+            s.pbsdf = rd[5];
             double loss = 0.0;
-            int state = 0;  // 0 invalid row, 1 ok, 2 dropped
-            if (tid < valid) {
-                bool finite = true;
-                for (int j = 0; j < NP; ++j) finite &= isfinite(col[j * kTLda]);
-                if (!finite) {  // non-finite network output row -> dropped (:251-254)
-                    for (int j = 0; j < kHidden; ++j) col[j * kTLda] = 0.f;
-                    state = 2;
-                } else {
-                    const float *rd = rowd + tid * 8;
-                    TrainRow s;
-                    s.wi = make_float3(rd[0], rd[1], rd[2]);
-                    s.p = rd[3]; s.q_s = rd[4]; s.pbsdf = rd[5];
-                    auto raw = [&](int j) { return col[j * kTLda]; };
-                    auto put = [&](int j, float g) { col[j * kTLda] = g; };
-                    bool ok = ref::kl_grad_row<N>(raw, s, b, e, gscale, put, loss);
-                    state = ok ? 1 : 2;
-                    for (int j = NP; j < kHidden; ++j) col[j * kTLda] = 0.f;
-                }
-            } else {
-                for (int j = 0; j < kHidden; ++j) col[j * kTLda] = 0.f;
-            }
-            rloss[tid] = (state == 1 && isfinite(loss)) ? loss : 0.0;
-            rstate[tid] = state == 1 && isfinite(loss) ? 1 : (state == 2 ? 2 : 0);
-            // delta4 in reference raw order, padded to 80 floats per row
-            float *g4 = sc.d4 + (row0 + tid) * 80;
-            if (tid < valid) {
-                for (int j = 0; j < D; ++j) g4[j] = col[packed_col(j, N) * kTLda];
-                for (int j = D; j < 80; ++j) g4[j] = 0.f;
-            } else {
-                for (int j = 0; j < 80; ++j) g4[j] = 0.f;
+            __syncwarp();  // the finiteness reads are done before any lane writes its columns
+            auto raw = [&](int j) { return col[j * kTLda]; };
+            auto put = [&](int j, float g) { col[j * kTLda] = g; };
+            const bool ok = ref::kl_grad_row_par<N, 4>(raw, s, b, e, gscale, part, put, loss);
+            for (int j = NP + part; j < kHidden; j += 4) col[j * kTLda] = 0.f;
+            if (part == 0) {
+                const int state = !vrow ? 0 : (!rfin ? 2 : (ok ? 1 : 2));  // 0 invalid row, 1 ok, 2 dropped
+                rloss[row] = (state == 1 && isfinite(loss)) ? loss : 0.0;
+                rstate[row] = state == 1 && isfinite(loss) ? 1 : (state == 2 ? 2 : 0);
             }
         }
         __syncthreads();
+        // delta4 in reference raw order, padded to 80 floats per row (K_dw operand)
+        for (int idx = tid; idx < kTrainRows * 80; idx += 256) {
+            const int r = idx / 80, j = idx % 80;
+            sc.d4[(row0 + r) * 80 + j] = (r < valid && j < D) ? da[packed_col(j, N) * kTLda + r] : 0.f;
+        }
         if (tid == 0) {  // tile statistics in row order (deterministic)
             double ls = 0.0;
             int lc = 0, dr = 0;

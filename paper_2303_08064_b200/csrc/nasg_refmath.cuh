@@ -418,5 +418,115 @@ __device__ __forceinline__ bool kl_grad_row(RawFn raw, const TrainRow &s, double
     return true;
 }
 
+
+// kl_grad_row with P consecutive lanes per row (the fp32 trainer: 4 lanes x 64
+// rows keep all 8 warps busy in the double-precision epilogue instead of 2).
+// Lane `part` owns lobes [part N/P, (part + 1) N/P): their decode, pdf, grad
+// log pdf and output columns; q_mix and the finiteness of the row's gradient
+// are combined over the P lanes with shuffles (q_mix summed pairwise rather
+// than in lobe order: the reference's value to double rounding).  Part 0 also
+// writes the selection-probability column, the header padding and the loss.
+// Every lane of the warp must call it (the shuffles use the full mask); rows
+// the caller does not use pass p = 0.  Returns the row status as kl_grad_row.
+template <int N, int P, class RawFn, class PutFn>
+__device__ __forceinline__ bool kl_grad_row_par(RawFn raw, const TrainRow &s, double b, double e, double gscale,
+                                                int part, PutFn put, double &loss) {
+    static_assert(N % P == 0 && (P & (P - 1)) == 0 && P <= 32, "lobes must split evenly over a power-of-2 group");
+    constexpr int H = packed_header(N), NL = N / P;
+    const int i0 = part * NL;
+    double w[N], c, c_sig;
+    decode_header<N>(raw, w, c, c_sig);
+    const V3 v = {(double)s.wi.x, (double)s.wi.y, (double)s.wi.z};
+    auto lobe_of = [&](int i, Lobe &L) {  // runtime lobe index: logits read from the caller's tile
+        float r[7];
+#pragma unroll
+        for (int k = 0; k < 7; ++k) r[k] = raw(H + 8 * i + k);
+        decode_lobe(r, L);
+    };
+    auto wsel = [&](int i) {  // w[i] for a runtime i without dynamic register indexing
+        double x = w[0];
+#pragma unroll
+        for (int j = 1; j < N; ++j) x = i == j ? w[j] : x;
+        return x;
+    };
+    double q_part = 0.0;
+#pragma unroll 1
+    for (int k = 0; k < NL; ++k) {
+        Lobe L;
+        lobe_of(i0 + k, L);
+        q_part += wsel(i0 + k) * lobe_pdf(L, v);
+    }
+    double q_mix = q_part;
+#pragma unroll
+    for (int o = 1; o < P; o <<= 1) q_mix += __shfl_xor_sync(0xffffffffu, q_mix, o);
+    const double c_eff = b * c;
+    const double q_hat = c_eff * q_mix + (1.0 - c_eff) * (double)s.pbsdf;
+    const bool live = s.p != 0.f;
+    const bool usable = isfinite(q_mix) && q_mix > 1e-300 && isfinite(q_hat) && q_hat > 1e-300 && s.q_s > 0.f;
+    const double ws = (double)s.p / (double)s.q_s;
+    const double mix_scale = e * (c_eff * q_mix / q_hat) + (1.0 - e);
+    const double scale = -ws * mix_scale;
+    bool finite = true;
+    const double c_clamped = c != c_sig ? 0.0 : 1.0;
+    const double dsig_c = c_sig * (1.0 - c_sig) * c_clamped;
+    const double gc = -ws * e * b * (q_mix - (double)s.pbsdf) / q_hat * dsig_c;
+    if (part == 0) finite &= isfinite(gc);
+    float gl_own[NL], go_own[NL][8];
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+        const int i = i0 + k;
+        Lobe L;
+        lobe_of(i, L);
+        const double wi = wsel(i);
+        const PGrad pg = grad_logpdf(L, wi, v, q_mix);
+        double dt[5] = {pg.d[0], pg.d[1], pg.d[2], pg.d[3], pg.d[4]};
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+            const double inv = L.pn[p] > 0.0 ? 1.0 / L.pn[p] : 0.0;
+            dt[1 + 2 * p] *= inv;
+            dt[2 + 2 * p] *= inv;
+        }
+        double go[8];
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk) go[kk] = scale * dt[kk] * 2.0 * L.sig[kk] * (1.0 - L.sig[kk]);
+        go[5] = L.lam_clamped ? 0.0 : scale * pg.d[5] * L.lambda;
+        go[6] = L.a_clamped ? 0.0 : scale * pg.d[6] * L.a;
+        go[7] = 0.0;
+        const double r_i = wi * lobe_pdf(L, v) / q_mix;
+        const double gl = scale * (r_i - wi);
+        finite &= isfinite(gl);
+        gl_own[k] = (float)(gl * gscale);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+            finite &= isfinite(go[kk]);
+            go_own[k][kk] = (float)(go[kk] * gscale);
+        }
+    }
+#pragma unroll
+    for (int o = 1; o < P; o <<= 1) finite &= __shfl_xor_sync(0xffffffffu, (int)finite, o) != 0;
+    __syncwarp();  // the group's reads of shared header columns precede every lane's writes
+    const bool emit = live && usable && finite;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+        const int i = i0 + k;
+        put(i, emit ? gl_own[k] : 0.f);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) put(H + 8 * i + kk, emit ? go_own[k][kk] : 0.f);
+    }
+    if (part == 0) {
+        put(N, emit ? (float)(gc * gscale) : 0.f);
+        for (int j = N + 1; j < H; ++j) put(j, 0.f);
+    }
+    loss = 0.0;
+    if (!live) return true;
+    if (!usable) {
+        loss = NAN;
+        return false;
+    }
+    if (!finite) return false;
+    loss = -ws * (e * log(q_hat) + (1.0 - e) * log(q_mix));
+    return true;
+}
+
 }  // namespace ref
 }  // namespace nasg
