@@ -118,22 +118,36 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
         tile_layer<128, kHidden, kEpiRelu>(actA, actA, W2, wbuf, nullptr, tid);
         tile_layer<128, kHidden, kEpiRelu>(actA, actA, W3, wbuf, nullptr, tid);
         tile_layer<128, kHidden, kEpiNone>(actA, actA, W4, wbuf, nullptr, tid);
-        if (tid < kTileRows) {
+        if constexpr (MODE == kModeSample || MODE == kModePdf) {
+            // double-precision epilogue on all 8 warps: 2 lanes per query, 4 lobes each
+            const int row = tid >> 1, part = tid & 1;
+            const int64_t q = row0 + row;
+            const bool valid = q < nrows;
+            const float *col = actA + row;
+            auto raw = [&](int j) { return col[j * kLda]; };
+            if constexpr (MODE == kModeSample) {
+                float c;
+                const float4 o = ref::guide_sample_par<N, 2>(raw, valid ? load_xi(a, q) : make_float4(0.f, 0.f, 0.f, 0.f),
+                                                             part, c);
+                if (valid && part == 0) {
+                    a.dir_pdf[q] = o;
+                    if (a.c) a.c[q] = c;
+                }
+            } else {
+                const float4 d = valid ? a.dir[q] : make_float4(0.f, 0.f, 1.f, 0.f);
+                const float2 p = ref::guide_pdf_par<N, 2>(raw, make_float3(d.x, d.y, d.z), a.b,
+                                                          (valid && a.bsdf_pdf) ? a.bsdf_pdf[q] : 0.f, part);
+                if (valid && part == 0) {
+                    if (a.mix_pdf) a.mix_pdf[q] = p.x;
+                    if (a.guided_pdf) a.guided_pdf[q] = p.y;
+                }
+            }
+        } else if (tid < kTileRows) {
             const int64_t q = row0 + tid;
             if (q < nrows) {
                 const float *col = actA + tid;
                 auto raw = [&](int j) { return col[j * kLda]; };
-                if (MODE == kModeSample) {
-                    float c;
-                    a.dir_pdf[q] = ref::guide_sample<N>(raw, load_xi(a, q), c);
-                    if (a.c) a.c[q] = c;
-                } else if (MODE == kModePdf) {
-                    float4 d = a.dir[q];
-                    float2 p = ref::guide_pdf<N>(raw, make_float3(d.x, d.y, d.z), a.b,
-                                                  a.bsdf_pdf ? a.bsdf_pdf[q] : 0.f);
-                    if (a.mix_pdf) a.mix_pdf[q] = p.x;
-                    if (a.guided_pdf) a.guided_pdf[q] = p.y;
-                } else if (MODE == kModeShade) {
+                if (MODE == kModeShade) {
                     float4 o0, o1;
                     ref::guide_shade<N>(raw, load_xi(a, q), a.b, a.sh_bsdf[q], a.sh_nee[q], o0, o1);
                     a.sh_out[2 * q] = o0;

@@ -258,6 +258,72 @@ __device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float
     o1 = make_float4((float)pn, (float)ce, tech ? 1.f : 0.f, (float)c);
 }
 
+// ---- lane-parallel forms for the fp32 query kernel: P consecutive lanes per
+// query, each decoding N/P lobes for the mixture pdf (combined by shuffles, so
+// the sum is pairwise instead of in lobe order: equal to double rounding).  The
+// lobe pick and the sample are computed redundantly by every lane of the group
+// (identical values).  All 32 lanes must call them (full-mask shuffles).
+template <int N>
+__device__ __forceinline__ double wsel(const double (&w)[N], int i) {  // w[i], runtime i, no local memory
+    double x = w[0];
+#pragma unroll
+    for (int j = 1; j < N; ++j) x = i == j ? w[j] : x;
+    return x;
+}
+
+template <int N, int P, class RawFn>
+__device__ __forceinline__ double mixture_pdf_par(RawFn raw, const double (&w)[N], const V3 &v, int part) {
+    constexpr int NL = N / P;
+    double pdf = 0.0;
+#pragma unroll
+    for (int k = 0; k < NL; ++k) {
+        const int i = part * NL + k;
+        float r[7];
+        load_lobe<N>(raw, i, r);
+        Lobe L;
+        decode_lobe(r, L);
+        pdf += wsel<N>(w, i) * lobe_pdf(L, v);
+    }
+#pragma unroll
+    for (int o = 1; o < P; o <<= 1) pdf += __shfl_xor_sync(0xffffffffu, pdf, o);
+    return pdf;
+}
+
+template <int N, int P, class RawFn>
+__device__ __forceinline__ float4 guide_sample_par(RawFn raw, float4 xi, int part, float &c_out) {
+    double w[N], c, c_sig;
+    decode_header<N>(raw, w, c, c_sig);
+    c_out = (float)c;
+    int pick = N - 1;
+    double acc = 0.0;
+    bool found = false;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        acc += w[i];
+        const bool hit = !found && (double)xi.x < acc;
+        pick = hit ? i : pick;
+        found |= hit;
+    }
+    float rs[7];
+    load_lobe<N>(raw, pick, rs);
+    Lobe Ls;
+    decode_lobe(rs, Ls);
+    const V3 v = lobe_sample(Ls, (double)xi.y, (double)xi.z, (double)xi.w);
+    const double pdf = mixture_pdf_par<N, P>(raw, w, v, part);
+    return make_float4((float)v.x, (float)v.y, (float)v.z, (float)pdf);
+}
+
+template <int N, int P, class RawFn>
+__device__ __forceinline__ float2 guide_pdf_par(RawFn raw, float3 dir, float b, float bsdf_pdf, int part) {
+    double w[N], c, c_sig;
+    decode_header<N>(raw, w, c, c_sig);
+    const V3 v = {(double)dir.x, (double)dir.y, (double)dir.z};
+    const double pdf = mixture_pdf_par<N, P>(raw, w, v, part);
+    const double ce = (double)b * c;
+    const double guided = ce <= 0.0 ? (double)bsdf_pdf : ce * pdf + (1.0 - ce) * (double)bsdf_pdf;
+    return make_float2((float)pdf, (float)guided);
+}
+
 // ---- KL gradient (guiding.cpp:96-176, sphdist.cpp:200-274) -----------------------
 struct Euler {
     double ct, sp, cp, st, ctau;
@@ -443,12 +509,7 @@ __device__ __forceinline__ bool kl_grad_row_par(RawFn raw, const TrainRow &s, do
         for (int k = 0; k < 7; ++k) r[k] = raw(H + 8 * i + k);
         decode_lobe(r, L);
     };
-    auto wsel = [&](int i) {  // w[i] for a runtime i without dynamic register indexing
-        double x = w[0];
-#pragma unroll
-        for (int j = 1; j < N; ++j) x = i == j ? w[j] : x;
-        return x;
-    };
+    auto wsel = [&](int i) { return ref::wsel<N>(w, i); };
     double q_part = 0.0;
 #pragma unroll 1
     for (int k = 0; k < NL; ++k) {
