@@ -74,7 +74,14 @@ public:
         check(nasg_query_pdf(ctx_, n, x, wo, nrm, dir, b, bsdf_pdf, mix_pdf, guided_pdf, stream));
     }
 
+    // guided scattering at wavefront vertices (nasg.h nasg_query_shade)
+    void shade(std::int64_t n, const int *n_dev, const float *x, const float *wo, const float *nrm, const float *xi,
+               const float *d_bsdf, const float *d_nee, float b, float *out, void *stream = nullptr) {
+        check(nasg_query_shade(ctx_, n, n_dev, x, wo, nrm, xi, d_bsdf, d_nee, b, out, stream));
+    }
+
     void set_precision(Precision p) { check(nasg_set_precision(ctx_, (int)p)); }
+    void set_train_precision(Precision p) { check(nasg_set_train_precision(ctx_, (int)p)); }
     std::vector<float> parameters(bool published = false) const {
         std::vector<float> w((size_t)nasg_n_weights(cfg_n()));
         check(nasg_get_weights(ctx_, w.data(), w.size(), published ? 1 : 0));
@@ -90,6 +97,71 @@ private:
     int cfg_n() const { return n_; }
     nasg_ctx *ctx_ = nullptr;
     int n_ = 8;
+};
+
+// ---- explicit mixtures (sphdist.hpp:33-121): NASG records and the vMF / SG baseline
+struct NasgRecord {  // NasgComponent (sphdist.hpp:33-38) as 3 x float4
+    float x_axis[3], lambda, y_axis[3], a, z_axis[3], epsilon;
+};
+struct VmfRecord {  // VmfComponent (sphdist.hpp:49-52)
+    float mu[3], lambda;
+};
+enum class Family { NASG = NASG_DIST_NASG, VMF = NASG_DIST_VMF };
+
+// mixture_pdf / vmf_mixture_pdf over n per-query mixtures of k components (device buffers)
+inline void mixture_pdf(Family f, std::int64_t n, int k, const void *comp, const float *w, const float *dir, float *pdf,
+                        void *stream = nullptr) {
+    check(nasg_dist_mixture_pdf((int)f, n, k, static_cast<const float *>(comp), w, dir, pdf, stream));
+}
+// mixture_sample / vmf_mixture_sample -> float4 (direction, mixture pdf)
+inline void mixture_sample(Family f, std::int64_t n, int k, const void *comp, const float *w, const float *xi,
+                           float *dir_pdf, void *stream = nullptr) {
+    check(nasg_dist_mixture_sample((int)f, n, k, static_cast<const float *>(comp), w, xi, dir_pdf, stream));
+}
+// nasg_grad_logpdf (8 floats per component) / vmf_grad_logpdf (4 floats per component)
+inline void grad_logpdf(Family f, std::int64_t n, int k, const void *comp, const float *w, const float *dir,
+                        float *grad, void *stream = nullptr) {
+    check(nasg_dist_grad_logpdf((int)f, n, k, static_cast<const float *>(comp), w, dir, grad, stream));
+}
+
+// SPEC run_fit: n_fits guide distributions of one family fitted to a target mixture
+struct FitResult {
+    std::vector<float> raw;  // n_fits x checkpoints x raw_dim
+    std::vector<double> kl;  // n_fits x checkpoints
+    int raw_dim = 0;
+};
+inline FitResult fit(const nasg_fit_config &cfg, int n_fits, Family target, int target_k, const void *target_comp,
+                     const float *target_w, int quad_nz = 256) {
+    FitResult r;
+    r.raw_dim = nasg_fit_raw_dim(cfg.model, cfg.n_components);
+    if (r.raw_dim < 0) throw Error(NASG_ERR_UNSUPPORTED, "unsupported fit model");
+    r.raw.resize((size_t)n_fits * cfg.checkpoints * r.raw_dim);
+    r.kl.resize((size_t)n_fits * cfg.checkpoints);
+    check(nasg_fit(&cfg, n_fits, (int)target, target_k, static_cast<const float *>(target_comp), target_w, nullptr,
+                   r.raw.data(), r.kl.data(), quad_nz));
+    return r;
+}
+
+// The SPEC tracer loop on one GPU's pixel rows (nasg_render_*).
+class Render {
+public:
+    Render(Guide &g, const nasg_render_config &cfg) { check(nasg_render_create(g.handle(), &cfg, &r_)); }
+    ~Render() { nasg_render_destroy(r_); }
+    Render(const Render &) = delete;
+    Render &operator=(const Render &) = delete;
+    nasg_render_stats iteration() {
+        nasg_render_stats st{};
+        check(nasg_render_iteration(r_, &st));
+        return st;
+    }
+    std::vector<float> image(std::int64_t pixels, bool last_frame = false) {
+        std::vector<float> rgb((size_t)pixels * 3);
+        check(nasg_render_image(r_, rgb.data(), last_frame ? 1 : 0));
+        return rgb;
+    }
+
+private:
+    nasg_render *r_ = nullptr;
 };
 
 }  // namespace nasg::gpu

@@ -11,10 +11,10 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.path.join(ROOT, "paper_2303_08064_b200", "lib")
 
 
-def build_example(tmp_path):
-    exe = str(tmp_path / "render_step")
+def build_example(tmp_path, name="render_step"):
+    exe = str(tmp_path / name)
     cmd = ["g++", "-std=c++20", "-I" + os.path.join(ROOT, "include"), "-I/usr/local/cuda/include",
-           os.path.join(ROOT, "examples", "render_step.cpp"), "-L" + LIB, "-lnasg_b200",
+           os.path.join(ROOT, "examples", name + ".cpp"), "-L" + LIB, "-lnasg_b200",
            "-L/usr/local/cuda/lib64", "-lcudart", "-Wl,-rpath," + LIB, "-o", exe]
     r = subprocess.run(cmd, capture_output=True, text=True)
     assert r.returncode == 0, r.stderr
@@ -39,6 +39,21 @@ def test_cpp_example_runs_on_gpu(tmp_path):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stderr
     assert "train: 16 steps" in r.stdout
+
+
+def test_cpp_fit_and_render_example_builds(tmp_path):
+    build_example(tmp_path, "fit_and_render")
+
+
+@pytest.mark.gpu
+def test_cpp_fit_and_render_example_runs_on_gpu(tmp_path):
+    exe = build_example(tmp_path, "fit_and_render")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    out = r.stdout
+    assert "render:" in out and "vmf:" in out and "fit:" in out
+    kl = [float(x) for x in out.split("fit: KL nasg8")[1].replace("vmf14", "").replace(",", " ").split()]
+    assert max(kl[:2]) < min(kl[2:]), out  # the anisotropic target favours NASG (PAPER Fig. 5)
 
 
 def test_mape_spec_examples():
