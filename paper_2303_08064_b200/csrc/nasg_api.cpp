@@ -245,8 +245,11 @@ void first_epoch_shuffle(uint32_t *ord, int64_t n, Pcg32 &rng) {
 
 int do_publish(nasg_ctx *c) {
     auto &P = c->pub[c->cur ^ 1];
-    // queries still reading that older snapshot on other streams finish first
+    // queries still reading that older snapshot on other streams finish first; the
+    // list then starts over (a destroyed event stays valid for waits already queued)
     for (auto &rd : P.readers) CUDA_TRY(cudaStreamWaitEvent(c->stream, rd.second, 0));
+    for (auto &rd : P.readers) cudaEventDestroy(rd.second);
+    P.readers.clear();
     CUDA_TRY(cudaMemcpyAsync(P.w, c->w, c->nw * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
     launch_pack_fp32(P.w, c->N, P.wp, nullptr, c->stream);
     c->launches++;
