@@ -882,7 +882,7 @@ int nasg_query_sample_host(nasg_ctx *c, int64_t n, const float *x, const float *
                            const float *xi, float *dir_pdf, float *cc) {
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
     if (n == 0) return NASG_OK;
-    const int64_t chunk = std::min<int64_t>(n, 1 << 20);
+    const int64_t chunk = std::min<int64_t>(n, 1 << 19);
     if (chunk > c->lane_cap) {
         for (int k = 0; k < 3; ++k) {
             if (c->lane_in[k]) cudaFree(c->lane_in[k]);
