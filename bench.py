@@ -220,9 +220,18 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     st = g.train_iteration(s, 1.0)
     g.close()
     rate = n * ws * args.train_steps / t
+    tf = rate / ws * FLOP_PER_SAMPLE / 1e12
+    pk, pk_kind = peaks()
+    # algorithmic FLOP of the whole step (fwd + dW + delta, 279,296 per sample) against the
+    # bf16 tensor peak; the step also moves 1,696 B/sample of bf16 activations through HBM
+    # twice for the split-K dW GEMM (K_dw runs at ~94 % of HBM, profiles/r1_train_bf16_ncu.md)
+    roof = {"bound": "tensor", "achieved": tf, "unit": "TFLOP/s",
+            "peak": pk["bf16_tflops"] if precision == "bf16" else 74.4,
+            "peak_kind": f"{pk_kind} bf16 burst" if precision == "bf16" else "nominal fp32 FFMA (148 SMs x 128 x 2 x 1.965 GHz)"}
+    roof["frac"] = tf / roof["peak"]
     return {"metric": f"train samples/s (config 3: 2^18 samples/step/GPU, fused fwd+KL+bwd+dW+Adam, {precision})",
             "value": rate, "unit": "samples/s", "ms_per_step": 1e3 * t / args.train_steps,
-            "achieved_tflops": rate / ws * FLOP_PER_SAMPLE / 1e12, "dtype": precision,
+            "achieved_tflops": tf, "roofline": roof, "dtype": precision,
             "gpu_launches": launches, "last_mean_loss": st.mean_loss}
 
 
