@@ -162,6 +162,18 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         // warpgroup-major tile order: a small batch (the render loop's t = 4096 is 32
         // tiles) spreads one tile per SM instead of three per SM on a third of them
         int64_t tile = (int64_t)g * gridDim.x + blockIdx.x;
+        // Small batch (no more tiles than CTAs): warpgroups 1 and 2 have no tile of
+        // their own and take lobes of warpgroup 0's KL gradient instead (the step's
+        // latency is one tile's chain; kl_grad_row_coop splits its longest link).
+        const bool coop = ntiles <= (int64_t)gridDim.x;
+        float *coop_sc = kl_scratch;                                          // [3N][128]
+        int *coop_flg = reinterpret_cast<int *>(kl_scratch + 3 * N * kKlScStride);  // [2 x 3][128]
+        auto coop_sync = [&](int k) {  // the three warpgroups of the CTA; k = 0, 1 inside the KL, 2 at entry
+            tc::fence_proxy_async_smem();  // delta4 chunks in the A tile -> visible to the tensor core
+            tc::tc_fence_before();
+            asm volatile("bar.sync %0, %1;" ::"r"(4 + k), "r"(kWGt * 128) : "memory");
+            tc::tc_fence_after();
+        };
         load_sample(tile);
         if ((warp & 3) == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
         for (; tile < ntiles; tile += stride) {
@@ -200,6 +212,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 issue(l, false);
             }
             wait_acc();
+            if (coop) coop_sync(2);  // the raw outputs are in tensor memory: helpers may read them
             // ---- KL gradient (fp32 stable forms) straight out of tensor memory:
             // header columns once, each lobe's 8 columns per pass; delta4 goes
             // to the A tile (K = NP) and the d4 block one 16-byte chunk at a time.
@@ -229,8 +242,12 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     tc::tmem_ld8_sync(my_tmem + HD + 8 * i, r);
                 };
                 auto put_lobe = [&](int i, const float (&g8)[8]) { put_chunk(HD / 8 + i, g8); };
-                st = kl_grad_row_fast<N>(valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr, put_lobe,
-                                         lossf, kl_scratch + g * (2 * N * kKlScStride) + t);
+                if (coop)
+                    st = kl_grad_row_coop<N, kWGt>(0, valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr,
+                                                   put_lobe, lossf, coop_sc + t, coop_flg + t, coop_sync);
+                else
+                    st = kl_grad_row_fast<N>(valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr,
+                                             put_lobe, lossf, kl_scratch + g * (2 * N * kKlScStride) + t);
                 if (st == kKlOk) {
 #pragma unroll
                     for (int c = 0; c < HD / 8; ++c) put_chunk(c, ghdr + 8 * c);
@@ -293,6 +310,38 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 if (l > 1) issue(l - 1, true);
             });
             tc::tc_fence_before();
+        }
+        if (coop && g > 0 && (int64_t)blockIdx.x < ntiles) {  // helper in warpgroup 0's KL
+            constexpr int HD = packed_header(N);
+            const int64_t tl = blockIdx.x;
+            load_sample(tl);
+            const bool valid = tl * 128 + t < count;
+            const uint32_t tm0 = tmem + ((uint32_t)((warp & 3) * 32) << 16);  // group 0's columns, this lane quarter
+            uint8_t *gd4 = tb.d4 + tl * (NP * 256) + blk_off(t, NP);
+            const uint32_t a4 = tc::smem_u32(smem + A_OFF) + blk_off(t, NP);  // group 0's A tile
+            auto put_lobe = [&](int i, const float (&g8)[8]) {
+                const uint32_t p0 = tc::pack_bf16x2(g8[0], g8[1]), p1 = tc::pack_bf16x2(g8[2], g8[3]),
+                               p2 = tc::pack_bf16x2(g8[4], g8[5]), p3 = tc::pack_bf16x2(g8[6], g8[7]);
+                const int c = HD / 8 + i;
+                tc::st_shared_v4(a4 + c * 128, p0, p1, p2, p3);
+                st_g16(gd4 + c * 128, p0, p1, p2, p3);
+            };
+            auto lobe = [&](int i, float (&r)[8]) {
+                __syncwarp();
+                tc::tmem_ld8_sync(tm0 + HD + 8 * i, r);
+            };
+            coop_sync(2);
+            float hdr[HD], ghdr[HD];
+            tc::tmem_ld16(tm0, hdr);
+            tc::tmem_ld_wait();
+            TrainRow srow;
+            srow.wi = make_float3(s3.x, s3.y, s3.z);
+            srow.p = s0.w;
+            srow.q_s = s1.w;
+            srow.pbsdf = s2.w;
+            float lossf = 0.f;
+            kl_grad_row_coop<N, kWGt>(g, valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr, put_lobe,
+                                      lossf, coop_sc + t, coop_flg + t, coop_sync);
         }
         if (clamped) atomicAdd(&s_clamped, clamped);
     }

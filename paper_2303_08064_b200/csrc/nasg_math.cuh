@@ -422,6 +422,78 @@ enum KlStatus : int {
     kKlDrop = 2,  // non-finite network row, unusable q, or non-finite gradient: dropped
 };
 
+// Pass 2 of the KL gradient for one lobe (guiding.cpp:118-152 with
+// nasg_grad_logpdf sphdist.cpp:200-274, fp32 stable forms): the lobe's 8 raw
+// logits r, its weighted pdf w_i pdf_i (wpi) and weight wi, 1 / q_mix and the
+// sample's scale -> the weight-logit gradient gl and the lobe's 8 packed columns.
+__device__ __forceinline__ void kl_lobe_grad(const float (&r)[8], const TrainRow &s, float wpi, float wi, float inv_q,
+                                             float scale, float &gl, float (&g8)[8], bool &finite) {
+    LobeG G;
+    decode_lobe_g(r, G);
+    const Lobe &L = G.L;
+    const float ri = wpi * inv_q;  // posterior responsibility
+    gl = scale * (ri - wi);
+    finite &= isfinite(gl);
+    // local frame of omega_i (stable fp32 forms, nasg_math.cuh header)
+    const float3 v = s.wi;
+    const float dz = dot3(v, L.z);
+    const float sg = dz >= 0.f ? 1.f : -1.f;
+    const float3 ev = make_float3(v.x - sg * L.z.x, v.y - sg * L.z.y, v.z - sg * L.z.z);
+    const float hh = 0.5f * dot3(ev, ev);
+    const float wl = dz >= 0.f ? hh : 2.f - hh, ql = dz >= 0.f ? 2.f - hh : hh;
+    const float dx = dot3(ev, L.x);
+    const float denom = fmaxf(wl * ql, 1e-12f);
+    const float t2 = fminf(fmaxf(dx * dx * rcp_fast(denom), 0.f), 1.f);
+    float g7[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d log q / d (ct, sp, cp, st, ctau, lambda, a)
+    if (fminf(wl, ql) >= 1e-6f && wpi > 0.f) {         // pole guard sphdist.cpp:205
+        const float lam = L.lambda, a = L.a;
+        float log_u = sel(wl < 1.f, log1p_fast(-0.5f * fminf(wl, 1.f)), __logf(0.5f * ql));
+        log_u = fmaxf(log_u, -27.631021f);
+        const float u = fmaxf(0.5f * ql, 1e-12f);
+        const float beta = a * t2, m = 1.f + beta;
+        const float um1 = expm1_fast(m * log_u), um = um1 + 1.f;
+        const float inv_u = rcp_fast(u), inv_den = rcp_fast(denom);
+        const float dG_dbeta = (2.f * lam * um + 1.f) * log_u;
+        const float dG_du = 2.f * lam * m * (um * inv_u) + beta * inv_u;
+        const float dt2_ddz = 2.f * dz * t2 * inv_den;
+        const float dG_ddz = 0.5f * dG_du + dG_dbeta * a * dt2_ddz;
+        const float dG_ddx = dG_dbeta * a * 2.f * dx * inv_den;
+        g7[5] = ri * (2.f * um1 - dlogk_dlambda(lam, L.one_m_emin));
+        g7[6] = ri * (t2 * dG_dbeta + 0.5f * rcp_fast(1.f + a));
+        const float ct = G.ct, st = fmaxf(G.st, 1e-9f), dst = -ct * rcp_fast(st);
+        const float cs = G.cp * v.x + G.sp * v.y;
+        float g_ct = dG_ddz * (dst * cs + v.z) + dG_ddx * (G.ctau * cs - dst * G.ctau * v.z);
+        float g_sp = dG_ddz * (st * v.y) + dG_ddx * (-G.stau * v.x + ct * G.ctau * v.y);
+        float g_cp = dG_ddz * (st * v.x) + dG_ddx * (ct * G.ctau * v.x + G.stau * v.y);
+        float g_st = dG_ddx * (-G.sp * v.x + G.cp * v.y);
+        float g_ctau = dG_ddx * (ct * G.cp * v.x + ct * G.sp * v.y - st * v.z);
+        float ps = G.cp * (G.cp * g_sp - G.sp * g_cp), pc = G.sp * (G.sp * g_cp - G.cp * g_sp);
+        g_sp = ps; g_cp = pc;
+        ps = G.ctau * (G.ctau * g_st - G.stau * g_ctau);
+        pc = G.stau * (G.stau * g_ctau - G.ctau * g_st);
+        g_st = ps; g_ctau = pc;
+        g7[0] = ri * g_ct; g7[1] = ri * g_sp; g7[2] = ri * g_cp; g7[3] = ri * g_st; g7[4] = ri * g_ctau;
+        bool ok = true;
+#pragma unroll
+        for (int k = 0; k < 7; ++k) ok &= isfinite(g7[k]);
+        if (!ok) {
+#pragma unroll
+            for (int k = 0; k < 7; ++k) g7[k] = 0.f;
+        }
+    }
+    const float inv1 = G.pn1 > 0.f ? rcp_fast(G.pn1) : 0.f, inv2 = G.pn2 > 0.f ? rcp_fast(G.pn2) : 0.f;
+    const float scl[5] = {1.f, inv1, inv1, inv2, inv2};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+        g8[k] = scale * g7[k] * scl[k] * 2.f * G.sig[k] * G.sigm[k];
+        finite &= isfinite(g8[k]);
+    }
+    g8[5] = G.lam_cl ? 0.f : scale * g7[5] * L.lambda;
+    g8[6] = G.a_cl ? 0.f : scale * g7[6] * L.a;
+    g8[7] = 0.f;
+    finite &= isfinite(g8[5]) && isfinite(g8[6]);
+}
+
 // One-sample KL gradient w.r.t. the packed raw outputs, fp32 restatement of
 // kl_loss_gradient (guiding.cpp:108-165) + nasg_grad_logpdf (sphdist.cpp:200-274)
 // in two O(N) passes over the lobes.  The raw row is never held whole:
@@ -518,78 +590,132 @@ __device__ __forceinline__ int kl_grad_row_fast(bool valid, const float (&hdr)[p
         float r[8];
         lobe(i, r);
         if (!go) continue;
-        LobeG G;
-        decode_lobe_g(r, G);
-        const Lobe &L = G.L;
         const float wpi = sc[i * kKlScStride], wi = sc[(N + i) * kKlScStride];
-        const float ri = wpi * inv_q;  // posterior responsibility
-        const float gl = scale * (ri - wi);
-        finite &= isfinite(gl);
+        float gl, g8[8];
+        kl_lobe_grad(r, s, wpi, wi, inv_q, scale, gl, g8, finite);
         sc[i * kKlScStride] = gl;
-        // local frame of omega_i (stable fp32 forms, nasg_math.cuh header)
-        const float3 v = s.wi;
-        const float dz = dot3(v, L.z);
-        const float sg = dz >= 0.f ? 1.f : -1.f;
-        const float3 ev = make_float3(v.x - sg * L.z.x, v.y - sg * L.z.y, v.z - sg * L.z.z);
-        const float hh = 0.5f * dot3(ev, ev);
-        const float wl = dz >= 0.f ? hh : 2.f - hh, ql = dz >= 0.f ? 2.f - hh : hh;
-        const float dx = dot3(ev, L.x);
-        const float denom = fmaxf(wl * ql, 1e-12f);
-        const float t2 = fminf(fmaxf(dx * dx * rcp_fast(denom), 0.f), 1.f);
-        float g7[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d log q / d (ct, sp, cp, st, ctau, lambda, a)
-        if (fminf(wl, ql) >= 1e-6f && wpi > 0.f) {         // pole guard sphdist.cpp:205
-            const float lam = L.lambda, a = L.a;
-            float log_u = sel(wl < 1.f, log1p_fast(-0.5f * fminf(wl, 1.f)), __logf(0.5f * ql));
-            log_u = fmaxf(log_u, -27.631021f);
-            const float u = fmaxf(0.5f * ql, 1e-12f);
-            const float beta = a * t2, m = 1.f + beta;
-            const float um1 = expm1_fast(m * log_u), um = um1 + 1.f;
-            const float inv_u = rcp_fast(u), inv_den = rcp_fast(denom);
-            const float dG_dbeta = (2.f * lam * um + 1.f) * log_u;
-            const float dG_du = 2.f * lam * m * (um * inv_u) + beta * inv_u;
-            const float dt2_ddz = 2.f * dz * t2 * inv_den;
-            const float dG_ddz = 0.5f * dG_du + dG_dbeta * a * dt2_ddz;
-            const float dG_ddx = dG_dbeta * a * 2.f * dx * inv_den;
-            g7[5] = ri * (2.f * um1 - dlogk_dlambda(lam, L.one_m_emin));
-            g7[6] = ri * (t2 * dG_dbeta + 0.5f * rcp_fast(1.f + a));
-            const float ct = G.ct, st = fmaxf(G.st, 1e-9f), dst = -ct * rcp_fast(st);
-            const float cs = G.cp * v.x + G.sp * v.y;
-            float g_ct = dG_ddz * (dst * cs + v.z) + dG_ddx * (G.ctau * cs - dst * G.ctau * v.z);
-            float g_sp = dG_ddz * (st * v.y) + dG_ddx * (-G.stau * v.x + ct * G.ctau * v.y);
-            float g_cp = dG_ddz * (st * v.x) + dG_ddx * (ct * G.ctau * v.x + G.stau * v.y);
-            float g_st = dG_ddx * (-G.sp * v.x + G.cp * v.y);
-            float g_ctau = dG_ddx * (ct * G.cp * v.x + ct * G.sp * v.y - st * v.z);
-            float ps = G.cp * (G.cp * g_sp - G.sp * g_cp), pc = G.sp * (G.sp * g_cp - G.cp * g_sp);
-            g_sp = ps; g_cp = pc;
-            ps = G.ctau * (G.ctau * g_st - G.stau * g_ctau);
-            pc = G.stau * (G.stau * g_ctau - G.ctau * g_st);
-            g_st = ps; g_ctau = pc;
-            g7[0] = ri * g_ct; g7[1] = ri * g_sp; g7[2] = ri * g_cp; g7[3] = ri * g_st; g7[4] = ri * g_ctau;
-            bool ok = true;
-#pragma unroll
-            for (int k = 0; k < 7; ++k) ok &= isfinite(g7[k]);
-            if (!ok) {
-#pragma unroll
-                for (int k = 0; k < 7; ++k) g7[k] = 0.f;
-            }
-        }
-        const float inv1 = G.pn1 > 0.f ? rcp_fast(G.pn1) : 0.f, inv2 = G.pn2 > 0.f ? rcp_fast(G.pn2) : 0.f;
-        const float scl[5] = {1.f, inv1, inv1, inv2, inv2};
-        float g8[8];
-#pragma unroll
-        for (int k = 0; k < 5; ++k) {
-            g8[k] = scale * g7[k] * scl[k] * 2.f * G.sig[k] * G.sigm[k];
-            finite &= isfinite(g8[k]);
-        }
-        g8[5] = G.lam_cl ? 0.f : scale * g7[5] * L.lambda;
-        g8[6] = G.a_cl ? 0.f : scale * g7[6] * L.a;
-        g8[7] = 0.f;
-        finite &= isfinite(g8[5]) && isfinite(g8[6]);
         put_lobe(i, g8);
     }
     if (!go) return status;
 #pragma unroll
     for (int i = 0; i < N; ++i) ghdr[i] = sc[i * kKlScStride];
+    if (!finite) return kKlDrop;
+    loss = -ws * (e * __logf(q_hat) + (1.f - e) * __logf(q_mix));
+    return kKlOk;
+}
+
+
+template <int N>
+__device__ __forceinline__ float wsel_f(const float (&w)[N], int i) {  // w[i] for a runtime i, in registers
+    float x = w[0];
+#pragma unroll
+    for (int j = 1; j < N; ++j) x = i == j ? w[j] : x;
+    return x;
+}
+
+// Cooperative kl_grad_row_fast for one tile shared by GW warpgroups (the bf16
+// trainer's small-batch regime, one tile per CTA): warpgroup g decodes and
+// differentiates lobes g, g + GW, ...  The row's per-lobe values cross through
+// shared memory — sc: this row's column of a [3N][kKlScStride] scratch
+// (w_i pdf_i, unused, weight-logit gradients), flg: [2 GW][kKlScStride]
+// finiteness flags — and q_mix is summed in lobe order, so every value equals
+// kl_grad_row_fast's.  sync(k), k = 0, 1, must be a barrier over all GW groups
+// (with the proxy / tensor-memory fences the caller's put_lobe needs).  Group 0
+// gets the header gradient, the status and the loss; the others return kKlZero.
+template <int N, int GW, class LobeFn, class PutLobeFn, class SyncFn>
+__device__ __forceinline__ int kl_grad_row_coop(int g, bool valid, const float (&hdr)[packed_header(N)], LobeFn lobe,
+                                                const TrainRow &s, float b, float e, float gscale,
+                                                float (&ghdr)[packed_header(N)], PutLobeFn put_lobe, float &loss,
+                                                float *sc, int *flg, SyncFn sync) {
+    constexpr int H = packed_header(N), S = kKlScStride;
+    float *wp_s = sc, *gl_s = sc + 2 * N * S;
+    loss = 0.f;
+    bool fin = true;
+#pragma unroll
+    for (int j = 0; j <= N; ++j) fin &= isfinite(hdr[j]);
+    float w[N], c, c_sig;
+    {
+        float mx = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < N; ++i) mx = fmaxf(mx, hdr[i]);
+        float sum = 0.f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) {
+            w[i] = __expf(hdr[i] - mx);
+            sum += w[i];
+        }
+        const float inv = rcp_fast(sum);
+#pragma unroll
+        for (int i = 0; i < N; ++i) w[i] *= inv;
+        float sm;
+        sigmoid_pair(hdr[N], c_sig, sm);
+        c = fminf(fmaxf(c_sig, kSelMin), kSelMax);
+    }
+    const bool live = valid && s.p != 0.f;
+#pragma unroll 1
+    for (int i = g; i < N; i += GW) {
+        float r[8];
+        lobe(i, r);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) fin &= isfinite(r[k]);
+        float wp = 0.f;
+        if (live) {
+            Lobe L;
+            decode_lobe(r, L);
+            wp = wsel_f<N>(w, i) * __expf(lobe_log_g_at(L, s.wi) - L.log_k);
+        }
+        wp_s[i * S] = wp;
+    }
+    flg[g * S] = fin;
+    sync(0);
+    float q_mix = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) q_mix += wp_s[i * S];
+#pragma unroll
+    for (int k = 0; k < GW; ++k) fin = fin && flg[k * S] != 0;
+    const float c_eff = b * c;
+    const float q_hat = c_eff * q_mix + (1.f - c_eff) * s.pbsdf;
+    int status = kKlOk;
+    if (!valid || (fin && !live)) {
+        status = kKlZero;
+    } else if (!fin) {
+        status = kKlDrop;
+    } else if (!(isfinite(q_mix) && q_mix > 0.f && isfinite(q_hat) && q_hat > 0.f) || !(s.q_s > 0.f)) {
+        loss = __int_as_float(0x7fc00000);
+        status = kKlDrop;
+    }
+    const bool go = status == kKlOk;
+    const float ws = s.p / s.q_s;
+    const float mix_scale = e * (c_eff * q_mix / q_hat) + (1.f - e);
+    const float scale = -ws * mix_scale * gscale;
+    const float inv_q = rcp_fast(q_mix);
+    bool finite = true;
+    if (g == 0) {
+        const float dsig = (c != c_sig) ? 0.f : c_sig * (1.f - c_sig);
+        const float gc = -ws * e * b * (q_mix - s.pbsdf) / q_hat * dsig * gscale;
+        finite &= isfinite(gc);
+        ghdr[N] = gc;
+#pragma unroll
+        for (int j = N + 1; j < H; ++j) ghdr[j] = 0.f;
+    }
+#pragma unroll 1
+    for (int i = g; i < N; i += GW) {
+        float r[8];
+        lobe(i, r);
+        if (!go) continue;
+        float gl, g8[8];
+        kl_lobe_grad(r, s, wp_s[i * S], wsel_f<N>(w, i), inv_q, scale, gl, g8, finite);
+        gl_s[i * S] = gl;
+        put_lobe(i, g8);
+    }
+    flg[(GW + g) * S] = finite;
+    sync(1);
+    if (g != 0) return kKlZero;
+#pragma unroll
+    for (int k = 0; k < GW; ++k) finite = finite && flg[(GW + k) * S] != 0;
+    if (!go) return status;
+#pragma unroll
+    for (int i = 0; i < N; ++i) ghdr[i] = gl_s[i * S];
     if (!finite) return kKlDrop;
     loss = -ws * (e * __logf(q_hat) + (1.f - e) * __logf(q_mix));
     return kKlOk;
