@@ -195,8 +195,20 @@ int nasg_dp_plan(const nasg_config *cfg, const int64_t *n_per_rank, int nranks, 
                  int64_t *local_count, int64_t *global_count, int32_t *reshuffle_before);
 int nasg_comm_unique_id(void *out_128_bytes);
 int nasg_comm_init(nasg_ctx *ctx, const void *unique_id_128_bytes, int rank, int nranks);
+/* Use a communicator the caller already has (an ncclComm_t, e.g. the one its
+ * own data-parallel framework created over the same ranks) instead of creating
+ * one; the context does not destroy it. */
+int nasg_attach_nccl(nasg_ctx *ctx, void *nccl_comm, int rank, int nranks);
 
 /* ---- counters (encode_clamp_count encoding.hpp:31-32) ------------------- */
+typedef struct {
+    uint64_t encode_clamps;    /* encode_clamp_count (encoding.hpp:31-32), this context */
+    uint64_t kernel_launches;  /* device kernels launched by this context */
+    int64_t adam_steps;        /* AdamState::t (net.hpp:115): applied, non-skipped updates */
+    int64_t iterations;        /* Trainer::iterations_ (train_iteration calls) */
+    int rank, nranks;          /* data-parallel position */
+} nasg_counters;
+int nasg_get_counters(nasg_ctx *ctx, nasg_counters *out);  /* synchronises the device */
 uint64_t nasg_encode_clamp_count(nasg_ctx *ctx);
 void nasg_reset_encode_clamp_count(nasg_ctx *ctx);
 /* Number of device kernel launches issued by this context since creation. */

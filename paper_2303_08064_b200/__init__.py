@@ -41,6 +41,11 @@ class _Stats(C.Structure):
                 ("skipped_updates", C.c_uint64)]
 
 
+class _Counters(C.Structure):
+    _fields_ = [("encode_clamps", C.c_uint64), ("kernel_launches", C.c_uint64), ("adam_steps", C.c_int64),
+                ("iterations", C.c_int64), ("rank", C.c_int), ("nranks", C.c_int)]
+
+
 class _RenderConfig(C.Structure):
     _fields_ = [("scene", C.c_int), ("width", C.c_int), ("height", C.c_int), ("row_begin", C.c_int),
                 ("row_end", C.c_int), ("seed", C.c_uint64), ("max_depth", C.c_int), ("rr_depth", C.c_int),
@@ -123,6 +128,8 @@ def lib():
         "nasg_adam_t": (i64, [vp]),
         "nasg_comm_unique_id": (i32, [vp]),
         "nasg_comm_init": (i32, [vp, vp, i32, i32]),
+        "nasg_attach_nccl": (i32, [vp, vp, i32, i32]),
+        "nasg_get_counters": (i32, [vp, vp]),
         "nasg_encode_clamp_count": (u64, [vp]),
         "nasg_reset_encode_clamp_count": (None, [vp]),
         "nasg_kernel_launches": (u64, [vp]),
@@ -323,6 +330,16 @@ class Guide:
     @property
     def kernel_launches(self) -> int:
         return lib().nasg_kernel_launches(self._h)
+
+    def counters(self) -> dict:
+        """nasg_get_counters: clamps, launches, Adam t, iterations, rank / nranks."""
+        c = _Counters()
+        _check(lib().nasg_get_counters(self._h, C.byref(c)))
+        return {k: getattr(c, k) for k, _ in _Counters._fields_}
+
+    def attach_nccl(self, comm_handle: int, rank: int, nranks: int):
+        """nasg_attach_nccl with an existing ncclComm_t (an integer handle)."""
+        _check(lib().nasg_attach_nccl(self._h, comm_handle, rank, nranks))
 
     @property
     def encode_clamp_count(self) -> int:

@@ -166,6 +166,7 @@ struct nasg_ctx {
     int64_t lane_cap = 0;
     // NCCL
     ncclComm_t comm = nullptr;
+    bool comm_owned = true;  // false: attached by the caller (nasg_attach_nccl), not destroyed here
     int rank = 0, nranks = 1;
     uint64_t launches = 0;
     cudaEvent_t pub_ev = nullptr;  // = pub[cur].ev
@@ -638,7 +639,7 @@ int nasg_destroy(nasg_ctx *c) {
     join_prefetch(c);
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    if (c->comm && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+    if (c->comm && c->comm_owned && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
     void *bufs[] = {c->tc_live, c->tcb.h0, c->tcb.h1, c->tcb.h2, c->tcb.h3, c->tcb.d1, c->tcb.d2, c->tcb.d3,
                     c->tcb.d4, c->tcb.tile_loss, c->tcb.tile_lc, c->tcb.tile_dr, c->tcb.partial,
                     c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->pub[0].w, c->pub[0].wp, c->pub[0].tc,
@@ -1146,7 +1147,40 @@ int nasg_comm_init(nasg_ctx *c, const void *uid, int rank, int nranks) {
     return NASG_OK;
 }
 
+int nasg_attach_nccl(nasg_ctx *c, void *comm, int rank, int nranks) {
+    if (!c || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !comm))
+        return fail(NASG_ERR_INVALID, "bad argument");
+    if (nranks == 1) return NASG_OK;
+    {
+        std::lock_guard<std::mutex> lk(g_nccl_mu);
+        if (!g_nccl.load()) return fail(NASG_ERR_NCCL, "libnccl.so.2 not loadable");
+    }
+    if (c->comm && c->comm_owned && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+    c->comm = static_cast<ncclComm_t>(comm);
+    c->comm_owned = false;
+    c->rank = rank;
+    c->nranks = nranks;
+    return NASG_OK;
+}
+
 // ---- counters / schedules ------------------------------------------------------------
+int nasg_get_counters(nasg_ctx *c, nasg_counters *out) {
+    if (!c || !out) return fail(NASG_ERR_INVALID, "null argument");
+    CUDA_TRY(cudaSetDevice(c->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    unsigned long long clamps = 0;
+    int64_t t = 0;
+    CUDA_TRY(cudaMemcpy(&clamps, c->d_clamp, sizeof(clamps), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(&t, c->d_adam_t, sizeof(t), cudaMemcpyDeviceToHost));
+    out->encode_clamps = clamps;
+    out->kernel_launches = c->launches;
+    out->adam_steps = t;
+    out->iterations = c->iterations;
+    out->rank = c->rank;
+    out->nranks = c->nranks;
+    return NASG_OK;
+}
+
 uint64_t nasg_encode_clamp_count(nasg_ctx *c) {
     if (!c) return 0;
     unsigned long long v = 0;

@@ -168,3 +168,18 @@ def test_checkpoint_roundtrip_with_oracle(orc, tmp_path):
     with pytest.raises(nasg.NasgError):
         g.load_checkpoint(p)
     g.close()
+
+
+def test_counters_track_the_trainer():
+    """nasg_get_counters: AdamState::t, Trainer::iterations_, the clamp counter."""
+    g = nasg.Guide(nasg.TrainerConfig(seed=4, sample_capacity=1024, batch_size=256))
+    c0 = g.counters()
+    assert c0["adam_steps"] == 0 and c0["iterations"] == 0 and c0["nranks"] == 1
+    s = torch.from_numpy(H.samples(np.random.default_rng(2), 1024)).cuda()
+    g.train_iteration(s, 1.0)
+    g.train_iteration(s, 0.5)
+    c1 = g.counters()
+    assert c1["iterations"] == 2 and c1["adam_steps"] == 8 == g.adam_t
+    assert c1["kernel_launches"] > c0["kernel_launches"]
+    g.attach_nccl(0, 0, 1)  # a single rank needs no communicator
+    g.close()
