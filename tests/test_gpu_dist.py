@@ -62,6 +62,19 @@ def test_dist_kernels_match_oracle(orc, kind, stress):
     assert np.all(np.abs(g - rg) <= 1e-5 * np.abs(rg) + 1e-6 * scale + 1e-30)
 
 
+def test_dist_single_query_many_lobes(orc):
+    rng = np.random.default_rng(31)
+    for kind in (nasg.DIST_NASG, nasg.DIST_VMF):
+        comp, w = records(kind, rng, 1, 32)
+        d = four(H.dirs(rng, 1))
+        xi = H.xis(rng, 1)
+        pdf = nasg.dist_mixture_pdf(kind, cu(comp), cu(w), cu(d)).cpu().numpy()
+        assert np.allclose(pdf, orc.dist_pdf(kind, comp, w, d), rtol=1e-6, atol=1e-30)
+        s = nasg.dist_mixture_sample(kind, cu(comp), cu(w), cu(xi)).cpu().numpy()
+        rs = orc.dist_sample(kind, comp, w, xi)
+        assert np.abs(s[:, :3] - rs[:, :3]).max() <= 2e-6
+
+
 def test_dist_empty_and_bad_args():
     c = torch.zeros((1, 1, 4), device="cuda")
     w = torch.ones((0, 1), device="cuda")
@@ -156,7 +169,7 @@ def test_fit_gradient_nasg_matches_kl_loss_gradient(orc):
     # (guiding.cpp:108-165) with q_sampling = p and p_bsdf = 1/(4 pi)
     rng = np.random.default_rng(12)
     tc, tw = H.vmf_records(rng, 1, 5)
-    for n_comp in (1, 8):
+    for n_comp in (1, 8, 16):
         raw = H.raw_outputs(rng, 1, n_comp=n_comp)[0]
         s4 = _target_samples(rng, nasg.DIST_VMF, tc[0], tw[0], 3000)
         s4[::50, 3] = 0.0  # p == 0 rows: zero gradient
