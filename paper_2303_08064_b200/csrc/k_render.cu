@@ -647,6 +647,7 @@ int nasg_render_destroy(nasg_render *r) {
     if (!r) return NASG_OK;
     if (r->stream) cudaStreamSynchronize(r->stream);
     if (r->tstream) cudaStreamSynchronize(r->tstream);
+    if (r->cfg.pipelined && r->ctx) ctx_set_pdl(r->ctx, true);
     for (void *p : r->bufs) cudaFree(p);
     if (r->h_acc) cudaFreeHost(r->h_acc);
     if (r->tstream) cudaStreamDestroy(r->tstream);
@@ -686,6 +687,8 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
     if (cudaMallocHost(&r->h_acc, 10 * sizeof(double)) != cudaSuccess) return fail_out(NASG_ERR_OOM);
     if (c.pipelined) {
+        // training shares the SMs with concurrent tracing: no early-started CTAs parked on them
+        ctx_set_pdl(ctx, false);
         if (cudaStreamCreateWithFlags(&r->tstream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&r->ev_train, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&r->ev_acc[0], cudaEventDisableTiming) != cudaSuccess ||

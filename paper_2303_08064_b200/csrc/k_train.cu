@@ -358,6 +358,8 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
                             const double *step_stats, double *acc, unsigned int *ticket) {
     __shared__ int s_skip;
     __shared__ float s_c1, s_c2;
+    pdl_trigger();
+    pdl_wait();  // the reduced gradient, its non-finite flag and the step statistics
     if (threadIdx.x == 0) {
         s_skip = *nonfinite != 0;
         const int64_t t = *adam_t + 1;
@@ -422,11 +424,10 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
 
 int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
                void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
-               unsigned int *ticket, cudaStream_t s) {
+               unsigned int *ticket, cudaStream_t s, bool pdl) {
     const int nw = n_weights(n_comp);
-    adam_kernel<<<(nw + 255) / 256, 256, 0, s>>>(n_comp, w, m, v, grad, lr, wp, wtp,
-                                                 static_cast<__nv_bfloat16 *>(tc_img), nonfinite, adam_t,
-                                                 step_stats, acc, ticket);
+    launch_pdl(pdl, adam_kernel, dim3((nw + 255) / 256), dim3(256), 0, s, n_comp, w, m, v, grad, lr, wp, wtp,
+               static_cast<__nv_bfloat16 *>(tc_img), nonfinite, adam_t, step_stats, acc, ticket);
     return 1;
 }
 

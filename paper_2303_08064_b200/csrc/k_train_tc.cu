@@ -99,6 +99,8 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();  // the weight image and the samples come from earlier work on the stream
 
     if (threadIdx.x == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
         tc::mbar_arrive_expect_tx(w_bar, IMG);
@@ -387,6 +389,8 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    pdl_trigger();
+    pdl_wait();  // the h / delta blocks of K_fb
     if (threadIdx.x == 0 && b1 > b0) {
         const uint32_t idesc = tc::idesc_bf16(128, FB, true, true);
         auto load = [&](int64_t blk, int s) {
@@ -446,6 +450,8 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
 // of the step (same fixed order as step_stats_kernel), saving a launch.
 __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, float *grad, int *nonfinite,
                                        int ntiles) {
+    pdl_trigger();
+    pdl_wait();  // K_dw's partials
     if (blockIdx.x == gridDim.x - 1) {
         __shared__ double sl[256], sc[256], sd[256];
         const int t = threadIdx.x;
@@ -493,7 +499,8 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
 
 int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
                   int64_t global_count, double b, double loss_blend, const Bounds &bounds, TcTrainBufs &tb,
-                  int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s) {
+                  int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s,
+                  bool pdl) {
     if (n_comp != 8 && n_comp != 4) return -1;
     const int64_t ntiles = (count + 127) / 128;
     const double gscale = 1.0 / (double)global_count;
@@ -503,22 +510,23 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
         if (n_comp == 8) {
             constexpr size_t sm = fb_smem<8>();
             cudaFuncSetAttribute(train_tc_fb_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            train_tc_fb_kernel<8><<<grid, kThreadsT, sm, s>>>(im, samples, order, count, gscale, b, loss_blend, bounds,
-                                                             tb, clamp_count);
+            launch_pdl(pdl, train_tc_fb_kernel<8>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, order, count, gscale, b,
+                       loss_blend, bounds, tb, clamp_count);
         } else {
             constexpr size_t sm = fb_smem<4>();
             cudaFuncSetAttribute(train_tc_fb_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            train_tc_fb_kernel<4><<<grid, kThreadsT, sm, s>>>(im, samples, order, count, gscale, b, loss_blend, bounds,
-                                                             tb, clamp_count);
+            launch_pdl(pdl, train_tc_fb_kernel<4>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, order, count, gscale, b,
+                       loss_blend, bounds, tb, clamp_count);
         }
         int splits = (int)(ntiles < tb.splits ? ntiles : tb.splits);
         const int bps = (int)((ntiles + splits - 1) / splits);
         splits = (int)((ntiles + bps - 1) / bps);
         const size_t sm = 2 * 65536 + 64;
         cudaFuncSetAttribute(train_tc_dw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        train_tc_dw_kernel<<<dim3(splits, 4), 128, sm, s>>>(tb, ntiles, bps, packed_width(n_comp));
+        launch_pdl(pdl, train_tc_dw_kernel, dim3(splits, 4), dim3(128), sm, s, tb, ntiles, bps, packed_width(n_comp));
         const int nw = n_weights(n_comp);
-        train_tc_reduce_kernel<<<(nw + 255) / 256 + 1, 256, 0, s>>>(tb, splits, n_comp, grad, nonfinite, (int)ntiles);
+        launch_pdl(pdl, train_tc_reduce_kernel, dim3((nw + 255) / 256 + 1), dim3(256), 0, s, tb, splits, n_comp, grad, nonfinite,
+                   (int)ntiles);
     }
     return 3;
 }

@@ -166,7 +166,8 @@ struct nasg_ctx {
     int64_t lane_cap = 0;
     // NCCL
     ncclComm_t comm = nullptr;
-    bool comm_owned = true;  // false: attached by the caller (nasg_attach_nccl), not destroyed here
+    bool comm_owned = true;
+    bool pdl = true;  // programmatic dependent launch of the training chain  // false: attached by the caller (nasg_attach_nccl), not destroyed here
     int rank = 0, nranks = 1;
     uint64_t launches = 0;
     cudaEvent_t pub_ev = nullptr;  // = pub[cur].ev
@@ -356,7 +357,7 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
     if (r) return r;
     if (count > 0 && tc) {
         const int k = train_tc_step(c->N, c->tc_live, samples, order, count, global_count, b, c->cfg.loss_blend,
-                                    c->bounds, c->tcb, c->num_sms, c->d_clamp, c->grad, c->d_nonfinite, s);
+                                    c->bounds, c->tcb, c->num_sms, c->d_clamp, c->grad, c->d_nonfinite, s, c->pdl);
         if (k < 0) return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for bf16 training");
         c->launches += k;
     } else if (count > 0) {
@@ -383,7 +384,7 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
     // skip decision, t, Adam, re-pack of every live image (the bf16 operands of
     // the next step included) and the statistics, in one launch
     train_adam(c->N, c->w, c->m, c->v, c->grad, c->cfg.learning_rate, c->wp, c->wtp, c->tc_live, c->d_nonfinite,
-               c->d_adam_t, c->d_step_stats, c->d_acc, c->d_ticket, s);
+               c->d_adam_t, c->d_step_stats, c->d_acc, c->d_ticket, s, c->pdl);
     c->launches += 1;
     CHECK_LAUNCH();
     return NASG_OK;
@@ -506,6 +507,10 @@ int ctx_prefetch_shuffle(nasg_ctx *c, int64_t n) {
         c->pf.rng_inc = rng.inc;
     });
     return NASG_OK;
+}
+
+void ctx_set_pdl(nasg_ctx *c, bool on) {
+    if (c) c->pdl = on;
 }
 
 int ctx_train_stats_async(nasg_ctx *c, double *acc, cudaStream_t s) {

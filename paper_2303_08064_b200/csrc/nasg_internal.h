@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 #include "nasg/nasg.h"
@@ -33,6 +34,8 @@ int64_t ctx_sample_capacity(const nasg_ctx *c);  // TrainerConfig::sample_capaci
 int ctx_nranks(const nasg_ctx *c);
 // start the next train_iteration's first-epoch shuffle for n rows on a host thread
 int ctx_prefetch_shuffle(nasg_ctx *c, int64_t n);
+// programmatic dependent launch of the training chain on (default) or off
+void ctx_set_pdl(nasg_ctx *c, bool on);
 // enqueue on s: copy the training statistics accumulators (5 doubles) to a
 // pinned host buffer and clear them; ctx_stats_from_acc converts after a sync
 int ctx_train_stats_async(nasg_ctx *c, double *pinned_acc5, cudaStream_t s);
@@ -78,6 +81,38 @@ struct QueryArgs {
 };
 
 #ifdef __CUDACC__
+// Programmatic dependent launch: a kernel of the training chain lets the next
+// one start its prologue (barrier init, TMEM allocation) while it still runs;
+// griddepcontrol.wait then blocks until the previous grid has completed and its
+// memory is visible, so it goes before the first read of the previous kernel's
+// output.  The dependent grid launches only once every block of this one has
+// started (and triggered), so waiting blocks can never starve it of SMs.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// pdl = false launches normally (no early start): when other streams run
+// concurrent work (the pipelined render loop), early-started CTAs waiting in
+// griddepcontrol.wait would hold SMs that work could use.
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+    if (!pdl) {
+        k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+        return cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
 __device__ __forceinline__ void load_query(const QueryArgs &a, int64_t q, float4 &x, float4 &wo, float4 &nrm) {
     if (a.packed) {
         const float *p = a.packed + q * 13;
@@ -137,7 +172,8 @@ struct TcTrainBufs {
 size_t tc_train_block_bytes(int n_comp);
 int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
                   int64_t global_count, double b, double loss_blend, const Bounds &bounds, TcTrainBufs &tb,
-                  int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s);
+                  int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s,
+                  bool pdl = true);
 int train_step_stats_n(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
                        double *step_stats, cudaStream_t s);
 
@@ -157,7 +193,7 @@ int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, 
 // set, statistics into acc, flag reset); ticket: a zeroed device counter.
 int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
                void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
-               unsigned int *ticket, cudaStream_t s);
+               unsigned int *ticket, cudaStream_t s, bool pdl = true);
 
 
 // ---- explicit mixtures and the fit (k_sphdist.cu) --------------------------
