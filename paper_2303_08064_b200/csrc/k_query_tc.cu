@@ -125,6 +125,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     __shared__ int s_clamped;
 
+    pdl_trigger();
+    pdl_wait();  // the queue (n_dev) and its rows come from the previous kernel on the stream
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = warp >> 2;        // warpgroup 0..3: named barrier g + 1
     const int m = g & 1;            // pair
@@ -400,7 +402,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 }
 
 template <int N>
-static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int num_sms, cudaStream_t s) {
+static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int num_sms, cudaStream_t s, bool pdl) {
     const int64_t ntiles = (a.n + 127) / 128;
     const int64_t supers = (ntiles + kPairs - 1) / kPairs;
     const int grid = (int)(supers < num_sms ? supers : num_sms);
@@ -412,7 +414,7 @@ static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int n
     case M: {                                                                              \
         auto k = query_tc_kernel<N, M>;                                                    \
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
-        k<<<grid, kThreads, sm, s>>>(im, a);                                               \
+        launch_pdl(pdl, k, dim3(grid), dim3(kThreads), sm, s, im, a);                       \
         break;                                                                             \
     }
         NASG_LAUNCH_TC(kModeSample)
@@ -424,10 +426,10 @@ static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int n
     return 1;
 }
 
-int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, int num_sms, cudaStream_t s) {
+int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, int num_sms, cudaStream_t s, bool pdl) {
     switch (n_comp) {
-        case 4: return query_tc_n<4>(mode, img, a, num_sms, s);
-        case 8: return query_tc_n<8>(mode, img, a, num_sms, s);
+        case 4: return query_tc_n<4>(mode, img, a, num_sms, s, pdl);
+        case 8: return query_tc_n<8>(mode, img, a, num_sms, s, pdl);
         default: return -1;
     }
 }

@@ -96,6 +96,8 @@ __device__ inline float4 f4(float3 v, float w) { return make_float4(v.x, v.y, v.
 __device__ inline float3 xyz(float4 v) { return make_float3(v.x, v.y, v.z); }
 
 __global__ void k_begin(Paths P, Frame F) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.n) return;
     const Scene &S = c_scene;
@@ -134,6 +136,8 @@ __global__ void k_begin(Paths P, Frame F) {
 // per-bounce queue reset; the previous bounce's queue length feeds the counter;
 // the list the coming bounce's survivors are appended to starts empty
 __global__ void k_queue_reset(Paths P, int next) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     P.ctr[1] += (unsigned long long)*P.qcount;
     *P.qcount = 0;
     P.nact[next] = 0;
@@ -303,6 +307,8 @@ __device__ __forceinline__ void update_path(Paths &P, const Frame &F, int bounce
 // start (warp-uniform strides, so whole warps vote together); late bounces,
 // where Russian roulette has ended most paths, touch only the survivors.
 __global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     const int *list = P.act[bounce & 1];
     const int cnt = P.nact[bounce & 1];
     const int lane = threadIdx.x & 31;
@@ -315,6 +321,8 @@ __global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
 // (one warp-aggregated atomic per warp; the list order never changes a path's
 // arithmetic, so the film stays bitwise deterministic)
 __global__ void k_update(Paths P, Frame F, int bounce) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     const int *list = P.act[bounce & 1];
     int *next = P.act[(bounce + 1) & 1];
     int *ncount = &P.nact[(bounce + 1) & 1];
@@ -347,6 +355,8 @@ __device__ inline int warp_incl_scan(int v) {
 }
 
 __global__ void k_scan_local(Paths P) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     __shared__ int wsum[32];
     const int64_t k = (int64_t)blockIdx.x * 1024 + threadIdx.x;
     const int c = (k < P.ncap && P.rpix[k] >= 0) ? P.rcnt[k] : 0;
@@ -365,6 +375,8 @@ __global__ void k_scan_local(Paths P) {
 }
 
 __global__ void k_scan_blocks(Paths P, int nblocks) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     __shared__ int wsum[32];
     const int i = threadIdx.x;
     const int c = i < nblocks ? P.bsum[i] : 0;
@@ -388,6 +400,8 @@ __global__ void k_scan_blocks(Paths P, int nblocks) {
 
 // per-vertex incident radiance by back-propagation -> TrainingSamples
 __global__ void k_records(Paths P) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= P.ncap) return;
     const int pi = P.rpix[r];
@@ -426,6 +440,8 @@ __global__ void k_records(Paths P) {
 }
 
 __global__ void k_accumulate(Paths P, float w, int first) {
+    pdl_trigger();
+    pdl_wait();  // every input comes from the previous kernel on the stream
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.n) return;
     float4 L = P.L[i];
@@ -575,6 +591,7 @@ struct nasg_render {
     std::vector<void *> bufs;
     int nranks = 1;
     int nsm = 148;
+    bool pdl = true;  // programmatic dependent launch of the trace chain (serial loop only)
     double *h_acc = nullptr;   // pinned 2 x 5: training statistics (lazy_train_stats / pipelined)
     bool acc_pending[2] = {false, false};
     // pipelined: trace i+1 overlaps training i (its own stream); two sample buffers
@@ -648,6 +665,7 @@ int nasg_render_destroy(nasg_render *r) {
     if (r->stream) cudaStreamSynchronize(r->stream);
     if (r->tstream) cudaStreamSynchronize(r->tstream);
     if (r->cfg.pipelined && r->ctx) ctx_set_pdl(r->ctx, true);
+    if (r->ctx) ctx_set_query_pdl(r->ctx, false);
     for (void *p : r->bufs) cudaFree(p);
     if (r->h_acc) cudaFreeHost(r->h_acc);
     if (r->tstream) cudaStreamDestroy(r->tstream);
@@ -686,9 +704,11 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     };
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
     if (cudaMallocHost(&r->h_acc, 10 * sizeof(double)) != cudaSuccess) return fail_out(NASG_ERR_OOM);
+    ctx_set_query_pdl(ctx, !c.pipelined);
     if (c.pipelined) {
         // training shares the SMs with concurrent tracing: no early-started CTAs parked on them
         ctx_set_pdl(ctx, false);
+        r->pdl = false;
         if (cudaStreamCreateWithFlags(&r->tstream, cudaStreamNonBlocking) != cudaSuccess ||
             cudaEventCreateWithFlags(&r->ev_train, cudaEventDisableTiming) != cudaSuccess ||
             cudaEventCreateWithFlags(&r->ev_acc[0], cudaEventDisableTiming) != cudaSuccess ||
@@ -765,13 +785,13 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
         if (rc != NASG_OK) return rc;
     }
     const unsigned g = grid_of(P.n);
-    k_begin<<<g, kBlock, 0, s>>>(P, F);
+    launch_pdl(r->pdl, k_begin, dim3(g), dim3(kBlock), 0, s, P, F);
     r->launches++;
     const bool guided = b > 0.0;
     const unsigned gb = std::min<unsigned>(g, (unsigned)r->nsm * 8u);  // list-walking bounce kernels
     for (int bounce = 0; bounce < c.max_depth; ++bounce) {
-        k_queue_reset<<<1, 1, 0, s>>>(P, (bounce + 1) & 1);
-        k_isect<<<gb, kBlock, 0, s>>>(P, F, bounce, guided ? 1 : 0);
+        launch_pdl(r->pdl, k_queue_reset, dim3(1), dim3(1), 0, s, P, (bounce + 1) & 1);
+        launch_pdl(r->pdl, k_isect, dim3(gb), dim3(kBlock), 0, s, P, F, bounce, guided ? 1 : 0);
         r->launches += 2;
         if (guided) {
             const int rc = nasg_query_shade(r->ctx, P.n, P.qcount, (const float *)P.qx, (const float *)P.qwo,
@@ -779,18 +799,18 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
                                             (const float *)P.qdn, (float)b, (float *)P.qout, s);
             if (rc != NASG_OK) return rc;
         }
-        k_update<<<gb, kBlock, 0, s>>>(P, F, bounce);
+        launch_pdl(r->pdl, k_update, dim3(gb), dim3(kBlock), 0, s, P, F, bounce);
         r->launches++;
     }
-    k_queue_reset<<<1, 1, 0, s>>>(P, c.max_depth & 1);
+    launch_pdl(r->pdl, k_queue_reset, dim3(1), dim3(1), 0, s, P, c.max_depth & 1);
     r->launches++;
     if (c.collect) {
         // pipelined: the training two iterations back read this sample buffer
         if (r->ev_train) RCUDA(cudaStreamWaitEvent(s, r->ev_train, 0));
         const int nb = (int)((P.ncap + 1023) / 1024);
-        k_scan_local<<<nb, 1024, 0, s>>>(P);
-        k_scan_blocks<<<1, 1024, 0, s>>>(P, nb);
-        k_records<<<grid_of(P.ncap), kBlock, 0, s>>>(P);
+        launch_pdl(r->pdl, k_scan_local, dim3(nb), dim3(1024), 0, s, P);
+        launch_pdl(r->pdl, k_scan_blocks, dim3(1), dim3(1024), 0, s, P, nb);
+        launch_pdl(r->pdl, k_records, dim3(grid_of(P.ncap)), dim3(kBlock), 0, s, P);
         r->launches += 3;
     }
     RCUDA(cudaGetLastError());
@@ -802,7 +822,7 @@ int launch_accumulate(nasg_render *r, int64_t iter) {
     const nasg_render_config &c = r->cfg;
     const int64_t mb = (int64_t)c.schedule_m * c.schedule_b;
     const double w = c.ramp ? (double)std::min<int64_t>(iter + 1, mb) / (double)mb : 1.0;
-    k_accumulate<<<grid_of(r->P.n), kBlock, 0, r->stream>>>(r->P, (float)w, iter == 0 ? 1 : 0);
+    launch_pdl(r->pdl, k_accumulate, dim3(grid_of(r->P.n)), dim3(kBlock), 0, r->stream, r->P, (float)w, iter == 0 ? 1 : 0);
     r->launches++;
     r->wsum += w;
     RCUDA(cudaGetLastError());

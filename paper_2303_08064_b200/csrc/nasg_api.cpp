@@ -167,7 +167,8 @@ struct nasg_ctx {
     // NCCL
     ncclComm_t comm = nullptr;
     bool comm_owned = true;
-    bool pdl = true;  // programmatic dependent launch of the training chain  // false: attached by the caller (nasg_attach_nccl), not destroyed here
+    bool pdl = true;  // programmatic dependent launch of the training chain
+    bool query_pdl = false;  // ... and of the query kernels (serial render loop)  // false: attached by the caller (nasg_attach_nccl), not destroyed here
     int rank = 0, nranks = 1;
     uint64_t launches = 0;
     cudaEvent_t pub_ev = nullptr;  // = pub[cur].ev
@@ -338,7 +339,7 @@ int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
     int r;
     if (c->precision == NASG_MLP_BF16) {
         if (!c->tc_pub) return fail(NASG_ERR_UNSUPPORTED, "bf16 tensor-core path not available for this N");
-        r = query_tc(c->N, mode, c->tc_pub, a, c->num_sms, s);
+        r = query_tc(c->N, mode, c->tc_pub, a, c->num_sms, s, c->query_pdl);
     } else {
         r = query_fp32(c->N, mode, c->wp_pub, a, c->num_sms, s);
     }
@@ -511,6 +512,10 @@ int ctx_prefetch_shuffle(nasg_ctx *c, int64_t n) {
 
 void ctx_set_pdl(nasg_ctx *c, bool on) {
     if (c) c->pdl = on;
+}
+
+void ctx_set_query_pdl(nasg_ctx *c, bool on) {
+    if (c) c->query_pdl = on;
 }
 
 int ctx_train_stats_async(nasg_ctx *c, double *acc, cudaStream_t s) {

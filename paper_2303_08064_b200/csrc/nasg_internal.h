@@ -36,6 +36,8 @@ int ctx_nranks(const nasg_ctx *c);
 int ctx_prefetch_shuffle(nasg_ctx *c, int64_t n);
 // programmatic dependent launch of the training chain on (default) or off
 void ctx_set_pdl(nasg_ctx *c, bool on);
+// programmatic dependent launch of the query kernels (set by the serial render loop)
+void ctx_set_query_pdl(nasg_ctx *c, bool on);
 // enqueue on s: copy the training statistics accumulators (5 doubles) to a
 // pinned host buffer and clear them; ctx_stats_from_acc converts after a sync
 int ctx_train_stats_async(nasg_ctx *c, double *pinned_acc5, cudaStream_t s);
@@ -137,7 +139,7 @@ __device__ __forceinline__ float4 load_xi(const QueryArgs &a, int64_t q) {
 int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, int num_sms,
                cudaStream_t s);
 int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, int num_sms,
-             cudaStream_t s);
+             cudaStream_t s, bool pdl = false);
 bool tc_supported(int n_comp);
 
 int decode_raw(int n_comp, bool sample, bool fast, int64_t n, const float *raw, const float4 *xi,
