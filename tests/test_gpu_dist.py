@@ -287,3 +287,34 @@ def test_expressiveness_nasg_vs_vmf():
     assert np.all(band_n < band_v), (band_n, band_v)
     iso_n, iso_v = np.median(res["isotropic"]["nasg8"]["kl_final"]), np.median(res["isotropic"]["vmf14"]["kl_final"])
     assert max(iso_n, iso_v) < 1e-3 or max(iso_n, iso_v) / min(iso_n, iso_v) <= 2.0, (iso_n, iso_v)
+
+
+def test_nasg_normalizer_monte_carlo():
+    # SPEC.md:542 (acceptance 1): for random components (lambda log-uniform in
+    # [1e-2, 1e2], a log-uniform up to 1e3) a Monte Carlo estimate of the
+    # integral of G/K over the sphere, drawn through the vMF sampler kernel (a
+    # defensive mixture: a vMF around the lobe axis and a near-uniform one),
+    # is 1 within 3 standard errors and 1 % for >= 99 % of components.
+    rng = np.random.default_rng(77)
+    nc, m = 200, 20000
+    f = H.frames(rng, nc)
+    lam = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), nc))
+    a = np.exp(rng.uniform(np.log(1e-2), np.log(1e3), nc))
+    rec = np.zeros((nc, 1, 12), np.float32)
+    rec[:, 0, 0:3], rec[:, 0, 3], rec[:, 0, 4:7], rec[:, 0, 7], rec[:, 0, 8:11] = f[:, 0], lam, f[:, 1], a, f[:, 2]
+    prop = np.zeros((nc, 2, 4), np.float32)
+    prop[:, 0, 0:3], prop[:, 0, 3] = f[:, 2], np.maximum(lam / 2.0, 1e-3)  # around the axis, wider than the lobe
+    prop[:, 1, 0:3], prop[:, 1, 3] = f[:, 2], 1e-3                         # ~uniform
+    pw = np.full((nc, 2), 0.5, np.float32)
+    rep = lambda x: torch.from_numpy(np.ascontiguousarray(x)).cuda().repeat_interleave(m, 0)
+    xi = cu(H.xis(rng, nc * m))
+    s = nasg.dist_mixture_sample(nasg.DIST_VMF, rep(prop), rep(pw), xi)
+    q = s[:, 3].double()
+    d = s.clone()
+    d[:, 3] = 0
+    p = nasg.dist_mixture_pdf(nasg.DIST_NASG, rep(rec), cu(np.ones((nc * m, 1), np.float32)), d).double()
+    ratio = (p / q).view(nc, m)
+    est = ratio.mean(1).cpu().numpy()
+    se = (ratio.std(1) / np.sqrt(m)).cpu().numpy()
+    ok = np.abs(est - 1.0) <= 3 * se + 0.01
+    assert ok.mean() >= 0.99, (ok.mean(), est[~ok][:5], se[~ok][:5])
