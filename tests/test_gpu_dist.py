@@ -294,9 +294,9 @@ def test_nasg_normalizer_monte_carlo():
     # [1e-2, 1e2], a log-uniform up to 1e3) a Monte Carlo estimate of the
     # integral of G/K over the sphere, drawn through the vMF sampler kernel (a
     # defensive mixture: a vMF around the lobe axis and a near-uniform one),
-    # is 1 within 3 standard errors and 1 % for >= 99 % of components.
+    # is 1 within 3 standard errors and 1 % for >= 99 % of 1000 components.
     rng = np.random.default_rng(77)
-    nc, m = 200, 20000
+    nc, m = 1000, 20000
     f = H.frames(rng, nc)
     lam = np.exp(rng.uniform(np.log(1e-2), np.log(1e2), nc))
     a = np.exp(rng.uniform(np.log(1e-2), np.log(1e3), nc))
@@ -318,3 +318,69 @@ def test_nasg_normalizer_monte_carlo():
     se = (ratio.std(1) / np.sqrt(m)).cpu().numpy()
     ok = np.abs(est - 1.0) <= 3 * se + 0.01
     assert ok.mean() >= 0.99, (ok.mean(), est[~ok][:5], se[~ok][:5])
+
+
+def _bin_masses(kind, comp, w, nz, nphi, sub=8):
+    """(n_mix, nz*nphi) bin masses of equal-area (z, phi) bins by a sub x sub midpoint rule of the GPU pdf."""
+    fz, fp = nz * sub, nphi * sub
+    z = -1.0 + (np.arange(fz) + 0.5) * 2.0 / fz
+    ph = (np.arange(fp) + 0.5) * 2 * np.pi / fp
+    Z, P = np.meshgrid(z, ph, indexing="ij")
+    r = np.sqrt(1 - Z * Z)
+    d = torch.from_numpy(np.stack([r * np.cos(P), r * np.sin(P), Z, 0 * Z], -1).reshape(-1, 4).astype(np.float32)).cuda()
+    m = d.shape[0]
+    out = []
+    for j in range(comp.shape[0]):
+        pdf = nasg.dist_mixture_pdf(kind, cu(comp[j:j + 1]).repeat(m, 1, 1), cu(w[j:j + 1]).repeat(m, 1), d)
+        out.append((pdf.double() * 4 * np.pi / m).view(nz, sub, nphi, sub).sum((1, 3)).reshape(-1).cpu().numpy())
+    return np.stack(out)
+
+
+def test_sampler_chi_square_100_components():
+    # SPEC.md:543 (acceptance 2): 10^5 samples of each of 100 random NASG lobes
+    # (epsilon = 0) binned on the 32 x 64 equal-area grid pass a chi-square test
+    # against quadrature bin masses at significance 1e-3 for >= 95 of them
+    from scipy import stats
+    rng = np.random.default_rng(123)
+    nc, ns, nz, nphi = 100, 100000, 32, 64
+    comp, w = H.nasg_records(rng, nc, 1, eps_frac=0.0)
+    comp[:, 0, 3] = np.exp(rng.uniform(np.log(0.3), np.log(30.0), nc))  # lobes the 32 x 64 bins resolve
+    comp[:, 0, 7] = np.exp(rng.uniform(np.log(1e-2), np.log(30.0), nc))
+    s = nasg.dist_mixture_sample(nasg.DIST_NASG, cu(comp).repeat_interleave(ns, 0), cu(w).repeat_interleave(ns, 0),
+                                 cu(H.xis(rng, nc * ns))).cpu().numpy().reshape(nc, ns, 4)
+    mass = _bin_masses(nasg.DIST_NASG, comp, w, nz, nphi)
+    passed = 0
+    for j in range(nc):
+        counts = np.bincount(_grid_bins(s[j, :, :3].astype(np.float64), nz, nphi), minlength=nz * nphi)
+        exp = mass[j] / mass[j].sum() * ns
+        keep = exp > 5
+        rest = counts[~keep].sum(), exp[~keep].sum()  # pooled tail bin
+        obs = np.append(counts[keep], rest[0])
+        ex = np.append(exp[keep], rest[1])
+        if ex[-1] < 5:
+            obs, ex = obs[:-1], ex[:-1]
+        chi2 = ((obs - ex) ** 2 / ex).sum()
+        passed += stats.chi2.sf(chi2, len(obs) - 1) > 1e-3
+    assert passed >= 95, passed
+
+
+def test_sg_reduction_sampler_two_sample():
+    # SPEC.md:544 (acceptance 3): with a = 0, eps = 0 the NASG sampler and the
+    # vMF sampler draw from the same distribution (two-sample chi-square, 16 x 32 bins)
+    from scipy import stats
+    rng = np.random.default_rng(5)
+    ns = 1 << 19
+    f = H.frames(rng, 1)
+    for lam in (0.5, 5.0, 40.0):
+        rec = np.zeros((1, 1, 12), np.float32)
+        rec[0, 0, 0:3], rec[0, 0, 3], rec[0, 0, 4:7], rec[0, 0, 8:11] = f[0, 0], lam, f[0, 1], f[0, 2]
+        vm = np.zeros((1, 1, 4), np.float32)
+        vm[0, 0, 0:3], vm[0, 0, 3] = f[0, 2], lam
+        one = cu(np.ones((ns, 1), np.float32))
+        a = nasg.dist_mixture_sample(nasg.DIST_NASG, cu(rec).repeat(ns, 1, 1), one, cu(H.xis(rng, ns))).cpu().numpy()
+        b = nasg.dist_mixture_sample(nasg.DIST_VMF, cu(vm).repeat(ns, 1, 1), one, cu(H.xis(rng, ns))).cpu().numpy()
+        ca = np.bincount(_grid_bins(a[:, :3].astype(np.float64), 16, 32), minlength=512)
+        cb = np.bincount(_grid_bins(b[:, :3].astype(np.float64), 16, 32), minlength=512)
+        keep = (ca + cb) > 10
+        chi2 = (((ca - cb)[keep] ** 2) / (ca + cb)[keep]).sum()
+        assert stats.chi2.sf(chi2, keep.sum() - 1) > 1e-3, (lam, chi2, keep.sum())
