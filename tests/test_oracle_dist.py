@@ -177,3 +177,34 @@ def test_nasg_grad_logpdf_central_differences(kind, request):
         err = np.abs(g - fd) / (np.abs(fd).max() + 1e-12)
         bad += err.max() > 1e-4
     assert bad == 0, bad
+
+
+@pytest.mark.parametrize("kind", ["orc", "ref"])
+def test_kl_loss_gradient_central_differences(kind, request):
+    # SPEC.md:545 (acceptance 4c): kl_loss_gradient end to end through decode
+    # (guiding.cpp:108-165) against central differences of loss_surrogate
+    # (:167-176), relative error < 1e-4.  Raw outputs and the steps are multiples
+    # of 2^-11, so raw +- h is exact in the float raw vector.
+    o = request.getfixturevalue(kind)
+    rng = np.random.default_rng(29)
+    h = 2.0 ** -10
+
+    def cd(raw, smp, b, step):  # central differences of loss_surrogate, all 65 coordinates
+        pert = np.repeat(raw, 130, 0)
+        for j in range(65):
+            pert[2 * j, j] += step
+            pert[2 * j + 1, j] -= step
+        _, _, loss = o.kl_grad(pert.astype(np.float32), np.repeat(smp, 130, 0), b)
+        return (loss[0::2] - loss[1::2]) / (2 * step)
+
+    for b in (0.5, 1.0):
+        raws = np.round(rng.normal(0.0, 0.7, (20, 65)) / (h / 2)) * (h / 2)
+        s = H.samples(rng, 20, zero_p_frac=0.0)
+        for r in range(20):
+            g, ok, _ = o.kl_grad(raws[r:r + 1].astype(np.float32), s[r:r + 1], b)
+            if not ok[0]:
+                continue
+            # Richardson extrapolation of the h and h/2 differences: O(h^4) truncation
+            fd = (4.0 * cd(raws[r:r + 1], s[r:r + 1], b, h / 2) - cd(raws[r:r + 1], s[r:r + 1], b, h)) / 3.0
+            scale = np.abs(fd).max()
+            assert np.all(np.abs(g[0] - fd) <= 1e-4 * scale + 1e-12), (r, np.abs(g[0] - fd).max() / scale)
