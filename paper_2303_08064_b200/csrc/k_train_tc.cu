@@ -13,9 +13,11 @@
 //   K_dw (train_tc_dw_kernel)  dW_l = h_l^T delta_{l+1} (net.hpp:102) as a
 //        split-K UMMA GEMM over 128-row blocks: both operands MN-major, TMA
 //        bulk copies into a 2-stage smem ring, fp32 accumulation in TMEM,
-//        per-split partials reduced in fixed order (deterministic).
-//   then the fp32 tail shared with the fp32 path: step stats, skip decision,
-//   Adam (k_train.cu), and a re-pack of the live bf16 image.
+//        per-split partials reduced in fixed order (deterministic) by
+//        train_tc_reduce_kernel, whose extra block sums the step statistics.
+//   then the one-launch optimizer tail shared with the fp32 path (k_train.cu
+//   adam_kernel: skip decision, t, Adam, re-pack of every live image).  The
+//   four launches of a step chain by programmatic dependent launch.
 #include <cuda_bf16.h>
 
 #include "nasg_internal.h"
