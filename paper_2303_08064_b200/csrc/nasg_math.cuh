@@ -102,6 +102,16 @@ __device__ __forceinline__ float sel(bool c, float a, float b) {
     return r;
 }
 
+// log u for u = 1 - w/2 = q/2 (w = 1 - dz, q = 1 + dz from lobe_local): the
+// log1p series below w = 1/2 (u near 1, where log(q/2) would cancel), MUFU.LG2
+// of q/2 above it (u <= 3/4, relative error ~1e-7): one logarithm per call.
+__device__ __forceinline__ float log_u_of(float w, float q) {
+    const float x = -0.5f * fminf(w, 0.5f);
+    const float sx = x * rcp_fast(2.f + x), s2 = sx * sx;
+    const float ser = 2.f * sx * fmaf(s2, fmaf(s2, fmaf(s2, 1.f / 7.f, 1.f / 5.f), 1.f / 3.f), 1.f);
+    return sel(w < 0.5f, ser, __logf(0.5f * q));
+}
+
 // log1p(x), x > -1: 2 atanh(x / (2 + x)) series for |x| < 1/4 (s^2 <= 0.0204,
 // so the dropped s^8/9 term is < 2e-8 relative), log(1 + x) from MUFU.LG2
 // otherwise (|log| > 0.22 there).
@@ -169,7 +179,7 @@ __device__ __forceinline__ void decode_lobe(const float r[7], Lobe &L) {
 
 // log G at v (sphdist.cpp:133-140), from local w = 1 - dz, q = 1 + dz, t2.
 __device__ __forceinline__ float lobe_log_g(const Lobe &L, float w, float q, float t2) {
-    float log_u = sel(w < 1.f, log1p_fast(-0.5f * fminf(w, 1.f)), __logf(0.5f * q));
+    float log_u = log_u_of(w, q);
     log_u = fmaxf(log_u, -27.631021f);  // u >= 1e-12
     const float beta = L.a * t2;
     const float lg = 2.f * L.lambda * expm1_fast((1.f + beta) * log_u) + beta * log_u;
@@ -447,7 +457,7 @@ __device__ __forceinline__ void kl_lobe_grad(const float (&r)[8], const TrainRow
     float g7[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // d log q / d (ct, sp, cp, st, ctau, lambda, a)
     if (fminf(wl, ql) >= 1e-6f && wpi > 0.f) {         // pole guard sphdist.cpp:205
         const float lam = L.lambda, a = L.a;
-        float log_u = sel(wl < 1.f, log1p_fast(-0.5f * fminf(wl, 1.f)), __logf(0.5f * ql));
+        float log_u = log_u_of(wl, ql);
         log_u = fmaxf(log_u, -27.631021f);
         const float u = fmaxf(0.5f * ql, 1e-12f);
         const float beta = a * t2, m = 1.f + beta;
