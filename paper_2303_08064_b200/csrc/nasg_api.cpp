@@ -145,6 +145,7 @@ struct nasg_ctx {
     int64_t *d_adam_t = nullptr;
     int *d_nonfinite = nullptr;
     unsigned int *d_ticket = nullptr;  // last-block ticket of the fused Adam kernel
+    cudaEvent_t xev = nullptr;  // reusable: orders the context stream after a caller stream
     double *d_step_stats = nullptr, *d_acc = nullptr;
     TrainScratch sc{};
     uint32_t *d_order = nullptr, *h_order[2] = {nullptr, nullptr};
@@ -603,6 +604,8 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     } while (0)
     if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
         return cleanup_fail(fail(NASG_ERR_CUDA, "stream create failed"));
+    if (cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming) != cudaSuccess)
+        return cleanup_fail(fail(NASG_ERR_CUDA, "event create failed"));
     for (auto &l : c->lanes)
         if (cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking) != cudaSuccess)
             return cleanup_fail(fail(NASG_ERR_CUDA, "stream create failed"));
@@ -667,6 +670,7 @@ int nasg_destroy(nasg_ctx *c) {
     for (auto l : c->lanes)
         if (l) cudaStreamDestroy(l);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->xev) cudaEventDestroy(c->xev);
     for (auto &P : c->pub) {
         if (P.ev) cudaEventDestroy(P.ev);
         for (auto &rd : P.readers) cudaEventDestroy(rd.second);
@@ -935,16 +939,22 @@ int nasg_query_sample_host(nasg_ctx *c, int64_t n, const float *x, const float *
 int nasg_train_step(nasg_ctx *c, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
                     int64_t global_count, double b, void *stream) {
     if (!c || count < 0 || global_count <= 0 || (count > 0 && !samples)) return fail(NASG_ERR_INVALID, "bad argument");
-    return train_step_impl(c, samples, order, count, global_count, b, pick(c, stream));
+    cudaStream_t s = pick(c, stream);
+    int r = train_step_impl(c, samples, order, count, global_count, b, s);
+    if (r) return r;
+    if (s != c->stream) {  // nasg_train_stats_take reads the accumulators on the context stream
+        CUDA_TRY(cudaEventRecord(c->xev, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->xev, 0));
+    }
+    return NASG_OK;
 }
 
 int nasg_train_stats_take(nasg_ctx *c, nasg_train_stats *st) {
     if (!c || !st) return fail(NASG_ERR_INVALID, "null argument");
-    double acc[5];
-    CUDA_TRY(cudaDeviceSynchronize());
+    double acc[5];  // the training steps that fed the accumulators are ordered before c->stream
     CUDA_TRY(cudaMemcpyAsync(acc, c->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
     CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, sizeof(acc), c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
     ctx_stats_from_acc(acc, st);
     return NASG_OK;
 }
@@ -1009,11 +1019,8 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     if (!c || n < 0 || (n > 0 && !samples)) return fail(NASG_ERR_INVALID, "bad argument");
     cudaStream_t s = pick(c, stream);
     if (s != c->stream) {  // the context's own stream carries publish; order it after s
-        cudaEvent_t ev;
-        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventRecord(ev, s));
-        CUDA_TRY(cudaStreamWaitEvent(c->stream, ev, 0));
-        cudaEventDestroy(ev);
+        CUDA_TRY(cudaEventRecord(c->xev, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->xev, 0));
     }
     if (n == 0 && c->nranks == 1) {  // empty buffer: no-op + publish (:198-202)
         ++c->iterations;
@@ -1101,11 +1108,8 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     }
     ++c->iterations;
     if (s != c->stream) {
-        cudaEvent_t ev;
-        CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        CUDA_TRY(cudaEventRecord(ev, s));
-        CUDA_TRY(cudaStreamWaitEvent(c->stream, ev, 0));
-        cudaEventDestroy(ev);
+        CUDA_TRY(cudaEventRecord(c->xev, s));
+        CUDA_TRY(cudaStreamWaitEvent(c->stream, c->xev, 0));
     }
     r = do_publish(c);
     if (r) return r;
