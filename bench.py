@@ -225,25 +225,31 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     trained = [torch.cuda.Event(), torch.cuda.Event()]
     e2e_steps = max(args.train_steps, 20)
-    barrier(ws)
-    t0 = time.perf_counter()
-    with torch.cuda.stream(cs):
-        bufs[0].copy_(hs, non_blocking=True)
-        copied[0].record(cs)
-    for k in range(e2e_steps):
-        b = k % 2
-        if k + 1 < e2e_steps:
-            with torch.cuda.stream(cs):
-                if k >= 1:
-                    cs.wait_event(trained[1 - b])  # step k - 1 is done with that buffer
-                bufs[1 - b].copy_(hs, non_blocking=True)
-                copied[1 - b].record(cs)
-        cur.wait_event(copied[b])
-        g.train_iteration(bufs[b], 1.0, stats=True)  # TrainStats read back every step
-        trained[b].record(cur)
-    torch.cuda.synchronize()
-    te = max_over_ranks(time.perf_counter() - t0, ws)
-    e2e = {"value": n * ws * e2e_steps / te, "unit": "samples/s", "steps": e2e_steps, "h2d_bytes_per_step": n * 64 * ws,
+
+    def e2e_trial():
+        barrier(ws)
+        t0 = time.perf_counter()
+        with torch.cuda.stream(cs):
+            bufs[0].copy_(hs, non_blocking=True)
+            copied[0].record(cs)
+        for k in range(e2e_steps):
+            b = k % 2
+            if k + 1 < e2e_steps:
+                with torch.cuda.stream(cs):
+                    if k >= 1:
+                        cs.wait_event(trained[1 - b])  # step k - 1 is done with that buffer
+                    bufs[1 - b].copy_(hs, non_blocking=True)
+                    copied[1 - b].record(cs)
+            cur.wait_event(copied[b])
+            g.train_iteration(bufs[b], 1.0, stats=True)  # TrainStats read back every step
+            trained[b].record(cur)
+        torch.cuda.synchronize()
+        return max_over_ranks(time.perf_counter() - t0, ws)
+
+    trials = sorted(e2e_trial() for _ in range(3))
+    te = trials[1]  # the median of three trials (the host-driven loop varies run to run)
+    e2e = {"value": n * ws * e2e_steps / te, "unit": "samples/s", "steps": e2e_steps, "trials": 3,
+           "trial_values": [n * ws * e2e_steps / x for x in trials], "h2d_bytes_per_step": n * 64 * ws,
            "d2h_bytes_per_step": 40 * ws, "api": "nasg_train_iteration (samples from pinned host memory, stats read back)"}
     t = max_over_ranks(sum(times), ws)
     st = g.train_iteration(s, 1.0)

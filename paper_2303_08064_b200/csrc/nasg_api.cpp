@@ -146,6 +146,7 @@ struct nasg_ctx {
     int *d_nonfinite = nullptr;
     unsigned int *d_ticket = nullptr;  // last-block ticket of the fused Adam kernel
     cudaEvent_t xev = nullptr;  // reusable: orders the context stream after a caller stream
+    double *h_acc = nullptr;    // pinned: TrainStats read-back (a D2H copy engine, never behind an upload)
     double *d_step_stats = nullptr, *d_acc = nullptr;
     TrainScratch sc{};
     uint32_t *d_order = nullptr, *h_order[2] = {nullptr, nullptr};
@@ -606,6 +607,8 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
         return cleanup_fail(fail(NASG_ERR_CUDA, "stream create failed"));
     if (cudaEventCreateWithFlags(&c->xev, cudaEventDisableTiming) != cudaSuccess)
         return cleanup_fail(fail(NASG_ERR_CUDA, "event create failed"));
+    if (cudaMallocHost(&c->h_acc, 5 * sizeof(double)) != cudaSuccess)
+        return cleanup_fail(fail(NASG_ERR_OOM, "cudaMallocHost failed"));
     for (auto &l : c->lanes)
         if (cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking) != cudaSuccess)
             return cleanup_fail(fail(NASG_ERR_CUDA, "stream create failed"));
@@ -671,6 +674,7 @@ int nasg_destroy(nasg_ctx *c) {
         if (l) cudaStreamDestroy(l);
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->xev) cudaEventDestroy(c->xev);
+    if (c->h_acc) cudaFreeHost(c->h_acc);
     for (auto &P : c->pub) {
         if (P.ev) cudaEventDestroy(P.ev);
         for (auto &rd : P.readers) cudaEventDestroy(rd.second);
@@ -951,10 +955,11 @@ int nasg_train_step(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
 
 int nasg_train_stats_take(nasg_ctx *c, nasg_train_stats *st) {
     if (!c || !st) return fail(NASG_ERR_INVALID, "null argument");
-    double acc[5];  // the training steps that fed the accumulators are ordered before c->stream
-    CUDA_TRY(cudaMemcpyAsync(acc, c->d_acc, sizeof(acc), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, sizeof(acc), c->stream));
+    // the training steps that fed the accumulators are ordered before c->stream
+    CUDA_TRY(cudaMemcpyAsync(c->h_acc, c->d_acc, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream));
     CUDA_TRY(cudaStreamSynchronize(c->stream));
+    const double *acc = c->h_acc;
     ctx_stats_from_acc(acc, st);
     return NASG_OK;
 }
