@@ -593,6 +593,7 @@ struct nasg_render {
     int nsm = 148;
     bool pdl = true;  // programmatic dependent launch of the trace chain (serial loop only)
     double *h_acc = nullptr;   // pinned 2 x 5: training statistics (lazy_train_stats / pipelined)
+    unsigned long long *h_ctr = nullptr;  // pinned: the iteration's counters
     bool acc_pending[2] = {false, false};
     // pipelined: trace i+1 overlaps training i (its own stream); two sample buffers
     nasg_train_sample *samples_buf[2] = {nullptr, nullptr};
@@ -668,6 +669,7 @@ int nasg_render_destroy(nasg_render *r) {
     if (r->ctx) ctx_set_query_pdl(r->ctx, false);
     for (void *p : r->bufs) cudaFree(p);
     if (r->h_acc) cudaFreeHost(r->h_acc);
+    if (r->h_ctr) cudaFreeHost(r->h_ctr);
     if (r->tstream) cudaStreamDestroy(r->tstream);
     for (cudaEvent_t e : {r->ev_train, r->ev_acc[0], r->ev_acc[1]})
         if (e) cudaEventDestroy(e);
@@ -704,6 +706,7 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     };
     if (cudaStreamCreateWithFlags(&r->stream, cudaStreamNonBlocking) != cudaSuccess) return fail_out(NASG_ERR_CUDA);
     if (cudaMallocHost(&r->h_acc, 10 * sizeof(double)) != cudaSuccess) return fail_out(NASG_ERR_OOM);
+    if (cudaMallocHost(&r->h_ctr, 8 * sizeof(unsigned long long)) != cudaSuccess) return fail_out(NASG_ERR_OOM);
     ctx_set_query_pdl(ctx, !c.pipelined);
     if (c.pipelined) {
         // training shares the SMs with concurrent tracing: no early-started CTAs parked on them
@@ -856,13 +859,13 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
         if ((rc = launch_trace(r, i, b, r->samples_buf[c.pipelined ? (i & 1) : 0])) != NASG_OK) return rc;
     }
     if ((rc = launch_accumulate(r, i)) != NASG_OK) return rc;
-    unsigned long long ctr[8];
+    unsigned long long *ctr = r->h_ctr;  // pinned: the read-back never waits behind an upload
 #ifdef NASG_RENDER_PROF
     cudaEventRecord(pf.b, s);
     pf.host[0] += ms_since(T0);
     auto T1 = std::chrono::steady_clock::now();
 #endif
-    RCUDA(cudaMemcpyAsync(ctr, P.ctr, sizeof(ctr), cudaMemcpyDeviceToHost, s));
+    RCUDA(cudaMemcpyAsync(ctr, P.ctr, 8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     RCUDA(cudaStreamSynchronize(s));
 #ifdef NASG_RENDER_PROF
     pf.host[1] += ms_since(T1);
