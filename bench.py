@@ -224,7 +224,7 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     cs, cur = torch.cuda.Stream(), torch.cuda.current_stream()
     copied = [torch.cuda.Event(), torch.cuda.Event()]
     trained = [torch.cuda.Event(), torch.cuda.Event()]
-    e2e_steps = max(args.train_steps, 20)
+    e2e_steps = max(args.train_steps, 40)
 
     def e2e_trial():
         barrier(ws)
@@ -251,6 +251,19 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     e2e = {"value": n * ws * e2e_steps / te, "unit": "samples/s", "steps": e2e_steps, "trials": 3,
            "trial_values": [n * ws * e2e_steps / x for x in trials], "h2d_bytes_per_step": n * 64 * ws,
            "d2h_bytes_per_step": 40 * ws, "api": "nasg_train_iteration (samples from pinned host memory, stats read back)"}
+    # the e2e step's own roofline: one step's 64 B/sample upload alone (CUDA events, best of 3)
+    best = float("inf")
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        with torch.cuda.stream(cs):
+            bufs[0].copy_(hs, non_blocking=True)
+        e1.record(cs)
+        e1.synchronize()
+        best = min(best, e0.elapsed_time(e1) * 1e-3)
+    e2e["pcie_h2d_gbs_measured"] = hs.numel() * hs.element_size() / best / 1e9
+    e2e["h2d_roofline_samples_per_s"] = n * ws / best
+    e2e["frac_of_h2d_roofline"] = e2e["value"] / e2e["h2d_roofline_samples_per_s"]
     t = max_over_ranks(sum(times), ws)
     st = g.train_iteration(s, 1.0)
     g.close()
