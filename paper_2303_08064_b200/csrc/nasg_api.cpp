@@ -376,7 +376,7 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
         CUDA_TRY(cudaMemsetAsync(c->d_step_stats, 0, 3 * sizeof(double), s));
     }
     CHECK_LAUNCH();
-    if (c->nranks > 1) {  // data-parallel exchange: sum of unnormalised-by-rank grads
+    if (c->comm) {  // data-parallel exchange (any attached communicator, 1 rank included): sum of unnormalised-by-rank grads
         ncclResult_t e1 = g_nccl.allReduce(c->grad, c->grad, c->nw, ncclFloat32, ncclSum, c->comm, s);
         ncclResult_t e2 = g_nccl.allReduce(c->d_step_stats, c->d_step_stats, 3, ncclFloat64, ncclSum, c->comm, s);
         if (e1 != ncclSuccess || e2 != ncclSuccess) return fail(NASG_ERR_NCCL, "ncclAllReduce failed");
@@ -1038,7 +1038,7 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     // the same deterministic schedule (single rank: exactly guiding.cpp:204-276).
     std::vector<int64_t> n_all((size_t)c->nranks, 0);
     n_all[(size_t)c->rank] = n;
-    if (c->nranks > 1) {
+    if (c->comm) {
         int64_t *d_n = nullptr;
         CUDA_TRY(cudaMalloc(&d_n, sizeof(int64_t) * c->nranks));
         CUDA_TRY(cudaMemcpyAsync(d_n + c->rank, &n, sizeof(int64_t), cudaMemcpyHostToDevice, s));
@@ -1151,7 +1151,6 @@ int nasg_comm_unique_id(void *out) {
 
 int nasg_comm_init(nasg_ctx *c, const void *uid, int rank, int nranks) {
     if (!c || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(NASG_ERR_INVALID, "bad argument");
-    if (nranks == 1) return NASG_OK;
     {
         std::lock_guard<std::mutex> lk(g_nccl_mu);
         if (!g_nccl.load()) return fail(NASG_ERR_NCCL, "libnccl.so.2 not loadable");
@@ -1159,8 +1158,11 @@ int nasg_comm_init(nasg_ctx *c, const void *uid, int rank, int nranks) {
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
     CUDA_TRY(cudaSetDevice(c->device));
+    if (c->comm && c->comm_owned && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+    c->comm = nullptr;
     ncclResult_t e = g_nccl.commInitRank(&c->comm, nranks, id, rank);
     if (e != ncclSuccess) return fail(NASG_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(e) : ""));
+    c->comm_owned = true;
     c->rank = rank;
     c->nranks = nranks;
     return NASG_OK;
@@ -1169,7 +1171,7 @@ int nasg_comm_init(nasg_ctx *c, const void *uid, int rank, int nranks) {
 int nasg_attach_nccl(nasg_ctx *c, void *comm, int rank, int nranks) {
     if (!c || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !comm))
         return fail(NASG_ERR_INVALID, "bad argument");
-    if (nranks == 1) return NASG_OK;
+    if (nranks == 1 && !comm) return NASG_OK;
     {
         std::lock_guard<std::mutex> lk(g_nccl_mu);
         if (!g_nccl.load()) return fail(NASG_ERR_NCCL, "libnccl.so.2 not loadable");

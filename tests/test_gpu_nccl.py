@@ -1,0 +1,62 @@
+"""The data-parallel exchange path of Trainer::train_iteration on a real NCCL
+communicator: with a communicator attached, every Adam step
+allreduces the unnormalised dW and the step statistics, re-checks the summed
+gradient for non-finite entries and only then runs Adam (guiding.cpp:244-273,
+net.hpp:137-158).
+
+The pool has one GPU, so the communicator here has one rank: the exchange is
+an identity, and the weights, Adam moments and statistics must be
+bit-identical to a context without a communicator on the same samples — the
+check that the NCCL code path itself (allreduce, allgather of buffer sizes,
+finite re-check) is wired correctly.  The N > 1 rank/plan/shard logic is
+covered with gloo in test_multi_rank.py.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2303_08064_b200 as nasg  # noqa: E402
+
+
+def _train(prec, samples, comm, iters=2):
+    g = nasg.Guide(nasg.TrainerConfig(seed=5, sample_capacity=len(samples), batch_size=2048))
+    g.train_precision = prec
+    if comm:
+        g.comm_init(nasg.Guide.comm_unique_id(), 0, 1)
+    l0 = g.kernel_launches
+    stats = [g.train_iteration(samples, 0.5) for _ in range(iters)]
+    torch.cuda.synchronize()
+    launches = g.kernel_launches - l0
+    w = g.get_weights()
+    g.close()
+    return w, stats, launches
+
+
+@pytest.mark.parametrize("prec", [nasg.NASG_MLP_FP32, nasg.NASG_MLP_BF16])
+def test_one_rank_nccl_exchange_is_bit_identical(prec):
+    s = torch.from_numpy(nasg.synth_samples(21, 8192)).cuda()
+    w_ref, st_ref, l_ref = _train(prec, s, comm=False)
+    w_dp, st_dp, l_dp = _train(prec, s, comm=True)
+    steps = sum(x.steps for x in st_ref)
+    assert steps == 8  # 2 iterations x ceil(8192 / 2048)
+    # the exchange really ran: one finite re-check launch per Adam step
+    assert l_dp - l_ref == steps
+    assert np.array_equal(w_ref.view(np.uint32), w_dp.view(np.uint32))
+    for a, b in zip(st_ref, st_dp):
+        assert (a.steps, a.dropped_samples, a.skipped_updates) == (b.steps, b.dropped_samples, b.skipped_updates)
+        assert a.mean_loss == b.mean_loss
+
+
+def test_one_rank_nccl_empty_buffer_is_noop():
+    g = nasg.Guide(nasg.TrainerConfig(seed=5))
+    g.comm_init(nasg.Guide.comm_unique_id(), 0, 1)
+    w0 = g.get_weights()
+    st = g.train_iteration(None, 1.0)
+    assert st.steps == 0
+    assert np.array_equal(w0, g.get_weights())
+    g.close()
