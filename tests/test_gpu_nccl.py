@@ -60,3 +60,25 @@ def test_one_rank_nccl_empty_buffer_is_noop():
     assert st.steps == 0
     assert np.array_equal(w0, g.get_weights())
     g.close()
+
+
+def test_one_rank_nccl_render_loop_is_bit_identical():
+    # the guided render loop (configs 4-5) trains through the same exchange: with a
+    # one-rank communicator the film and the weights must not change by a bit
+    lo, hi = nasg.scene_bounds(nasg.SCENE_BOX)
+    out = []
+    for comm in (False, True):
+        g = nasg.Guide(nasg.TrainerConfig(seed=7), bmin=lo, bmax=hi)
+        g.precision = g.train_precision = nasg.NASG_MLP_BF16
+        if comm:
+            g.comm_init(nasg.Guide.comm_unique_id(), 0, 1)
+        r = nasg.Render(g, scene=nasg.SCENE_BOX, width=80, height=64, schedule_m=1, schedule_b=4)
+        try:
+            for _ in range(4):
+                r.iteration()
+            out.append((r.image(), g.get_weights()))
+        finally:
+            r.close()
+            g.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1].view(np.uint32), out[1][1].view(np.uint32))
