@@ -194,6 +194,9 @@ int64_t nasg_adam_t(nasg_ctx *ctx);
 int nasg_dp_plan(const nasg_config *cfg, const int64_t *n_per_rank, int nranks, int rank, int max_steps,
                  int64_t *local_count, int64_t *global_count, int32_t *reshuffle_before);
 int nasg_comm_unique_id(void *out_128_bytes);
+/* Create this rank's NCCL communicator (any nranks >= 1).  Once a context has a
+ * communicator every Adam step runs the exchange (dW + statistics allreduce and
+ * the finite re-check); with one rank it is an identity, bit for bit. */
 int nasg_comm_init(nasg_ctx *ctx, const void *unique_id_128_bytes, int rank, int nranks);
 /* Use a communicator the caller already has (an ncclComm_t, e.g. the one its
  * own data-parallel framework created over the same ranks) instead of creating
