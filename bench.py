@@ -38,6 +38,9 @@ METRIC = "NASG guided queries/sec (fwd+sample+pdf) & train samples/sec, 1–8 B2
 FLOP_PER_QUERY = 2 * (64 * 128 + 128 * 128 + 128 * 128 + 128 * 65)  # 98,560
 BYTES_PER_QUERY = 68  # 36 B x/wo/n + 16 B xi in + 16 B dir+pdf out (algorithmic)
 FLOP_PER_SAMPLE = 279_296  # fwd 98,560 + dW 98,560 + delta 82,176
+# the fp32 (accuracy) path runs on the FFMA pipe: 148 SMs x 128 lanes x 2 FLOP x 1.965 GHz
+FP32_FFMA_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+FP32_PEAK_KIND = "nominal fp32 FFMA (148 SMs x 128 x 2 x 1.965 GHz)"
 
 
 def peaks():
@@ -104,6 +107,18 @@ def dist_init():
     return ws, rank, local
 
 
+def self_launch(n):
+    """`python bench.py --gpus N` outside torchrun: start N ranks (one per GPU) the
+    way the driver does and return their exit status."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def max_over_ranks(x, ws):
     if ws == 1:
         return x
@@ -120,46 +135,83 @@ def barrier(ws):
         dist.barrier()
 
 
-def cpu_reference_rate(n_total, seconds, threads=None):
-    """The reference's own query path (infer_guide + mixture_sample), OpenMP over queries."""
-    from oracle.oracle import Oracle, available
-    import paper_2303_08064_b200 as nasg
+def cpu_info():
+    """Host CPU model and the cores this process may use (stated beside every CPU number)."""
+    model = "unknown"
+    try:
+        model = next(l.split(":", 1)[1].strip() for l in open("/proc/cpuinfo") if l.startswith("model name"))
+    except (OSError, StopIteration):
+        pass
+    usable = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    return {"cpu_model": model, "nproc": usable, "logical_cpus": os.cpu_count()}
+
+
+def _cpu_oracle():
+    """The reference build (oracle/_ref) if present, else the C restatement.  Inputs
+    come from the checker's own generator (byte-identical to nasg.synth_*, pinned
+    by tests/test_abi.py), so a CPU leg never maps the CUDA library."""
+    from oracle.oracle import Oracle, available, LIBS
     kind = "reference" if available("ref") else "port"
     o = Oracle("ref" if kind == "reference" else "orc")
-    threads = threads or os.cpu_count()
+    return o, kind, os.path.relpath(LIBS["ref" if kind == "reference" else "orc"], ROOT)
+
+
+def cpu_reference_rate(n_total, seconds, threads=None, chunk=1 << 14, steps=None, warmup=1):
+    """The reference's own query path (infer_guide + mixture_sample per query,
+    guiding.cpp:284-293 + sphdist.cpp:183-198), OpenMP over queries.  With `steps`
+    it times exactly that many chunks after `warmup` untimed ones; otherwise it
+    runs chunks for up to `seconds`."""
+    o, kind, so = _cpu_oracle()
+    threads = threads or len(os.sched_getaffinity(0))
     w = o.init_network(0)
-    chunk = 1 << 14
-    x, wo, nrm, xi = nasg.synth_queries(12345, chunk)
+    x, wo, nrm, xi = o.synth_queries(12345, chunk)
     q9 = np.ascontiguousarray(np.concatenate([x[:, :3], wo[:, :3], nrm[:, :3]], 1))
-    o.query_sample(w, q9[:256], xi[:256], threads=threads)  # warm-up (thread pool)
-    done, t0 = 0, time.perf_counter()
-    while done < n_total and time.perf_counter() - t0 < seconds:
+    o.query_sample(w, q9[:256], xi[:256], threads=threads)  # thread pool warm-up
+    for _ in range(warmup):
         o.query_sample(w, q9, xi, threads=threads)
+    done, t0, per = 0, time.perf_counter(), []
+    while (done < n_total and time.perf_counter() - t0 < seconds) if steps is None else len(per) < steps:
+        t1 = time.perf_counter()
+        o.query_sample(w, q9, xi, threads=threads)
+        per.append(time.perf_counter() - t1)
         done += chunk
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "queries/s", "cores": threads, "kind": kind,
-            "sample": f"{done} synthetic queries (infer_guide+mixture_sample per query, N=8, "
-                      f"{threads} OpenMP threads, {dt:.1f} s)"}
+    return {"value": done / dt, "unit": "queries/s", "cores": threads, "kind": kind, "library": so,
+            "ms_per_step": 1e3 * statistics.mean(per),
+            "sample": f"{done} synthetic queries in steps of {chunk} (infer_guide+mixture_sample per query, N=8, "
+                      f"{threads} OpenMP threads, {dt:.1f} s)", **cpu_info()}
 
 
 def cpu_reference_train_rate(seconds=8.0):
     """The reference's own Trainer::train_iteration (oracle/_ref, single-threaded by
     design, guiding.cpp:196-282) on config-1 sized buffers (S = 2^14 samples, t = 2^12)."""
-    from oracle.oracle import Oracle, available
-    import paper_2303_08064_b200 as nasg
-    kind = "reference" if available("ref") else "port"
-    o = Oracle("ref" if kind == "reference" else "orc")
+    o, kind, so = _cpu_oracle()
     n = 1 << 14
     tr = o.trainer(capacity=n, batch=1 << 12, seed=3)
-    s = nasg.synth_samples(11, n)
+    s = o.synth_samples(11, n)
     done, t0 = 0, time.perf_counter()
     while time.perf_counter() - t0 < seconds:
         tr.train(s, 1.0)
         done += n
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": "samples/s", "cores": 1, "kind": kind,
+    return {"value": done / dt, "unit": "samples/s", "cores": 1, "kind": kind, "library": so,
             "sample": f"{done} synthetic samples through train_iteration (S = t*4 = 16384, 4 Adam steps per call), "
-                      f"{dt:.1f} s, 1 thread"}
+                      f"{dt:.1f} s, 1 thread", **cpu_info()}
+
+
+def cpu_reference_default_train():
+    """One default Trainer::train_iteration (S = 2^16, t = 2^12: 16 Adam steps) of the
+    reference (single-threaded by design, guiding.cpp:196-282) — config 1's train leg."""
+    o, kind, so = _cpu_oracle()
+    n = 1 << 16
+    tr = o.trainer(capacity=n, batch=1 << 12, seed=3)
+    s = o.synth_samples(11, n)
+    t0 = time.perf_counter()
+    st = tr.train(s, 1.0)
+    dt = time.perf_counter() - t0
+    return {"value": n / dt, "unit": "samples/s", "seconds_per_iteration": dt, "steps": st["steps"], "cores": 1,
+            "kind": kind, "library": so, "sample": "one train_iteration of 65,536 synthetic samples, 1 thread",
+            **cpu_info()}
 
 
 def bench_config(n, ws):
@@ -170,15 +222,21 @@ def bench_config(n, ws):
 
 
 def run_reference(args, ws, rank):
+    """`--impl reference`: the reference's own CPU query path on all host cores, on this
+    arm's workload; each step is a bounded sample of 2^19 of the config's queries
+    (the whole K + W run takes seconds).  Rank 0 alone runs (no CUDA, no NCCL)."""
     if rank != 0:
         return
-    cb = cpu_reference_rate(args.queries * args.steps, args.cpu_seconds)
+    chunk = min(args.queries, 1 << 19)
+    cb = cpu_reference_rate(0, 0, chunk=chunk, steps=args.steps, warmup=args.warmup)
     line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "queries/s",
-            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": bench_config(args.queries, ws),
             "cpu_baseline": cb, "e2e": {"value": cb["value"], "unit": "queries/s",
                                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not args.no_train:
+        line["train"] = {"cpu_baseline": cpu_reference_train_rate(4.0)}
     print(json.dumps(line), flush=True)
 
 
@@ -200,7 +258,7 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     import torch
     n = args.train_samples
     # global S = t = ws * 2^18: the data-parallel plan gives every rank its own 2^18 rows per step
-    g = g_cls(nasg.TrainerConfig(seed=3, sample_capacity=n * ws, batch_size=n * ws))
+    g = g_cls(nasg.TrainerConfig(seed=3, sample_capacity=n * ws, batch_size=n * ws), device=torch.cuda.current_device())
     g.train_precision = nasg.NASG_MLP_BF16 if precision == "bf16" else nasg.NASG_MLP_FP32
     if ws > 1:
         import torch.distributed as dist
@@ -273,14 +331,66 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     # algorithmic FLOP of the whole step (fwd + dW + delta, 279,296 per sample) against the
     # bf16 tensor peak; the step also moves 1,696 B/sample of bf16 activations through HBM
     # twice for the split-K dW GEMM (K_dw runs at ~94 % of HBM, profiles/r1_train_bf16_ncu.md)
-    roof = {"bound": "tensor", "achieved": tf, "unit": "TFLOP/s",
-            "peak": pk["bf16_tflops"] if precision == "bf16" else 74.4,
-            "peak_kind": f"{pk_kind} bf16 burst" if precision == "bf16" else "nominal fp32 FFMA (148 SMs x 128 x 2 x 1.965 GHz)"}
+    roof = {"bound": "tensor" if precision == "bf16" else "fp32-ffma", "achieved": tf, "unit": "TFLOP/s",
+            "peak": pk["bf16_tflops"] if precision == "bf16" else FP32_FFMA_TFLOPS,
+            "peak_kind": f"{pk_kind} bf16 burst" if precision == "bf16" else FP32_PEAK_KIND}
     roof["frac"] = tf / roof["peak"]
     return {"metric": f"train samples/s (config 3: 2^18 samples/step/GPU, fused fwd+KL+bwd+dW+Adam, {precision})",
             "value": rate, "unit": "samples/s", "ms_per_step": 1e3 * t / args.train_steps,
             "achieved_tflops": tf, "roofline": roof, "e2e": e2e, "dtype": precision,
             "gpu_launches": launches, "last_mean_loss": st.mean_loss}
+
+
+def bench_config1(nasg, args, ws, rank):
+    """Config 1 of BASELINE.json, the reference's own default case: 65,536 synthetic
+    queries (fwd + sample + pdf) and one default train_iteration (S = 2^16 samples,
+    t = 2^12 -> 16 Adam steps, guiding.hpp:122-130), on this GPU, beside the same
+    workload through oracle/_ref on the host (rank 0 only)."""
+    import torch
+    q = 1 << 16
+    host = nasg.synth_queries(4242, q, first=rank * q)
+    dev = [torch.from_numpy(a).cuda() for a in host]
+    out = torch.empty((q, 4), dtype=torch.float32, device="cuda")
+    stream = torch.cuda.current_stream()
+    res = {"workload": "config 1: 65,536 queries (fwd+sample+pdf) + one default train_iteration "
+                       "(S=2^16, t=2^12, 16 Adam steps)"}
+    g = nasg.Guide(nasg.TrainerConfig(seed=0), device=torch.cuda.current_device())
+    for prec, name in ((nasg.NASG_MLP_BF16, "bf16"), (nasg.NASG_MLP_FP32, "fp32")):
+        g.precision = prec
+        for _ in range(3):
+            g.query_sample(*dev, dir_pdf=out)
+        torch.cuda.synchronize()
+        t = sum(time_events(lambda: g.query_sample(*dev, dir_pdf=out), 20, stream)) / 20
+        res[f"query_{name}"] = {"queries_per_s": q / t, "us_per_batch": 1e6 * t}
+    g.close()
+    samples = torch.from_numpy(nasg.synth_samples(11, q, first=rank * q)).cuda()
+    pk, pk_kind = peaks()
+    for name, prec in (("bf16", nasg.NASG_MLP_BF16), ("fp32", nasg.NASG_MLP_FP32)):
+        g = nasg.Guide(nasg.TrainerConfig(seed=3), device=torch.cuda.current_device())
+        g.train_precision = prec
+        for _ in range(3):
+            g.train_iteration(samples, 1.0, stats=False)
+        torch.cuda.synchronize()
+        l0 = g.kernel_launches
+        ts = time_events(lambda: g.train_iteration(samples, 1.0, stats=False), 10, stream)
+        launches = (g.kernel_launches - l0) // 10
+        st = g.train_iteration(samples, 1.0)
+        g.close()
+        t = sum(ts) / len(ts)
+        tf = q * FLOP_PER_SAMPLE / t / 1e12
+        peak = pk["bf16_tflops"] if name == "bf16" else FP32_FFMA_TFLOPS
+        res[f"train_iteration_{name}"] = {
+            "ms_per_iteration": 1e3 * t, "samples_per_s": q / t, "steps": st.steps, "launches_per_iteration": launches,
+            "roofline": {"bound": "tensor" if name == "bf16" else "fp32-ffma", "achieved": tf, "unit": "TFLOP/s",
+                         "peak": peak, "frac": tf / peak,
+                         "peak_kind": f"{pk_kind} bf16 burst" if name == "bf16" else FP32_PEAK_KIND,
+                         "note": "16 latency-bound steps of t = 4096 rows"}}
+    if rank == 0 and not args.no_cpu:
+        res["cpu_baseline"] = {"query": cpu_reference_rate(0, 0, chunk=q, steps=3, warmup=1),
+                               "train_iteration": cpu_reference_default_train()}
+    del dev, out, samples
+    torch.cuda.empty_cache()
+    return res
 
 
 def bench_sweep(nasg, args, ws, rank):
@@ -292,7 +402,7 @@ def bench_sweep(nasg, args, ws, rank):
     host = nasg.synth_queries(77, nmax, first=rank * nmax)
     dev = [torch.from_numpy(a).cuda() for a in host]
     res = torch.empty((nmax, 4), dtype=torch.float32, device="cuda")
-    g = nasg.Guide(nasg.TrainerConfig(seed=0))
+    g = nasg.Guide(nasg.TrainerConfig(seed=0), device=torch.cuda.current_device())
     stream = torch.cuda.current_stream()
     for prec, name in ((nasg.NASG_MLP_BF16, "bf16"), (nasg.NASG_MLP_FP32, "fp32")):
         g.precision = prec
@@ -318,11 +428,12 @@ def bench_render(nasg, args, ws, rank, width, height, iters, label, pipelined=Fa
     path per pixel of this rank's rows (wavefront tracer, NEE+MIS, guided scattering
     through the fused network query), sample collection, one train_iteration (S = 2^16,
     t = 2^12: 16 Adam steps, data-parallel over ranks through NCCL) and accumulation.
-    Rows are split evenly over ranks (strong scaling of the fixed image)."""
+    Rows are dealt to the ranks in interleaved 8-row bands (strong scaling of the
+    fixed image)."""
     import torch
     scene = nasg.SCENE_CRACK
     lo, hi = nasg.scene_bounds(scene)
-    g = nasg.Guide(nasg.TrainerConfig(seed=5), bmin=lo, bmax=hi)
+    g = nasg.Guide(nasg.TrainerConfig(seed=5), device=torch.cuda.current_device(), bmin=lo, bmax=hi)
     g.precision = nasg.NASG_MLP_BF16
     g.train_precision = nasg.NASG_MLP_BF16
     if ws > 1:
@@ -330,8 +441,9 @@ def bench_render(nasg, args, ws, rank, width, height, iters, label, pipelined=Fa
         uid = [g.comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         g.comm_init(uid[0], rank, ws)
-    rb, re = rank * height // ws, (rank + 1) * height // ws
-    r = nasg.Render(g, scene=scene, width=width, height=height, row_begin=rb, row_end=re, seed=3,
+    # interleaved tile rows (bands of 8 rows dealt round-robin over the ranks): every
+    # rank gets the same mix of scene content, so the per-rank trace time balances
+    r = nasg.Render(g, scene=scene, width=width, height=height, row_band=8, shard=rank, nshards=ws, seed=3,
                     lazy_train_stats=True, pipelined=pipelined)
     torch.cuda.synchronize()
     barrier(ws)
@@ -348,6 +460,7 @@ def bench_render(nasg, args, ws, rank, width, height, iters, label, pipelined=Fa
     launches = g.kernel_launches + r.kernel_launches - l0
     img = r.image()
     finite = bool(np.isfinite(img).all())
+    r_rows = r.rows
     r.close()
     g.close()
     return {"workload": label, "scene": "crack (box lit through a slit: anisotropic indirect light)",
@@ -355,6 +468,7 @@ def bench_render(nasg, args, ws, rank, width, height, iters, label, pipelined=Fa
             "paths_per_s": width * height * iters / dt, "vertices_per_s_rank0": verts / dt,
             "guided_queries_per_s_rank0": guided / dt, "train_samples_per_iteration_rank0": kept / iters,
             "gpu_launches_rank0": launches, "final_b": st["b"], "image_finite": finite, "scaling": "strong",
+            "sharding": f"interleaved 8-row bands, rank {rank} of {ws} renders {r_rows} rows",
             "loop": ("pipelined: tracing of iteration i+1 overlaps training i on a second stream (snapshot one "
                      "iteration staler)" if pipelined else "serial SPEC loop: trace i -> train i -> publish -> trace i+1"),
             "cpu_baseline": None, "note": "the reference specifies this tracer (SPEC.md:378-478) but ships no code"}
@@ -373,15 +487,21 @@ def main():
     ap.add_argument("--no-train", action="store_true")
     ap.add_argument("--no-render", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-config1", action="store_true")
     ap.add_argument("--render-4k-iters", type=int, default=64)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    ws, rank, local = dist_init()
     if args.impl == "reference":
-        run_reference(args, ws, rank)
+        # the CPU reference arm: no CUDA context, no process group; rank 0 alone works
+        run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
         return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(self_launch(args.gpus))
+    if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
+    ws, rank, local = dist_init()
 
     import torch
     import paper_2303_08064_b200 as nasg
@@ -476,6 +596,7 @@ def main():
     del dev, out, cbuf
     torch.cuda.empty_cache()
 
+    config1 = None if args.no_config1 else bench_config1(nasg, args, ws, rank)
     sweep = None if args.no_sweep else bench_sweep(nasg, args, ws, rank)
     train = None if args.no_train else {p: bench_train(nasg.Guide, nasg, args, ws, rank, p) for p in ("bf16", "fp32")}
     render = None
@@ -486,10 +607,10 @@ def main():
                                                     "config 4: 1024x1024, 512 spp, interleaved train/render",
                                                     pipelined=True),
                   "config5": bench_render(nasg, args, ws, rank, 3840, 2160, args.render_4k_iters,
-                                          f"config 5: 3840x2160 sharded by pixel rows over {ws} GPU(s), "
+                                          f"config 5: 3840x2160 sharded by interleaved pixel rows over {ws} GPU(s), "
                                           f"{args.render_4k_iters} spp"),
                   "config5_pipelined": bench_render(nasg, args, ws, rank, 3840, 2160, args.render_4k_iters,
-                                                    f"config 5: 3840x2160 sharded by pixel rows over {ws} GPU(s), "
+                                                    f"config 5: 3840x2160 sharded by interleaved pixel rows over {ws} GPU(s), "
                                                     f"{args.render_4k_iters} spp", pipelined=True)}
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -502,7 +623,7 @@ def main():
                 "scaling": "weak", "vs_baseline": None, "dtype": dtype, "data": "synthetic",
                 "config": bench_config(n, ws),
                 "e2e": e2e, "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches,
-                "clocks": clk.summary(), "sweep": sweep, "train": train, "render": render}
+                "clocks": clk.summary(), "config1": config1, "sweep": sweep, "train": train, "render": render}
         print(json.dumps(line), flush=True)
 
 

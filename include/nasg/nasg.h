@@ -210,6 +210,8 @@ typedef struct {
     int64_t adam_steps;        /* AdamState::t (net.hpp:115): applied, non-skipped updates */
     int64_t iterations;        /* Trainer::iterations_ (train_iteration calls) */
     int rank, nranks;          /* data-parallel position */
+    uint64_t collectives;      /* NCCL launches issued: one grouped dW + statistics allreduce
+                                  per Adam step, one buffer-size allgather per train_iteration */
 } nasg_counters;
 int nasg_get_counters(nasg_ctx *ctx, nasg_counters *out);  /* synchronises the device */
 uint64_t nasg_encode_clamp_count(nasg_ctx *ctx);
@@ -228,8 +230,11 @@ double nasg_stride_update(double l, uint64_t collected, uint64_t capacity);
  * Russian roulette from depth 5 (cap 0.95), max depth 16, per-vertex radiance
  * back-propagation into TrainingSamples for one pixel per l x l tile, then
  * train_iteration, stride_update and the progressive w_i ramp (SPEC accumulate).
- * Multi-GPU: each rank renders the pixel rows [row_begin, row_end) and trains
- * data-parallel through the context's NCCL communicator (nasg_comm_init). */
+ * Multi-GPU: each rank renders either the contiguous pixel rows [row_begin,
+ * row_end) or (row_band > 0) every nshards-th band of row_band rows starting
+ * with band `shard` — interleaved tile rows, so every rank sees the same mix
+ * of scene content — and trains data-parallel through the context's NCCL
+ * communicator (nasg_comm_init). */
 typedef struct nasg_render nasg_render;
 enum { NASG_SCENE_FURNACE = 0, NASG_SCENE_BOX = 1, NASG_SCENE_CRACK = 2, NASG_SCENE_DARK = 3, NASG_SCENE_ATTIC = 4 };
 typedef struct {
@@ -253,6 +258,11 @@ typedef struct {
                               published); 1: tracing of i+1 overlaps training i on a second stream,
                               so iteration i traces with the snapshot of training i-2 (one
                               iteration staler), and stats.train is training i-2's */
+    int row_band;          /* > 0: interleaved sharding in bands of row_band rows (row_begin /
+                              row_end ignored); this rank owns bands shard, shard + nshards, ...
+                              and its image is those rows in order; collection tiles are laid
+                              over that compacted image */
+    int shard, nshards;    /* this rank's band phase and the band period (row_band > 0) */
 } nasg_render_config;
 typedef struct {
     int64_t iteration;     /* the iteration just rendered */

@@ -1079,3 +1079,62 @@ int orc_load_checkpoint(const char *path, float *w, int max_floats, int *n_comp)
     if (n_comp) *n_comp = (int)n;
     return (int)total;
 }
+
+/* ---------------- synthetic workloads ----------------
+ * Byte-identical restatement of the product's nasg_synth_queries /
+ * nasg_synth_samples, so the CPU arms of bench.py never load the CUDA library
+ * (pinned by tests/test_abi.py::test_synth_generators_match). */
+static float synth_f24(pcg_t *g) { return (float)(pcg_next(g) >> 8) * 0x1p-24f; }
+
+static void synth_sphere(pcg_t *g, float *out) {
+    const double z = 1.0 - 2.0 * synth_f24(g);
+    const double phi = 2.0 * 3.14159265358979323846 * synth_f24(g);
+    const double t = 1.0 - z * z;
+    const double rr = sqrt(t > 0.0 ? t : 0.0);
+    out[0] = (float)(rr * cos(phi));
+    out[1] = (float)(rr * sin(phi));
+    out[2] = (float)z;
+    out[3] = 0.f;
+}
+
+void orc_synth_queries(uint64_t seed, int64_t first, int64_t n, const float *bmin, const float *bmax, float *x,
+                       float *wo, float *nrm, float *xi) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        pcg_t g;
+        pcg_seed(&g, orc_hash_combine(seed, (uint64_t)(first + i)), 0x51);
+        for (int k = 0; k < 3; ++k) x[4 * i + k] = bmin[k] + (bmax[k] - bmin[k]) * synth_f24(&g);
+        x[4 * i + 3] = 0.f;
+        synth_sphere(&g, wo + 4 * i);
+        synth_sphere(&g, nrm + 4 * i);
+        for (int k = 0; k < 4; ++k) xi[4 * i + k] = synth_f24(&g);
+    }
+}
+
+void orc_synth_samples(uint64_t seed, int64_t first, int64_t n, const float *bmin, const float *bmax, float *out16) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        pcg_t g;
+        pcg_seed(&g, orc_hash_combine(seed, (uint64_t)(first + i)), 0x53);
+        float *s = out16 + 16 * i;
+        float wo[4], nn[4], wi[4];
+        for (int k = 0; k < 3; ++k) s[k] = bmin[k] + (bmax[k] - bmin[k]) * synth_f24(&g);
+        synth_sphere(&g, wo);
+        synth_sphere(&g, nn);
+        synth_sphere(&g, wi);
+        for (int k = 0; k < 3; ++k) {
+            s[4 + k] = wo[k];
+            s[8 + k] = nn[k];
+            s[12 + k] = wi[k];
+        }
+        const double dn = (double)wi[0] * nn[0] + (double)wi[1] * nn[1] + (double)wi[2] * nn[2];
+        const double cosn = dn > 0.0 ? dn : 0.0;
+        const double mu[3] = {sin(2.0 * s[0]) + 0.5, cos(3.0 * s[1]), 1.0 + 0.5 * sin((double)s[2])};
+        const double inv = 1.0 / sqrt(mu[0] * mu[0] + mu[1] * mu[1] + mu[2] * mu[2]);
+        const double d = (wi[0] * mu[0] + wi[1] * mu[1] + wi[2] * mu[2]) * inv;
+        s[3] = (float)(exp(20.0 * (d - 1.0)) * cosn);
+        s[7] = (float)(1.0 / (4.0 * 3.14159265358979323846));
+        s[11] = (float)(cosn / 3.14159265358979323846);
+        s[15] = 0.f;
+    }
+}

@@ -74,6 +74,11 @@ void orc_set_reverse_sum(int on);
 int orc_save_checkpoint(const char *path, const float *w, int out_dim, int n_comp);
 int orc_load_checkpoint(const char *path, float *w, int max_floats, int *n_comp);
 
+/* synthetic workloads: byte-identical to nasg_synth_queries / nasg_synth_samples */
+void orc_synth_queries(uint64_t seed, int64_t first, int64_t n, const float *bmin, const float *bmax, float *x,
+                       float *wo, float *nrm, float *xi);
+void orc_synth_samples(uint64_t seed, int64_t first, int64_t n, const float *bmin, const float *bmax, float *out16);
+
 #ifdef __cplusplus
 }
 #endif

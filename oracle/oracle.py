@@ -20,9 +20,19 @@ import subprocess
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
+def _host_has_v3() -> bool:
+    """x86-64-v3 (AVX2 + FMA + BMI2) on this host: the reference build in _ref/
+    uses it; a host without it loads the generic build of the same code."""
+    try:
+        flags = next(l for l in open("/proc/cpuinfo") if l.startswith("flags")).split()
+        return all(f in flags for f in ("avx2", "fma", "bmi2", "movbe"))
+    except (OSError, StopIteration):
+        return False
+
+
 LIBS = {
     "orc": os.path.join(HERE, "build", "libnasg_oracle.so"),
-    "ref": os.path.join(HERE, "_ref", "libnasg_ref.so"),
+    "ref": os.path.join(HERE, "_ref", "libnasg_ref.so" if _host_has_v3() else "libnasg_ref_generic.so"),
 }
 
 _f32p = np.ctypeslib.ndpointer(np.float32, flags="C_CONTIGUOUS")
@@ -62,6 +72,8 @@ _SIGS = {
     "trainer_set_weights": (None, [_vp, _f32p]),
     "save_checkpoint": (_int, [C.c_char_p, _f32p, _int, _int]),
     "load_checkpoint": (_int, [C.c_char_p, _f32p, _int, C.POINTER(C.c_int)]),
+    "synth_queries": (None, [_u64, _i64, _i64, _f32p, _f32p, _f32p, _f32p, _f32p, _f32p]),
+    "synth_samples": (None, [_u64, _i64, _i64, _f32p, _f32p, _f32p]),
 }
 
 
@@ -258,6 +270,19 @@ class Oracle:
         if total < 0:
             raise IOError(f"checkpoint load failed ({total}): {path}")
         return w[:total].copy(), n.value
+
+    # ---- synthetic workloads (byte-identical to nasg.synth_*) -------------------
+    def synth_queries(self, seed, n, first=0, bmin=(-1, -1, -1), bmax=(1, 1, 1)):
+        """(n,4) float32 x4: x, wo, nrm, xi — SURVEY §8d synthetic queries."""
+        arrs = [np.empty((n, 4), np.float32) for _ in range(4)]
+        self._synth_queries(seed, first, n, _f3(bmin), _f3(bmax), *arrs)
+        return tuple(arrs)
+
+    def synth_samples(self, seed, n, first=0, bmin=(-1, -1, -1), bmax=(1, 1, 1)):
+        """(n,16) float32 training samples (nasg_train_sample layout)."""
+        out = np.empty((n, 16), np.float32)
+        self._synth_samples(seed, first, n, _f3(bmin), _f3(bmax), out)
+        return out
 
     # ---- trainer --------------------------------------------------------------
     def set_reverse_sum(self, on: bool):

@@ -493,4 +493,60 @@ int ref_load_checkpoint(const char *path, float *w, int max_floats, int *n_comp)
     }
 }
 
+// ---- synthetic workloads ---------------------------------------------
+// Byte-identical restatement of the product's nasg_synth_queries / nasg_synth_samples
+// (paper_2303_08064_b200/csrc/nasg_api.cpp) on the reference's own Pcg32 and
+// hash_combine (math.hpp:81-121), so the reference arm of bench.py builds its
+// inputs without loading the CUDA library (tests/test_abi.py pins the equality).
+static float synth_f24(Pcg32 &r) { return (float)(r.next_u32() >> 8) * 0x1p-24f; }
+
+static void synth_sphere(Pcg32 &r, float *out) {
+    const double z = 1.0 - 2.0 * synth_f24(r);
+    const double phi = 2.0 * 3.14159265358979323846 * synth_f24(r);
+    const double rr = std::sqrt(std::max(0.0, 1.0 - z * z));
+    out[0] = (float)(rr * std::cos(phi));
+    out[1] = (float)(rr * std::sin(phi));
+    out[2] = (float)z;
+    out[3] = 0.f;
+}
+
+void ref_synth_queries(uint64_t seed, int64_t first, int64_t n, const float *bmin, const float *bmax, float *x,
+                       float *wo, float *nrm, float *xi) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        Pcg32 r(hash_combine(seed, (uint64_t)(first + i)), 0x51);
+        for (int k = 0; k < 3; ++k) x[4 * i + k] = bmin[k] + (bmax[k] - bmin[k]) * synth_f24(r);
+        x[4 * i + 3] = 0.f;
+        synth_sphere(r, wo + 4 * i);
+        synth_sphere(r, nrm + 4 * i);
+        for (int k = 0; k < 4; ++k) xi[4 * i + k] = synth_f24(r);
+    }
+}
+
+void ref_synth_samples(uint64_t seed, int64_t first, int64_t n, const float *bmin, const float *bmax, float *out16) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        Pcg32 r(hash_combine(seed, (uint64_t)(first + i)), 0x53);
+        float *s = out16 + 16 * i;
+        float wo[4], nn[4], wi[4];
+        for (int k = 0; k < 3; ++k) s[k] = bmin[k] + (bmax[k] - bmin[k]) * synth_f24(r);
+        synth_sphere(r, wo);
+        synth_sphere(r, nn);
+        synth_sphere(r, wi);
+        for (int k = 0; k < 3; ++k) {
+            s[4 + k] = wo[k];
+            s[8 + k] = nn[k];
+            s[12 + k] = wi[k];
+        }
+        const double cosn = std::max(0.0, (double)wi[0] * nn[0] + (double)wi[1] * nn[1] + (double)wi[2] * nn[2]);
+        const double mu[3] = {std::sin(2.0 * s[0]) + 0.5, std::cos(3.0 * s[1]), 1.0 + 0.5 * std::sin((double)s[2])};
+        const double inv = 1.0 / std::sqrt(mu[0] * mu[0] + mu[1] * mu[1] + mu[2] * mu[2]);
+        const double d = (wi[0] * mu[0] + wi[1] * mu[1] + wi[2] * mu[2]) * inv;
+        s[3] = (float)(std::exp(20.0 * (d - 1.0)) * cosn);
+        s[7] = (float)(1.0 / (4.0 * 3.14159265358979323846));
+        s[11] = (float)(cosn / 3.14159265358979323846);
+        s[15] = 0.f;
+    }
+}
+
 } // extern "C"

@@ -43,7 +43,7 @@ class _Stats(C.Structure):
 
 class _Counters(C.Structure):
     _fields_ = [("encode_clamps", C.c_uint64), ("kernel_launches", C.c_uint64), ("adam_steps", C.c_int64),
-                ("iterations", C.c_int64), ("rank", C.c_int), ("nranks", C.c_int)]
+                ("iterations", C.c_int64), ("rank", C.c_int), ("nranks", C.c_int), ("collectives", C.c_uint64)]
 
 
 class _RenderConfig(C.Structure):
@@ -51,7 +51,7 @@ class _RenderConfig(C.Structure):
                 ("row_end", C.c_int), ("seed", C.c_uint64), ("max_depth", C.c_int), ("rr_depth", C.c_int),
                 ("guiding", C.c_int), ("collect", C.c_int), ("ramp", C.c_int), ("schedule_m", C.c_int),
                 ("schedule_b", C.c_int), ("nee", C.c_int), ("lazy_train_stats", C.c_int),
-                ("pipelined", C.c_int)]
+                ("pipelined", C.c_int), ("row_band", C.c_int), ("shard", C.c_int), ("nshards", C.c_int)]
 
 
 class _RenderStats(C.Structure):
@@ -267,8 +267,16 @@ class Guide:
     functions, batched over device tensors.
     """
 
-    def __init__(self, config: TrainerConfig | None = None, device: int = 0, bmin=(-1, -1, -1), bmax=(1, 1, 1)):
+    def __init__(self, config: TrainerConfig | None = None, device: int | None = None, bmin=(-1, -1, -1),
+                 bmax=(1, 1, 1)):
+        """device: CUDA ordinal (default: torch's current device, else 0)."""
         self.config = config or TrainerConfig()
+        if device is None:
+            try:
+                import torch
+                device = torch.cuda.current_device() if torch.cuda.is_available() else 0
+            except ImportError:
+                device = 0
         cfg = _Config(self.config.n_components, self.config.sample_capacity, self.config.batch_size,
                       self.config.step_factor, self.config.learning_rate, self.config.loss_blend, self.config.seed)
         h = C.c_void_p()
@@ -491,7 +499,7 @@ class Render:
                  row_begin: int = 0, row_end: int = 0, seed: int = 1, guiding: bool = True,
                  collect: bool = True, ramp: bool = True, max_depth: int = 16, rr_depth: int = 5,
                  schedule_m: int = 4, schedule_b: int = 64, nee: bool = True, lazy_train_stats: bool = False,
-                 pipelined: bool = False):
+                 pipelined: bool = False, row_band: int = 0, shard: int = 0, nshards: int = 1):
         cfg = _RenderConfig()
         lib().nasg_render_config_default(C.byref(cfg))
         cfg.scene, cfg.width, cfg.height = scene, width, height
@@ -502,11 +510,16 @@ class Render:
         cfg.nee = int(nee)
         cfg.lazy_train_stats = int(lazy_train_stats)
         cfg.pipelined = int(pipelined)
+        cfg.row_band, cfg.shard, cfg.nshards = row_band, shard, nshards
         h = C.c_void_p()
         _check(lib().nasg_render_create(guide._h, C.byref(cfg), C.byref(h)))
         self._h, self.guide = h, guide
         self.width = width
-        self.rows = (row_end if row_end > 0 else height) - row_begin
+        if row_band > 0:
+            self.rows = sum(min(height, (k + 1) * row_band) - k * row_band
+                            for k in range(shard, -(-height // row_band), nshards))
+        else:
+            self.rows = (row_end if row_end > 0 else height) - row_begin
 
     def iteration(self) -> dict:
         st = _RenderStats()

@@ -85,12 +85,21 @@ struct Paths {
 struct Frame {
     uint64_t seed, iter;
     int width, height, row0;
+    int band, shard, nshards;  // interleaved sharding (band > 0): see frame_row
     float l;          // collection stride
-    int tile_row0;    // floor(row0 / l)
+    int tile_row0;    // floor(row0 / l) (0 with interleaving: tiles over the compacted rows)
     int ntx;          // tiles per row
     int collect, max_depth, rr_depth;
     int nee;
 };
+
+// Image row of this rank's local row lr: contiguous rows from row0, or the
+// lr-th row of the bands shard, shard + nshards, ... of `band` rows each.
+__device__ __forceinline__ int frame_row(const Frame &F, int lr) {
+    if (F.band <= 0) return F.row0 + lr;
+    const int k = lr / F.band;
+    return (k * F.nshards + F.shard) * F.band + (lr - k * F.band);
+}
 
 __device__ inline float4 f4(float3 v, float w) { return make_float4(v.x, v.y, v.z, w); }
 __device__ inline float3 xyz(float4 v) { return make_float3(v.x, v.y, v.z); }
@@ -101,7 +110,7 @@ __global__ void k_begin(Paths P, Frame F) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= P.n) return;
     const Scene &S = c_scene;
-    const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
+    const int px = (int)(i % F.width), py = frame_row(F, (int)(i / F.width));
     const uint64_t pix = (uint64_t)py * F.width + px;
     const float jx = rnd(F.seed, pix, F.iter, 0, 0), jy = rnd(F.seed, pix, F.iter, 0, 1);
     const float sx = 2.f * (px + jx) / F.width - 1.f, sy = 1.f - 2.f * (py + jy) / F.height;
@@ -117,11 +126,14 @@ __global__ void k_begin(Paths P, Frame F) {
     if (i == 0) P.nact[0] = (int)P.n;
     int rank = -1;
     if (F.collect) {  // one pixel per l x l tile (PAPER §6), uniformly at random per tile and iteration
-        const int tx = (int)floorf(px / F.l), ty = (int)floorf(py / F.l);
+        // tiles over the image rows, or over the compacted local rows with interleaving
+        const int ry = F.band > 0 ? (int)(i / F.width) : py;
+        const uint64_t cseed = F.seed ^ 0x636f6c6cull ^ ((uint64_t)F.shard << 40);
+        const int tx = (int)floorf(px / F.l), ty = (int)floorf(ry / F.l);
         const uint64_t tile = ((uint64_t)ty << 32) | (uint32_t)tx;
-        const int cx = (int)floorf((tx + rnd(F.seed ^ 0x636f6c6cull, tile, F.iter, 0, 0)) * F.l);
-        const int cy = (int)floorf((ty + rnd(F.seed ^ 0x636f6c6cull, tile, F.iter, 0, 1)) * F.l);
-        if (cx == px && cy == py) {
+        const int cx = (int)floorf((tx + rnd(cseed, tile, F.iter, 0, 0)) * F.l);
+        const int cy = (int)floorf((ty + rnd(cseed, tile, F.iter, 0, 1)) * F.l);
+        if (cx == px && cy == ry) {
             const int64_t r = (int64_t)(ty - F.tile_row0) * F.ntx + tx;
             if (r >= 0 && r < P.ncap) {
                 rank = (int)r;
@@ -146,7 +158,7 @@ __global__ void k_queue_reset(Paths P, int next) {
 __device__ __forceinline__ void isect_path(Paths &P, const Frame &F, int bounce, int guided, int64_t i) {
     if (!P.alive[i]) return;
     const Scene &S = c_scene;
-    const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
+    const int px = (int)(i % F.width), py = frame_row(F, (int)(i / F.width));
     const uint64_t pix = (uint64_t)py * F.width + px;
     auto R = [&](uint32_t dim) { return rnd(F.seed, pix, F.iter, (uint32_t)bounce + 1, dim); };
     const float3 o = xyz(P.o[i]), d = xyz(P.d[i]);
@@ -231,7 +243,7 @@ __device__ __forceinline__ void update_path(Paths &P, const Frame &F, int bounce
     if (!P.pending[i]) return;
     P.pending[i] = 0;
     const Scene &S = c_scene;
-    const int px = (int)(i % F.width), py = F.row0 + (int)(i / F.width);
+    const int px = (int)(i % F.width), py = frame_row(F, (int)(i / F.width));
     const uint64_t pix = (uint64_t)py * F.width + px;
     const float4 vx = P.vx[i];
     const Mat &m = S.mats[(int)vx.w];
@@ -663,6 +675,7 @@ int nasg_render_scene_bounds(int scene, float bmin[3], float bmax[3]) {
 
 int nasg_render_destroy(nasg_render *r) {
     if (!r) return NASG_OK;
+    DeviceScope ds_(ctx_device(r->ctx));
     if (r->stream) cudaStreamSynchronize(r->stream);
     if (r->tstream) cudaStreamSynchronize(r->tstream);
     if (r->cfg.pipelined && r->ctx) ctx_set_pdl(r->ctx, true);
@@ -680,8 +693,22 @@ int nasg_render_destroy(nasg_render *r) {
 
 int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render **out) {
     if (!ctx || !cfg || !out) return NASG_ERR_INVALID;
+    DeviceScope ds_(ctx_device(ctx));
     *out = nullptr;
     nasg_render_config c = *cfg;
+    int band_rows = 0;  // rows owned with interleaving
+    if (c.row_band > 0) {
+        if (c.nshards < 1 || c.shard < 0 || c.shard >= c.nshards || c.height <= 0) return NASG_ERR_INVALID;
+        const int nb = (c.height + c.row_band - 1) / c.row_band;
+        for (int k = c.shard; k < nb; k += c.nshards) band_rows += std::min(c.height, (k + 1) * c.row_band) - k * c.row_band;
+        if (band_rows == 0) return NASG_ERR_INVALID;  // more shards than bands
+        c.row_begin = 0;
+        c.row_end = band_rows;
+    } else {
+        c.row_band = 0;
+        c.shard = 0;
+        c.nshards = 1;
+    }
     if (c.row_end <= 0) c.row_end = c.height;
     if (c.width <= 0 || c.height <= 0 || c.row_begin < 0 || c.row_end > c.height || c.row_begin >= c.row_end ||
         c.max_depth < 1 || c.max_depth > kMaxDepthCap || c.schedule_m < 1 || c.schedule_b < 1)
@@ -772,8 +799,11 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
     F.width = c.width;
     F.height = c.height;
     F.row0 = c.row_begin;
+    F.band = c.row_band;
+    F.shard = c.shard;
+    F.nshards = c.nshards;
     F.l = (float)r->l;
-    F.tile_row0 = (int)std::floor(c.row_begin / r->l);
+    F.tile_row0 = c.row_band > 0 ? 0 : (int)std::floor(c.row_begin / r->l);
     F.ntx = (int)std::ceil(c.width / r->l) + 1;
     F.collect = c.collect;
     F.max_depth = c.max_depth;
@@ -840,6 +870,7 @@ double blend_of(const nasg_render *r, int64_t iter) {
 
 int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
     if (!r) return NASG_ERR_INVALID;
+    DeviceScope ds_(ctx_device(r->ctx));
     const nasg_render_config &c = r->cfg;
     Paths &P = r->P;
     cudaStream_t s = r->stream;
@@ -944,6 +975,7 @@ int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
 
 int nasg_render_image(nasg_render *r, float *rgb, int which) {
     if (!r || !rgb) return NASG_ERR_INVALID;
+    DeviceScope ds_(ctx_device(r->ctx));
     const Paths &P = r->P;
     std::vector<float4> h((size_t)P.n);
     RCUDA(cudaMemcpyAsync(h.data(), which ? P.frame : P.film, P.n * sizeof(float4), cudaMemcpyDeviceToHost,

@@ -355,13 +355,29 @@ int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, 
 __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict__ m, float *__restrict__ v,
                             const float *__restrict__ g, float lr, float *__restrict__ wp, float *__restrict__ wtp,
                             __nv_bfloat16 *__restrict__ tc_img, int *nonfinite, int64_t *adam_t,
-                            const double *step_stats, double *acc, unsigned int *ticket) {
+                            const double *step_stats, double *acc, unsigned int *ticket, int recheck) {
     __shared__ int s_skip;
     __shared__ float s_c1, s_c2;
     pdl_trigger();
     pdl_wait();  // the reduced gradient, its non-finite flag and the step statistics
+    if (recheck) {
+        // data-parallel step: the skip decision (net.hpp:140-144) is taken on the
+        // allreduced gradient, identically on every rank.  Every block checks its
+        // slice into nonfinite[1], then a grid barrier (the launch is cooperative,
+        // so all blocks are co-resident) publishes the global verdict.
+        const int e0 = blockIdx.x * blockDim.x + threadIdx.x;
+        const int bad = e0 < n_weights(n_comp) && !isfinite(g[e0]);
+        if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(nonfinite + 1, 1);
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(ticket + 1, 1u);
+            while (*(volatile unsigned int *)(ticket + 1) < gridDim.x) __nanosleep(32);
+            __threadfence();
+        }
+        __syncthreads();
+    }
     if (threadIdx.x == 0) {
-        s_skip = *nonfinite != 0;
+        s_skip = *(volatile int *)(nonfinite + (recheck ? 1 : 0)) != 0;
         const int64_t t = *adam_t + 1;
         // corr = 1 - beta^t computed as powf would (float result), net.hpp:146-147
         s_c1 = 1.0f - (float)pow((double)0.9f, (double)(float)t);
@@ -411,7 +427,9 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
         if (atomicAdd(ticket, 1u) == gridDim.x - 1) {  // last block: every block has read flag and t
             const int sk = s_skip;
             if (!sk) *adam_t = *adam_t + 1;
-            *nonfinite = 0;
+            nonfinite[0] = 0;
+            nonfinite[1] = 0;
+            ticket[1] = 0;  // grid barrier of a recheck launch: every block is past it
             acc[0] += step_stats[0];
             acc[1] += step_stats[1];
             acc[2] += step_stats[2];
@@ -424,10 +442,10 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
 
 int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
                void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
-               unsigned int *ticket, cudaStream_t s, bool pdl) {
+               unsigned int *ticket, cudaStream_t s, bool pdl, bool recheck) {
     const int nw = n_weights(n_comp);
-    launch_pdl(pdl, adam_kernel, dim3((nw + 255) / 256), dim3(256), 0, s, n_comp, w, m, v, grad, lr, wp, wtp,
-               static_cast<__nv_bfloat16 *>(tc_img), nonfinite, adam_t, step_stats, acc, ticket);
+    launch_ex(pdl, recheck, adam_kernel, dim3((nw + 255) / 256), dim3(256), 0, s, n_comp, w, m, v, grad, lr, wp,
+               wtp, static_cast<__nv_bfloat16 *>(tc_img), nonfinite, adam_t, step_stats, acc, ticket, recheck ? 1 : 0);
     return 1;
 }
 

@@ -93,6 +93,10 @@ struct Nccl {
                               cudaStream_t) = nullptr;
     ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*commCount)(const ncclComm_t, int *) = nullptr;
+    ncclResult_t (*commCuDevice)(const ncclComm_t, int *) = nullptr;
     const char *(*errStr)(ncclResult_t) = nullptr;
     bool load() {
         if (h) return true;
@@ -105,7 +109,12 @@ struct Nccl {
         commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
         allGather = (decltype(allGather))dlsym(h, "ncclAllGather");
         errStr = (decltype(errStr))dlsym(h, "ncclGetErrorString");
-        return getUniqueId && commInitRank && allReduce && allGather && commDestroy;
+        groupStart = (decltype(groupStart))dlsym(h, "ncclGroupStart");
+        groupEnd = (decltype(groupEnd))dlsym(h, "ncclGroupEnd");
+        commCount = (decltype(commCount))dlsym(h, "ncclCommCount");
+        commCuDevice = (decltype(commCuDevice))dlsym(h, "ncclCommCuDevice");
+        return getUniqueId && commInitRank && allReduce && allGather && commDestroy && groupStart && groupEnd &&
+               commCount && commCuDevice;
     }
 };
 Nccl g_nccl;
@@ -169,16 +178,21 @@ struct nasg_ctx {
     // NCCL
     ncclComm_t comm = nullptr;
     bool comm_owned = true;
+    // per-iteration buffer-size exchange (allocated with the communicator)
+    int64_t *d_nall = nullptr, *h_nall = nullptr;
+    cudaEvent_t nall_ev = nullptr;
     bool pdl = true;  // programmatic dependent launch of the training chain
     bool query_pdl = false;  // ... and of the query kernels (serial render loop)  // false: attached by the caller (nasg_attach_nccl), not destroyed here
     int rank = 0, nranks = 1;
     uint64_t launches = 0;
+    uint64_t collectives = 0;  // NCCL launches (grouped exchange per step, allgather per iteration)
     cudaEvent_t pub_ev = nullptr;  // = pub[cur].ev
 };
 
 namespace nasg {
 int64_t ctx_sample_capacity(const nasg_ctx *c) { return c ? (int64_t)c->cfg.sample_capacity : 0; }
 int ctx_nranks(const nasg_ctx *c) { return c ? c->nranks : 1; }
+int ctx_device(const nasg_ctx *c) { return c ? c->device : 0; }
 }  // namespace nasg
 
 namespace {
@@ -376,18 +390,23 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
         CUDA_TRY(cudaMemsetAsync(c->d_step_stats, 0, 3 * sizeof(double), s));
     }
     CHECK_LAUNCH();
-    if (c->comm) {  // data-parallel exchange (any attached communicator, 1 rank included): sum of unnormalised-by-rank grads
+    if (c->comm) {
+        // data-parallel exchange (any attached communicator, 1 rank included): the
+        // sum of the ranks' unnormalised-by-rank gradients and step statistics, as
+        // ONE grouped NCCL launch per Adam step
+        ncclResult_t e0 = g_nccl.groupStart();
         ncclResult_t e1 = g_nccl.allReduce(c->grad, c->grad, c->nw, ncclFloat32, ncclSum, c->comm, s);
         ncclResult_t e2 = g_nccl.allReduce(c->d_step_stats, c->d_step_stats, 3, ncclFloat64, ncclSum, c->comm, s);
-        if (e1 != ncclSuccess || e2 != ncclSuccess) return fail(NASG_ERR_NCCL, "ncclAllReduce failed");
-        CUDA_TRY(cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int), s));
-        check_finite(c->grad, c->nw, c->d_nonfinite, s);
-        c->launches++;
+        ncclResult_t e3 = g_nccl.groupEnd();
+        if (e0 != ncclSuccess || e1 != ncclSuccess || e2 != ncclSuccess || e3 != ncclSuccess)
+            return fail(NASG_ERR_NCCL, "grouped ncclAllReduce failed");
+        c->collectives++;
     }
-    // skip decision, t, Adam, re-pack of every live image (the bf16 operands of
-    // the next step included) and the statistics, in one launch
+    // skip decision (re-taken on the reduced gradient when one was exchanged), t,
+    // Adam, re-pack of every live image (the bf16 operands of the next step
+    // included) and the statistics, in one launch
     train_adam(c->N, c->w, c->m, c->v, c->grad, c->cfg.learning_rate, c->wp, c->wtp, c->tc_live, c->d_nonfinite,
-               c->d_adam_t, c->d_step_stats, c->d_acc, c->d_ticket, s, c->pdl);
+               c->d_adam_t, c->d_step_stats, c->d_acc, c->d_ticket, s, c->pdl, c->comm != nullptr);
     c->launches += 1;
     CHECK_LAUNCH();
     return NASG_OK;
@@ -572,7 +591,7 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(NASG_ERR_INVALID, "bad device ordinal");
-    CUDA_TRY(cudaSetDevice(device));
+    DeviceScope ds_(device);  // the caller's current device is restored on return
     cudaDeviceProp prop{};
     CUDA_TRY(cudaGetDeviceProperties(&prop, device));
     if (prop.major != 10 || prop.minor != 0)
@@ -626,8 +645,8 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     if (tc_supported(c->N)) ALLOC(c->tc_live, tc_image_bytes(c->N));
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));
-    ALLOC(c->d_nonfinite, sizeof(int));
-    ALLOC(c->d_ticket, sizeof(unsigned int));
+    ALLOC(c->d_nonfinite, 2 * sizeof(int));
+    ALLOC(c->d_ticket, 2 * sizeof(unsigned int));
     ALLOC(c->d_step_stats, 3 * sizeof(double));
     ALLOC(c->d_acc, 5 * sizeof(double));
 #undef ALLOC
@@ -635,8 +654,8 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     cudaMemsetAsync(c->v, 0, wb, c->stream);
     cudaMemsetAsync(c->d_clamp, 0, sizeof(unsigned long long), c->stream);
     cudaMemsetAsync(c->d_adam_t, 0, sizeof(int64_t), c->stream);
-    cudaMemsetAsync(c->d_nonfinite, 0, sizeof(int), c->stream);
-    cudaMemsetAsync(c->d_ticket, 0, sizeof(unsigned int), c->stream);
+    cudaMemsetAsync(c->d_nonfinite, 0, 2 * sizeof(int), c->stream);
+    cudaMemsetAsync(c->d_ticket, 0, 2 * sizeof(unsigned int), c->stream);
     cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream);
     std::vector<float> w(c->nw);
     init_network(cfg->seed, c->N, w.data());
@@ -651,12 +670,14 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
 }
 
 int nasg_destroy(nasg_ctx *c) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c) return NASG_OK;
     join_prefetch(c);
-    cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->comm && c->comm_owned && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
-    void *bufs[] = {c->tc_live, c->tcb.h0, c->tcb.h1, c->tcb.h2, c->tcb.h3, c->tcb.d1, c->tcb.d2, c->tcb.d3,
+    if (c->h_nall) cudaFreeHost(c->h_nall);
+    if (c->nall_ev) cudaEventDestroy(c->nall_ev);
+    void *bufs[] = {c->d_nall, c->tc_live, c->tcb.h0, c->tcb.h1, c->tcb.h2, c->tcb.h3, c->tcb.d1, c->tcb.d2, c->tcb.d3,
                     c->tcb.d4, c->tcb.tile_loss, c->tcb.tile_lc, c->tcb.tile_dr, c->tcb.partial,
                     c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->pub[0].w, c->pub[0].wp, c->pub[0].tc,
                     c->pub[1].w, c->pub[1].wp, c->pub[1].tc, c->d_clamp,
@@ -684,6 +705,7 @@ int nasg_destroy(nasg_ctx *c) {
 }
 
 int nasg_set_weights(nasg_ctx *c, const float *host_w, size_t n) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
     if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
     CUDA_TRY(cudaDeviceSynchronize());  // training may be in flight on a caller stream
@@ -695,6 +717,7 @@ int nasg_set_weights(nasg_ctx *c, const float *host_w, size_t n) {
 }
 
 int nasg_get_weights(nasg_ctx *c, float *host_w, size_t n, int published) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
     if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
     CUDA_TRY(cudaDeviceSynchronize());  // host-synchronous getter: order after all caller streams
@@ -705,6 +728,7 @@ int nasg_get_weights(nasg_ctx *c, float *host_w, size_t n, int published) {
 }
 
 int nasg_publish(nasg_ctx *c) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c) return fail(NASG_ERR_INVALID, "null context");
     return do_publish(c);
 }
@@ -731,6 +755,7 @@ int nasg_get_train_precision(nasg_ctx *c) { return c ? c->train_precision : -1; 
 
 // NASGNET1 (net.cpp:31-82): magic, u32 N, u32 5, u32 dims[5], row-major f32 W1..W4.
 int nasg_save_checkpoint(nasg_ctx *c, const char *path) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || !path) return fail(NASG_ERR_INVALID, "null argument");
     std::vector<float> w(c->nw);
     int r = nasg_get_weights(c, w.data(), w.size(), 0);
@@ -752,6 +777,7 @@ int nasg_save_checkpoint(nasg_ctx *c, const char *path) {
 }
 
 int nasg_load_checkpoint(nasg_ctx *c, const char *path) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || !path) return fail(NASG_ERR_INVALID, "null argument");
     FILE *f = std::fopen(path, "rb");
     if (!f) return fail(NASG_ERR_IO, std::string("cannot open checkpoint: ") + path);
@@ -788,6 +814,7 @@ int nasg_load_checkpoint(nasg_ctx *c, const char *path) {
 // ---- queries --------------------------------------------------------------------
 int nasg_query_sample(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, const float *xi,
                       float *dir_pdf, float *cc, void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
     QueryArgs a = base_args(c, n);
     a.x = (const float4 *)x; a.wo = (const float4 *)wo; a.nrm = (const float4 *)nrm; a.xi = (const float4 *)xi;
@@ -796,6 +823,7 @@ int nasg_query_sample(nasg_ctx *c, int64_t n, const float *x, const float *wo, c
 }
 
 int nasg_query_sample_packed(nasg_ctx *c, int64_t n, const float *q13, float *dir_pdf, float *cc, void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!q13 || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
     QueryArgs a = base_args(c, n);
     a.packed = q13;
@@ -807,6 +835,7 @@ int nasg_query_sample_packed(nasg_ctx *c, int64_t n, const float *q13, float *di
 // Packed host rows (52 B/query in, 16 + 4 B out): the PCIe-lean form of
 // nasg_query_sample_host, same 3-lane H2D / kernel / D2H pipeline.
 int nasg_query_sample_host_packed(nasg_ctx *c, int64_t n, const float *q13, float *dir_pdf, float *cc) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!q13 || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
     if (n == 0) return NASG_OK;
     // 2^19-row chunks (27 MB in): 1.013e9 q/s from pinned rows on one B200,
@@ -845,6 +874,7 @@ int nasg_query_sample_host_packed(nasg_ctx *c, int64_t n, const float *q13, floa
 
 int nasg_query_pdf(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, const float *dir,
                    float b, const float *bsdf_pdf, float *mix_pdf, float *guided_pdf, void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !dir))) return fail(NASG_ERR_INVALID, "bad argument");
     QueryArgs a = base_args(c, n);
     a.x = (const float4 *)x; a.wo = (const float4 *)wo; a.nrm = (const float4 *)nrm; a.dir = (const float4 *)dir;
@@ -854,6 +884,7 @@ int nasg_query_pdf(nasg_ctx *c, int64_t n, const float *x, const float *wo, cons
 
 int nasg_query_shade(nasg_ctx *c, int64_t n, const int *n_dev, const float *x, const float *wo, const float *nrm,
                      const float *xi, const float *d_bsdf, const float *d_nee, float b, float *out, void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !xi || !d_bsdf || !d_nee || !out)))
         return fail(NASG_ERR_INVALID, "bad argument");
     QueryArgs a = base_args(c, n);
@@ -865,6 +896,7 @@ int nasg_query_shade(nasg_ctx *c, int64_t n, const int *n_dev, const float *x, c
 
 int nasg_query_raw(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm, float *raw,
                    void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !raw))) return fail(NASG_ERR_INVALID, "bad argument");
     QueryArgs a = base_args(c, n);
     a.x = (const float4 *)x; a.wo = (const float4 *)wo; a.nrm = (const float4 *)nrm; a.raw = raw;
@@ -873,6 +905,7 @@ int nasg_query_raw(nasg_ctx *c, int64_t n, const float *x, const float *wo, cons
 
 int nasg_decode_sample_raw(nasg_ctx *c, int64_t n, const float *raw, const float *xi, float *dir_pdf, float *cc,
                            void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!raw || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
     if (n == 0) return NASG_OK;
     if (decode_raw(c->N, true, c->precision == NASG_MLP_BF16, n, raw, (const float4 *)xi, nullptr, 0.f, nullptr, (float4 *)dir_pdf, cc, nullptr,
@@ -885,6 +918,7 @@ int nasg_decode_sample_raw(nasg_ctx *c, int64_t n, const float *raw, const float
 
 int nasg_decode_pdf_raw(nasg_ctx *c, int64_t n, const float *raw, const float *dir, float b, const float *bsdf_pdf,
                         float *mix_pdf, float *guided_pdf, void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!raw || !dir))) return fail(NASG_ERR_INVALID, "bad argument");
     if (n == 0) return NASG_OK;
     if (decode_raw(c->N, false, c->precision == NASG_MLP_BF16, n, raw, nullptr, (const float4 *)dir, b, bsdf_pdf, nullptr, nullptr, mix_pdf,
@@ -899,6 +933,7 @@ int nasg_decode_pdf_raw(nasg_ctx *c, int64_t n, const float *raw, const float *d
 // D2H(i), so copies in both directions overlap the kernels of other chunks.
 int nasg_query_sample_host(nasg_ctx *c, int64_t n, const float *x, const float *wo, const float *nrm,
                            const float *xi, float *dir_pdf, float *cc) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && (!x || !wo || !nrm || !xi || !dir_pdf))) return fail(NASG_ERR_INVALID, "bad argument");
     if (n == 0) return NASG_OK;
     const int64_t chunk = std::min<int64_t>(n, 1 << 19);
@@ -942,6 +977,7 @@ int nasg_query_sample_host(nasg_ctx *c, int64_t n, const float *x, const float *
 // ---- training -----------------------------------------------------------------------
 int nasg_train_step(nasg_ctx *c, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
                     int64_t global_count, double b, void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || count < 0 || global_count <= 0 || (count > 0 && !samples)) return fail(NASG_ERR_INVALID, "bad argument");
     cudaStream_t s = pick(c, stream);
     int r = train_step_impl(c, samples, order, count, global_count, b, s);
@@ -954,6 +990,7 @@ int nasg_train_step(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
 }
 
 int nasg_train_stats_take(nasg_ctx *c, nasg_train_stats *st) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || !st) return fail(NASG_ERR_INVALID, "null argument");
     // the training steps that fed the accumulators are ordered before c->stream
     CUDA_TRY(cudaMemcpyAsync(c->h_acc, c->d_acc, 5 * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -1021,6 +1058,7 @@ int nasg_dp_plan(const nasg_config *cfg, const int64_t *n_per_rank, int nranks, 
 // Trainer::train_iteration (guiding.cpp:196-282).
 int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *samples, double b,
                          nasg_train_stats *stats, void *stream) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || n < 0 || (n > 0 && !samples)) return fail(NASG_ERR_INVALID, "bad argument");
     cudaStream_t s = pick(c, stream);
     if (s != c->stream) {  // the context's own stream carries publish; order it after s
@@ -1038,15 +1076,16 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     // the same deterministic schedule (single rank: exactly guiding.cpp:204-276).
     std::vector<int64_t> n_all((size_t)c->nranks, 0);
     n_all[(size_t)c->rank] = n;
-    if (c->comm) {
-        int64_t *d_n = nullptr;
-        CUDA_TRY(cudaMalloc(&d_n, sizeof(int64_t) * c->nranks));
-        CUDA_TRY(cudaMemcpyAsync(d_n + c->rank, &n, sizeof(int64_t), cudaMemcpyHostToDevice, s));
-        if (g_nccl.allGather(d_n + c->rank, d_n, 1, ncclInt64, c->comm, s) != ncclSuccess)
+    if (c->comm) {  // buffers allocated with the communicator; one event wait, no device-wide sync
+        c->h_nall[c->rank] = n;
+        CUDA_TRY(cudaMemcpyAsync(c->d_nall + c->rank, c->h_nall + c->rank, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+        if (g_nccl.allGather(c->d_nall + c->rank, c->d_nall, 1, ncclInt64, c->comm, s) != ncclSuccess)
             return fail(NASG_ERR_NCCL, "ncclAllGather of buffer sizes failed");
-        CUDA_TRY(cudaMemcpyAsync(n_all.data(), d_n, sizeof(int64_t) * c->nranks, cudaMemcpyDeviceToHost, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
-        cudaFree(d_n);
+        c->collectives++;
+        CUDA_TRY(cudaMemcpyAsync(c->h_nall, c->d_nall, sizeof(int64_t) * c->nranks, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaEventRecord(c->nall_ev, s));
+        CUDA_TRY(cudaEventSynchronize(c->nall_ev));
+        std::copy(c->h_nall, c->h_nall + c->nranks, n_all.begin());
     }
     const int max_steps = c->cfg.step_factor * ((c->cfg.sample_capacity + c->cfg.batch_size - 1) / c->cfg.batch_size);
     std::vector<int64_t> local(max_steps), global(max_steps);
@@ -1123,6 +1162,7 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
 }
 
 int nasg_get_last_grad(nasg_ctx *c, float *host_g, size_t n) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || !host_g || n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "bad argument");
     CUDA_TRY(cudaDeviceSynchronize());
     CUDA_TRY(cudaMemcpyAsync(host_g, c->grad, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
@@ -1131,6 +1171,7 @@ int nasg_get_last_grad(nasg_ctx *c, float *host_g, size_t n) {
 }
 
 int64_t nasg_adam_t(nasg_ctx *c) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c) return -1;
     int64_t t = 0;
     if (cudaDeviceSynchronize() != cudaSuccess) return -1;
@@ -1149,43 +1190,76 @@ int nasg_comm_unique_id(void *out) {
     return NASG_OK;
 }
 
+namespace {
+// Binds `comm` (already created) as the context's communicator: the size
+// exchange buffers are (re)allocated first, so a failure leaves the previous
+// communicator and its rank/nranks in place.
+int bind_comm(nasg_ctx *c, ncclComm_t comm, bool owned, int rank, int nranks) {
+    int64_t *d = nullptr, *h = nullptr;
+    if (cudaMalloc(&d, sizeof(int64_t) * nranks) != cudaSuccess ||
+        cudaMallocHost(&h, sizeof(int64_t) * nranks) != cudaSuccess) {
+        cudaGetLastError();
+        if (d) cudaFree(d);
+        return fail(NASG_ERR_OOM, "communicator buffers");
+    }
+    if (!c->nall_ev && cudaEventCreateWithFlags(&c->nall_ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaFree(d);
+        cudaFreeHost(h);
+        return fail(NASG_ERR_CUDA, "event create failed");
+    }
+    cudaDeviceSynchronize();  // nothing may still use the old communicator
+    if (c->comm && c->comm_owned && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
+    if (c->d_nall) cudaFree(c->d_nall);
+    if (c->h_nall) cudaFreeHost(c->h_nall);
+    c->d_nall = d;
+    c->h_nall = h;
+    c->comm = comm;
+    c->comm_owned = owned;
+    c->rank = rank;
+    c->nranks = nranks;
+    return NASG_OK;
+}
+}  // namespace
+
 int nasg_comm_init(nasg_ctx *c, const void *uid, int rank, int nranks) {
     if (!c || !uid || nranks < 1 || rank < 0 || rank >= nranks) return fail(NASG_ERR_INVALID, "bad argument");
+    DeviceScope ds(c->device);
     {
         std::lock_guard<std::mutex> lk(g_nccl_mu);
         if (!g_nccl.load()) return fail(NASG_ERR_NCCL, "libnccl.so.2 not loadable");
     }
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
-    CUDA_TRY(cudaSetDevice(c->device));
-    if (c->comm && c->comm_owned && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
-    c->comm = nullptr;
-    ncclResult_t e = g_nccl.commInitRank(&c->comm, nranks, id, rank);
-    if (e != ncclSuccess) return fail(NASG_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(e) : ""));
-    c->comm_owned = true;
-    c->rank = rank;
-    c->nranks = nranks;
-    return NASG_OK;
+    ncclComm_t comm = nullptr;  // the old communicator stays bound until the new one exists
+    ncclResult_t e = g_nccl.commInitRank(&comm, nranks, id, rank);
+    if (e != ncclSuccess)
+        return fail(NASG_ERR_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errStr ? g_nccl.errStr(e) : ""));
+    int r = bind_comm(c, comm, true, rank, nranks);
+    if (r) g_nccl.commDestroy(comm);
+    return r;
 }
 
 int nasg_attach_nccl(nasg_ctx *c, void *comm, int rank, int nranks) {
     if (!c || nranks < 1 || rank < 0 || rank >= nranks || (nranks > 1 && !comm))
         return fail(NASG_ERR_INVALID, "bad argument");
     if (nranks == 1 && !comm) return NASG_OK;
+    DeviceScope ds(c->device);
     {
         std::lock_guard<std::mutex> lk(g_nccl_mu);
         if (!g_nccl.load()) return fail(NASG_ERR_NCCL, "libnccl.so.2 not loadable");
     }
-    if (c->comm && c->comm_owned && g_nccl.commDestroy) g_nccl.commDestroy(c->comm);
-    c->comm = static_cast<ncclComm_t>(comm);
-    c->comm_owned = false;
-    c->rank = rank;
-    c->nranks = nranks;
-    return NASG_OK;
+    int count = 0, dev = -1;
+    ncclComm_t cm = static_cast<ncclComm_t>(comm);
+    if (g_nccl.commCount(cm, &count) != ncclSuccess || g_nccl.commCuDevice(cm, &dev) != ncclSuccess)
+        return fail(NASG_ERR_NCCL, "cannot query the communicator");
+    if (count != nranks) return fail(NASG_ERR_INVALID, "communicator size != nranks");
+    if (dev != c->device) return fail(NASG_ERR_INVALID, "communicator is bound to another device");
+    return bind_comm(c, cm, false, rank, nranks);
 }
 
 // ---- counters / schedules ------------------------------------------------------------
 int nasg_get_counters(nasg_ctx *c, nasg_counters *out) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c || !out) return fail(NASG_ERR_INVALID, "null argument");
     CUDA_TRY(cudaSetDevice(c->device));
     CUDA_TRY(cudaDeviceSynchronize());
@@ -1199,10 +1273,12 @@ int nasg_get_counters(nasg_ctx *c, nasg_counters *out) {
     out->iterations = c->iterations;
     out->rank = c->rank;
     out->nranks = c->nranks;
+    out->collectives = c->collectives;
     return NASG_OK;
 }
 
 uint64_t nasg_encode_clamp_count(nasg_ctx *c) {
+    DeviceScope ds_(c ? c->device : -1);
     if (!c) return 0;
     unsigned long long v = 0;
     cudaStreamSynchronize(c->stream);
@@ -1212,6 +1288,7 @@ uint64_t nasg_encode_clamp_count(nasg_ctx *c) {
 }
 
 void nasg_reset_encode_clamp_count(nasg_ctx *c) {
+    DeviceScope ds_(c ? c->device : -1);
     if (c) cudaMemset(c->d_clamp, 0, sizeof(unsigned long long));
 }
 

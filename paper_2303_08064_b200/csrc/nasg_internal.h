@@ -29,6 +29,26 @@ __host__ __device__ constexpr int packed_width(int n) { return packed_header(n) 
 
 __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHidden * kHidden + kHidden * (8 * n + 1); }
 
+// Makes `dev` current for the scope of one C-ABI call and restores the caller's
+// device afterwards (one process may drive several contexts; a torch rank's
+// current device must not move under it).
+struct DeviceScope {
+    int prev = -1;
+    explicit DeviceScope(int dev) {
+        if (dev < 0) return;
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != dev) cudaSetDevice(dev);
+        else prev = -1;
+    }
+    ~DeviceScope() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+int ctx_device(const nasg_ctx *c);
+
 // context accessors for the render loop (k_render.cu; nasg_ctx is opaque there)
 int64_t ctx_sample_capacity(const nasg_ctx *c);  // TrainerConfig::sample_capacity S
 int ctx_nranks(const nasg_ctx *c);
@@ -95,10 +115,12 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // pdl = false launches normally (no early start): when other streams run
 // concurrent work (the pipelined render loop), early-started CTAs waiting in
 // griddepcontrol.wait would hold SMs that work could use.
+// cooperative = true additionally guarantees that every block of the grid is
+// resident at once (a kernel with an in-kernel grid barrier).
 template <class... KArgs, class... Args>
-inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                              Args &&...args) {
-    if (!pdl) {
+inline cudaError_t launch_ex(bool pdl, bool cooperative, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args &&...args) {
+    if (!pdl && !cooperative) {
         k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
         return cudaGetLastError();
     }
@@ -107,12 +129,25 @@ inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 blo
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na++].val.programmaticStreamSerializationAllowed = 1;
+    }
+    if (cooperative) {
+        at[na].id = cudaLaunchAttributeCooperative;
+        at[na++].val.cooperative = 1;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
+
+template <class... KArgs, class... Args>
+inline cudaError_t launch_pdl(bool pdl, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args &&...args) {
+    return launch_ex(pdl, false, k, grid, block, smem, s, std::forward<Args>(args)...);
 }
 
 __device__ __forceinline__ void load_query(const QueryArgs &a, int64_t q, float4 &x, float4 &wo, float4 &nrm) {
@@ -192,10 +227,13 @@ int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, 
 // acc[0..4] = loss_sum, loss_count, dropped, skipped, steps
 // Fused optimizer tail of one step (skip decision, t, bias corrections,
 // adam_step, re-pack of the fp32 images and of the bf16 image when tc_img is
-// set, statistics into acc, flag reset); ticket: a zeroed device counter.
+// set, statistics into acc, flag reset); nonfinite and ticket: 2 zeroed device
+// words each.  recheck: the gradient was allreduced, so the skip flag is
+// recomputed on it inside the launch (nonfinite[1], a grid barrier on
+// ticket[1]; cooperative launch).
 int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
                void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
-               unsigned int *ticket, cudaStream_t s, bool pdl = true);
+               unsigned int *ticket, cudaStream_t s, bool pdl = true, bool recheck = false);
 
 
 // ---- explicit mixtures and the fit (k_sphdist.cu) --------------------------

@@ -80,3 +80,17 @@ def test_create_without_gpu_fails_cleanly():
         pass
     with pytest.raises(nasg.NasgError):
         nasg.Guide()
+
+
+@pytest.mark.parametrize("kind", ["orc", "ref"])
+def test_synth_generators_match(kind, orc, request):
+    """The CPU checkers' generators are byte-identical to the library's, so the
+    reference arm of bench.py times the same inputs without loading the CUDA .so."""
+    o = orc if kind == "orc" else request.getfixturevalue("ref")
+    for seed, n, first, lo, hi in ((5, 3000, 0, (-1, -1, -1), (1, 1, 1)), (2024, 777, 123456, (-3, 0, 2), (5, 1, 9))):
+        a = nasg.synth_queries(seed, n, first=first, bmin=lo, bmax=hi)
+        b = o.synth_queries(seed, n, first=first, bmin=lo, bmax=hi)
+        for x, y in zip(a, b):
+            assert x.tobytes() == y.tobytes()
+        assert nasg.synth_samples(seed, n, first=first, bmin=lo, bmax=hi).tobytes() == \
+            o.synth_samples(seed, n, first=first, bmin=lo, bmax=hi).tobytes()
