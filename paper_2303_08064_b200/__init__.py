@@ -20,7 +20,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libnasg_b200.so")
+# NASG_LIB selects another build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("NASG_LIB") or os.path.join(_HERE, "lib", "libnasg_b200.so")
 
 NASG_MLP_FP32 = 0
 NASG_MLP_BF16 = 1
