@@ -111,6 +111,8 @@ def lib():
         "nasg_get_precision": (i32, [vp]),
         "nasg_set_train_precision": (i32, [vp, i32]),
         "nasg_get_train_precision": (i32, [vp]),
+        "nasg_set_zero_row_skip": (i32, [vp, i32]),
+        "nasg_get_zero_row_skip": (i32, [vp]),
         "nasg_save_checkpoint": (i32, [vp, C.c_char_p]),
         "nasg_load_checkpoint": (i32, [vp, C.c_char_p]),
         "nasg_query_sample": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp]),
@@ -329,6 +331,15 @@ class Guide:
     @train_precision.setter
     def train_precision(self, p: int):
         _check(lib().nasg_set_train_precision(self._h, int(p)))
+
+    @property
+    def zero_row_skip(self) -> bool:
+        """bf16 trainer: p = 0 rows counted without the network pass (nasg_set_zero_row_skip)."""
+        return lib().nasg_get_zero_row_skip(self._h) == 1
+
+    @zero_row_skip.setter
+    def zero_row_skip(self, on: bool):
+        _check(lib().nasg_set_zero_row_skip(self._h, 1 if on else 0))
 
     def save_checkpoint(self, path: str):
         _check(lib().nasg_save_checkpoint(self._h, path.encode()))

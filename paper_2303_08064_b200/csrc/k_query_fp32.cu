@@ -20,7 +20,7 @@ namespace nasg {
 // wp : W1[64][128] W2[128][128] W3[128][128] W4p[128][128] (packed cols)
 // wtp: W2^T[128][128] W3^T[128][128] W4p^T[128][128] (rows = packed col)
 __global__ void pack_fp32_kernel(const float *__restrict__ w, int n_comp, float *__restrict__ wp,
-                                 float *__restrict__ wtp) {
+                                 float *__restrict__ wtp, int *wbig) {
     const int D = 8 * n_comp + 1;
     const int NP = packed_width(n_comp);
     const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
@@ -43,6 +43,7 @@ __global__ void pack_fp32_kernel(const float *__restrict__ w, int n_comp, float 
             v = j >= 0 ? w[o3 + k * D + j] : 0.f;
         }
         wp[e] = v;
+        if (wbig && !(fabsf(v) < kSafeWeight)) atomicOr(wbig, 1);
         if (wtp && e >= o1) {  // transposed W2, W3, W4p
             const int l = e < o2 ? 0 : (e < o3 ? 1 : 2);
             const int base = l == 0 ? o1 : (l == 1 ? o2 : o3);
@@ -52,8 +53,8 @@ __global__ void pack_fp32_kernel(const float *__restrict__ w, int n_comp, float 
     }
 }
 
-void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStream_t s) {
-    pack_fp32_kernel<<<148, 256, 0, s>>>(w, n_comp, wp, wtp);
+void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStream_t s, int *wbig) {
+    pack_fp32_kernel<<<148, 256, 0, s>>>(w, n_comp, wp, wtp, wbig);
 }
 
 // ------------------------------------------------------------- encoding --

@@ -355,7 +355,7 @@ int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, 
 __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict__ m, float *__restrict__ v,
                             const float *__restrict__ g, float lr, float *__restrict__ wp, float *__restrict__ wtp,
                             __nv_bfloat16 *__restrict__ tc_img, int *nonfinite, int64_t *adam_t,
-                            const double *step_stats, double *acc, unsigned int *ticket, int recheck) {
+                            const double *step_stats, double *acc, unsigned int *ticket, int recheck, int *wbig) {
     __shared__ int s_skip;
     __shared__ float s_c1, s_c2;
     pdl_trigger();
@@ -397,6 +397,7 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
         m[e] = mi;
         v[e] = vi;
         w[e] = wi;
+        if (!(fabsf(wi) < kSafeWeight)) atomicOr(wbig, 1);  // sticky until the next host re-pack
         // re-pack (same mappings as pack_fp32_kernel and pack_tc_kernel)
         const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
         int l, n, k;  // layer, output column (packed for the last layer), input row
@@ -442,10 +443,10 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
 
 int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
                void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
-               unsigned int *ticket, cudaStream_t s, bool pdl, bool recheck) {
+               unsigned int *ticket, cudaStream_t s, bool pdl, bool recheck, int *wbig) {
     const int nw = n_weights(n_comp);
     launch_ex(pdl, recheck, adam_kernel, dim3((nw + 255) / 256), dim3(256), 0, s, n_comp, w, m, v, grad, lr, wp,
-               wtp, static_cast<__nv_bfloat16 *>(tc_img), nonfinite, adam_t, step_stats, acc, ticket, recheck ? 1 : 0);
+               wtp, static_cast<__nv_bfloat16 *>(tc_img), nonfinite, adam_t, step_stats, acc, ticket, recheck ? 1 : 0, wbig);
     return 1;
 }
 

@@ -66,6 +66,129 @@ __device__ __forceinline__ uint32_t gate_mask(uint32_t flags, int j) {
     return r;
 }
 
+// 128-row blocks of `rows` and how the dW GEMM spreads them over `splits`
+// CTAs (the same plan on the host and, for a classified step, on the device)
+__host__ __device__ __forceinline__ void split_plan(int64_t rows, int splits, int64_t &nb, int &bps) {
+    nb = (rows + 127) / 128;
+    bps = nb > 0 ? (int)((nb + splits - 1) / splits) : 0;
+}
+
+// ------------------------------------------------------------- classify --
+// Rows with p = 0 take the zero-gradient path of kl_loss_gradient
+// (guiding.cpp:112: zero gradient, valid) and loss_surrogate returns 0 for them
+// (:170), counted (:267-270): the network output of such a row is only needed
+// to decide "drop" when it is not finite (:247-250), which cannot happen while
+// every weight is below kSafeWeight and the row's inputs are finite with
+// |direction components| <= 2.  Those rows are counted and skipped; the rest
+// (in row order, as source indices through the epoch permutation) form the
+// step's list for K_fb and K_dw.  One pass, order-preserving, deterministic:
+// 1024 rows per block, block offsets by decoupled look-back.
+constexpr int kClsThreads = 256, kClsRpt = 4, kClsRows = kClsThreads * kClsRpt;
+constexpr int kClsEpochBits = 26, kClsValBits = 36;
+
+__device__ __forceinline__ bool finite_dir(float4 v) {
+    return fabsf(v.x) <= 2.f && fabsf(v.y) <= 2.f && fabsf(v.z) <= 2.f;  // false for NaN
+}
+
+__global__ void __launch_bounds__(kClsThreads)
+train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint32_t *__restrict__ order, int64_t count,
+                      const int *__restrict__ wbig, Bounds bd, uint32_t *__restrict__ live,
+                      unsigned long long *state, uint32_t epoch, int64_t *cls, unsigned long long *clamp_count) {
+    __shared__ int s_cnt[kClsRpt * 8], s_off[kClsRpt * 8];
+    __shared__ long long s_prefix;
+    __shared__ int s_clamped;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t base = (int64_t)blockIdx.x * kClsRows;
+    if (tid == 0) s_clamped = 0;
+    pdl_wait();  // samples, order and the last Adam step's weight flag
+    const bool big = *(volatile const int *)wbig != 0;
+    uint32_t src[kClsRpt];
+#pragma unroll
+    for (int i = 0; i < kClsRpt; ++i) {
+        const int64_t row = base + i * kClsThreads + tid;
+        src[i] = row < count ? (order ? order[row] : (uint32_t)row) : 0u;
+    }
+    float4 a[kClsRpt], o[kClsRpt], n[kClsRpt];
+#pragma unroll
+    for (int i = 0; i < kClsRpt; ++i) {
+        const int64_t row = base + i * kClsThreads + tid;
+        if (row < count) {
+            const float4 *sp = reinterpret_cast<const float4 *>(samples + src[i]);
+            a[i] = sp[0]; o[i] = sp[1]; n[i] = sp[2];
+        }
+    }
+    uint32_t bits = 0;
+    int clamped = 0;
+#pragma unroll
+    for (int i = 0; i < kClsRpt; ++i) {
+        const int64_t row = base + i * kClsThreads + tid;
+        bool lv = false;
+        if (row < count) {
+            const bool zero = !big && a[i].w == 0.f && isfinite(a[i].x) && isfinite(a[i].y) && isfinite(a[i].z) &&
+                              finite_dir(o[i]) && finite_dir(n[i]);
+            lv = !zero;
+            if (zero) {  // its encode is skipped too: count its clamped coordinates here
+                const float xs[3] = {a[i].x, a[i].y, a[i].z};
+#pragma unroll
+                for (int ax = 0; ax < 3; ++ax) {
+                    const float t = bd.inv_ext[ax] > 0.f ? (xs[ax] - bd.bmin[ax]) * bd.inv_ext[ax] : 0.5f;
+                    clamped += (t < 0.f || t > 1.f) ? 1 : 0;
+                }
+            }
+        }
+        const uint32_t bl = __ballot_sync(0xffffffffu, lv);
+        if (lane == 0) s_cnt[i * 8 + warp] = __popc(bl);
+        bits |= (lv ? 1u : 0u) << i;
+    }
+    if (clamped) atomicAdd(&s_clamped, clamped);
+    __syncthreads();
+    if (warp == 0) {  // (i, warp) counts in row order -> exclusive offsets; block total; look-back
+        const int v = s_cnt[lane];
+        int inc = v;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, inc, d);
+            if (lane >= d) inc += u;
+        }
+        s_off[lane] = inc - v;
+        const int total = __shfl_sync(0xffffffffu, inc, 31);
+        if (lane == 0) {
+            const unsigned long long tag = (unsigned long long)epoch << (kClsValBits + 2);
+            const unsigned long long kA = 1ull << kClsValBits, kP = 2ull << kClsValBits;
+            const unsigned long long vmask = (1ull << kClsValBits) - 1ull;
+            long long prefix = 0;
+            if (blockIdx.x == 0) {
+                atomicExch(state, tag | kP | (unsigned long long)total);
+            } else {
+                atomicExch(state + blockIdx.x, tag | kA | (unsigned long long)total);
+                for (int64_t j = (int64_t)blockIdx.x - 1;;) {
+                    const unsigned long long w = *(volatile unsigned long long *)(state + j);
+                    if ((w >> (kClsValBits + 2)) != epoch || !(w & (kA | kP))) continue;  // not yet published
+                    prefix += (long long)(w & vmask);
+                    if (w & kP) break;
+                    --j;
+                }
+                atomicExch(state + blockIdx.x, tag | kP | (unsigned long long)(prefix + total));
+            }
+            s_prefix = prefix;
+            if (blockIdx.x == gridDim.x - 1) {
+                cls[0] = prefix + total;
+                cls[1] = count - (prefix + total);
+            }
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && s_clamped && clamp_count) atomicAdd(clamp_count, (unsigned long long)s_clamped);
+    const int64_t p0 = s_prefix;
+#pragma unroll
+    for (int i = 0; i < kClsRpt; ++i) {
+        const bool lv = (bits >> i) & 1u;
+        const uint32_t bl = __ballot_sync(0xffffffffu, lv);
+        if (lv) live[p0 + s_off[i * 8 + warp] + __popc(bl & ((1u << lane) - 1u))] = src[i];
+    }
+    pdl_trigger();
+}
+
 }  // namespace
 
 size_t tc_train_block_bytes(int n_comp) {  // bf16 bytes per 128-row block over all 8 arrays
@@ -75,8 +198,8 @@ size_t tc_train_block_bytes(int n_comp) {  // bf16 bytes per 128-row block over 
 template <int N>
 __global__ void __launch_bounds__(kThreadsT, 1)
 train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__restrict__ samples,
-                   const uint32_t *__restrict__ order, int64_t count, double gscale, double b, double e, Bounds bd,
-                   TcTrainBufs tb, unsigned long long *clamp_count) {
+                   const uint32_t *__restrict__ order, int64_t count, const int64_t *live_count, double gscale,
+                   double b, double e, Bounds bd, TcTrainBufs tb, unsigned long long *clamp_count) {
     constexpr int NP = packed_width(N);
     constexpr uint32_t IMG = img_bytes(N);
     constexpr uint32_t A_OFF = align1k(IMG);
@@ -89,7 +212,6 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
     __shared__ int s_clamped;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t ntiles = (count + 127) / 128;
     if (threadIdx.x == 0) {
         for (int g = 0; g < kWGt; ++g) tc::mbar_init(&acc_full[g], 1);
         tc::mbar_init(w_bar, 1);
@@ -102,7 +224,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     pdl_trigger();
-    pdl_wait();  // the weight image and the samples come from earlier work on the stream
+    pdl_wait();  // the weight image, the samples and the classified rows come from earlier work on the stream
+    if (live_count) count = *live_count;  // rows that need the network (order = their list)
+    const int64_t ntiles = (count + 127) / 128;
 
     if (threadIdx.x == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
         tc::mbar_arrive_expect_tx(w_bar, IMG);
@@ -364,7 +488,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
 //   L0: A = delta1, B = h0 -> dW1^T   L1: A = h1, B = delta2 -> dW2
 //   L2: A = h2, B = delta3 -> dW3     L3: A = h3, B = delta4 -> dW4 (packed cols)
 __global__ void __launch_bounds__(128, 1)
-train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
+train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np, const int64_t *live_count) {
     extern __shared__ __align__(1024) uint8_t smem[];
     const int L = blockIdx.y;
     const uint8_t *A = L == 0 ? tb.d1 : (L == 1 ? tb.h1 : (L == 2 ? tb.h2 : tb.h3));
@@ -377,7 +501,6 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
     uint64_t *done = full + 4;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(full + 5);
     const int warp = threadIdx.x >> 5;
-    const int64_t b0 = (int64_t)blockIdx.x * bps, b1 = min(nblocks, b0 + bps);
     if (threadIdx.x == 0) {
         for (int s = 0; s < 2; ++s) {
             tc::mbar_init(&full[s], 1);
@@ -393,6 +516,8 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
     const uint32_t tmem = *tmem_slot;
     pdl_trigger();
     pdl_wait();  // the h / delta blocks of K_fb
+    if (live_count) split_plan(*live_count, gridDim.x, nblocks, bps);
+    const int64_t b0 = (int64_t)blockIdx.x * bps, b1 = min(nblocks, b0 + bps);
     if (threadIdx.x == 0 && b1 > b0) {
         const uint32_t idesc = tc::idesc_bf16(128, FB, true, true);
         auto load = [&](int64_t blk, int s) {
@@ -451,9 +576,18 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np) {
 // grid's extra last block reduces the per-tile loss / count / drop statistics
 // of the step (same fixed order as step_stats_kernel), saving a launch.
 __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, float *grad, int *nonfinite,
-                                       int ntiles) {
+                                       int ntiles, const int64_t *cls) {
     pdl_trigger();
     pdl_wait();  // K_dw's partials
+    double zero_rows = 0.0;
+    if (cls) {  // the classified step: live tiles, the splits that got blocks, rows skipped as zero-gradient
+        int64_t nb;
+        int bps;
+        split_plan(cls[0], splits, nb, bps);
+        ntiles = (int)nb;
+        splits = bps > 0 ? (int)((nb + bps - 1) / bps) : 0;
+        zero_rows = (double)cls[1];
+    }
     if (blockIdx.x == gridDim.x - 1) {
         __shared__ double sl[256], sc[256], sd[256];
         const int t = threadIdx.x;
@@ -473,9 +607,9 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
             }
             __syncthreads();
         }
-        if (t == 0) {
+        if (t == 0) {  // zero-gradient rows: loss 0, counted (guiding.cpp:170, :267-270)
             tb.step_stats[0] = sl[0];
-            tb.step_stats[1] = sc[0];
+            tb.step_stats[1] = sc[0] + zero_rows;
             tb.step_stats[2] = sd[0];
         }
         return;
@@ -506,31 +640,55 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
     if (n_comp != 8 && n_comp != 4) return -1;
     const int64_t ntiles = (count + 127) / 128;
     const double gscale = 1.0 / (double)global_count;
+    int launches = 0;
     if (ntiles > 0) {
+        // zero-gradient rows out of the network pass (train_classify_kernel): K_fb
+        // walks the list of the others, K_dw and the reduction size themselves
+        // from its length on the device.  Only when there are more tiles than
+        // SMs: below that every tile already has its own CTA (the step is one
+        // tile's latency chain) and the extra launch would only add to it.
+        const int64_t *live_count = nullptr;
+        const uint32_t *rows = order;
+        if (tb.skip_zero && ntiles > num_sms) {
+            const int nblk = (int)((count + kClsRows - 1) / kClsRows);
+            if (++tb.scan_epoch >= (1u << kClsEpochBits)) {  // look-back tags wrapped: start clean
+                cudaMemsetAsync(tb.scan_state, 0, tb.scan_cap * sizeof(unsigned long long), s);
+                tb.scan_epoch = 1;
+            }
+            launch_pdl(pdl, train_classify_kernel, dim3(nblk), dim3(kClsThreads), 0, s, samples, order, count, tb.wbig,
+                       bounds, tb.live, tb.scan_state, tb.scan_epoch, tb.cls, clamp_count);
+            live_count = tb.cls;
+            rows = tb.live;
+            ++launches;
+        }
         const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
         const uint8_t *im = static_cast<const uint8_t *>(img);
         if (n_comp == 8) {
             constexpr size_t sm = fb_smem<8>();
             cudaFuncSetAttribute(train_tc_fb_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(pdl, train_tc_fb_kernel<8>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, order, count, gscale, b,
-                       loss_blend, bounds, tb, clamp_count);
+            launch_pdl(pdl, train_tc_fb_kernel<8>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, rows, count,
+                       live_count, gscale, b, loss_blend, bounds, tb, clamp_count);
         } else {
             constexpr size_t sm = fb_smem<4>();
             cudaFuncSetAttribute(train_tc_fb_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(pdl, train_tc_fb_kernel<4>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, order, count, gscale, b,
-                       loss_blend, bounds, tb, clamp_count);
+            launch_pdl(pdl, train_tc_fb_kernel<4>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, rows, count,
+                       live_count, gscale, b, loss_blend, bounds, tb, clamp_count);
         }
+        int64_t nb;
+        int bps;
         int splits = (int)(ntiles < tb.splits ? ntiles : tb.splits);
-        const int bps = (int)((ntiles + splits - 1) / splits);
-        splits = (int)((ntiles + bps - 1) / bps);
+        split_plan(count, splits, nb, bps);
+        if (!live_count) splits = (int)((ntiles + bps - 1) / bps);  // every launched split gets blocks
         const size_t sm = 2 * 65536 + 64;
         cudaFuncSetAttribute(train_tc_dw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        launch_pdl(pdl, train_tc_dw_kernel, dim3(splits, 4), dim3(128), sm, s, tb, ntiles, bps, packed_width(n_comp));
+        launch_pdl(pdl, train_tc_dw_kernel, dim3(splits, 4), dim3(128), sm, s, tb, ntiles, bps, packed_width(n_comp),
+                   live_count);
         const int nw = n_weights(n_comp);
-        launch_pdl(pdl, train_tc_reduce_kernel, dim3((nw + 255) / 256 + 1), dim3(256), 0, s, tb, splits, n_comp, grad, nonfinite,
-                   (int)ntiles);
+        launch_pdl(pdl, train_tc_reduce_kernel, dim3((nw + 255) / 256 + 1), dim3(256), 0, s, tb, splits, n_comp, grad,
+                   nonfinite, (int)ntiles, live_count);
+        launches += 3;
     }
-    return 3;
+    return launches;
 }
 
 }  // namespace nasg

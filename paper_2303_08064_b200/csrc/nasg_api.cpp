@@ -153,6 +153,7 @@ struct nasg_ctx {
     // Adam / step state on device
     int64_t *d_adam_t = nullptr;
     int *d_nonfinite = nullptr;
+    int *d_wbig = nullptr;  // some live weight >= kSafeWeight or not finite (disables zero-row skipping)
     unsigned int *d_ticket = nullptr;  // last-block ticket of the fused Adam kernel
     cudaEvent_t xev = nullptr;  // reusable: orders the context stream after a caller stream
     double *h_acc = nullptr;    // pinned: TrainStats read-back (a D2H copy engine, never behind an upload)
@@ -303,7 +304,8 @@ int note_reader(nasg_ctx *c, cudaStream_t s) {
 }
 
 int repack_live(nasg_ctx *c) {
-    launch_pack_fp32(c->w, c->N, c->wp, c->wtp, c->stream);
+    CUDA_TRY(cudaMemsetAsync(c->d_wbig, 0, sizeof(int), c->stream));
+    launch_pack_fp32(c->w, c->N, c->wp, c->wtp, c->stream, c->d_wbig);
     c->launches++;
     if (c->tc_live) {
         launch_pack_tc(c->w, c->N, c->tc_live, c->stream);
@@ -334,6 +336,17 @@ int ensure_tc_scratch(nasg_ctx *c, int64_t count) {
         t.splits = 2 * 37;  // 4 layers x 74 splits ~ 2 waves over 148 SMs
         CUDA_TRY(cudaMalloc(&t.partial, (size_t)4 * t.splits * 128 * 128 * sizeof(float)));
     }
+    if (t.live) cudaFree(t.live);
+    if (t.scan_state) cudaFree(t.scan_state);
+    t.live = nullptr;
+    t.scan_state = nullptr;
+    t.scan_cap = (blocks * 128 + 1023) / 1024;
+    CUDA_TRY(cudaMalloc(&t.live, (size_t)blocks * 128 * sizeof(uint32_t)));
+    CUDA_TRY(cudaMalloc(&t.scan_state, (size_t)t.scan_cap * sizeof(unsigned long long)));
+    CUDA_TRY(cudaMemset(t.scan_state, 0, (size_t)t.scan_cap * sizeof(unsigned long long)));
+    t.scan_epoch = 0;
+    if (!t.cls) CUDA_TRY(cudaMalloc(&t.cls, 2 * sizeof(int64_t)));
+    t.wbig = c->d_wbig;
     t.step_stats = c->d_step_stats;
     t.max_blocks = blocks;
     return NASG_OK;
@@ -366,20 +379,23 @@ int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
 }
 
 // One minibatch step (guiding.cpp:236-276) on rows samples[order[0..count)].
+// count_clamps: the reference encodes every buffer row once per train_iteration
+// (guiding.cpp:209-214), so encode clamps are counted on a row's first-epoch visit only.
 int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
-                    int64_t global_count, double b, cudaStream_t s) {
+                    int64_t global_count, double b, cudaStream_t s, bool count_clamps = true) {
+    unsigned long long *clamp = count_clamps ? c->d_clamp : nullptr;
     if (count <= 0 && c->nranks == 1) return NASG_OK;
     const bool tc = c->train_precision == NASG_MLP_BF16;
     int r = tc ? ensure_tc_scratch(c, std::max<int64_t>(count, 1)) : ensure_scratch(c, std::max<int64_t>(count, 1));
     if (r) return r;
     if (count > 0 && tc) {
         const int k = train_tc_step(c->N, c->tc_live, samples, order, count, global_count, b, c->cfg.loss_blend,
-                                    c->bounds, c->tcb, c->num_sms, c->d_clamp, c->grad, c->d_nonfinite, s, c->pdl);
+                                    c->bounds, c->tcb, c->num_sms, clamp, c->grad, c->d_nonfinite, s, c->pdl);
         if (k < 0) return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for bf16 training");
         c->launches += k;
     } else if (count > 0) {
         if (train_forward_backward(c->N, c->wp, c->wtp, samples, order, count, global_count, b,
-                                   c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, c->d_clamp, s) < 0)
+                                   c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, clamp, s) < 0)
             return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for training");
         train_dw(c->N, count, c->sc, c->grad, s);
         train_reduce(c->N, c->sc, c->grad, c->d_nonfinite, s);
@@ -406,7 +422,7 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
     // Adam, re-pack of every live image (the bf16 operands of the next step
     // included) and the statistics, in one launch
     train_adam(c->N, c->w, c->m, c->v, c->grad, c->cfg.learning_rate, c->wp, c->wtp, c->tc_live, c->d_nonfinite,
-               c->d_adam_t, c->d_step_stats, c->d_acc, c->d_ticket, s, c->pdl, c->comm != nullptr);
+               c->d_adam_t, c->d_step_stats, c->d_acc, c->d_ticket, s, c->pdl, c->comm != nullptr, c->d_wbig);
     c->launches += 1;
     CHECK_LAUNCH();
     return NASG_OK;
@@ -646,6 +662,7 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));
     ALLOC(c->d_nonfinite, 2 * sizeof(int));
+    ALLOC(c->d_wbig, sizeof(int));
     ALLOC(c->d_ticket, 2 * sizeof(unsigned int));
     ALLOC(c->d_step_stats, 3 * sizeof(double));
     ALLOC(c->d_acc, 5 * sizeof(double));
@@ -655,6 +672,7 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     cudaMemsetAsync(c->d_clamp, 0, sizeof(unsigned long long), c->stream);
     cudaMemsetAsync(c->d_adam_t, 0, sizeof(int64_t), c->stream);
     cudaMemsetAsync(c->d_nonfinite, 0, 2 * sizeof(int), c->stream);
+    cudaMemsetAsync(c->d_wbig, 0, sizeof(int), c->stream);
     cudaMemsetAsync(c->d_ticket, 0, 2 * sizeof(unsigned int), c->stream);
     cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream);
     std::vector<float> w(c->nw);
@@ -679,6 +697,7 @@ int nasg_destroy(nasg_ctx *c) {
     if (c->nall_ev) cudaEventDestroy(c->nall_ev);
     void *bufs[] = {c->d_nall, c->tc_live, c->tcb.h0, c->tcb.h1, c->tcb.h2, c->tcb.h3, c->tcb.d1, c->tcb.d2, c->tcb.d3,
                     c->tcb.d4, c->tcb.tile_loss, c->tcb.tile_lc, c->tcb.tile_dr, c->tcb.partial,
+                    c->tcb.live, c->tcb.cls, c->tcb.scan_state, c->d_wbig,
                     c->w, c->m, c->v, c->grad, c->wp, c->wtp, c->pub[0].w, c->pub[0].wp, c->pub[0].tc,
                     c->pub[1].w, c->pub[1].wp, c->pub[1].tc, c->d_clamp,
                     c->d_adam_t, c->d_ticket, c->d_nonfinite, c->d_step_stats, c->d_acc, c->d_order,
@@ -752,6 +771,14 @@ int nasg_set_train_precision(nasg_ctx *c, int p) {
 }
 
 int nasg_get_train_precision(nasg_ctx *c) { return c ? c->train_precision : -1; }
+
+int nasg_set_zero_row_skip(nasg_ctx *c, int on) {
+    if (!c) return fail(NASG_ERR_INVALID, "null context");
+    c->tcb.skip_zero = on != 0;
+    return NASG_OK;
+}
+
+int nasg_get_zero_row_skip(nasg_ctx *c) { return c ? (c->tcb.skip_zero ? 1 : 0) : -1; }
 
 // NASGNET1 (net.cpp:31-82): magic, u32 N, u32 5, u32 dims[5], row-major f32 W1..W4.
 int nasg_save_checkpoint(nasg_ctx *c, const char *path) {
@@ -1134,7 +1161,9 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
     };
     if (stats) CUDA_TRY(cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), s));
     int64_t cursor = 0;
+    int epoch = 0;
     for (int step = 0; step < steps; ++step) {
+        if (resh[step] && step > 0) ++epoch;
         if (resh[step] && !whole) {
             r = reshuffle();
             if (r) return r;
@@ -1142,7 +1171,8 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
             CUDA_TRY(cudaEventRecord(c->order_ev[c->order_slot], s));
             cursor = 0;
         }
-        r = train_step_impl(c, samples, whole ? nullptr : c->d_order + cursor, local[step], global[step], b, s);
+        r = train_step_impl(c, samples, whole ? nullptr : c->d_order + cursor, local[step], global[step], b, s,
+                            epoch == 0);
         if (r) return r;
         cursor += local[step];
     }

@@ -70,7 +70,15 @@ struct Bounds {
 };
 
 // ---- kernels: packing -------------------------------------------------------
-void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStream_t s);
+// wbig (nullable) is OR-ed with 1 when a weight is not finite or |w| >= kSafeWeight
+void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStream_t s, int *wbig = nullptr);
+
+// Weight magnitude below which no forward pass can overflow for inputs with
+// |feature| <= 2 (one-blob bins in [0,1], pad 1, direction components <= 2):
+// |raw| <= 64 * 2 * 128^3 * B^4 = 2.7e36 < FLT_MAX at B = 1e7, bf16 rounding
+// of the activations included.  Zero-gradient rows skip the network only
+// while every weight is below it (train_classify_kernel).
+constexpr float kSafeWeight = 1e7f;
 // bf16 weight image for the tcgen05 kernel (smem image, UMMA core-matrix layout)
 size_t tc_image_bytes(int n_comp);
 void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s);
@@ -205,6 +213,15 @@ struct TcTrainBufs {
     float *partial;  // [4 layers][splits][128][128]
     int splits;
     int64_t max_blocks;
+    // zero-gradient row skipping (train_classify_kernel): the step's rows that
+    // need the network, in row order, and {live count, zero-row count}
+    bool skip_zero = true;
+    uint32_t *live = nullptr;
+    int64_t *cls = nullptr;
+    unsigned long long *scan_state = nullptr;  // decoupled look-back words, one per classify block
+    int64_t scan_cap = 0;
+    uint32_t scan_epoch = 0;
+    const int *wbig = nullptr;  // set while some weight is >= kSafeWeight (or not finite)
 };
 size_t tc_train_block_bytes(int n_comp);
 int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
@@ -233,7 +250,7 @@ int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, 
 // ticket[1]; cooperative launch).
 int train_adam(int n_comp, float *w, float *m, float *v, const float *grad, float lr, float *wp, float *wtp,
                void *tc_img, int *nonfinite, int64_t *adam_t, const double *step_stats, double *acc,
-               unsigned int *ticket, cudaStream_t s, bool pdl = true, bool recheck = false);
+               unsigned int *ticket, cudaStream_t s, bool pdl, bool recheck, int *wbig);
 
 
 // ---- explicit mixtures and the fit (k_sphdist.cu) --------------------------
