@@ -324,21 +324,45 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     e2e["frac_of_h2d_roofline"] = e2e["value"] / e2e["h2d_roofline_samples_per_s"]
     t = max_over_ranks(sum(times), ws)
     st = g.train_iteration(s, 1.0)
+    dense = None
+    if precision == "bf16":
+        # the same step with every row through the network (zero-row skip off):
+        # the dense rate, and the work the skip saves on this buffer
+        g.zero_row_skip = False
+        for i in range(3):
+            g.train_iteration(s, 1.0, stats=False)
+        torch.cuda.synchronize()
+        barrier(ws)
+        td = max_over_ranks(sum(time_events(lambda: g.train_iteration(s, 1.0, stats=False), args.train_steps,
+                                            stream)), ws)
+        dense = {"value": n * ws * args.train_steps / td, "unit": "samples/s",
+                 "ms_per_step": 1e3 * td / args.train_steps,
+                 "achieved_tflops": n * args.train_steps * FLOP_PER_SAMPLE / td / 1e12}
+        g.zero_row_skip = True
     g.close()
     rate = n * ws * args.train_steps / t
-    tf = rate / ws * FLOP_PER_SAMPLE / 1e12
+    # rows with p = 0 need no network pass (zero gradient, loss 0: guiding.cpp:112,170):
+    # the executed work is the live rows' 279,296 FLOP each
+    live = float(np.mean(s[:, 3].cpu().numpy() != 0.0)) if precision == "bf16" else 1.0
+    tf = rate / ws * live * FLOP_PER_SAMPLE / 1e12
     pk, pk_kind = peaks()
-    # algorithmic FLOP of the whole step (fwd + dW + delta, 279,296 per sample) against the
-    # bf16 tensor peak; the step also moves 1,696 B/sample of bf16 activations through HBM
-    # twice for the split-K dW GEMM (K_dw runs at ~94 % of HBM, profiles/r1_train_bf16_ncu.md)
+    # executed FLOP of the step (fwd + dW + delta, 279,296 per live sample) against the
+    # bf16 tensor peak; the step also moves 1,696 B per live sample of bf16 activations
+    # through HBM twice for the split-K dW GEMM (K_dw is HBM-bound, profiles/r1_train_bf16_ncu.md)
     roof = {"bound": "tensor" if precision == "bf16" else "fp32-ffma", "achieved": tf, "unit": "TFLOP/s",
             "peak": pk["bf16_tflops"] if precision == "bf16" else FP32_FFMA_TFLOPS,
-            "peak_kind": f"{pk_kind} bf16 burst" if precision == "bf16" else FP32_PEAK_KIND}
+            "peak_kind": f"{pk_kind} bf16 burst" if precision == "bf16" else FP32_PEAK_KIND,
+            "live_row_fraction": live,
+            "note": "FLOP counted for the rows that need the network (p != 0); the zero-gradient rows "
+                    "are classified and counted without it" if precision == "bf16" else "every row"}
     roof["frac"] = tf / roof["peak"]
-    return {"metric": f"train samples/s (config 3: 2^18 samples/step/GPU, fused fwd+KL+bwd+dW+Adam, {precision})",
-            "value": rate, "unit": "samples/s", "ms_per_step": 1e3 * t / args.train_steps,
-            "achieved_tflops": tf, "roofline": roof, "e2e": e2e, "dtype": precision,
-            "gpu_launches": launches, "last_mean_loss": st.mean_loss}
+    out = {"metric": f"train samples/s (config 3: 2^18 samples/step/GPU, fused fwd+KL+bwd+dW+Adam, {precision})",
+           "value": rate, "unit": "samples/s", "ms_per_step": 1e3 * t / args.train_steps,
+           "achieved_tflops": tf, "roofline": roof, "e2e": e2e, "dtype": precision,
+           "gpu_launches": launches, "last_mean_loss": st.mean_loss}
+    if dense:
+        out["dense_no_zero_row_skip"] = dense
+    return out
 
 
 def bench_config1(nasg, args, ws, rank):

@@ -52,6 +52,15 @@ if what in ("all", "train"):
             st = g.train_iteration(s, 0.5)
             torch.cuda.synchronize()
             g.close()
+    # a step with more tiles than SMs: the zero-row classification (look-back
+    # compaction) and the runtime-sized K_fb / K_dw / reduction
+    big = 160 * 128 + 77
+    s = torch.from_numpy(nasg.synth_samples(4, big)).cuda()
+    g = nasg.Guide(nasg.TrainerConfig(seed=2, sample_capacity=big, batch_size=big))
+    g.train_precision = nasg.NASG_MLP_BF16
+    g.train_iteration(s, 0.5)
+    torch.cuda.synchronize()
+    g.close()
     print("train ok")
 
 if what in ("all", "render"):
