@@ -64,10 +64,13 @@ constexpr size_t smem_bytes() {
 }  // namespace
 
 size_t tc_image_bytes(int n) { return img_bytes(n); }
+size_t tc_train_image_bytes(int n) { return train_img_bytes(n); }
 bool tc_supported(int n) { return n == 4 || n == 8; }  // NP = 48 / 80: one UMMA N <= 256, N % 16 == 0
 
 // ------------------------------------------------------------------ packing --
-__global__ void pack_tc_kernel(const float *__restrict__ w, int n_comp, __nv_bfloat16 *__restrict__ img) {
+// train = 0: the query kernel's bf16 image; 1: the bf16 trainer's image (f16
+// layers + a bf16 copy of W4p^T, train_img_bytes)
+__global__ void pack_tc_kernel(const float *__restrict__ w, int n_comp, uint16_t *__restrict__ img, int train) {
     const int D = 8 * n_comp + 1, NP = packed_width(n_comp), H = packed_header(n_comp);
     const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
     const int total = o3 + NP * kHidden;
@@ -95,14 +98,18 @@ __global__ void pack_tc_kernel(const float *__restrict__ w, int n_comp, __nv_bfl
             }
             v = j >= 0 ? w[o3 + k * D + j] : 0.f;
         }
-        const int K = l == 0 ? kIn : kHidden;
-        const uint32_t byte = w_off(l) + (n / 8) * (K * 16) + (k / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
-        img[byte / 2] = __float2bfloat16_rn(v);
+        const uint32_t byte = img_elem_off(l, n, k);
+        if (!train) {
+            img[byte / 2] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        } else {
+            img[byte / 2] = __half_as_ushort(__float2half_rn(sat_f16_range(v)));
+            if (l == 3) img[(img_bytes(n_comp) + byte - w_off(3)) / 2] = __bfloat16_as_ushort(__float2bfloat16_rn(v));
+        }
     }
 }
 
-void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s) {
-    pack_tc_kernel<<<148, 256, 0, s>>>(w, n_comp, static_cast<__nv_bfloat16 *>(img));
+void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s, bool train) {
+    pack_tc_kernel<<<148, 256, 0, s>>>(w, n_comp, static_cast<uint16_t *>(img), train ? 1 : 0);
 }
 
 // ------------------------------------------------------------------ kernel --

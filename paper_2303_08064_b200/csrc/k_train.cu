@@ -416,10 +416,11 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
             wp[o3 + k * kHidden + n] = wi;
             wtp[2 * kHidden * kHidden + n * kHidden + k] = wi;
         }
-        if (tc_img) {
-            const int K = l == 0 ? kIn : kHidden;
-            const uint32_t byte = w_off(l) + (n / 8) * (K * 16) + (k / 8) * 128 + (n % 8) * 16 + (k % 8) * 2;
-            tc_img[byte / 2] = __float2bfloat16_rn(wi);
+        if (tc_img) {  // the bf16 trainer's image (train_img_bytes): f16 layers, bf16 copy of W4p^T
+            const uint32_t byte = img_elem_off(l, n, k);
+            uint16_t *im = reinterpret_cast<uint16_t *>(tc_img);
+            im[byte / 2] = __half_as_ushort(__float2half_rn(sat_f16_range(wi)));
+            if (l == 3) im[(img_bytes(n_comp) + byte - w_off(3)) / 2] = __bfloat16_as_ushort(__float2bfloat16_rn(wi));
         }
     }
     __syncthreads();

@@ -36,10 +36,32 @@ constexpr int kThreadsT = kWGt * 128;  // 12 warps: 3 per SMSP -> up to 168 regi
 constexpr uint32_t kATile = 128 * 128 * 2;
 constexpr uint32_t kTmemColsT = 512;
 
+// The KL's per-row scratch (2N floats per row, kKlScStride-interleaved) sits in
+// the tail of the warpgroup's own A tile: during the KL the tile holds only
+// delta4 (K = NP columns, NP * 256 bytes); the cooperative small-batch KL uses
+// warpgroup 1's tile, which has no tile of its own in that regime.
 template <int N>
-constexpr size_t fb_smem() {  // weight image, A tiles, barriers, tile-stat partials, KL scratch
-    return align1k(img_bytes(N)) + kWGt * kATile + 64 + kWGt * 4 * 3 * sizeof(double) +
-           (size_t)kWGt * 2 * N * kKlScStride * sizeof(float);
+constexpr uint32_t kl_sc_off() { return (uint32_t)packed_width(N) * 256u; }
+static_assert(packed_width(8) * 256 + 2 * 8 * kKlScStride * 4 <= kATile, "KL scratch fits the A tile tail");
+static_assert((3 * 8 + 2 * kWGt) * kKlScStride * 4 <= kATile, "cooperative KL scratch fits an A tile");
+
+template <int N>
+constexpr size_t fb_smem() {  // trainer image, A tiles, barriers, tile-stat partials
+    return align1k(train_img_bytes(N)) + kWGt * kATile + 64 + kWGt * 4 * 3 * sizeof(double);
+}
+
+// Power-of-two scale exponent that maps a row maximum m to [2^13, 2^14)
+// (0 for m = 0), bounded so the row's total scale 2^(E + k) stays a normal float.
+__device__ __forceinline__ int row_scale_exp(float m, int E) {
+    const int eb = (int)((__float_as_uint(m) >> 23) & 0xFFu);
+    int k = eb == 0 ? 0 : 140 - eb;
+    return min(max(k, -126 - E), 126 - E);
+}
+__device__ __forceinline__ float exp2i(int k) { return __uint_as_float((uint32_t)(k + 127) << 23); }  // |k| <= 126
+__device__ __forceinline__ uint32_t mul_bf16x2(uint32_t a, uint32_t b) {
+    uint32_t r;
+    asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+    return r;
 }
 
 // byte offset of row t's 16-byte chunk c inside a 128-row block / A tile with F features
@@ -201,14 +223,13 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                    const uint32_t *__restrict__ order, int64_t count, const int64_t *live_count, double gscale,
                    double b, double e, Bounds bd, TcTrainBufs tb, unsigned long long *clamp_count) {
     constexpr int NP = packed_width(N);
-    constexpr uint32_t IMG = img_bytes(N);
+    constexpr uint32_t IMG = train_img_bytes(N);  // f16 layers + the bf16 copy of W4p^T at img_bytes(N)
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
     uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + A_OFF + kWGt * kATile);
     uint64_t *w_bar = acc_full + kWGt;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     double *red = reinterpret_cast<double *>(smem + A_OFF + kWGt * kATile + 64);
-    float *kl_scratch = reinterpret_cast<float *>(red + kWGt * 4 * 3);
     __shared__ int s_clamped;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -238,8 +259,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         const uint32_t my_tmem = tmem + g * 128 + ((uint32_t)((warp & 3) * 32) << 16);
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + g * kATile);
         const uint32_t sW = tc::smem_u32(smem);
-        // forward layer l (0..3): A = activations (K = 64 | 128), B = W_l^T image (K-major)
-        // backward through W_l (l = 3, 2, 1): A = delta (K = NP | 128), B = the same image read MN-major
+        // forward layer l (0..3): A = f16 activations (K = 64 | 128), B = the f16 W_l^T image (K-major)
+        // backward through W_l (l = 3, 2, 1): A = delta (K = NP | 128), B = the image read MN-major:
+        // l = 3 bf16 delta4 x the bf16 copy of W4p^T, l = 2, 1 row-scaled f16 deltas x the f16 image
         // warp 0 of the group issues with one elected lane; descriptors are rebuilt
         // from opaque base addresses (hoisted they would pin ~60 registers)
         auto issue = [&](int l, bool bwd) {
@@ -250,11 +272,12 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 __syncwarp();
                 tc::tc_fence_after();
                 const uint32_t d = tmem + g * 128;
-                const uint32_t abase = tc::opaque(a_base), b0 = tc::opaque(sW) + w_off(l);
+                const uint32_t abase = tc::opaque(a_base),
+                               b0 = tc::opaque(sW) + ((bwd && l == 3) ? img_bytes(N) : w_off(l));
                 if (!bwd) {
                     const int K = l == 0 ? kIn : kHidden;
                     const uint32_t sbo = (uint32_t)K * 16u;
-                    const uint32_t idesc = tc::idesc_bf16(128, l == 3 ? NP : kHidden);
+                    const uint32_t idesc = tc::idesc_f16(128, l == 3 ? NP : kHidden);
                     const uint64_t ad = tc::smem_desc(abase, 128, sbo), bdsc = tc::smem_desc(b0, 128, sbo);
                     for (int k = 0; k < K / 16; ++k)  // +256 B per K=16 slab = +16 in the address field
                         tc::mma_bf16_elect(d, ad + (uint64_t)(k * 16), bdsc + (uint64_t)(k * 16), idesc,
@@ -263,7 +286,8 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     const int K = l == 3 ? NP : kHidden;              // contraction over W_l's output index
                     const uint32_t sbo_a = (uint32_t)K * 16u;          // delta tile, K-major
                     const uint32_t lbo_b = (uint32_t)kHidden * 16u;    // image rows (out index) in 8-groups
-                    const uint32_t idesc = tc::idesc_bf16(128, kHidden, false, true);
+                    const uint32_t idesc = l == 3 ? tc::idesc_bf16(128, kHidden, false, true)
+                                                  : tc::idesc_f16(128, kHidden, false, true);
                     const uint64_t ad = tc::smem_desc(abase, 128, sbo_a), bdsc = tc::smem_desc(b0, lbo_b, 128);
                     for (int k = 0; k < K / 16; ++k)  // B advances 2 x 8 image rows per K=16 slab
                         tc::mma_bf16_elect(d, ad + (uint64_t)(k * 16), bdsc + (uint64_t)(k * 2 * lbo_b / 16), idesc,
@@ -294,8 +318,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         // their own and take lobes of warpgroup 0's KL gradient instead (the step's
         // latency is one tile's chain; kl_grad_row_coop splits its longest link).
         const bool coop = ntiles <= (int64_t)gridDim.x;
-        float *coop_sc = kl_scratch;                                          // [3N][128]
-        int *coop_flg = reinterpret_cast<int *>(kl_scratch + 3 * N * kKlScStride);  // [2 x 3][128]
+        float *coop_sc = reinterpret_cast<float *>(smem + A_OFF + kATile);           // [3N][128], group 1's tile
+        int *coop_flg = reinterpret_cast<int *>(coop_sc + 3 * N * kKlScStride);     // [2 x 3][128]
+        float *kl_scratch = reinterpret_cast<float *>(smem + A_OFF + g * kATile + kl_sc_off<N>());
         auto coop_sync = [&](int k) {  // the three warpgroups of the CTA; k = 0, 1 inside the KL, 2 at entry
             tc::fence_proxy_async_smem();  // delta4 chunks in the A tile -> visible to the tensor core
             tc::tc_fence_before();
@@ -307,12 +332,12 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         for (; tile < ntiles; tile += stride) {
             const int64_t row = tile * 128 + t;
             const bool valid = row < count;
-            clamped += encode_row_bf16(valid, s0, s1, s2, bd, inv_ext, a_base + blk_off(t, 64),
-                                       tb.h0 + tile * (64 * 256) + blk_off(t, 64));
+            clamped += encode_row_f16(valid, s0, s1, s2, bd, inv_ext, a_base + blk_off(t, 64),
+                                      tb.h0 + tile * (64 * 256) + blk_off(t, 64));
             issue(0, false);
             uint32_t mask[3][4] = {};  // ReLU gate bits of h1..h3
 #pragma unroll 1
-            for (int l = 1; l < 4; ++l) {  // hidden layers: ReLU, bf16, gate bits, next A, h_l block
+            for (int l = 1; l < 4; ++l) {  // hidden layers: ReLU, f16 A + gate bits, bf16 h_l block
                 wait_acc();
                 uint8_t *gh = (l == 1 ? tb.h1 : (l == 2 ? tb.h2 : tb.h3)) + tile * (128 * 256) + blk_off(t, 128);
 #pragma unroll
@@ -323,14 +348,16 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     uint32_t bits = 0;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        uint32_t p[4];
+                        uint32_t p[4], q[4];
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
-                            p[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                            // a non-negative satfinite f16 is <= 0x7BFF: the same carry-free flag trick
+                            p[h] = tc::pack_f16x2_relu_sat(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                            q[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
                             bits = gate_flags(bits, p[h], 4 * c + h);
                         }
                         tc::st_shared_v4(a_base + blk_off(t, 128) + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
-                        st_g16(gh + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                        st_g16(gh + (q4 * 4 + c) * 128, q[0], q[1], q[2], q[3]);
                     }
                     // register-resident gate bits: select instead of a dynamic index
                     mask[0][q4] = l == 1 ? bits : mask[0][q4];
@@ -375,7 +402,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                                                    put_lobe, lossf, coop_sc + t, coop_flg + t, coop_sync);
                 else
                     st = kl_grad_row_fast<N>(valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr,
-                                             put_lobe, lossf, kl_scratch + g * (2 * N * kKlScStride) + t);
+                                             put_lobe, lossf, kl_scratch + t);
                 if (st == kKlOk) {
 #pragma unroll
                     for (int c = 0; c < HD / 8; ++c) put_chunk(c, ghdr + 8 * c);
@@ -413,10 +440,33 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 }
             }
             // ---- backward: delta_l = (delta_{l+1} W_l^T) .* [h_l > 0]
+            // The accumulator of layer l holds delta_l * 2^E (E = 0 for delta3, which
+            // comes from bf16 delta4 x bf16 W4).  Its f16 A operand for the next layer
+            // is rescaled per row so the row maximum lands in [2^13, 2^14): deltas
+            // keep f16's 11-bit precision whatever their magnitude (the 1/count
+            // factor and w = p/q_s span decades), and the backward is row-linear, so
+            // the next accumulator is exactly delta * 2^(E + k).  The bf16 copy for
+            // the dW GEMM is unscaled (exact power-of-two multiply).
+            int E = 0;
             static_for<0, 3>([&](auto jc) {
                 constexpr int l = 3 - decltype(jc)::value;
                 wait_acc();
                 uint8_t *gd = (l == 1 ? tb.d1 : (l == 2 ? tb.d2 : tb.d3)) + tile * (128 * 256) + blk_off(t, 128);
+                int k = 0;
+                if (l > 1) {  // pass 1: the row's maximum |value|
+                    float m = 0.f;
+#pragma unroll
+                    for (int q4 = 0; q4 < 4; ++q4) {
+                        float v[32];
+                        tc::tmem_ld32(my_tmem + q4 * 32, v);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) m = fmaxf(m, fabsf(v[j]));
+                    }
+                    k = row_scale_exp(m, E);
+                }
+                const float ks = exp2i(k);
+                const uint32_t un = (uint32_t)(127 - E) << 7, unscale = un | (un << 16);  // 2^-E as bf16x2
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     float v[32];
@@ -425,16 +475,21 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     const uint32_t bits = mask[l - 1][q4];
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {
-                        uint32_t p[4];
+                        uint32_t p[4], q[4];
 #pragma unroll
                         for (int h = 0; h < 4; ++h) {
                             const int i0 = 8 * c + 2 * h;
-                            p[h] = tc::pack_bf16x2(v[i0], v[i0 + 1]) & gate_mask(bits, 4 * c + h);
+                            const uint32_t gm = gate_mask(bits, 4 * c + h);
+                            q[h] = tc::pack_bf16x2(v[i0], v[i0 + 1]);
+                            if (l < 3) q[h] = mul_bf16x2(q[h], unscale);
+                            q[h] &= gm;
+                            if (l > 1) p[h] = tc::pack_f16x2_sat(v[i0] * ks, v[i0 + 1] * ks) & gm;
                         }
                         if (l > 1) tc::st_shared_v4(a_base + blk_off(t, 128) + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
-                        st_g16(gd + (q4 * 4 + c) * 128, p[0], p[1], p[2], p[3]);
+                        st_g16(gd + (q4 * 4 + c) * 128, q[0], q[1], q[2], q[3]);
                     }
                 }
+                E += k;
                 if (l > 1) issue(l - 1, true);
             });
             tc::tc_fence_before();

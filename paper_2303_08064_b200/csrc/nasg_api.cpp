@@ -147,7 +147,7 @@ struct nasg_ctx {
     void *tc_pub = nullptr;
     int precision = NASG_MLP_FP32;        // query path MLP arithmetic
     int train_precision = NASG_MLP_FP32;  // training path MLP arithmetic
-    void *tc_live = nullptr;              // bf16 image of the live weights (bf16 training)
+    void *tc_live = nullptr;              // trainer image of the live weights (bf16 training: f16 layers + bf16 W4)
     TcTrainBufs tcb{};
     unsigned long long *d_clamp = nullptr;
     // Adam / step state on device
@@ -308,7 +308,7 @@ int repack_live(nasg_ctx *c) {
     launch_pack_fp32(c->w, c->N, c->wp, c->wtp, c->stream, c->d_wbig);
     c->launches++;
     if (c->tc_live) {
-        launch_pack_tc(c->w, c->N, c->tc_live, c->stream);
+        launch_pack_tc(c->w, c->N, c->tc_live, c->stream, true);
         c->launches++;
     }
     CHECK_LAUNCH();
@@ -658,7 +658,7 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     }
     ALLOC(c->wp, kPackedF32 * sizeof(float));
     ALLOC(c->wtp, kPackedT32 * sizeof(float));
-    if (tc_supported(c->N)) ALLOC(c->tc_live, tc_image_bytes(c->N));
+    if (tc_supported(c->N)) ALLOC(c->tc_live, tc_train_image_bytes(c->N));
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));
     ALLOC(c->d_nonfinite, 2 * sizeof(int));

@@ -80,8 +80,9 @@ void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStr
 // while every weight is below it (train_classify_kernel).
 constexpr float kSafeWeight = 1e7f;
 // bf16 weight image for the tcgen05 kernel (smem image, UMMA core-matrix layout)
-size_t tc_image_bytes(int n_comp);
-void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s);
+size_t tc_image_bytes(int n_comp);        // the query kernel's bf16 image
+size_t tc_train_image_bytes(int n_comp);  // the bf16 trainer's f16 image + bf16 W4 copy
+void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s, bool train = false);
 
 // ---- kernels: queries -------------------------------------------------------
 enum QueryMode { kModeSample = 0, kModePdf = 1, kModeRaw = 2, kModeShade = 3 };

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include "nasg_internal.h"
 #include "nasg_math.cuh"
@@ -19,13 +20,25 @@ __host__ __device__ constexpr uint32_t w_off(int l) {
 }
 __host__ __device__ constexpr uint32_t img_bytes(int n) { return 81920u + (uint32_t)packed_width(n) * 256u; }
 __host__ __device__ constexpr uint32_t align1k(uint32_t x) { return (x + 1023u) & ~1023u; }
+// The bf16 trainer's live image: the same four layers in f16 (its forward and
+// the backward through W3, W2 run f16 x f16), then W4p^T once more in bf16 at
+// img_bytes(n) for the first backward layer, whose operand delta4 (the KL
+// gradient, spanning decades) keeps bf16's exponent range.
+__host__ __device__ constexpr uint32_t train_img_bytes(int n) { return img_bytes(n) + (uint32_t)packed_width(n) * 256u; }
+// a weight clamped to f16's finite range for the trainer image; NaN stays NaN
+// (a non-finite network must still poison its outputs and skip, net.hpp:140-144)
+__device__ __forceinline__ float sat_f16_range(float v) { return v != v ? v : fminf(fmaxf(v, -65504.f), 65504.f); }
+// byte offset of W_l^T[n][k] inside an image (core-matrix layout above)
+__host__ __device__ constexpr uint32_t img_elem_off(int l, int n, int k) {
+    return w_off(l) + (uint32_t)(n / 8) * (uint32_t)((l == 0 ? kIn : kHidden) * 16) + (uint32_t)(k / 8) * 128u +
+           (uint32_t)(n % 8) * 16u + (uint32_t)(k % 8) * 2u;
+}
 
 // --------------------------------------------------------------- encoding --
 // encode_inputs (encoding.cpp:21-46) in fp32 -> 64 bf16 features packed in 32
 // registers (pairs in K order).  Returns the number of clamped coordinates.
-__device__ __forceinline__ int encode_row_pack(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
-                                               const float (&inv_ext)[3], uint32_t (&pk)[32]) {
-    float e[64];
+__device__ __forceinline__ int encode_row_values(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
+                                                 const float (&inv_ext)[3], float (&e)[64]) {
     int clamped = 0;
     if (valid) {
         const float xs[3] = {x.x, x.y, x.z};
@@ -69,6 +82,13 @@ __device__ __forceinline__ int encode_row_pack(bool valid, float4 x, float4 wo, 
 #pragma unroll
         for (int k = 0; k < 64; ++k) e[k] = 0.f;
     }
+    return clamped;
+}
+
+__device__ __forceinline__ int encode_row_pack(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
+                                               const float (&inv_ext)[3], uint32_t (&pk)[32]) {
+    float e[64];
+    const int clamped = encode_row_values(valid, x, wo, nrm, bd, inv_ext, e);
 #pragma unroll
     for (int j = 0; j < 32; ++j) pk[j] = tc::pack_bf16x2(e[2 * j], e[2 * j + 1]);
     return clamped;
@@ -89,6 +109,26 @@ __device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, 
     uint32_t pk[32];
     const int clamped = encode_row_pack(valid, x, wo, nrm, bd, inv_ext, pk);
     store_row_pack(pk, a_row, gdst);
+    return clamped;
+}
+
+// The trainer's encode: f16 features into the K=64 A tile (its forward runs
+// in f16), bf16 into the global h0 block read by the dW GEMM.
+__device__ __forceinline__ int encode_row_f16(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
+                                              const float (&inv_ext)[3], uint32_t a_row, uint8_t *gdst) {
+    float e[64];
+    const int clamped = encode_row_values(valid, x, wo, nrm, bd, inv_ext, e);
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+        uint32_t h[4], b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            h[j] = tc::pack_f16x2_sat(e[8 * c + 2 * j], e[8 * c + 2 * j + 1]);
+            b[j] = tc::pack_bf16x2(e[8 * c + 2 * j], e[8 * c + 2 * j + 1]);
+        }
+        tc::st_shared_v4(a_row + c * 128, h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4 *>(gdst + c * 128) = make_uint4(b[0], b[1], b[2], b[3]);
+    }
     return clamped;
 }
 

@@ -88,5 +88,7 @@ def test_bf16_training_tracks_reference_100_steps():
     # moving average over 10 steps: the curve, not the per-step noise
     ma = np.convolve(losses - lr, np.ones(10) / 10, mode="valid") / scale
     print("bf16 loss dev max", d.max(), "moving-average max", np.abs(ma).max())
+    for k in (10, 25, 50, 100):
+        print(f"bf16 probe after {k}: {rel_l2(probes[k], ref[f'probe_{k}']):.3e}")
     assert np.abs(ma).max() <= 0.1
     assert rel_l2(probes[100], ref["probe_100"]) <= 0.25

@@ -1,14 +1,24 @@
 """bf16 tensor-core training path (k_train_tc.cu).
 
-Stated bf16 training contract:
-  * the step computes exactly the bf16 pipeline it claims: bf16 activations,
-    double KL gradient of the fp32 raw outputs scaled by 1/count and rounded
-    to bf16, bf16 deltas through W^T with the ReLU gates, dW in fp32 from
-    bf16 operands — vs a numpy emulation of that pipeline, rel-L2 <= 2e-3
-    (accumulation order; one-ulp bf16 flips);
-  * vs the fp32 reference gradient: rel-L2 <= 0.35 (measured 0.13-0.22: bf16
-    activations and deltas, 8-bit mantissas, summed over thousands of rows
-    with cancellation);
+Stated training contract of the tensor-core trainer ("bf16" path: bf16
+deltas into the dW GEMM, f16 where f16's precision is the point):
+  * forward in f16 (f16 weights and activations, fp32 accumulation, ReLU on
+    the f16 conversion, saturating at +-65504), raw outputs fp32;
+  * KL gradient of the fp32 raw outputs (fp32 stable forms) scaled by
+    1/count, rounded to bf16 (delta4);
+  * delta3 = delta4 x W4^T with a bf16 copy of W4, then deltas carried in f16
+    with a per-row power-of-two scale (row maximum in [2^13, 2^14)) through
+    the f16 W3, W2;
+  * dW = h^T delta from bf16 copies of h and of the unscaled deltas, fp32
+    accumulation;
+    vs a numpy emulation of exactly that pipeline: rel-L2 <= 2e-3
+    (accumulation order; one-ulp flips);
+  * vs the fp32 reference gradient: rel-L2 <= 0.2 (emulated 0.012 / 0.12 for
+    these two inputs; the bf16 forward it replaced: 0.13-0.22).  What is left
+    is the KL gradient's conditioning, not the arithmetic of the trainer: the
+    f16 forward moves raw outputs by 5e-4 relative, and 99.8 % of the squared
+    dW difference at n = 2^15 comes from 8 rows whose per-row gradient changes
+    by up to 64 % under that perturbation;
   * the loss of a multi-iteration run tracks the fp32 reference within 6 %.
 """
 import numpy as np
@@ -42,21 +52,49 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-def emulate_bf16_step(orc, w, samples, b, count):
+def f16(x):
+    """Round-to-nearest-even to IEEE half, saturating at +-65504 (cvt.rn.satfinite)."""
+    x = np.clip(np.asarray(x, np.float32), -65504.0, 65504.0)
+    return x.astype(np.float16).astype(np.float64)
+
+
+def row_scale_exp(acc, E):
+    """k with max|row| * 2^k in [2^13, 2^14) (0 for a zero row), total scale kept normal."""
+    m = np.max(np.abs(acc.astype(np.float32)), axis=1)
+    eb = ((m.view(np.uint32) >> 23) & 0xFF).astype(np.int64)
+    k = np.where(eb == 0, 0, 140 - eb)
+    return np.clip(k, -126 - E, 126 - E)
+
+
+def emulate_tc_step(orc, w, samples, b, count):
     q9 = np.concatenate([samples[:, 0:3], samples[:, 4:7], samples[:, 8:11]], 1)
     enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
-    W = [bf16(x.astype(np.float32)).astype(np.float64) for x in split_w(w)]
-    hs = [bf16(enc).astype(np.float64)]
+    W = split_w(w)
+    W16 = [f16(x) for x in W]
+    W4b = bf16(W[3].astype(np.float32)).astype(np.float64)
+    a16 = [f16(enc)]                                  # f16 A operands of the forward
+    hb = [bf16(enc).astype(np.float64)]               # bf16 copies for dW
     for l in range(3):
-        hs.append(bf16(np.maximum(hs[-1] @ W[l], 0).astype(np.float32)).astype(np.float64))
-    raw = (hs[3] @ W[3]).astype(np.float32)
+        acc = (a16[-1] @ W16[l]).astype(np.float32)
+        a16.append(f16(np.maximum(acc, 0)))
+        hb.append(bf16(np.maximum(acc, 0)).astype(np.float64))
+    raw = (a16[3] @ W16[3]).astype(np.float32)
     g, ok, _ = orc.kl_grad(raw, samples, b)
-    d = bf16((g * (1.0 / count)).astype(np.float32)).astype(np.float64)
+    d4 = bf16((g * (1.0 / count)).astype(np.float32)).astype(np.float64)
     dw = [None] * 4
-    for l in (3, 2, 1, 0):
-        dw[l] = hs[l].T @ d
-        if l > 0:
-            d = bf16(((d @ W[l].T) * (hs[l] > 0)).astype(np.float32)).astype(np.float64)
+    dw[3] = hb[3].T @ d4
+    acc = (d4 @ W4b.T).astype(np.float32)             # delta3 (unscaled)
+    E = np.zeros(len(acc), np.int64)
+    for l in (2, 1, 0):
+        gate = a16[l + 1] > 0
+        d = bf16(acc).astype(np.float64) * np.exp2(-E)[:, None] * gate
+        dw[l] = hb[l].T @ d
+        if l == 0:
+            break
+        k = row_scale_exp(acc, E)
+        A = f16((acc * np.exp2(k)[:, None].astype(np.float32)).astype(np.float32)) * gate
+        E = E + k
+        acc = (A @ W16[l].T).astype(np.float32)
     return np.concatenate([x.ravel() for x in dw])
 
 
@@ -68,14 +106,15 @@ def test_tc_gradient_matches_bf16_emulation(orc, n):
     w0 = g.get_weights()
     g.train_step(torch.from_numpy(s).cuda(), None, n, n, 1.0)
     grad = g.last_grad()
-    emu = emulate_bf16_step(orc, w0, s, 1.0, n)
+    emu = emulate_tc_step(orc, w0, s, 1.0, n)
     assert rel_l2(grad, emu) <= 2e-3, rel_l2(grad, emu)
     # vs the fp32 reference pipeline
     q9 = np.concatenate([s[:, 0:3], s[:, 4:7], s[:, 8:11]], 1)
     enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
     gr, ok, loss = orc.kl_grad(orc.forward(w0, enc), s, 1.0)
     ref = orc.backward(w0, enc, (gr * (1.0 / n)).astype(np.float32))
-    assert rel_l2(grad, ref) <= 0.35, rel_l2(grad, ref)
+    print("dW rel-L2 vs emulation", rel_l2(grad, emu), "vs fp32 reference", rel_l2(grad, ref))
+    assert rel_l2(grad, ref) <= 0.2, rel_l2(grad, ref)
     st = g.train_stats_take()
     assert st.steps == 1 and abs(st.dropped_samples - int((~ok).sum())) <= max(2, n // 1000)
     g.close()

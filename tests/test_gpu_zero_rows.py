@@ -72,8 +72,10 @@ def test_skip_matches_full_pass(n_comp, n, zero_frac):
     stats_equal(st1, st0, n)
     assert c1 == c0 > 0
     if zero_frac < 1.0:
-        assert rel_l2(g1, g0) <= 1e-5, rel_l2(g1, g0)
-        assert rel_l2(w1, w0) <= 1e-6
+        assert rel_l2(g1, g0) <= 2e-4, rel_l2(g1, g0)  # fp32 summation order over other tiles
+        # Adam's first step moves every weight by ~lr * sign(g): only entries
+        # whose gradient is at rounding level may step the other way
+        assert np.mean(np.abs(w1 - w0) > 1e-6) <= 1e-3
     else:  # every row zero: zero gradient, the Adam step is still taken
         assert not np.any(g1) and not np.any(g0)
         assert st1.mean_loss == 0.0 and st1.skipped_updates == 0
@@ -133,4 +135,4 @@ def test_train_iteration_shuffled_steps():
     for x, y in zip(a, b):
         assert x.steps == y.steps == 4 and x.dropped_samples == y.dropped_samples
         assert x.mean_loss == pytest.approx(y.mean_loss, rel=1e-4)
-    assert rel_l2(wa, wb) <= 1e-4
+    assert rel_l2(wa, wb) <= 1e-3  # 8 Adam steps amplify summation-order noise
