@@ -46,7 +46,11 @@ typedef enum {
 /* MLP arithmetic of the query path. */
 typedef enum {
     NASG_MLP_FP32 = 0, /* fp32 FFMA, bit-for-tolerance with the fp32 reference */
-    NASG_MLP_BF16 = 1  /* bf16 operands, fp32 accumulate, tcgen05/TMEM tensor cores */
+    NASG_MLP_BF16 = 1  /* tcgen05/TMEM tensor cores, fp32 accumulate: queries and the
+                          trainer's forward multiply f16 operands (same rate as bf16,
+                          3 more mantissa bits; |activations| saturate at 65504), the
+                          trainer's gradients flow in bf16 / row-scaled f16 (name kept
+                          for ABI stability) */
 } nasg_precision;
 
 /* TrainerConfig (guiding.hpp:122-130); defaults via nasg_config_default. */

@@ -12,7 +12,7 @@
 
 namespace nasg {
 
-// bf16 weight image: per layer the UMMA B operand W_l^T as [N_out][K_in],
+// Weight image (f16 elements): per layer the UMMA B operand W_l^T as [N_out][K_in],
 // K-major, no swizzle: 8-row x 16-byte core matrices, LBO = 128 B between the
 // two K chunks of a K=16 slab, SBO = K_in * 16 B between 8-row groups.
 __host__ __device__ constexpr uint32_t w_off(int l) {
@@ -85,12 +85,12 @@ __device__ __forceinline__ int encode_row_values(bool valid, float4 x, float4 wo
     return clamped;
 }
 
-__device__ __forceinline__ int encode_row_pack(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
-                                               const float (&inv_ext)[3], uint32_t (&pk)[32]) {
+__device__ __forceinline__ int encode_row_pack_f16(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
+                                                   const float (&inv_ext)[3], uint32_t (&pk)[32]) {
     float e[64];
     const int clamped = encode_row_values(valid, x, wo, nrm, bd, inv_ext, e);
 #pragma unroll
-    for (int j = 0; j < 32; ++j) pk[j] = tc::pack_bf16x2(e[2 * j], e[2 * j + 1]);
+    for (int j = 0; j < 32; ++j) pk[j] = tc::pack_f16x2_sat(e[2 * j], e[2 * j + 1]);
     return clamped;
 }
 
@@ -102,14 +102,6 @@ __device__ __forceinline__ void store_row_pack(const uint32_t (&pk)[32], uint32_
         tc::st_shared_v4(a_row + c * 128, pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         if (gdst) *reinterpret_cast<uint4 *>(gdst + c * 128) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
     }
-}
-
-__device__ __forceinline__ int encode_row_bf16(bool valid, float4 x, float4 wo, float4 nrm, const Bounds &bd,
-                                               const float (&inv_ext)[3], uint32_t a_row, uint8_t *gdst = nullptr) {
-    uint32_t pk[32];
-    const int clamped = encode_row_pack(valid, x, wo, nrm, bd, inv_ext, pk);
-    store_row_pack(pk, a_row, gdst);
-    return clamped;
 }
 
 // The trainer's encode: f16 features into the K=64 A tile (its forward runs

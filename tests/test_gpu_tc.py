@@ -1,15 +1,17 @@
-"""GPU parity of the bf16 tensor-core (tcgen05/TMEM) query path.
+"""GPU parity of the tensor-core (tcgen05/TMEM) query path (NASG_MLP_BF16:
+kind::f16 UMMAs with f16 operands, fp32 accumulation).
 
-Stated bf16 contract, checked here:
-  * the tensor-core MLP computes exactly bf16(inputs) x bf16(weights) with fp32
-    accumulation and bf16 re-quantisation after each ReLU: vs a numpy emulation
-    of that arithmetic, >= 95 % of rows agree to 1e-4 (accumulation order) and
-    max |d raw| <= 3e-2 (one-ulp bf16 rounding flips of a hidden activation);
-  * vs the fp32 oracle: raw |d| p99 <= 1e-2 (random init);
+Stated contract, checked here:
+  * the tensor-core MLP computes exactly f16(inputs) x f16(weights) with fp32
+    accumulation and f16 re-quantisation after each ReLU: vs a numpy emulation
+    of that arithmetic, >= 90 % of rows agree to 1e-4 (accumulation order) and
+    max |d raw| <= 3e-3 (one-ulp f16 rounding flips of a hidden activation);
+  * vs the fp32 oracle: raw |d| p99 <= 2e-3 (measured 7e-4 at random init;
+    bf16 operands gave 1e-2);
   * K3 stage (fp32 epilogue) given identical raw outputs: direction and pdf
     within 1e-3 for all benign queries and >= 99.9 % of stress queries;
-  * end to end vs the oracle: pdf relative p50 <= 5e-3, lobe-selection
-    mismatch (|d dir| > 0.05) <= 1 %.
+  * end to end vs the oracle: pdf relative p50 <= 1e-3 (measured 3.4e-4),
+    lobe-selection mismatch (|d dir| > 0.05) <= 0.2 % (measured 0.03 %).
 """
 import numpy as np
 import pytest
@@ -43,16 +45,21 @@ def bf16(x):
     return r.astype(np.uint32).view(np.float32)
 
 
-def emulate_bf16_mlp(w, enc):
+def f16(x):
+    """Round-to-nearest-even to IEEE half (saturating at +-65504), as float64."""
+    return np.clip(np.asarray(x, np.float32), -65504.0, 65504.0).astype(np.float16).astype(np.float64)
+
+
+def emulate_tc_mlp(w, enc):
     dims = [64, 128, 128, 128, 65]
     Ws, off = [], 0
     for l in range(4):
         n = dims[l] * dims[l + 1]
-        Ws.append(bf16(w[off:off + n].reshape(dims[l], dims[l + 1])).astype(np.float64))
+        Ws.append(f16(w[off:off + n].reshape(dims[l], dims[l + 1])))
         off += n
-    h = bf16(enc).astype(np.float64)
+    h = f16(enc)
     for l in range(3):
-        h = bf16(np.maximum(h @ Ws[l], 0).astype(np.float32)).astype(np.float64)
+        h = f16(np.maximum(h @ Ws[l], 0).astype(np.float32))
     return (h @ Ws[3]).astype(np.float32)
 
 
@@ -65,23 +72,23 @@ def guide():
 
 
 @pytest.mark.parametrize("n", [1, 129, 385, 5000, (1 << 16) + 3])
-def test_tc_raw_matches_bf16_emulation(guide, orc, n):
+def test_tc_raw_matches_f16_emulation(guide, orc, n):
     rng = np.random.default_rng(n)
     q9 = H.queries(rng, n, outside=0.1)
     raw = guide.query_raw(*split_q(q9)).cpu().numpy()
     enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
     w = guide.get_weights(published=True)
-    emu = emulate_bf16_mlp(w, enc)
+    emu = emulate_tc_mlp(w, enc)
     err = np.abs(raw - emu)
-    # fp32 accumulation order only, except where a hidden activation sits on a
-    # bf16 rounding boundary and flips by one bf16 ulp (rare, bounded)
-    # (~5e-5 per activation, 384 activations per row -> a few % of rows)
+    # fp32 accumulation order only, except where a hidden activation sits on an
+    # f16 rounding boundary and flips by one f16 ulp (rare, bounded)
     rows_off = (err.max(axis=1) > 1e-4).mean()
-    assert rows_off <= 0.05, rows_off
-    assert err.max() <= 3e-2, err.max()
     fp32 = orc.forward(w, enc)
     d = np.abs(raw - fp32)
-    assert np.percentile(d, 99) <= 1e-2, np.percentile(d, 99)
+    print(f"n={n} rows off emulation {rows_off:.4f} max {err.max():.2e} vs fp32 p99 {np.percentile(d, 99):.2e}")
+    assert rows_off <= 0.1, rows_off  # measured 4-6 %
+    assert err.max() <= 3e-3, err.max()  # measured <= 1.2e-3
+    assert np.percentile(d, 99) <= 2e-3, np.percentile(d, 99)
 
 
 def test_tc_clamp_counter(guide, orc):
@@ -128,10 +135,12 @@ def test_tc_query_sample_end_to_end(guide, orc):
     ref, cref = orc.query_sample(guide.get_weights(published=True), q9, xi, threads=8)
     ddir = np.linalg.norm(out[:, :3] - ref[:, :3], axis=1)
     same = ddir <= 0.05
-    assert 1 - same.mean() <= 0.01, 1 - same.mean()
     dpdf = np.abs(out[same, 3] - ref[same, 3]) / ref[same, 3]
-    assert np.median(dpdf) <= 5e-3, np.median(dpdf)
-    assert np.abs(c.cpu().numpy() - cref).max() <= 2e-2
+    print(f"lobe mismatch {1 - same.mean():.2e} pdf p50 {np.median(dpdf):.2e} p99 {np.percentile(dpdf, 99):.2e} "
+          f"c max {np.abs(c.cpu().numpy() - cref).max():.2e}")
+    assert 1 - same.mean() <= 2e-3, 1 - same.mean()
+    assert np.median(dpdf) <= 1e-3, np.median(dpdf)
+    assert np.abs(c.cpu().numpy() - cref).max() <= 5e-3
 
 
 def test_tc_query_pdf_consistent_with_sample(guide):
@@ -165,6 +174,7 @@ def test_tc_matches_fp32_path_statistically(guide):
     b, _ = guide.query_sample(*dev)
     guide.precision = nasg.NASG_MLP_BF16
     same = (a[:, :3] - b[:, :3]).norm(dim=1) < 0.05
-    assert same.float().mean().item() >= 0.99
     rel = ((a[same, 3] - b[same, 3]).abs() / b[same, 3]).median().item()
-    assert rel <= 5e-3
+    print(f"tc vs fp32 path: same lobe {same.float().mean().item():.5f} pdf p50 {rel:.2e}")
+    assert same.float().mean().item() >= 0.998
+    assert rel <= 1e-3

@@ -79,7 +79,8 @@ def test_fp32_training_tracks_reference_100_steps():
 
 
 def test_bf16_training_tracks_reference_100_steps():
-    """The bf16 tensor-core trainer follows the same loss curve within a few %."""
+    """The tensor-core trainer follows the reference's curve and, on the probe
+    set, stays within 3x of the reference's own reassociation drift."""
     ref = _load("train_curve_ref.npz")
     lr = ref["losses"]
     losses, probes = run_curve(nasg.NASG_MLP_BF16, len(lr), ref["probe_q9"])
@@ -90,5 +91,12 @@ def test_bf16_training_tracks_reference_100_steps():
     print("bf16 loss dev max", d.max(), "moving-average max", np.abs(ma).max())
     for k in (10, 25, 50, 100):
         print(f"bf16 probe after {k}: {rel_l2(probes[k], ref[f'probe_{k}']):.3e}")
-    assert np.abs(ma).max() <= 0.1
-    assert rel_l2(probes[100], ref["probe_100"]) <= 0.25
+    # f16 forward / scaled f16 backward (k_train_tc.cu): measured moving-average
+    # deviation 2.9 %, probe rel-L2 0.060 / 0.089 / 0.099 / 0.133 after
+    # 10 / 25 / 50 / 100 steps vs the reversed-sum reference's 0.031 / 0.090 /
+    # 0.102 / 0.126 (the fp32 trainer: 0.040 / 0.098 / 0.107 / 0.131)
+    assert np.abs(ma).max() <= 0.06
+    rev = _load("train_curve_rev.npz")
+    for k in (10, 25, 50, 100):
+        dr = rel_l2(rev[f"probe_{k}"], ref[f"probe_{k}"])
+        assert rel_l2(probes[k], ref[f"probe_{k}"]) <= 3 * dr + 1e-3, k
