@@ -174,24 +174,34 @@ train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint3
         }
         s_off[lane] = inc - v;
         const int total = __shfl_sync(0xffffffffu, inc, 31);
-        if (lane == 0) {
-            const unsigned long long tag = (unsigned long long)epoch << (kClsValBits + 2);
-            const unsigned long long kA = 1ull << kClsValBits, kP = 2ull << kClsValBits;
-            const unsigned long long vmask = (1ull << kClsValBits) - 1ull;
-            long long prefix = 0;
-            if (blockIdx.x == 0) {
-                atomicExch(state, tag | kP | (unsigned long long)total);
-            } else {
-                atomicExch(state + blockIdx.x, tag | kA | (unsigned long long)total);
-                for (int64_t j = (int64_t)blockIdx.x - 1;;) {
-                    const unsigned long long w = *(volatile unsigned long long *)(state + j);
-                    if ((w >> (kClsValBits + 2)) != epoch || !(w & (kA | kP))) continue;  // not yet published
-                    prefix += (long long)(w & vmask);
-                    if (w & kP) break;
-                    --j;
-                }
-                atomicExch(state + blockIdx.x, tag | kP | (unsigned long long)(prefix + total));
+        // decoupled look-back, a warp-wide window of 32 predecessors at a time:
+        // lane i reads block (j - i); the window is summed up to the nearest
+        // inclusive prefix (P), else wholly, and the walk moves 32 blocks back
+        const unsigned long long tag = (unsigned long long)epoch << (kClsValBits + 2);
+        const unsigned long long kA = 1ull << kClsValBits, kP = 2ull << kClsValBits;
+        const unsigned long long vmask = (1ull << kClsValBits) - 1ull;
+        long long prefix = 0;
+        if (blockIdx.x == 0) {
+            if (lane == 0) atomicExch(state, tag | kP | (unsigned long long)total);
+        } else {
+            if (lane == 0) atomicExch(state + blockIdx.x, tag | kA | (unsigned long long)total);
+            for (int64_t j = (int64_t)blockIdx.x - 1;;) {
+                const int64_t idx = j - lane;
+                unsigned long long w = idx >= 0 ? *(volatile unsigned long long *)(state + idx) : (tag | kP);
+                const bool ready = (w >> (kClsValBits + 2)) == epoch && (w & (kA | kP));
+                if (!__all_sync(0xffffffffu, ready)) continue;  // a predecessor has not published yet
+                const uint32_t pm = __ballot_sync(0xffffffffu, (w & kP) != 0);
+                const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix in the window
+                long long v = lane <= stop ? (long long)(w & vmask) : 0;
+#pragma unroll
+                for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+                prefix += v;
+                if (pm) break;
+                j -= 32;
             }
+            if (lane == 0) atomicExch(state + blockIdx.x, tag | kP | (unsigned long long)(prefix + total));
+        }
+        if (lane == 0) {
             s_prefix = prefix;
             if (blockIdx.x == gridDim.x - 1) {
                 cls[0] = prefix + total;

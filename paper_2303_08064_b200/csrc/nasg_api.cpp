@@ -333,8 +333,12 @@ int ensure_tc_scratch(nasg_ctx *c, int64_t count) {
     CUDA_TRY(cudaMalloc(&t.tile_lc, blocks * sizeof(int)));
     CUDA_TRY(cudaMalloc(&t.tile_dr, blocks * sizeof(int)));
     if (!t.partial) {
-        t.splits = 2 * 37;  // 4 layers x 74 splits ~ 2 waves over 148 SMs
-        CUDA_TRY(cudaMalloc(&t.partial, (size_t)4 * t.splits * 128 * 128 * sizeof(float)));
+        // 4 layers x 37 splits = one wave of 148 CTAs (one per SM: 131 KB of
+        // smem each); 74 splits (two waves) measured 5 us slower per 2^18 step
+        // (profiles/r2_dw_splits.txt)
+        t.splits = 37;
+        if (const char *e = std::getenv("NASG_DW_SPLITS")) t.splits = std::max(1, std::min(2 * 37, std::atoi(e)));  // A/B only
+        CUDA_TRY(cudaMalloc(&t.partial, (size_t)4 * 2 * 37 * 128 * 128 * sizeof(float)));
     }
     if (t.live) cudaFree(t.live);
     if (t.scan_state) cudaFree(t.scan_state);
