@@ -122,8 +122,14 @@ int nasg_get_train_precision(nasg_ctx *ctx);
  * Default on. */
 int nasg_set_zero_row_skip(nasg_ctx *ctx, int on);
 int nasg_get_zero_row_skip(nasg_ctx *ctx);
-/* save_checkpoint / load_checkpoint (net.hpp:163-167, net.cpp:31-82): NASGNET1. */
+/* save_checkpoint / load_checkpoint (net.hpp:163-167, net.cpp:31-82): NASGNET1,
+ * byte-identical with the reference's file.  nasg_save_checkpoint_ex with
+ * NASG_CKPT_OPTIMIZER appends the Adam state (t, m, v) as a trailing chunk the
+ * reference's loader skips; nasg_load_checkpoint restores it when present (the
+ * reference persists weights only, so its resume restarts Adam). */
+enum { NASG_CKPT_OPTIMIZER = 1 };
 int nasg_save_checkpoint(nasg_ctx *ctx, const char *path);
+int nasg_save_checkpoint_ex(nasg_ctx *ctx, const char *path, int flags);
 int nasg_load_checkpoint(nasg_ctx *ctx, const char *path);
 
 /* ---- queries (device buffers; read the published snapshot) -------------- */

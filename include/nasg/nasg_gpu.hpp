@@ -88,7 +88,9 @@ public:
         return w;
     }
     void set_parameters(std::span<const float> w) { check(nasg_set_weights(ctx_, w.data(), w.size())); }
-    void save_checkpoint(const std::string &p) { check(nasg_save_checkpoint(ctx_, p.c_str())); }
+    void save_checkpoint(const std::string &p, bool optimizer = false) {
+        check(optimizer ? nasg_save_checkpoint_ex(ctx_, p.c_str(), NASG_CKPT_OPTIMIZER) : nasg_save_checkpoint(ctx_, p.c_str()));
+    }
     void load_checkpoint(const std::string &p) { check(nasg_load_checkpoint(ctx_, p.c_str())); }
 
     nasg_ctx *handle() { return ctx_; }

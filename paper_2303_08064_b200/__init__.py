@@ -114,6 +114,7 @@ def lib():
         "nasg_set_zero_row_skip": (i32, [vp, i32]),
         "nasg_get_zero_row_skip": (i32, [vp]),
         "nasg_save_checkpoint": (i32, [vp, C.c_char_p]),
+        "nasg_save_checkpoint_ex": (i32, [vp, C.c_char_p, i32]),
         "nasg_load_checkpoint": (i32, [vp, C.c_char_p]),
         "nasg_query_sample": (i32, [vp, i64, vp, vp, vp, vp, vp, vp, vp]),
         "nasg_query_pdf": (i32, [vp, i64, vp, vp, vp, vp, f32, vp, vp, vp, vp]),
@@ -341,8 +342,12 @@ class Guide:
     def zero_row_skip(self, on: bool):
         _check(lib().nasg_set_zero_row_skip(self._h, 1 if on else 0))
 
-    def save_checkpoint(self, path: str):
-        _check(lib().nasg_save_checkpoint(self._h, path.encode()))
+    def save_checkpoint(self, path: str, optimizer: bool = False):
+        """NASGNET1 weights; optimizer=True appends the Adam state (nasg_save_checkpoint_ex)."""
+        if optimizer:
+            _check(lib().nasg_save_checkpoint_ex(self._h, path.encode(), 1))
+        else:
+            _check(lib().nasg_save_checkpoint(self._h, path.encode()))
 
     def load_checkpoint(self, path: str):
         _check(lib().nasg_load_checkpoint(self._h, path.encode()))

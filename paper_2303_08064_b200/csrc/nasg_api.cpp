@@ -785,12 +785,27 @@ int nasg_set_zero_row_skip(nasg_ctx *c, int on) {
 int nasg_get_zero_row_skip(nasg_ctx *c) { return c ? (c->tcb.skip_zero ? 1 : 0) : -1; }
 
 // NASGNET1 (net.cpp:31-82): magic, u32 N, u32 5, u32 dims[5], row-major f32 W1..W4.
-int nasg_save_checkpoint(nasg_ctx *c, const char *path) {
+// With NASG_CKPT_OPTIMIZER the Adam state follows as a trailing chunk
+// ("NASGADM1", u64 t, u32 n, f32 m[n], f32 v[n]); the reference's loader reads
+// the weights and ignores what follows them (net.cpp:54-82), so such a file
+// still loads there.
+int nasg_save_checkpoint(nasg_ctx *c, const char *path) { return nasg_save_checkpoint_ex(c, path, 0); }
+
+int nasg_save_checkpoint_ex(nasg_ctx *c, const char *path, int flags) {
     DeviceScope ds_(c ? c->device : -1);
     if (!c || !path) return fail(NASG_ERR_INVALID, "null argument");
-    std::vector<float> w(c->nw);
+    if (flags & ~NASG_CKPT_OPTIMIZER) return fail(NASG_ERR_INVALID, "unknown checkpoint flags");
+    std::vector<float> w(c->nw), m, v;
     int r = nasg_get_weights(c, w.data(), w.size(), 0);
     if (r) return r;
+    int64_t t = 0;
+    if (flags & NASG_CKPT_OPTIMIZER) {
+        m.resize(c->nw);
+        v.resize(c->nw);
+        CUDA_TRY(cudaMemcpy(m.data(), c->m, c->nw * sizeof(float), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(v.data(), c->v, c->nw * sizeof(float), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(&t, c->d_adam_t, sizeof(t), cudaMemcpyDeviceToHost));
+    }
     FILE *f = std::fopen(path, "wb");
     if (!f) return fail(NASG_ERR_IO, std::string("cannot open checkpoint for writing: ") + path);
     auto u32 = [&](uint32_t v) {
@@ -803,6 +818,16 @@ int nasg_save_checkpoint(nasg_ctx *c, const char *path) {
     const uint32_t dims[5] = {(uint32_t)kIn, (uint32_t)kHidden, (uint32_t)kHidden, (uint32_t)kHidden, (uint32_t)c->D};
     for (uint32_t d : dims) u32(d);
     bool ok = std::fwrite(w.data(), sizeof(float), w.size(), f) == w.size();
+    if (flags & NASG_CKPT_OPTIMIZER) {
+        ok &= std::fwrite("NASGADM1", 1, 8, f) == 8;
+        for (int k = 0; k < 8; ++k) {
+            const unsigned char b = (unsigned char)((uint64_t)t >> (8 * k));
+            ok &= std::fwrite(&b, 1, 1, f) == 1;
+        }
+        u32((uint32_t)c->nw);
+        ok &= std::fwrite(m.data(), sizeof(float), m.size(), f) == m.size();
+        ok &= std::fwrite(v.data(), sizeof(float), v.size(), f) == v.size();
+    }
     ok &= std::fclose(f) == 0;
     return ok ? NASG_OK : fail(NASG_ERR_IO, std::string("short write on checkpoint: ") + path);
 }
@@ -837,9 +862,41 @@ int nasg_load_checkpoint(nasg_ctx *c, const char *path) {
     }
     std::vector<float> w(c->nw);
     ok &= std::fread(w.data(), sizeof(float), w.size(), f) == w.size();
+    if (!ok) {
+        std::fclose(f);
+        return fail(NASG_ERR_IO, std::string("truncated checkpoint: ") + path);
+    }
+    // optional Adam chunk (nasg_save_checkpoint_ex); anything else after the
+    // weights is ignored, as the reference's loader does
+    bool adam = false;
+    uint64_t t = 0;
+    std::vector<float> m, v;
+    char tag[8];
+    if (std::fread(tag, 1, 8, f) == 8 && std::memcmp(tag, "NASGADM1", 8) == 0) {
+        unsigned char b[8];
+        bool ok2 = std::fread(b, 1, 8, f) == 8;
+        for (int k = 0; k < 8; ++k) t |= (uint64_t)b[k] << (8 * k);
+        const uint32_t nw = u32();
+        ok2 &= ok && nw == (uint32_t)c->nw;
+        if (ok2) {
+            m.resize(nw);
+            v.resize(nw);
+            ok2 &= std::fread(m.data(), sizeof(float), nw, f) == nw && std::fread(v.data(), sizeof(float), nw, f) == nw;
+        }
+        if (!ok2) {
+            std::fclose(f);
+            return fail(NASG_ERR_IO, std::string("truncated or mismatched optimizer chunk in checkpoint: ") + path);
+        }
+        adam = true;
+    }
     std::fclose(f);
-    if (!ok) return fail(NASG_ERR_IO, std::string("truncated checkpoint: ") + path);
-    return nasg_set_weights(c, w.data(), w.size());
+    int r = nasg_set_weights(c, w.data(), w.size());
+    if (r || !adam) return r;
+    const int64_t ts = (int64_t)t;
+    CUDA_TRY(cudaMemcpy(c->m, m.data(), m.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->v, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(c->d_adam_t, &ts, sizeof(ts), cudaMemcpyHostToDevice));
+    return NASG_OK;
 }
 
 // ---- queries --------------------------------------------------------------------

@@ -85,10 +85,17 @@ def test_decode_sample_raw_matches_oracle(guide, orc, stress):
     assert np.allclose(c, cref, rtol=1e-6)
     ddir, dpdf = _dir_pdf_check(out, ref)
     bad = (ddir > 1e-3) | (dpdf > 1e-3)
+    # a lobe-selection flip (xi_sel within rounding of a cumulative weight) sends
+    # the sample to another lobe: a different direction altogether; every other
+    # query outside 1e-3 is a genuine miss of the same lobe's sample
+    flip = ddir > 0.05
+    miss = bad & ~flip
+    print(f"stress={stress}: outside 1e-3 {bad.mean():.2e} (lobe flips {flip.mean():.2e}, same-lobe misses "
+          f"{miss.mean():.2e}; max same-lobe dir {ddir[~flip].max():.2e} pdf {dpdf[~flip].max():.2e})")
     if not stress:
         assert not bad.any(), (ddir.max(), dpdf.max())
     else:
-        assert bad.mean() <= 1e-3, (bad.mean(), ddir.max(), dpdf.max())
+        assert flip.mean() <= 1e-4 and miss.mean() <= 1e-3, (flip.mean(), miss.mean())
 
 
 @pytest.mark.parametrize("stress", [False, True])

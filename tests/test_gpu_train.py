@@ -170,6 +170,44 @@ def test_checkpoint_roundtrip_with_oracle(orc, tmp_path):
     g.close()
 
 
+@pytest.mark.parametrize("prec", [nasg.NASG_MLP_FP32, nasg.NASG_MLP_BF16])
+def test_checkpoint_with_optimizer_resumes_bit_exactly(orc, tmp_path, prec):
+    """Weights + Adam state (t, m, v) saved and restored into a fresh context:
+    training continues exactly as if never interrupted (whole-buffer steps, so
+    the epoch shuffle does not depend on the iteration counter).  The file's
+    NASGNET1 prefix still loads in the reference's loader."""
+    n = 4096
+    s = torch.from_numpy(nasg.synth_samples(8, n)).cuda()
+    cfg = nasg.TrainerConfig(seed=31, sample_capacity=n, batch_size=n)
+    a = nasg.Guide(cfg)
+    a.train_precision = prec
+    for _ in range(3):
+        a.train_iteration(s, 0.5)
+    p = str(tmp_path / "resume.nasg")
+    a.save_checkpoint(p, optimizer=True)
+    w_saved, nc = orc.load_checkpoint(p)
+    assert nc == 8 and np.array_equal(w_saved, a.get_weights())
+    for _ in range(2):
+        a.train_iteration(s, 0.5)
+    b = nasg.Guide(nasg.TrainerConfig(seed=99, sample_capacity=n, batch_size=n))
+    b.train_precision = prec
+    b.load_checkpoint(p)
+    assert b.adam_t == 3
+    for _ in range(2):
+        b.train_iteration(s, 0.5)
+    assert b.adam_t == a.adam_t == 5
+    assert np.array_equal(a.get_weights(), b.get_weights())
+    # without the chunk the Adam state is left as it was (the reference's resume restarts Adam)
+    c = nasg.Guide(nasg.TrainerConfig(seed=99, sample_capacity=n, batch_size=n))
+    c.save_checkpoint(str(tmp_path / "plain.nasg"))
+    c.load_checkpoint(p)
+    assert c.adam_t == 3
+    c.load_checkpoint(str(tmp_path / "plain.nasg"))
+    assert c.adam_t == 3
+    for g in (a, b, c):
+        g.close()
+
+
 def test_counters_track_the_trainer():
     """nasg_get_counters: AdamState::t, Trainer::iterations_, the clamp counter."""
     g = nasg.Guide(nasg.TrainerConfig(seed=4, sample_capacity=1024, batch_size=256))

@@ -284,6 +284,22 @@ def test_checkpoint_roundtrip_cross(orc, ref, tmp_path):
         orc.load_checkpoint(p1)
 
 
+def test_reference_loader_skips_the_optimizer_chunk(ref, tmp_path):
+    """nasg_save_checkpoint_ex(NASG_CKPT_OPTIMIZER) appends the Adam state after
+    the NASGNET1 weights ("NASGADM1", u64 t, u32 n, f32 m[n], f32 v[n]); the
+    reference's load_checkpoint (net.cpp:54-82) reads the weights and ignores it."""
+    import struct
+    w = ref.init_network(23)
+    p = str(tmp_path / "adam.nasg")
+    assert ref.save_checkpoint(p, w) == 0
+    rng = np.random.default_rng(1)
+    m, v = rng.normal(size=w.size).astype(np.float32), rng.random(w.size).astype(np.float32)
+    with open(p, "ab") as f:
+        f.write(b"NASGADM1" + struct.pack("<QI", 1234, w.size) + m.tobytes() + v.tobytes())
+    w2, n = ref.load_checkpoint(p)
+    assert n == 8 and np.array_equal(w2, w)
+
+
 # ------------------------------------------------------- golden fixtures ----
 def _golden(name):
     path = os.path.join(GOLDEN, name)
