@@ -17,26 +17,31 @@
 namespace nasg {
 
 // ---------------------------------------------------------------- packing --
-// wp : W1[64][128] W2[128][128] W3[128][128] W4p[128][128] (packed cols)
-// wtp: W2^T[128][128] W3^T[128][128] W4p^T[128][128] (rows = packed col)
+// wp : W1[64][128] W2[128][128] W3[128][128], W4p as f32_out_blocks blocks of
+//      [128][128] (packed cols, block b = packed cols [128 b, 128 b + 128))
+// wtp: W2^T[128][128] W3^T[128][128] W4p^T[128 x blocks][128] (rows = packed col)
 __global__ void pack_fp32_kernel(const float *__restrict__ w, int n_comp, float *__restrict__ wp,
                                  float *__restrict__ wtp, int *wbig) {
     const int D = 8 * n_comp + 1;
     const int NP = packed_width(n_comp);
     const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < kPackedF32; e += gridDim.x * blockDim.x) {
+    const int total = packed_f32_floats(n_comp);
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         float v;
+        int pc = 0, k = 0;
         if (e < o3) {
             v = w[e];
         } else {
-            const int k = (e - o3) / kHidden, col = (e - o3) % kHidden;
-            int j = -1;  // reference raw index of packed column col
-            if (col < NP) {
+            const int bk = (e - o3) / (kHidden * 128), rem = (e - o3) % (kHidden * 128);
+            k = rem / 128;
+            pc = bk * 128 + rem % 128;
+            int j = -1;  // reference raw index of packed column pc
+            if (pc < NP) {
                 const int H = packed_header(n_comp);
-                if (col < n_comp) j = 7 * n_comp + col;
-                else if (col == n_comp) j = 8 * n_comp;
-                else if (col >= H) {
-                    const int i = (col - H) / 8, kk = (col - H) % 8;
+                if (pc < n_comp) j = 7 * n_comp + pc;
+                else if (pc == n_comp) j = 8 * n_comp;
+                else if (pc >= H) {
+                    const int i = (pc - H) / 8, kk = (pc - H) % 8;
                     j = kk < 5 ? 5 * i + kk : (kk == 5 ? 5 * n_comp + 2 * i : (kk == 6 ? 5 * n_comp + 2 * i + 1 : -1));
                 }
             }
@@ -45,10 +50,14 @@ __global__ void pack_fp32_kernel(const float *__restrict__ w, int n_comp, float 
         wp[e] = v;
         if (wbig && !(fabsf(v) < kSafeWeight)) atomicOr(wbig, 1);
         if (wtp && e >= o1) {  // transposed W2, W3, W4p
-            const int l = e < o2 ? 0 : (e < o3 ? 1 : 2);
-            const int base = l == 0 ? o1 : (l == 1 ? o2 : o3);
-            const int k = (e - base) / kHidden, col = (e - base) % kHidden;
-            wtp[l * kHidden * kHidden + col * kHidden + k] = v;
+            if (e < o3) {
+                const int l = e < o2 ? 0 : 1;
+                const int base = l == 0 ? o1 : o2;
+                const int kk = (e - base) / kHidden, col = (e - base) % kHidden;
+                wtp[l * kHidden * kHidden + col * kHidden + kk] = v;
+            } else {
+                wtp[2 * kHidden * kHidden + pc * kHidden + k] = v;
+            }
         }
     }
 }
@@ -83,6 +92,10 @@ __device__ __forceinline__ int encode_row(const float4 x, const float4 wo, const
 }
 
 // ---------------------------------------------------------- fused kernel --
+// feature rows of the activation tile: the hidden width, or the packed raw width when wider
+constexpr int act_rows(int n) { return packed_width(n) > kHidden ? packed_width(n) : kHidden; }
+constexpr size_t query_smem(int n) { return (size_t)(act_rows(n) * kLda + 2 * kChunk * 128) * sizeof(float); }
+
 template <int N, int MODE>
 __global__ void __launch_bounds__(256, 2)
 query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
@@ -91,8 +104,8 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
     // registers until every thread has read its last input chunk (tile_layer's
     // chunk barrier), so ~84 KB of smem -> two CTAs per SM, and one CTA's
     // half-occupied NASG epilogue overlaps the other's FFMA GEMMs
-    float *actA = smem;                      // [128][kLda]
-    float *wbuf = actA + kHidden * kLda;     // [2][16][128]
+    float *actA = smem;                      // [max(128, NP)][kLda]
+    float *wbuf = actA + act_rows(N) * kLda; // [2][16][128]
     __shared__ int s_clamped;
     const int tid = threadIdx.x;
     const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
@@ -118,6 +131,10 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
         tile_layer<128, kIn, kEpiRelu>(actA, actA, W1, wbuf, nullptr, tid);
         tile_layer<128, kHidden, kEpiRelu>(actA, actA, W2, wbuf, nullptr, tid);
         tile_layer<128, kHidden, kEpiRelu>(actA, actA, W3, wbuf, nullptr, tid);
+        if constexpr (packed_width(N) > 128) {  // packed columns [128, NP) first, into rows the layer does not read
+            tile_layer<128, kHidden, kEpiNone, kLda, packed_width(N) - 128>(actA, actA + 128 * kLda,
+                                                                            W4 + kHidden * 128, wbuf, nullptr, tid);
+        }
         tile_layer<128, kHidden, kEpiNone>(actA, actA, W4, wbuf, nullptr, tid);
         if constexpr (MODE == kModeSample || MODE == kModePdf) {
             // double-precision epilogue on all 8 warps: 2 lanes per query, 4 lobes each
@@ -164,7 +181,6 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
     if (tid == 0 && s_clamped && a.clamp_count) atomicAdd(a.clamp_count, (unsigned long long)s_clamped);
 }
 
-constexpr size_t kQuerySmem = (kHidden * kLda + 2 * kChunk * 128) * sizeof(float);
 
 template <int N>
 static int query_fp32_n(QueryMode mode, const float *wp, const QueryArgs &a, int num_sms, cudaStream_t s) {
@@ -175,8 +191,8 @@ static int query_fp32_n(QueryMode mode, const float *wp, const QueryArgs &a, int
 #define NASG_LAUNCH(M)                                                                             \
     case M: {                                                                                      \
         auto k = query_fp32_kernel<N, M>;                                                          \
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kQuerySmem);     \
-        k<<<grid, 256, kQuerySmem, s>>>(wp, a);                                                    \
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)query_smem(N));  \
+        k<<<grid, 256, query_smem(N), s>>>(wp, a);                                                 \
         break;                                                                                     \
     }
         NASG_LAUNCH(kModeSample)
@@ -189,9 +205,10 @@ static int query_fp32_n(QueryMode mode, const float *wp, const QueryArgs &a, int
 }
 
 int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, int num_sms, cudaStream_t s) {
-    switch (n_comp) {  // packed W4 must fit 128 columns: H + 8N <= 128
+    switch (n_comp) {  // N = 16: the last layer in two 128-column blocks (NP = 160)
         case 4: return query_fp32_n<4>(mode, wp, a, num_sms, s);
         case 8: return query_fp32_n<8>(mode, wp, a, num_sms, s);
+        case 16: return query_fp32_n<16>(mode, wp, a, num_sms, s);
         default: return -1;
     }
 }

@@ -32,7 +32,7 @@ constexpr int kOffH1 = kOffH0 + kIn * kTLda;
 constexpr int kOffH2 = kOffH1 + kHidden * kTLda;
 constexpr int kOffH3 = kOffH2 + kHidden * kTLda;
 constexpr int kOffDA = kOffH3 + kHidden * kTLda;
-constexpr int kOffDB = kOffDA + kHidden * kTLda;
+constexpr int kOffDB = kOffDA + 160 * kTLda;  // da holds the packed raw outputs / delta4: NP <= 160 rows
 constexpr int kOffW = kOffDB + kHidden * kTLda;
 constexpr int kOffRow = kOffW + 2 * kChunk * 128;          // 64 x 8 per-row sample data
 constexpr int kOffLoss = kOffRow + kTrainRows * 8;          // 64 double losses + 64 int states
@@ -112,6 +112,9 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
         tile_layer<kTrainRows, kHidden, kEpiRelu, kTLda>(h1, h2, W2, wbuf, nullptr, tid);
         tile_layer<kTrainRows, kHidden, kEpiRelu, kTLda>(h2, h3, W3, wbuf, nullptr, tid);
         tile_layer<kTrainRows, kHidden, kEpiNone, kTLda>(h3, da, W4, wbuf, nullptr, tid);
+        if constexpr (NP > 128)  // packed columns [128, NP): the second 128-column block of W4p
+            tile_layer<kTrainRows, kHidden, kEpiNone, kTLda, NP - 128>(h3, da + 128 * kTLda, W4 + kHidden * 128, wbuf,
+                                                                        nullptr, tid);
         store_rows<kIn>(h0, sc.h0, row0, valid, tid);
         store_rows<kHidden>(h1, sc.h1, row0, valid, tid);
         store_rows<kHidden>(h2, sc.h2, row0, valid, tid);
@@ -145,10 +148,11 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
             }
         }
         __syncthreads();
-        // delta4 in reference raw order, padded to 80 floats per row (K_dw operand)
-        for (int idx = tid; idx < kTrainRows * 80; idx += 256) {
-            const int r = idx / 80, j = idx % 80;
-            sc.d4[(row0 + r) * 80 + j] = (r < valid && j < D) ? da[packed_col(j, N) * kTLda + r] : 0.f;
+        // delta4 in reference raw order, padded to d4_stride(N) floats per row (K_dw operand)
+        constexpr int DS = d4_stride(N);
+        for (int idx = tid; idx < kTrainRows * DS; idx += 256) {
+            const int r = idx / DS, j = idx % DS;
+            sc.d4[(row0 + r) * DS + j] = (r < valid && j < D) ? da[packed_col(j, N) * kTLda + r] : 0.f;
         }
         if (tid == 0) {  // tile statistics in row order (deterministic)
             double ls = 0.0;
@@ -164,7 +168,7 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
             sc.tile_dropped[tile] = dr;
         }
         // ---- K6: delta propagation with ReLU gates (net.hpp:101-107)
-        tile_layer<kTrainRows, kHidden, kEpiMask, kTLda>(da, db, T4, wbuf, h3, tid);
+        tile_layer<kTrainRows, f32_bwd_k(N), kEpiMask, kTLda>(da, db, T4, wbuf, h3, tid);
         store_rows<kHidden>(db, sc.d3, row0, valid, tid);
         tile_layer<kTrainRows, kHidden, kEpiMask, kTLda>(db, da, T3, wbuf, h2, tid);
         store_rows<kHidden>(da, sc.d2, row0, valid, tid);
@@ -183,8 +187,8 @@ int train_forward_backward(int n_comp, const float *wp, const float *wtp, const 
     if (ntiles == 0) return 0;
     const int grid = ntiles < num_sms ? ntiles : num_sms;
     const double gscale = 1.0 / (double)global_count;  // guiding.cpp:262
-    if (n_comp != 8 && n_comp != 4) return -1;
-    auto k = n_comp == 8 ? train_fb_kernel<8> : train_fb_kernel<4>;
+    if (n_comp != 8 && n_comp != 4 && n_comp != 16) return -1;
+    auto k = n_comp == 8 ? train_fb_kernel<8> : (n_comp == 4 ? train_fb_kernel<4> : train_fb_kernel<16>);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
     k<<<grid, 256, kFbSmem, s>>>(wp, wtp, samples, order, count, gscale, b, loss_blend, bounds, sc, clamp_count);
     return 1;
@@ -194,7 +198,7 @@ int train_forward_backward(int n_comp, const float *wp, const float *wtp, const 
 // partial[split][layer block] = sum over this split's rows of H^T Delta.
 template <int M>
 __global__ void __launch_bounds__(256)
-dw_kernel(const float *__restrict__ Hm, const float *__restrict__ Dm, int ldd, int n_out,
+dw_kernel(const float *__restrict__ Hm, const float *__restrict__ Dm, int ldd, int n_out, int ldo,
           int64_t rows, int rows_per_split, float *__restrict__ partial, size_t partial_stride) {
     __shared__ __align__(16) float As[2][kChunk][M];
     __shared__ __align__(16) float Bs[2][kChunk][128];
@@ -259,7 +263,7 @@ dw_kernel(const float *__restrict__ Hm, const float *__restrict__ Dm, int ldd, i
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int n = (j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4);
-            if (n < n_out) out[(size_t)m * n_out + n] = acc[i][j];
+            if (n < n_out) out[(size_t)m * ldo + n] = acc[i][j];
         }
     }
 }
@@ -286,12 +290,16 @@ int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStrea
     const size_t stride = (size_t)nw;
     float *p = sc.dw_partial;
     const size_t o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
-    dw_kernel<64><<<splits, 256, 0, s>>>(sc.h0, sc.d1, 128, 128, rows, rps, p, stride);
-    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h1, sc.d2, 128, 128, rows, rps, p + o1, stride);
-    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h2, sc.d3, 128, 128, rows, rps, p + o2, stride);
-    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h3, sc.d4, 80, D, rows, rps, p + o3, stride);
+    dw_kernel<64><<<splits, 256, 0, s>>>(sc.h0, sc.d1, 128, 128, 128, rows, rps, p, stride);
+    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h1, sc.d2, 128, 128, 128, rows, rps, p + o1, stride);
+    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h2, sc.d3, 128, 128, 128, rows, rps, p + o2, stride);
+    // dW4 [128][D] in 128-column blocks of delta4 (two for N = 16)
+    const int ds = d4_stride(n_comp);
+    for (int c0 = 0; c0 < D; c0 += 128)
+        dw_kernel<128><<<splits, 256, 0, s>>>(sc.h3, sc.d4 + c0, ds, D - c0 < 128 ? D - c0 : 128, D, rows, rps,
+                                               p + o3 + c0, stride);
     sc.last_splits = splits;
-    return 1;
+    return 3 + (D + 127) / 128;  // launches
 }
 
 int train_reduce(int n_comp, const TrainScratch &sc, float *grad, int *nonfinite, cudaStream_t s) {
@@ -413,7 +421,7 @@ __global__ void adam_kernel(int n_comp, float *__restrict__ w, float *__restrict
             k = (e - o3) / D;
             n = packed_col((e - o3) % D, n_comp);
             l = 3;
-            wp[o3 + k * kHidden + n] = wi;
+            wp[o3 + (n / 128) * (kHidden * 128) + k * 128 + n % 128] = wi;
             wtp[2 * kHidden * kHidden + n * kHidden + k] = wi;
         }
         if (tc_img) {  // the bf16 trainer's image (train_img_bytes): f16 layers, bf16 copy of W4p^T

@@ -203,7 +203,7 @@ int ensure_scratch(nasg_ctx *c, int64_t count) {
     if (rows <= c->sc.max_rows) return NASG_OK;
     TrainScratch &s = c->sc;
     float **bufs[8] = {&s.h0, &s.h1, &s.h2, &s.h3, &s.d1, &s.d2, &s.d3, &s.d4};
-    const int widths[8] = {64, 128, 128, 128, 128, 128, 128, 80};
+    const int widths[8] = {64, 128, 128, 128, 128, 128, 128, d4_stride(c->N)};
     for (int i = 0; i < 8; ++i) {
         if (*bufs[i]) cudaFree(*bufs[i]);
         *bufs[i] = nullptr;
@@ -401,10 +401,10 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
         if (train_forward_backward(c->N, c->wp, c->wtp, samples, order, count, global_count, b,
                                    c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, clamp, s) < 0)
             return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for training");
-        train_dw(c->N, count, c->sc, c->grad, s);
+        const int ndw = train_dw(c->N, count, c->sc, c->grad, s);
         train_reduce(c->N, c->sc, c->grad, c->d_nonfinite, s);
         train_step_stats(c->sc, count, c->d_step_stats, s);
-        c->launches += 8;
+        c->launches += 3 + ndw;  // forward/backward, dW GEMMs, reduction, statistics
     } else {
         CUDA_TRY(cudaMemsetAsync(c->grad, 0, c->nw * sizeof(float), s));
         CUDA_TRY(cudaMemsetAsync(c->d_step_stats, 0, 3 * sizeof(double), s));
@@ -604,8 +604,8 @@ void nasg_config_default(nasg_config *c) {
 
 int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const float bmax[3], nasg_ctx **out) {
     if (!cfg || !out || !bmin || !bmax) return fail(NASG_ERR_INVALID, "null argument");
-    if (cfg->n_components != 4 && cfg->n_components != 8)
-        return fail(NASG_ERR_UNSUPPORTED, "n_components must be 4 or 8 in this build");
+    if (cfg->n_components != 4 && cfg->n_components != 8 && cfg->n_components != 16)
+        return fail(NASG_ERR_UNSUPPORTED, "n_components must be 4, 8 or 16 in this build");
     if (cfg->batch_size <= 0 || cfg->sample_capacity <= 0 || cfg->step_factor <= 0)
         return fail(NASG_ERR_INVALID, "batch_size, sample_capacity, step_factor must be > 0");
     int ndev = 0;
@@ -655,13 +655,13 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     ALLOC(c->w, wb); ALLOC(c->m, wb); ALLOC(c->v, wb); ALLOC(c->grad, wb);
     for (auto &P : c->pub) {
         ALLOC(P.w, wb);
-        ALLOC(P.wp, kPackedF32 * sizeof(float));
+        ALLOC(P.wp, packed_f32_floats(c->N) * sizeof(float));
         if (tc_supported(c->N)) ALLOC(P.tc, tc_image_bytes(c->N));
         if (cudaEventCreateWithFlags(&P.ev, cudaEventDisableTiming) != cudaSuccess)
             return cleanup_fail(fail(NASG_ERR_CUDA, "event create failed"));
     }
-    ALLOC(c->wp, kPackedF32 * sizeof(float));
-    ALLOC(c->wtp, kPackedT32 * sizeof(float));
+    ALLOC(c->wp, packed_f32_floats(c->N) * sizeof(float));
+    ALLOC(c->wtp, packed_t32_floats(c->N) * sizeof(float));
     if (tc_supported(c->N)) ALLOC(c->tc_live, tc_train_image_bytes(c->N));
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));

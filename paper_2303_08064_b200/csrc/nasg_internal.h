@@ -15,17 +15,26 @@ constexpr int kHidden = 128;   // net.hpp:14
 constexpr int kBins = 19;      // encoding.hpp:11
 constexpr int kTileRows = 128; // query tile (one TMEM lane / thread per row)
 
-// fp32 packed weight image used by the SIMT kernels: W1[64][128], W2, W3,
-// W4[128][128] (columns in the packed raw order, zero-padded to 128).
-constexpr int kPackedF32 = kIn * kHidden + 3 * kHidden * kHidden;  // 57344 floats
-// transposed copies for the backward delta GEMMs: W2^T, W3^T [128][128] and
-// W4^T [128 packed cols][128] (rows >= NP are zero).
-constexpr int kPackedT32 = 3 * kHidden * kHidden;
 
 // Packed raw-output layout of the last layer (see nasg_math.cuh): header of
 // round_up(N + 1, 16) columns (weight logits, selection logit), then 8 columns per lobe.
 __host__ __device__ constexpr int packed_header(int n) { return ((n + 1 + 15) / 16) * 16; }
 __host__ __device__ constexpr int packed_width(int n) { return packed_header(n) + 8 * n; }
+
+// fp32 packed weight image used by the SIMT kernels: W1[64][128], W2, W3, then
+// the last layer in the packed raw order as f32_out_blocks(n) blocks of
+// [128 k][128 packed cols] (zero-padded): one block for N <= 8, two for N = 16.
+__host__ __device__ constexpr int f32_out_blocks(int n) { return (packed_width(n) + 127) / 128; }
+__host__ __device__ constexpr int packed_f32_floats(int n) {
+    return kIn * kHidden + 2 * kHidden * kHidden + f32_out_blocks(n) * kHidden * 128;
+}
+// transposed copies for the backward delta GEMMs: W2^T, W3^T [128][128] and
+// W4p^T [128 x blocks packed cols][128] (rows >= NP are zero).
+__host__ __device__ constexpr int packed_t32_floats(int n) { return 2 * kHidden * kHidden + f32_out_blocks(n) * 128 * kHidden; }
+// contraction length of the backward through W4p^T: NP rounded up to 16 (>= 128)
+__host__ __device__ constexpr int f32_bwd_k(int n) { return packed_width(n) <= 128 ? 128 : (packed_width(n) + 15) / 16 * 16; }
+// row stride of the fp32 trainer's delta4 (reference raw order, zero-padded)
+__host__ __device__ constexpr int d4_stride(int n) { return 8 * n + 1 <= 80 ? 80 : 256; }
 
 __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHidden * kHidden + kHidden * (8 * n + 1); }
 

@@ -37,8 +37,9 @@ enum Epi { kEpiNone = 0, kEpiRelu = 1, kEpiMask = 2 };
 
 // OUT[n][r] (feature-major) = epi( sum_k IN[k][r] * W[k][n] ).
 // kEpiMask multiplies by [MASK[n][r] > 0] (ReLU gate of backward, net.hpp:106).
-// Must be called by all 256 threads; ends with a __syncthreads().
-template <int TM, int K, int EPI, int LDA = kLda>
+// Must be called by all 256 threads; ends with a __syncthreads().  Only output
+// features n < NOUT are stored (the second 128-column block of a wide layer).
+template <int TM, int K, int EPI, int LDA = kLda, int NOUT = 128>
 __device__ __forceinline__ void tile_layer(const float *in, float *out,
                                            const float *__restrict__ W, float *wbuf,
                                            const float *mask, int tid) {
@@ -86,6 +87,7 @@ __device__ __forceinline__ void tile_layer(const float *in, float *out,
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
         const int n = (j < 4) ? tx * 4 + j : 64 + tx * 4 + (j - 4);
+        if (NOUT < 128 && n >= NOUT) continue;
 #pragma unroll
         for (int h = 0; h < RM / 4; ++h) {
             float4 v = make_float4(acc[4 * h][j], acc[4 * h + 1][j], acc[4 * h + 2][j], acc[4 * h + 3][j]);

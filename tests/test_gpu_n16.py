@@ -1,0 +1,173 @@
+"""N = 16 lobes (D = 129 raw outputs, packed width 160; the paper's component
+sweep, PAPER Table 4: C = 4 / 16 / 32) through every kernel, against the CPU
+oracle with the same tolerances as the N = 8 tests.  The packed last layer is
+wider than one 128-column block: the fp32 kernels run it as two blocks, the
+tensor-core query kernel with one MLP/NASG pair per SM (UMMA N = 160), the
+tensor-core trainer with one warpgroup chain per CTA.  Checked:
+  init bit-exact; fp32 raw outputs 2e-5; fp32 query sample / pdf and the decode
+  parity entries 1e-3 relative; bf16 query within the bf16 path's stated
+  tolerance; one fp32 training step's gradient rel-L2 1e-4; the bf16 training
+  step's gradient vs the fp32 one; one render iteration end to end."""
+import numpy as np
+import pytest
+
+import nasg_testutil as H
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2303_08064_b200 as nasg  # noqa: E402
+
+N, D = 16, 129
+
+
+def dev4(a3):
+    a = np.zeros((len(a3), 4), np.float32)
+    a[:, : min(4, a3.shape[1])] = a3[:, :4]
+    return torch.from_numpy(a).cuda()
+
+
+def split(q9):
+    return dev4(q9[:, 0:3]), dev4(q9[:, 3:6]), dev4(q9[:, 6:9])
+
+
+@pytest.fixture(scope="module")
+def guide():
+    g = nasg.Guide(nasg.TrainerConfig(n_components=N, seed=404))
+    yield g
+    g.close()
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def test_init_and_raw_outputs(guide, orc):
+    assert np.array_equal(guide.get_weights(), orc.init_network(404, out_dim=D))
+    q9 = H.queries(np.random.default_rng(1), 4099, outside=0.1)
+    raw = guide.query_raw(*split(q9)).cpu().numpy()
+    enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
+    ref = orc.forward(guide.get_weights(published=True), enc, out_dim=D)
+    assert raw.shape == (4099, D)
+    assert np.all(np.abs(raw - ref) <= 2e-5 * (1 + np.abs(ref)))
+
+
+@pytest.mark.parametrize("stress", [False, True])
+def test_decode_entries(guide, orc, stress):
+    rng = np.random.default_rng(7 + stress)
+    n = 1 << 15
+    raw, xi = H.raw_outputs(rng, n, n_comp=N, stress=stress), H.xis(rng, n)
+    guide.precision = nasg.NASG_MLP_FP32
+    out, c = guide.decode_sample_raw(torch.from_numpy(raw).cuda(), torch.from_numpy(xi).cuda())
+    ref, cref = orc.decode_sample(raw, xi, n_comp=N, threads=8)
+    out = out.cpu().numpy().astype(np.float64)
+    ddir = np.linalg.norm(out[:, :3] - ref[:, :3], axis=1)
+    dpdf = np.abs(out[:, 3] - ref[:, 3]) / np.maximum(ref[:, 3], 1e-30)
+    bad = (ddir > 1e-3) | (dpdf > 1e-3)
+    assert (bad.mean() <= 1e-3) if stress else (not bad.any()), (bad.mean(), ddir.max(), dpdf.max())
+    assert np.allclose(c.cpu().numpy(), cref, rtol=1e-6)
+    dirs = H.dirs(rng, n)
+    bsdf = rng.random(n).astype(np.float32)
+    mix, gd = guide.decode_pdf_raw(torch.from_numpy(raw).cuda(), dev4(dirs), 0.7, torch.from_numpy(bsdf).cuda())
+    mref, gref = orc.decode_pdf(raw, dirs, 0.7, bsdf, n_comp=N)
+    rm = np.abs(mix.cpu().numpy() - mref) / np.maximum(mref, 1e-30)
+    big = mref > 1e-30
+    assert ((rm[big] > 1e-3).mean() <= 1e-3) if stress else rm.max() <= 1e-3
+
+
+def test_query_sample_fp32_and_bf16(guide, orc):
+    rng = np.random.default_rng(9)
+    n = 1 << 16
+    q9, xi = H.queries(rng, n), H.xis(rng, n)
+    ref, cref = orc.query_sample(guide.get_weights(published=True), q9, xi, out_dim=D, threads=8)
+    ref = ref.astype(np.float64)
+    for prec in (nasg.NASG_MLP_FP32, nasg.NASG_MLP_BF16):
+        guide.precision = prec
+        c = torch.empty(n, dtype=torch.float32, device="cuda")
+        out, _ = guide.query_sample(*split(q9), torch.from_numpy(xi).cuda(), c=c)
+        out = out.cpu().numpy().astype(np.float64)
+        ddir = np.linalg.norm(out[:, :3] - ref[:, :3], axis=1)
+        dpdf = np.abs(out[:, 3] - ref[:, 3]) / ref[:, 3]
+        if prec == nasg.NASG_MLP_FP32:
+            assert ddir.max() <= 1e-3 and dpdf.max() <= 1e-3, (ddir.max(), dpdf.max())
+            assert np.allclose(c.cpu().numpy(), cref, rtol=1e-5)
+        else:  # bf16 MLP: same bar as the N = 8 smoke check
+            off = (ddir > 0.1) | (dpdf > 0.1)
+            assert off.mean() <= 0.02 and np.median(dpdf) <= 5e-3, (off.mean(), np.median(dpdf))
+    guide.precision = nasg.NASG_MLP_FP32
+
+
+def test_query_pdf_fp32(guide, orc):
+    rng = np.random.default_rng(10)
+    n = 20000
+    q9, dirs = H.queries(rng, n), H.dirs(rng, n)
+    bsdf = rng.random(n).astype(np.float32)
+    guide.precision = nasg.NASG_MLP_FP32
+    mix, gd = guide.query_pdf(*split(q9), dev4(dirs), 0.5, torch.from_numpy(bsdf).cuda())
+    enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
+    raw = orc.forward(guide.get_weights(published=True), enc, out_dim=D)
+    mref, gref = orc.decode_pdf(raw, dirs, 0.5, bsdf, n_comp=N)
+    assert np.max(np.abs(mix.cpu().numpy() - mref) / mref) <= 1e-3
+    assert np.max(np.abs(gd.cpu().numpy() - gref) / gref) <= 1e-3
+
+
+def _oracle_grad(orc, w, samples, b, e=0.2):
+    q9 = np.concatenate([samples[:, 0:3], samples[:, 4:7], samples[:, 8:11]], 1)
+    enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
+    raw = orc.forward(w, enc, out_dim=D)
+    g, ok, loss = orc.kl_grad(raw, samples, b, e, n_comp=N)
+    og = (g * (1.0 / len(samples))).astype(np.float32)
+    return orc.backward(w, enc, og, out_dim=D), ok
+
+
+@pytest.mark.parametrize("b", [0.0, 1.0])
+def test_training_step_gradients(orc, b):
+    s = H.samples(np.random.default_rng(int(10 * b) + 3), 3000)
+    ds = torch.from_numpy(s).cuda()
+    grads = {}
+    for prec in (nasg.NASG_MLP_FP32, nasg.NASG_MLP_BF16):
+        g = nasg.Guide(nasg.TrainerConfig(n_components=N, seed=88, batch_size=3000, sample_capacity=3000))
+        g.train_precision = prec
+        w0 = g.get_weights()
+        g.train_step(ds, None, len(s), len(s), b)
+        grads[prec] = g.last_grad()
+        st = g.train_stats_take()
+        assert st.steps == 1
+        g.close()
+    ref, ok = _oracle_grad(orc, w0, s, b)
+    assert rel_l2(grads[nasg.NASG_MLP_FP32], ref) <= 1e-4
+    # bf16 operands / activations: the gradient direction is the reference's
+    gb = grads[nasg.NASG_MLP_BF16].astype(np.float64)
+    cos = float(gb @ ref / (np.linalg.norm(gb) * np.linalg.norm(ref)))
+    assert cos >= 0.98 and rel_l2(gb, ref) <= 0.2, (cos, rel_l2(gb, ref))
+
+
+def test_train_iteration_tracks_oracle(orc):
+    s = nasg.synth_samples(6, 2048)
+    g = nasg.Guide(nasg.TrainerConfig(n_components=N, seed=7, sample_capacity=2048, batch_size=512))
+    t = orc.trainer(n_comp=N, capacity=2048, batch=512, seed=7)
+    st = g.train_iteration(torch.from_numpy(s).cuda(), 1.0)
+    sr = t.train(s, 1.0)
+    assert st.steps == sr["steps"] == 4
+    assert st.mean_loss == pytest.approx(sr["mean_loss"], rel=1e-3)
+    assert rel_l2(g.get_weights(), t.weights()) <= 1e-3
+    g.close()
+
+
+def test_render_iteration_n16():
+    lo, hi = nasg.scene_bounds(nasg.SCENE_BOX)
+    g = nasg.Guide(nasg.TrainerConfig(n_components=N, seed=5), bmin=lo, bmax=hi)
+    g.precision = nasg.NASG_MLP_BF16
+    g.train_precision = nasg.NASG_MLP_BF16
+    r = nasg.Render(g, scene=nasg.SCENE_BOX, width=64, height=64, seed=2, schedule_m=1, schedule_b=1)
+    try:
+        for _ in range(4):
+            st = r.iteration()
+        assert st["guided_vertices"] > 0 and st["train"].steps > 0 and st["nonfinite_paths"] == 0
+        assert np.isfinite(r.image()).all()
+    finally:
+        r.close()
+        g.close()
