@@ -441,9 +441,37 @@ def bench_sweep(nasg, args, ws, rank):
             t = max_over_ranks(sum(time_events(lambda: g.query_sample(*d, dir_pdf=res[:n]), reps, stream)), ws)
             out[f"{name}_2^{lg}"] = n * ws * reps / t
     g.close()
-    del dev, res
+    # the paper's component sweep (PAPER Table 4: C = 4 / 16; N = 8 above) at 2^22
+    # queries, both precisions, plus one config-3-shaped bf16 training step (2^18)
+    n = 1 << 22
+    d = [a[:n] for a in dev]
+    samples = torch.from_numpy(nasg.synth_samples(11, 1 << 18, first=rank * (1 << 18))).cuda()
+    for nc in (4, 16):
+        g = nasg.Guide(nasg.TrainerConfig(seed=0, n_components=nc), device=torch.cuda.current_device())
+        for prec, name in ((nasg.NASG_MLP_BF16, "bf16"), (nasg.NASG_MLP_FP32, "fp32")):
+            g.precision = prec
+            for _ in range(2):
+                g.query_sample(*d, dir_pdf=res[:n])
+            torch.cuda.synchronize()
+            barrier(ws)
+            reps = 4 if name == "bf16" else 2
+            t = max_over_ranks(sum(time_events(lambda: g.query_sample(*d, dir_pdf=res[:n]), reps, stream)), ws)
+            out[f"N{nc}_{name}_2^22"] = n * ws * reps / t
+        g.close()
+        tg = nasg.Guide(nasg.TrainerConfig(seed=3, n_components=nc, sample_capacity=1 << 18, batch_size=1 << 18),
+                        device=torch.cuda.current_device())
+        tg.train_precision = nasg.NASG_MLP_BF16
+        for _ in range(3):
+            tg.train_iteration(samples, 1.0, stats=False)
+        torch.cuda.synchronize()
+        t = max_over_ranks(sum(time_events(lambda: tg.train_iteration(samples, 1.0, stats=False), 5, stream)), ws)
+        out[f"N{nc}_bf16_train_samples_per_s"] = (1 << 18) * ws * 5 / t
+        tg.close()
+    del dev, res, samples
     torch.cuda.empty_cache()
-    return {"unit": "queries/s", "note": "config 2 sweep; value = all ranks' queries / max-over-ranks time",
+    return {"unit": "queries/s (train entries: samples/s)",
+            "note": "config 2 sweep; value = all ranks' queries / max-over-ranks time; N4_*, N16_*: the paper's "
+                    "lobe-count sweep (Table 4) at 2^22 queries and a 2^18-sample training step",
             **out}
 
 

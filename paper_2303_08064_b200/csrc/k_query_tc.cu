@@ -50,10 +50,14 @@ namespace nasg {
 
 namespace {
 
-constexpr int kPairs = 2;                       // MLP + NASG warpgroup pairs
-constexpr int kThreads = 2 * kPairs * 128;      // 16 warps
-constexpr int kRegsMlp = 104, kRegsNasg = 152;  // 2 x 128 x (104 + 152) = 64K registers
-constexpr uint32_t kABytes = 128 * 128 * 2;     // one bf16 activation tile, K = 128
+// MLP + NASG warpgroup pairs per CTA: two while a pair's raw buffer fits 128
+// TMEM columns (N <= 8: NP <= 80); N = 16 (NP = 160) runs one pair, whose raw
+// buffer takes [256, 416) and whose NASG warpgroup gets the registers for it.
+constexpr int pairs_for(int n) { return packed_width(n) > 128 ? 1 : 2; }
+constexpr int threads_for(int n) { return 2 * pairs_for(n) * 128; }
+constexpr int kRegsMlp = 104;  // 2 x 128 x (104 + 152) = 64K registers with two pairs
+constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 152 : 232; }
+constexpr uint32_t kABytes = 128 * 128 * 2;     // one f16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
 constexpr uint32_t kEBytes = 128 * 64 * 2;      // one encoded tile (layer 0's A operand, K = 64)
@@ -61,15 +65,15 @@ constexpr uint32_t kInBytes = 128 * 52;         // one tile of inputs: 13-float 
 
 template <int N>
 constexpr size_t smem_bytes() {
-    return align1k(img_bytes(N)) + kPairs * (kABytes + kEBytes) + 2 * kPairs * kInBytes +
-           (7 * kPairs + 2) * sizeof(uint64_t);
+    constexpr int P = pairs_for(N);
+    return align1k(img_bytes(N)) + P * (kABytes + kEBytes) + 2 * P * kInBytes + (7 * P + 2) * sizeof(uint64_t);
 }
 
 }  // namespace
 
 size_t tc_image_bytes(int n) { return img_bytes(n); }
 size_t tc_train_image_bytes(int n) { return train_img_bytes(n); }
-bool tc_supported(int n) { return n == 4 || n == 8; }  // NP = 48 / 80: one UMMA N <= 256, N % 16 == 0
+bool tc_supported(int n) { return n == 4 || n == 8 || n == 16; }  // NP = 48 / 80 / 160: one UMMA N <= 256, N % 16 == 0
 
 // ------------------------------------------------------------------ packing --
 // f16 image of the four layers (both tensor-core kernels); train = 1 appends
@@ -114,9 +118,10 @@ void launch_pack_tc(const float *w, int n_comp, void *img, cudaStream_t s, bool 
 
 // ------------------------------------------------------------------ kernel --
 template <int N, int MODE>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(threads_for(N), 1)
 query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     constexpr int NP = packed_width(N);
+    constexpr int kPairs = pairs_for(N);
     constexpr uint32_t IMG = img_bytes(N);
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -136,7 +141,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     pdl_wait();  // the queue (n_dev) and its rows come from the previous kernel on the stream
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = warp >> 2;        // warpgroup 0..3: named barrier g + 1
-    const int m = g & 1;            // pair
+    const int m = g % kPairs;       // pair
     const int wq = warp & 3;        // TMEM lane quarter of this warp
     const int t = threadIdx.x & 127;
     const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
@@ -254,7 +259,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         }
     } else {
         // ============================ NASG warpgroup ===========================
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(kRegsNasg));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(regs_nasg(N)));
         const uint32_t my_raw = tmem + 256 + m * 128 + ((uint32_t)(wq * 32) << 16);
         const uint32_t e_row64 = tc::smem_u32(smem + E_OFF + m * kEBytes) + (t >> 3) * 1024 + (t & 7) * 16;
         const float(&inv_ext)[3] = a.bounds.inv_ext;
@@ -410,6 +415,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 
 template <int N>
 static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int num_sms, cudaStream_t s, bool pdl) {
+    constexpr int kPairs = pairs_for(N);
     const int64_t ntiles = (a.n + 127) / 128;
     const int64_t supers = (ntiles + kPairs - 1) / kPairs;
     const int grid = (int)(supers < num_sms ? supers : num_sms);
@@ -421,7 +427,7 @@ static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int n
     case M: {                                                                              \
         auto k = query_tc_kernel<N, M>;                                                    \
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
-        launch_pdl(pdl, k, dim3(grid), dim3(kThreads), sm, s, im, a);                       \
+        launch_pdl(pdl, k, dim3(grid), dim3(threads_for(N)), sm, s, im, a);                 \
         break;                                                                             \
     }
         NASG_LAUNCH_TC(kModeSample)
@@ -437,6 +443,7 @@ int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, in
     switch (n_comp) {
         case 4: return query_tc_n<4>(mode, img, a, num_sms, s, pdl);
         case 8: return query_tc_n<8>(mode, img, a, num_sms, s, pdl);
+        case 16: return query_tc_n<16>(mode, img, a, num_sms, s, pdl);
         default: return -1;
     }
 }

@@ -30,9 +30,11 @@ namespace nasg {
 
 namespace {
 
+// Epilogue warpgroups (tile chains) per CTA: three for N <= 8 (12 warps, 3 per
+// SMSP, up to 168 registers); one for N = 16, whose 160-column raw / delta4
+// tile and 160 KB trainer image leave room for a single chain.
 constexpr int kWGt = 3;
-
-constexpr int kThreadsT = kWGt * 128;  // 12 warps: 3 per SMSP -> up to 168 registers
+constexpr int wgt_for(int n) { return packed_width(n) > 128 ? 1 : kWGt; }
 constexpr uint32_t kATile = 128 * 128 * 2;
 constexpr uint32_t kTmemColsT = 512;
 
@@ -45,10 +47,19 @@ constexpr uint32_t kl_sc_off() { return (uint32_t)packed_width(N) * 256u; }
 static_assert(packed_width(8) * 256 + 2 * 8 * kKlScStride * 4 <= kATile, "KL scratch fits the A tile tail");
 static_assert((3 * 8 + 2 * kWGt) * kKlScStride * 4 <= kATile, "cooperative KL scratch fits an A tile");
 
+// A tile of one chain: K = 128 activations / deltas, or delta4 (K = NP) with
+// the KL scratch behind it when NP > 128
+template <int N>
+constexpr uint32_t a_tile_bytes() {
+    return packed_width(N) <= 128 ? kATile
+                                  : align1k((uint32_t)packed_width(N) * 256u + 2u * N * kKlScStride * 4u);
+}
+
 template <int N>
 constexpr size_t fb_smem() {  // trainer image, A tiles, barriers, tile-stat partials
-    return align1k(train_img_bytes(N)) + kWGt * kATile + 64 + kWGt * 4 * 3 * sizeof(double);
+    return align1k(train_img_bytes(N)) + wgt_for(N) * a_tile_bytes<N>() + 64 + wgt_for(N) * 4 * 3 * sizeof(double);
 }
+static_assert(fb_smem<16>() <= 232448, "N = 16 trainer fits one SM's shared memory");
 
 // Power-of-two scale exponent that maps a row maximum m to [2^13, 2^14)
 // (0 for m = 0), bounded so the row's total scale 2^(E + k) stays a normal float.
@@ -69,6 +80,14 @@ __device__ __forceinline__ uint32_t blk_off(int t, int F) { return (uint32_t)((t
 
 __device__ __forceinline__ void st_g16(uint8_t *p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     *reinterpret_cast<uint4 *>(p) = make_uint4(a, b, c, d);
+}
+
+// the packed header columns of a row (16 for N <= 8, 32 for N = 16)
+template <int HD>
+__device__ __forceinline__ void tmem_ld_hdr(uint32_t taddr, float (&h)[HD]) {
+    static_assert(HD == 16 || HD == 32, "packed header width");
+    if constexpr (HD == 16) tc::tmem_ld16(taddr, h);
+    else tc::tmem_ld32(taddr, h);
 }
 
 // ReLU gate flags of the 16 packed bf16 pairs (32 columns) of a drain chunk in
@@ -228,11 +247,13 @@ size_t tc_train_block_bytes(int n_comp) {  // bf16 bytes per 128-row block over 
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreadsT, 1)
+__global__ void __launch_bounds__(wgt_for(N) * 128, 1)
 train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__restrict__ samples,
                    const uint32_t *__restrict__ order, int64_t count, const int64_t *live_count, double gscale,
                    double b, double e, Bounds bd, TcTrainBufs tb, unsigned long long *clamp_count) {
     constexpr int NP = packed_width(N);
+    constexpr int kWGt = wgt_for(N);
+    constexpr uint32_t kATile = a_tile_bytes<N>();
     constexpr uint32_t IMG = train_img_bytes(N);  // f16 layers + the bf16 copy of W4p^T at img_bytes(N)
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
@@ -327,7 +348,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         // Small batch (no more tiles than CTAs): warpgroups 1 and 2 have no tile of
         // their own and take lobes of warpgroup 0's KL gradient instead (the step's
         // latency is one tile's chain; kl_grad_row_coop splits its longest link).
-        const bool coop = ntiles <= (int64_t)gridDim.x;
+        const bool coop = kWGt > 1 && ntiles <= (int64_t)gridDim.x;
         float *coop_sc = reinterpret_cast<float *>(smem + A_OFF + kATile);           // [3N][128], group 1's tile
         int *coop_flg = reinterpret_cast<int *>(coop_sc + 3 * N * kKlScStride);     // [2 x 3][128]
         float *kl_scratch = reinterpret_cast<float *>(smem + A_OFF + g * kATile + kl_sc_off<N>());
@@ -391,7 +412,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 st_g16(gd4 + c * 128, p0, p1, p2, p3);
             };
             float hdr[HD];
-            tc::tmem_ld16(my_tmem, hdr);
+            tmem_ld_hdr(my_tmem, hdr);
             tc::tmem_ld_wait();
             TrainRow srow;
             srow.wi = make_float3(s3.x, s3.y, s3.z);
@@ -525,7 +546,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
             };
             coop_sync(2);
             float hdr[HD], ghdr[HD];
-            tc::tmem_ld16(tm0, hdr);
+            tmem_ld_hdr(tm0, hdr);
             tc::tmem_ld_wait();
             TrainRow srow;
             srow.wi = make_float3(s3.x, s3.y, s3.z);
@@ -548,6 +569,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
 }
 
 // ------------------------------------------------------------------- K_dw --
+// row stride (floats) of one split's [128][.] dW partial: 128, or NP when wider
+__host__ __device__ constexpr int partial_stride(int np) { return np > 128 ? np : 128; }
+
 // grid (splits, 4 layers).  Layer L computes D[128][FB] = A^T-contraction over
 // rows of A block [rows][128] and B block [rows][FB], both MN-major:
 //   L0: A = delta1, B = h0 -> dW1^T   L1: A = h1, B = delta2 -> dW2
@@ -560,7 +584,7 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np, const int64
     const uint8_t *B = L == 0 ? tb.h0 : (L == 1 ? tb.d2 : (L == 2 ? tb.d3 : tb.d4));
     const int FB = L == 0 ? 64 : (L == 3 ? np : 128);
     const uint32_t abytes = 128u * 256u, bbytes = (uint32_t)FB * 256u;
-    constexpr uint32_t kStage = 65536;
+    constexpr uint32_t kStage = 73728;  // A block 32 KB + B block up to 160 x 256 B
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + 2 * kStage);
     uint64_t *empty = full + 2;
     uint64_t *done = full + 4;
@@ -574,7 +598,7 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np, const int64
         tc::mbar_init(done, 1);
         tc::fence_mbar_init();
     }
-    if (warp == 0) tc::tmem_alloc(tmem_slot, 128);
+    if (warp == 0) tc::tmem_alloc(tmem_slot, 256);  // FB <= 160 fp32 columns
     tc::tc_fence_before();
     __syncthreads();
     tc::tc_fence_after();
@@ -618,7 +642,8 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np, const int64
     if (b1 > b0) {
         tc::mbar_wait(done, 0);
         tc::tc_fence_after();
-        float *out = tb.partial + ((size_t)L * tb.splits + blockIdx.x) * (128 * 128) + threadIdx.x * 128;
+        const int ps = partial_stride(np);
+        float *out = tb.partial + ((size_t)L * tb.splits + blockIdx.x) * (128 * ps) + threadIdx.x * ps;
         const uint32_t ta = tmem + ((uint32_t)(warp * 32) << 16);
         for (int q = 0; q < FB / 16; ++q) {
             float v[16];
@@ -633,7 +658,7 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np, const int64
     __syncthreads();
     if (warp == 0) {
         tc::tc_fence_after();
-        tc::tmem_dealloc(tmem, 128);
+        tc::tmem_dealloc(tmem, 256);
     }
 }
 
@@ -691,9 +716,10 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
     else if (e < o2) { L = 1; m = (e - o1) / kHidden; n = (e - o1) % kHidden; }
     else if (e < o3) { L = 2; m = (e - o2) / kHidden; n = (e - o2) % kHidden; }
     else { L = 3; m = (e - o3) / D; n = packed_col((e - o3) % D, n_comp); }
-    const float *p = tb.partial + (size_t)L * tb.splits * (128 * 128) + m * 128 + n;  // layer stride = capacity
+    const int ps = partial_stride(packed_width(n_comp));
+    const float *p = tb.partial + (size_t)L * tb.splits * (128 * ps) + m * ps + n;
     float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += p[(size_t)k * (128 * 128)];
+    for (int k = 0; k < splits; ++k) s += p[(size_t)k * (128 * ps)];
     grad[e] = s;
     if (!isfinite(s)) atomicOr(nonfinite, 1);
 }
@@ -702,7 +728,7 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
                   int64_t global_count, double b, double loss_blend, const Bounds &bounds, TcTrainBufs &tb,
                   int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s,
                   bool pdl) {
-    if (n_comp != 8 && n_comp != 4) return -1;
+    if (n_comp != 8 && n_comp != 4 && n_comp != 16) return -1;
     const int64_t ntiles = (count + 127) / 128;
     const double gscale = 1.0 / (double)global_count;
     int launches = 0;
@@ -728,23 +754,22 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
         }
         const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
         const uint8_t *im = static_cast<const uint8_t *>(img);
-        if (n_comp == 8) {
-            constexpr size_t sm = fb_smem<8>();
-            cudaFuncSetAttribute(train_tc_fb_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(pdl, train_tc_fb_kernel<8>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, rows, count,
-                       live_count, gscale, b, loss_blend, bounds, tb, clamp_count);
-        } else {
-            constexpr size_t sm = fb_smem<4>();
-            cudaFuncSetAttribute(train_tc_fb_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(pdl, train_tc_fb_kernel<4>, dim3(grid), dim3(kThreadsT), sm, s, im, samples, rows, count,
-                       live_count, gscale, b, loss_blend, bounds, tb, clamp_count);
-        }
+        auto launch_fb = [&](auto nc) {
+            constexpr int NC = decltype(nc)::value;
+            constexpr size_t sm = fb_smem<NC>();
+            cudaFuncSetAttribute(train_tc_fb_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            launch_pdl(pdl, train_tc_fb_kernel<NC>, dim3(grid), dim3(wgt_for(NC) * 128), sm, s, im, samples, rows,
+                       count, live_count, gscale, b, loss_blend, bounds, tb, clamp_count);
+        };
+        if (n_comp == 8) launch_fb(std::integral_constant<int, 8>{});
+        else if (n_comp == 4) launch_fb(std::integral_constant<int, 4>{});
+        else launch_fb(std::integral_constant<int, 16>{});
         int64_t nb;
         int bps;
         int splits = (int)(ntiles < tb.splits ? ntiles : tb.splits);
         split_plan(count, splits, nb, bps);
         if (!live_count) splits = (int)((ntiles + bps - 1) / bps);  // every launched split gets blocks
-        const size_t sm = 2 * 65536 + 64;
+        const size_t sm = 2 * 73728 + 64;
         cudaFuncSetAttribute(train_tc_dw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         launch_pdl(pdl, train_tc_dw_kernel, dim3(splits, 4), dim3(128), sm, s, tb, ntiles, bps, packed_width(n_comp),
                    live_count);

@@ -5,7 +5,7 @@ wider than one 128-column block: the fp32 kernels run it as two blocks, the
 tensor-core query kernel with one MLP/NASG pair per SM (UMMA N = 160), the
 tensor-core trainer with one warpgroup chain per CTA.  Checked:
   init bit-exact; fp32 raw outputs 2e-5; fp32 query sample / pdf and the decode
-  parity entries 1e-3 relative; bf16 query within the bf16 path's stated
+  parity entries 1e-3 relative; tensor-core query within the N = 8 path's stated
   tolerance; one fp32 training step's gradient rel-L2 1e-4; the bf16 training
   step's gradient vs the fp32 one; one render iteration end to end."""
 import numpy as np
@@ -94,9 +94,11 @@ def test_query_sample_fp32_and_bf16(guide, orc):
         if prec == nasg.NASG_MLP_FP32:
             assert ddir.max() <= 1e-3 and dpdf.max() <= 1e-3, (ddir.max(), dpdf.max())
             assert np.allclose(c.cpu().numpy(), cref, rtol=1e-5)
-        else:  # bf16 MLP: same bar as the N = 8 smoke check
-            off = (ddir > 0.1) | (dpdf > 0.1)
-            assert off.mean() <= 0.02 and np.median(dpdf) <= 5e-3, (off.mean(), np.median(dpdf))
+        else:  # tensor-core MLP (f16 operands): the N = 8 path's bar (test_gpu_tc.py)
+            same = ddir <= 0.05
+            p50 = np.median(dpdf[same])
+            print(f"N={N} tensor-core query: lobe mismatch {1 - same.mean():.2e} pdf p50 {p50:.2e}")
+            assert 1 - same.mean() <= 2e-3 and p50 <= 1e-3, (1 - same.mean(), p50)
     guide.precision = nasg.NASG_MLP_FP32
 
 
@@ -142,7 +144,8 @@ def test_training_step_gradients(orc, b):
     # bf16 operands / activations: the gradient direction is the reference's
     gb = grads[nasg.NASG_MLP_BF16].astype(np.float64)
     cos = float(gb @ ref / (np.linalg.norm(gb) * np.linalg.norm(ref)))
-    assert cos >= 0.98 and rel_l2(gb, ref) <= 0.2, (cos, rel_l2(gb, ref))
+    print(f"N={N} b={b} tensor-core train gradient: cos {cos:.5f} rel-L2 {rel_l2(gb, ref):.3e}")
+    assert cos >= 0.995 and rel_l2(gb, ref) <= 0.1, (cos, rel_l2(gb, ref))  # measured cos >= 0.9988, rel <= 0.053
 
 
 def test_train_iteration_tracks_oracle(orc):
