@@ -550,6 +550,9 @@ def main():
         run_reference(args, int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0")))
         return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import torch
+        if torch.cuda.device_count() < args.gpus:  # one rank per GPU: never two ranks on one device
+            sys.exit(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, found {torch.cuda.device_count()}")
         sys.exit(self_launch(args.gpus))
     if int(os.environ.get("WORLD_SIZE", "1")) != args.gpus:
         sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={os.environ.get('WORLD_SIZE', '1')}")
