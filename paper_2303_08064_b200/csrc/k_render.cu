@@ -869,6 +869,7 @@ double blend_of(const nasg_render *r, int64_t iter) {
 }  // namespace
 
 int nasg_render_iteration(nasg_render *r, nasg_render_stats *stats) {
+    nasg::NvtxRange nv_("nasg_render_iteration");
     if (!r) return NASG_ERR_INVALID;
     DeviceScope ds_(ctx_device(r->ctx));
     const nasg_render_config &c = r->cfg;

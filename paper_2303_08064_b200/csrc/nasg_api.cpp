@@ -368,6 +368,8 @@ QueryArgs base_args(nasg_ctx *c, int64_t n) {
 }
 
 int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
+    static const char *const kNames[] = {"nasg_query_sample", "nasg_query_pdf", "nasg_query_raw", "nasg_query_shade"};
+    NvtxRange nv_(kNames[(int)mode & 3]);
     if (a.n == 0) return NASG_OK;
     if (s != c->stream) CUDA_TRY(cudaStreamWaitEvent(s, c->pub_ev, 0));  // read a complete snapshot
     int r;
@@ -388,6 +390,7 @@ int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
 // (guiding.cpp:209-214), so encode clamps are counted on a row's first-epoch visit only.
 int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
                     int64_t global_count, double b, cudaStream_t s, bool count_clamps = true) {
+    NvtxRange nv_("nasg_train_step");
     unsigned long long *clamp = count_clamps ? c->d_clamp : nullptr;
     if (count <= 0 && c->nranks == 1) return NASG_OK;
     const bool tc = c->train_precision == NASG_MLP_BF16;
@@ -753,6 +756,7 @@ int nasg_get_weights(nasg_ctx *c, float *host_w, size_t n, int published) {
 
 int nasg_publish(nasg_ctx *c) {
     DeviceScope ds_(c ? c->device : -1);
+    NvtxRange nv_("nasg_publish");
     if (!c) return fail(NASG_ERR_INVALID, "null context");
     return do_publish(c);
 }
@@ -1148,6 +1152,7 @@ int nasg_dp_plan(const nasg_config *cfg, const int64_t *n_per_rank, int nranks, 
 int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *samples, double b,
                          nasg_train_stats *stats, void *stream) {
     DeviceScope ds_(c ? c->device : -1);
+    NvtxRange nv_("nasg_train_iteration");
     if (!c || n < 0 || (n > 0 && !samples)) return fail(NASG_ERR_INVALID, "bad argument");
     cudaStream_t s = pick(c, stream);
     if (s != c->stream) {  // the context's own stream carries publish; order it after s

@@ -2,6 +2,7 @@
 // kernel translation units.  Not part of the C ABI.
 #pragma once
 
+#include <nvtx3/nvToolsExt.h>
 #include <cstdint>
 #include <utility>
 #include <cuda_runtime.h>
@@ -37,6 +38,16 @@ __host__ __device__ constexpr int f32_bwd_k(int n) { return packed_width(n) <= 1
 __host__ __device__ constexpr int d4_stride(int n) { return 8 * n + 1 <= 80 ? 80 : 256; }
 
 __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHidden * kHidden + kHidden * (8 * n + 1); }
+
+// NVTX range for the scope of a host call (header-only NVTX 3: free unless a
+// profiler is attached): train iterations / steps, query launches, render
+// iterations and publishes show up as named ranges on the profiler timeline.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 // Makes `dev` current for the scope of one C-ABI call and restores the caller's
 // device afterwards (one process may drive several contexts; a torch rank's
