@@ -55,8 +55,8 @@ namespace {
 // buffer takes [256, 416) and whose NASG warpgroup gets the registers for it.
 constexpr int pairs_for(int n) { return packed_width(n) > 128 ? 1 : 2; }
 constexpr int threads_for(int n) { return 2 * pairs_for(n) * 128; }
-constexpr int kRegsMlp = 104;  // 2 x 128 x (104 + 152) = 64K registers with two pairs
-constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 152 : 232; }
+constexpr int kRegsMlp = 96;  // 2 x 128 x (96 + 160) = 64K registers with two pairs
+constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 160 : 232; }
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one f16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
