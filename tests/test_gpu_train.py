@@ -153,6 +153,30 @@ def test_data_parallel_shards_equal_full_batch(orc):
     g.close()
 
 
+@pytest.mark.parametrize("n,cut", [(4000, 1500), (60000, 21000)])
+def test_data_parallel_shards_equal_full_batch_tensor_core(n, cut):
+    """The same contract on the tensor-core trainer: shards of 1500 / 2500 rows
+    (one tile per CTA) and of 21000 / 39000 rows (more tiles than SMs: the
+    zero-row classification runs on each shard with the shard's own order slice)."""
+    s = H.samples(np.random.default_rng(n), n, zero_p_frac=0.3)
+    g = nasg.Guide(nasg.TrainerConfig(seed=31))
+    g.train_precision = nasg.NASG_MLP_BF16
+    w0 = g.get_weights()
+    ds = torch.from_numpy(s).cuda()
+    order = torch.from_numpy(np.random.default_rng(1).permutation(n).astype(np.int32)).cuda()
+    parts = []
+    for lo, hi in ((0, cut), (cut, n)):
+        g.set_weights(w0)
+        g.train_step(ds, order[lo:], hi - lo, n, 1.0)
+        parts.append(g.last_grad().astype(np.float64))
+        g.train_stats_take()
+    g.set_weights(w0)
+    g.train_step(ds, order, n, n, 1.0)
+    full = g.last_grad()
+    assert rel_l2(parts[0] + parts[1], full) <= 1e-4  # bf16 copies, tensor-core sums in other orders
+    g.close()
+
+
 def test_checkpoint_roundtrip_with_oracle(orc, tmp_path):
     g = nasg.Guide(nasg.TrainerConfig(seed=44))
     p = str(tmp_path / "w.nasg")
