@@ -26,6 +26,18 @@
 #include "tc_common.cuh"
 #include "tc_ptx.cuh"
 
+// Development-only phase timestamps of K_fb (build with EXTRA=-DNASG_TRACE into
+// a scratch directory; the shipped library compiles them out): clock64() of
+// thread 0 of warpgroup 0 in CTA 0 at fixed points of its first 16 tiles.
+#ifdef NASG_TRACE
+__device__ unsigned long long g_fb_trace[16 * 16];
+extern "C" int nasg_fb_trace_read(void *host) { return (int)cudaMemcpyFromSymbol(host, g_fb_trace, sizeof(g_fb_trace)); }
+#define FB_TRACE(k, slot) \
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (k) < 16) g_fb_trace[(k) * 16 + (slot)] = clock64();
+#else
+#define FB_TRACE(k, slot)
+#endif
+
 namespace nasg {
 
 namespace {
@@ -277,6 +289,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
     const uint32_t tmem = *tmem_slot;
     pdl_trigger();
     pdl_wait();  // the weight image, the samples and the classified rows come from earlier work on the stream
+    FB_TRACE(0, 15)
     if (live_count) count = *live_count;  // rows that need the network (order = their list)
     const int64_t ntiles = (count + 127) / 128;
 
@@ -360,11 +373,15 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         };
         load_sample(tile);
         if ((warp & 3) == 0) tc::mbar_wait(w_bar, 0);  // weights resident before the first MMA issue
-        for (; tile < ntiles; tile += stride) {
+        FB_TRACE(0, 14)
+        int ktr = 0;
+        for (; tile < ntiles; tile += stride, ++ktr) {
+            FB_TRACE(ktr, 0)
             const int64_t row = tile * 128 + t;
             const bool valid = row < count;
             clamped += encode_row_f16(valid, s0, s1, s2, bd, inv_ext, a_base + blk_off(t, 64),
                                       tb.h0 + tile * (64 * 256) + blk_off(t, 64));
+            FB_TRACE(ktr, 1)
             issue(0, false);
             uint32_t mask[3][4] = {};  // ReLU gate bits of h1..h3
 #pragma unroll 1
@@ -396,8 +413,10 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     mask[2][q4] = l == 3 ? bits : mask[2][q4];
                 }
                 issue(l, false);
+                FB_TRACE(ktr, 1 + l)
             }
             wait_acc();
+            FB_TRACE(ktr, 5)
             if (coop) coop_sync(2);  // the raw outputs are in tensor memory: helpers may read them
             // ---- KL gradient (fp32 stable forms) straight out of tensor memory:
             // header columns once, each lobe's 8 columns per pass; delta4 goes
@@ -447,6 +466,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
             // 0 invalid row, 1 loss counted, 2 dropped, 3 ok but loss not finite
             const int state = !valid ? 0 : (st == kKlDrop ? 2 : ((st == kKlZero || isfinite(lossf)) ? 1 : 3));
             const double loss = lossf;
+            FB_TRACE(ktr, 6)
             issue(3, true);
             load_sample(tile + stride);  // prefetch: in flight through the backward pass
             {  // tile statistics, deterministic order (warp tree, then warps 0..3)
@@ -522,6 +542,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 }
                 E += k;
                 if (l > 1) issue(l - 1, true);
+                FB_TRACE(ktr, 10 - l)
             });
             tc::tc_fence_before();
         }
