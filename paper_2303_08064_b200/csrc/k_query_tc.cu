@@ -55,8 +55,12 @@ namespace {
 // buffer takes [256, 416) and whose NASG warpgroup gets the registers for it.
 constexpr int pairs_for(int n) { return packed_width(n) > 128 ? 1 : 2; }
 constexpr int threads_for(int n) { return 2 * pairs_for(n) * 128; }
-constexpr int kRegsMlp = 96;  // 2 x 128 x (96 + 160) = 64K registers with two pairs
-constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 160 : 232; }
+// setmaxnreg split between the MLP and the NASG warpgroup (2 x 128 x 256 = 64K
+// registers with two pairs): N = 8 runs NASG-bound (96 / 160 measured +0.9 %
+// over 104 / 152), N = 4's lighter epilogue leaves the MLP side the longer
+// chain (104 / 152: 9.08e9 vs 8.43e9 q/s), N = 16 has one pair
+constexpr int regs_mlp(int n) { return n == 8 ? 96 : 104; }
+constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 256 - regs_mlp(n) : 232; }
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one f16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
@@ -178,7 +182,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 
     if (g < kPairs) {
         // ============================ MLP warpgroup ============================
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(kRegsMlp));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(regs_mlp(N)));
         const uint32_t my_acc = tmem + m * 128 + ((uint32_t)(wq * 32) << 16);
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + m * kABytes);
         const uint32_t e_base = tc::smem_u32(smem + E_OFF + m * kEBytes);
