@@ -24,6 +24,10 @@
 // The MLP chain (4 MMA round trips) is bound by latency, the NASG side by
 // instruction issue; this split keeps the chain free of every instruction
 // that can run elsewhere.  setmaxnreg moves registers from MLP to NASG groups.
+// N = 16 (NP = 160): one MLP warpgroup and two NASG warpgroups ("slots") that
+// take its tiles alternately, each with its own E buffer, input stage and raw
+// buffer (TMEM [128 + 160 j, ...)) — the 16-lobe epilogue is about twice the
+// MLP's work per tile.
 // Only the 52 B/query of inputs and 16-20 B/query of outputs touch HBM.
 #include <cuda_bf16.h>
 
@@ -40,7 +44,7 @@
 __device__ unsigned long long g_trace[2 * 32 * 16];
 extern "C" int nasg_trace_read(void *host) { return (int)cudaMemcpyFromSymbol(host, g_trace, sizeof(g_trace)); }
 #define NASG_TRACE_AT(role, k, slot)                                                   \
-    if (blockIdx.x == 0 && t == 0 && m == 0 && (k) < 32)                               \
+    if (blockIdx.x == 0 && t == 0 && m == 0 && j == 0 && (k) < 32)                     \
         g_trace[((role) * 32 + (k)) * 16 + (slot)] = clock64();
 #else
 #define NASG_TRACE_AT(role, k, slot)
@@ -50,17 +54,30 @@ namespace nasg {
 
 namespace {
 
-// MLP + NASG warpgroup pairs per CTA: two while a pair's raw buffer fits 128
-// TMEM columns (N <= 8: NP <= 80); N = 16 (NP = 160) runs one pair, whose raw
-// buffer takes [256, 416) and whose NASG warpgroup gets the registers for it.
+// MLP warpgroups ("pairs") per CTA and NASG warpgroups ("slots") per MLP
+// warpgroup.  N <= 8 (NP <= 80): two pairs of one MLP + one NASG warpgroup, raw
+// buffers TMEM [256 + 128 m, ...).  N = 16 (NP = 160): one MLP warpgroup feeding
+// two NASG warpgroups that take its tiles alternately (the 16-lobe epilogue is
+// twice the MLP's work per tile), raw buffers TMEM [128, 288) and [288, 448).
 constexpr int pairs_for(int n) { return packed_width(n) > 128 ? 1 : 2; }
-constexpr int threads_for(int n) { return 2 * pairs_for(n) * 128; }
-// setmaxnreg split between the MLP and the NASG warpgroup (2 x 128 x 256 = 64K
-// registers with two pairs): N = 8 runs NASG-bound (96 / 160 measured +0.9 %
-// over 104 / 152), N = 4's lighter epilogue leaves the MLP side the longer
-// chain (104 / 152: 9.08e9 vs 8.43e9 q/s), N = 16 has one pair
-constexpr int regs_mlp(int n) { return n == 8 ? 96 : 104; }
-constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 256 - regs_mlp(n) : 232; }
+constexpr int slots_for(int n) { return packed_width(n) > 128 ? 2 : 1; }
+constexpr int threads_for(int n) { return pairs_for(n) * (1 + slots_for(n)) * 128; }
+constexpr uint32_t raw_col(int n, int lane) {  // first TMEM column of NASG lane (pair m, slot j) = m * S + j
+    return pairs_for(n) == 2 ? 256u + 128u * (uint32_t)lane : 128u + 160u * (uint32_t)lane;
+}
+// setmaxnreg split between the MLP and the NASG warpgroups.  The NASG groups
+// can only grow into what the MLP groups release from the launch allocation
+// (the kernel's register count: 128 at 512 threads, 168 at 384), or they wait
+// forever: P x 4 x (launch - MLP) >= P x S x 4 x (NASG - launch).
+//   N <= 8 (launch 128): N = 8 runs NASG-bound (96 / 160 measured +0.9 % over
+//   104 / 152), N = 4's lighter epilogue leaves the MLP side the longer chain
+//   (104 / 152: 9.50e9 vs 8.46e9 q/s);  N = 16 (launch 168): 96 / 200 / 200.
+constexpr int regs_mlp(int n) { return n == 4 ? 104 : 96; }
+constexpr int launch_regs(int n) { return pairs_for(n) == 2 ? 128 : 168; }
+constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 256 - regs_mlp(n) : 200; }
+static_assert(4 * (launch_regs(16) - regs_mlp(16)) >= 2 * 4 * (regs_nasg(16) - launch_regs(16)),
+              "N = 16: the NASG groups' setmaxnreg.inc fits what the MLP group releases");
+static_assert(4 * (launch_regs(8) - regs_mlp(8)) >= 4 * (regs_nasg(8) - launch_regs(8)), "N = 8 register split");
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one f16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
@@ -69,8 +86,8 @@ constexpr uint32_t kInBytes = 128 * 52;         // one tile of inputs: 13-float 
 
 template <int N>
 constexpr size_t smem_bytes() {
-    constexpr int P = pairs_for(N);
-    return align1k(img_bytes(N)) + P * (kABytes + kEBytes) + 2 * P * kInBytes + (7 * P + 2) * sizeof(uint64_t);
+    constexpr int P = pairs_for(N), Q = pairs_for(N) * slots_for(N);
+    return align1k(img_bytes(N)) + P * kABytes + Q * kEBytes + 2 * Q * kInBytes + (P + 6 * Q + 2) * sizeof(uint64_t);
 }
 
 }  // namespace
@@ -125,27 +142,29 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(threads_for(N), 1)
 query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     constexpr int NP = packed_width(N);
-    constexpr int kPairs = pairs_for(N);
+    constexpr int kPairs = pairs_for(N), S = slots_for(N), Q = kPairs * S;
     constexpr uint32_t IMG = img_bytes(N);
     constexpr uint32_t A_OFF = align1k(IMG);
     extern __shared__ __align__(1024) uint8_t smem[];
-    constexpr uint32_t E_OFF = A_OFF + kPairs * kABytes;    // encoded tiles E_m
-    constexpr uint32_t IN_OFF = E_OFF + kPairs * kEBytes;   // input staging: [pair][2 buffers]
-    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + IN_OFF + 2 * kPairs * kInBytes);
-    uint64_t *raw_full = acc_full + kPairs;
-    uint64_t *raw_empty = raw_full + kPairs;
-    uint64_t *in_full = raw_empty + kPairs;  // [pair][buffer]
-    uint64_t *e_full = in_full + 2 * kPairs;
-    uint64_t *e_empty = e_full + kPairs;
-    uint64_t *w_bar = e_empty + kPairs;
+    constexpr uint32_t E_OFF = A_OFF + kPairs * kABytes;    // encoded tiles E_l, one per NASG lane
+    constexpr uint32_t IN_OFF = E_OFF + Q * kEBytes;        // input staging: [NASG lane][2 buffers]
+    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + IN_OFF + 2 * Q * kInBytes);  // [pair]
+    uint64_t *raw_full = acc_full + kPairs;  // [NASG lane] from here on
+    uint64_t *raw_empty = raw_full + Q;
+    uint64_t *in_full = raw_empty + Q;  // [lane][buffer]
+    uint64_t *e_full = in_full + 2 * Q;
+    uint64_t *e_empty = e_full + Q;
+    uint64_t *w_bar = e_empty + Q;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(w_bar + 1);
     __shared__ int s_clamped;
 
     pdl_trigger();
     pdl_wait();  // the queue (n_dev) and its rows come from the previous kernel on the stream
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int g = warp >> 2;        // warpgroup 0..3: named barrier g + 1
-    const int m = g % kPairs;       // pair
+    const int g = warp >> 2;        // warpgroup: named barrier g + 1
+    // warpgroups [0, P): MLP of pair g; then the NASG warpgroups, lane (pair m, slot j)
+    const int m = g < kPairs ? g : (g - kPairs) % kPairs;
+    const int j = g < kPairs ? 0 : (g - kPairs) / kPairs;
     const int wq = warp & 3;        // TMEM lane quarter of this warp
     const int t = threadIdx.x & 127;
     const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
@@ -156,8 +175,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     if ((int64_t)blockIdx.x * kPairs >= ntiles) return;
 
     if (threadIdx.x == 0) {
-        for (int i = 0; i < kPairs; ++i) {
-            tc::mbar_init(&acc_full[i], 1);
+        for (int i = 0; i < kPairs; ++i) tc::mbar_init(&acc_full[i], 1);
+        for (int i = 0; i < Q; ++i) {
             tc::mbar_init(&raw_full[i], 1);
             tc::mbar_init(&raw_empty[i], 4);  // one arrival per NASG warp
             tc::mbar_init(&in_full[2 * i], 1);
@@ -185,15 +204,18 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(regs_mlp(N)));
         const uint32_t my_acc = tmem + m * 128 + ((uint32_t)(wq * 32) << 16);
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + m * kABytes);
-        const uint32_t e_base = tc::smem_u32(smem + E_OFF + m * kEBytes);
+        const uint32_t e_base0 = tc::smem_u32(smem + E_OFF + m * S * kEBytes);  // + slot * kEBytes
         const uint32_t a_row128 = a_base + (t >> 3) * 2048 + (t & 7) * 16;  // K = 128 layout
         const uint32_t sW = tc::smem_u32(smem);
         uint32_t acc_ph = 0;
         // The A operand is complete in smem (and our TMEM reads are done): warp 0
-        // issues layer L with one elected lane.  Layer 0 reads E_m (once the NASG
-        // group has filled it), layers 1-2 accumulate into the group's TMEM
-        // columns, the output layer into the pair's raw buffer once it is empty.
+        // issues layer L with one elected lane.  Layer 0 reads E of the NASG lane
+        // that owns tile k (once it has filled it), layers 1-2 accumulate into the
+        // group's TMEM columns, the output layer into that lane's raw buffer once
+        // it is empty.  Tile k of the pair goes to slot k % S.
         auto issue = [&](int L, int64_t k) {
+            const int lk = m * S + (int)(k % S);
+            const int64_t ks = k / S;  // use count of that lane's buffers
             if (L > 0) {
                 tc::fence_proxy_async_smem();
                 tc::tc_fence_before();
@@ -201,8 +223,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             }
             if (wq == 0) {
                 __syncwarp();
-                if (L == 0) tc::mbar_wait(&e_full[m], (uint32_t)(k & 1));
-                if (L == 3 && k > 0) tc::mbar_wait(&raw_empty[m], (uint32_t)((k - 1) & 1));
+                if (L == 0) tc::mbar_wait(&e_full[lk], (uint32_t)(ks & 1));
+                if (L == 3 && ks > 0) tc::mbar_wait(&raw_empty[lk], (uint32_t)((ks - 1) & 1));
                 tc::tc_fence_after();
                 auto chain = [&](auto lc) {
                     constexpr int LL = decltype(lc)::value;
@@ -211,16 +233,16 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     // descriptors rebuilt at issue time from opaque copies of the base
                     // addresses: hoisted out of the tile loop they would occupy ~60
                     // registers and spill
-                    const uint32_t abase = tc::opaque(LL == 0 ? e_base : a_base);
+                    const uint32_t abase = tc::opaque(LL == 0 ? e_base0 + (uint32_t)(k % S) * kEBytes : a_base);
                     const uint32_t bbase = tc::opaque(sW) + w_off(LL);
                     const uint64_t ad = tc::smem_desc(abase, 128, K * 16);
                     const uint64_t bd = tc::smem_desc(bbase, 128, K * 16);
-                    const uint32_t d = tmem + (LL == 3 ? 256 : 0) + m * 128;
+                    const uint32_t d = tmem + (LL == 3 ? raw_col(N, lk) : (uint32_t)m * 128u);
 #pragma unroll
                     for (int kk = 0; kk < K / 16; ++kk)  // +256 B per K=16 slab = +16 in the address field
                         tc::mma_bf16_elect(d, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc,
                                            kk > 0 ? 1u : 0u);
-                    tc::mma_commit_elect(LL == 3 ? &raw_full[m] : &acc_full[m]);
+                    tc::mma_commit_elect(LL == 3 ? &raw_full[lk] : &acc_full[m]);
                 };
                 switch (L) {
                     case 0: chain(std::integral_constant<int, 0>{}); break;
@@ -242,7 +264,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 //  which still read the A tile: commits track all earlier MMAs)
                 wg_wait_acc(&acc_full[m], acc_ph, g, wq);
                 NASG_TRACE_AT(0, k, 2 * l)
-                if (l == 1 && t == 0) tc::mbar_arrive(&e_empty[m]);  // layer 0 has consumed E_m
+                if (l == 1 && t == 0) tc::mbar_arrive(&e_empty[m * S + (int)(k % S)]);  // layer 0 has consumed E
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
                     float v[32];
@@ -264,8 +286,10 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     } else {
         // ============================ NASG warpgroup ===========================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(regs_nasg(N)));
-        const uint32_t my_raw = tmem + 256 + m * 128 + ((uint32_t)(wq * 32) << 16);
-        const uint32_t e_row64 = tc::smem_u32(smem + E_OFF + m * kEBytes) + (t >> 3) * 1024 + (t & 7) * 16;
+        const int ln = m * S + j;  // this warpgroup's NASG lane: its E, input stage and raw buffer
+        const uint32_t my_raw = tmem + raw_col(N, ln) + ((uint32_t)(wq * 32) << 16);
+        const uint32_t e_row64 = tc::smem_u32(smem + E_OFF + ln * kEBytes) + (t >> 3) * 1024 + (t & 7) * 16;
+        const int64_t lstride = stride * S;  // this lane's tiles: every S-th tile of the pair
         const float(&inv_ext)[3] = a.bounds.inv_ext;
         int clamped = 0;
         // Inputs arrive two tiles ahead by TMA bulk copies into a double-buffered
@@ -274,8 +298,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         auto load_tile = [&](int64_t tl, int buf) {  // thread 0 only
             if (tl >= ntiles) return;
             const int64_t q0 = tl * 128, rows = min((int64_t)128, nrows - q0);
-            uint64_t *bar = &in_full[2 * m + buf];
-            uint8_t *dst = smem + IN_OFF + (2 * m + buf) * kInBytes;
+            uint64_t *bar = &in_full[2 * ln + buf];
+            uint8_t *dst = smem + IN_OFF + (2 * ln + buf) * kInBytes;
             if (!tma_in) {
                 tc::mbar_arrive_expect_tx(bar, 0);
             } else if (a.packed) {
@@ -290,14 +314,14 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 tc::bulk_g2s(dst + 4096, a.nrm + q0, bytes, bar);
             }
         };
-        // encode tile tl (the pair's kt-th) into E_m and hand it to the MLP group
+        // encode tile tl (this lane's kt-th) into its E and hand it to the MLP group
         auto encode = [&](int64_t tl, int64_t kt) {
             const int buf = (int)(kt & 1);
-            tc::mbar_wait(&in_full[2 * m + buf], (uint32_t)((kt >> 1) & 1));
+            tc::mbar_wait(&in_full[2 * ln + buf], (uint32_t)((kt >> 1) & 1));
             const int64_t q = tl * 128 + t;
             const bool valid = q < nrows;
             float4 x = make_float4(0.f, 0.f, 0.f, 0.f), wo = x, nrm = x;
-            const uint8_t *src = smem + IN_OFF + (2 * m + buf) * kInBytes;
+            const uint8_t *src = smem + IN_OFF + (2 * ln + buf) * kInBytes;
             if (valid) {
                 if (!tma_in) {
                     load_query(a, q, x, wo, nrm);
@@ -323,25 +347,25 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             tc::fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core
             wg_sync(g);
             if (t == 0) {
-                tc::mbar_arrive(&e_full[m]);
-                load_tile(tl + 2 * stride, buf);  // every row of this buffer has been read
+                tc::mbar_arrive(&e_full[ln]);
+                load_tile(tl + 2 * lstride, buf);  // every row of this buffer has been read
             }
         };
-        int64_t tile = (int64_t)blockIdx.x * kPairs + m;
+        int64_t tile = (int64_t)blockIdx.x * kPairs + m + (int64_t)j * stride;
         if (t == 0) {
             load_tile(tile, 0);
-            load_tile(tile + stride, 1);
+            load_tile(tile + lstride, 1);
         }
         if (tile < ntiles) encode(tile, 0);
         uint32_t e_ph = 0;
-        for (int64_t k = 0; tile < ntiles; tile += stride, ++k) {
+        for (int64_t k = 0; tile < ntiles; tile += lstride, ++k) {
             // the next tile's encoding first: the MLP needs it right after this
             // tile's output layer, the raw outputs arrive only then
             NASG_TRACE_AT(1, k, 0)
-            if (tile + stride < ntiles) {
-                wg_wait_acc(&e_empty[m], e_ph, g, wq);
+            if (tile + lstride < ntiles) {
+                wg_wait_acc(&e_empty[ln], e_ph, g, wq);
                 NASG_TRACE_AT(1, k, 1)
-                encode(tile + stride, k + 1);
+                encode(tile + lstride, k + 1);
             }
             NASG_TRACE_AT(1, k, 2)
             const int64_t q = tile * 128 + t;
@@ -360,7 +384,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 }
             }
             uint32_t ph = (uint32_t)(k & 1);
-            wg_wait_acc(&raw_full[m], ph, g, wq);
+            wg_wait_acc(&raw_full[ln], ph, g, wq);
             NASG_TRACE_AT(1, k, 3)
             float raw[NP];
             {
@@ -382,7 +406,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             }
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&raw_empty[m]);  // buffer free for the next output layer
+            if (lane == 0) tc::mbar_arrive(&raw_empty[ln]);  // buffer free for the next output layer
             if (valid) {
                 auto rawf = [&](int j) { return raw[j]; };
                 if constexpr (MODE == kModeSample) {
@@ -430,6 +454,9 @@ static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int n
 #define NASG_LAUNCH_TC(M)                                                                  \
     case M: {                                                                              \
         auto k = query_tc_kernel<N, M>;                                                    \
+        cudaFuncAttributes fa;                                                             \
+        if (cudaFuncGetAttributes(&fa, k) != cudaSuccess || fa.numRegs != launch_regs(N))  \
+            return -2; /* the setmaxnreg split assumes this launch allocation */           \
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
         launch_pdl(pdl, k, dim3(grid), dim3(threads_for(N)), sm, s, im, a);                 \
         break;                                                                             \

@@ -379,6 +379,7 @@ int run_query(nasg_ctx *c, QueryMode mode, const QueryArgs &a, cudaStream_t s) {
     } else {
         r = query_fp32(c->N, mode, c->wp_pub, a, c->num_sms, s);
     }
+    if (r == -2) return fail(NASG_ERR_CUDA, "query kernel register allocation differs from its setmaxnreg split");
     if (r < 0) return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for this path");
     c->launches += r;
     CHECK_LAUNCH();
