@@ -454,9 +454,11 @@ static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int n
 #define NASG_LAUNCH_TC(M)                                                                  \
     case M: {                                                                              \
         auto k = query_tc_kernel<N, M>;                                                    \
-        cudaFuncAttributes fa;                                                             \
-        if (cudaFuncGetAttributes(&fa, k) != cudaSuccess || fa.numRegs != launch_regs(N))  \
-            return -2; /* the setmaxnreg split assumes this launch allocation */           \
+        static const bool regs_ok = [&] {  /* the setmaxnreg split assumes this allocation */ \
+            cudaFuncAttributes fa;                                                         \
+            return cudaFuncGetAttributes(&fa, k) == cudaSuccess && fa.numRegs == launch_regs(N); \
+        }();                                                                               \
+        if (!regs_ok) return -2;                                                           \
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
         launch_pdl(pdl, k, dim3(grid), dim3(threads_for(N)), sm, s, im, a);                 \
         break;                                                                             \

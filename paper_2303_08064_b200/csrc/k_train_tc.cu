@@ -220,7 +220,10 @@ train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint3
                 const int64_t idx = j - lane;
                 unsigned long long w = idx >= 0 ? *(volatile unsigned long long *)(state + idx) : (tag | kP);
                 const bool ready = (w >> (kClsValBits + 2)) == epoch && (w & (kA | kP));
-                if (!__all_sync(0xffffffffu, ready)) continue;  // a predecessor has not published yet
+                if (!__all_sync(0xffffffffu, ready)) {  // a predecessor has not published yet
+                    __nanosleep(32);
+                    continue;
+                }
                 const uint32_t pm = __ballot_sync(0xffffffffu, (w & kP) != 0);
                 const int stop = pm ? __ffs(pm) - 1 : 31;  // nearest inclusive prefix in the window
                 long long v = lane <= stop ? (long long)(w & vmask) : 0;
