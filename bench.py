@@ -344,18 +344,21 @@ def bench_train(g_cls, nasg, args, ws, rank, precision):
     # rows with p = 0 need no network pass (zero gradient, loss 0: guiding.cpp:112,170):
     # the executed work is the live rows' 279,296 FLOP each
     live = float(np.mean(s[:, 3].cpu().numpy() != 0.0)) if precision == "bf16" else 1.0
-    tf = rate / ws * live * FLOP_PER_SAMPLE / 1e12
+    # algorithmic FLOP of the step (279,296 per training sample: fwd + dW +
+    # delta) against the bf16 tensor peak; the executed FLOP are the rows that need the
+    # network (p != 0, `live_row_fraction`), the zero-gradient rows are classified and
+    # counted without it.  The step also moves ~1.7 KB per live row of bf16 activations
+    # through HBM twice for the split-K dW GEMM (K_dw is HBM-bound, profiles/r2_ncu_summary.md)
+    tf = rate / ws * FLOP_PER_SAMPLE / 1e12
     pk, pk_kind = peaks()
-    # executed FLOP of the step (fwd + dW + delta, 279,296 per live sample) against the
-    # bf16 tensor peak; the step also moves 1,696 B per live sample of bf16 activations
-    # through HBM twice for the split-K dW GEMM (K_dw is HBM-bound, profiles/r1_train_bf16_ncu.md)
     roof = {"bound": "tensor" if precision == "bf16" else "fp32-ffma", "achieved": tf, "unit": "TFLOP/s",
             "peak": pk["bf16_tflops"] if precision == "bf16" else FP32_FFMA_TFLOPS,
             "peak_kind": f"{pk_kind} bf16 burst" if precision == "bf16" else FP32_PEAK_KIND,
-            "live_row_fraction": live,
-            "note": "FLOP counted for the rows that need the network (p != 0); the zero-gradient rows "
-                    "are classified and counted without it" if precision == "bf16" else "every row"}
+            "live_row_fraction": live, "executed_tflops": tf * live, "executed_frac": None,
+            "note": "achieved = samples/s x 279,296 algorithmic FLOP per sample; executed = the rows with "
+                    "p != 0, which are the only ones through the network" if precision == "bf16" else "every row"}
     roof["frac"] = tf / roof["peak"]
+    roof["executed_frac"] = tf * live / roof["peak"]
     out = {"metric": f"train samples/s (config 3: 2^18 samples/step/GPU, fused fwd+KL+bwd+dW+Adam, {precision})",
            "value": rate, "unit": "samples/s", "ms_per_step": 1e3 * t / args.train_steps,
            "achieved_tflops": tf, "roofline": roof, "e2e": e2e, "dtype": precision,
