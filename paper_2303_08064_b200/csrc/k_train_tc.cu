@@ -1,15 +1,19 @@
-// bf16 tensor-core training step (Trainer::train_iteration inner loop,
-// guiding.cpp:236-276) — the fast training path; fp32 master weights + Adam.
+// Tensor-core training step (NASG_MLP_BF16; Trainer::train_iteration inner
+// loop, guiding.cpp:236-276) — the fast training path; fp32 master weights + Adam.
 //
-//   K_fb (train_tc_fb_kernel)  persistent, 3 epilogue warpgroups x 128-row tiles,
-//        like the query kernel: gather + encode -> 4 forward UMMA layers (TMEM
-//        accumulators, ReLU fused into the bf16 conversion, ReLU gate bits kept
-//        in registers) -> KL gradient of every row in fp32 (kl_grad_row_fast,
-//        nasg_math.cuh; guiding.cpp:108-165) -> delta4 -> 3 backward UMMA
-//        layers delta_l = (delta_{l+1} W_l^T) .* [h_l > 0] (net.hpp:101-107)
-//        that read the SAME smem weight images as the forward, as MN-major B
-//        operands.  Every h_l / delta_l tile is written once to HBM as bf16 in
-//        the tensor-core's core-matrix layout.
+//   classify (train_classify_kernel, steps with more tiles than SMs): the rows
+//        with p = 0 are counted as zero-gradient rows; the others form the list
+//        K_fb and K_dw work on.
+//   K_fb (train_tc_fb_kernel)  persistent, 3 epilogue warpgroups x 128-row tiles
+//        (1 at N = 16), like the query kernel: gather + encode -> 4 forward UMMA
+//        layers on f16 operands (TMEM accumulators, ReLU fused into the f16
+//        conversion, ReLU gate bits kept in registers) -> KL gradient of every
+//        row in fp32 (kl_grad_row_fast, nasg_math.cuh; guiding.cpp:108-165) ->
+//        delta4 (bf16) -> 3 backward UMMA layers delta_l = (delta_{l+1} W_l^T)
+//        .* [h_l > 0] (net.hpp:101-107) that read the SAME smem weight image as
+//        the forward as MN-major B operands (through a bf16 copy of W4 for
+//        delta4, then row-scaled f16 deltas).  Every h_l / delta_l tile is
+//        written once to HBM as bf16 in the tensor core's core-matrix layout.
 //   K_dw (train_tc_dw_kernel)  dW_l = h_l^T delta_{l+1} (net.hpp:102) as a
 //        split-K UMMA GEMM over 128-row blocks: both operands MN-major, TMA
 //        bulk copies into a 2-stage smem ring, fp32 accumulation in TMEM,
@@ -102,11 +106,11 @@ __device__ __forceinline__ void tmem_ld_hdr(uint32_t taddr, float (&h)[HD]) {
     else tc::tmem_ld32(taddr, h);
 }
 
-// ReLU gate flags of the 16 packed bf16 pairs (32 columns) of a drain chunk in
+// ReLU gate flags of the 16 packed f16 pairs (32 columns) of a drain chunk in
 // one register: pair j's halves set bits 15 - j and 31 - j.  After the ReLU
-// conversion every half is a non-negative bf16 <= 0x7FC0, so adding 0x7FFF to
-// it sets its top bit exactly when it is non-zero, without a carry into the
-// other half (3 instructions per pair: add, shift, and-or).
+// satfinite conversion every half is a non-negative f16 <= 0x7BFF, so adding
+// 0x7FFF to it sets its top bit exactly when it is non-zero, without a carry
+// into the other half (3 instructions per pair: add, shift, and-or).
 __device__ __forceinline__ uint32_t gate_flags(uint32_t acc, uint32_t p, int j) {
     const uint32_t q = p + 0x7FFF7FFFu;
     return acc | ((q >> j) & (0x80008000u >> j));
