@@ -59,8 +59,8 @@ template <int N>
 __global__ void __launch_bounds__(256, 1)
 train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
                 const nasg_train_sample *__restrict__ samples, const uint32_t *__restrict__ order,
-                int64_t count, double gscale, double b, double e, Bounds bd, TrainScratch sc,
-                unsigned long long *clamp_count) {
+                int64_t count, const int64_t *live_count, double gscale, double b, double e, Bounds bd,
+                TrainScratch sc, unsigned long long *clamp_count) {
     constexpr int H = packed_header(N), NP = packed_width(N), D = 8 * N + 1;
     extern __shared__ __align__(16) float sm[];
     float *h0 = sm + kOffH0, *h1 = sm + kOffH1, *h2 = sm + kOffH2, *h3 = sm + kOffH3;
@@ -72,6 +72,7 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
     const int tid = threadIdx.x;
     const float *W1 = wp, *W2 = W1 + kIn * kHidden, *W3 = W2 + kHidden * kHidden, *W4 = W3 + kHidden * kHidden;
     const float *T2 = wtp, *T3 = T2 + kHidden * kHidden, *T4 = T3 + kHidden * kHidden;
+    if (live_count) count = *live_count;  // the classified step: rows that need the network (order = their list)
     const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
     if (tid == 0) s_clamped = 0;
     __syncthreads();
@@ -180,9 +181,9 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
 }
 
 int train_forward_backward(int n_comp, const float *wp, const float *wtp, const nasg_train_sample *samples,
-                           const uint32_t *order, int64_t count, int64_t global_count, double b, double loss_blend,
-                           const Bounds &bounds, TrainScratch &sc, int num_sms, unsigned long long *clamp_count,
-                           cudaStream_t s) {
+                           const uint32_t *order, int64_t count, const int64_t *live_count, int64_t global_count,
+                           double b, double loss_blend, const Bounds &bounds, TrainScratch &sc, int num_sms,
+                           unsigned long long *clamp_count, cudaStream_t s) {
     const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
     if (ntiles == 0) return 0;
     const int grid = ntiles < num_sms ? ntiles : num_sms;
@@ -190,7 +191,8 @@ int train_forward_backward(int n_comp, const float *wp, const float *wtp, const 
     if (n_comp != 8 && n_comp != 4 && n_comp != 16) return -1;
     auto k = n_comp == 8 ? train_fb_kernel<8> : (n_comp == 4 ? train_fb_kernel<4> : train_fb_kernel<16>);
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
-    k<<<grid, 256, kFbSmem, s>>>(wp, wtp, samples, order, count, gscale, b, loss_blend, bounds, sc, clamp_count);
+    k<<<grid, 256, kFbSmem, s>>>(wp, wtp, samples, order, count, live_count, gscale, b, loss_blend, bounds, sc,
+                                 clamp_count);
     return 1;
 }
 
@@ -199,11 +201,17 @@ int train_forward_backward(int n_comp, const float *wp, const float *wtp, const 
 template <int M>
 __global__ void __launch_bounds__(256)
 dw_kernel(const float *__restrict__ Hm, const float *__restrict__ Dm, int ldd, int n_out, int ldo,
-          int64_t rows, int rows_per_split, float *__restrict__ partial, size_t partial_stride) {
+          int64_t rows, int rows_per_split, float *__restrict__ partial, size_t partial_stride,
+          const int64_t *live_count) {
     __shared__ __align__(16) float As[2][kChunk][M];
     __shared__ __align__(16) float Bs[2][kChunk][128];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
     const int split = blockIdx.x;
+    if (live_count) {  // the classified step: its rows, spread over the launched splits
+        rows = ((*live_count + kTrainRows - 1) / kTrainRows) * kTrainRows;
+        rows_per_split = (int)((rows + gridDim.x - 1) / gridDim.x);
+        rows_per_split = ((rows_per_split + kChunk - 1) / kChunk) * kChunk;
+    }
     const int64_t r0 = (int64_t)split * rows_per_split;
     const int64_t r1 = min(rows, r0 + rows_per_split);
     constexpr int RM = M / 16;
@@ -278,7 +286,9 @@ __global__ void dw_reduce_kernel(const float *__restrict__ partial, int splits, 
     if (!isfinite(s)) atomicOr(nonfinite, 1);
 }
 
-int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStream_t s) {
+// live_count (the classified step): the row count on the device, the splits
+// re-spread over it by the kernel; splits without rows write zero partials.
+int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStream_t s, const int64_t *live_count) {
     const int D = 8 * n_comp + 1;
     const int nw = n_weights(n_comp);
     const int64_t rows = ((count + kTrainRows - 1) / kTrainRows) * kTrainRows;  // zero-padded tail
@@ -290,14 +300,14 @@ int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStrea
     const size_t stride = (size_t)nw;
     float *p = sc.dw_partial;
     const size_t o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
-    dw_kernel<64><<<splits, 256, 0, s>>>(sc.h0, sc.d1, 128, 128, 128, rows, rps, p, stride);
-    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h1, sc.d2, 128, 128, 128, rows, rps, p + o1, stride);
-    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h2, sc.d3, 128, 128, 128, rows, rps, p + o2, stride);
+    dw_kernel<64><<<splits, 256, 0, s>>>(sc.h0, sc.d1, 128, 128, 128, rows, rps, p, stride, live_count);
+    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h1, sc.d2, 128, 128, 128, rows, rps, p + o1, stride, live_count);
+    dw_kernel<128><<<splits, 256, 0, s>>>(sc.h2, sc.d3, 128, 128, 128, rows, rps, p + o2, stride, live_count);
     // dW4 [128][D] in 128-column blocks of delta4 (two for N = 16)
     const int ds = d4_stride(n_comp);
     for (int c0 = 0; c0 < D; c0 += 128)
         dw_kernel<128><<<splits, 256, 0, s>>>(sc.h3, sc.d4 + c0, ds, D - c0 < 128 ? D - c0 : 128, D, rows, rps,
-                                               p + o3 + c0, stride);
+                                               p + o3 + c0, stride, live_count);
     sc.last_splits = splits;
     return 3 + (D + 127) / 128;  // launches
 }
@@ -312,9 +322,10 @@ int train_reduce(int n_comp, const TrainScratch &sc, float *grad, int *nonfinite
 // One block: strided per-thread partial sums, then a fixed-shape tree
 // (deterministic for a given tile count).
 __global__ void step_stats_kernel(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
-                                  double *step_stats) {
+                                  double *step_stats, const int64_t *cls, int tile_rows) {
     __shared__ double sl[256], sc[256], sd[256];
     const int t = threadIdx.x;
+    if (cls) ntiles = (int)((cls[0] + tile_rows - 1) / tile_rows);  // the classified step's tiles
     double ls = 0.0, lc = 0.0, dr = 0.0;
     for (int i = t; i < ntiles; i += 256) {
         ls += tile_loss[i];
@@ -333,20 +344,22 @@ __global__ void step_stats_kernel(const double *tile_loss, const int *tile_lc, c
     }
     if (t == 0) {
         step_stats[0] = sl[0];
-        step_stats[1] = sc[0];
+        step_stats[1] = sc[0] + (cls ? (double)cls[1] : 0.0);  // zero-gradient rows: loss 0, counted
         step_stats[2] = sd[0];
     }
 }
 
 int train_step_stats_n(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
                        double *step_stats, cudaStream_t s) {
-    step_stats_kernel<<<1, 256, 0, s>>>(tile_loss, tile_lc, tile_dr, ntiles, step_stats);
+    step_stats_kernel<<<1, 256, 0, s>>>(tile_loss, tile_lc, tile_dr, ntiles, step_stats, nullptr, 1);
     return 1;
 }
 
-int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s) {
+int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s, const int64_t *cls) {
     const int ntiles = (int)((count + kTrainRows - 1) / kTrainRows);
-    return train_step_stats_n(sc.tile_loss, sc.tile_loss_count, sc.tile_dropped, ntiles, step_stats, s);
+    step_stats_kernel<<<1, 256, 0, s>>>(sc.tile_loss, sc.tile_loss_count, sc.tile_dropped, ntiles, step_stats, cls,
+                                        kTrainRows);
+    return 1;
 }
 
 

@@ -752,6 +752,18 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
     if (!isfinite(s)) atomicOr(nonfinite, 1);
 }
 
+int train_classify(const nasg_train_sample *samples, const uint32_t *order, int64_t count, TcTrainBufs &tb,
+                   const Bounds &bounds, unsigned long long *clamp_count, cudaStream_t s, bool pdl) {
+    const int nblk = (int)((count + kClsRows - 1) / kClsRows);
+    if (++tb.scan_epoch >= (1u << kClsEpochBits)) {  // look-back tags wrapped: start clean
+        cudaMemsetAsync(tb.scan_state, 0, tb.scan_cap * sizeof(unsigned long long), s);
+        tb.scan_epoch = 1;
+    }
+    launch_pdl(pdl, train_classify_kernel, dim3(nblk), dim3(kClsThreads), 0, s, samples, order, count, tb.wbig, bounds,
+               tb.live, tb.scan_state, tb.scan_epoch, tb.cls, clamp_count);
+    return 1;
+}
+
 int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples, const uint32_t *order, int64_t count,
                   int64_t global_count, double b, double loss_blend, const Bounds &bounds, TcTrainBufs &tb,
                   int num_sms, unsigned long long *clamp_count, float *grad, int *nonfinite, cudaStream_t s,
@@ -769,16 +781,9 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
         const int64_t *live_count = nullptr;
         const uint32_t *rows = order;
         if (tb.skip_zero && ntiles > num_sms) {
-            const int nblk = (int)((count + kClsRows - 1) / kClsRows);
-            if (++tb.scan_epoch >= (1u << kClsEpochBits)) {  // look-back tags wrapped: start clean
-                cudaMemsetAsync(tb.scan_state, 0, tb.scan_cap * sizeof(unsigned long long), s);
-                tb.scan_epoch = 1;
-            }
-            launch_pdl(pdl, train_classify_kernel, dim3(nblk), dim3(kClsThreads), 0, s, samples, order, count, tb.wbig,
-                       bounds, tb.live, tb.scan_state, tb.scan_epoch, tb.cls, clamp_count);
+            launches += train_classify(samples, order, count, tb, bounds, clamp_count, s, pdl);
             live_count = tb.cls;
             rows = tb.live;
-            ++launches;
         }
         const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
         const uint8_t *im = static_cast<const uint8_t *>(img);

@@ -341,19 +341,29 @@ int ensure_tc_scratch(nasg_ctx *c, int64_t count) {
         const int ps = packed_width(c->N) > 128 ? packed_width(c->N) : 128;  // partial_stride (k_train_tc.cu)
         CUDA_TRY(cudaMalloc(&t.partial, (size_t)4 * 2 * 37 * 128 * ps * sizeof(float)));
     }
+    t.step_stats = c->d_step_stats;
+    t.max_blocks = blocks;
+    return NASG_OK;
+}
+
+// The zero-row classification's buffers (train_classify, both trainers): the
+// step's row list (u32 per row), one look-back word per 1024 rows, {live, zero}.
+int ensure_classify(nasg_ctx *c, int64_t count) {
+    TcTrainBufs &t = c->tcb;
+    const int64_t rows = ((count + 1023) / 1024) * 1024;
+    if (!t.cls) CUDA_TRY(cudaMalloc(&t.cls, 2 * sizeof(int64_t)));
+    t.wbig = c->d_wbig;
+    if (rows <= t.live_cap) return NASG_OK;
     if (t.live) cudaFree(t.live);
     if (t.scan_state) cudaFree(t.scan_state);
     t.live = nullptr;
     t.scan_state = nullptr;
-    t.scan_cap = (blocks * 128 + 1023) / 1024;
-    CUDA_TRY(cudaMalloc(&t.live, (size_t)blocks * 128 * sizeof(uint32_t)));
+    t.scan_cap = rows / 1024;
+    CUDA_TRY(cudaMalloc(&t.live, (size_t)rows * sizeof(uint32_t)));
     CUDA_TRY(cudaMalloc(&t.scan_state, (size_t)t.scan_cap * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemset(t.scan_state, 0, (size_t)t.scan_cap * sizeof(unsigned long long)));
     t.scan_epoch = 0;
-    if (!t.cls) CUDA_TRY(cudaMalloc(&t.cls, 2 * sizeof(int64_t)));
-    t.wbig = c->d_wbig;
-    t.step_stats = c->d_step_stats;
-    t.max_blocks = blocks;
+    t.live_cap = rows;
     return NASG_OK;
 }
 
@@ -396,6 +406,7 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
     if (count <= 0 && c->nranks == 1) return NASG_OK;
     const bool tc = c->train_precision == NASG_MLP_BF16;
     int r = tc ? ensure_tc_scratch(c, std::max<int64_t>(count, 1)) : ensure_scratch(c, std::max<int64_t>(count, 1));
+    if (!r) r = ensure_classify(c, std::max<int64_t>(count, 1));
     if (r) return r;
     if (count > 0 && tc) {
         const int k = train_tc_step(c->N, c->tc_live, samples, order, count, global_count, b, c->cfg.loss_blend,
@@ -403,12 +414,21 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
         if (k < 0) return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for bf16 training");
         c->launches += k;
     } else if (count > 0) {
-        if (train_forward_backward(c->N, c->wp, c->wtp, samples, order, count, global_count, b,
+        // zero-gradient rows out of the network pass, as on the tensor-core path,
+        // when the step has more 64-row tiles than SMs
+        const int64_t *live_count = nullptr;
+        const uint32_t *rows = order;
+        if (c->tcb.skip_zero && (count + 63) / 64 > c->num_sms) {
+            c->launches += train_classify(samples, order, count, c->tcb, c->bounds, clamp, s, false);
+            live_count = c->tcb.cls;
+            rows = c->tcb.live;
+        }
+        if (train_forward_backward(c->N, c->wp, c->wtp, samples, rows, count, live_count, global_count, b,
                                    c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, clamp, s) < 0)
             return fail(NASG_ERR_UNSUPPORTED, "n_components not compiled for training");
-        const int ndw = train_dw(c->N, count, c->sc, c->grad, s);
+        const int ndw = train_dw(c->N, count, c->sc, c->grad, s, live_count);
         train_reduce(c->N, c->sc, c->grad, c->d_nonfinite, s);
-        train_step_stats(c->sc, count, c->d_step_stats, s);
+        train_step_stats(c->sc, count, c->d_step_stats, s, live_count);
         c->launches += 3 + ndw;  // forward/backward, dW GEMMs, reduction, statistics
     } else {
         CUDA_TRY(cudaMemsetAsync(c->grad, 0, c->nw * sizeof(float), s));

@@ -241,6 +241,7 @@ struct TcTrainBufs {
     int64_t *cls = nullptr;
     unsigned long long *scan_state = nullptr;  // decoupled look-back words, one per classify block
     int64_t scan_cap = 0;
+    int64_t live_cap = 0;
     uint32_t scan_epoch = 0;
     const int *wbig = nullptr;  // set while some weight is >= kSafeWeight (or not finite)
 };
@@ -252,15 +253,23 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
 int train_step_stats_n(const double *tile_loss, const int *tile_lc, const int *tile_dr, int ntiles,
                        double *step_stats, cudaStream_t s);
 
+// live_count (nullable): the classified step's row count on the device (order = its list)
 int train_forward_backward(int n_comp, const float *wp, const float *wtp,
                            const nasg_train_sample *samples, const uint32_t *order,
-                           int64_t count, int64_t global_count, double b, double loss_blend,
-                           const Bounds &bounds, TrainScratch &sc, int num_sms,
+                           int64_t count, const int64_t *live_count, int64_t global_count, double b,
+                           double loss_blend, const Bounds &bounds, TrainScratch &sc, int num_sms,
                            unsigned long long *clamp_count, cudaStream_t s);
-int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStream_t s);
+int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStream_t s,
+             const int64_t *live_count = nullptr);
 int train_reduce(int n_comp, const TrainScratch &sc, float *grad, int *nonfinite, cudaStream_t s);
 int check_finite(const float *x, int n, int *nonfinite, cudaStream_t s);
-int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s);
+int train_step_stats(const TrainScratch &sc, int64_t count, double *step_stats, cudaStream_t s,
+                     const int64_t *cls = nullptr);
+// zero-gradient row classification (k_train_tc.cu): the step's rows through the
+// epoch order; p = 0 rows (finite inputs, weights below kSafeWeight) counted in
+// tb.cls[1] (their encode clamps counted), the others listed in tb.live, tb.cls[0]
+int train_classify(const nasg_train_sample *samples, const uint32_t *order, int64_t count, TcTrainBufs &tb,
+                   const Bounds &bounds, unsigned long long *clamp_count, cudaStream_t s, bool pdl);
 // skip decision, Adam t / bias corrections, accumulation of step stats into
 // acc[0..4] = loss_sum, loss_count, dropped, skipped, steps
 // Fused optimizer tail of one step (skip decision, t, bias corrections,

@@ -30,10 +30,10 @@ def rel_l2(a, b):
     return np.linalg.norm(a - b) / nb if nb > 0 else np.linalg.norm(a)
 
 
-def step(s, skip, n_comp=8, weights=None, outside=False):
+def step(s, skip, n_comp=8, weights=None, outside=False, prec=nasg.NASG_MLP_BF16):
     n = len(s)
     g = nasg.Guide(nasg.TrainerConfig(seed=13, batch_size=n, sample_capacity=n, n_components=n_comp))
-    g.train_precision = nasg.NASG_MLP_BF16
+    g.train_precision = prec
     g.zero_row_skip = skip
     if weights is not None:
         g.set_weights(weights)
@@ -79,6 +79,22 @@ def test_skip_matches_full_pass(n_comp, n, zero_frac):
     else:  # every row zero: zero gradient, the Adam step is still taken
         assert not np.any(g1) and not np.any(g0)
         assert st1.mean_loss == 0.0 and st1.skipped_updates == 0
+
+
+@pytest.mark.parametrize("n,zero_frac", [(20000, 0.5), (40000, 0.95), (12000, 1.0)])
+def test_skip_matches_full_pass_fp32_trainer(n, zero_frac):
+    """The fp32 (FFMA) trainer classifies too (steps with more 64-row tiles than SMs):
+    the same gradient up to fp32 summation order, counts, loss and clamp counts."""
+    rng = np.random.default_rng(n + 7)
+    s = outside_positions(H.samples(rng, n, zero_p_frac=zero_frac), rng)
+    g1, st1, c1, w1 = step(s, True, prec=nasg.NASG_MLP_FP32)
+    g0, st0, c0, w0 = step(s, False, prec=nasg.NASG_MLP_FP32)
+    stats_equal(st1, st0, n)
+    assert c1 == c0 > 0
+    if zero_frac < 1.0:
+        assert rel_l2(g1, g0) <= 1e-5, rel_l2(g1, g0)
+    else:
+        assert not np.any(g1) and not np.any(g0)
 
 
 def test_nonfinite_inputs_with_zero_p_are_dropped_like_the_reference():
