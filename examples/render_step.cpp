@@ -38,6 +38,11 @@ int main() {
         nasg::gpu::TrainStats st = guide.train_iteration({ds, (size_t)n}, nasg_blend_coefficient(4, 4, 64));
         std::printf("dir0 = (%f %f %f) pdf %f; train: %d steps, mean loss %g, dropped %llu\n", o[0], o[1], o[2],
                     o[3], st.steps, st.mean_loss, (unsigned long long)st.dropped_samples);
+        // resume point: weights (the reference's NASGNET1 file) + the Adam state
+        guide.save_checkpoint("render_step.nasg", /*optimizer=*/true);
+        nasg::gpu::Guide resumed(nasg::gpu::TrainerConfig{}, 0, bmin, bmax);
+        resumed.load_checkpoint("render_step.nasg");
+        std::printf("resumed: %s\n", resumed.parameters() == guide.parameters() ? "same weights" : "DIFFERENT");
         cudaFree(ds);
         cudaFree(d);
     } catch (const nasg::gpu::Error &e) {

@@ -112,14 +112,14 @@ int nasg_get_precision(nasg_ctx *ctx);
 int nasg_set_train_precision(nasg_ctx *ctx, int precision);
 int nasg_get_train_precision(nasg_ctx *ctx);
 /* Zero-gradient rows (p_value == 0: kl_loss_gradient returns a zero gradient,
- * guiding.cpp:112, and loss_surrogate 0, :170) skip the network pass of the
- * bf16 trainer: they are counted in TrainStats exactly as the reference counts
+ * guiding.cpp:112, and loss_surrogate 0, :170) skip the network pass of both
+ * trainers: they are counted in TrainStats exactly as the reference counts
  * them, and the step's gradient is the same sum over the other rows.  Only
  * while every weight is below 1e7 in magnitude and the row's inputs are finite
  * (then its output is provably finite, so the reference would not drop it,
  * :247-250); otherwise the row takes the full path.  Applied to steps with
- * more 128-row tiles than SMs (smaller steps are one tile per SM either way).
- * Default on. */
+ * more tiles (128 rows tensor core, 64 fp32) than SMs (smaller steps are one
+ * tile per SM either way).  Default on. */
 int nasg_set_zero_row_skip(nasg_ctx *ctx, int on);
 int nasg_get_zero_row_skip(nasg_ctx *ctx);
 /* save_checkpoint / load_checkpoint (net.hpp:163-167, net.cpp:31-82): NASGNET1,

@@ -82,6 +82,8 @@ public:
 
     void set_precision(Precision p) { check(nasg_set_precision(ctx_, (int)p)); }
     void set_train_precision(Precision p) { check(nasg_set_train_precision(ctx_, (int)p)); }
+    // p = 0 rows counted without the network pass (nasg_set_zero_row_skip; default on)
+    void set_zero_row_skip(bool on) { check(nasg_set_zero_row_skip(ctx_, on ? 1 : 0)); }
     std::vector<float> parameters(bool published = false) const {
         std::vector<float> w((size_t)nasg_n_weights(cfg_n()));
         check(nasg_get_weights(ctx_, w.data(), w.size(), published ? 1 : 0));

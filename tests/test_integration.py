@@ -36,9 +36,10 @@ def test_cpp_example_builds_and_fails_cleanly_without_gpu(tmp_path):
 @pytest.mark.gpu
 def test_cpp_example_runs_on_gpu(tmp_path):
     exe = build_example(tmp_path)
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120, cwd=str(tmp_path))
     assert r.returncode == 0, r.stderr
     assert "train: 16 steps" in r.stdout
+    assert "resumed: same weights" in r.stdout
 
 
 def test_cpp_fit_and_render_example_builds(tmp_path):
