@@ -707,17 +707,17 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
         zero_rows = (double)cls[1];
     }
     if (blockIdx.x == gridDim.x - 1) {
-        __shared__ double sl[256], sc[256], sd[256];
+        __shared__ double sl[128], sc[128], sd[128];
         const int t = threadIdx.x;
         double ls = 0.0, lc = 0.0, dr = 0.0;
-        for (int i = t; i < ntiles; i += 256) {
+        for (int i = t; i < ntiles; i += 128) {
             ls += tb.tile_loss[i];
             lc += tb.tile_lc[i];
             dr += tb.tile_dr[i];
         }
         sl[t] = ls; sc[t] = lc; sd[t] = dr;
         __syncthreads();
-        for (int h = 128; h > 0; h >>= 1) {
+        for (int h = 64; h > 0; h >>= 1) {
             if (t < h) {
                 sl[t] += sl[t + h];
                 sc[t] += sc[t + h];
@@ -732,10 +732,16 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
         }
         return;
     }
+    // 4 warps per block share 32 consecutive weights: warp q sums the splits
+    // k = q, q + 4, ...; the four partial sums are added in fixed order
+    // ((s0 + s1) + (s2 + s3)): deterministic, a quarter of the dependent chain
+    __shared__ float quarter[4][32];
     const int nw = n_weights(n_comp), D = 8 * n_comp + 1;
     const int o1 = kIn * kHidden, o2 = o1 + kHidden * kHidden, o3 = o2 + kHidden * kHidden;
-    int e = blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= nw) return;
+    const int q = threadIdx.x >> 5;
+    int e = blockIdx.x * 32 + (threadIdx.x & 31);
+    const bool has = e < nw;
+    if (!has) e = nw - 1;
     int L, m, n;
     // dW1^T[n_out][k_in] partials: consecutive threads take consecutive k_in so
     // the split loads coalesce; the canonical W1 index (k_in * 128 + n_out) is
@@ -747,9 +753,15 @@ __global__ void train_tc_reduce_kernel(TcTrainBufs tb, int splits, int n_comp, f
     const int ps = partial_stride(packed_width(n_comp));
     const float *p = tb.partial + (size_t)L * tb.splits * (128 * ps) + m * ps + n;
     float s = 0.f;
-    for (int k = 0; k < splits; ++k) s += p[(size_t)k * (128 * ps)];
-    grad[e] = s;
-    if (!isfinite(s)) atomicOr(nonfinite, 1);
+    for (int k = q; k < splits; k += 4) s += p[(size_t)k * (128 * ps)];
+    quarter[q][threadIdx.x & 31] = s;
+    __syncthreads();
+    if (q == 0 && has) {
+        const int l = threadIdx.x & 31;
+        s = (quarter[0][l] + quarter[1][l]) + (quarter[2][l] + quarter[3][l]);
+        grad[e] = s;
+        if (!isfinite(s)) atomicOr(nonfinite, 1);
+    }
 }
 
 int train_classify(const nasg_train_sample *samples, const uint32_t *order, int64_t count, TcTrainBufs &tb,
@@ -807,7 +819,7 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
         launch_pdl(pdl, train_tc_dw_kernel, dim3(splits, 4), dim3(128), sm, s, tb, ntiles, bps, packed_width(n_comp),
                    live_count);
         const int nw = n_weights(n_comp);
-        launch_pdl(pdl, train_tc_reduce_kernel, dim3((nw + 255) / 256 + 1), dim3(256), 0, s, tb, splits, n_comp, grad,
+        launch_pdl(pdl, train_tc_reduce_kernel, dim3((nw + 31) / 32 + 1), dim3(128), 0, s, tb, splits, n_comp, grad,
                    nonfinite, (int)ntiles, live_count);
         launches += 3;
     }
