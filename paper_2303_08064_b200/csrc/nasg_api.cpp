@@ -337,7 +337,6 @@ int ensure_tc_scratch(nasg_ctx *c, int64_t count) {
         // smem each); 74 splits (two waves) measured 5 us slower per 2^18 step
         // (profiles/r2_dw_splits.txt)
         t.splits = 37;
-        if (const char *e = std::getenv("NASG_DW_SPLITS")) t.splits = std::max(1, std::min(2 * 37, std::atoi(e)));  // A/B only
         const int ps = packed_width(c->N) > 128 ? packed_width(c->N) : 128;  // partial_stride (k_train_tc.cu)
         CUDA_TRY(cudaMalloc(&t.partial, (size_t)4 * 2 * 37 * 128 * ps * sizeof(float)));
     }
