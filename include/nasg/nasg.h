@@ -62,6 +62,12 @@ typedef struct {
     float learning_rate;  /* 0.002 */
     double loss_blend;    /* e = 0.2 */
     uint64_t seed;        /* 0 */
+    int hidden_units;     /* 128 (kHiddenUnits, net.hpp); 64 is the paper's smaller
+                             network (Table 4): it runs on the 128-wide kernels with
+                             the extra units' weights held at exactly zero, which
+                             computes the 64-unit network exactly (same cost as 128).
+                             0 means 128. Weights, gradients and checkpoints are
+                             exchanged in the 64-unit canonical layout. */
 } nasg_config;
 
 /* TrainStats (guiding.hpp:132-137). */
@@ -97,6 +103,7 @@ int nasg_destroy(nasg_ctx *ctx);
 const char *nasg_status_string(int status);
 const char *nasg_last_error(void);  /* thread-local detail of the last failure */
 int nasg_n_weights(int n_components); /* 64*128 + 2*128*128 + 128*(8N+1) */
+int nasg_n_weights_hu(int n_components, int hidden_units); /* 64*H + 2*H*H + H*(8N+1) */
 
 /* ---- parameters / snapshots (Trainer::parameters/mutable_parameters/publish/
  * snapshot guiding.hpp:151-157; NetworkSnapshot net.hpp:161) -------------- */

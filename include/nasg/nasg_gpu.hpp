@@ -33,6 +33,7 @@ struct TrainerConfig {
     float learning_rate = 0.002f;
     double loss_blend = 0.2;
     std::uint64_t seed = 0;
+    int hidden_units = 128;  // 64: the paper's smaller network (nasg.h)
 };
 
 using TrainStats = nasg_train_stats;        // TrainStats (guiding.hpp:132-137)
@@ -45,9 +46,10 @@ class Guide {
 public:
     Guide(const TrainerConfig &c, int device, const float bmin[3], const float bmax[3]) {
         nasg_config cfg{c.n_components, c.sample_capacity, c.batch_size, c.step_factor,
-                        c.learning_rate, c.loss_blend, c.seed};
+                        c.learning_rate, c.loss_blend, c.seed, c.hidden_units};
         check(nasg_create(&cfg, device, bmin, bmax, &ctx_));
         n_ = c.n_components;
+        hu_ = c.hidden_units ? c.hidden_units : 128;
     }
     ~Guide() { nasg_destroy(ctx_); }
     Guide(const Guide &) = delete;
@@ -85,7 +87,7 @@ public:
     // p = 0 rows counted without the network pass (nasg_set_zero_row_skip; default on)
     void set_zero_row_skip(bool on) { check(nasg_set_zero_row_skip(ctx_, on ? 1 : 0)); }
     std::vector<float> parameters(bool published = false) const {
-        std::vector<float> w((size_t)nasg_n_weights(cfg_n()));
+        std::vector<float> w((size_t)nasg_n_weights_hu(cfg_n(), hu_));
         check(nasg_get_weights(ctx_, w.data(), w.size(), published ? 1 : 0));
         return w;
     }
@@ -100,7 +102,7 @@ public:
 private:
     int cfg_n() const { return n_; }
     nasg_ctx *ctx_ = nullptr;
-    int n_ = 8;
+    int n_ = 8, hu_ = 128;
 };
 
 // ---- explicit mixtures (sphdist.hpp:33-121): NASG records and the vMF / SG baseline

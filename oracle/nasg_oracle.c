@@ -87,9 +87,12 @@ static size_t layer_offset(int out_dim, int l) {
 
 /* init_network<float> net.hpp:43-57: Pcg32(hash_mix(seed), 0xda3e39cb94b95bdb),
  * row-major fill with (u*2-1)*sqrt(6/fan_in). */
-void orc_init_network(uint64_t seed, int out_dim, float *w) {
-    int d[5];
-    layer_dims(out_dim, d);
+void orc_init_network(uint64_t seed, int out_dim, float *w) { orc_init_network_hu(seed, ORC_HIDDEN, out_dim, w); }
+
+/* The same fill with kHiddenUnits = hidden (the paper's Table 4 sweep; the
+ * reference fixes 128): the canonical hidden-H layout, W1[64][H] .. W4[H][D]. */
+void orc_init_network_hu(uint64_t seed, int hidden, int out_dim, float *w) {
+    int d[5] = {ORC_IN, hidden, hidden, hidden, out_dim};
     pcg_t g;
     pcg_seed(&g, orc_hash_mix(seed), 0xda3e39cb94b95bdbull);
     for (int l = 0; l < 4; ++l) {

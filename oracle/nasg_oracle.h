@@ -27,6 +27,7 @@ uint64_t orc_hash_combine(uint64_t a, uint64_t b);
 void orc_pcg32(uint64_t initstate, uint64_t initseq, int n, uint32_t *out);
 
 void orc_init_network(uint64_t seed, int out_dim, float *w_out);
+void orc_init_network_hu(uint64_t seed, int hidden, int out_dim, float *w_out);
 void orc_one_blob(double x, int k, float *out);
 uint64_t orc_encode(int64_t n, const float *q9, const float *bmin, const float *bmax,
                     float *out64);

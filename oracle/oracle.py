@@ -88,8 +88,33 @@ def available(kind: str) -> bool:
     return os.path.exists(LIBS[kind])
 
 
-def n_weights(out_dim: int) -> int:
-    return 64 * 128 + 2 * 128 * 128 + 128 * out_dim
+def n_weights(out_dim: int, hidden: int = 128) -> int:
+    return 64 * hidden + 2 * hidden * hidden + hidden * out_dim
+
+
+def _layer_shapes(hidden, out_dim):
+    return [(64, hidden), (hidden, hidden), (hidden, hidden), (hidden, out_dim)]
+
+
+def embed_hidden(w, hidden, out_dim=65):
+    """Canonical hidden-H weights -> the 128-wide layout with the extra units
+    zero (the oracle then computes the hidden-H network exactly)."""
+    out, src = [], 0
+    for (r, c), (R, Cc) in zip(_layer_shapes(hidden, out_dim), _layer_shapes(128, out_dim)):
+        blk = np.zeros((R, Cc), np.float32)
+        blk[:r, :c] = np.asarray(w[src:src + r * c], np.float32).reshape(r, c)
+        out.append(blk.ravel())
+        src += r * c
+    return np.concatenate(out)
+
+
+def extract_hidden(w, hidden, out_dim=65):
+    """Inverse of embed_hidden."""
+    out, src = [], 0
+    for (r, c), (R, Cc) in zip(_layer_shapes(hidden, out_dim), _layer_shapes(128, out_dim)):
+        out.append(np.asarray(w[src:src + R * Cc]).reshape(R, Cc)[:r, :c].ravel())
+        src += R * Cc
+    return np.concatenate(out).astype(np.float32)
 
 
 def _ptr(a):
@@ -114,6 +139,10 @@ class Oracle:
             fn.restype = res
             fn.argtypes = args
             setattr(self, "_" + name, fn)
+        if kind == "orc":  # restatement-only extension (the reference fixes kHiddenUnits = 128)
+            fn = self.lib.orc_init_network_hu
+            fn.restype, fn.argtypes = None, [_u64, _int, _int, _f32p]
+            self._init_network_hu = fn
 
     # ---- L0 / encoder / net ------------------------------------------------
     def pcg32(self, state, seq, n):
@@ -124,6 +153,12 @@ class Oracle:
     def init_network(self, seed, out_dim=65):
         w = np.empty(n_weights(out_dim), np.float32)
         self._init_network(seed, out_dim, w)
+        return w
+
+    def init_network_hu(self, seed, hidden, out_dim=65):
+        """init_network with kHiddenUnits = hidden, canonical hidden-H layout."""
+        w = np.empty(n_weights(out_dim, hidden), np.float32)
+        self._init_network_hu(seed, hidden, out_dim, w)
         return w
 
     def one_blob(self, x, k=19):

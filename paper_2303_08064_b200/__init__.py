@@ -34,7 +34,7 @@ class NasgError(RuntimeError):
 class _Config(C.Structure):
     _fields_ = [("n_components", C.c_int), ("sample_capacity", C.c_int), ("batch_size", C.c_int),
                 ("step_factor", C.c_int), ("learning_rate", C.c_float), ("loss_blend", C.c_double),
-                ("seed", C.c_uint64)]
+                ("seed", C.c_uint64), ("hidden_units", C.c_int)]
 
 
 class _Stats(C.Structure):
@@ -74,6 +74,7 @@ class TrainerConfig:
     learning_rate: float = 0.002
     loss_blend: float = 0.2
     seed: int = 0
+    hidden_units: int = 128  # kHiddenUnits (net.hpp); 64 = the paper's smaller network (nasg.h)
 
 
 @dataclass
@@ -104,6 +105,7 @@ def lib():
         "nasg_status_string": (C.c_char_p, [i32]),
         "nasg_last_error": (C.c_char_p, []),
         "nasg_n_weights": (i32, [i32]),
+        "nasg_n_weights_hu": (i32, [i32, i32]),
         "nasg_set_weights": (i32, [vp, vp, sz]),
         "nasg_get_weights": (i32, [vp, vp, sz, i32]),
         "nasg_publish": (i32, [vp]),
@@ -210,8 +212,8 @@ def _stream(stream):
     return h if h else _CUDA_STREAM_LEGACY
 
 
-def n_weights(n_components: int = 8) -> int:
-    return lib().nasg_n_weights(n_components)
+def n_weights(n_components: int = 8, hidden_units: int = 128) -> int:
+    return lib().nasg_n_weights_hu(n_components, hidden_units)
 
 
 def blend_coefficient(iteration: int, m: int = 4, b_steps: int = 64) -> float:
@@ -251,7 +253,7 @@ def dp_plan(config: TrainerConfig, n_per_rank, rank: int):
     """Data-parallel minibatch plan of one train_iteration (host-only, see nasg.h):
     returns (local_count, global_count, reshuffle_before) arrays, one entry per step."""
     cfg = _Config(config.n_components, config.sample_capacity, config.batch_size, config.step_factor,
-                  config.learning_rate, config.loss_blend, config.seed)
+                  config.learning_rate, config.loss_blend, config.seed, config.hidden_units)
     n_all = np.ascontiguousarray(n_per_rank, np.int64)
     max_steps = config.step_factor * -(-config.sample_capacity // config.batch_size)
     loc = np.zeros(max_steps, np.int64)
@@ -282,7 +284,8 @@ class Guide:
             except ImportError:
                 device = 0
         cfg = _Config(self.config.n_components, self.config.sample_capacity, self.config.batch_size,
-                      self.config.step_factor, self.config.learning_rate, self.config.loss_blend, self.config.seed)
+                      self.config.step_factor, self.config.learning_rate, self.config.loss_blend, self.config.seed,
+                      self.config.hidden_units)
         h = C.c_void_p()
         lo, hi = _f3(bmin), _f3(bmax)
         _check(lib().nasg_create(C.byref(cfg), device, lo.ctypes.data, hi.ctypes.data, C.byref(h)))
@@ -290,7 +293,7 @@ class Guide:
         self.device = device
         self.n_components = self.config.n_components
         self.out_dim = 8 * self.n_components + 1
-        self.nw = n_weights(self.n_components)
+        self.nw = n_weights(self.n_components, self.config.hidden_units)
 
     def close(self):
         if getattr(self, "_h", None):

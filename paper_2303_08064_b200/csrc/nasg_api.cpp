@@ -73,9 +73,11 @@ struct Pcg32 {
     float next_f24() { return (float)(next() >> 8) * 0x1p-24f; }
 };
 
-// init_network<float> (net.hpp:43-57), bit-exact.
-void init_network(uint64_t seed, int n_comp, float *w) {
-    const int dims[5] = {kIn, kHidden, kHidden, kHidden, 8 * n_comp + 1};
+// init_network<float> (net.hpp:43-57), bit-exact; `hidden` is kHiddenUnits
+// (128 in the reference; 64 fills the same PCG32 stream over the smaller
+// matrices, the paper's Table 4 network).
+void init_network(uint64_t seed, int n_comp, int hidden, float *w) {
+    const int dims[5] = {kIn, hidden, hidden, hidden, 8 * n_comp + 1};
     Pcg32 rng(hash_mix(seed), 0xda3e39cb94b95bdbull);
     for (int l = 0; l < 4; ++l) {
         const double limit = std::sqrt(6.0 / dims[l]);
@@ -120,11 +122,46 @@ struct Nccl {
 Nccl g_nccl;
 std::mutex g_nccl_mu;
 
+// Canonical weight count of a network with `hidden` units per hidden layer.
+size_t n_weights_hu(int n_comp, int hidden) {
+    return (size_t)kIn * hidden + 2u * hidden * hidden + (size_t)hidden * (8 * n_comp + 1);
+}
+
+// A hidden-64 network lives in the 128-wide device layout with the extra
+// units' rows and columns zero.  Their gradients are exactly zero (their
+// activations are ReLU(0) = 0 and their outgoing weights are 0), so Adam keeps
+// them at zero and every kernel computes the 64-unit network unchanged.
+// embed: canonical hidden-H layout -> 128-wide layout; extract: the inverse.
+void hu_embed(int n_comp, int hidden, const float *e, float *w) {
+    const int D = 8 * n_comp + 1;
+    const int rows[4] = {kIn, hidden, hidden, hidden}, cols[4] = {hidden, hidden, hidden, D};
+    const int wrows[4] = {kIn, kHidden, kHidden, kHidden}, wcols[4] = {kHidden, kHidden, kHidden, D};
+    std::fill(w, w + n_weights(n_comp), 0.f);
+    for (int l = 0; l < 4; ++l) {
+        for (int r = 0; r < rows[l]; ++r)
+            std::copy(e + (size_t)r * cols[l], e + (size_t)r * cols[l] + cols[l], w + (size_t)r * wcols[l]);
+        e += (size_t)rows[l] * cols[l];
+        w += (size_t)wrows[l] * wcols[l];
+    }
+}
+void hu_extract(int n_comp, int hidden, const float *w, float *e) {
+    const int D = 8 * n_comp + 1;
+    const int rows[4] = {kIn, hidden, hidden, hidden}, cols[4] = {hidden, hidden, hidden, D};
+    const int wrows[4] = {kIn, kHidden, kHidden, kHidden}, wcols[4] = {kHidden, kHidden, kHidden, D};
+    for (int l = 0; l < 4; ++l) {
+        for (int r = 0; r < rows[l]; ++r)
+            std::copy(w + (size_t)r * wcols[l], w + (size_t)r * wcols[l] + cols[l], e + (size_t)r * cols[l]);
+        e += (size_t)rows[l] * cols[l];
+        w += (size_t)wrows[l] * wcols[l];
+    }
+}
+
 }  // namespace
 
 struct nasg_ctx {
     nasg_config cfg{};
     int device = 0, N = 8, D = 65, nw = 0, num_sms = 148;
+    int hu = kHidden, nw_ext = 0;  // hidden units; canonical (caller-facing) weight count
     Bounds bounds{};
     float bmax[3]{};
     cudaStream_t stream = nullptr;
@@ -615,6 +652,9 @@ const char *nasg_status_string(int s) {
 const char *nasg_last_error(void) { return g_err.c_str(); }
 
 int nasg_n_weights(int n_components) { return n_weights(n_components); }
+int nasg_n_weights_hu(int n_components, int hidden_units) {
+    return (int)n_weights_hu(n_components, hidden_units ? hidden_units : kHidden);
+}
 
 void nasg_config_default(nasg_config *c) {
     c->n_components = 8;
@@ -624,6 +664,7 @@ void nasg_config_default(nasg_config *c) {
     c->learning_rate = 0.002f;
     c->loss_blend = 0.2;
     c->seed = 0;
+    c->hidden_units = kHidden;
 }
 
 int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const float bmax[3], nasg_ctx **out) {
@@ -632,6 +673,8 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
         return fail(NASG_ERR_UNSUPPORTED, "n_components must be 4, 8 or 16 in this build");
     if (cfg->batch_size <= 0 || cfg->sample_capacity <= 0 || cfg->step_factor <= 0)
         return fail(NASG_ERR_INVALID, "batch_size, sample_capacity, step_factor must be > 0");
+    if (cfg->hidden_units != 0 && cfg->hidden_units != 64 && cfg->hidden_units != kHidden)
+        return fail(NASG_ERR_UNSUPPORTED, "hidden_units must be 64 or 128 in this build");
     int ndev = 0;
     CUDA_TRY(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return fail(NASG_ERR_INVALID, "bad device ordinal");
@@ -647,6 +690,9 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     c->N = cfg->n_components;
     c->D = 8 * c->N + 1;
     c->nw = n_weights(c->N);
+    c->hu = cfg->hidden_units ? cfg->hidden_units : kHidden;
+    c->cfg.hidden_units = c->hu;
+    c->nw_ext = (int)n_weights_hu(c->N, c->hu);
     c->num_sms = prop.multiProcessorCount;
     for (int k = 0; k < 3; ++k) {
         c->bounds.bmin[k] = bmin[k];
@@ -704,7 +750,13 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     cudaMemsetAsync(c->d_ticket, 0, 2 * sizeof(unsigned int), c->stream);
     cudaMemsetAsync(c->d_acc, 0, 5 * sizeof(double), c->stream);
     std::vector<float> w(c->nw);
-    init_network(cfg->seed, c->N, w.data());
+    if (c->hu == kHidden) {
+        init_network(cfg->seed, c->N, kHidden, w.data());
+    } else {
+        std::vector<float> e(c->nw_ext);
+        init_network(cfg->seed, c->N, c->hu, e.data());
+        hu_embed(c->N, c->hu, e.data(), w.data());
+    }
     if (cudaMemcpyAsync(c->w, w.data(), wb, cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
         return cleanup_fail(fail(NASG_ERR_CUDA, "weight upload failed"));
     int r = repack_live(c);
@@ -751,10 +803,44 @@ int nasg_destroy(nasg_ctx *c) {
     return NASG_OK;
 }
 
+// Device 128-wide parameter vector -> caller's canonical layout (host-synchronous).
+static int copy_out_wide(nasg_ctx *c, const float *dev, float *host) {
+    CUDA_TRY(cudaDeviceSynchronize());  // host-synchronous getter: order after all caller streams
+    if (c->hu == kHidden) {
+        CUDA_TRY(cudaMemcpyAsync(host, dev, c->nw * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        return NASG_OK;
+    }
+    std::vector<float> wide(c->nw);
+    CUDA_TRY(cudaMemcpyAsync(wide.data(), dev, c->nw * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    hu_extract(c->N, c->hu, wide.data(), host);
+    return NASG_OK;
+}
+
+// Caller's canonical layout -> device 128-wide parameter vector (synchronous).
+static int copy_in_wide(nasg_ctx *c, const float *host, float *dev) {
+    std::vector<float> wide;
+    if (c->hu != kHidden) {
+        wide.resize(c->nw);
+        hu_embed(c->N, c->hu, host, wide.data());
+        host = wide.data();
+    }
+    CUDA_TRY(cudaMemcpy(dev, host, c->nw * sizeof(float), cudaMemcpyHostToDevice));
+    return NASG_OK;
+}
+
 int nasg_set_weights(nasg_ctx *c, const float *host_w, size_t n) {
     DeviceScope ds_(c ? c->device : -1);
     if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
-    if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
+    if (n != (size_t)c->nw_ext) return fail(NASG_ERR_INVALID, "weight count mismatch");
+    std::vector<float> wide;
+    if (c->hu != kHidden) {
+        wide.resize(c->nw);
+        hu_embed(c->N, c->hu, host_w, wide.data());
+        host_w = wide.data();
+        n = wide.size();
+    }
     CUDA_TRY(cudaDeviceSynchronize());  // training may be in flight on a caller stream
     CUDA_TRY(cudaMemcpyAsync(c->w, host_w, n * sizeof(float), cudaMemcpyHostToDevice, c->stream));
     int r = repack_live(c);
@@ -766,12 +852,8 @@ int nasg_set_weights(nasg_ctx *c, const float *host_w, size_t n) {
 int nasg_get_weights(nasg_ctx *c, float *host_w, size_t n, int published) {
     DeviceScope ds_(c ? c->device : -1);
     if (!c || !host_w) return fail(NASG_ERR_INVALID, "null argument");
-    if (n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "weight count mismatch");
-    CUDA_TRY(cudaDeviceSynchronize());  // host-synchronous getter: order after all caller streams
-    CUDA_TRY(cudaMemcpyAsync(host_w, published ? c->w_pub : c->w, n * sizeof(float), cudaMemcpyDeviceToHost,
-                             c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    return NASG_OK;
+    if (n != (size_t)c->nw_ext) return fail(NASG_ERR_INVALID, "weight count mismatch");
+    return copy_out_wide(c, published ? c->w_pub : c->w, host_w);
 }
 
 int nasg_publish(nasg_ctx *c) {
@@ -820,15 +902,14 @@ int nasg_save_checkpoint_ex(nasg_ctx *c, const char *path, int flags) {
     DeviceScope ds_(c ? c->device : -1);
     if (!c || !path) return fail(NASG_ERR_INVALID, "null argument");
     if (flags & ~NASG_CKPT_OPTIMIZER) return fail(NASG_ERR_INVALID, "unknown checkpoint flags");
-    std::vector<float> w(c->nw), m, v;
+    std::vector<float> w(c->nw_ext), m, v;
     int r = nasg_get_weights(c, w.data(), w.size(), 0);
     if (r) return r;
     int64_t t = 0;
     if (flags & NASG_CKPT_OPTIMIZER) {
-        m.resize(c->nw);
-        v.resize(c->nw);
-        CUDA_TRY(cudaMemcpy(m.data(), c->m, c->nw * sizeof(float), cudaMemcpyDeviceToHost));
-        CUDA_TRY(cudaMemcpy(v.data(), c->v, c->nw * sizeof(float), cudaMemcpyDeviceToHost));
+        m.resize(c->nw_ext);
+        v.resize(c->nw_ext);
+        if ((r = copy_out_wide(c, c->m, m.data())) || (r = copy_out_wide(c, c->v, v.data()))) return r;
         CUDA_TRY(cudaMemcpy(&t, c->d_adam_t, sizeof(t), cudaMemcpyDeviceToHost));
     }
     FILE *f = std::fopen(path, "wb");
@@ -840,7 +921,7 @@ int nasg_save_checkpoint_ex(nasg_ctx *c, const char *path, int flags) {
     std::fwrite("NASGNET1", 1, 8, f);
     u32((uint32_t)c->N);
     u32(5);
-    const uint32_t dims[5] = {(uint32_t)kIn, (uint32_t)kHidden, (uint32_t)kHidden, (uint32_t)kHidden, (uint32_t)c->D};
+    const uint32_t dims[5] = {(uint32_t)kIn, (uint32_t)c->hu, (uint32_t)c->hu, (uint32_t)c->hu, (uint32_t)c->D};
     for (uint32_t d : dims) u32(d);
     bool ok = std::fwrite(w.data(), sizeof(float), w.size(), f) == w.size();
     if (flags & NASG_CKPT_OPTIMIZER) {
@@ -849,7 +930,7 @@ int nasg_save_checkpoint_ex(nasg_ctx *c, const char *path, int flags) {
             const unsigned char b = (unsigned char)((uint64_t)t >> (8 * k));
             ok &= std::fwrite(&b, 1, 1, f) == 1;
         }
-        u32((uint32_t)c->nw);
+        u32((uint32_t)c->nw_ext);
         ok &= std::fwrite(m.data(), sizeof(float), m.size(), f) == m.size();
         ok &= std::fwrite(v.data(), sizeof(float), v.size(), f) == v.size();
     }
@@ -880,12 +961,12 @@ int nasg_load_checkpoint(nasg_ctx *c, const char *path) {
     }
     uint32_t dims[5];
     for (auto &d : dims) d = u32();
-    if ((int)n != c->N || dims[0] != (uint32_t)kIn || dims[1] != (uint32_t)kHidden || dims[2] != (uint32_t)kHidden ||
-        dims[3] != (uint32_t)kHidden || dims[4] != (uint32_t)c->D) {
+    if ((int)n != c->N || dims[0] != (uint32_t)kIn || dims[1] != (uint32_t)c->hu || dims[2] != (uint32_t)c->hu ||
+        dims[3] != (uint32_t)c->hu || dims[4] != (uint32_t)c->D) {
         std::fclose(f);
         return fail(NASG_ERR_INVALID, "checkpoint shape does not match this context");
     }
-    std::vector<float> w(c->nw);
+    std::vector<float> w(c->nw_ext);
     ok &= std::fread(w.data(), sizeof(float), w.size(), f) == w.size();
     if (!ok) {
         std::fclose(f);
@@ -902,7 +983,7 @@ int nasg_load_checkpoint(nasg_ctx *c, const char *path) {
         bool ok2 = std::fread(b, 1, 8, f) == 8;
         for (int k = 0; k < 8; ++k) t |= (uint64_t)b[k] << (8 * k);
         const uint32_t nw = u32();
-        ok2 &= ok && nw == (uint32_t)c->nw;
+        ok2 &= ok && nw == (uint32_t)c->nw_ext;
         if (ok2) {
             m.resize(nw);
             v.resize(nw);
@@ -918,8 +999,7 @@ int nasg_load_checkpoint(nasg_ctx *c, const char *path) {
     int r = nasg_set_weights(c, w.data(), w.size());
     if (r || !adam) return r;
     const int64_t ts = (int64_t)t;
-    CUDA_TRY(cudaMemcpy(c->m, m.data(), m.size() * sizeof(float), cudaMemcpyHostToDevice));
-    CUDA_TRY(cudaMemcpy(c->v, v.data(), v.size() * sizeof(float), cudaMemcpyHostToDevice));
+    if ((r = copy_in_wide(c, m.data(), c->m)) || (r = copy_in_wide(c, v.data(), c->v))) return r;
     CUDA_TRY(cudaMemcpy(c->d_adam_t, &ts, sizeof(ts), cudaMemcpyHostToDevice));
     return NASG_OK;
 }
@@ -1280,11 +1360,8 @@ int nasg_train_iteration(nasg_ctx *c, int64_t n, const nasg_train_sample *sample
 
 int nasg_get_last_grad(nasg_ctx *c, float *host_g, size_t n) {
     DeviceScope ds_(c ? c->device : -1);
-    if (!c || !host_g || n != (size_t)c->nw) return fail(NASG_ERR_INVALID, "bad argument");
-    CUDA_TRY(cudaDeviceSynchronize());
-    CUDA_TRY(cudaMemcpyAsync(host_g, c->grad, n * sizeof(float), cudaMemcpyDeviceToHost, c->stream));
-    CUDA_TRY(cudaStreamSynchronize(c->stream));
-    return NASG_OK;
+    if (!c || !host_g || n != (size_t)c->nw_ext) return fail(NASG_ERR_INVALID, "bad argument");
+    return copy_out_wide(c, c->grad, host_g);
 }
 
 int64_t nasg_adam_t(nasg_ctx *c) {

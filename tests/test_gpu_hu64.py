@@ -1,0 +1,178 @@
+"""hidden_units = 64 (the paper's smaller network, PAPER Table 4; the reference
+fixes kHiddenUnits = 128, net.hpp) against the oracle run on the zero-embedded
+128-wide weights, which computes the 64-unit network exactly:
+  init bit-exact to init_network with kHiddenUnits = 64; fp32 raw outputs 2e-5;
+  fp32 / tensor-core queries at the N = 8 bars; one training step's gradient in
+  the canonical 64-unit layout; a train_iteration against the oracle trainer
+  (whose padded entries must stay exactly zero); checkpoints carry the 64-unit
+  dims and refuse a 128-unit context."""
+import os
+
+import numpy as np
+import pytest
+
+import nasg_testutil as H
+from oracle.oracle import embed_hidden, extract_hidden
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2303_08064_b200 as nasg  # noqa: E402
+
+HU, D = 64, 65
+NW = 64 * HU + 2 * HU * HU + HU * D
+
+
+def dev4(a3):
+    a = np.zeros((len(a3), 4), np.float32)
+    a[:, :3] = a3[:, :3]
+    return torch.from_numpy(a).cuda()
+
+
+def split(q9):
+    return dev4(q9[:, 0:3]), dev4(q9[:, 3:6]), dev4(q9[:, 6:9])
+
+
+def rel_l2(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+@pytest.fixture(scope="module")
+def guide():
+    g = nasg.Guide(nasg.TrainerConfig(seed=404, hidden_units=HU))
+    yield g
+    g.close()
+
+
+def test_weight_count_and_bad_sizes():
+    assert nasg.n_weights(8, 64) == NW == 16448
+    assert nasg.n_weights(8, 128) == nasg.n_weights(8) == 49280
+    for bad in (32, 96, 256):
+        with pytest.raises(nasg.NasgError):
+            nasg.Guide(nasg.TrainerConfig(hidden_units=bad))
+
+
+def test_init_and_raw_outputs(guide, orc):
+    w = guide.get_weights()
+    assert w.shape == (NW,)
+    assert np.array_equal(w, orc.init_network_hu(404, HU))
+    q9 = H.queries(np.random.default_rng(1), 4099, outside=0.1)
+    guide.precision = nasg.NASG_MLP_FP32
+    raw = guide.query_raw(*split(q9)).cpu().numpy()
+    enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
+    ref = orc.forward(embed_hidden(w, HU), enc)
+    assert np.all(np.abs(raw - ref) <= 2e-5 * (1 + np.abs(ref)))
+
+
+def test_set_weights_roundtrip(guide):
+    w = guide.get_weights()
+    w2 = (w * 0.5).astype(np.float32)
+    guide.set_weights(w2)
+    assert np.array_equal(guide.get_weights(), w2)
+    assert np.array_equal(guide.get_weights(published=True), w2)
+    guide.set_weights(w)
+
+
+def test_query_sample_fp32_and_tc(guide, orc):
+    rng = np.random.default_rng(9)
+    n = 1 << 16
+    q9, xi = H.queries(rng, n), H.xis(rng, n)
+    ref, cref = orc.query_sample(embed_hidden(guide.get_weights(published=True), HU), q9, xi, threads=8)
+    ref = ref.astype(np.float64)
+    for prec in (nasg.NASG_MLP_FP32, nasg.NASG_MLP_BF16):
+        guide.precision = prec
+        c = torch.empty(n, dtype=torch.float32, device="cuda")
+        out, _ = guide.query_sample(*split(q9), torch.from_numpy(xi).cuda(), c=c)
+        out = out.cpu().numpy().astype(np.float64)
+        ddir = np.linalg.norm(out[:, :3] - ref[:, :3], axis=1)
+        dpdf = np.abs(out[:, 3] - ref[:, 3]) / ref[:, 3]
+        if prec == nasg.NASG_MLP_FP32:
+            assert ddir.max() <= 1e-3 and dpdf.max() <= 1e-3, (ddir.max(), dpdf.max())
+            assert np.allclose(c.cpu().numpy(), cref, rtol=1e-5)
+        else:  # f16 operands: the N = 8 path's bar (test_gpu_tc.py)
+            same = ddir <= 0.05
+            p50 = np.median(dpdf[same])
+            print(f"HU={HU} tensor-core query: lobe mismatch {1 - same.mean():.2e} pdf p50 {p50:.2e}")
+            assert 1 - same.mean() <= 2e-3 and p50 <= 1e-3, (1 - same.mean(), p50)
+    guide.precision = nasg.NASG_MLP_FP32
+
+
+@pytest.mark.parametrize("b", [0.0, 1.0])
+def test_training_step_gradient(orc, b):
+    s = H.samples(np.random.default_rng(int(10 * b) + 3), 3000)
+    ds = torch.from_numpy(s).cuda()
+    grads = {}
+    for prec in (nasg.NASG_MLP_FP32, nasg.NASG_MLP_BF16):
+        g = nasg.Guide(nasg.TrainerConfig(seed=88, batch_size=3000, sample_capacity=3000, hidden_units=HU))
+        g.train_precision = prec
+        w0 = g.get_weights()
+        g.train_step(ds, None, len(s), len(s), b)
+        grads[prec] = g.last_grad()
+        assert grads[prec].shape == (NW,)
+        g.close()
+    q9 = np.concatenate([s[:, 0:3], s[:, 4:7], s[:, 8:11]], 1)
+    enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
+    we = embed_hidden(w0, HU)
+    raw = orc.forward(we, enc)
+    og, _, _ = orc.kl_grad(raw, s, b, 0.2)
+    full = orc.backward(we, enc, (og * (1.0 / len(s))).astype(np.float32))
+    # the padded units' gradient is exactly zero in the oracle too
+    assert np.array_equal(embed_hidden(extract_hidden(full, HU), HU), full)
+    ref = extract_hidden(full, HU).astype(np.float64)
+    assert rel_l2(grads[nasg.NASG_MLP_FP32], ref) <= 1e-4
+    gb = grads[nasg.NASG_MLP_BF16].astype(np.float64)
+    cos = float(gb @ ref / (np.linalg.norm(gb) * np.linalg.norm(ref)))
+    print(f"HU={HU} b={b} tensor-core train gradient: cos {cos:.5f} rel-L2 {rel_l2(gb, ref):.3e}")
+    assert cos >= 0.995 and rel_l2(gb, ref) <= 0.1, (cos, rel_l2(gb, ref))
+
+
+@pytest.mark.parametrize("prec", ["fp32", "bf16"])
+def test_train_iteration_tracks_oracle(orc, prec):
+    s = nasg.synth_samples(6, 4096)
+    g = nasg.Guide(nasg.TrainerConfig(seed=7, sample_capacity=4096, batch_size=1024, hidden_units=HU))
+    g.train_precision = nasg.NASG_MLP_FP32 if prec == "fp32" else nasg.NASG_MLP_BF16
+    t = orc.trainer(capacity=4096, batch=1024, seed=7)
+    t.set_weights(embed_hidden(g.get_weights(), HU))
+    losses = []
+    for it in range(3):
+        st = g.train_iteration(torch.from_numpy(s).cuda(), 1.0)
+        sr = t.train(s, 1.0)
+        assert st.steps == sr["steps"] == 4
+        losses.append((st.mean_loss, sr["mean_loss"]))
+    wt = t.weights()
+    assert np.array_equal(embed_hidden(extract_hidden(wt, HU), HU), wt)  # padded entries stayed 0
+    if prec == "fp32":
+        assert all(a == pytest.approx(b, rel=1e-3) for a, b in losses), losses
+        assert rel_l2(g.get_weights(), extract_hidden(wt, HU)) <= 1e-3
+    else:
+        assert all(a == pytest.approx(b, rel=0.02) for a, b in losses), losses
+        assert rel_l2(g.get_weights(), extract_hidden(wt, HU)) <= 0.05
+    g.close()
+
+
+def test_checkpoint_dims_and_resume(tmp_path, orc):
+    p = str(tmp_path / "hu64.nasg")
+    s = nasg.synth_samples(3, 2048)
+    cfg = nasg.TrainerConfig(seed=11, sample_capacity=2048, batch_size=2048, hidden_units=HU)  # whole-buffer steps
+    g = nasg.Guide(cfg)
+    g.train_iteration(torch.from_numpy(s).cuda(), 1.0)
+    g.save_checkpoint(p, optimizer=True)
+    raw = open(p, "rb").read()
+    dims = np.frombuffer(raw[16:36], np.uint32)
+    assert list(dims) == [64, HU, HU, HU, D]
+    assert len(raw) == 36 + 4 * NW + 8 + 8 + 4 + 8 * NW
+    g2 = nasg.Guide(cfg)
+    g2.load_checkpoint(p)
+    assert np.array_equal(g2.get_weights(), g.get_weights())
+    g.train_iteration(torch.from_numpy(s).cuda(), 1.0)
+    g2.train_iteration(torch.from_numpy(s).cuda(), 1.0)
+    assert np.array_equal(g2.get_weights(), g.get_weights())  # Adam state resumed in the 64-unit layout
+    g128 = nasg.Guide(nasg.TrainerConfig(seed=1))
+    with pytest.raises(nasg.NasgError):
+        g128.load_checkpoint(p)
+    for x in (g, g2, g128):
+        x.close()
+    os.remove(p)

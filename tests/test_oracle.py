@@ -334,3 +334,26 @@ def test_restatement_matches_golden_kl(orc):
     assert np.array_equal(ok, g["ok"])
     assert np.allclose(gr, g["grad"], rtol=1e-12, atol=1e-300)
     assert np.allclose(loss, g["loss"], rtol=1e-12, equal_nan=True)
+
+
+def test_init_hidden_units_and_embedding(orc):
+    """init_network with kHiddenUnits = H: H = 128 is the reference's init;
+    embed/extract (the hidden-64 device layout) round-trip; the zero-embedded
+    network's outputs equal a direct float64 hidden-64 forward."""
+    from oracle.oracle import embed_hidden, extract_hidden
+    assert np.array_equal(orc.init_network_hu(5, 128), orc.init_network(5))
+    w = orc.init_network_hu(5, 64)
+    assert w.shape == (16448,)
+    we = embed_hidden(w, 64)
+    assert we.shape == (49280,) and np.array_equal(extract_hidden(we, 64), w)
+    enc, _ = orc.encode(H.queries(np.random.default_rng(3), 257), H.BMIN, H.BMAX)
+    out = orc.forward(we, enc)
+    mats, o = [], 0
+    for r, c in [(64, 64), (64, 64), (64, 64), (64, 65)]:
+        mats.append(w[o:o + r * c].reshape(r, c).astype(np.float64))
+        o += r * c
+    h = enc.astype(np.float64)
+    for m in mats[:3]:
+        h = np.maximum(h @ m, 0.0)
+    ref = h @ mats[3]
+    assert np.allclose(out, ref, rtol=1e-4, atol=1e-5)
