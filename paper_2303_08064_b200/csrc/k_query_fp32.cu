@@ -97,7 +97,7 @@ constexpr int act_rows(int n) { return packed_width(n) > kHidden ? packed_width(
 constexpr size_t query_smem(int n) { return (size_t)(act_rows(n) * kLda + 2 * kChunk * 128) * sizeof(float); }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(256, 2)
+__global__ void __launch_bounds__(256, 2 * query_smem(N) <= 232448 ? 2 : 1)  // one CTA per SM at N = 32
 query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
     extern __shared__ __align__(16) float smem[];
     // one activation tile, updated in place: each layer keeps its outputs in
@@ -131,10 +131,13 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
         tile_layer<128, kIn, kEpiRelu>(actA, actA, W1, wbuf, nullptr, tid);
         tile_layer<128, kHidden, kEpiRelu>(actA, actA, W2, wbuf, nullptr, tid);
         tile_layer<128, kHidden, kEpiRelu>(actA, actA, W3, wbuf, nullptr, tid);
-        if constexpr (packed_width(N) > 128) {  // packed columns [128, NP) first, into rows the layer does not read
-            tile_layer<128, kHidden, kEpiNone, kLda, packed_width(N) - 128>(actA, actA + 128 * kLda,
-                                                                            W4 + kHidden * 128, wbuf, nullptr, tid);
-        }
+        constexpr int NP = packed_width(N);
+        if constexpr (NP > 256)  // packed columns past 128 first, into rows the layer does not read
+            tile_layer<128, kHidden, kEpiNone, kLda, NP - 256>(actA, actA + 256 * kLda, W4 + 2 * kHidden * 128, wbuf,
+                                                               nullptr, tid);
+        if constexpr (NP > 128)
+            tile_layer<128, kHidden, kEpiNone, kLda, (NP - 128 < 128 ? NP - 128 : 128)>(
+                actA, actA + 128 * kLda, W4 + kHidden * 128, wbuf, nullptr, tid);
         tile_layer<128, kHidden, kEpiNone>(actA, actA, W4, wbuf, nullptr, tid);
         if constexpr (MODE == kModeSample || MODE == kModePdf) {
             // double-precision epilogue on all 8 warps: 2 lanes per query, 4 lobes each
@@ -185,7 +188,8 @@ query_fp32_kernel(const float *__restrict__ wp, QueryArgs a) {
 template <int N>
 static int query_fp32_n(QueryMode mode, const float *wp, const QueryArgs &a, int num_sms, cudaStream_t s) {
     const int64_t ntiles = (a.n + kTileRows - 1) / kTileRows;
-    const int grid = (int)(ntiles < 2 * num_sms ? ntiles : 2 * num_sms);  // two CTAs per SM
+    constexpr int per_sm = 2 * query_smem(N) <= 232448 ? 2 : 1;  // two CTAs per SM (one at N = 32)
+    const int grid = (int)(ntiles < per_sm * num_sms ? ntiles : per_sm * num_sms);
     if (grid == 0) return 0;
     switch (mode) {
 #define NASG_LAUNCH(M)                                                                             \
@@ -209,6 +213,7 @@ int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, 
         case 4: return query_fp32_n<4>(mode, wp, a, num_sms, s);
         case 8: return query_fp32_n<8>(mode, wp, a, num_sms, s);
         case 16: return query_fp32_n<16>(mode, wp, a, num_sms, s);
+        case 32: return query_fp32_n<32>(mode, wp, a, num_sms, s);  // NP = 304: three blocks
         default: return -1;
     }
 }
@@ -270,6 +275,7 @@ int decode_raw(int n_comp, bool sample, bool fast, int64_t n, const float *raw, 
         case 4: NASG_DR(4);
         case 8: NASG_DR(8);
         case 16: NASG_DR(16);
+        case 32: NASG_DR(32);
         default: return -1;
     }
 #undef NASG_DR

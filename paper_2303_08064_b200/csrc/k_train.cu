@@ -26,18 +26,23 @@ namespace nasg {
 constexpr int kTrainRows = 64;
 constexpr int kTLda = kTrainRows + 4;  // 68
 
-// smem carve-up of K_fb (floats)
+// smem carve-up of K_fb (floats).  da holds the packed raw outputs / delta4
+// (160 rows for NP <= 160); db the next delta.  For N = 32 (NP = 304) the
+// backward runs in place in da instead (tile_layer writes its outputs only
+// after every thread has read its last input chunk), which keeps the tile
+// inside one SM's shared memory.
 constexpr int kOffH0 = 0;
 constexpr int kOffH1 = kOffH0 + kIn * kTLda;
 constexpr int kOffH2 = kOffH1 + kHidden * kTLda;
 constexpr int kOffH3 = kOffH2 + kHidden * kTLda;
 constexpr int kOffDA = kOffH3 + kHidden * kTLda;
-constexpr int kOffDB = kOffDA + 160 * kTLda;  // da holds the packed raw outputs / delta4: NP <= 160 rows
-constexpr int kOffW = kOffDB + kHidden * kTLda;
-constexpr int kOffRow = kOffW + 2 * kChunk * 128;          // 64 x 8 per-row sample data
-constexpr int kOffLoss = kOffRow + kTrainRows * 8;          // 64 double losses + 64 int states
-constexpr int kFbFloats = kOffLoss + kTrainRows * 3;
-constexpr size_t kFbSmem = kFbFloats * sizeof(float);
+constexpr bool bwd_in_place(int n) { return packed_width(n) > 160; }
+constexpr int off_db(int n) { return bwd_in_place(n) ? kOffDA : kOffDA + 160 * kTLda; }
+constexpr int off_w(int n) { return bwd_in_place(n) ? kOffDA + packed_width(n) * kTLda : off_db(n) + kHidden * kTLda; }
+constexpr int off_row(int n) { return off_w(n) + 2 * kChunk * 128; }   // 64 x 8 per-row sample data
+constexpr int off_loss(int n) { return off_row(n) + kTrainRows * 8; }  // 64 double losses + 64 int states
+constexpr size_t fb_smem_f32(int n) { return (size_t)(off_loss(n) + kTrainRows * 3) * sizeof(float); }
+static_assert(fb_smem_f32(32) <= 232448 && fb_smem_f32(16) <= 232448, "fp32 trainer tile fits one SM");
 
 // feature-major smem [F][kTLda] -> row-major global [rows][F], rows < valid
 template <int F>
@@ -64,10 +69,10 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
     constexpr int H = packed_header(N), NP = packed_width(N), D = 8 * N + 1;
     extern __shared__ __align__(16) float sm[];
     float *h0 = sm + kOffH0, *h1 = sm + kOffH1, *h2 = sm + kOffH2, *h3 = sm + kOffH3;
-    float *da = sm + kOffDA, *db = sm + kOffDB, *wbuf = sm + kOffW;
-    float *rowd = sm + kOffRow;
-    double *rloss = reinterpret_cast<double *>(sm + kOffLoss);
-    int *rstate = reinterpret_cast<int *>(sm + kOffLoss + 2 * kTrainRows);
+    float *da = sm + kOffDA, *db = sm + off_db(N), *wbuf = sm + off_w(N);
+    float *rowd = sm + off_row(N);
+    double *rloss = reinterpret_cast<double *>(sm + off_loss(N));
+    int *rstate = reinterpret_cast<int *>(sm + off_loss(N) + 2 * kTrainRows);
     __shared__ int s_clamped;
     const int tid = threadIdx.x;
     const float *W1 = wp, *W2 = W1 + kIn * kHidden, *W3 = W2 + kHidden * kHidden, *W4 = W3 + kHidden * kHidden;
@@ -113,9 +118,12 @@ train_fb_kernel(const float *__restrict__ wp, const float *__restrict__ wtp,
         tile_layer<kTrainRows, kHidden, kEpiRelu, kTLda>(h1, h2, W2, wbuf, nullptr, tid);
         tile_layer<kTrainRows, kHidden, kEpiRelu, kTLda>(h2, h3, W3, wbuf, nullptr, tid);
         tile_layer<kTrainRows, kHidden, kEpiNone, kTLda>(h3, da, W4, wbuf, nullptr, tid);
-        if constexpr (NP > 128)  // packed columns [128, NP): the second 128-column block of W4p
-            tile_layer<kTrainRows, kHidden, kEpiNone, kTLda, NP - 128>(h3, da + 128 * kTLda, W4 + kHidden * 128, wbuf,
-                                                                        nullptr, tid);
+        if constexpr (NP > 128)  // packed columns [128, NP): the further 128-column blocks of W4p
+            tile_layer<kTrainRows, kHidden, kEpiNone, kTLda, (NP - 128 < 128 ? NP - 128 : 128)>(
+                h3, da + 128 * kTLda, W4 + kHidden * 128, wbuf, nullptr, tid);
+        if constexpr (NP > 256)
+            tile_layer<kTrainRows, kHidden, kEpiNone, kTLda, NP - 256>(h3, da + 256 * kTLda, W4 + 2 * kHidden * 128,
+                                                                        wbuf, nullptr, tid);
         store_rows<kIn>(h0, sc.h0, row0, valid, tid);
         store_rows<kHidden>(h1, sc.h1, row0, valid, tid);
         store_rows<kHidden>(h2, sc.h2, row0, valid, tid);
@@ -188,12 +196,19 @@ int train_forward_backward(int n_comp, const float *wp, const float *wtp, const 
     if (ntiles == 0) return 0;
     const int grid = ntiles < num_sms ? ntiles : num_sms;
     const double gscale = 1.0 / (double)global_count;  // guiding.cpp:262
-    if (n_comp != 8 && n_comp != 4 && n_comp != 16) return -1;
-    auto k = n_comp == 8 ? train_fb_kernel<8> : (n_comp == 4 ? train_fb_kernel<4> : train_fb_kernel<16>);
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFbSmem);
-    k<<<grid, 256, kFbSmem, s>>>(wp, wtp, samples, order, count, live_count, gscale, b, loss_blend, bounds, sc,
-                                 clamp_count);
-    return 1;
+    auto go = [&](auto kern, size_t smem) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        kern<<<grid, 256, smem, s>>>(wp, wtp, samples, order, count, live_count, gscale, b, loss_blend, bounds, sc,
+                                     clamp_count);
+        return 1;
+    };
+    switch (n_comp) {
+        case 4: return go(train_fb_kernel<4>, fb_smem_f32(4));
+        case 8: return go(train_fb_kernel<8>, fb_smem_f32(8));
+        case 16: return go(train_fb_kernel<16>, fb_smem_f32(16));
+        case 32: return go(train_fb_kernel<32>, fb_smem_f32(32));
+        default: return -1;
+    }
 }
 
 // ------------------------------------------------------------------ K_dw --
@@ -303,7 +318,7 @@ int train_dw(int n_comp, int64_t count, TrainScratch &sc, float *grad, cudaStrea
     dw_kernel<64><<<splits, 256, 0, s>>>(sc.h0, sc.d1, 128, 128, 128, rows, rps, p, stride, live_count);
     dw_kernel<128><<<splits, 256, 0, s>>>(sc.h1, sc.d2, 128, 128, 128, rows, rps, p + o1, stride, live_count);
     dw_kernel<128><<<splits, 256, 0, s>>>(sc.h2, sc.d3, 128, 128, 128, rows, rps, p + o2, stride, live_count);
-    // dW4 [128][D] in 128-column blocks of delta4 (two for N = 16)
+    // dW4 [128][D] in 128-column blocks of delta4 (two for N = 16, three for N = 32)
     const int ds = d4_stride(n_comp);
     for (int c0 = 0; c0 < D; c0 += 128)
         dw_kernel<128><<<splits, 256, 0, s>>>(sc.h3, sc.d4 + c0, ds, D - c0 < 128 ? D - c0 : 128, D, rows, rps,

@@ -669,8 +669,8 @@ void nasg_config_default(nasg_config *c) {
 
 int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const float bmax[3], nasg_ctx **out) {
     if (!cfg || !out || !bmin || !bmax) return fail(NASG_ERR_INVALID, "null argument");
-    if (cfg->n_components != 4 && cfg->n_components != 8 && cfg->n_components != 16)
-        return fail(NASG_ERR_UNSUPPORTED, "n_components must be 4, 8 or 16 in this build");
+    if (cfg->n_components != 4 && cfg->n_components != 8 && cfg->n_components != 16 && cfg->n_components != 32)
+        return fail(NASG_ERR_UNSUPPORTED, "n_components must be 4, 8, 16 or 32 in this build");
     if (cfg->batch_size <= 0 || cfg->sample_capacity <= 0 || cfg->step_factor <= 0)
         return fail(NASG_ERR_INVALID, "batch_size, sample_capacity, step_factor must be > 0");
     if (cfg->hidden_units != 0 && cfg->hidden_units != 64 && cfg->hidden_units != kHidden)

@@ -24,7 +24,8 @@ __host__ __device__ constexpr int packed_width(int n) { return packed_header(n) 
 
 // fp32 packed weight image used by the SIMT kernels: W1[64][128], W2, W3, then
 // the last layer in the packed raw order as f32_out_blocks(n) blocks of
-// [128 k][128 packed cols] (zero-padded): one block for N <= 8, two for N = 16.
+// [128 k][128 packed cols] (zero-padded): one block for N <= 8, two for N = 16,
+// three for N = 32.
 __host__ __device__ constexpr int f32_out_blocks(int n) { return (packed_width(n) + 127) / 128; }
 __host__ __device__ constexpr int packed_f32_floats(int n) {
     return kIn * kHidden + 2 * kHidden * kHidden + f32_out_blocks(n) * kHidden * 128;
@@ -34,8 +35,9 @@ __host__ __device__ constexpr int packed_f32_floats(int n) {
 __host__ __device__ constexpr int packed_t32_floats(int n) { return 2 * kHidden * kHidden + f32_out_blocks(n) * 128 * kHidden; }
 // contraction length of the backward through W4p^T: NP rounded up to 16 (>= 128)
 __host__ __device__ constexpr int f32_bwd_k(int n) { return packed_width(n) <= 128 ? 128 : (packed_width(n) + 15) / 16 * 16; }
-// row stride of the fp32 trainer's delta4 (reference raw order, zero-padded)
-__host__ __device__ constexpr int d4_stride(int n) { return 8 * n + 1 <= 80 ? 80 : 256; }
+// row stride of the fp32 trainer's delta4 (reference raw order, zero-padded;
+// whole 128-column blocks past 80 so K_dw's block reads stay inside the row)
+__host__ __device__ constexpr int d4_stride(int n) { return 8 * n + 1 <= 80 ? 80 : (8 * n + 1 + 127) / 128 * 128; }
 
 __host__ __device__ inline int n_weights(int n) { return kIn * kHidden + 2 * kHidden * kHidden + kHidden * (8 * n + 1); }
 
