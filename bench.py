@@ -444,12 +444,13 @@ def bench_sweep(nasg, args, ws, rank):
             t = max_over_ranks(sum(time_events(lambda: g.query_sample(*d, dir_pdf=res[:n]), reps, stream)), ws)
             out[f"{name}_2^{lg}"] = n * ws * reps / t
     g.close()
-    # the paper's component sweep (PAPER Table 4: C = 4 / 16; N = 8 above) at 2^22
-    # queries, both precisions, plus one config-3-shaped bf16 training step (2^18)
+    # the paper's component sweep (PAPER Table 4: C = 4 / 16 / 32; N = 8 above) at
+    # 2^22 queries, both precisions, plus one config-3-shaped training step (2^18;
+    # bf16, fp32 for N = 32 whose tensor-core trainer is not built)
     n = 1 << 22
     d = [a[:n] for a in dev]
     samples = torch.from_numpy(nasg.synth_samples(11, 1 << 18, first=rank * (1 << 18))).cuda()
-    for nc in (4, 16):
+    for nc in (4, 16, 32):
         g = nasg.Guide(nasg.TrainerConfig(seed=0, n_components=nc), device=torch.cuda.current_device())
         for prec, name in ((nasg.NASG_MLP_BF16, "bf16"), (nasg.NASG_MLP_FP32, "fp32")):
             g.precision = prec
@@ -463,18 +464,30 @@ def bench_sweep(nasg, args, ws, rank):
         g.close()
         tg = nasg.Guide(nasg.TrainerConfig(seed=3, n_components=nc, sample_capacity=1 << 18, batch_size=1 << 18),
                         device=torch.cuda.current_device())
-        tg.train_precision = nasg.NASG_MLP_BF16
+        tprec = "fp32" if nc == 32 else "bf16"
+        tg.train_precision = nasg.NASG_MLP_FP32 if nc == 32 else nasg.NASG_MLP_BF16
         for _ in range(3):
             tg.train_iteration(samples, 1.0, stats=False)
         torch.cuda.synchronize()
         t = max_over_ranks(sum(time_events(lambda: tg.train_iteration(samples, 1.0, stats=False), 5, stream)), ws)
-        out[f"N{nc}_bf16_train_samples_per_s"] = (1 << 18) * ws * 5 / t
+        out[f"N{nc}_{tprec}_train_samples_per_s"] = (1 << 18) * ws * 5 / t
         tg.close()
+    # hidden width 64 (PAPER Table 4; runs on the 128-wide kernels, exact, same cost)
+    g = nasg.Guide(nasg.TrainerConfig(seed=0, hidden_units=64), device=torch.cuda.current_device())
+    g.precision = nasg.NASG_MLP_BF16
+    for _ in range(2):
+        g.query_sample(*d, dir_pdf=res[:n])
+    torch.cuda.synchronize()
+    barrier(ws)
+    t = max_over_ranks(sum(time_events(lambda: g.query_sample(*d, dir_pdf=res[:n]), 4, stream)), ws)
+    out["HU64_bf16_2^22"] = n * ws * 4 / t
+    g.close()
     del dev, res, samples
     torch.cuda.empty_cache()
     return {"unit": "queries/s (train entries: samples/s)",
-            "note": "config 2 sweep; value = all ranks' queries / max-over-ranks time; N4_*, N16_*: the paper's "
-                    "lobe-count sweep (Table 4) at 2^22 queries and a 2^18-sample training step",
+            "note": "config 2 sweep; value = all ranks' queries / max-over-ranks time; N4_*, N16_*, N32_*: the "
+                    "paper's lobe-count sweep (Table 4) at 2^22 queries and a 2^18-sample training step; HU64_*: "
+                    "the 64-unit network (zero-embedded in the 128-wide kernels)",
             **out}
 
 

@@ -27,7 +27,10 @@
 // N = 16 (NP = 160): one MLP warpgroup and two NASG warpgroups ("slots") that
 // take its tiles alternately, each with its own E buffer, input stage and raw
 // buffer (TMEM [128 + 160 j, ...)) — the 16-lobe epilogue is about twice the
-// MLP's work per tile.
+// MLP's work per tile.  N = 32 (NP = 304): one MLP and one NASG warpgroup, raw
+// buffer TMEM [128, 432) written by two output MMAs (N = 256 + 48); the NASG
+// group streams the row's lobes out of tensor memory (the 304 columns do not
+// fit in registers) and keeps the launch's register allocation (no setmaxnreg).
 // Only the 52 B/query of inputs and 16-20 B/query of outputs touch HBM.
 #include <cuda_bf16.h>
 
@@ -60,7 +63,8 @@ namespace {
 // two NASG warpgroups that take its tiles alternately (the 16-lobe epilogue is
 // twice the MLP's work per tile), raw buffers TMEM [128, 288) and [288, 448).
 constexpr int pairs_for(int n) { return packed_width(n) > 128 ? 1 : 2; }
-constexpr int slots_for(int n) { return packed_width(n) > 128 ? 2 : 1; }
+constexpr int slots_for(int n) { return packed_width(n) > 256 ? 1 : (packed_width(n) > 128 ? 2 : 1); }
+constexpr bool streamed(int n) { return packed_width(n) > 256; }  // N = 32: lobes streamed from TMEM
 constexpr int threads_for(int n) { return pairs_for(n) * (1 + slots_for(n)) * 128; }
 constexpr uint32_t raw_col(int n, int lane) {  // first TMEM column of NASG lane (pair m, slot j) = m * S + j
     return pairs_for(n) == 2 ? 256u + 128u * (uint32_t)lane : 128u + 160u * (uint32_t)lane;
@@ -94,7 +98,10 @@ constexpr size_t smem_bytes() {
 
 size_t tc_image_bytes(int n) { return img_bytes(n); }
 size_t tc_train_image_bytes(int n) { return train_img_bytes(n); }
-bool tc_supported(int n) { return n == 4 || n == 8 || n == 16; }  // NP = 48 / 80 / 160: one UMMA N <= 256, N % 16 == 0
+// queries: NP = 48 / 80 / 160 / 304 (N % 16 == 0; two output MMAs past 256)
+bool tc_supported(int n) { return n == 4 || n == 8 || n == 16 || n == 32; }
+// training: the trainer's f16 image + bf16 W4 copy + delta4 tile fit one SM up to N = 16
+bool tc_train_supported(int n) { return n == 4 || n == 8 || n == 16; }
 
 // ------------------------------------------------------------------ packing --
 // f16 image of the four layers (both tensor-core kernels); train = 1 appends
@@ -201,7 +208,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 
     if (g < kPairs) {
         // ============================ MLP warpgroup ============================
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(regs_mlp(N)));
+        if constexpr (!streamed(N)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(regs_mlp(N)));
         const uint32_t my_acc = tmem + m * 128 + ((uint32_t)(wq * 32) << 16);
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + m * kABytes);
         const uint32_t e_base0 = tc::smem_u32(smem + E_OFF + m * S * kEBytes);  // + slot * kEBytes
@@ -229,7 +236,9 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                 auto chain = [&](auto lc) {
                     constexpr int LL = decltype(lc)::value;
                     constexpr int K = LL == 0 ? kIn : kHidden;
-                    constexpr uint32_t idesc = tc::idesc_f16(128, LL == 3 ? NP : kHidden);
+                    constexpr int NO = LL == 3 ? NP : kHidden;  // output columns
+                    constexpr int N0 = NO > 256 ? 256 : NO;     // first MMA's columns (UMMA N <= 256)
+                    constexpr uint32_t idesc = tc::idesc_f16(128, N0);
                     // descriptors rebuilt at issue time from opaque copies of the base
                     // addresses: hoisted out of the tile loop they would occupy ~60
                     // registers and spill
@@ -242,6 +251,14 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     for (int kk = 0; kk < K / 16; ++kk)  // +256 B per K=16 slab = +16 in the address field
                         tc::mma_bf16_elect(d, ad + (uint64_t)(kk * 16), bd + (uint64_t)(kk * 16), idesc,
                                            kk > 0 ? 1u : 0u);
+                    if constexpr (NO > 256) {  // packed columns [256, NP): image rows 256.. (32 row groups on)
+                        constexpr uint32_t idesc1 = tc::idesc_f16(128, NO - 256);
+                        const uint64_t bd1 = tc::smem_desc(bbase + 32u * (uint32_t)(K * 16), 128, K * 16);
+#pragma unroll
+                        for (int kk = 0; kk < K / 16; ++kk)
+                            tc::mma_bf16_elect(d + 256u, ad + (uint64_t)(kk * 16), bd1 + (uint64_t)(kk * 16), idesc1,
+                                               kk > 0 ? 1u : 0u);
+                    }
                     tc::mma_commit_elect(LL == 3 ? &raw_full[lk] : &acc_full[m]);
                 };
                 switch (L) {
@@ -285,7 +302,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         }
     } else {
         // ============================ NASG warpgroup ===========================
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(regs_nasg(N)));
+        if constexpr (!streamed(N)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(regs_nasg(N)));
         const int ln = m * S + j;  // this warpgroup's NASG lane: its E, input stage and raw buffer
         const uint32_t my_raw = tmem + raw_col(N, ln) + ((uint32_t)(wq * 32) << 16);
         const uint32_t e_row64 = tc::smem_u32(smem + E_OFF + ln * kEBytes) + (t >> 3) * 1024 + (t & 7) * 16;
@@ -386,6 +403,73 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             uint32_t ph = (uint32_t)(k & 1);
             wg_wait_acc(&raw_full[ln], ph, g, wq);
             NASG_TRACE_AT(1, k, 3)
+            if constexpr (streamed(N)) {
+                // every lane runs the tensor-memory loads (warp-collective), valid row or not
+                constexpr int HD = packed_header(N);
+                float hdr[HD];
+                {
+                    float v[16];
+#pragma unroll
+                    for (int c0 = 0; c0 < HD; c0 += 16) {
+                        tc::tmem_ld16(my_raw + c0, v);
+                        tc::tmem_ld_wait();
+#pragma unroll
+                        for (int jj = 0; jj < 16; ++jj) hdr[c0 + jj] = v[jj];
+                    }
+                }
+                auto hraw = [&](int jj) { return hdr[jj]; };
+                auto lobe7 = [&](int i, float (&r)[7]) {
+                    float r8[8];
+                    __syncwarp();
+                    tc::tmem_ld8_sync(my_raw + HD + 8 * i, r8);
+#pragma unroll
+                    for (int kk = 0; kk < 7; ++kk) r[kk] = r8[kk];
+                };
+                if constexpr (MODE == kModeSample) {
+                    float c;
+                    const float4 o = guide_sample_src<N>(hraw, lobe7, xi, c);
+                    if (valid) {
+                        a.dir_pdf[q] = o;
+                        if (a.c) a.c[q] = c;
+                    }
+                } else if constexpr (MODE == kModePdf) {
+                    const float2 p = guide_pdf_src<N>(hraw, lobe7, make_float3(dir.x, dir.y, dir.z), a.b, bsdf);
+                    if (valid) {
+                        if (a.mix_pdf) a.mix_pdf[q] = p.x;
+                        if (a.guided_pdf) a.guided_pdf[q] = p.y;
+                    }
+                } else if constexpr (MODE == kModeShade) {
+                    float4 o0, o1;
+                    guide_shade_src<N>(hraw, lobe7, xi, a.b, dir, dnee, o0, o1);
+                    if (valid) {
+                        a.sh_out[2 * q] = o0;
+                        a.sh_out[2 * q + 1] = o1;
+                    }
+                } else {  // raw outputs in the reference order (packed_col)
+                    constexpr int D = 8 * N + 1;
+                    float *dst = a.raw + q * D;
+                    if (valid) {
+#pragma unroll
+                        for (int i = 0; i <= N; ++i) dst[i < N ? 7 * N + i : 8 * N] = hdr[i];
+                    }
+#pragma unroll 1
+                    for (int i = 0; i < N; ++i) {
+                        float r[7];
+                        lobe7(i, r);
+                        if (valid) {
+#pragma unroll
+                            for (int kk = 0; kk < 5; ++kk) dst[5 * i + kk] = r[kk];
+                            dst[5 * N + 2 * i] = r[5];
+                            dst[5 * N + 2 * i + 1] = r[6];
+                        }
+                    }
+                }
+                tc::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&raw_empty[ln]);  // buffer free for the next output layer
+                NASG_TRACE_AT(1, k, 4)
+                continue;
+            }
             float raw[NP];
             {
                 float v[32];
@@ -456,7 +540,8 @@ static int query_tc_n(QueryMode mode, const void *img, const QueryArgs &a, int n
         auto k = query_tc_kernel<N, M>;                                                    \
         static const bool regs_ok = [&] {  /* the setmaxnreg split assumes this allocation */ \
             cudaFuncAttributes fa;                                                         \
-            return cudaFuncGetAttributes(&fa, k) == cudaSuccess && fa.numRegs == launch_regs(N); \
+            return cudaFuncGetAttributes(&fa, k) == cudaSuccess &&                         \
+                   (streamed(N) || fa.numRegs == launch_regs(N));                          \
         }();                                                                               \
         if (!regs_ok) return -2;                                                           \
         cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);     \
@@ -477,6 +562,7 @@ int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, in
         case 4: return query_tc_n<4>(mode, img, a, num_sms, s, pdl);
         case 8: return query_tc_n<8>(mode, img, a, num_sms, s, pdl);
         case 16: return query_tc_n<16>(mode, img, a, num_sms, s, pdl);
+        case 32: return query_tc_n<32>(mode, img, a, num_sms, s, pdl);
         default: return -1;
     }
 }

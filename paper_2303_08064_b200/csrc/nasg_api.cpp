@@ -732,7 +732,7 @@ int nasg_create(const nasg_config *cfg, int device, const float bmin[3], const f
     }
     ALLOC(c->wp, packed_f32_floats(c->N) * sizeof(float));
     ALLOC(c->wtp, packed_t32_floats(c->N) * sizeof(float));
-    if (tc_supported(c->N)) ALLOC(c->tc_live, tc_train_image_bytes(c->N));
+    if (tc_train_supported(c->N)) ALLOC(c->tc_live, tc_train_image_bytes(c->N));
     ALLOC(c->d_clamp, sizeof(unsigned long long));
     ALLOC(c->d_adam_t, sizeof(int64_t));
     ALLOC(c->d_nonfinite, 2 * sizeof(int));

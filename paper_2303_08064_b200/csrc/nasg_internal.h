@@ -206,7 +206,8 @@ int query_fp32(int n_comp, QueryMode mode, const float *wp, const QueryArgs &a, 
                cudaStream_t s);
 int query_tc(int n_comp, QueryMode mode, const void *img, const QueryArgs &a, int num_sms,
              cudaStream_t s, bool pdl = false);
-bool tc_supported(int n_comp);
+bool tc_supported(int n_comp);        // tensor-core query kernel compiled for this N
+bool tc_train_supported(int n_comp);  // tensor-core trainer compiled for this N
 
 int decode_raw(int n_comp, bool sample, bool fast, int64_t n, const float *raw, const float4 *xi,
                const float4 *dir, float b, const float *bsdf_pdf, float4 *dir_pdf, float *c,

@@ -261,8 +261,12 @@ __device__ __forceinline__ void lobe_logits(RawFn raw, int i, float (&r)[7]) {
 
 // decode + inverse-CDF lobe pick + sample + mixture pdf at the sample
 // (infer_guide's decode, mixture_sample sphdist.cpp:183-198).
-template <int N, class RawFn>
-__device__ __forceinline__ float4 guide_sample(RawFn raw, float4 xi, float &c_out) {
+// The epilogues read the header through hraw(j) (j <= N) and each lobe's seven
+// logits through lobe7(i, r) with a compile-time i: from a register array of the
+// packed row (RawFn forms below), or streamed lobe by lobe from tensor memory by
+// the 32-lobe tensor-core query, whose 304-column row does not fit in registers.
+template <int N, class HdrFn, class Lobe7Fn>
+__device__ __forceinline__ float4 guide_sample_src(HdrFn raw, Lobe7Fn lobe7, float4 xi, float &c_out) {
     float w[N];
     decode_header<N>(raw, w, c_out);
     int pick = N - 1;
@@ -279,7 +283,7 @@ __device__ __forceinline__ float4 guide_sample(RawFn raw, float4 xi, float &c_ou
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         float r[7];
-        lobe_logits<N>(raw, i, r);
+        lobe7(i, r);
 #pragma unroll
         for (int k = 0; k < 7; ++k) rs[k] = (i == 0 || i == pick) ? r[k] : rs[k];
     });
@@ -291,7 +295,7 @@ __device__ __forceinline__ float4 guide_sample(RawFn raw, float4 xi, float &c_ou
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         float r[7];
-        lobe_logits<N>(raw, i, r);
+        lobe7(i, r);
         Lobe L;
         decode_lobe(r, L);
         // the picked lobe uses the sampler's exact local coordinates; selecting
@@ -304,23 +308,31 @@ __device__ __forceinline__ float4 guide_sample(RawFn raw, float4 xi, float &c_ou
     });
     return make_float4(v.x, v.y, v.z, pdf);
 }
+template <int N, class RawFn>
+__device__ __forceinline__ float4 guide_sample(RawFn raw, float4 xi, float &c_out) {
+    return guide_sample_src<N>(raw, [&](int i, float (&r)[7]) { lobe_logits<N>(raw, i, r); }, xi, c_out);
+}
 
 // mixture_pdf and guided_pdf at a given direction (guiding.cpp:81-85).
-template <int N, class RawFn>
-__device__ __forceinline__ float2 guide_pdf(RawFn raw, float3 v, float b, float bsdf_pdf) {
+template <int N, class HdrFn, class Lobe7Fn>
+__device__ __forceinline__ float2 guide_pdf_src(HdrFn raw, Lobe7Fn lobe7, float3 v, float b, float bsdf_pdf) {
     float w[N], c;
     decode_header<N>(raw, w, c);
     float pdf = 0.f;
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         float r[7];
-        lobe_logits<N>(raw, i, r);
+        lobe7(i, r);
         Lobe L;
         decode_lobe(r, L);
         pdf += w[i] * __expf(lobe_log_g_at(L, v) - L.log_k);
     });
     const float ce = b * c;
     return make_float2(pdf, ce <= 0.f ? bsdf_pdf : ce * pdf + (1.f - ce) * bsdf_pdf);
+}
+template <int N, class RawFn>
+__device__ __forceinline__ float2 guide_pdf(RawFn raw, float3 v, float b, float bsdf_pdf) {
+    return guide_pdf_src<N>(raw, [&](int i, float (&r)[7]) { lobe_logits<N>(raw, i, r); }, v, b, bsdf_pdf);
 }
 
 // Guided scattering at one path vertex (SPEC tracer trace_path; guided_pdf
@@ -330,9 +342,9 @@ __device__ __forceinline__ float2 guide_pdf(RawFn raw, float3 v, float b, float 
 // mixture pdf at the chosen direction and at the NEE direction dnee.xyz (the
 // NEE pdf comes from the same network evaluation).
 //   o0 = (dir, q_mix(dir)),  o1 = (q_mix(nee) or 0 if dnee.w <= 0, c', guided ? 1 : 0, c)
-template <int N, class RawFn>
-__device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float4 dbsdf, float4 dnee, float4 &o0,
-                                            float4 &o1) {
+template <int N, class HdrFn, class Lobe7Fn>
+__device__ __forceinline__ void guide_shade_src(HdrFn raw, Lobe7Fn lobe7, float4 xi, float b, float4 dbsdf,
+                                                float4 dnee, float4 &o0, float4 &o1) {
     float w[N], c;
     decode_header<N>(raw, w, c);
     const float ce = b * c;
@@ -351,7 +363,7 @@ __device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         float r[7];
-        lobe_logits<N>(raw, i, r);
+        lobe7(i, r);
 #pragma unroll
         for (int k = 0; k < 7; ++k) rs[k] = (i == 0 || i == pick) ? r[k] : rs[k];
     });
@@ -365,7 +377,7 @@ __device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         float r[7];
-        lobe_logits<N>(raw, i, r);
+        lobe7(i, r);
         Lobe L;
         decode_lobe(r, L);
         float wl, ql, t2l;
@@ -377,6 +389,11 @@ __device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float
     });
     o0 = make_float4(v.x, v.y, v.z, pv);
     o1 = make_float4(dnee.w > 0.f ? pn : 0.f, ce, tech ? 1.f : 0.f, c);
+}
+template <int N, class RawFn>
+__device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float4 dbsdf, float4 dnee, float4 &o0,
+                                            float4 &o1) {
+    guide_shade_src<N>(raw, [&](int i, float (&r)[7]) { lobe_logits<N>(raw, i, r); }, xi, b, dbsdf, dnee, o0, o1);
 }
 
 // ---- KL gradient in fp32 (bf16 training path) --------------------------------

@@ -1,11 +1,12 @@
 """N = 32 lobes (D = 257 raw outputs, NP = 304 packed columns; the largest
-point of the paper's component sweep, PAPER Table 4) on the fp32 path, against
-the CPU oracle with the N = 4 / 8 tolerances: init bit-exact; raw outputs 2e-5;
-decode / query sample / pdf 1e-3 relative; one training step's gradient rel-L2
-1e-4; a train_iteration tracking the oracle trainer; one render iteration.
-The tensor-core kernels are not built for N = 32 (their f16 weight image plus
-the 304-column delta4 tile exceed one SM's shared memory): asking
-for them fails with NASG_ERR_UNSUPPORTED."""
+point of the paper's component sweep, PAPER Table 4), against the CPU oracle
+with the N = 4 / 8 tolerances: init bit-exact; fp32 raw outputs 2e-5; decode /
+query sample / pdf 1e-3 relative; one training step's gradient rel-L2 1e-4; a
+train_iteration tracking the oracle trainer; one render iteration.  The
+tensor-core query (lobes streamed from tensor memory) at the N = 8 path's bars;
+the tensor-core trainer is not built for N = 32 (its f16 image, bf16 W4 copy and
+304-column delta4 tile exceed one SM's shared memory): asking for
+it fails with NASG_ERR_UNSUPPORTED."""
 import numpy as np
 import pytest
 
@@ -43,12 +44,45 @@ def rel_l2(a, b):
     return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
 
 
-def test_tensor_core_paths_refused(guide):
-    with pytest.raises(nasg.NasgError):
-        guide.precision = nasg.NASG_MLP_BF16
+def test_tensor_core_trainer_refused(guide):
     with pytest.raises(nasg.NasgError):
         guide.train_precision = nasg.NASG_MLP_BF16
-    assert guide.precision == nasg.NASG_MLP_FP32
+    assert guide.train_precision == nasg.NASG_MLP_FP32
+
+
+def test_tc_query_raw_sample_pdf(guide, orc):
+    rng = np.random.default_rng(21)
+    n = (1 << 15) + 77  # a ragged last tile
+    q9, xi = H.queries(rng, n), H.xis(rng, n)
+    w = guide.get_weights(published=True)
+    enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
+    ref_raw = orc.forward(w, enc, out_dim=D)
+    guide.precision = nasg.NASG_MLP_BF16
+    try:
+        raw = guide.query_raw(*split(q9)).cpu().numpy().astype(np.float64)
+        err = np.abs(raw - ref_raw) / (1 + np.abs(ref_raw))
+        print(f"N={N} tensor-core raw: max {err.max():.2e} p99 {np.quantile(err, 0.99):.2e}")
+        assert err.max() <= 5e-3 and np.quantile(err, 0.99) <= 2e-3, (err.max(), np.quantile(err, 0.99))
+        ref, cref = orc.query_sample(w, q9, xi, out_dim=D, threads=8)
+        c = torch.empty(n, dtype=torch.float32, device="cuda")
+        out, _ = guide.query_sample(*split(q9), torch.from_numpy(xi).cuda(), c=c)
+        out = out.cpu().numpy().astype(np.float64)
+        ddir = np.linalg.norm(out[:, :3] - ref[:, :3], axis=1)
+        dpdf = np.abs(out[:, 3] - ref[:, 3]) / ref[:, 3]
+        same = ddir <= 0.05
+        p50 = np.median(dpdf[same])
+        print(f"N={N} tensor-core query: lobe mismatch {1 - same.mean():.2e} pdf p50 {p50:.2e}")
+        assert 1 - same.mean() <= 2e-3 and p50 <= 1e-3, (1 - same.mean(), p50)
+        assert np.median(np.abs(c.cpu().numpy() - cref) / cref) <= 1e-3
+        dirs = H.dirs(rng, n)
+        bsdf = rng.random(n).astype(np.float32)
+        mix, gd = guide.query_pdf(*split(q9), dev4(dirs), 0.5, torch.from_numpy(bsdf).cuda())
+        mref, gref = orc.decode_pdf(ref_raw, dirs, 0.5, bsdf, n_comp=N)
+        rm = np.abs(mix.cpu().numpy() - mref) / mref
+        print(f"N={N} tensor-core pdf: p50 {np.median(rm):.2e} p99 {np.quantile(rm, 0.99):.2e}")
+        assert np.median(rm) <= 1e-3 and np.quantile(rm, 0.99) <= 5e-3
+    finally:
+        guide.precision = nasg.NASG_MLP_FP32
 
 
 def test_init_and_raw_outputs(guide, orc):
@@ -148,6 +182,7 @@ def test_checkpoint_roundtrip(tmp_path, orc):
 def test_render_iteration_n32():
     lo, hi = nasg.scene_bounds(nasg.SCENE_BOX)
     g = nasg.Guide(nasg.TrainerConfig(n_components=N, seed=5), bmin=lo, bmax=hi)
+    g.precision = nasg.NASG_MLP_BF16  # tensor-core shading queries, fp32 training
     r = nasg.Render(g, scene=nasg.SCENE_BOX, width=64, height=64, seed=2, schedule_m=1, schedule_b=1)
     try:
         for _ in range(3):
