@@ -35,7 +35,11 @@ def test_status_strings_and_config_default():
     d = nasg.TrainerConfig()
     assert (cfg.n_components, cfg.sample_capacity, cfg.batch_size, cfg.step_factor) == (8, 1 << 16, 1 << 12, 1)
     assert cfg.learning_rate == pytest.approx(d.learning_rate) and cfg.loss_blend == d.loss_blend
+    assert cfg.hidden_units == d.hidden_units == 128  # the last field: the ctypes layout matches nasg.h
+    assert C.sizeof(cfg) == 48
     assert nasg.n_weights(8) == 49280
+    assert nasg.n_weights(32) == 64 * 128 + 2 * 128 * 128 + 128 * 257
+    assert nasg.n_weights(8, 64) == 64 * 64 + 2 * 64 * 64 + 64 * 65
 
 
 def test_schedules_match_reference(orc):
