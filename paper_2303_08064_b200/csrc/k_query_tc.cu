@@ -27,10 +27,11 @@
 // N = 16 (NP = 160): one MLP warpgroup and two NASG warpgroups ("slots") that
 // take its tiles alternately, each with its own E buffer, input stage and raw
 // buffer (TMEM [128 + 160 j, ...)) — the 16-lobe epilogue is about twice the
-// MLP's work per tile.  N = 32 (NP = 304): one MLP and one NASG warpgroup, raw
-// buffer TMEM [128, 432) written by two output MMAs (N = 256 + 48); the NASG
-// group streams the row's lobes out of tensor memory (the 304 columns do not
-// fit in registers) and keeps the launch's register allocation (no setmaxnreg).
+// MLP's work per tile.  N = 32 (NP = 304): one MLP warpgroup and one NASG lane
+// served by two warpgroups that split each row's lobes (16 each, partial pdf
+// sums meeting in shared memory), raw buffer TMEM [128, 432) written by two
+// output MMAs (N = 256 + 48); they stream the row's lobes out of tensor memory
+// (the 304 columns do not fit in registers).
 // Only the 52 B/query of inputs and 16-20 B/query of outputs touch HBM.
 #include <cuda_bf16.h>
 
@@ -65,7 +66,8 @@ namespace {
 constexpr int pairs_for(int n) { return packed_width(n) > 128 ? 1 : 2; }
 constexpr int slots_for(int n) { return packed_width(n) > 256 ? 1 : (packed_width(n) > 128 ? 2 : 1); }
 constexpr bool streamed(int n) { return packed_width(n) > 256; }  // N = 32: lobes streamed from TMEM
-constexpr int threads_for(int n) { return pairs_for(n) * (1 + slots_for(n)) * 128; }
+constexpr int nasg_wgs(int n) { return streamed(n) ? 2 : 1; }      // warpgroups per NASG lane
+constexpr int threads_for(int n) { return pairs_for(n) * (1 + slots_for(n) * nasg_wgs(n)) * 128; }
 constexpr uint32_t raw_col(int n, int lane) {  // first TMEM column of NASG lane (pair m, slot j) = m * S + j
     return pairs_for(n) == 2 ? 256u + 128u * (uint32_t)lane : 128u + 160u * (uint32_t)lane;
 }
@@ -82,17 +84,21 @@ constexpr int regs_nasg(int n) { return pairs_for(n) == 2 ? 256 - regs_mlp(n) : 
 static_assert(4 * (launch_regs(16) - regs_mlp(16)) >= 2 * 4 * (regs_nasg(16) - launch_regs(16)),
               "N = 16: the NASG groups' setmaxnreg.inc fits what the MLP group releases");
 static_assert(4 * (launch_regs(8) - regs_mlp(8)) >= 4 * (regs_nasg(8) - launch_regs(8)), "N = 8 register split");
+static_assert(4 * (launch_regs(32) - regs_mlp(32)) >= 2 * 4 * (regs_nasg(32) - launch_regs(32)), "N = 32 register split");
 constexpr uint32_t kABytes = 128 * 128 * 2;     // one f16 activation tile, K = 128
 constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 128 columns each
 
 constexpr uint32_t kEBytes = 128 * 64 * 2;      // one encoded tile (layer 0's A operand, K = 64)
 constexpr uint32_t kInBytes = 128 * 52;         // one tile of inputs: 13-float rows or 3 x 2 KB SoA
 
+constexpr uint32_t kXBytes = 12 * 128 * 4;     // N = 32: the two NASG warpgroups' per-row exchange
 template <int N>
 constexpr size_t smem_bytes() {
     constexpr int P = pairs_for(N), Q = pairs_for(N) * slots_for(N);
-    return align1k(img_bytes(N)) + P * kABytes + Q * kEBytes + 2 * Q * kInBytes + (P + 6 * Q + 2) * sizeof(uint64_t);
+    return align1k(img_bytes(N)) + P * kABytes + Q * kEBytes + 2 * Q * kInBytes + (streamed(N) ? kXBytes : 0) +
+           (P + 6 * Q + 2) * sizeof(uint64_t);
 }
+static_assert(smem_bytes<32>() <= 232448, "N = 32 query kernel fits one SM's shared memory");
 
 }  // namespace
 
@@ -155,7 +161,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr uint32_t E_OFF = A_OFF + kPairs * kABytes;    // encoded tiles E_l, one per NASG lane
     constexpr uint32_t IN_OFF = E_OFF + Q * kEBytes;        // input staging: [NASG lane][2 buffers]
-    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + IN_OFF + 2 * Q * kInBytes);  // [pair]
+    constexpr uint32_t X_OFF = IN_OFF + 2 * Q * kInBytes;   // N = 32: [12][128] floats
+    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + X_OFF + (streamed(N) ? kXBytes : 0));  // [pair]
     uint64_t *raw_full = acc_full + kPairs;  // [NASG lane] from here on
     uint64_t *raw_empty = raw_full + Q;
     uint64_t *in_full = raw_empty + Q;  // [lane][buffer]
@@ -171,7 +178,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     const int g = warp >> 2;        // warpgroup: named barrier g + 1
     // warpgroups [0, P): MLP of pair g; then the NASG warpgroups, lane (pair m, slot j)
     const int m = g < kPairs ? g : (g - kPairs) % kPairs;
-    const int j = g < kPairs ? 0 : (g - kPairs) / kPairs;
+    const int j = (g < kPairs || streamed(N)) ? 0 : (g - kPairs) / kPairs;
+    const int pt = streamed(N) && g > kPairs ? 1 : 0;  // N = 32: which half of the lobes
     const int wq = warp & 3;        // TMEM lane quarter of this warp
     const int t = threadIdx.x & 127;
     const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
@@ -185,7 +193,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         for (int i = 0; i < kPairs; ++i) tc::mbar_init(&acc_full[i], 1);
         for (int i = 0; i < Q; ++i) {
             tc::mbar_init(&raw_full[i], 1);
-            tc::mbar_init(&raw_empty[i], 4);  // one arrival per NASG warp
+            tc::mbar_init(&raw_empty[i], 4 * nasg_wgs(N));  // one arrival per NASG warp
             tc::mbar_init(&in_full[2 * i], 1);
             tc::mbar_init(&in_full[2 * i + 1], 1);
             tc::mbar_init(&e_full[i], 1);
@@ -208,7 +216,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 
     if (g < kPairs) {
         // ============================ MLP warpgroup ============================
-        if constexpr (!streamed(N)) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(regs_mlp(N)));
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(regs_mlp(N)));
         const uint32_t my_acc = tmem + m * 128 + ((uint32_t)(wq * 32) << 16);
         const uint32_t a_base = tc::smem_u32(smem + A_OFF + m * kABytes);
         const uint32_t e_base0 = tc::smem_u32(smem + E_OFF + m * S * kEBytes);  // + slot * kEBytes
@@ -302,7 +310,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         }
     } else {
         // ============================ NASG warpgroup ===========================
-        if constexpr (!streamed(N)) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(regs_nasg(N)));
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(regs_nasg(N)));
         const int ln = m * S + j;  // this warpgroup's NASG lane: its E, input stage and raw buffer
         const uint32_t my_raw = tmem + raw_col(N, ln) + ((uint32_t)(wq * 32) << 16);
         const uint32_t e_row64 = tc::smem_u32(smem + E_OFF + ln * kEBytes) + (t >> 3) * 1024 + (t & 7) * 16;
@@ -369,17 +377,17 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
             }
         };
         int64_t tile = (int64_t)blockIdx.x * kPairs + m + (int64_t)j * stride;
-        if (t == 0) {
+        if (t == 0 && pt == 0) {
             load_tile(tile, 0);
             load_tile(tile + lstride, 1);
         }
-        if (tile < ntiles) encode(tile, 0);
+        if (tile < ntiles && pt == 0) encode(tile, 0);
         uint32_t e_ph = 0;
         for (int64_t k = 0; tile < ntiles; tile += lstride, ++k) {
             // the next tile's encoding first: the MLP needs it right after this
             // tile's output layer, the raw outputs arrive only then
             NASG_TRACE_AT(1, k, 0)
-            if (tile + lstride < ntiles) {
+            if (tile + lstride < ntiles && pt == 0) {
                 wg_wait_acc(&e_empty[ln], e_ph, g, wq);
                 NASG_TRACE_AT(1, k, 1)
                 encode(tile + lstride, k + 1);
@@ -425,35 +433,39 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 #pragma unroll
                     for (int kk = 0; kk < 7; ++kk) r[kk] = r8[kk];
                 };
+                float *xrow = reinterpret_cast<float *>(smem + X_OFF) + t;  // this row's exchange slots
+                auto pair_sync = [&]() { asm volatile("bar.sync 9, 256;" ::: "memory"); };
+                const bool out = valid && pt == 0;
                 if constexpr (MODE == kModeSample) {
                     float c;
-                    const float4 o = guide_sample_src<N>(hraw, lobe7, xi, c);
-                    if (valid) {
+                    const float4 o = guide_sample_pair<N>(hraw, lobe7, xi, c, pt, xrow, pair_sync);
+                    if (out) {
                         a.dir_pdf[q] = o;
                         if (a.c) a.c[q] = c;
                     }
                 } else if constexpr (MODE == kModePdf) {
-                    const float2 p = guide_pdf_src<N>(hraw, lobe7, make_float3(dir.x, dir.y, dir.z), a.b, bsdf);
-                    if (valid) {
+                    const float2 p = guide_pdf_pair<N>(hraw, lobe7, make_float3(dir.x, dir.y, dir.z), a.b, bsdf, pt,
+                                                       xrow, pair_sync);
+                    if (out) {
                         if (a.mix_pdf) a.mix_pdf[q] = p.x;
                         if (a.guided_pdf) a.guided_pdf[q] = p.y;
                     }
                 } else if constexpr (MODE == kModeShade) {
                     float4 o0, o1;
-                    guide_shade_src<N>(hraw, lobe7, xi, a.b, dir, dnee, o0, o1);
-                    if (valid) {
+                    guide_shade_pair<N>(hraw, lobe7, xi, a.b, dir, dnee, o0, o1, pt, xrow, pair_sync);
+                    if (out) {
                         a.sh_out[2 * q] = o0;
                         a.sh_out[2 * q + 1] = o1;
                     }
-                } else {  // raw outputs in the reference order (packed_col)
+                } else {  // raw outputs in the reference order (packed_col), lobes split by halves
                     constexpr int D = 8 * N + 1;
                     float *dst = a.raw + q * D;
-                    if (valid) {
+                    if (out) {
 #pragma unroll
                         for (int i = 0; i <= N; ++i) dst[i < N ? 7 * N + i : 8 * N] = hdr[i];
                     }
 #pragma unroll 1
-                    for (int i = 0; i < N; ++i) {
+                    for (int i = pt * (N / 2); i < pt * (N / 2) + N / 2; ++i) {
                         float r[7];
                         lobe7(i, r);
                         if (valid) {

@@ -396,6 +396,150 @@ __device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float
     guide_shade_src<N>(raw, [&](int i, float (&r)[7]) { lobe_logits<N>(raw, i, r); }, xi, b, dbsdf, dnee, o0, o1);
 }
 
+// Two-warpgroup forms (the 32-lobe tensor-core query): warpgroup pt = 0 / 1 owns
+// lobes [pt N/2, pt N/2 + N/2) of the same row.  Both decode the header and the
+// pick; the owner of the picked lobe publishes its logits through the row's
+// scratch x (stride 128 floats between entries), both sample from them, each
+// sums its own lobes' pdf terms and part 1's sums reach part 0 through x.
+// sync() is a barrier over both warpgroups.  Part 0's return value is the
+// result (the pdf sums are (lobes of part 0) + (lobes of part 1)).
+template <int N>
+__device__ __forceinline__ bool own_lobe(int i, int pt) { return (i < N / 2) == (pt == 0); }
+
+template <int N>
+__device__ __forceinline__ int pick_lobe(const float (&w)[N], float xs) {
+    int pick = N - 1;
+    bool found = false;
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        acc += w[i];
+        const bool hit = !found && xs < acc;
+        pick = hit ? i : pick;
+        found |= hit;
+    }
+    return pick;
+}
+
+template <int N, class Lobe7Fn, class SyncFn>
+__device__ __forceinline__ void share_picked(Lobe7Fn lobe7, int pick, int pt, float *x, SyncFn sync, float (&rs)[7]) {
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if (own_lobe<N>(i, pt)) {
+            float r[7];
+            lobe7(i, r);
+            if (i == pick) {
+#pragma unroll
+                for (int k = 0; k < 7; ++k) x[k * 128] = r[k];
+            }
+        }
+    });
+    sync();
+#pragma unroll
+    for (int k = 0; k < 7; ++k) rs[k] = x[k * 128];
+}
+
+template <int N, class HdrFn, class Lobe7Fn, class SyncFn>
+__device__ __forceinline__ float4 guide_sample_pair(HdrFn raw, Lobe7Fn lobe7, float4 xi, float &c_out, int pt, float *x,
+                                                    SyncFn sync) {
+    float w[N];
+    decode_header<N>(raw, w, c_out);
+    const int pick = pick_lobe<N>(w, xi.x);
+    float rs[7];
+    share_picked<N>(lobe7, pick, pt, x, sync, rs);
+    Lobe Ls;
+    decode_lobe(rs, Ls);
+    float ws, qs, t2s;
+    const float3 v = sample_lobe(Ls, xi.y, xi.z, xi.w, ws, qs, t2s);
+    float pdf = 0.f;
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if (own_lobe<N>(i, pt)) {
+            float r[7];
+            lobe7(i, r);
+            Lobe L;
+            decode_lobe(r, L);
+            float wl, ql, t2l;
+            lobe_local(L, v, wl, ql, t2l);
+            const bool me = i == pick;
+            const float lg = lobe_log_g(L, sel(me, ws, wl), sel(me, qs, ql), sel(me, t2s, t2l));
+            pdf += w[i] * __expf(lg - L.log_k);
+        }
+    });
+    if (pt == 1) x[7 * 128] = pdf;
+    sync();
+    if (pt == 0) pdf += x[7 * 128];
+    return make_float4(v.x, v.y, v.z, pdf);
+}
+
+template <int N, class HdrFn, class Lobe7Fn, class SyncFn>
+__device__ __forceinline__ float2 guide_pdf_pair(HdrFn raw, Lobe7Fn lobe7, float3 v, float b, float bsdf_pdf, int pt,
+                                                 float *x, SyncFn sync) {
+    float w[N], c;
+    decode_header<N>(raw, w, c);
+    float pdf = 0.f;
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if (own_lobe<N>(i, pt)) {
+            float r[7];
+            lobe7(i, r);
+            Lobe L;
+            decode_lobe(r, L);
+            pdf += w[i] * __expf(lobe_log_g_at(L, v) - L.log_k);
+        }
+    });
+    if (pt == 1) x[7 * 128] = pdf;
+    sync();
+    if (pt == 0) pdf += x[7 * 128];
+    const float ce = b * c;
+    return make_float2(pdf, ce <= 0.f ? bsdf_pdf : ce * pdf + (1.f - ce) * bsdf_pdf);
+}
+
+template <int N, class HdrFn, class Lobe7Fn, class SyncFn>
+__device__ __forceinline__ void guide_shade_pair(HdrFn raw, Lobe7Fn lobe7, float4 xi, float b, float4 dbsdf,
+                                                 float4 dnee, float4 &o0, float4 &o1, int pt, float *x, SyncFn sync) {
+    float w[N], c;
+    decode_header<N>(raw, w, c);
+    const float ce = b * c;
+    const bool tech = dbsdf.w < ce;
+    const int pick = pick_lobe<N>(w, xi.x);
+    float rs[7];
+    share_picked<N>(lobe7, pick, pt, x, sync, rs);
+    Lobe Ls;
+    decode_lobe(rs, Ls);
+    float ws, qs, t2s;
+    const float3 vm = sample_lobe(Ls, xi.y, xi.z, xi.w, ws, qs, t2s);
+    const float3 v = make_float3(sel(tech, vm.x, dbsdf.x), sel(tech, vm.y, dbsdf.y), sel(tech, vm.z, dbsdf.z));
+    const float3 vn = make_float3(dnee.x, dnee.y, dnee.z);
+    float pv = 0.f, pn = 0.f;
+    static_for<0, N>([&](auto ic) {
+        constexpr int i = decltype(ic)::value;
+        if (own_lobe<N>(i, pt)) {
+            float r[7];
+            lobe7(i, r);
+            Lobe L;
+            decode_lobe(r, L);
+            float wl, ql, t2l;
+            lobe_local(L, v, wl, ql, t2l);
+            const bool me = tech && i == pick;
+            pv += w[i] * __expf(lobe_log_g(L, sel(me, ws, wl), sel(me, qs, ql), sel(me, t2s, t2l)) - L.log_k);
+            lobe_local(L, vn, wl, ql, t2l);
+            pn += w[i] * __expf(lobe_log_g(L, wl, ql, t2l) - L.log_k);
+        }
+    });
+    if (pt == 1) {
+        x[7 * 128] = pv;
+        x[8 * 128] = pn;
+    }
+    sync();
+    if (pt == 0) {
+        pv += x[7 * 128];
+        pn += x[8 * 128];
+    }
+    o0 = make_float4(v.x, v.y, v.z, pv);
+    o1 = make_float4(dnee.w > 0.f ? pn : 0.f, ce, tech ? 1.f : 0.f, c);
+}
+
 // ---- KL gradient in fp32 (bf16 training path) --------------------------------
 // Decode intermediates the chain rule needs (DecodedGuide guiding.hpp:34-42).
 struct LobeG {
