@@ -66,6 +66,30 @@ void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStr
     pack_fp32_kernel<<<148, 256, 0, s>>>(w, n_comp, wp, wtp, wbig);
 }
 
+// Snapshot copy of up to three device buffers (16-byte multiples) in one launch.
+struct Copy3 {
+    const uint4 *src[3];
+    uint4 *dst[3];
+    int64_t n16[3];
+};
+__global__ void copy3_kernel(Copy3 c) {
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < c.n16[k];
+             i += (int64_t)gridDim.x * blockDim.x)
+            c.dst[k][i] = c.src[k][i];
+}
+
+void launch_copy3(const void *const src[3], void *const dst[3], const size_t bytes[3], cudaStream_t s) {
+    Copy3 c{};
+    for (int k = 0; k < 3; ++k) {
+        c.src[k] = static_cast<const uint4 *>(src[k]);
+        c.dst[k] = static_cast<uint4 *>(dst[k]);
+        c.n16[k] = src[k] ? (int64_t)(bytes[k] / 16) : 0;
+    }
+    copy3_kernel<<<148, 256, 0, s>>>(c);
+}
+
 // ------------------------------------------------------------- encoding --
 // One-blob encoding of one query into column r of the feature-major tile.
 // t = (p - min) / ext in double as in encoding.cpp:30; bins in fp32.

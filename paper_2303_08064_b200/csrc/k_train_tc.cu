@@ -265,7 +265,14 @@ size_t tc_train_block_bytes(int n_comp) {  // bf16 bytes per 128-row block over 
     return (size_t)(64 + 3 * 128 + 3 * 128 + packed_width(n_comp)) * 256;
 }
 
-template <int N>
+// COOP (host-chosen when the step has no more tiles than SMs, kWGt > 1): one
+// tile per CTA, and its three warpgroups split every phase of that tile's chain
+// instead of warpgroup 0 running it alone: the forward and backward drains by
+// 16-column units (unit u belongs to warpgroup u % 3; the ReLU gate bits stay
+// with the warpgroup that drained those columns, the backward's row maximum is
+// combined through shared memory) and the KL by lobes (kl_grad_row_coop).
+// Warpgroup 0's warp 0 issues every MMA, after a barrier over all three.
+template <int N, bool COOP>
 __global__ void __launch_bounds__(wgt_for(N) * 128, 1)
 train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__restrict__ samples,
                    const uint32_t *__restrict__ order, int64_t count, const int64_t *live_count, double gscale,
@@ -307,8 +314,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
     }
     {
         const int g = warp >> 2, t = threadIdx.x & 127;
-        const uint32_t my_tmem = tmem + g * 128 + ((uint32_t)((warp & 3) * 32) << 16);
-        const uint32_t a_base = tc::smem_u32(smem + A_OFF + g * kATile);
+        const int gt = COOP ? 0 : g;  // the warpgroup whose tile (accumulator, A tile) this thread works on
+        const uint32_t my_tmem = tmem + gt * 128 + ((uint32_t)((warp & 3) * 32) << 16);
+        const uint32_t a_base = tc::smem_u32(smem + A_OFF + gt * kATile);
         const uint32_t sW = tc::smem_u32(smem);
         // forward layer l (0..3): A = f16 activations (K = 64 | 128), B = the f16 W_l^T image (K-major)
         // backward through W_l (l = 3, 2, 1): A = delta (K = NP | 128), B = the image read MN-major:
@@ -318,8 +326,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         auto issue = [&](int l, bool bwd) {
             tc::fence_proxy_async_smem();
             tc::tc_fence_before();
-            wg_sync(g);
-            if ((warp & 3) == 0) {
+            if constexpr (COOP) asm volatile("bar.sync 8, %0;" ::"r"(kWGt * 128) : "memory");
+            else wg_sync(g);
+            if ((warp & 3) == 0 && (!COOP || g == 0)) {
                 __syncwarp();
                 tc::tc_fence_after();
                 const uint32_t d = tmem + g * 128;
@@ -348,7 +357,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
             }
         };
         uint32_t acc_ph = 0;
-        auto wait_acc = [&]() { wg_wait_acc(&acc_full[g], acc_ph, g, warp & 3); };
+        auto wait_acc = [&]() { wg_wait_acc(&acc_full[gt], acc_ph, g, warp & 3); };
         const float(&inv_ext)[3] = bd.inv_ext;
         int clamped = 0;
         const int64_t stride = (int64_t)gridDim.x * kWGt;
@@ -364,11 +373,13 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         };
         // warpgroup-major tile order: a small batch (the render loop's t = 4096 is 32
         // tiles) spreads one tile per SM instead of three per SM on a third of them
-        int64_t tile = (int64_t)g * gridDim.x + blockIdx.x;
+        int64_t tile = COOP ? (int64_t)blockIdx.x : (int64_t)g * gridDim.x + blockIdx.x;
         // Small batch (no more tiles than CTAs): warpgroups 1 and 2 have no tile of
         // their own and take lobes of warpgroup 0's KL gradient instead (the step's
         // latency is one tile's chain; kl_grad_row_coop splits its longest link).
-        const bool coop = kWGt > 1 && ntiles <= (int64_t)gridDim.x;
+        // COOP: they also take their units of every drain.
+        const bool coop = COOP || (kWGt > 1 && ntiles <= (int64_t)gridDim.x);
+        float *rowmax = reinterpret_cast<float *>(smem + A_OFF + (kWGt - 1) * kATile);  // COOP: [3][128]
         float *coop_sc = reinterpret_cast<float *>(smem + A_OFF + kATile);           // [3N][128], group 1's tile
         int *coop_flg = reinterpret_cast<int *>(coop_sc + 3 * N * kKlScStride);     // [2 x 3][128]
         float *kl_scratch = reinterpret_cast<float *>(smem + A_OFF + g * kATile + kl_sc_off<N>());
@@ -386,14 +397,46 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
             FB_TRACE(ktr, 0)
             const int64_t row = tile * 128 + t;
             const bool valid = row < count;
-            clamped += encode_row_f16(valid, s0, s1, s2, bd, inv_ext, a_base + blk_off(t, 64),
-                                      tb.h0 + tile * (64 * 256) + blk_off(t, 64));
+            if (!COOP || g == 0)
+                clamped += encode_row_f16(valid, s0, s1, s2, bd, inv_ext, a_base + blk_off(t, 64),
+                                          tb.h0 + tile * (64 * 256) + blk_off(t, 64));
             FB_TRACE(ktr, 1)
             issue(0, false);
-            uint32_t mask[3][4] = {};  // ReLU gate bits of h1..h3
+            uint32_t mask[3][4] = {};  // ReLU gate bits of h1..h3 (COOP: [layer][unit slot])
 #pragma unroll 1
             for (int l = 1; l < 4; ++l) {  // hidden layers: ReLU, f16 A + gate bits, bf16 h_l block
                 wait_acc();
+                if constexpr (COOP) {  // this warpgroup's 16-column units u = g, g + 3, g + 6
+                    uint8_t *gh = (l == 1 ? tb.h1 : (l == 2 ? tb.h2 : tb.h3)) + tile * (128 * 256) + blk_off(t, 128);
+#pragma unroll
+                    for (int sl = 0; sl < 3; ++sl) {
+                        const int u = g + 3 * sl;
+                        if (u < 8) {
+                            float v[16];
+                            tc::tmem_ld16(my_tmem + u * 16, v);
+                            tc::tmem_ld_wait();
+                            uint32_t bits = 0;
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                uint32_t p[4], q[4];
+#pragma unroll
+                                for (int h = 0; h < 4; ++h) {
+                                    p[h] = tc::pack_f16x2_relu_sat(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                                    q[h] = tc::pack_bf16x2_relu(v[8 * c + 2 * h], v[8 * c + 2 * h + 1]);
+                                    bits = gate_flags(bits, p[h], 4 * c + h);
+                                }
+                                tc::st_shared_v4(a_base + blk_off(t, 128) + (2 * u + c) * 128, p[0], p[1], p[2], p[3]);
+                                st_g16(gh + (2 * u + c) * 128, q[0], q[1], q[2], q[3]);
+                            }
+                            mask[0][sl] = l == 1 ? bits : mask[0][sl];
+                            mask[1][sl] = l == 2 ? bits : mask[1][sl];
+                            mask[2][sl] = l == 3 ? bits : mask[2][sl];
+                        }
+                    }
+                    issue(l, false);
+                    FB_TRACE(ktr, 1 + l)
+                    continue;
+                }
                 uint8_t *gh = (l == 1 ? tb.h1 : (l == 2 ? tb.h2 : tb.h3)) + tile * (128 * 256) + blk_off(t, 128);
 #pragma unroll
                 for (int q4 = 0; q4 < 4; ++q4) {
@@ -455,8 +498,9 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                 };
                 auto put_lobe = [&](int i, const float (&g8)[8]) { put_chunk(HD / 8 + i, g8); };
                 if (coop)
-                    st = kl_grad_row_coop<N, kWGt>(0, valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr,
-                                                   put_lobe, lossf, coop_sc + t, coop_flg + t, coop_sync);
+                    st = kl_grad_row_coop<N, kWGt>(COOP ? g : 0, valid, hdr, lobe, srow, (float)b, (float)e,
+                                                   (float)gscale, ghdr, put_lobe, lossf, coop_sc + t, coop_flg + t,
+                                                   coop_sync);
                 else
                     st = kl_grad_row_fast<N>(valid, hdr, lobe, srow, (float)b, (float)e, (float)gscale, ghdr,
                                              put_lobe, lossf, kl_scratch + t);
@@ -465,7 +509,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     for (int c = 0; c < HD / 8; ++c) put_chunk(c, ghdr + 8 * c);
                 }
             }
-            if (st != kKlOk) {  // zero row: invalid, p = 0 or dropped
+            if (st != kKlOk && (!COOP || g == 0)) {  // zero row: invalid, p = 0 or dropped
                 const float z8[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll 1
                 for (int c = 0; c < NP / 8; ++c) put_chunk(c, z8);
@@ -476,7 +520,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
             FB_TRACE(ktr, 6)
             issue(3, true);
             load_sample(tile + stride);  // prefetch: in flight through the backward pass
-            {  // tile statistics, deterministic order (warp tree, then warps 0..3)
+            if (!COOP || g == 0) {  // tile statistics, deterministic order (warp tree, then warps 0..3)
                 double ls = state == 1 ? loss : 0.0, lc = state == 1 ? 1.0 : 0.0, dr = state == 2 ? 1.0 : 0.0;
 #pragma unroll
                 for (int o = 16; o > 0; o >>= 1) {
@@ -509,6 +553,60 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
             static_for<0, 3>([&](auto jc) {
                 constexpr int l = 3 - decltype(jc)::value;
                 wait_acc();
+                if constexpr (COOP) {  // this warpgroup's units; the row maximum combined over the three
+                    uint8_t *gd = (l == 1 ? tb.d1 : (l == 2 ? tb.d2 : tb.d3)) + tile * (128 * 256) + blk_off(t, 128);
+                    int k = 0;
+                    if (l > 1) {
+                        float m = 0.f;
+#pragma unroll
+                        for (int sl = 0; sl < 3; ++sl) {
+                            const int u = g + 3 * sl;
+                            if (u < 8) {
+                                float v[16];
+                                tc::tmem_ld16(my_tmem + u * 16, v);
+                                tc::tmem_ld_wait();
+#pragma unroll
+                                for (int jj = 0; jj < 16; ++jj) m = fmaxf(m, fabsf(v[jj]));
+                            }
+                        }
+                        rowmax[g * 128 + t] = m;
+                        asm volatile("bar.sync 10, %0;" ::"r"(kWGt * 128) : "memory");
+                        m = fmaxf(fmaxf(rowmax[t], rowmax[128 + t]), rowmax[256 + t]);
+                        k = row_scale_exp(m, E);
+                    }
+                    const float ks = exp2i(k);
+                    const uint32_t un = (uint32_t)(127 - E) << 7, unscale = un | (un << 16);  // 2^-E as bf16x2
+#pragma unroll
+                    for (int sl = 0; sl < 3; ++sl) {
+                        const int u = g + 3 * sl;
+                        if (u < 8) {
+                            float v[16];
+                            tc::tmem_ld16(my_tmem + u * 16, v);
+                            tc::tmem_ld_wait();
+                            const uint32_t bits = mask[l - 1][sl];
+#pragma unroll
+                            for (int c = 0; c < 2; ++c) {
+                                uint32_t p[4], q[4];
+#pragma unroll
+                                for (int h = 0; h < 4; ++h) {
+                                    const int i0 = 8 * c + 2 * h;
+                                    const uint32_t gm = gate_mask(bits, 4 * c + h);
+                                    q[h] = tc::pack_bf16x2(v[i0], v[i0 + 1]);
+                                    if (l < 3) q[h] = mul_bf16x2(q[h], unscale);
+                                    q[h] &= gm;
+                                    if (l > 1) p[h] = tc::pack_f16x2_sat(v[i0] * ks, v[i0 + 1] * ks) & gm;
+                                }
+                                if (l > 1)
+                                    tc::st_shared_v4(a_base + blk_off(t, 128) + (2 * u + c) * 128, p[0], p[1], p[2], p[3]);
+                                st_g16(gd + (2 * u + c) * 128, q[0], q[1], q[2], q[3]);
+                            }
+                        }
+                    }
+                    E += k;
+                    if (l > 1) issue(l - 1, true);
+                    FB_TRACE(ktr, 10 - l)
+                    return;
+                }
                 uint8_t *gd = (l == 1 ? tb.d1 : (l == 2 ? tb.d2 : tb.d3)) + tile * (128 * 256) + blk_off(t, 128);
                 int k = 0;
                 if (l > 1) {  // pass 1: the row's maximum |value|
@@ -553,7 +651,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
             });
             tc::tc_fence_before();
         }
-        if (coop && g > 0 && (int64_t)blockIdx.x < ntiles) {  // helper in warpgroup 0's KL
+        if (!COOP && coop && g > 0 && (int64_t)blockIdx.x < ntiles) {  // helper in warpgroup 0's KL
             constexpr int HD = packed_header(N);
             const int64_t tl = blockIdx.x;
             load_sample(tl);
@@ -799,12 +897,23 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
         }
         const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
         const uint8_t *im = static_cast<const uint8_t *>(img);
+        // one tile per CTA and no classification: the three warpgroups split the tile's chain
+        const bool coop_split = !live_count && ntiles <= num_sms && getenv("NASG_NO_COOP_SPLIT") == nullptr;
         auto launch_fb = [&](auto nc) {
             constexpr int NC = decltype(nc)::value;
             constexpr size_t sm = fb_smem<NC>();
-            cudaFuncSetAttribute(train_tc_fb_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            launch_pdl(pdl, train_tc_fb_kernel<NC>, dim3(grid), dim3(wgt_for(NC) * 128), sm, s, im, samples, rows,
-                       count, live_count, gscale, b, loss_blend, bounds, tb, clamp_count);
+            auto go = [&](auto kern) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+                launch_pdl(pdl, kern, dim3(grid), dim3(wgt_for(NC) * 128), sm, s, im, samples, rows, count,
+                           live_count, gscale, b, loss_blend, bounds, tb, clamp_count);
+            };
+            if constexpr (wgt_for(NC) > 1) {
+                if (coop_split) {
+                    go(train_tc_fb_kernel<NC, true>);
+                    return;
+                }
+            }
+            go(train_tc_fb_kernel<NC, false>);
         };
         if (n_comp == 8) launch_fb(std::integral_constant<int, 8>{});
         else if (n_comp == 4) launch_fb(std::integral_constant<int, 4>{});

@@ -307,12 +307,21 @@ int do_publish(nasg_ctx *c) {
     for (auto &rd : P.readers) CUDA_TRY(cudaStreamWaitEvent(c->stream, rd.second, 0));
     for (auto &rd : P.readers) cudaEventDestroy(rd.second);
     P.readers.clear();
-    CUDA_TRY(cudaMemcpyAsync(P.w, c->w, c->nw * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
-    launch_pack_fp32(P.w, c->N, P.wp, nullptr, c->stream);
-    c->launches++;
-    if (P.tc) {
-        launch_pack_tc(P.w, c->N, P.tc, c->stream);
+    if (!P.tc || c->tc_live) {
+        // the live packed images are current with c->w (every Adam step and every
+        // host weight change re-packs them), and the query image is the first
+        // img_bytes of the trainer's: the snapshot is three copies in one launch
+        const void *src[3] = {c->w, c->wp, P.tc ? c->tc_live : nullptr};
+        void *dst[3] = {P.w, P.wp, P.tc};
+        const size_t bytes[3] = {c->nw * sizeof(float), packed_f32_floats(c->N) * sizeof(float),
+                                 P.tc ? tc_image_bytes(c->N) : 0};
+        launch_copy3(src, dst, bytes, c->stream);
         c->launches++;
+    } else {  // N = 32: a query image without a trainer image
+        CUDA_TRY(cudaMemcpyAsync(P.w, c->w, c->nw * sizeof(float), cudaMemcpyDeviceToDevice, c->stream));
+        launch_pack_fp32(P.w, c->N, P.wp, nullptr, c->stream);
+        launch_pack_tc(P.w, c->N, P.tc, c->stream);
+        c->launches += 2;
     }
     CHECK_LAUNCH();
     CUDA_TRY(cudaEventRecord(P.ev, c->stream));

@@ -94,6 +94,8 @@ struct Bounds {
 // ---- kernels: packing -------------------------------------------------------
 // wbig (nullable) is OR-ed with 1 when a weight is not finite or |w| >= kSafeWeight
 void launch_pack_fp32(const float *w, int n_comp, float *wp, float *wtp, cudaStream_t s, int *wbig = nullptr);
+// one-launch copy of up to three buffers (null src: skipped; sizes multiples of 16 B)
+void launch_copy3(const void *const src[3], void *const dst[3], const size_t bytes[3], cudaStream_t s);
 
 // Weight magnitude below which no forward pass can overflow for inputs with
 // |feature| <= 2 (one-blob bins in [0,1], pad 1, direction components <= 2):
