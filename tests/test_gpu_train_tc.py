@@ -144,3 +144,23 @@ def test_tc_training_empty_and_ragged():
     assert st.steps == 4 and st.skipped_updates == 0 and np.isfinite(st.mean_loss)
     assert g.train_iteration(None, 1.0).steps == 0
     g.close()
+
+
+@pytest.mark.parametrize("n_comp", [4, 8])
+def test_coop_split_bit_identical(monkeypatch, n_comp):
+    """The small-batch K_fb variant whose three warpgroups split the tile chain
+    (train_tc_fb_kernel<N, true>) computes the same bits as warpgroup 0 alone
+    (NASG_NO_COOP_SPLIT selects the latter): gradient, loss and weights."""
+    s = torch.from_numpy(H.samples(np.random.default_rng(17), 5000)).cuda()
+    out = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("NASG_NO_COOP_SPLIT", "1")
+        g = nasg.Guide(nasg.TrainerConfig(n_components=n_comp, seed=21, sample_capacity=5000, batch_size=5000))
+        g.train_precision = nasg.NASG_MLP_BF16
+        st = g.train_iteration(s, 0.7)
+        out.append((g.last_grad(), st.mean_loss, g.get_weights()))
+        g.close()
+    monkeypatch.delenv("NASG_NO_COOP_SPLIT", raising=False)
+    (g0, l0, w0), (g1, l1, w1) = out
+    assert np.array_equal(g0, g1) and l0 == l1 and np.array_equal(w0, w1)
