@@ -65,7 +65,10 @@ namespace {
 // twice the MLP's work per tile), raw buffers TMEM [128, 288) and [288, 448).
 constexpr int pairs_for(int n) { return packed_width(n) > 128 ? 1 : 2; }
 constexpr int slots_for(int n) { return packed_width(n) > 256 ? 1 : (packed_width(n) > 128 ? 2 : 1); }
-constexpr bool streamed(int n) { return packed_width(n) > 256; }  // N = 32: lobes streamed from TMEM
+// N = 32: the row's lobes streamed from TMEM by two warpgroups per NASG lane (the
+// 304 columns do not fit in registers).  The same split at N = 8 (four NASG
+// warpgroups at 96 registers, MLP at 48) ran at 5.77e9 vs 8.02e9 q/s: reverted.
+constexpr bool streamed(int n) { return packed_width(n) > 256; }
 constexpr int nasg_wgs(int n) { return streamed(n) ? 2 : 1; }      // warpgroups per NASG lane
 constexpr int threads_for(int n) { return pairs_for(n) * (1 + slots_for(n) * nasg_wgs(n)) * 128; }
 constexpr uint32_t raw_col(int n, int lane) {  // first TMEM column of NASG lane (pair m, slot j) = m * S + j
@@ -91,12 +94,10 @@ constexpr uint32_t kTmemCols = 512;             // [acc0 | acc1 | raw0 | raw1], 
 constexpr uint32_t kEBytes = 128 * 64 * 2;      // one encoded tile (layer 0's A operand, K = 64)
 constexpr uint32_t kInBytes = 128 * 52;         // one tile of inputs: 13-float rows or 3 x 2 KB SoA
 
-constexpr uint32_t kXBytes = 12 * 128 * 4;     // N = 32: the two NASG warpgroups' per-row exchange
 template <int N>
 constexpr size_t smem_bytes() {
     constexpr int P = pairs_for(N), Q = pairs_for(N) * slots_for(N);
-    return align1k(img_bytes(N)) + P * kABytes + Q * kEBytes + 2 * Q * kInBytes + (streamed(N) ? kXBytes : 0) +
-           (P + 6 * Q + 2) * sizeof(uint64_t);
+    return align1k(img_bytes(N)) + P * kABytes + Q * kEBytes + 2 * Q * kInBytes + (P + 6 * Q + 2) * sizeof(uint64_t);
 }
 static_assert(smem_bytes<32>() <= 232448, "N = 32 query kernel fits one SM's shared memory");
 
@@ -161,8 +162,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     extern __shared__ __align__(1024) uint8_t smem[];
     constexpr uint32_t E_OFF = A_OFF + kPairs * kABytes;    // encoded tiles E_l, one per NASG lane
     constexpr uint32_t IN_OFF = E_OFF + Q * kEBytes;        // input staging: [NASG lane][2 buffers]
-    constexpr uint32_t X_OFF = IN_OFF + 2 * Q * kInBytes;   // N = 32: [12][128] floats
-    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + X_OFF + (streamed(N) ? kXBytes : 0));  // [pair]
+    uint64_t *acc_full = reinterpret_cast<uint64_t *>(smem + IN_OFF + 2 * Q * kInBytes);  // [pair]
     uint64_t *raw_full = acc_full + kPairs;  // [NASG lane] from here on
     uint64_t *raw_empty = raw_full + Q;
     uint64_t *in_full = raw_empty + Q;  // [lane][buffer]
@@ -177,9 +177,11 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = warp >> 2;        // warpgroup: named barrier g + 1
     // warpgroups [0, P): MLP of pair g; then the NASG warpgroups, lane (pair m, slot j)
-    const int m = g < kPairs ? g : (g - kPairs) % kPairs;
-    const int j = (g < kPairs || streamed(N)) ? 0 : (g - kPairs) / kPairs;
-    const int pt = streamed(N) && g > kPairs ? 1 : 0;  // N = 32: which half of the lobes
+    // warpgroups [P, P + Q): NASG lanes 0..Q-1 (part 0); streamed: [P + Q, P + 2Q) their part 1
+    const int lnq = g < kPairs ? 0 : (g - kPairs) % Q;
+    const int pt = g < kPairs ? 0 : (g - kPairs) / Q;  // which half of the lobes (streamed)
+    const int m = g < kPairs ? g : lnq / S;
+    const int j = g < kPairs ? 0 : lnq % S;
     const int wq = warp & 3;        // TMEM lane quarter of this warp
     const int t = threadIdx.x & 127;
     const int64_t nrows = a.n_dev ? min((int64_t)*a.n_dev, a.n) : a.n;  // a wavefront queue sets n_dev
@@ -433,26 +435,55 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
 #pragma unroll
                     for (int kk = 0; kk < 7; ++kk) r[kk] = r8[kk];
                 };
-                float *xrow = reinterpret_cast<float *>(smem + X_OFF) + t;  // this row's exchange slots
-                auto pair_sync = [&]() { asm volatile("bar.sync 9, 256;" ::: "memory"); };
+                // the lane's two warpgroups exchange through tensor memory behind the
+                // raw columns: [0, 8) part 0's picked logits, [8, 16) part 1's, [16, 18) sums
+                struct Xchg {
+                    uint32_t base;
+                    int pt, bar;
+                    __device__ __forceinline__ void sync() const {
+                        tc::tmem_st_wait();
+                        tc::tc_fence_before();
+                        asm volatile("bar.sync %0, 256;" ::"r"(bar) : "memory");
+                        tc::tc_fence_after();
+                    }
+                    __device__ __forceinline__ void picked(float (&rs)[7], bool own) const {
+                        const float v8[8] = {rs[0], rs[1], rs[2], rs[3], rs[4], rs[5], rs[6], 0.f};
+                        tc::tmem_st8(base + 8u * (uint32_t)pt, v8);
+                        sync();
+                        float o[8];
+                        tc::tmem_ld8_sync(base + 8u * (uint32_t)(1 - pt), o);
+#pragma unroll
+                        for (int k = 0; k < 7; ++k) rs[k] = own ? rs[k] : o[k];
+                    }
+                    __device__ __forceinline__ void to0(float &a, float &b) const {
+                        if (pt == 1) tc::tmem_st2(base + 16u, a, b);
+                        sync();
+                        if (pt == 0) {
+                            float x, y;
+                            tc::tmem_ld2_sync(base + 16u, x, y);
+                            a += x;
+                            b += y;
+                        }
+                    }
+                };
+                Xchg xc{my_raw + (uint32_t)NP, pt, 9 + ln};
                 const bool out = valid && pt == 0;
                 if constexpr (MODE == kModeSample) {
                     float c;
-                    const float4 o = guide_sample_pair<N>(hraw, lobe7, xi, c, pt, xrow, pair_sync);
+                    const float4 o = guide_sample_pair<N>(hraw, lobe7, xi, c, pt, xc);
                     if (out) {
                         a.dir_pdf[q] = o;
                         if (a.c) a.c[q] = c;
                     }
                 } else if constexpr (MODE == kModePdf) {
-                    const float2 p = guide_pdf_pair<N>(hraw, lobe7, make_float3(dir.x, dir.y, dir.z), a.b, bsdf, pt,
-                                                       xrow, pair_sync);
+                    const float2 p = guide_pdf_pair<N>(hraw, lobe7, make_float3(dir.x, dir.y, dir.z), a.b, bsdf, pt, xc);
                     if (out) {
                         if (a.mix_pdf) a.mix_pdf[q] = p.x;
                         if (a.guided_pdf) a.guided_pdf[q] = p.y;
                     }
                 } else if constexpr (MODE == kModeShade) {
                     float4 o0, o1;
-                    guide_shade_pair<N>(hraw, lobe7, xi, a.b, dir, dnee, o0, o1, pt, xrow, pair_sync);
+                    guide_shade_pair<N>(hraw, lobe7, xi, a.b, dir, dnee, o0, o1, pt, xc);
                     if (out) {
                         a.sh_out[2 * q] = o0;
                         a.sh_out[2 * q + 1] = o1;

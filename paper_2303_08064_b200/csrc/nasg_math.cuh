@@ -396,13 +396,13 @@ __device__ __forceinline__ void guide_shade(RawFn raw, float4 xi, float b, float
     guide_shade_src<N>(raw, [&](int i, float (&r)[7]) { lobe_logits<N>(raw, i, r); }, xi, b, dbsdf, dnee, o0, o1);
 }
 
-// Two-warpgroup forms (the 32-lobe tensor-core query): warpgroup pt = 0 / 1 owns
-// lobes [pt N/2, pt N/2 + N/2) of the same row.  Both decode the header and the
-// pick; the owner of the picked lobe publishes its logits through the row's
-// scratch x (stride 128 floats between entries), both sample from them, each
-// sums its own lobes' pdf terms and part 1's sums reach part 0 through x.
-// sync() is a barrier over both warpgroups.  Part 0's return value is the
-// result (the pdf sums are (lobes of part 0) + (lobes of part 1)).
+// Two-warpgroup forms (the split-lobe tensor-core query): warpgroup pt = 0 / 1
+// owns lobes [pt N/2, pt N/2 + N/2) of the same row.  Both decode the header and
+// the pick; the owner of the picked lobe passes its logits to the other
+// (xc.picked), both sample from them, each sums its own lobes' pdf terms and
+// part 1's sums reach part 0 (xc.to0).  Part 0's return value is the result (the
+// pdf sums are (lobes of part 0) + (lobes of part 1)).  xc is the kernel's
+// exchange between the two warpgroups (through tensor memory).
 template <int N>
 __device__ __forceinline__ bool own_lobe(int i, int pt) { return (i < N / 2) == (pt == 0); }
 
@@ -421,32 +421,29 @@ __device__ __forceinline__ int pick_lobe(const float (&w)[N], float xs) {
     return pick;
 }
 
-template <int N, class Lobe7Fn, class SyncFn>
-__device__ __forceinline__ void share_picked(Lobe7Fn lobe7, int pick, int pt, float *x, SyncFn sync, float (&rs)[7]) {
+template <int N, class Lobe7Fn, class Xchg>
+__device__ __forceinline__ void share_picked(Lobe7Fn lobe7, int pick, int pt, Xchg &xc, float (&rs)[7]) {
+#pragma unroll
+    for (int k = 0; k < 7; ++k) rs[k] = 0.f;
     static_for<0, N>([&](auto ic) {
         constexpr int i = decltype(ic)::value;
         if (own_lobe<N>(i, pt)) {
             float r[7];
             lobe7(i, r);
-            if (i == pick) {
 #pragma unroll
-                for (int k = 0; k < 7; ++k) x[k * 128] = r[k];
-            }
+            for (int k = 0; k < 7; ++k) rs[k] = i == pick ? r[k] : rs[k];
         }
     });
-    sync();
-#pragma unroll
-    for (int k = 0; k < 7; ++k) rs[k] = x[k * 128];
+    xc.picked(rs, own_lobe<N>(pick, pt));
 }
 
-template <int N, class HdrFn, class Lobe7Fn, class SyncFn>
-__device__ __forceinline__ float4 guide_sample_pair(HdrFn raw, Lobe7Fn lobe7, float4 xi, float &c_out, int pt, float *x,
-                                                    SyncFn sync) {
+template <int N, class HdrFn, class Lobe7Fn, class Xchg>
+__device__ __forceinline__ float4 guide_sample_pair(HdrFn raw, Lobe7Fn lobe7, float4 xi, float &c_out, int pt, Xchg &xc) {
     float w[N];
     decode_header<N>(raw, w, c_out);
     const int pick = pick_lobe<N>(w, xi.x);
     float rs[7];
-    share_picked<N>(lobe7, pick, pt, x, sync, rs);
+    share_picked<N>(lobe7, pick, pt, xc, rs);
     Lobe Ls;
     decode_lobe(rs, Ls);
     float ws, qs, t2s;
@@ -466,15 +463,14 @@ __device__ __forceinline__ float4 guide_sample_pair(HdrFn raw, Lobe7Fn lobe7, fl
             pdf += w[i] * __expf(lg - L.log_k);
         }
     });
-    if (pt == 1) x[7 * 128] = pdf;
-    sync();
-    if (pt == 0) pdf += x[7 * 128];
+    float dummy = 0.f;
+    xc.to0(pdf, dummy);
     return make_float4(v.x, v.y, v.z, pdf);
 }
 
-template <int N, class HdrFn, class Lobe7Fn, class SyncFn>
+template <int N, class HdrFn, class Lobe7Fn, class Xchg>
 __device__ __forceinline__ float2 guide_pdf_pair(HdrFn raw, Lobe7Fn lobe7, float3 v, float b, float bsdf_pdf, int pt,
-                                                 float *x, SyncFn sync) {
+                                                 Xchg &xc) {
     float w[N], c;
     decode_header<N>(raw, w, c);
     float pdf = 0.f;
@@ -488,23 +484,22 @@ __device__ __forceinline__ float2 guide_pdf_pair(HdrFn raw, Lobe7Fn lobe7, float
             pdf += w[i] * __expf(lobe_log_g_at(L, v) - L.log_k);
         }
     });
-    if (pt == 1) x[7 * 128] = pdf;
-    sync();
-    if (pt == 0) pdf += x[7 * 128];
+    float dummy = 0.f;
+    xc.to0(pdf, dummy);
     const float ce = b * c;
     return make_float2(pdf, ce <= 0.f ? bsdf_pdf : ce * pdf + (1.f - ce) * bsdf_pdf);
 }
 
-template <int N, class HdrFn, class Lobe7Fn, class SyncFn>
+template <int N, class HdrFn, class Lobe7Fn, class Xchg>
 __device__ __forceinline__ void guide_shade_pair(HdrFn raw, Lobe7Fn lobe7, float4 xi, float b, float4 dbsdf,
-                                                 float4 dnee, float4 &o0, float4 &o1, int pt, float *x, SyncFn sync) {
+                                                 float4 dnee, float4 &o0, float4 &o1, int pt, Xchg &xc) {
     float w[N], c;
     decode_header<N>(raw, w, c);
     const float ce = b * c;
     const bool tech = dbsdf.w < ce;
     const int pick = pick_lobe<N>(w, xi.x);
     float rs[7];
-    share_picked<N>(lobe7, pick, pt, x, sync, rs);
+    share_picked<N>(lobe7, pick, pt, xc, rs);
     Lobe Ls;
     decode_lobe(rs, Ls);
     float ws, qs, t2s;
@@ -527,15 +522,7 @@ __device__ __forceinline__ void guide_shade_pair(HdrFn raw, Lobe7Fn lobe7, float
             pn += w[i] * __expf(lobe_log_g(L, wl, ql, t2l) - L.log_k);
         }
     });
-    if (pt == 1) {
-        x[7 * 128] = pv;
-        x[8 * 128] = pn;
-    }
-    sync();
-    if (pt == 0) {
-        pv += x[7 * 128];
-        pn += x[8 * 128];
-    }
+    xc.to0(pv, pn);
     o0 = make_float4(v.x, v.y, v.z, pv);
     o1 = make_float4(dnee.w > 0.f ? pn : 0.f, ce, tech ? 1.f : 0.f, c);
 }
