@@ -66,12 +66,12 @@ struct Paths {
     float *prev_pdf;        // q-hat of the last scatter; < 0: camera ray or delta bounce
     int *alive, *pending;   // pending: a non-delta vertex waiting for K_update
     int *act[2];            // compacted lists of the paths alive at the start of a bounce (by parity)
-    int *nact;              // their lengths [2]
+    int *nact;              // their lengths, one per bounce [kMaxDepthCap + 1] (zeroed per iteration)
     float4 *vx, *vn, *vwo, *vdb, *vdn, *vnee;
     int *slot, *rank, *bsdf_ok;
     // guide queue
     float4 *qx, *qwo, *qn, *qxi, *qdb, *qdn, *qout;
-    int *qcount;
+    int *qcount;            // guided queries queued at each bounce [kMaxDepthCap] (zeroed per iteration)
     // training records [depth][ncap]
     int64_t ncap;
     float4 *rx, *rwo, *rn, *rwi, *rfc, *rbeta, *rlb;
@@ -147,14 +147,6 @@ __global__ void k_begin(Paths P, Frame F) {
 
 // per-bounce queue reset; the previous bounce's queue length feeds the counter;
 // the list the coming bounce's survivors are appended to starts empty
-__global__ void k_queue_reset(Paths P, int next) {
-    pdl_trigger();
-    pdl_wait();  // every input comes from the previous kernel on the stream
-    P.ctr[1] += (unsigned long long)*P.qcount;
-    *P.qcount = 0;
-    P.nact[next] = 0;
-}
-
 __device__ __forceinline__ void isect_path(Paths &P, const Frame &F, int bounce, int guided, int64_t i) {
     if (!P.alive[i]) return;
     const Scene &S = c_scene;
@@ -228,7 +220,7 @@ __device__ __forceinline__ void isect_path(Paths &P, const Frame &F, int bounce,
     P.pending[i] = 1;
     int slot = -1;
     if (guided) {
-        slot = atomicAdd(P.qcount, 1);
+        slot = atomicAdd(&P.qcount[bounce], 1);
         P.qx[slot] = f4(h.x, 0.f);
         P.qwo[slot] = f4(wo, 0.f);
         P.qn[slot] = f4(n, 0.f);
@@ -322,7 +314,7 @@ __global__ void k_isect(Paths P, Frame F, int bounce, int guided) {
     pdl_trigger();
     pdl_wait();  // every input comes from the previous kernel on the stream
     const int *list = P.act[bounce & 1];
-    const int cnt = P.nact[bounce & 1];
+    const int cnt = P.nact[bounce];
     const int lane = threadIdx.x & 31;
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); w < cnt;
          w += (int64_t)gridDim.x * blockDim.x)
@@ -337,8 +329,8 @@ __global__ void k_update(Paths P, Frame F, int bounce) {
     pdl_wait();  // every input comes from the previous kernel on the stream
     const int *list = P.act[bounce & 1];
     int *next = P.act[(bounce + 1) & 1];
-    int *ncount = &P.nact[(bounce + 1) & 1];
-    const int cnt = P.nact[bounce & 1];
+    int *ncount = &P.nact[bounce + 1];
+    const int cnt = P.nact[bounce];
     const int lane = threadIdx.x & 31;
     for (int64_t w = (int64_t)blockIdx.x * blockDim.x + (threadIdx.x & ~31); w < cnt;
          w += (int64_t)gridDim.x * blockDim.x) {
@@ -451,10 +443,15 @@ __global__ void k_records(Paths P) {
     }
 }
 
-__global__ void k_accumulate(Paths P, float w, int first) {
+__global__ void k_accumulate(Paths P, float w, int first, int depth) {
     pdl_trigger();
     pdl_wait();  // every input comes from the previous kernel on the stream
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i == 0) {  // guided vertices of the iteration: the per-bounce query counts
+        unsigned long long q = 0;
+        for (int k = 0; k < depth; ++k) q += (unsigned long long)P.qcount[k];
+        P.ctr[1] = q;
+    }
     if (i >= P.n) return;
     float4 L = P.L[i];
     if (!(isfinite(L.x) && isfinite(L.y) && isfinite(L.z))) {  // discarded, counted, never on film
@@ -764,9 +761,9 @@ int nasg_render_create(nasg_ctx *ctx, const nasg_render_config *cfg, nasg_render
     if ((rc = alloc(r, &(ptr), (size_t)(count))) != NASG_OK) return fail_out(rc);
     A(P.o, P.n) A(P.d, P.n) A(P.beta, P.n) A(P.L, P.n) A(P.prev_pdf, P.n) A(P.alive, P.n) A(P.pending, P.n)
     A(P.vx, P.n) A(P.vn, P.n) A(P.vwo, P.n) A(P.vdb, P.n) A(P.vdn, P.n) A(P.vnee, P.n)
-    A(P.slot, P.n) A(P.rank, P.n) A(P.bsdf_ok, P.n) A(P.act[0], P.n) A(P.act[1], P.n) A(P.nact, 2)
+    A(P.slot, P.n) A(P.rank, P.n) A(P.bsdf_ok, P.n) A(P.act[0], P.n) A(P.act[1], P.n) A(P.nact, kMaxDepthCap + 1)
     A(P.qx, P.n) A(P.qwo, P.n) A(P.qn, P.n) A(P.qxi, P.n) A(P.qdb, P.n) A(P.qdn, P.n) A(P.qout, 2 * P.n)
-    A(P.qcount, 1)
+    A(P.qcount, kMaxDepthCap)
     const size_t nrec = (size_t)P.ncap * kMaxDepthCap;
     A(P.rx, nrec) A(P.rwo, nrec) A(P.rn, nrec) A(P.rwi, nrec) A(P.rfc, nrec) A(P.rbeta, nrec) A(P.rlb, nrec)
     A(P.rcnt, P.ncap) A(P.rpix, P.ncap) A(P.roff, P.ncap) A(P.bsum, 1024) A(P.boff, 1024)
@@ -810,7 +807,8 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
     F.rr_depth = c.rr_depth;
     F.nee = c.nee;
     RCUDA(cudaMemsetAsync(P.ctr, 0, 8 * sizeof(unsigned long long), s));
-    RCUDA(cudaMemsetAsync(P.qcount, 0, sizeof(int), s));
+    RCUDA(cudaMemsetAsync(P.qcount, 0, kMaxDepthCap * sizeof(int), s));
+    RCUDA(cudaMemsetAsync(P.nact, 0, (kMaxDepthCap + 1) * sizeof(int), s));
     if (c.collect) RCUDA(cudaMemsetAsync(P.rpix, 0xff, P.ncap * sizeof(int), s));
     // the buffer is usually full (kept = S): shuffle it on a host thread while the GPU traces
     if (c.collect) {
@@ -822,12 +820,12 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
     r->launches++;
     const bool guided = b > 0.0;
     const unsigned gb = std::min<unsigned>(g, (unsigned)r->nsm * 8u);  // list-walking bounce kernels
+    // per-bounce list lengths and query counts (zeroed above): no reset launches
     for (int bounce = 0; bounce < c.max_depth; ++bounce) {
-        launch_pdl(r->pdl, k_queue_reset, dim3(1), dim3(1), 0, s, P, (bounce + 1) & 1);
         launch_pdl(r->pdl, k_isect, dim3(gb), dim3(kBlock), 0, s, P, F, bounce, guided ? 1 : 0);
-        r->launches += 2;
+        r->launches += 1;
         if (guided) {
-            const int rc = nasg_query_shade(r->ctx, P.n, P.qcount, (const float *)P.qx, (const float *)P.qwo,
+            const int rc = nasg_query_shade(r->ctx, P.n, P.qcount + bounce, (const float *)P.qx, (const float *)P.qwo,
                                             (const float *)P.qn, (const float *)P.qxi, (const float *)P.qdb,
                                             (const float *)P.qdn, (float)b, (float *)P.qout, s);
             if (rc != NASG_OK) return rc;
@@ -835,8 +833,6 @@ int launch_trace(nasg_render *r, int64_t iter, double b, nasg_train_sample *samp
         launch_pdl(r->pdl, k_update, dim3(gb), dim3(kBlock), 0, s, P, F, bounce);
         r->launches++;
     }
-    launch_pdl(r->pdl, k_queue_reset, dim3(1), dim3(1), 0, s, P, c.max_depth & 1);
-    r->launches++;
     if (c.collect) {
         // pipelined: the training two iterations back read this sample buffer
         if (r->ev_train) RCUDA(cudaStreamWaitEvent(s, r->ev_train, 0));
@@ -855,7 +851,8 @@ int launch_accumulate(nasg_render *r, int64_t iter) {
     const nasg_render_config &c = r->cfg;
     const int64_t mb = (int64_t)c.schedule_m * c.schedule_b;
     const double w = c.ramp ? (double)std::min<int64_t>(iter + 1, mb) / (double)mb : 1.0;
-    launch_pdl(r->pdl, k_accumulate, dim3(grid_of(r->P.n)), dim3(kBlock), 0, r->stream, r->P, (float)w, iter == 0 ? 1 : 0);
+    launch_pdl(r->pdl, k_accumulate, dim3(grid_of(r->P.n)), dim3(kBlock), 0, r->stream, r->P, (float)w, iter == 0 ? 1 : 0,
+               r->cfg.max_depth);
     r->launches++;
     r->wsum += w;
     RCUDA(cudaGetLastError());
