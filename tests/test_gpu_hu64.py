@@ -176,3 +176,21 @@ def test_checkpoint_dims_and_resume(tmp_path, orc):
     for x in (g, g2, g128):
         x.close()
     os.remove(p)
+
+
+@pytest.mark.parametrize("n_comp", [4, 16, 32])
+def test_hidden64_other_lobe_counts(orc, n_comp):
+    """The 64-unit embedding for every compiled lobe count: init and raw outputs."""
+    d = 8 * n_comp + 1
+    g = nasg.Guide(nasg.TrainerConfig(seed=9, n_components=n_comp, hidden_units=HU))
+    try:
+        w = g.get_weights()
+        assert w.shape == (64 * HU + 2 * HU * HU + HU * d,)
+        assert np.array_equal(w, orc.init_network_hu(9, HU, out_dim=d))
+        q9 = H.queries(np.random.default_rng(5), 1000)
+        raw = g.query_raw(*split(q9)).cpu().numpy()
+        enc, _ = orc.encode(q9, H.BMIN, H.BMAX)
+        ref = orc.forward(embed_hidden(w, HU, out_dim=d), enc, out_dim=d)
+        assert np.all(np.abs(raw - ref) <= 2e-5 * (1 + np.abs(ref)))
+    finally:
+        g.close()

@@ -192,3 +192,24 @@ def test_render_iteration_n32():
     finally:
         r.close()
         g.close()
+
+
+@pytest.mark.parametrize("n", [0, 1, 127, 129])
+def test_tc_query_tiny_batches(guide, orc, n):
+    """Empty and sub-tile batches through the two-warpgroup N = 32 epilogue."""
+    rng = np.random.default_rng(100 + n)
+    q9, xi = H.queries(rng, max(n, 1)), H.xis(rng, max(n, 1))
+    q9, xi = q9[:n], xi[:n]
+    guide.precision = nasg.NASG_MLP_BF16
+    try:
+        out, _ = guide.query_sample(*split(q9), torch.from_numpy(xi).cuda())
+        assert out.shape[0] == n
+        if n:
+            ref, _ = orc.query_sample(guide.get_weights(published=True), q9, xi, out_dim=D, threads=8)
+            o = out.cpu().numpy().astype(np.float64)
+            ddir = np.linalg.norm(o[:, :3] - ref[:, :3], axis=1)
+            same = ddir <= 0.05
+            assert same.mean() >= 0.99 and np.all(np.isfinite(o))
+            assert np.median(np.abs(o[same, 3] - ref[same, 3]) / ref[same, 3]) <= 1e-3
+    finally:
+        guide.precision = nasg.NASG_MLP_FP32
