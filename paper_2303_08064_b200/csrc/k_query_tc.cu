@@ -28,8 +28,9 @@
 // take its tiles alternately, each with its own E buffer, input stage and raw
 // buffer (TMEM [128 + 160 j, ...)) — the 16-lobe epilogue is about twice the
 // MLP's work per tile.  N = 32 (NP = 304): one MLP warpgroup and one NASG lane
-// served by two warpgroups that split each row's lobes (16 each, partial pdf
-// sums meeting in shared memory), raw buffer TMEM [128, 432) written by two
+// served by two warpgroups that split each row's lobes (16 each; the picked
+// lobe's logits and the partial pdf sums cross through TMEM columns behind the
+// raw buffer), raw buffer TMEM [128, 432) written by two
 // output MMAs (N = 256 + 48); they stream the row's lobes out of tensor memory
 // (the 304 columns do not fit in registers).
 // Only the 52 B/query of inputs and 16-20 B/query of outputs touch HBM.
