@@ -211,6 +211,8 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    NASG_CHECK(tc::dynamic_smem_bytes() >= smem_bytes<N>(), "query kernel: dynamic shared memory");
+    NASG_CHECK((tmem & 0xFFFFu) == 0u, "query kernel: TMEM allocation starts at column 0");
     if (threadIdx.x == 0) {  // weights: TMA bulk copies global -> smem, once per CTA
         tc::mbar_arrive_expect_tx(w_bar, IMG);
         for (uint32_t off = 0; off < IMG; off += 16384)
@@ -315,6 +317,9 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
         // ============================ NASG warpgroup ===========================
         asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(regs_nasg(N)));
         const int ln = m * S + j;  // this warpgroup's NASG lane: its E, input stage and raw buffer
+        NASG_CHECK(ln < Q && raw_col(N, ln) + (uint32_t)NP + (streamed(N) ? 18u : 0u) <= kTmemCols &&
+                       (kPairs == 1 || raw_col(N, ln) >= (uint32_t)kPairs * 128u),
+                   "query kernel: NASG lane's raw / exchange columns inside TMEM, clear of the accumulators");
         const uint32_t my_raw = tmem + raw_col(N, ln) + ((uint32_t)(wq * 32) << 16);
         const uint32_t e_row64 = tc::smem_u32(smem + E_OFF + ln * kEBytes) + (t >> 3) * 1024 + (t & 7) * 16;
         const int64_t lstride = stride * S;  // this lane's tiles: every S-th tile of the pair

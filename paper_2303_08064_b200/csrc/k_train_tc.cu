@@ -254,7 +254,11 @@ train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint3
     for (int i = 0; i < kClsRpt; ++i) {
         const bool lv = (bits >> i) & 1u;
         const uint32_t bl = __ballot_sync(0xffffffffu, lv);
-        if (lv) live[p0 + s_off[i * 8 + warp] + __popc(bl & ((1u << lane) - 1u))] = src[i];
+        if (lv) {
+            const int64_t at = p0 + s_off[i * 8 + warp] + __popc(bl & ((1u << lane) - 1u));
+            NASG_CHECK(at < count, "classify: live list index");
+            live[at] = src[i];
+        }
     }
     pdl_trigger();
 }
@@ -301,6 +305,8 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
     __syncthreads();
     tc::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    NASG_CHECK(tc::dynamic_smem_bytes() >= fb_smem<N>(), "K_fb: dynamic shared memory");
+    NASG_CHECK((kWGt - 1) * 128 + packed_width(N) <= (int)kTmemColsT, "K_fb: accumulators inside TMEM");
     pdl_trigger();
     pdl_wait();  // the weight image, the samples and the classified rows come from earlier work on the stream
     FB_TRACE(0, 15)
@@ -395,6 +401,7 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
         int ktr = 0;
         for (; tile < ntiles; tile += stride, ++ktr) {
             FB_TRACE(ktr, 0)
+            NASG_CHECK(tile < tb.max_blocks, "K_fb: tile inside the h / delta block arrays");
             const int64_t row = tile * 128 + t;
             const bool valid = row < count;
             if (!COOP || g == 0)
@@ -733,6 +740,9 @@ train_tc_dw_kernel(TcTrainBufs tb, int64_t nblocks, int bps, int np, const int64
     pdl_wait();  // the h / delta blocks of K_fb
     if (live_count) split_plan(*live_count, gridDim.x, nblocks, bps);
     const int64_t b0 = (int64_t)blockIdx.x * bps, b1 = min(nblocks, b0 + bps);
+    NASG_CHECK(tc::dynamic_smem_bytes() >= 2 * kStage + 64 && (int)blockIdx.x < tb.splits && nblocks <= tb.max_blocks &&
+                   FB <= 256,
+               "K_dw: shared memory, split index, block range, accumulator columns");
     if (threadIdx.x == 0 && b1 > b0) {
         const uint32_t idesc = tc::idesc_bf16(128, FB, true, true);
         auto load = [&](int64_t blk, int s) {

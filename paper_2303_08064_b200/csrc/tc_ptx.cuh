@@ -4,6 +4,9 @@
 #pragma once
 
 #include <cstdint>
+#ifdef NASG_CHECKED
+#include <cstdio>
+#endif
 #include <cuda_runtime.h>
 
 namespace nasg {
@@ -39,8 +42,51 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
 // Blocking wait on a phase.  The suspend-time hint lets the hardware park the
 // warp until the phase completes instead of re-polling, so waiting warps do
 // not steal issue slots from the epilogue warps that share the SM.
+#ifdef NASG_CHECKED
+// Checked builds (EXTRA=-DNASG_CHECKED, profiles/r2_checked_build.txt): the
+// kernels' protocol invariants — shared-memory and tensor-memory ranges, tile and
+// list indices, and every mbarrier wait bounded to ~4 s — trap with a message
+// instead of corrupting memory or hanging.  Compiled out of the library.
+#define NASG_CHECK(cond, what)                                                                              \
+    do {                                                                                                     \
+        if (!(cond)) {                                                                                       \
+            printf("NASG_CHECK failed: %s [%s:%d] block %d thread %d\n", what, __FILE__, __LINE__, blockIdx.x, \
+                   threadIdx.x);                                                                             \
+            __trap();                                                                                        \
+        }                                                                                                    \
+    } while (0)
+#else
+#define NASG_CHECK(cond, what) \
+    do {                       \
+    } while (0)
+#endif
+
+__device__ __forceinline__ uint32_t dynamic_smem_bytes() {
+    uint32_t r;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(r));
+    return r;
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+#ifdef NASG_CHECKED
+    for (int it = 0;; ++it) {
+        uint32_t ok;
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(ok)
+            : "r"(a), "r"(parity), "r"(1000000)
+            : "memory");
+        if (ok) break;
+        if (it > 4000) {
+            printf("NASG_CHECK failed: mbarrier wait (smem 0x%x parity %u) block %d thread %d\n", a, parity,
+                   blockIdx.x, threadIdx.x);
+            __trap();
+        }
+    }
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -48,6 +94,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n\t}" ::"r"(a),
         "r"(parity), "r"(0x989680)
         : "memory");
+#endif
 }
 
 // ---- TMA bulk copy global -> shared (1D), completes on an mbarrier ------------
