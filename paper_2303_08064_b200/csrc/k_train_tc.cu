@@ -345,19 +345,21 @@ train_tc_fb_kernel(const uint8_t *__restrict__ img, const nasg_train_sample *__r
                     const uint32_t sbo = (uint32_t)K * 16u;
                     const uint32_t idesc = tc::idesc_f16(128, l == 3 ? NP : kHidden);
                     const uint64_t ad = tc::smem_desc(abase, 128, sbo), bdsc = tc::smem_desc(b0, 128, sbo);
-                    for (int k = 0; k < K / 16; ++k)  // +256 B per K=16 slab = +16 in the address field
-                        tc::mma_bf16_elect(d, ad + (uint64_t)(k * 16), bdsc + (uint64_t)(k * 16), idesc,
-                                           k > 0 ? 1u : 0u);
+                    // +256 B per K=16 slab = +16 in the address field
+                    if (l == 0) tc::mma_f16_chain_elect<kIn / 16>(d, ad, bdsc, idesc);
+                    else tc::mma_f16_chain_elect<kHidden / 16>(d, ad, bdsc, idesc);
                 } else {
-                    const int K = l == 3 ? NP : kHidden;              // contraction over W_l's output index
-                    const uint32_t sbo_a = (uint32_t)K * 16u;          // delta tile, K-major
-                    const uint32_t lbo_b = (uint32_t)kHidden * 16u;    // image rows (out index) in 8-groups
+                    constexpr uint32_t lbo_b = (uint32_t)kHidden * 16u;  // image rows (out index) in 8-groups
                     const uint32_t idesc = l == 3 ? tc::idesc_bf16(128, kHidden, false, true)
                                                   : tc::idesc_f16(128, kHidden, false, true);
-                    const uint64_t ad = tc::smem_desc(abase, 128, sbo_a), bdsc = tc::smem_desc(b0, lbo_b, 128);
-                    for (int k = 0; k < K / 16; ++k)  // B advances 2 x 8 image rows per K=16 slab
-                        tc::mma_bf16_elect(d, ad + (uint64_t)(k * 16), bdsc + (uint64_t)(k * 2 * lbo_b / 16), idesc,
-                                           k > 0 ? 1u : 0u);
+                    const uint64_t bdsc = tc::smem_desc(b0, lbo_b, 128);
+                    // contraction over W_l's output index; B advances 2 x 8 image rows per K=16 slab
+                    if (l == 3)
+                        tc::mma_f16_chain_elect<NP / 16, 16, 2 * lbo_b / 16>(
+                            d, tc::smem_desc(abase, 128, (uint32_t)NP * 16u), bdsc, idesc);
+                    else
+                        tc::mma_f16_chain_elect<kHidden / 16, 16, 2 * lbo_b / 16>(
+                            d, tc::smem_desc(abase, 128, (uint32_t)kHidden * 16u), bdsc, idesc);
                 }
                 tc::mma_commit_elect(&acc_full[g]);
             }
