@@ -261,7 +261,7 @@ query_tc_kernel(const uint8_t *__restrict__ img, QueryArgs a) {
                     const uint64_t bd = tc::smem_desc(bbase, 128, K * 16);
                     const uint32_t d = tmem + (LL == 3 ? raw_col(N, lk) : (uint32_t)m * 128u);
                     // +256 B per K=16 slab = +16 in the address field
-                    tc::mma_f16_chain_elect<K / 16>(d, ad, bd, idesc);
+                    tc::mma_f16_chain_elect<K / 16, 16, 16, (N != 4)>(d, ad, bd, idesc);
                     if constexpr (NO > 256) {  // packed columns [256, NP): image rows 256.. (32 row groups on)
                         constexpr uint32_t idesc1 = tc::idesc_f16(128, NO - 256);
                         const uint64_t bd1 = tc::smem_desc(bbase + 32u * (uint32_t)(K * 16), 128, K * 16);

@@ -148,36 +148,56 @@ __device__ __forceinline__ void mma_bf16_elect(uint32_t d_tmem, uint64_t adesc, 
         "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-// NK MMAs of one K-chain in one elected issue block (one elect and the
-// descriptor steps in the uniform datapath instead of an elect + register
-// moves per MMA: the MLP chain's issue cost, 4.9 k -> 4.4 k static
-// instructions in the query kernel).  Slab kk uses adesc + kk*AINC and
-// bdesc + kk*BINC (descriptor address units of 16 B); the first MMA accumulates
-// into D when acc != 0, the others always.
-template <int NK, int AINC = 16, int BINC = 16>
+// NK MMAs of one K-chain in one elected issue block instead of an elect and
+// register moves per MMA.  Slab kk uses adesc + kk*AINC and bdesc + kk*BINC
+// (descriptor address units of 16 B); the first MMA accumulates into D when
+// acc != 0, the others always.  BRANCH: the elected lane branches into an
+// unpredicated block, so ptxas keeps the chain in uniform registers
+// (back-to-back UTCHMMA: the query kernel 4.9 k -> 3.8 k static instructions);
+// otherwise every MMA is predicated on the elect (4.4 k), which measured faster
+// for the N = 4 query only (profiles/r2_query_knobs.txt).
+#define NASG_MMA_STEP_B "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+#define NASG_MMA_STEP_P "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
+#define NASG_MMA_HEAD_B                                             \
+    "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t"               \
+    "elect.sync _|e, 0xffffffff;\n\t@!e bra MMA_SKIP_%=;\n\t"          \
+    "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.u32 pt, 0, 0;\n\t"              \
+    "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t"                             \
+    "tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pf;\n\t"
+#define NASG_MMA_HEAD_P                                             \
+    "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t"               \
+    "elect.sync _|e, 0xffffffff;\n\t"                                  \
+    "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.u32 pt, 0, 0;\n\t"              \
+    "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t"                             \
+    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pf;\n\t"
+#define NASG_MMA_TAIL_B "MMA_SKIP_%=:\n\t}"
+#define NASG_MMA_TAIL_P "}"
+#define NASG_MMA_ARGS ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "n"(AINC), "n"(BINC)
+#define NASG_MMA_CHAIN(H, S, T)                                                                              \
+    if constexpr (NK == 3) asm volatile(H S S T NASG_MMA_ARGS);                                             \
+    else if constexpr (NK == 4) asm volatile(H S S S T NASG_MMA_ARGS);                                      \
+    else if constexpr (NK == 5) asm volatile(H S S S S T NASG_MMA_ARGS);                                    \
+    else if constexpr (NK == 8) asm volatile(H S S S S S S S T NASG_MMA_ARGS);                              \
+    else if constexpr (NK == 10) asm volatile(H S S S S S S S S S T NASG_MMA_ARGS);                         \
+    else asm volatile(H S S S S S S S S S S S S S S S S S S T NASG_MMA_ARGS);
+template <int NK, int AINC = 16, int BINC = 16, bool BRANCH = true>
 __device__ __forceinline__ void mma_f16_chain_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                     uint32_t acc = 0) {
     static_assert(NK == 3 || NK == 4 || NK == 5 || NK == 8 || NK == 10 || NK == 19, "K / 16 slabs");
-#define NASG_MMA_STEP "add.s64 a, a, %5;\n\tadd.s64 b, b, %6;\n\t@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pt;\n\t"
-#define NASG_MMA_HEAD                                                        \
-    "{\n\t.reg .pred e, pf, pt;\n\t.reg .b64 a, b;\n\t"                     \
-    "elect.sync _|e, 0xffffffff;\n\t"                                        \
-    "setp.ne.b32 pf, %4, 0;\n\tsetp.eq.u32 pt, 0, 0;\n\t"                    \
-    "mov.b64 a, %1;\n\tmov.b64 b, %2;\n\t"                                   \
-    "@e tcgen05.mma.cta_group::1.kind::f16 [%0], a, b, %3, pf;\n\t"
-#define NASG_MMA_ARGS ::"r"(d_tmem), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "n"(AINC), "n"(BINC)
-#define S1 NASG_MMA_STEP
-    if constexpr (NK == 3) asm volatile(NASG_MMA_HEAD S1 S1 "}" NASG_MMA_ARGS);
-    else if constexpr (NK == 4) asm volatile(NASG_MMA_HEAD S1 S1 S1 "}" NASG_MMA_ARGS);
-    else if constexpr (NK == 5) asm volatile(NASG_MMA_HEAD S1 S1 S1 S1 "}" NASG_MMA_ARGS);
-    else if constexpr (NK == 8) asm volatile(NASG_MMA_HEAD S1 S1 S1 S1 S1 S1 S1 "}" NASG_MMA_ARGS);
-    else if constexpr (NK == 10) asm volatile(NASG_MMA_HEAD S1 S1 S1 S1 S1 S1 S1 S1 S1 "}" NASG_MMA_ARGS);
-    else asm volatile(NASG_MMA_HEAD S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 S1 "}" NASG_MMA_ARGS);
-#undef S1
-#undef NASG_MMA_ARGS
-#undef NASG_MMA_HEAD
-#undef NASG_MMA_STEP
+    if constexpr (BRANCH) {
+        NASG_MMA_CHAIN(NASG_MMA_HEAD_B, NASG_MMA_STEP_B, NASG_MMA_TAIL_B)
+    } else {
+        NASG_MMA_CHAIN(NASG_MMA_HEAD_P, NASG_MMA_STEP_P, NASG_MMA_TAIL_P)
+    }
 }
+#undef NASG_MMA_CHAIN
+#undef NASG_MMA_ARGS
+#undef NASG_MMA_TAIL_P
+#undef NASG_MMA_TAIL_B
+#undef NASG_MMA_HEAD_P
+#undef NASG_MMA_HEAD_B
+#undef NASG_MMA_STEP_P
+#undef NASG_MMA_STEP_B
 __device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\t"
