@@ -194,8 +194,12 @@ int nasg_query_sample_host_packed(nasg_ctx *ctx, int64_t n, const float *q13, fl
 /* ---- training (Trainer::train_iteration guiding.hpp:149, guiding.cpp:196-282)
  * Runs T = nu*ceil(S/t) minibatch steps over the n samples (epochs reshuffled
  * with the reference's PCG32 Fisher-Yates), then publishes.  n == 0 is a
- * no-op + publish.  samples is a device array.  Blocks until stats are ready
- * when stats != NULL. */
+ * no-op + publish.  samples is a device array, complete when the call's first
+ * kernel starts: stream order guarantees it, except after a producer kernel on
+ * the same stream that releases its dependents early (programmatic dependent
+ * launch, griddepcontrol.launch_dependents) — the step's first kernel reads the
+ * rows before its own programmatic wait.  Blocks until stats are ready when
+ * stats != NULL. */
 int nasg_train_iteration(nasg_ctx *ctx, int64_t n, const nasg_train_sample *samples,
                          double blend_b, nasg_train_stats *stats, void *stream);
 /* One data-parallel minibatch step on rows samples[order[0..count)] with the

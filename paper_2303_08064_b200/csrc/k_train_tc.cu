@@ -139,7 +139,11 @@ __host__ __device__ __forceinline__ void split_plan(int64_t rows, int splits, in
 // |direction components| <= 2.  Those rows are counted and skipped; the rest
 // (in row order, as source indices through the epoch permutation) form the
 // step's list for K_fb and K_dw.  One pass, order-preserving, deterministic:
-// 1024 rows per block, block offsets by decoupled look-back.
+// 1024 rows per block, block offsets by decoupled look-back.  Consecutive
+// steps alternate between two lists, so the classification of step s + 1 runs
+// before the programmatic wait — overlapping step s's reduction and Adam — and
+// only the weight flag (written by that Adam) is read after it: in the rare
+// case it is set (some weight >= kSafeWeight), every row is kept instead.
 constexpr int kClsThreads = 256, kClsRpt = 4, kClsRows = kClsThreads * kClsRpt;
 constexpr int kClsEpochBits = 26, kClsValBits = 36;
 
@@ -153,12 +157,12 @@ train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint3
                       unsigned long long *state, uint32_t epoch, int64_t *cls, unsigned long long *clamp_count) {
     __shared__ int s_cnt[kClsRpt * 8], s_off[kClsRpt * 8];
     __shared__ long long s_prefix;
-    __shared__ int s_clamped;
+    __shared__ int s_clamped, s_total;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t base = (int64_t)blockIdx.x * kClsRows;
     if (tid == 0) s_clamped = 0;
-    pdl_wait();  // samples, order and the last Adam step's weight flag
-    const bool big = *(volatile const int *)wbig != 0;
+    // the samples and the order were written before the previous step (host
+    // uploads and copies are stream-ordered; a whole-buffer step has no order)
     uint32_t src[kClsRpt];
 #pragma unroll
     for (int i = 0; i < kClsRpt; ++i) {
@@ -181,7 +185,7 @@ train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint3
         const int64_t row = base + i * kClsThreads + tid;
         bool lv = false;
         if (row < count) {
-            const bool zero = !big && a[i].w == 0.f && isfinite(a[i].x) && isfinite(a[i].y) && isfinite(a[i].z) &&
+            const bool zero = a[i].w == 0.f && isfinite(a[i].x) && isfinite(a[i].y) && isfinite(a[i].z) &&
                               finite_dir(o[i]) && finite_dir(n[i]);
             lv = !zero;
             if (zero) {  // its encode is skipped too: count its clamped coordinates here
@@ -197,7 +201,6 @@ train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint3
         if (lane == 0) s_cnt[i * 8 + warp] = __popc(bl);
         bits |= (lv ? 1u : 0u) << i;
     }
-    if (clamped) atomicAdd(&s_clamped, clamped);
     __syncthreads();
     if (warp == 0) {  // (i, warp) counts in row order -> exclusive offsets; block total; look-back
         const int v = s_cnt[lane];
@@ -241,14 +244,31 @@ train_classify_kernel(const nasg_train_sample *__restrict__ samples, const uint3
         }
         if (lane == 0) {
             s_prefix = prefix;
-            if (blockIdx.x == gridDim.x - 1) {
-                cls[0] = prefix + total;
-                cls[1] = count - (prefix + total);
-            }
+            s_total = total;
         }
     }
     __syncthreads();
+    pdl_wait();  // the previous step's Adam (its weight flag) and its readers of this list are done
+    if (*(volatile const int *)wbig != 0) {  // rare: no row may skip the network; keep every row
+#pragma unroll
+        for (int i = 0; i < kClsRpt; ++i) {
+            const int64_t row = base + i * kClsThreads + tid;
+            if (row < count) live[row] = src[i];
+        }
+        if (blockIdx.x == 0 && tid == 0) {
+            cls[0] = count;
+            cls[1] = 0;
+        }
+        pdl_trigger();
+        return;
+    }
+    if (clamped) atomicAdd(&s_clamped, clamped);  // the skipped rows' encode clamps (their encode is skipped)
+    __syncthreads();
     if (tid == 0 && s_clamped && clamp_count) atomicAdd(clamp_count, (unsigned long long)s_clamped);
+    if (tid == 0 && blockIdx.x == gridDim.x - 1) {  // {live, zero} after the weight flag is known
+        cls[0] = s_prefix + s_total;
+        cls[1] = count - (s_prefix + s_total);
+    }
     const int64_t p0 = s_prefix;
 #pragma unroll
     for (int i = 0; i < kClsRpt; ++i) {
@@ -881,8 +901,9 @@ int train_classify(const nasg_train_sample *samples, const uint32_t *order, int6
         cudaMemsetAsync(tb.scan_state, 0, tb.scan_cap * sizeof(unsigned long long), s);
         tb.scan_epoch = 1;
     }
+    tb.cls_par ^= 1;  // the other list: the previous step's readers may still be running
     launch_pdl(pdl, train_classify_kernel, dim3(nblk), dim3(kClsThreads), 0, s, samples, order, count, tb.wbig, bounds,
-               tb.live, tb.scan_state, tb.scan_epoch, tb.cls, clamp_count);
+               tb.cur_live(), tb.scan_state, tb.scan_epoch, tb.cur_cls(), clamp_count);
     return 1;
 }
 
@@ -904,8 +925,8 @@ int train_tc_step(int n_comp, const void *img, const nasg_train_sample *samples,
         const uint32_t *rows = order;
         if (tb.skip_zero && ntiles > num_sms) {
             launches += train_classify(samples, order, count, tb, bounds, clamp_count, s, pdl);
-            live_count = tb.cls;
-            rows = tb.live;
+            live_count = tb.cur_cls();
+            rows = tb.cur_live();
         }
         const int grid = (int)(ntiles < num_sms ? ntiles : num_sms);
         const uint8_t *im = static_cast<const uint8_t *>(img);

@@ -396,7 +396,7 @@ int ensure_tc_scratch(nasg_ctx *c, int64_t count) {
 int ensure_classify(nasg_ctx *c, int64_t count) {
     TcTrainBufs &t = c->tcb;
     const int64_t rows = ((count + 1023) / 1024) * 1024;
-    if (!t.cls) CUDA_TRY(cudaMalloc(&t.cls, 2 * sizeof(int64_t)));
+    if (!t.cls) CUDA_TRY(cudaMalloc(&t.cls, 4 * sizeof(int64_t)));
     t.wbig = c->d_wbig;
     if (rows <= t.live_cap) return NASG_OK;
     if (t.live) cudaFree(t.live);
@@ -404,7 +404,7 @@ int ensure_classify(nasg_ctx *c, int64_t count) {
     t.live = nullptr;
     t.scan_state = nullptr;
     t.scan_cap = rows / 1024;
-    CUDA_TRY(cudaMalloc(&t.live, (size_t)rows * sizeof(uint32_t)));
+    CUDA_TRY(cudaMalloc(&t.live, 2 * (size_t)rows * sizeof(uint32_t)));
     CUDA_TRY(cudaMalloc(&t.scan_state, (size_t)t.scan_cap * sizeof(unsigned long long)));
     CUDA_TRY(cudaMemset(t.scan_state, 0, (size_t)t.scan_cap * sizeof(unsigned long long)));
     t.scan_epoch = 0;
@@ -465,8 +465,8 @@ int train_step_impl(nasg_ctx *c, const nasg_train_sample *samples, const uint32_
         const uint32_t *rows = order;
         if (c->tcb.skip_zero && (count + 63) / 64 > c->num_sms) {
             c->launches += train_classify(samples, order, count, c->tcb, c->bounds, clamp, s, false);
-            live_count = c->tcb.cls;
-            rows = c->tcb.live;
+            live_count = c->tcb.cur_cls();
+            rows = c->tcb.cur_live();
         }
         if (train_forward_backward(c->N, c->wp, c->wtp, samples, rows, count, live_count, global_count, b,
                                    c->cfg.loss_blend, c->bounds, c->sc, c->num_sms, clamp, s) < 0)

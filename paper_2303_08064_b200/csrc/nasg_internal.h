@@ -242,8 +242,11 @@ struct TcTrainBufs {
     // zero-gradient row skipping (train_classify_kernel): the step's rows that
     // need the network, in row order, and {live count, zero-row count}
     bool skip_zero = true;
-    uint32_t *live = nullptr;
-    int64_t *cls = nullptr;
+    uint32_t *live = nullptr;  // two lists of live_cap rows: consecutive steps alternate
+    int64_t *cls = nullptr;    // two {live, zero} pairs, same alternation
+    int cls_par = 0;           // the list / pair the last train_classify wrote
+    uint32_t *cur_live() const { return live + (size_t)cls_par * (size_t)live_cap; }
+    int64_t *cur_cls() const { return cls + 2 * cls_par; }
     unsigned long long *scan_state = nullptr;  // decoupled look-back words, one per classify block
     int64_t scan_cap = 0;
     int64_t live_cap = 0;
