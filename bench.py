@@ -241,14 +241,18 @@ def run_reference(args, ws, rank):
 
 
 def time_events(fn, k, stream):
+    """k back-to-back steps between two CUDA events on `stream` (no event between
+    steps: an event record in the stream would cut the programmatic early start
+    of each step's first kernel); returns the mean step time k times."""
     import torch
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(k + 1)]
-    ev[0].record(stream)
-    for i in range(k):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(k):
         fn()
-        ev[i + 1].record(stream)
-    ev[-1].synchronize()
-    return [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(k)]
+    e1.record(stream)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    return [t / k] * k
 
 
 def bench_train(g_cls, nasg, args, ws, rank, precision):
