@@ -245,3 +245,42 @@ def test_counters_track_the_trainer():
     assert c1["kernel_launches"] > c0["kernel_launches"]
     g.attach_nccl(0, 0, 1)  # a single rank needs no communicator
     g.close()
+
+
+def test_event_ordered_uploads_match_synchronised():
+    """The large-batch step classifies its rows before its programmatic wait;
+    samples uploaded on another stream and ordered by an event wait must still
+    be the ones it reads: per-step stats and the final weights equal a run that
+    synchronises before every step (profiles/pdl_event_check.py at full size)."""
+    n = 1 << 17
+    hosts = [torch.from_numpy(nasg.synth_samples(100 + k, n)).pin_memory() for k in range(3)]
+
+    def run(synced):
+        g = nasg.Guide(nasg.TrainerConfig(seed=3, sample_capacity=n, batch_size=n))
+        g.train_precision = nasg.NASG_MLP_BF16
+        bufs = [torch.empty((n, 16), dtype=torch.float32, device="cuda") for _ in range(2)]
+        cs, cur = torch.cuda.Stream(), torch.cuda.current_stream()
+        copied = [torch.cuda.Event(), torch.cuda.Event()]
+        trained = [torch.cuda.Event(), torch.cuda.Event()]
+        out = []
+        for k in range(12):
+            b = k % 2
+            with torch.cuda.stream(cs):
+                if k >= 2:
+                    cs.wait_event(trained[b])
+                bufs[b].copy_(hosts[k % 3], non_blocking=True)
+                copied[b].record(cs)
+            if synced:
+                torch.cuda.synchronize()
+            cur.wait_event(copied[b])
+            st = g.train_iteration(bufs[b], 1.0, stats=True)
+            trained[b].record(cur)
+            out.append((st.mean_loss, st.dropped_samples))
+        torch.cuda.synchronize()
+        w = g.get_weights()
+        g.close()
+        return out, w
+
+    a, wa = run(False)
+    b, wb = run(True)
+    assert a == b and np.array_equal(wa, wb)
