@@ -268,7 +268,8 @@ double nasg_stride_update(double l, uint64_t collected, uint64_t capacity);
  * of scene content — and trains data-parallel through the context's NCCL
  * communicator (nasg_comm_init). */
 typedef struct nasg_render nasg_render;
-enum { NASG_SCENE_FURNACE = 0, NASG_SCENE_BOX = 1, NASG_SCENE_CRACK = 2, NASG_SCENE_DARK = 3, NASG_SCENE_ATTIC = 4 };
+enum { NASG_SCENE_FURNACE = 0, NASG_SCENE_BOX = 1, NASG_SCENE_CRACK = 2, NASG_SCENE_DARK = 3, NASG_SCENE_ATTIC = 4,
+       NASG_SCENE_INDIRECT = 5 /* SPEC acceptance 7: room lit only by the ceiling's bounce */ };
 typedef struct {
     int scene;             /* NASG_SCENE_* */
     int width, height;     /* full image */

@@ -61,7 +61,7 @@ class _RenderStats(C.Structure):
                 ("kept", C.c_int64), ("nonfinite_paths", C.c_int64), ("train", _Stats)]
 
 
-SCENE_FURNACE, SCENE_BOX, SCENE_CRACK, SCENE_DARK, SCENE_ATTIC = 0, 1, 2, 3, 4
+SCENE_FURNACE, SCENE_BOX, SCENE_CRACK, SCENE_DARK, SCENE_ATTIC, SCENE_INDIRECT = 0, 1, 2, 3, 4, 5
 
 
 @dataclass

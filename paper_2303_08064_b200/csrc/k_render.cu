@@ -527,20 +527,29 @@ static bool build_scene(int kind, int w, int h, Scene &s) {
         const float lo[3] = {-1.5f, -1.5f, -0.5f}, hi[3] = {1.5f, 1.5f, 2.5f};
         std::memcpy(s.bmin, lo, sizeof(lo));
         std::memcpy(s.bmax, hi, sizeof(hi));
-    } else if (kind == NASG_SCENE_BOX || kind == NASG_SCENE_CRACK || kind == NASG_SCENE_ATTIC) {
-        const bool crack = kind != NASG_SCENE_BOX;
+    } else if (kind == NASG_SCENE_BOX || kind == NASG_SCENE_CRACK || kind == NASG_SCENE_ATTIC ||
+               kind == NASG_SCENE_INDIRECT) {
+        const bool indirect = kind == NASG_SCENE_INDIRECT;
+        const bool crack = kind != NASG_SCENE_BOX && !indirect;
         const int mw = addm(mat(kLambert, white)), mr = addm(mat(kLambert, red)), mg = addm(mat(kLambert, green));
         const int mgl = addm(mat(kPhong, f3(0.8f, 0.8f, 0.8f), 60.f));
         const int mmi = addm(mat(kMirror, f3(0.95f, 0.95f, 0.95f)));
         const float3 le = kind == NASG_SCENE_BOX ? f3(17.f, 12.f, 4.f)
-                          : (kind == NASG_SCENE_CRACK ? f3(60.f, 48.f, 30.f) : f3(400.f, 320.f, 200.f));
+                          : (kind == NASG_SCENE_CRACK ? f3(60.f, 48.f, 30.f)
+                             : (indirect ? f3(100.f, 80.f, 50.f) : f3(400.f, 320.f, 200.f)));
         const int mle = addm(mat(kEmitter, f3(0.f, 0.f, 0.f), 0.f, le));
         addp(quad(f3(0.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), f3(1.f, 0.f, 0.f), crack ? mgl : mw));
         addp(quad(f3(0.f, 1.f, 0.f), f3(1.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), mw));  // ceiling
         addp(quad(f3(0.f, 0.f, 1.f), f3(0.f, 1.f, 0.f), f3(1.f, 0.f, 0.f), mw));  // back
         addp(quad(f3(0.f, 0.f, 0.f), f3(0.f, 1.f, 0.f), f3(0.f, 0.f, 1.f), mr));  // left
         addp(quad(f3(1.f, 0.f, 0.f), f3(0.f, 0.f, 1.f), f3(0.f, 1.f, 0.f), mg));  // right
-        if (kind == NASG_SCENE_BOX) {
+        if (indirect) {  // SPEC acceptance 7's "indirect-illumination box": a panel under the
+                         // ceiling facing up, so everything below it is lit only by light that
+                         // bounced off the ceiling and upper walls (NEE finds no unoccluded light)
+            addp(quad(f3(0.35f, 0.8f, 0.35f), f3(0.f, 0.f, 0.3f), f3(0.3f, 0.f, 0.f), mle));
+            addp(sphere(f3(0.3f, 0.2f, 0.6f), 0.2f, mw));
+            addp(sphere(f3(0.72f, 0.18f, 0.35f), 0.18f, mmi));
+        } else if (kind == NASG_SCENE_BOX) {
             addp(quad(f3(0.4f, 0.999f, 0.4f), f3(0.2f, 0.f, 0.f), f3(0.f, 0.f, 0.2f), mle));
             addp(sphere(f3(0.3f, 0.2f, 0.62f), 0.2f, mgl));
             addp(sphere(f3(0.72f, 0.18f, 0.35f), 0.18f, mmi));

@@ -260,7 +260,7 @@ def frame_means(scene, frames, skip=1, **kw):
         g.close()
 
 
-@pytest.mark.parametrize("scene", [nasg.SCENE_BOX, nasg.SCENE_CRACK])
+@pytest.mark.parametrize("scene", [nasg.SCENE_BOX, nasg.SCENE_CRACK, nasg.SCENE_INDIRECT])
 def test_nee_mis_matches_brute_force(scene):
     """NEE + balance-heuristic MIS against the scattering-only estimator, unguided and
     guided (b = 1 after the first frame): all three must share one mean.  A light
@@ -275,9 +275,10 @@ def test_nee_mis_matches_brute_force(scene):
 
 
 def test_guiding_lowers_mape_on_the_box():
-    """Direction of effect (SPEC acceptance 7 analogue, PAPER Table 3 'Box'): at 512 spp the
-    guided render's MAPE against a 16k-spp unguided reference is lower than the unguided
-    render's.  Measured 0.84-0.86x here; the SPEC's 0.8x target is recorded in DESIGN.md."""
+    """Direction of effect on the directly lit Cornell box (PAPER Table 3 'Box' is lit
+    directly too): at 512 spp the guided render's MAPE against a 16k-spp unguided reference
+    is lower than the unguided render's (0.87x measured: NEE already handles most of this
+    scene's light).  SPEC acceptance 7 itself is the indirect box below."""
     def render(guiding, spp, seed, collect):
         g, r = make(nasg.SCENE_BOX, width=128, height=128, seed=seed, guiding=guiding, collect=collect,
                     ramp=guiding)
@@ -292,3 +293,25 @@ def test_guiding_lowers_mape_on_the_box():
     u = nasg.mape(render(False, 512, 1, False), ref)
     gd = nasg.mape(render(True, 512, 1, True), ref)
     assert gd < 0.95 * u, (gd, u)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_spec_acceptance_7_indirect_box(seed):
+    """SPEC acceptance 7: on the shipped indirect-illumination box at 512 spp with a fixed
+    seed, guided MAPE <= 0.8x unguided MAPE (reference: 16k-spp unguided render, distinct
+    seed; SPEC defaults N = 8, S = 2^16, t = 2^12, e = 0.2, M = 4, B = 64, ramp on).
+    Measured 0.715 (seed 1) and 0.730 (seed 2), profiles/r2_indirect_probe.txt."""
+    def render(guiding, spp, s):
+        g, r = make(nasg.SCENE_INDIRECT, width=128, height=128, seed=s, guiding=guiding, collect=guiding,
+                    ramp=guiding)
+        try:
+            for _ in range(spp):
+                r.iteration()
+            return r.image()
+        finally:
+            r.close()
+            g.close()
+    ref = render(False, 16384, 99)
+    u = nasg.mape(render(False, 512, seed), ref)
+    gd = nasg.mape(render(True, 512, seed), ref)
+    assert gd <= 0.8 * u, (gd, u, gd / u)

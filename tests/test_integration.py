@@ -79,7 +79,8 @@ def test_mape_spec_examples():
 
 def test_render_scene_bounds():
     import paper_2303_08064_b200 as nasg
-    for s in (nasg.SCENE_FURNACE, nasg.SCENE_BOX, nasg.SCENE_CRACK, nasg.SCENE_DARK, nasg.SCENE_ATTIC):
+    for s in (nasg.SCENE_FURNACE, nasg.SCENE_BOX, nasg.SCENE_CRACK, nasg.SCENE_DARK, nasg.SCENE_ATTIC,
+              nasg.SCENE_INDIRECT):
         lo, hi = nasg.scene_bounds(s)
         assert np.all(hi > lo)
     with pytest.raises(nasg.NasgError):
