@@ -315,3 +315,21 @@ def test_spec_acceptance_7_indirect_box(seed):
     u = nasg.mape(render(False, 512, seed), ref)
     gd = nasg.mape(render(True, 512, seed), ref)
     assert gd <= 0.8 * u, (gd, u, gd / u)
+
+
+def test_spec_acceptance_9_determinism_on_the_indirect_box():
+    """SPEC acceptance 9: two full guided renders of acceptance 7's scene at 32 spp with
+    identical configs (SPEC defaults, online training on) give bitwise-identical films
+    and network weights."""
+    out = []
+    for _ in range(2):
+        g, r = make(nasg.SCENE_INDIRECT, width=128, height=128, seed=1)
+        try:
+            for _ in range(32):
+                r.iteration()
+            out.append((np.asarray(r.image()).copy(), g.get_weights()))
+        finally:
+            r.close()
+            g.close()
+    assert np.array_equal(out[0][0], out[1][0])
+    assert np.array_equal(out[0][1], out[1][1])
