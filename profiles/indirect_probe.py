@@ -1,11 +1,13 @@
-# guided / unguided MAPE (SPEC acceptance 7) on candidate indirect-illumination box scenes
+# guided / unguided MAPE (SPEC acceptance 7) on the render scenes
+# usage: indirect_probe.py SCENES [REF_SPP] [fp32|bf16]  (query + trainer precision; default tensor core)
 import sys, time
 sys.path.insert(0, '/root/repo')
 import paper_2303_08064_b200 as nasg
+PREC = nasg.NASG_MLP_FP32 if len(sys.argv) > 3 and sys.argv[3] == 'fp32' else nasg.NASG_MLP_BF16
 def render(scene, guiding, spp, seed, size=128):
     lo, hi = nasg.scene_bounds(scene)
     g = nasg.Guide(nasg.TrainerConfig(seed=seed), bmin=lo, bmax=hi)
-    g.precision = nasg.NASG_MLP_BF16; g.train_precision = nasg.NASG_MLP_BF16
+    g.precision = PREC; g.train_precision = PREC
     r = nasg.Render(g, scene=scene, width=size, height=size, seed=seed, guiding=guiding, collect=guiding, ramp=guiding)
     try:
         for _ in range(spp): r.iteration()
